@@ -1,0 +1,266 @@
+"""fp64 CPU oracle of the hot path (ctypes wrapper over oracle/oracle.c).
+
+TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke(), tools/make_data.py
+and bench.py's cpu_baseline / ``--impl reference`` legs may import this
+package.  The product path (paper_2603_28907_b200) never imports it.
+
+Besides the C kernels this module holds the plain-Python parts of the oracle:
+the leapfrog / HMC transition (readings R19/R20) and the inverse
+heights map used by tools/make_data.py to place chains near the truth.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import math
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRC = os.path.join(_HERE, "oracle.c")
+
+_dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_fp = np.ctypeslib.ndpointer(dtype=np.float32, flags="C_CONTIGUOUS")
+_ip = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+_lp = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+_up = np.ctypeslib.ndpointer(dtype=np.uint32, flags="C_CONTIGUOUS")
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with plain gcc (-O2, no fast-math, no FMA contraction)."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-std=c11", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
+               "-shared", "-fPIC", "-o", _SO, _SRC, "-lm"]
+        subprocess.check_call(cmd)
+    return _SO
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ct.CDLL(_SO)
+        L.or_problem_new.restype = ct.c_void_p
+        L.or_problem_new.argtypes = [ct.c_int, ct.c_int, _fp, _fp, ct.c_float,
+                                     ct.c_double, ct.c_double, ct.c_double, ct.c_double, ct.c_double,
+                                     ct.c_double, ct.c_double, ct.c_int, _fp, ct.c_long,
+                                     _ip, _fp, _fp, _ip]
+        L.or_problem_free.argtypes = [ct.c_void_p]
+        L.or_torus_spectrum.argtypes = [ct.c_int, ct.c_int, ct.c_double,
+                                        ct.POINTER(ct.c_double), ct.POINTER(ct.c_double)]
+        L.or_prior_surface.restype = ct.c_double
+        L.or_prior_surface.argtypes = [ct.c_int, ct.c_int, ct.c_double, _dp, _dp]
+        L.or_heights.argtypes = [ct.c_void_p, _dp, _dp, _dp]
+        L.or_ray_extent.argtypes = [ct.c_void_p, ct.c_long, ct.POINTER(ct.c_double), ct.POINTER(ct.c_double)]
+        L.or_traversal.restype = ct.c_int
+        L.or_traversal.argtypes = [ct.c_void_p, ct.c_long, _ip, _dp, _dp, ct.c_int]
+        L.or_path_lengths.argtypes = [ct.c_void_p, ct.c_int, _dp, _dp, _dp, ct.c_void_p]
+        L.or_loglik_grad_H.argtypes = [ct.c_void_p, ct.c_int, _dp, _dp, _dp, _dp, ct.c_void_p, _lp]
+        L.or_logpost_grad.argtypes = [ct.c_void_p, ct.c_int, _dp, _dp, _dp, _dp, _dp, _dp,
+                                      ct.c_void_p, _lp]
+        L.or_philox4x32_10.argtypes = [_up, _up, _up]
+        L.or_momenta.argtypes = [ct.c_int, ct.c_uint64, ct.c_uint64, ct.c_uint64, _dp]
+        L.or_mh_uniform.restype = ct.c_double
+        L.or_mh_uniform.argtypes = [ct.c_uint64, ct.c_uint64, ct.c_uint64]
+        L.or_num_threads.restype = ct.c_int
+        _lib = L
+    return _lib
+
+
+def num_threads() -> int:
+    return lib().or_num_threads()
+
+
+def torus_spectrum(nx: int, ny: int, r: float):
+    """(σ, ln det Q) of the periodic CAR precision Q = diag(A1) - rA."""
+    s, ld = ct.c_double(), ct.c_double()
+    lib().or_torus_spectrum(nx, ny, r, ct.byref(s), ct.byref(ld))
+    return s.value, ld.value
+
+
+def prior_surface(x: np.ndarray, r: float):
+    """log N(x; 0, Q^-1) and its gradient for one [nx][ny] surface."""
+    x = np.ascontiguousarray(x, np.float64)
+    g = np.zeros_like(x)
+    v = lib().or_prior_surface(x.shape[0], x.shape[1], r, x, g)
+    return v, g
+
+
+def philox4x32_10(ctr, key) -> np.ndarray:
+    out = np.zeros(4, np.uint32)
+    lib().or_philox4x32_10(np.asarray(ctr, np.uint32), np.asarray(key, np.uint32), out)
+    return out
+
+
+def momenta(P: int, seed: int, it: int, chain: int) -> np.ndarray:
+    out = np.zeros(P, np.float64)
+    lib().or_momenta(P, seed, it, chain, out)
+    return out
+
+
+def mh_uniform(seed: int, it: int, chain: int) -> float:
+    return lib().or_mh_uniform(seed, it, chain)
+
+
+class Problem:
+    """The canonical fp32 problem (paper_2603_28907_b200.inputs.make_problem) in fp64."""
+
+    def __init__(self, prob: dict):
+        L = lib()
+        self.prob = prob
+        self.nx = len(prob["node_x"])
+        self.ny = len(prob["node_y"])
+        self.N = self.nx * self.ny
+        self.P = 2 * self.N
+        self.R = len(prob["ray_det"])
+        self.z_top = float(prob["z_top"])
+        self.car_r = [float(v) for v in prob["car_r"]]
+        self._keep = [np.ascontiguousarray(prob[k]) for k in
+                      ("node_x", "node_y", "det_xyz", "ray_det", "ray_dir", "ray_w", "counts")]
+        nxa, nya, det, rdet, rdir, rw, cnt = self._keep
+        self.h = L.or_problem_new(self.nx, self.ny, nxa.astype(np.float32), nya.astype(np.float32),
+                                  float(prob["z_top"]), prob["rho_muck"], prob["rho_air"],
+                                  prob["rho_rock"], prob["rho_ext"], prob["att_len"],
+                                  self.car_r[0], self.car_r[1], len(det),
+                                  np.ascontiguousarray(det, np.float32).ravel(), self.R,
+                                  np.ascontiguousarray(rdet, np.int32),
+                                  np.ascontiguousarray(rdir, np.float32).ravel(),
+                                  np.ascontiguousarray(rw, np.float32),
+                                  np.ascontiguousarray(cnt, np.int32))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().or_problem_free(self.h)
+            self.h = None
+
+    # -- pieces ---------------------------------------------------------
+    def sigma(self):
+        return [torus_spectrum(self.nx, self.ny, r)[0] for r in self.car_r]
+
+    def heights(self, x: np.ndarray):
+        """x [2][nx][ny] -> (H [2][nx][ny], dH [3][nx][ny])."""
+        x = np.ascontiguousarray(x, np.float64).reshape(2, self.nx, self.ny)
+        H = np.zeros_like(x)
+        dH = np.zeros((3, self.nx, self.ny))
+        lib().or_heights(self.h, x, H, dH)
+        return H, dH
+
+    def ray_extent(self, q: int):
+        s, le = ct.c_double(), ct.c_double()
+        lib().or_ray_extent(self.h, q, ct.byref(s), ct.byref(le))
+        return s.value, le.value
+
+    def traversal(self, q: int):
+        """[(i, j)] int32 [n][2], s_in [n], s_out [n]."""
+        cap = 2 * (self.nx + self.ny) + 8
+        ij = np.zeros(2 * cap, np.int32)
+        si = np.zeros(cap)
+        so = np.zeros(cap)
+        n = lib().or_traversal(self.h, q, ij, si, so, cap)
+        assert n <= cap
+        return ij[:2 * n].reshape(n, 2), si[:n], so[:n]
+
+    def path_lengths(self, H: np.ndarray, with_min_g1: bool = False):
+        """H [C][2][nx][ny] -> L [C][R][3] (muck, air, rock), O [C][R] (, min|g'| [C][R])."""
+        H = np.ascontiguousarray(H, np.float64).reshape(-1, 2, self.nx, self.ny)
+        C = H.shape[0]
+        L = np.zeros((C, self.R, 3))
+        O = np.zeros((C, self.R))
+        mg = np.zeros((C, self.R)) if with_min_g1 else None
+        lib().or_path_lengths(self.h, C, H, L, O, mg.ctypes.data if with_min_g1 else None)
+        return (L, O, mg) if with_min_g1 else (L, O)
+
+    def loglik_grad_H(self, H: np.ndarray, with_sens: bool = False):
+        """Per chain ll_dev, ll_std, dll/dH [C][2][nx][ny] (, sens) and work counters."""
+        H = np.ascontiguousarray(H, np.float64).reshape(-1, 2, self.nx, self.ny)
+        C = H.shape[0]
+        ll = np.zeros(C)
+        lls = np.zeros(C)
+        G = np.zeros_like(H)
+        sens = np.zeros(C)
+        cnt = np.zeros(4, np.int64)
+        lib().or_loglik_grad_H(self.h, C, H, ll, lls, G, sens.ctypes.data, cnt)
+        out = dict(ll_dev=ll, ll_std=lls, dldH=G, counters=cnt)
+        if with_sens:
+            out["sens"] = sens
+        return out
+
+    def logpost_grad(self, x: np.ndarray):
+        """x [C][P] -> dict(logp [C], grad [C][P], ll_dev, ll_std, prior, sens, counters)."""
+        x = np.ascontiguousarray(x, np.float64).reshape(-1, self.P)
+        C = x.shape[0]
+        logp = np.zeros(C)
+        g = np.zeros_like(x)
+        ll = np.zeros(C)
+        lls = np.zeros(C)
+        pr = np.zeros(C)
+        sens = np.zeros(C)
+        cnt = np.zeros(4, np.int64)
+        lib().or_logpost_grad(self.h, C, x, logp, g, ll, lls, pr, sens.ctypes.data, cnt)
+        return dict(logp=logp, grad=g, ll_dev=ll, ll_std=lls, prior=pr, sens=sens, counters=cnt)
+
+    def loglik_offset(self) -> float:
+        """Σ_p (C ln C - C - ln Γ(C+1)): ll_std - ll_dev (R15)."""
+        c = np.asarray(self.prob["counts"], np.float64)
+        t = np.where(c > 0, c * np.log(np.where(c > 0, c, 1.0)), 0.0) - c
+        from scipy.special import gammaln
+        return float(np.sum(t - gammaln(c + 1.0)))
+
+    # -- inverse map (for chain placement only) -------------------------
+    def latent_from_heights(self, H: np.ndarray) -> np.ndarray:
+        """x with heights(x) = H: x0 = σ0 Φ^-1(H0/z_top), x1 = σ1 Φ^-1((H1-H0)/(z_top-H0))."""
+        from scipy.special import ndtri
+        s = self.sigma()
+        H = np.asarray(H, np.float64).reshape(2, self.nx, self.ny)
+        x0 = s[0] * ndtri(H[0] / self.z_top)
+        x1 = s[1] * ndtri((H[1] - H[0]) / (self.z_top - H[0]))
+        return np.stack([x0, x1]).reshape(-1)
+
+
+# ---------------------------------------------------------------------------
+# Hamiltonian Monte Carlo.  Plain Python: velocity-Verlet with
+# identity mass (R19), accept iff ln u < -ΔH (Metropolis correction).
+# ---------------------------------------------------------------------------
+
+def leapfrog(x, p, eps, L, logp_grad):
+    """L kick-drift-kick steps.  logp_grad(x [C][P]) -> (logp [C], grad [C][P]).
+
+    eps: scalar or [C].  Returns (x, p, logp, grad) after L steps.
+    """
+    x = np.array(x, np.float64)
+    p = np.array(p, np.float64)
+    e = np.asarray(eps, np.float64).reshape(-1, 1) if np.ndim(eps) else float(eps)
+    lp, g = logp_grad(x)
+    for _ in range(L):
+        p = p + 0.5 * e * g
+        x = x + e * p
+        lp, g = logp_grad(x)
+        p = p + 0.5 * e * g
+    return x, p, lp, g
+
+
+def hmc_step(x, eps, L, logp_grad, seed, it, chain_offset=0):
+    """One HMC transition per chain with Philox momenta and MH uniforms.
+
+    Returns (x_new, accept_prob [C], accepted [C] bool, logp_new, dH [C]).
+    """
+    x = np.array(x, np.float64)
+    C, P = x.shape
+    p0 = np.stack([momenta(P, seed, it, chain_offset + c) for c in range(C)])
+    lp0, _ = logp_grad(x)
+    x1, p1, lp1, _ = leapfrog(x, p0, eps, L, logp_grad)
+    H0 = -lp0 + 0.5 * np.sum(p0 * p0, axis=1)
+    H1 = -lp1 + 0.5 * np.sum(p1 * p1, axis=1)
+    dH = H1 - H0
+    u = np.array([mh_uniform(seed, it, chain_offset + c) for c in range(C)])
+    with np.errstate(over="ignore", invalid="ignore"):
+        acc_prob = np.where(np.isfinite(dH), np.minimum(1.0, np.exp(-dH)), 0.0)
+    accepted = np.isfinite(dH) & (dH <= 1000.0) & (np.log(u) < -dH)
+    x_new = np.where(accepted[:, None], x1, x)
+    lp_new = np.where(accepted, lp1, lp0)
+    return x_new, acc_prob, accepted, lp_new, dH
