@@ -1,0 +1,191 @@
+/*
+ * mt.h — C ABI of the B200-native hot path of arXiv 2603.28907 ("Bayesian
+ * muon tomography of block caves"): batched log-posterior + gradient over cave
+ * geometries for many MCMC chains x many detector rays, and the fused HMC
+ * leapfrog that consumes it.
+ *
+ * Citations: "P:a-b" = PAPER.md lines a-b (paper text, /root/reference at build
+ * time); "R<k>" = reading k in DESIGN.md "Readings of the paper".
+ *
+ * CONVENTIONS (all entry points)
+ *  - Return 0 (MT_OK) or a nonzero MT_E* code; mt_last_error() gives a
+ *    thread-local message for the last nonzero return.
+ *  - Ownership: mt_problem_create deep-copies every host array it is given;
+ *    the caller may free them on return.  The problem owns its device buffers
+ *    and workspace; mt_problem_destroy frees them.  State arrays (x, p, grad,
+ *    logp, eps, status, accept_prob, accepted, H, dldH, L, O) are CALLER-OWNED
+ *    DEVICE memory on the problem's device (e.g. torch CUDA tensors),
+ *    C-contiguous; the library never frees them.
+ *  - Layout of one chain's parameter block (P = 2*n_x*n_y floats): [l][ix][iy],
+ *    iy fastest (right-most-fastest); l = 0 muck top (paper layer
+ *    1), l = 1 cave back (paper layer 2) (R4).  A state block is
+ *    [C][P].  Heights H and dldH use the same [C][2][n_x][n_y] layout, metres
+ *    above the detector plane z = 0 (R5).
+ *  - Streams: per-evaluation calls are asynchronous and stream-ordered on the
+ *    given cudaStream_t (NULL = legacy default stream); there is no implicit
+ *    device sync.  One stream at a time per problem (the workspace is not
+ *    re-entrant).  mt_problem_create / destroy and mt_debug_traversal are
+ *    synchronous.  Per-evaluation calls are CUDA-graph capturable.
+ *  - Non-finite results are not an error return: per-chain status bits
+ *    (1 = non-finite logp/grad, 2 = HMC divergence, rejected).
+ */
+#ifndef MT_H
+#define MT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mt_problem mt_problem;
+typedef struct CUstream_st *mt_stream; /* == cudaStream_t */
+
+enum {
+  MT_OK = 0,
+  MT_EINVAL = 1, /* bad descriptor / argument (message says which) */
+  MT_ENOMEM = 2, /* device or host allocation failed */
+  MT_ECUDA = 3,  /* CUDA runtime error (message holds cudaGetErrorString) */
+  MT_ENCCL = 4,  /* reserved: in-library collectives */
+  MT_ESTATE = 5  /* call not valid in the current state */
+};
+
+enum { MT_STATUS_NONFINITE = 1, MT_STATUS_DIVERGENT = 2 };
+
+/* Problem description (all pointers are HOST memory, read during create).
+ * Geometry (R2/R3): control nodes at (node_x[i], node_y[j]); the
+ * surfaces are bilinear in each cell.  Coordinates must be multiples of
+ * 2^-12 m with |v| < 2^11 m (exact traversal predicates, HP3).
+ * Rays (R10/R11): one ray per pixel from detector ray_det[p] in unit
+ * direction ray_dir[p] (d_z > 0); expected counts λ_p = ray_w[p]*exp(-O_p/att_len)
+ * (R9) with opacity O_p = ∫ρ du through muck (z < H0), air
+ * (H0 <= z < H1), rock (H1 <= z < z_top) inside the footprint and rho_ext
+ * beyond a side exit up to z_top (R7).  Observed counts C_p ~ Poisson(λ_p)
+ * (P:403-404).  Prior (R13/R14): x_l ~ N(0, Q_l^-1), Q_l = 4I - r_l A
+ * on the periodic 4-neighbour grid, heights by the Gaussian copula
+ * ǔ = Φ(x/σ_l) and stick-breaking H0 = ǔ0 z_top, H1 = H0 + ǔ1 (z_top - H0). */
+typedef struct {
+  int32_t n_x, n_y;          /* nodes per axis, >= 3, n_x*n_y <= 4096 */
+  const float *node_x;       /* [n_x] strictly increasing */
+  const float *node_y;       /* [n_y] strictly increasing */
+  float z_top;               /* known flat top surface (m above z = 0) (R6) */
+  float rho_muck, rho_air, rho_rock, rho_ext; /* g/cm^3, >= 0 (R8) */
+  float att_len;             /* Λ > 0, g/cm^3*m (R9) */
+  float car_r[2];            /* CAR r_l in [0, 1) */
+  int32_t n_det;
+  const float *det_xyz;      /* [n_det][3]; x,y strictly inside the footprint, z == 0 */
+  int64_t n_rays;
+  const int32_t *ray_det;    /* [n_rays] detector index */
+  const float *ray_dir;      /* [n_rays][3] unit (|1-|d|| <= 1e-6), d_z > 0 */
+  const float *ray_w;        /* [n_rays] exposure x solid angle x efficiency, > 0 */
+  const int32_t *counts;     /* [n_rays] observed C_p >= 0 */
+  int64_t ray_lo, ray_hi;    /* this rank's ray shard [ray_lo, ray_hi); (0, n_rays) unsharded */
+  int32_t device;            /* CUDA device ordinal */
+  int32_t max_chains;        /* capacity of the per-chain workspace */
+} mt_problem_desc;
+
+/* Validate the description, precompute per-ray constants (in-box extent,
+ * exterior rock length, deviance-centred log-weight) in double on the host,
+ * upload them as an fp32 SoA, allocate the workspace.  Synchronous.
+ * Errors: MT_EINVAL (message names the offending field), MT_ENOMEM, MT_ECUDA. */
+int mt_problem_create(const mt_problem_desc *desc, mt_problem **out);
+
+/* Free everything the problem owns.  NULL-safe.  Synchronous. */
+int mt_problem_destroy(mt_problem *p);
+
+/* P = 2*n_x*n_y parameters per chain; rays in this shard. */
+int32_t mt_num_params(const mt_problem *p);
+int64_t mt_num_rays(const mt_problem *p);
+
+/* Σ_p (C_p ln C_p - C_p - ln Γ(C_p+1)) over this shard: add it to the
+ * deviance-centred log-likelihood returned below to get the standard Poisson
+ * log-likelihood Σ_p [C_p ln λ_p - λ_p - ln Γ(C_p+1)] (R15). */
+double mt_loglik_offset(const mt_problem *p);
+
+/* σ_l (marginal std of the torus CAR field, P:589-590 / R14) and ln det Q_l. */
+int mt_prior_constants(const mt_problem *p, double sigma[2], double logdetQ[2]);
+
+/* Unnormalised log-posterior and its gradient for C chains.
+ *   x     [C][P] float  latent CAR fields (device)
+ *   logp  [C]   double  Σ_p ℓ_p^dev + Σ_l log N(x_l; 0, Q_l^-1)   (device)
+ *                       where ℓ_p^dev = C_p(ln λ_p - ln C_p) - λ_p + C_p (R15)
+ *   grad  [C][P] float  ∂logp/∂x (device)
+ *   status[C] int32 or NULL (device)
+ * With a ray shard (ray_lo > 0 or ray_hi < n_rays) the likelihood part covers
+ * the shard only and the prior is added on the shard with ray_lo == 0, so a
+ * SUM over shards gives the full result.  Errors: MT_EINVAL (C < 0,
+ * C > max_chains, NULL pointer), MT_ECUDA. */
+int mt_logpost_grad(mt_problem *p, int32_t C, const float *x, double *logp, float *grad,
+                    int32_t *status, mt_stream stream);
+
+/* L velocity-Verlet (kick-drift-kick) steps with identity mass (P:625-642,
+ * R19), per-chain step size eps[C] (device).  On entry logp/grad must hold the
+ * values at x (e.g. from mt_logpost_grad); on return x, p, logp, grad are
+ * advanced by L steps.  L >= 0. */
+int mt_leapfrog(mt_problem *p, int32_t C, float *x, float *mom, double *logp, float *grad,
+                const float *eps, int32_t L, mt_stream stream);
+
+/* Momenta p ~ N(0, I) from Philox4x32-10: key = (seed lo, seed hi), counter =
+ * (q, chain_offset + c, iter mod 2^32, 0) for parameters 4q..4q+3, uniforms
+ * (k + 1/2) 2^-32, Box-Muller on word pairs (0,1), (2,3) (R22). */
+int mt_draw_momenta(mt_problem *p, int32_t C, float *mom, uint64_t seed, uint64_t iter,
+                    uint64_t chain_offset, mt_stream stream);
+
+/* One HMC transition per chain: draw momenta as above, L leapfrog
+ * steps, Hamiltonian H = -logp + |p|^2/2, accept iff ln u < -ΔH with u from
+ * Philox counter (0, chain, iter, 1) word 0; divergent (ΔH > 1000 or
+ * non-finite) proposals are rejected and flagged.  x/logp/grad are updated in
+ * place (restored on reject).  accept_prob [C] float = min(1, exp(-ΔH));
+ * accepted [C] int32; status [C] or NULL. */
+int mt_hmc_step(mt_problem *p, int32_t C, float *x, double *logp, float *grad, const float *eps,
+                int32_t L, uint64_t seed, uint64_t iter, uint64_t chain_offset, float *accept_prob,
+                int32_t *accepted, int32_t *status, mt_stream stream);
+
+/* ---- parity / debug entry points (not on the hot path) ---------------- */
+
+/* Heights map of x (device [C][P] -> device H [C][2][n_x][n_y]). */
+int mt_heights(mt_problem *p, int32_t C, const float *x, float *H, mt_stream stream);
+
+/* Deviance-centred log-likelihood (device ll [C], double) and ∂ll/∂H (device
+ * dldH [C][2][n_x][n_y]) for caller-given heights H (device, same layout):
+ * the trace/adjoint path alone. */
+int mt_loglik_heights(mt_problem *p, int32_t C, const float *H, double *ll, float *dldH,
+                      mt_stream stream);
+
+/* In-box path lengths per (chain, ray of this shard): L [C][R][3] = (muck,
+ * air, rock) and opacity O [C][R] (device) for caller-given heights H. */
+int mt_path_lengths(mt_problem *p, int32_t C, const float *H, float *L, float *O,
+                    mt_stream stream);
+
+/* Ordered cells (i, j) of ray `ray` (index within this shard), with s_in,
+ * s_out; HOST outputs, up to cap entries, *n = number of cells.  Synchronous;
+ * runs the same device traversal the trace kernel uses. */
+int mt_debug_traversal(mt_problem *p, int64_t ray, int32_t *ij, float *s_in, float *s_out,
+                       int32_t cap, int32_t *n);
+
+/* Raw Philox4x32-10 words (device in ctr [n][4], out [n][4]; key host). */
+int mt_philox(const uint32_t *ctr, uint32_t key0, uint32_t key1, uint32_t *out, int64_t n,
+              mt_stream stream);
+/* Same counters through cuRAND's curand_Philox4x32_10 (library cross-check). */
+int mt_philox_curand(const uint32_t *ctr, uint32_t key0, uint32_t key1, uint32_t *out, int64_t n,
+                     mt_stream stream);
+
+/* ---- measurement ------------------------------------------------------- */
+
+/* Start/stop recording CUDA events around every trace-kernel launch (on the
+ * launching stream).  mt_timing_read returns the summed device time of the
+ * trace launches (ms), their number, the chain x ray pairs they processed, and
+ * the total number of kernels this problem launched since mt_timing_start. */
+int mt_timing_start(mt_problem *p, int32_t max_records);
+int mt_timing_read(mt_problem *p, double *trace_ms, int64_t *trace_launches, double *pairs,
+                   int64_t *all_launches);
+
+/* FP32 FFMA throughput microbenchmark on `device` (TFLOP/s, FMA = 2 flops). */
+int mt_measure_fp32_peak(int32_t device, double *tflops, double *sm_clock_mhz);
+
+const char *mt_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MT_H */

@@ -1,0 +1,294 @@
+"""Thin ctypes binding of libmt.so (include/mt.h).  Argument marshalling only:
+every step of the hot path runs in the CUDA kernels behind the C ABI.  PyTorch
+supplies device memory and streams.  There is no fallback: if libmt.so is
+missing or no CUDA device is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(_HERE, "libmt.so")
+
+MT_STATUS_NONFINITE = 1
+MT_STATUS_DIVERGENT = 2
+
+
+class MTError(RuntimeError):
+    pass
+
+
+class _Desc(ct.Structure):
+    _fields_ = [
+        ("n_x", ct.c_int32), ("n_y", ct.c_int32),
+        ("node_x", ct.c_void_p), ("node_y", ct.c_void_p),
+        ("z_top", ct.c_float),
+        ("rho_muck", ct.c_float), ("rho_air", ct.c_float), ("rho_rock", ct.c_float), ("rho_ext", ct.c_float),
+        ("att_len", ct.c_float),
+        ("car_r", ct.c_float * 2),
+        ("n_det", ct.c_int32), ("det_xyz", ct.c_void_p),
+        ("n_rays", ct.c_int64), ("ray_det", ct.c_void_p), ("ray_dir", ct.c_void_p),
+        ("ray_w", ct.c_void_p), ("counts", ct.c_void_p),
+        ("ray_lo", ct.c_int64), ("ray_hi", ct.c_int64),
+        ("device", ct.c_int32), ("max_chains", ct.c_int32),
+    ]
+
+
+EXPORTS = [
+    "mt_problem_create", "mt_problem_destroy", "mt_num_params", "mt_num_rays", "mt_loglik_offset",
+    "mt_prior_constants", "mt_logpost_grad", "mt_leapfrog", "mt_draw_momenta", "mt_hmc_step",
+    "mt_heights", "mt_loglik_heights", "mt_path_lengths", "mt_debug_traversal", "mt_philox",
+    "mt_philox_curand", "mt_timing_start", "mt_timing_read", "mt_measure_fp32_peak", "mt_last_error",
+]
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(SO_PATH):
+            raise MTError(f"{SO_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ct.CDLL(SO_PATH)
+        vp, i32, i64, u32, u64, dbl = ct.c_void_p, ct.c_int32, ct.c_int64, ct.c_uint32, ct.c_uint64, ct.c_double
+        sig = {
+            "mt_problem_create": ([ct.POINTER(_Desc), ct.POINTER(vp)], ct.c_int),
+            "mt_problem_destroy": ([vp], ct.c_int),
+            "mt_num_params": ([vp], i32),
+            "mt_num_rays": ([vp], i64),
+            "mt_loglik_offset": ([vp], dbl),
+            "mt_prior_constants": ([vp, vp, vp], ct.c_int),
+            "mt_logpost_grad": ([vp, i32, vp, vp, vp, vp, vp], ct.c_int),
+            "mt_leapfrog": ([vp, i32, vp, vp, vp, vp, vp, i32, vp], ct.c_int),
+            "mt_draw_momenta": ([vp, i32, vp, u64, u64, u64, vp], ct.c_int),
+            "mt_hmc_step": ([vp, i32, vp, vp, vp, vp, i32, u64, u64, u64, vp, vp, vp, vp], ct.c_int),
+            "mt_heights": ([vp, i32, vp, vp, vp], ct.c_int),
+            "mt_loglik_heights": ([vp, i32, vp, vp, vp, vp], ct.c_int),
+            "mt_path_lengths": ([vp, i32, vp, vp, vp, vp], ct.c_int),
+            "mt_debug_traversal": ([vp, i64, vp, vp, vp, i32, vp], ct.c_int),
+            "mt_philox": ([vp, u32, u32, vp, i64, vp], ct.c_int),
+            "mt_philox_curand": ([vp, u32, u32, vp, i64, vp], ct.c_int),
+            "mt_timing_start": ([vp, i32], ct.c_int),
+            "mt_timing_read": ([vp, vp, vp, vp, vp], ct.c_int),
+            "mt_measure_fp32_peak": ([i32, vp, vp], ct.c_int),
+            "mt_last_error": ([], ct.c_char_p),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        msg = lib().mt_last_error().decode(errors="replace")
+        raise MTError(f"{what} failed (code {rc}): {msg}")
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def _dev_tensor(t, dtype, shape, device, name):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise MTError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype or not t.is_contiguous():
+        raise MTError(f"{name} must be contiguous {dtype}")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise MTError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if t.device.index != device:
+        raise MTError(f"{name} is on cuda:{t.device.index}, problem on cuda:{device}")
+    return t
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ct.c_void_p(s.cuda_stream)
+
+
+class Problem:
+    """A canonical problem bound to one CUDA device (mt_problem_create)."""
+
+    def __init__(self, prob: dict, device: int = 0, max_chains: int = 1,
+                 ray_lo: int = 0, ray_hi: Optional[int] = None):
+        self._keep = {
+            "node_x": np.ascontiguousarray(prob["node_x"], np.float32),
+            "node_y": np.ascontiguousarray(prob["node_y"], np.float32),
+            "det_xyz": np.ascontiguousarray(prob["det_xyz"], np.float32),
+            "ray_det": np.ascontiguousarray(prob["ray_det"], np.int32),
+            "ray_dir": np.ascontiguousarray(prob["ray_dir"], np.float32),
+            "ray_w": np.ascontiguousarray(prob["ray_w"], np.float32),
+            "counts": np.ascontiguousarray(prob["counts"], np.int32),
+        }
+        k = self._keep
+        R = len(k["ray_det"])
+        d = _Desc()
+        d.n_x, d.n_y = len(k["node_x"]), len(k["node_y"])
+        d.node_x, d.node_y = k["node_x"].ctypes.data, k["node_y"].ctypes.data
+        d.z_top = float(prob["z_top"])
+        d.rho_muck, d.rho_air = float(prob["rho_muck"]), float(prob["rho_air"])
+        d.rho_rock, d.rho_ext = float(prob["rho_rock"]), float(prob["rho_ext"])
+        d.att_len = float(prob["att_len"])
+        d.car_r[0], d.car_r[1] = float(prob["car_r"][0]), float(prob["car_r"][1])
+        d.n_det = len(k["det_xyz"])
+        d.det_xyz = k["det_xyz"].ctypes.data
+        d.n_rays = R
+        d.ray_det, d.ray_dir = k["ray_det"].ctypes.data, k["ray_dir"].ctypes.data
+        d.ray_w, d.counts = k["ray_w"].ctypes.data, k["counts"].ctypes.data
+        d.ray_lo = ray_lo
+        d.ray_hi = R if ray_hi is None else ray_hi
+        d.device = device
+        d.max_chains = max_chains
+        h = ct.c_void_p()
+        _check(lib().mt_problem_create(ct.byref(d), ct.byref(h)), "mt_problem_create")
+        self.h = h
+        self.device = device
+        self.max_chains = max_chains
+        self.nx, self.ny = d.n_x, d.n_y
+        self.P = lib().mt_num_params(h)
+        self.R = lib().mt_num_rays(h)
+        self.loglik_offset = lib().mt_loglik_offset(h)
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            lib().mt_problem_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def prior_constants(self):
+        s = (ct.c_double * 2)()
+        ld = (ct.c_double * 2)()
+        _check(lib().mt_prior_constants(self.h, s, ld), "mt_prior_constants")
+        return list(s), list(ld)
+
+    # -- hot path ----------------------------------------------------------
+    def logpost_grad(self, x, logp=None, grad=None, status=None, stream=None):
+        import torch
+        C = x.shape[0]
+        _dev_tensor(x, torch.float32, (C, self.P), self.device, "x")
+        if logp is None:
+            logp = torch.empty(C, dtype=torch.float64, device=x.device)
+        if grad is None:
+            grad = torch.empty_like(x)
+        _check(lib().mt_logpost_grad(self.h, C, _ptr(x), _ptr(logp), _ptr(grad), _ptr(status),
+                                     _stream(stream)), "mt_logpost_grad")
+        return logp, grad
+
+    def leapfrog(self, x, p, logp, grad, eps, L: int, stream=None):
+        import torch
+        C = x.shape[0]
+        for t, n, dt, sh in ((x, "x", torch.float32, (C, self.P)), (p, "p", torch.float32, (C, self.P)),
+                             (logp, "logp", torch.float64, (C,)), (grad, "grad", torch.float32, (C, self.P)),
+                             (eps, "eps", torch.float32, (C,))):
+            _dev_tensor(t, dt, sh, self.device, n)
+        _check(lib().mt_leapfrog(self.h, C, _ptr(x), _ptr(p), _ptr(logp), _ptr(grad), _ptr(eps), L,
+                                 _stream(stream)), "mt_leapfrog")
+
+    def draw_momenta(self, C: int, seed: int, it: int, chain_offset: int = 0, out=None, stream=None):
+        import torch
+        if out is None:
+            out = torch.empty((C, self.P), dtype=torch.float32, device=f"cuda:{self.device}")
+        _check(lib().mt_draw_momenta(self.h, C, _ptr(out), seed, it, chain_offset, _stream(stream)),
+               "mt_draw_momenta")
+        return out
+
+    def hmc_step(self, x, logp, grad, eps, L: int, seed: int, it: int, chain_offset: int = 0,
+                 accept_prob=None, accepted=None, status=None, stream=None):
+        import torch
+        C = x.shape[0]
+        dev = x.device
+        if accept_prob is None:
+            accept_prob = torch.empty(C, dtype=torch.float32, device=dev)
+        if accepted is None:
+            accepted = torch.empty(C, dtype=torch.int32, device=dev)
+        for t, n, dt, sh in ((x, "x", torch.float32, (C, self.P)), (logp, "logp", torch.float64, (C,)),
+                             (grad, "grad", torch.float32, (C, self.P)), (eps, "eps", torch.float32, (C,))):
+            _dev_tensor(t, dt, sh, self.device, n)
+        _check(lib().mt_hmc_step(self.h, C, _ptr(x), _ptr(logp), _ptr(grad), _ptr(eps), L, seed, it,
+                                 chain_offset, _ptr(accept_prob), _ptr(accepted), _ptr(status),
+                                 _stream(stream)), "mt_hmc_step")
+        return accept_prob, accepted
+
+    # -- parity / debug ------------------------------------------------------
+    def heights(self, x, stream=None):
+        import torch
+        C = x.shape[0]
+        _dev_tensor(x, torch.float32, (C, self.P), self.device, "x")
+        H = torch.empty_like(x)
+        _check(lib().mt_heights(self.h, C, _ptr(x), _ptr(H), _stream(stream)), "mt_heights")
+        return H.view(C, 2, self.nx, self.ny)
+
+    def loglik_heights(self, H, stream=None):
+        import torch
+        C = H.shape[0]
+        H = H.reshape(C, self.P)
+        _dev_tensor(H, torch.float32, (C, self.P), self.device, "H")
+        ll = torch.empty(C, dtype=torch.float64, device=H.device)
+        G = torch.empty_like(H)
+        _check(lib().mt_loglik_heights(self.h, C, _ptr(H), _ptr(ll), _ptr(G), _stream(stream)),
+               "mt_loglik_heights")
+        return ll, G.view(C, 2, self.nx, self.ny)
+
+    def path_lengths(self, H, stream=None):
+        import torch
+        C = H.shape[0]
+        H = H.reshape(C, self.P)
+        _dev_tensor(H, torch.float32, (C, self.P), self.device, "H")
+        L = torch.empty((C, self.R, 3), dtype=torch.float32, device=H.device)
+        O = torch.empty((C, self.R), dtype=torch.float32, device=H.device)
+        _check(lib().mt_path_lengths(self.h, C, _ptr(H), _ptr(L), _ptr(O), _stream(stream)),
+               "mt_path_lengths")
+        return L, O
+
+    def debug_traversal(self, ray: int, cap: Optional[int] = None):
+        cap = cap or 2 * (self.nx + self.ny) + 8
+        ij = np.zeros(2 * cap, np.int32)
+        si = np.zeros(cap, np.float32)
+        so = np.zeros(cap, np.float32)
+        n = ct.c_int32()
+        _check(lib().mt_debug_traversal(self.h, ray, ij.ctypes.data, si.ctypes.data, so.ctypes.data,
+                                        cap, ct.byref(n)), "mt_debug_traversal")
+        m = n.value
+        assert m <= cap
+        return ij[:2 * m].reshape(m, 2), si[:m], so[:m]
+
+    # -- measurement ------------------------------------------------------------
+    def timing_start(self, max_records: int = 4096):
+        _check(lib().mt_timing_start(self.h, max_records), "mt_timing_start")
+
+    def timing_read(self):
+        ms, n, pairs, alln = ct.c_double(), ct.c_int64(), ct.c_double(), ct.c_int64()
+        _check(lib().mt_timing_read(self.h, ct.byref(ms), ct.byref(n), ct.byref(pairs), ct.byref(alln)),
+               "mt_timing_read")
+        return dict(trace_ms=ms.value, trace_launches=n.value, pairs=pairs.value, all_launches=alln.value)
+
+
+def philox(ctr, key, use_curand: bool = False, stream=None):
+    """Raw Philox4x32-10 words for device counters ctr [n][4] (uint32 as int32 tensor)."""
+    import torch
+    n = ctr.shape[0]
+    out = torch.empty_like(ctr)
+    f = lib().mt_philox_curand if use_curand else lib().mt_philox
+    _check(f(_ptr(ctr), key[0], key[1], _ptr(out), n, _stream(stream)), "mt_philox")
+    return out
+
+
+def measure_fp32_peak(device: int = 0):
+    tf, mhz = ct.c_double(), ct.c_double()
+    _check(lib().mt_measure_fp32_peak(device, ct.byref(tf), ct.byref(mhz)), "mt_measure_fp32_peak")
+    return tf.value, mhz.value

@@ -1,0 +1,464 @@
+// api.cu — C ABI of libmt (include/mt.h): problem validation and setup,
+// per-evaluation orchestration (heights -> trace -> finish), leapfrog and
+// HMC transitions, debug/parity exports, measurement hooks.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <new>
+#include <string>
+#include <vector>
+
+#include "mt_internal.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_err(cudaError_t e, const char *where) {
+  return set_err(MT_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define CK(call)                                                  \
+  do {                                                            \
+    cudaError_t e_ = (call);                                      \
+    if (e_ != cudaSuccess) return cuda_err(e_, #call);            \
+  } while (0)
+
+struct DevGuard {
+  int prev = -1, want;
+  explicit DevGuard(int d) : want(d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DevGuard() {
+    if (prev >= 0 && prev != want) cudaSetDevice(prev);
+  }
+};
+
+bool on_grid(double v) {  // multiple of 2^-12 with |v| < 2^11 (HP3)
+  return fabs(v) < 2048.0 && floor(v * 4096.0) == v * 4096.0;
+}
+
+// Torus spectrum of Q = 4I - rA: σ² = mean(1/λ_ab),
+// ln det Q = Σ ln λ_ab, λ_ab = 4 - 2r(cos 2πa/nx + cos 2πb/ny).
+void torus(int nx, int ny, double r, double *sigma, double *logdet) {
+  double s = 0, ld = 0;
+  for (int a = 0; a < nx; a++)
+    for (int b = 0; b < ny; b++) {
+      double lam = 4.0 - 2.0 * r * (cos(2.0 * M_PI * a / nx) + cos(2.0 * M_PI * b / ny));
+      s += 1.0 / lam;
+      ld += log(lam);
+    }
+  *sigma = sqrt(s / ((double)nx * ny));
+  *logdet = ld;
+}
+
+int check_ptr(const void *ptr, const char *name) {
+  if (!ptr) return set_err(MT_EINVAL, "%s is NULL", name);
+  return 0;
+}
+
+int check_chains(const mt_problem *p, int32_t C) {
+  if (!p) return set_err(MT_EINVAL, "problem is NULL");
+  if (C < 0) return set_err(MT_EINVAL, "C = %d < 0", C);
+  if (C > p->max_chains) return set_err(MT_EINVAL, "C = %d > max_chains = %d", C, p->max_chains);
+  return 0;
+}
+
+void free_all(mt_problem *p) {
+  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_H, p->d_G,
+                  p->d_band, p->d_ll, p->d_x0, p->d_g0, p->d_mom, p->d_kin0, p->d_kin1, p->d_lp0};
+  for (void *b : bufs)
+    if (b) cudaFree(b);
+  for (auto e : p->ev_a) cudaEventDestroy(e);
+  for (auto e : p->ev_b) cudaEventDestroy(e);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *mt_last_error(void) { return g_err.c_str(); }
+
+int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
+  if (!out) return set_err(MT_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!d) return set_err(MT_EINVAL, "desc is NULL");
+  // ---- validation (messages name the field) ----
+  if (d->n_x < 3 || d->n_y < 3) return set_err(MT_EINVAL, "n_x, n_y must be >= 3 (torus stencil)");
+  if (d->n_x > MT_MAX_AXIS || d->n_y > MT_MAX_AXIS || d->n_x * d->n_y > MT_MAX_NODES)
+    return set_err(MT_EINVAL, "grid %dx%d exceeds %d nodes per surface", d->n_x, d->n_y, MT_MAX_NODES);
+  if (check_ptr(d->node_x, "node_x") || check_ptr(d->node_y, "node_y")) return MT_EINVAL;
+  for (int i = 0; i < d->n_x; i++) {
+    if (!on_grid(d->node_x[i])) return set_err(MT_EINVAL, "node_x[%d] not on the 2^-12 m grid", i);
+    if (i && !(d->node_x[i] > d->node_x[i - 1])) return set_err(MT_EINVAL, "node_x not increasing at %d", i);
+  }
+  for (int j = 0; j < d->n_y; j++) {
+    if (!on_grid(d->node_y[j])) return set_err(MT_EINVAL, "node_y[%d] not on the 2^-12 m grid", j);
+    if (j && !(d->node_y[j] > d->node_y[j - 1])) return set_err(MT_EINVAL, "node_y not increasing at %d", j);
+  }
+  if (!(d->z_top > 0) || !isfinite(d->z_top)) return set_err(MT_EINVAL, "z_top must be > 0");
+  if (!(d->rho_muck >= 0 && d->rho_air >= 0 && d->rho_rock >= 0 && d->rho_ext >= 0))
+    return set_err(MT_EINVAL, "densities must be >= 0");
+  if (!(d->att_len > 0) || !isfinite(d->att_len)) return set_err(MT_EINVAL, "att_len must be > 0");
+  for (int l = 0; l < 2; l++)
+    if (!(d->car_r[l] >= 0.f && d->car_r[l] < 1.f)) return set_err(MT_EINVAL, "car_r[%d] not in [0,1)", l);
+  if (d->n_det < 1 || check_ptr(d->det_xyz, "det_xyz")) return set_err(MT_EINVAL, "n_det < 1 or det_xyz NULL");
+  float X0 = d->node_x[0], X1 = d->node_x[d->n_x - 1], Y0 = d->node_y[0], Y1 = d->node_y[d->n_y - 1];
+  for (int k = 0; k < d->n_det; k++) {
+    const float *o = d->det_xyz + 3 * k;
+    if (!on_grid(o[0]) || !on_grid(o[1])) return set_err(MT_EINVAL, "det_xyz[%d] not on the 2^-12 m grid", k);
+    if (!(o[0] > X0 && o[0] < X1 && o[1] > Y0 && o[1] < Y1))
+      return set_err(MT_EINVAL, "detector %d not strictly inside the footprint", k);
+    if (o[2] != 0.f) return set_err(MT_EINVAL, "detector %d: z must be 0 (the floor, R5)", k);
+  }
+  if (d->n_rays < 0) return set_err(MT_EINVAL, "n_rays < 0");
+  if (d->n_rays > 0 && (check_ptr(d->ray_det, "ray_det") || check_ptr(d->ray_dir, "ray_dir") ||
+                        check_ptr(d->ray_w, "ray_w") || check_ptr(d->counts, "counts")))
+    return MT_EINVAL;
+  if (d->ray_lo < 0 || d->ray_hi < d->ray_lo || d->ray_hi > d->n_rays)
+    return set_err(MT_EINVAL, "ray shard [%lld, %lld) invalid", (long long)d->ray_lo, (long long)d->ray_hi);
+  if (d->max_chains < 0) return set_err(MT_EINVAL, "max_chains < 0");
+  for (int64_t q = d->ray_lo; q < d->ray_hi; q++) {
+    if (d->ray_det[q] < 0 || d->ray_det[q] >= d->n_det) return set_err(MT_EINVAL, "ray_det[%lld] out of range", (long long)q);
+    const float *v = d->ray_dir + 3 * q;
+    double nrm = sqrt((double)v[0] * v[0] + (double)v[1] * v[1] + (double)v[2] * v[2]);
+    if (!(v[2] > 0.f)) return set_err(MT_EINVAL, "ray_dir[%lld]: d_z must be > 0", (long long)q);
+    if (!(fabs(nrm - 1.0) <= 1e-6)) return set_err(MT_EINVAL, "ray_dir[%lld] not unit (|d| = %.9g)", (long long)q, nrm);
+    if (!(d->ray_w[q] > 0.f) || !isfinite(d->ray_w[q])) return set_err(MT_EINVAL, "ray_w[%lld] must be > 0", (long long)q);
+    if (d->counts[q] < 0 || d->counts[q] >= (1 << 24)) return set_err(MT_EINVAL, "counts[%lld] out of range", (long long)q);
+  }
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (d->device < 0 || d->device >= ndev) return set_err(MT_EINVAL, "device %d not present (%d devices)", d->device, ndev);
+
+  mt_problem *p = new (std::nothrow) mt_problem();
+  if (!p) return set_err(MT_ENOMEM, "host allocation failed");
+  DevGuard g(d->device);
+  p->device = d->device;
+  cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, d->device);
+  p->nx = d->n_x; p->ny = d->n_y; p->N = d->n_x * d->n_y; p->P = 2 * p->N;
+  p->R = d->ray_hi - d->ray_lo;
+  p->ray_lo = d->ray_lo;
+  p->max_chains = d->max_chains;
+  p->z_top = d->z_top;
+  p->car_r[0] = d->car_r[0]; p->car_r[1] = d->car_r[1];
+  p->prior_on = d->ray_lo == 0;
+  for (int l = 0; l < 2; l++) torus(p->nx, p->ny, d->car_r[l], &p->sigma[l], &p->logdetQ[l]);
+  p->tc.nx = p->nx; p->tc.ny = p->ny; p->tc.N = p->N;
+  p->tc.z_top = d->z_top;
+  p->tc.k0 = d->rho_muck - d->rho_air;
+  p->tc.k1 = d->rho_air - d->rho_rock;
+  p->tc.inv_att = (float)(1.0 / (double)d->att_len);
+  if (const char *e = getenv("MT_TRACE_K")) p->trace_k = atoi(e);
+  if (const char *e = getenv("MT_TRACE_S")) p->trace_s = atoi(e);
+
+  // ---- per-ray constants in double (a0) ----
+  std::vector<float4> ra(p->R), rb(p->R);
+  std::vector<float> ob(p->R);
+  double off = 0.0;
+  const double Lam = d->att_len;
+  for (int64_t q = 0; q < p->R; q++) {
+    int64_t g_ = d->ray_lo + q;
+    const float *o = d->det_xyz + 3 * d->ray_det[g_];
+    const float *v = d->ray_dir + 3 * g_;
+    double dx = v[0], dy = v[1], dz = v[2];
+    double s_top = ((double)d->z_top - o[2]) / dz, s = s_top;
+    if (dx > 0) s = fmin(s, ((double)X1 - o[0]) / dx);
+    if (dx < 0) s = fmin(s, ((double)X0 - o[0]) / dx);
+    if (dy > 0) s = fmin(s, ((double)Y1 - o[1]) / dy);
+    if (dy < 0) s = fmin(s, ((double)Y0 - o[1]) / dy);
+    double L_ext = s_top - s;
+    double C = d->counts[g_], w = d->ray_w[g_];
+    double obase = (double)d->rho_rock * s + (double)d->rho_ext * L_ext;
+    double tb = log(w) - (C > 0 ? log(C) : 0.0) - obase / Lam;
+    ra[q] = make_float4(o[0], o[1], v[0], v[1]);
+    rb[q] = make_float4(v[2], (float)s, (float)tb, (float)C);
+    ob[q] = (float)obase;
+    off += (C > 0 ? C * log(C) : 0.0) - C - lgamma(C + 1.0);
+  }
+  p->loglik_offset = off;
+
+  // ---- device buffers ----
+  size_t R = (size_t)(p->R > 0 ? p->R : 1), MC = (size_t)(p->max_chains > 0 ? p->max_chains : 1);
+  size_t P = p->P;
+  cudaError_t e = cudaSuccess;
+#define ALLOC(ptr, bytes)                                        \
+  if (e == cudaSuccess) e = cudaMalloc((void **)&(ptr), (bytes));
+  ALLOC(p->d_X, sizeof(float) * p->nx);
+  ALLOC(p->d_Y, sizeof(float) * p->ny);
+  ALLOC(p->d_ray_a, sizeof(float4) * R);
+  ALLOC(p->d_ray_b, sizeof(float4) * R);
+  ALLOC(p->d_obase, sizeof(float) * R);
+  ALLOC(p->d_H, sizeof(float) * MC * P);
+  ALLOC(p->d_G, sizeof(float) * MC * P);
+  ALLOC(p->d_band, sizeof(float4) * MC);
+  ALLOC(p->d_ll, sizeof(double) * MC);
+  ALLOC(p->d_x0, sizeof(float) * MC * P);
+  ALLOC(p->d_g0, sizeof(float) * MC * P);
+  ALLOC(p->d_mom, sizeof(float) * MC * P);
+  ALLOC(p->d_kin0, sizeof(float) * MC);
+  ALLOC(p->d_kin1, sizeof(float) * MC);
+  ALLOC(p->d_lp0, sizeof(double) * MC);
+#undef ALLOC
+  if (e != cudaSuccess) {
+    free_all(p);
+    delete p;
+    return e == cudaErrorMemoryAllocation ? set_err(MT_ENOMEM, "cudaMalloc: %s", cudaGetErrorString(e))
+                                          : cuda_err(e, "cudaMalloc");
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(p->d_X, d->node_x, sizeof(float) * p->nx, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(p->d_Y, d->node_y, sizeof(float) * p->ny, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && p->R > 0) e = cudaMemcpy(p->d_ray_a, ra.data(), sizeof(float4) * p->R, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && p->R > 0) e = cudaMemcpy(p->d_ray_b, rb.data(), sizeof(float4) * p->R, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && p->R > 0) e = cudaMemcpy(p->d_obase, ob.data(), sizeof(float) * p->R, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(p->d_G, 0, sizeof(float) * MC * P);
+  if (e == cudaSuccess) e = cudaMemset(p->d_ll, 0, sizeof(double) * MC);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    free_all(p);
+    delete p;
+    return cuda_err(e, "mt_problem_create upload");
+  }
+  *out = p;
+  return MT_OK;
+}
+
+int mt_problem_destroy(mt_problem *p) {
+  if (!p) return MT_OK;
+  DevGuard g(p->device);
+  cudaDeviceSynchronize();
+  free_all(p);
+  delete p;
+  return MT_OK;
+}
+
+int32_t mt_num_params(const mt_problem *p) { return p ? p->P : 0; }
+int64_t mt_num_rays(const mt_problem *p) { return p ? p->R : 0; }
+double mt_loglik_offset(const mt_problem *p) { return p ? p->loglik_offset : 0.0; }
+
+int mt_prior_constants(const mt_problem *p, double sigma[2], double logdetQ[2]) {
+  if (!p || !sigma || !logdetQ) return set_err(MT_EINVAL, "NULL argument");
+  for (int l = 0; l < 2; l++) { sigma[l] = p->sigma[l]; logdetQ[l] = p->logdetQ[l]; }
+  return MT_OK;
+}
+
+int mt_logpost_grad(mt_problem *p, int32_t C, const float *x, double *logp, float *grad,
+                    int32_t *status, mt_stream stream) {
+  if (int r = check_chains(p, C)) return r;
+  if (C == 0) return MT_OK;
+  if (check_ptr(x, "x") || check_ptr(logp, "logp") || check_ptr(grad, "grad")) return MT_EINVAL;
+  DevGuard g(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(launch_heights(p, C, x, p->d_H, p->d_band, s));
+  CK(launch_trace(p, TRACE_LL, C, p->d_H, p->d_band, p->d_G, p->d_ll, nullptr, nullptr, s));
+  CK(launch_finish(p, FIN_PLAIN, C, const_cast<float *>(x), grad, logp, status, nullptr, nullptr,
+                   nullptr, s));
+  return MT_OK;
+}
+
+int mt_leapfrog(mt_problem *p, int32_t C, float *x, float *mom, double *logp, float *grad,
+                const float *eps, int32_t L, mt_stream stream) {
+  if (int r = check_chains(p, C)) return r;
+  if (L < 0) return set_err(MT_EINVAL, "L = %d < 0", L);
+  if (C == 0 || L == 0) return MT_OK;
+  if (check_ptr(x, "x") || check_ptr(mom, "p") || check_ptr(logp, "logp") || check_ptr(grad, "grad") ||
+      check_ptr(eps, "eps"))
+    return MT_EINVAL;
+  DevGuard g(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(launch_kick_drift(p, C, x, mom, grad, eps, s));
+  for (int step = 1; step <= L; step++) {
+    CK(launch_trace(p, TRACE_LL, C, p->d_H, p->d_band, p->d_G, p->d_ll, nullptr, nullptr, s));
+    CK(launch_finish(p, step < L ? FIN_STEP : FIN_LAST, C, x, grad, logp, nullptr, mom, eps,
+                     p->d_kin1, s));
+  }
+  return MT_OK;
+}
+
+int mt_draw_momenta(mt_problem *p, int32_t C, float *mom, uint64_t seed, uint64_t iter,
+                    uint64_t chain_offset, mt_stream stream) {
+  if (int r = check_chains(p, C)) return r;
+  if (C == 0) return MT_OK;
+  if (check_ptr(mom, "p")) return MT_EINVAL;
+  DevGuard g(p->device);
+  CK(launch_momenta(p, C, mom, seed, iter, chain_offset, (cudaStream_t)stream));
+  return MT_OK;
+}
+
+int mt_hmc_step(mt_problem *p, int32_t C, float *x, double *logp, float *grad, const float *eps,
+                int32_t L, uint64_t seed, uint64_t iter, uint64_t chain_offset, float *accept_prob,
+                int32_t *accepted, int32_t *status, mt_stream stream) {
+  if (int r = check_chains(p, C)) return r;
+  if (L < 1) return set_err(MT_EINVAL, "L = %d < 1", L);
+  if (C == 0) return MT_OK;
+  if (check_ptr(x, "x") || check_ptr(logp, "logp") || check_ptr(grad, "grad") || check_ptr(eps, "eps") ||
+      check_ptr(accept_prob, "accept_prob") || check_ptr(accepted, "accepted"))
+    return MT_EINVAL;
+  DevGuard g(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(launch_hmc_begin(p, C, x, logp, grad, eps, seed, iter, chain_offset, s));
+  for (int step = 1; step <= L; step++) {
+    CK(launch_trace(p, TRACE_LL, C, p->d_H, p->d_band, p->d_G, p->d_ll, nullptr, nullptr, s));
+    CK(launch_finish(p, step < L ? FIN_STEP : FIN_LAST, C, x, grad, logp, status, p->d_mom, eps,
+                     p->d_kin1, s));
+  }
+  CK(launch_hmc_end(p, C, x, logp, grad, seed, iter, chain_offset, accept_prob, accepted, status, s));
+  return MT_OK;
+}
+
+int mt_heights(mt_problem *p, int32_t C, const float *x, float *H, mt_stream stream) {
+  if (int r = check_chains(p, C)) return r;
+  if (C == 0) return MT_OK;
+  if (check_ptr(x, "x") || check_ptr(H, "H")) return MT_EINVAL;
+  DevGuard g(p->device);
+  CK(launch_heights(p, C, x, H, p->d_band, (cudaStream_t)stream));
+  return MT_OK;
+}
+
+// band of caller-given heights (min/max per surface) through the K3 reduce
+// path is not needed: compute it with a tiny kernel-free approach by reusing
+// the heights kernel's band reduction on H directly.
+__global__ void k_band_of(const float *H, int N, float4 *band) {
+  const float *Hc = H + (size_t)blockIdx.x * 2 * N;
+  float a = 3e38f, b = -3e38f, c = 3e38f, d = -3e38f;
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    a = fminf(a, Hc[k]); b = fmaxf(b, Hc[k]);
+    c = fminf(c, Hc[N + k]); d = fmaxf(d, Hc[N + k]);
+  }
+  __shared__ float sh[4][256];
+  sh[0][threadIdx.x] = a; sh[1][threadIdx.x] = b; sh[2][threadIdx.x] = c; sh[3][threadIdx.x] = d;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)blockDim.x; k++) {
+      a = fminf(a, sh[0][k]); b = fmaxf(b, sh[1][k]); c = fminf(c, sh[2][k]); d = fmaxf(d, sh[3][k]);
+    }
+    band[blockIdx.x] = make_float4(a, b, c, d);
+  }
+}
+
+int mt_loglik_heights(mt_problem *p, int32_t C, const float *H, double *ll, float *dldH,
+                      mt_stream stream) {
+  if (int r = check_chains(p, C)) return r;
+  if (C == 0) return MT_OK;
+  if (check_ptr(H, "H") || check_ptr(ll, "ll") || check_ptr(dldH, "dldH")) return MT_EINVAL;
+  DevGuard g(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  k_band_of<<<C, 256, 0, s>>>(H, p->N, p->d_band);
+  p->all_launches++;
+  CK(cudaGetLastError());
+  CK(cudaMemsetAsync(ll, 0, sizeof(double) * C, s));
+  CK(cudaMemsetAsync(dldH, 0, sizeof(float) * (size_t)C * p->P, s));
+  CK(launch_trace(p, TRACE_LL, C, H, p->d_band, dldH, ll, nullptr, nullptr, s));
+  return MT_OK;
+}
+
+int mt_path_lengths(mt_problem *p, int32_t C, const float *H, float *L, float *O, mt_stream stream) {
+  if (int r = check_chains(p, C)) return r;
+  if (C == 0) return MT_OK;
+  if (check_ptr(H, "H") || check_ptr(L, "L") || check_ptr(O, "O")) return MT_EINVAL;
+  DevGuard g(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  k_band_of<<<C, 256, 0, s>>>(H, p->N, p->d_band);
+  p->all_launches++;
+  CK(cudaGetLastError());
+  CK(launch_trace(p, TRACE_PATH, C, H, p->d_band, nullptr, nullptr, L, O, s));
+  return MT_OK;
+}
+
+int mt_debug_traversal(mt_problem *p, int64_t ray, int32_t *ij, float *s_in, float *s_out,
+                       int32_t cap, int32_t *n) {
+  if (!p) return set_err(MT_EINVAL, "problem is NULL");
+  if (ray < 0 || ray >= p->R) return set_err(MT_EINVAL, "ray %lld out of range", (long long)ray);
+  if (cap < 0 || !n || (cap > 0 && (!ij || !s_in || !s_out))) return set_err(MT_EINVAL, "bad output buffers");
+  DevGuard g(p->device);
+  int c = cap > 0 ? cap : 1;
+  int32_t *d_ij = nullptr, *d_n = nullptr;
+  float *d_si = nullptr, *d_so = nullptr;
+  CK(cudaMalloc(&d_ij, sizeof(int32_t) * 2 * c));
+  CK(cudaMalloc(&d_si, sizeof(float) * c));
+  CK(cudaMalloc(&d_so, sizeof(float) * c));
+  CK(cudaMalloc(&d_n, sizeof(int32_t)));
+  cudaError_t e = launch_debug_traversal(p, ray, d_ij, d_si, d_so, cap, d_n);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(n, d_n, sizeof(int32_t), cudaMemcpyDeviceToHost);
+  int m = (e == cudaSuccess) ? (*n < cap ? *n : cap) : 0;
+  if (e == cudaSuccess && m > 0) e = cudaMemcpy(ij, d_ij, sizeof(int32_t) * 2 * m, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && m > 0) e = cudaMemcpy(s_in, d_si, sizeof(float) * m, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && m > 0) e = cudaMemcpy(s_out, d_so, sizeof(float) * m, cudaMemcpyDeviceToHost);
+  cudaFree(d_ij); cudaFree(d_si); cudaFree(d_so); cudaFree(d_n);
+  if (e != cudaSuccess) return cuda_err(e, "mt_debug_traversal");
+  return MT_OK;
+}
+
+int mt_philox(const uint32_t *ctr, uint32_t key0, uint32_t key1, uint32_t *out, int64_t n,
+              mt_stream stream) {
+  if (n < 0 || (n > 0 && (!ctr || !out))) return set_err(MT_EINVAL, "bad philox arguments");
+  CK(launch_philox(ctr, key0, key1, out, n, 0, (cudaStream_t)stream));
+  return MT_OK;
+}
+
+int mt_philox_curand(const uint32_t *ctr, uint32_t key0, uint32_t key1, uint32_t *out, int64_t n,
+                     mt_stream stream) {
+  if (n < 0 || (n > 0 && (!ctr || !out))) return set_err(MT_EINVAL, "bad philox arguments");
+  CK(launch_philox(ctr, key0, key1, out, n, 1, (cudaStream_t)stream));
+  return MT_OK;
+}
+
+int mt_timing_start(mt_problem *p, int32_t max_records) {
+  if (!p || max_records < 0) return set_err(MT_EINVAL, "bad timing arguments");
+  DevGuard g(p->device);
+  while ((int)p->ev_a.size() < max_records) {
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    p->ev_a.push_back(a);
+    p->ev_b.push_back(b);
+  }
+  p->n_rec = 0;
+  p->trace_launches = 0;
+  p->all_launches = 0;
+  p->pairs = 0;
+  p->timing = true;
+  return MT_OK;
+}
+
+int mt_timing_read(mt_problem *p, double *trace_ms, int64_t *trace_launches, double *pairs,
+                   int64_t *all_launches) {
+  if (!p) return set_err(MT_EINVAL, "problem is NULL");
+  DevGuard g(p->device);
+  double tot = 0;
+  for (int k = 0; k < p->n_rec; k++) {
+    CK(cudaEventSynchronize(p->ev_b[k]));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, p->ev_a[k], p->ev_b[k]));
+    tot += ms;
+  }
+  if (trace_ms) *trace_ms = tot;
+  if (trace_launches) *trace_launches = p->trace_launches;
+  if (pairs) *pairs = p->pairs;
+  if (all_launches) *all_launches = p->all_launches;
+  p->timing = false;
+  return MT_OK;
+}
+
+int mt_measure_fp32_peak(int32_t device, double *tflops, double *sm_clock_mhz) {
+  if (!tflops || !sm_clock_mhz) return set_err(MT_EINVAL, "NULL argument");
+  DevGuard g(device);
+  CK(run_fp32_peak(device, tflops, sm_clock_mhz));
+  return MT_OK;
+}
+
+}  // extern "C"

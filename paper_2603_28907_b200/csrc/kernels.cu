@@ -1,0 +1,505 @@
+// kernels.cu — K1 (latent -> heights), K3 (chain rule + CAR prior + logpost,
+// fused leapfrog kick/drift + next heights), HMC begin/end (Philox momenta,
+// Metropolis), raw Philox, FP32 peak microbenchmark.  B200 / sm_100a.
+//
+// All per-chain kernels use one 256-thread block per chain: a chain's state is
+// P = 2 n_x n_y <= 8192 floats, so a block streams it once (coalesced), does
+// the 5-point periodic stencil from shared memory and reduces per-chain
+// scalars without atomics.
+#include <curand_philox4x32_x.h>
+#include <math.h>
+
+#include "mt_internal.cuh"
+
+namespace {
+
+constexpr double kTClamp = 10.0;  // R18
+
+struct NodeH {
+  float H0, H1;      // heights (fp32, computed in fp64)
+  double J0, J10, J11;  // ∂H0/∂x0, ∂H1/∂x0, ∂H1/∂x1
+};
+
+// Gaussian copula + stick-breaking: ǔ = Φ(clamp(x/σ)),
+// H0 = ǔ0 z_top, H1 = H0 + ǔ1 (z_top - H0).  fp64 internally (HP2 lever 2).
+__device__ __forceinline__ NodeH node_heights(float x0, float x1, double is0, double is1,
+                                              float z_top, bool want_jac) {
+  NodeH o;
+  double t0 = (double)x0 * is0, t1 = (double)x1 * is1;
+  bool c0 = fabs(t0) > kTClamp, c1 = fabs(t1) > kTClamp;
+  t0 = fmin(fmax(t0, -kTClamp), kTClamp);
+  t1 = fmin(fmax(t1, -kTClamp), kTClamp);
+  double u0 = 0.5 * erfc(-t0 * M_SQRT1_2), u1 = 0.5 * erfc(-t1 * M_SQRT1_2);
+  double zt = (double)z_top;
+  double h0 = u0 * zt, h1 = h0 + u1 * (zt - h0);
+  o.H0 = (float)h0;
+  o.H1 = (float)h1;
+  if (want_jac) {
+    const double inv_sqrt_2pi = 0.39894228040143267794;
+    double d0 = c0 ? 0.0 : exp(-0.5 * t0 * t0) * inv_sqrt_2pi * is0;
+    double d1 = c1 ? 0.0 : exp(-0.5 * t1 * t1) * inv_sqrt_2pi * is1;
+    o.J0 = zt * d0;
+    o.J10 = (1.0 - u1) * zt * d0;
+    o.J11 = (zt - h0) * d1;
+  }
+  return o;
+}
+
+__device__ __forceinline__ float warp_min(float v) {
+  for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide reductions (256 threads): band min/max and up to 2 double sums.
+struct BlockRed {
+  float mn0, mx0, mn1, mx1;
+  double s0, s1;
+  int bad;
+};
+
+__device__ __forceinline__ BlockRed block_reduce(BlockRed v) {
+  __shared__ float sh[4][MT_THREADS / 32];
+  __shared__ double sd[2][MT_THREADS / 32];
+  __shared__ int sb[MT_THREADS / 32];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v.mn0 = warp_min(v.mn0); v.mx0 = warp_max(v.mx0);
+  v.mn1 = warp_min(v.mn1); v.mx1 = warp_max(v.mx1);
+  v.s0 = warp_sum(v.s0); v.s1 = warp_sum(v.s1);
+  v.bad = __any_sync(0xffffffffu, v.bad);
+  if (lane == 0) {
+    sh[0][w] = v.mn0; sh[1][w] = v.mx0; sh[2][w] = v.mn1; sh[3][w] = v.mx1;
+    sd[0][w] = v.s0; sd[1][w] = v.s1; sb[w] = v.bad;
+  }
+  __syncthreads();
+  BlockRed r = {3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f, 0.0, 0.0, 0};
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < nw; k++) {
+      r.mn0 = fminf(r.mn0, sh[0][k]); r.mx0 = fmaxf(r.mx0, sh[1][k]);
+      r.mn1 = fminf(r.mn1, sh[2][k]); r.mx1 = fmaxf(r.mx1, sh[3][k]);
+      r.s0 += sd[0][k]; r.s1 += sd[1][k]; r.bad |= sb[k];
+    }
+  }
+  return r;  // valid in thread 0
+}
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al. SC'11), the counter-based generator of R22.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 philox10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; r++) {
+    uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+__device__ __forceinline__ double u01(uint32_t w) { return ((double)w + 0.5) * 2.3283064365386963e-10; }
+
+// Momenta for parameters 4q..4q+3 of global chain `chain` (Box-Muller, fp64).
+__device__ __forceinline__ void momenta4(uint64_t seed, uint64_t iter, uint64_t chain, int q,
+                                         double z[4]) {
+  uint4 w = philox10(make_uint4((uint32_t)q, (uint32_t)chain, (uint32_t)iter, 0u),
+                     make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+  uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    double rad = sqrt(-2.0 * log(u01(ww[2 * h])));
+    double sn, cs;
+    sincospi(2.0 * u01(ww[2 * h + 1]), &sn, &cs);
+    z[2 * h] = rad * cs;
+    z[2 * h + 1] = rad * sn;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// K1: heights + per-chain band (min/max of each surface's node heights)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(MT_THREADS) k_heights(FinishArgs a, const float *x) {
+  int c = blockIdx.x;
+  const float *xc = x + (size_t)c * a.P;
+  float *Hc = a.H + (size_t)c * 2 * a.N;
+  BlockRed v = {3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f, 0.0, 0.0, 0};
+  for (int k = threadIdx.x; k < a.N; k += blockDim.x) {
+    NodeH h = node_heights(xc[k], xc[a.N + k], a.inv_sigma[0], a.inv_sigma[1], a.z_top, false);
+    Hc[k] = h.H0;
+    Hc[a.N + k] = h.H1;
+    v.mn0 = fminf(v.mn0, h.H0); v.mx0 = fmaxf(v.mx0, h.H0);
+    v.mn1 = fminf(v.mn1, h.H1); v.mx1 = fmaxf(v.mx1, h.H1);
+  }
+  BlockRed r = block_reduce(v);
+  if (threadIdx.x == 0) a.band[c] = make_float4(r.mn0, r.mx0, r.mn1, r.mx1);
+}
+
+// ---------------------------------------------------------------------------
+// K3: ∂ℓ/∂H -> ∂/∂x by the chain rule, CAR prior value and gradient (5-point
+// periodic stencil), logpost assembly (fp64), and in
+// leapfrog mode the fused kick / drift / next-heights update.
+// ---------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(MT_THREADS) k_finish(FinishArgs a) {
+  extern __shared__ float xs[];  // [2N] current x of this chain
+  const int c = blockIdx.x, N = a.N, ny = a.ny, nx = a.nx;
+  float *xc = a.x + (size_t)c * a.P;
+  for (int k = threadIdx.x; k < a.P; k += blockDim.x) xs[k] = xc[k];
+  __syncthreads();
+  float *Gc = const_cast<float *>(a.G) + (size_t)c * 2 * N;
+  float *gc = a.grad + (size_t)c * a.P;
+  float *pc = MODE != FIN_PLAIN ? a.mom + (size_t)c * a.P : nullptr;
+  float *Hc = a.H + (size_t)c * 2 * N;
+  const float eps = MODE != FIN_PLAIN ? a.eps[c] : 0.f;
+  BlockRed v = {3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f, 0.0, 0.0, 0};
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    const int i = k / ny, j = k - i * ny;
+    float x0 = xs[k], x1 = xs[N + k];
+    NodeH h = node_heights(x0, x1, a.inv_sigma[0], a.inv_sigma[1], a.z_top, true);
+    float G0 = Gc[k], G1 = Gc[N + k];
+    Gc[k] = 0.f;
+    Gc[N + k] = 0.f;
+    double gx0 = (double)G0 * h.J0 + (double)G1 * h.J10;
+    double gx1 = (double)G1 * h.J11;
+    if (a.prior_on) {
+      const int ip = (i + 1 == nx ? 0 : i + 1) * ny + j, im = (i == 0 ? nx - 1 : i - 1) * ny + j;
+      const int jp = i * ny + (j + 1 == ny ? 0 : j + 1), jm = i * ny + (j == 0 ? ny - 1 : j - 1);
+#pragma unroll
+      for (int l = 0; l < 2; l++) {
+        const float *xl = xs + l * N;
+        double xv = xl[k];
+        double Qx = 4.0 * xv - (double)a.car_r[l] * ((double)xl[ip] + xl[im] + xl[jp] + xl[jm]);
+        v.s0 += xv * Qx;
+        if (l == 0) gx0 -= Qx; else gx1 -= Qx;
+      }
+    }
+    float g0f = (float)gx0, g1f = (float)gx1;
+    gc[k] = g0f;
+    gc[N + k] = g1f;
+    v.bad |= !(isfinite(g0f) && isfinite(g1f));
+    if (MODE == FIN_STEP) {  // close this step's half kick, open the next: p += ε g; x += ε p
+      float p0 = pc[k] + eps * g0f, p1 = pc[N + k] + eps * g1f;
+      pc[k] = p0;
+      pc[N + k] = p1;
+      float xn0 = x0 + eps * p0, xn1 = x1 + eps * p1;
+      xc[k] = xn0;
+      xc[N + k] = xn1;
+      NodeH hn = node_heights(xn0, xn1, a.inv_sigma[0], a.inv_sigma[1], a.z_top, false);
+      Hc[k] = hn.H0;
+      Hc[N + k] = hn.H1;
+      v.mn0 = fminf(v.mn0, hn.H0); v.mx0 = fmaxf(v.mx0, hn.H0);
+      v.mn1 = fminf(v.mn1, hn.H1); v.mx1 = fmaxf(v.mx1, hn.H1);
+    } else if (MODE == FIN_LAST) {  // final half kick
+      float p0 = pc[k] + 0.5f * eps * g0f, p1 = pc[N + k] + 0.5f * eps * g1f;
+      pc[k] = p0;
+      pc[N + k] = p1;
+      v.s1 += 0.5 * ((double)p0 * p0 + (double)p1 * p1);
+    }
+  }
+  BlockRed r = block_reduce(v);
+  if (threadIdx.x == 0) {
+    double lp = a.ll[c] + (a.prior_on ? -0.5 * r.s0 + a.prior_const : 0.0);
+    a.ll[c] = 0.0;
+    a.logp[c] = lp;
+    int bad = r.bad || !isfinite(lp);
+    if (a.status) a.status[c] = bad ? MT_STATUS_NONFINITE : 0;
+    if (MODE == FIN_STEP) a.band[c] = make_float4(r.mn0, r.mx0, r.mn1, r.mx1);
+    if (MODE == FIN_LAST && a.kin) a.kin[c] = (float)r.s1;
+  }
+}
+
+// first half kick + drift + heights: p += ε/2 g; x += ε p; H(x)
+__global__ void __launch_bounds__(MT_THREADS) k_kick_drift(FinishArgs a) {
+  const int c = blockIdx.x, N = a.N;
+  float *xc = a.x + (size_t)c * a.P, *pc = a.mom + (size_t)c * a.P;
+  const float *gc = a.grad + (size_t)c * a.P;
+  float *Hc = a.H + (size_t)c * 2 * N;
+  const float eps = a.eps[c];
+  BlockRed v = {3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f, 0.0, 0.0, 0};
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    float p0 = pc[k] + 0.5f * eps * gc[k], p1 = pc[N + k] + 0.5f * eps * gc[N + k];
+    pc[k] = p0;
+    pc[N + k] = p1;
+    float x0 = xc[k] + eps * p0, x1 = xc[N + k] + eps * p1;
+    xc[k] = x0;
+    xc[N + k] = x1;
+    NodeH h = node_heights(x0, x1, a.inv_sigma[0], a.inv_sigma[1], a.z_top, false);
+    Hc[k] = h.H0;
+    Hc[N + k] = h.H1;
+    v.mn0 = fminf(v.mn0, h.H0); v.mx0 = fmaxf(v.mx0, h.H0);
+    v.mn1 = fminf(v.mn1, h.H1); v.mx1 = fmaxf(v.mx1, h.H1);
+  }
+  BlockRed r = block_reduce(v);
+  if (threadIdx.x == 0) a.band[c] = make_float4(r.mn0, r.mx0, r.mn1, r.mx1);
+}
+
+// HMC begin: Philox momenta, kinetic energy, save (x, grad, logp), first
+// half kick + drift + heights.
+__global__ void __launch_bounds__(MT_THREADS) k_hmc_begin(FinishArgs a, const double *logp,
+                                                          float *x0s, float *g0s, double *lp0,
+                                                          float *kin0, uint64_t seed,
+                                                          uint64_t iter, uint64_t chain_offset) {
+  const int c = blockIdx.x, N = a.N, P = a.P;
+  float *xc = a.x + (size_t)c * P, *pc = a.mom + (size_t)c * P;
+  const float *gc = a.grad + (size_t)c * P;
+  float *Hc = a.H + (size_t)c * 2 * N;
+  const float eps = a.eps[c];
+  const int nq = (P + 3) / 4;
+  BlockRed v = {3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f, 0.0, 0.0, 0};
+  for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+    double z[4];
+    momenta4(seed, iter, chain_offset + c, q, z);
+#pragma unroll
+    for (int m = 0; m < 4; m++) {
+      int k = 4 * q + m;
+      if (k < P) {
+        float pz = (float)z[m];
+        v.s0 += 0.5 * (double)pz * pz;
+        float g = gc[k], xv = xc[k];
+        x0s[(size_t)c * P + k] = xv;
+        g0s[(size_t)c * P + k] = g;
+        float ph = pz + 0.5f * eps * g;
+        pc[k] = ph;
+        xc[k] = xv + eps * ph;
+      }
+    }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    NodeH h = node_heights(xc[k], xc[N + k], a.inv_sigma[0], a.inv_sigma[1], a.z_top, false);
+    Hc[k] = h.H0;
+    Hc[N + k] = h.H1;
+    v.mn0 = fminf(v.mn0, h.H0); v.mx0 = fmaxf(v.mx0, h.H0);
+    v.mn1 = fminf(v.mn1, h.H1); v.mx1 = fmaxf(v.mx1, h.H1);
+  }
+  BlockRed r = block_reduce(v);
+  if (threadIdx.x == 0) {
+    a.band[c] = make_float4(r.mn0, r.mx0, r.mn1, r.mx1);
+    kin0[c] = (float)r.s0;
+    lp0[c] = logp[c];
+  }
+}
+
+// HMC end: H = -logp + |p|^2/2, accept iff ln u < -ΔH (u: Philox counter
+// (0, chain, iter, 1)), divergence (ΔH > 1000 or non-finite) -> reject.
+__global__ void __launch_bounds__(MT_THREADS) k_hmc_end(FinishArgs a, const float *x0s,
+                                                        const float *g0s, const double *lp0,
+                                                        const float *kin0, const float *kin1,
+                                                        uint64_t seed, uint64_t iter,
+                                                        uint64_t chain_offset, float *acc_prob,
+                                                        int32_t *accepted) {
+  __shared__ int s_acc;
+  const int c = blockIdx.x, P = a.P;
+  if (threadIdx.x == 0) {
+    double H0 = -lp0[c] + (double)kin0[c];
+    double H1 = -a.logp[c] + (double)kin1[c];
+    double dH = H1 - H0;
+    uint4 w = philox10(make_uint4(0u, (uint32_t)(chain_offset + c), (uint32_t)iter, 1u),
+                       make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+    double u = u01(w.x);
+    bool fin = isfinite(dH);
+    bool div = !fin || dH > 1000.0;
+    bool acc = fin && !div && log(u) < -dH;
+    acc_prob[c] = fin ? (float)fmin(1.0, exp(-dH)) : 0.f;
+    accepted[c] = acc ? 1 : 0;
+    if (a.status) a.status[c] = (acc ? a.status[c] : 0) | (div ? MT_STATUS_DIVERGENT : 0);
+    if (!acc) a.logp[c] = lp0[c];
+    s_acc = acc;
+  }
+  __syncthreads();
+  if (!s_acc) {
+    for (int k = threadIdx.x; k < P; k += blockDim.x) {
+      a.x[(size_t)c * P + k] = x0s[(size_t)c * P + k];
+      a.grad[(size_t)c * P + k] = g0s[(size_t)c * P + k];
+    }
+  }
+}
+
+__global__ void k_momenta(int C, int P, float *mom, uint64_t seed, uint64_t iter,
+                          uint64_t chain_offset) {
+  const int nq = (P + 3) / 4;
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)C * nq) return;
+  int c = (int)(t / nq), q = (int)(t - (int64_t)c * nq);
+  double z[4];
+  momenta4(seed, iter, chain_offset + c, q, z);
+  for (int m = 0; m < 4; m++)
+    if (4 * q + m < P) mom[(size_t)c * P + 4 * q + m] = (float)z[m];
+}
+
+__global__ void k_philox(const uint4 *ctr, uint2 key, uint4 *out, int64_t n, int use_curand) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  out[t] = use_curand ? curand_Philox4x32_10(ctr[t], key) : philox10(ctr[t], key);
+}
+
+__global__ void k_ffma(float *out, int iters, float a, float b, long long *cycles) {
+  float x[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) x[k] = threadIdx.x * 1e-3f + k;
+  long long t0 = clock64();
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int u = 0; u < 8; u++)
+#pragma unroll
+      for (int k = 0; k < 8; k++) x[k] = fmaf(x[k], a, b);
+  }
+  long long t1 = clock64();
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; k++) s += x[k];
+  if (s == 1234.5f) out[0] = s;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *cycles = t1 - t0;
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+static FinishArgs base_args(mt_problem *p, int C) {
+  FinishArgs a{};
+  a.nx = p->nx; a.ny = p->ny; a.N = p->N; a.P = p->P; a.C = C;
+  a.z_top = p->z_top;
+  a.inv_sigma[0] = 1.0 / p->sigma[0];
+  a.inv_sigma[1] = 1.0 / p->sigma[1];
+  a.car_r[0] = p->car_r[0];
+  a.car_r[1] = p->car_r[1];
+  a.prior_const = 0.0;
+  for (int l = 0; l < 2; l++) a.prior_const += 0.5 * p->logdetQ[l] - 0.5 * p->N * log(2.0 * M_PI);
+  a.prior_on = p->prior_on;
+  a.G = p->d_G;
+  a.ll = p->d_ll;
+  a.H = p->d_H;
+  a.band = p->d_band;
+  return a;
+}
+
+cudaError_t launch_heights(mt_problem *p, int C, const float *x, float *H, float4 *band,
+                           cudaStream_t s) {
+  if (C <= 0) return cudaSuccess;
+  FinishArgs a = base_args(p, C);
+  a.H = H;
+  a.band = band;
+  k_heights<<<C, MT_THREADS, 0, s>>>(a, x);
+  p->all_launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finish(mt_problem *p, int mode, int C, float *x, float *grad, double *logp,
+                          int32_t *status, float *mom, const float *eps, float *kin,
+                          cudaStream_t s) {
+  if (C <= 0) return cudaSuccess;
+  FinishArgs a = base_args(p, C);
+  a.x = x; a.grad = grad; a.logp = logp; a.status = status; a.mom = mom; a.eps = eps; a.kin = kin;
+  size_t smem = (size_t)p->P * sizeof(float);
+  static bool attr[3] = {false, false, false};
+  if (smem > 48 * 1024 && !attr[mode]) {
+    if (mode == FIN_PLAIN)
+      cudaFuncSetAttribute(k_finish<FIN_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    if (mode == FIN_STEP)
+      cudaFuncSetAttribute(k_finish<FIN_STEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    if (mode == FIN_LAST)
+      cudaFuncSetAttribute(k_finish<FIN_LAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    attr[mode] = true;
+  }
+  if (mode == FIN_PLAIN) k_finish<FIN_PLAIN><<<C, MT_THREADS, smem, s>>>(a);
+  else if (mode == FIN_STEP) k_finish<FIN_STEP><<<C, MT_THREADS, smem, s>>>(a);
+  else k_finish<FIN_LAST><<<C, MT_THREADS, smem, s>>>(a);
+  p->all_launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kick_drift(mt_problem *p, int C, float *x, float *mom, const float *grad,
+                              const float *eps, cudaStream_t s) {
+  if (C <= 0) return cudaSuccess;
+  FinishArgs a = base_args(p, C);
+  a.x = x; a.mom = mom; a.grad = const_cast<float *>(grad); a.eps = eps;
+  k_kick_drift<<<C, MT_THREADS, 0, s>>>(a);
+  p->all_launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hmc_begin(mt_problem *p, int C, float *x, const double *logp,
+                             const float *grad, const float *eps, uint64_t seed, uint64_t iter,
+                             uint64_t chain_offset, cudaStream_t s) {
+  FinishArgs a = base_args(p, C);
+  a.x = x; a.mom = p->d_mom; a.grad = const_cast<float *>(grad); a.eps = eps;
+  k_hmc_begin<<<C, MT_THREADS, 0, s>>>(a, logp, p->d_x0, p->d_g0, p->d_lp0, p->d_kin0, seed, iter,
+                                       chain_offset);
+  p->all_launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hmc_end(mt_problem *p, int C, float *x, double *logp, float *grad,
+                           uint64_t seed, uint64_t iter, uint64_t chain_offset, float *acc_prob,
+                           int32_t *accepted, int32_t *status, cudaStream_t s) {
+  FinishArgs a = base_args(p, C);
+  a.x = x; a.logp = logp; a.grad = grad; a.status = status;
+  k_hmc_end<<<C, MT_THREADS, 0, s>>>(a, p->d_x0, p->d_g0, p->d_lp0, p->d_kin0, p->d_kin1, seed,
+                                     iter, chain_offset, acc_prob, accepted);
+  p->all_launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_momenta(mt_problem *p, int C, float *mom, uint64_t seed, uint64_t iter,
+                           uint64_t chain_offset, cudaStream_t s) {
+  if (C <= 0) return cudaSuccess;
+  int64_t n = (int64_t)C * ((p->P + 3) / 4);
+  k_momenta<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(C, p->P, mom, seed, iter, chain_offset);
+  p->all_launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_philox(const uint32_t *ctr, uint32_t k0, uint32_t k1, uint32_t *out, int64_t n,
+                          int use_curand, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  k_philox<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(reinterpret_cast<const uint4 *>(ctr),
+                                                       make_uint2(k0, k1),
+                                                       reinterpret_cast<uint4 *>(out), n, use_curand);
+  return cudaGetLastError();
+}
+
+cudaError_t run_fp32_peak(int device, double *tflops, double *mhz) {
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) return e;
+  float *out;
+  long long *cyc;
+  cudaMalloc(&out, sizeof(float));
+  cudaMalloc(&cyc, sizeof(long long));
+  int blocks = prop.multiProcessorCount * 4, threads = 512, iters = 4096;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  k_ffma<<<blocks, threads>>>(out, 64, 1.0000001f, 1e-7f, cyc);  // warm-up
+  double best = 0, best_mhz = 0;
+  for (int rep = 0; rep < 10; rep++) {
+    cudaEventRecord(e0);
+    k_ffma<<<blocks, threads>>>(out, iters, 1.0000001f, 1e-7f, cyc);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    long long cycles = 0;
+    cudaMemcpy(&cycles, cyc, sizeof(long long), cudaMemcpyDeviceToHost);
+    double fl = 2.0 * 64.0 * iters * (double)blocks * threads;
+    double tf = fl / (ms * 1e-3) / 1e12;
+    if (tf > best) { best = tf; best_mhz = cycles / (ms * 1e3); }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  cudaFree(cyc);
+  *tflops = best;
+  *mhz = best_mhz;
+  return cudaGetLastError();
+}

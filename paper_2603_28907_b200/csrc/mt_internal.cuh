@@ -1,0 +1,122 @@
+// mt_internal.cuh — internal types of libmt (B200 / sm_100a).  Not part of the
+// C ABI; never included by oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/mt.h"
+
+#define MT_MAX_AXIS 128
+#define MT_MAX_NODES 4096
+#define MT_THREADS 256
+
+// Per-problem constants every trace launch needs (passed by value).
+struct TraceConsts {
+  int nx, ny, N;     // nodes per axis, nodes per surface
+  float z_top;
+  float k0, k1;      // ∂O/∂B0 = ρ_muck - ρ_air, ∂O/∂B1 = ρ_air - ρ_rock
+  float inv_att;     // 1/Λ
+};
+
+// Ray SoA, one entry per ray of the shard:
+//   a = {o_x, o_y, d_x, d_y}
+//   b = {d_z, s_exit, t_base, C}
+// with t_base = ln w - [C > 0] ln C - (ρ_rock s_exit + ρ_ext L_ext)/Λ, so that
+// t = t_base - (k0 B0 + k1 B1)/Λ = ln(λ/C) (C > 0) or ln λ (C = 0).
+struct TraceArgs {
+  TraceConsts tc;
+  const float *X, *Y;           // node coordinates
+  const float4 *ray_a, *ray_b;
+  const float *obase;           // ρ_rock s_exit + ρ_ext L_ext (path-length export only)
+  int64_t R;                    // rays in the shard
+  int64_t rays_per_block;
+  int C;                        // chains in this call
+  const float *H;               // [C][2][N] heights
+  const float4 *band;           // [C] (min H0, max H0, min H1, max H1)
+  float *G;                     // [C][2][N] ∂ℓ/∂H accumulator (atomic adds)
+  double *ll;                   // [C] deviance-centred log-likelihood accumulator
+  float *Lout, *Oout;           // path-length export: [C][R][3], [C][R]
+};
+
+enum { TRACE_LL = 0, TRACE_PATH = 1 };
+
+struct FinishArgs {
+  int nx, ny, N, P, C;
+  float z_top;
+  double inv_sigma[2];
+  float car_r[2];
+  double prior_const;           // Σ_l (1/2 ln det Q_l - N/2 ln 2π)
+  int prior_on;
+  const float *G;               // ∂ℓ/∂H [C][2N] (zeroed after use)
+  double *ll;                   // [C] (zeroed after use)
+  float *x;                     // [C][P]
+  float *grad;                  // [C][P]
+  double *logp;                 // [C]
+  int32_t *status;              // [C] or null
+  float *mom;                   // [C][P] leapfrog momenta
+  const float *eps;             // [C]
+  float *H;                     // [C][2N] heights of the updated x (leapfrog)
+  float4 *band;                 // [C]
+  float *kin;                   // [C] 1/2 |p|^2 after the last half kick
+};
+
+enum { FIN_PLAIN = 0, FIN_STEP = 1, FIN_LAST = 2 };
+
+struct mt_problem {
+  int device = 0;
+  int num_sms = 148;
+  int nx = 0, ny = 0, N = 0, P = 0;
+  int64_t R = 0, ray_lo = 0;
+  int max_chains = 0;
+  float z_top = 0;
+  float car_r[2] = {0, 0};
+  double sigma[2] = {0, 0}, logdetQ[2] = {0, 0};
+  double loglik_offset = 0;
+  int prior_on = 1;
+  TraceConsts tc{};
+  float *d_X = nullptr, *d_Y = nullptr;
+  float4 *d_ray_a = nullptr, *d_ray_b = nullptr;
+  float *d_obase = nullptr;
+  float *d_H = nullptr, *d_G = nullptr;
+  float4 *d_band = nullptr;
+  double *d_ll = nullptr;
+  // HMC workspace
+  float *d_x0 = nullptr, *d_g0 = nullptr, *d_mom = nullptr, *d_kin0 = nullptr, *d_kin1 = nullptr;
+  double *d_lp0 = nullptr;
+  // trace launch shape
+  int trace_k = 0;              // chains per block (0 = auto)
+  int trace_s = 0;              // ray splits (0 = auto)
+  // measurement
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_a, ev_b;
+  int n_rec = 0;
+  int64_t trace_launches = 0, all_launches = 0;
+  double pairs = 0;
+};
+
+// launchers (kernels.cu)
+cudaError_t launch_heights(mt_problem *p, int C, const float *x, float *H, float4 *band,
+                           cudaStream_t s);
+cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const float4 *band,
+                         float *G, double *ll, float *L, float *O, cudaStream_t s);
+cudaError_t launch_finish(mt_problem *p, int mode, int C, float *x, float *grad, double *logp,
+                          int32_t *status, float *mom, const float *eps, float *kin,
+                          cudaStream_t s);
+cudaError_t launch_kick_drift(mt_problem *p, int C, float *x, float *mom, const float *grad,
+                              const float *eps, cudaStream_t s);
+cudaError_t launch_hmc_begin(mt_problem *p, int C, float *x, const double *logp,
+                             const float *grad, const float *eps, uint64_t seed, uint64_t iter,
+                             uint64_t chain_offset, cudaStream_t s);
+cudaError_t launch_hmc_end(mt_problem *p, int C, float *x, double *logp, float *grad,
+                           uint64_t seed, uint64_t iter, uint64_t chain_offset, float *acc_prob,
+                           int32_t *accepted, int32_t *status, cudaStream_t s);
+cudaError_t launch_momenta(mt_problem *p, int C, float *mom, uint64_t seed, uint64_t iter,
+                           uint64_t chain_offset, cudaStream_t s);
+cudaError_t launch_debug_traversal(mt_problem *p, int64_t ray, int32_t *d_ij, float *d_si,
+                                   float *d_so, int cap, int32_t *d_n);
+cudaError_t launch_philox(const uint32_t *ctr, uint32_t k0, uint32_t k1, uint32_t *out,
+                          int64_t n, int use_curand, cudaStream_t s);
+cudaError_t run_fp32_peak(int device, double *tflops, double *mhz);

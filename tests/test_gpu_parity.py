@@ -1,0 +1,281 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the
+same seeded inputs.  Tolerances are BASELINE.json north_star's, read as in
+DESIGN.md "Tolerances":
+  traversal   bit-exact (i, j) lists
+  lengths     |L_dev - L_ora| <= 1e-5 * L_tot per (chain, ray, unit)
+  logpost     |Δ| <= 1e-4 |logp_ora| per chain (deviance-centred form + prior)
+  gradient    ||Δ||_2 <= 1e-3 ||g_ora||_2 per chain
+  leapfrog    ||x10_dev - x10_ora||_2 <= 1e-3 ||x10_ora||_2 per chain
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from paper_2603_28907_b200 import Problem, inputs, philox  # noqa: E402
+
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module")
+def gpu(problems):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cache = {}
+
+    def get(name, max_chains=None, **kw):
+        key = (name, max_chains, tuple(sorted(kw.items())))
+        if key not in cache:
+            cfg = inputs.CONFIGS[name]
+            cache[key] = Problem(problems(name), device=0, max_chains=max_chains or cfg.chains, **kw)
+        return cache[key]
+    return get
+
+
+def rel_l2(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+# ---------------------------------------------------------------------------
+# traversal (integer, bit-exact)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name,nsample", [("tiny", None), ("small", 3000), ("medium", 2000)])
+def test_traversal_bit_exact(gpu, oracle_problem, name, nsample):
+    mp, op = gpu(name), oracle_problem(name)
+    rays = range(op.R) if nsample is None else np.random.default_rng(7).choice(op.R, nsample, replace=False)
+    for q in rays:
+        q = int(q)
+        ij_d, si_d, so_d = mp.debug_traversal(q)
+        ij_o, si_o, so_o = op.traversal(q)
+        assert np.array_equal(ij_d, ij_o), q
+        assert np.allclose(so_d, so_o, rtol=2e-6, atol=1e-5), q
+
+
+# ---------------------------------------------------------------------------
+# path lengths and likelihood/adjoint from identical heights
+# ---------------------------------------------------------------------------
+def identical_heights(prob, C, seed, scale=2.0):
+    return inputs.perturbed_heights(prob["H_true"], C, seed, scale=scale)
+
+
+@pytest.mark.parametrize("name,C", [("tiny", 4), ("small", 8), ("medium", 2)])
+def test_path_lengths_identical_heights(gpu, oracle_problem, name, C):
+    mp, op = gpu(name), oracle_problem(name)
+    H = identical_heights(op.prob, C, 100 + C)
+    L_d, O_d = mp.path_lengths(torch.from_numpy(H).to(DEV))
+    L_o, O_o = op.path_lengths(H.astype(np.float64))
+    Ltot = L_o.sum(2)
+    err = np.abs(L_d.cpu().numpy().astype(np.float64) - L_o).max(2)
+    bad = err > 1e-5 * Ltot
+    assert bad.sum() == 0, f"{bad.sum()} of {bad.size} (chain, ray) pairs exceed 1e-5 L_tot; max rel {np.max(err / Ltot):.3g}"
+    assert np.allclose(O_d.cpu().numpy(), O_o, rtol=2e-5)
+
+
+@pytest.mark.parametrize("name,C", [("tiny", 4), ("small", 8), ("medium", 2)])
+def test_loglik_and_adjoint_identical_heights(gpu, oracle_problem, name, C):
+    mp, op = gpu(name), oracle_problem(name)
+    H = identical_heights(op.prob, C, 200 + C, scale=1.0)
+    ll_d, G_d = mp.loglik_heights(torch.from_numpy(H).to(DEV))
+    out = op.loglik_grad_H(H.astype(np.float64))
+    ll_d = ll_d.cpu().numpy()
+    G_d = G_d.cpu().numpy().astype(np.float64)
+    for c in range(C):
+        assert abs(ll_d[c] - out["ll_dev"][c]) <= 1e-4 * abs(out["ll_dev"][c]), (c, ll_d[c], out["ll_dev"][c])
+        assert rel_l2(G_d[c], out["dldH"][c]) <= 1e-3, (c, rel_l2(G_d[c], out["dldH"][c]))
+
+
+def test_heights_map(gpu, oracle_problem):
+    mp, op = gpu("small"), oracle_problem("small")
+    x = inputs.chain_states(op.prob["x_true"], 8, 2, scale=0.3)
+    H_d = mp.heights(torch.from_numpy(x).to(DEV)).cpu().numpy()
+    H_o = np.stack([op.heights(xc.astype(np.float64))[0] for xc in x])
+    # fp64 internally, one fp32 rounding at the end
+    assert np.allclose(H_d, H_o, rtol=1.5 * 2 ** -24, atol=0)
+
+
+# ---------------------------------------------------------------------------
+# end-to-end log-posterior and gradient from x
+# ---------------------------------------------------------------------------
+def e2e_check(mp, op, x, chains, logp_d, grad_d):
+    out = op.logpost_grad(x[chains].astype(np.float64))
+    fails = []
+    for k, c in enumerate(chains):
+        e_lp = abs(logp_d[c] - out["logp"][k]) / abs(out["logp"][k])
+        e_g = rel_l2(grad_d[c].astype(np.float64), out["grad"][k])
+        if e_lp > 1e-4 or e_g > 1e-3:
+            fails.append((int(c), e_lp, e_g))
+    return fails
+
+
+@pytest.mark.parametrize("name", ["tiny", "small"])
+def test_logpost_grad_end_to_end(gpu, oracle_problem, name):
+    mp, op = gpu(name), oracle_problem(name)
+    cfg = inputs.CONFIGS[name]
+    x = inputs.chain_states(op.prob["x_true"], cfg.chains, cfg.seed)
+    logp, grad = mp.logpost_grad(torch.from_numpy(x).to(DEV))
+    fails = e2e_check(mp, op, x, np.arange(cfg.chains), logp.cpu().numpy(), grad.cpu().numpy())
+    assert not fails, fails
+
+
+def test_logpost_grad_medium_bench_launch(gpu, oracle_problem):
+    """Full Medium size, in the launch configuration bench.py times (1024 chains),
+    compared on sampled chains the oracle computes one by one."""
+    mp, op = gpu("medium"), oracle_problem("medium")
+    cfg = inputs.CONFIGS["medium"]
+    x = inputs.chain_states(op.prob["x_true"], cfg.chains, cfg.seed)
+    logp, grad = mp.logpost_grad(torch.from_numpy(x).to(DEV))
+    chains = np.array([0, 511, 1023])
+    fails = e2e_check(mp, op, x, chains, logp.cpu().numpy(), grad.cpu().numpy())
+    assert not fails, fails
+
+
+# ---------------------------------------------------------------------------
+# momenta, leapfrog, HMC
+# ---------------------------------------------------------------------------
+def test_philox_bit_exact_vs_oracle_and_curand(gpu):
+    rng = np.random.default_rng(3)
+    ctr = rng.integers(0, 2 ** 32, size=(4096, 4), dtype=np.uint64).astype(np.uint32)
+    key = [int(v) for v in rng.integers(0, 2 ** 32, size=2, dtype=np.uint64)]
+    c = torch.from_numpy(ctr.view(np.int32)).to(DEV)
+    d = philox(c, key).cpu().numpy().view(np.uint32)
+    cu = philox(c, key, use_curand=True).cpu().numpy().view(np.uint32)
+    assert np.array_equal(d, cu)
+    for k in range(0, 4096, 97):
+        assert np.array_equal(d[k], oracle.philox4x32_10(ctr[k], key))
+
+
+def test_momenta_match_oracle(gpu, oracle_problem):
+    mp = gpu("small")
+    P = mp.P
+    seed, it, off = 0xDEADBEEF12345678, 17, 40
+    p_d = mp.draw_momenta(8, seed, it, off).cpu().numpy()
+    for c in range(8):
+        assert np.allclose(p_d[c], oracle.momenta(P, seed, it, off + c), rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.parametrize("name,C", [("tiny", 4), ("small", 16)])
+def test_leapfrog_10_steps(gpu, oracle_problem, name, C):
+    mp, op = gpu(name), oracle_problem(name)
+    cfg = inputs.CONFIGS[name]
+    x0 = inputs.chain_states(op.prob["x_true"], C, cfg.seed)
+    seed = inputs.philox_key(cfg)
+    x = torch.from_numpy(x0).to(DEV)
+    p = mp.draw_momenta(C, seed, 0)
+    p0 = p.cpu().numpy().astype(np.float64)
+    logp, grad = mp.logpost_grad(x)
+    eps = torch.full((C,), cfg.eps, dtype=torch.float32, device=DEV)
+    mp.leapfrog(x, p, logp, grad, eps, 10)
+    xo, po, lpo, go = oracle.leapfrog(x0.astype(np.float64), p0, cfg.eps, 10,
+                                      lambda xx: (lambda o: (o["logp"], o["grad"]))(op.logpost_grad(xx)))
+    xd = x.cpu().numpy().astype(np.float64)
+    for c in range(C):
+        assert rel_l2(xd[c], xo[c]) <= 1e-3, (c, rel_l2(xd[c], xo[c]))
+        disp = np.linalg.norm(xd[c] - xo[c]) / np.linalg.norm(xo[c] - x0[c])
+        assert disp < 0.05, (c, disp)   # diagnostic: displacement-relative error
+    assert np.allclose(logp.cpu().numpy(), lpo, rtol=1e-4)
+
+
+def test_hmc_step_matches_oracle_decisions(gpu, oracle_problem):
+    name, C = "small", 16
+    mp, op = gpu(name), oracle_problem(name)
+    cfg = inputs.CONFIGS[name]
+    x0 = inputs.chain_states(op.prob["x_true"], C, cfg.seed)
+    seed = inputs.philox_key(cfg)
+    x = torch.from_numpy(x0).to(DEV)
+    logp, grad = mp.logpost_grad(x)
+    eps = torch.full((C,), cfg.eps, dtype=torch.float32, device=DEV)
+    ap, acc = mp.hmc_step(x, logp, grad, eps, 10, seed, 3)
+    lg = lambda xx: (lambda o: (o["logp"], o["grad"]))(op.logpost_grad(xx))  # noqa: E731
+    xo, apo, acco, lpo, dHo = oracle.hmc_step(x0.astype(np.float64), cfg.eps, 10, lg, seed, 3)
+    u = np.array([oracle.mh_uniform(seed, 3, c) for c in range(C)])
+    clear = np.abs(np.log(u) + dHo) > 0.05      # decisions far from the threshold must agree
+    acc = acc.cpu().numpy().astype(bool)
+    assert clear.sum() >= C // 2
+    assert np.array_equal(acc[clear], acco[clear])
+    assert np.allclose(ap.cpu().numpy()[clear], apo[clear], atol=0.02)
+    xd = x.cpu().numpy()
+    for c in np.nonzero(clear)[0]:
+        assert rel_l2(xd[c], xo[c]) <= 1e-3
+
+
+# ---------------------------------------------------------------------------
+# edge cases
+# ---------------------------------------------------------------------------
+def test_zero_chains_and_bad_arguments(gpu):
+    from paper_2603_28907_b200 import MTError
+    mp = gpu("tiny")
+    x = torch.zeros((0, mp.P), device=DEV)
+    lp, g = mp.logpost_grad(x)
+    assert lp.numel() == 0
+    with pytest.raises(MTError):
+        mp.logpost_grad(torch.zeros((mp.max_chains + 1, mp.P), device=DEV))
+
+
+def test_ragged_rays_small_grid_and_zero_counts(problems):
+    """n = 3 grid, 1000 rays (not a multiple of the block), zero counts,
+    detectors near the walls, a vertical ray, axis-parallel rays."""
+    base = problems("tiny")
+    X = inputs.quantize([0.0, 40.0, 100.0]).astype(np.float32)
+    rng = np.random.default_rng(11)
+    dets = inputs.quantize(np.array([[0.5, 0.5], [99.25, 50.0], [40.0, 40.0], [70.0, 3.0]]))
+    dets = np.concatenate([dets, np.zeros((4, 1))], 1).astype(np.float32)
+    R = 1000
+    th = rng.uniform(0, 1.3, R)
+    ph = rng.uniform(0, 2 * np.pi, R)
+    d = np.stack([np.sin(th) * np.cos(ph), np.sin(th) * np.sin(ph), np.cos(th)], 1)
+    d[0] = [0, 0, 1]
+    d[1] = [np.sin(0.5), 0, np.cos(0.5)]
+    d[2] = [0, -np.sin(0.7), np.cos(0.7)]
+    prob = dict(base, node_x=X, node_y=X.copy(), det_xyz=dets, ray_det=rng.integers(0, 4, R).astype(np.int32),
+                ray_dir=d.astype(np.float32), ray_w=rng.uniform(200, 2000, R).astype(np.float32),
+                counts=np.where(rng.random(R) < 0.2, 0, rng.integers(1, 900, R)).astype(np.int32))
+    op = oracle.Problem(prob)
+    mp = Problem(prob, device=0, max_chains=3)
+    xx, yy = np.meshgrid(X.astype(np.float64), X.astype(np.float64), indexing="ij")
+    H = np.stack([np.stack([110 + 0.2 * xx - 0.1 * yy + 3 * c, 160 + 0.1 * yy + 5 * np.sin(xx / 20) + c])
+                  for c in range(3)]).astype(np.float32)
+    L_d, _ = mp.path_lengths(torch.from_numpy(H).to(DEV))
+    L_o, _ = op.path_lengths(H.astype(np.float64))
+    assert np.all(np.abs(L_d.cpu().numpy() - L_o).max(2) <= 1e-5 * L_o.sum(2))
+    ll_d, G_d = mp.loglik_heights(torch.from_numpy(H).to(DEV))
+    out = op.loglik_grad_H(H.astype(np.float64))
+    assert np.allclose(ll_d.cpu().numpy(), out["ll_dev"], rtol=1e-4)
+    for c in range(3):
+        assert rel_l2(G_d.cpu().numpy()[c].astype(np.float64), out["dldH"][c]) <= 1e-3
+    for q in range(0, R, 37):
+        assert np.array_equal(mp.debug_traversal(q)[0], op.traversal(q)[0])
+
+
+def test_nonfinite_state_sets_status_only_for_that_chain(gpu):
+    mp = gpu("small", max_chains=64)
+    cfg = inputs.CONFIGS["small"]
+    from paper_2603_28907_b200 import inputs as I
+    x = torch.from_numpy(I.chain_states(mp_x_true(), 4, cfg.seed)).to(DEV)
+    x[2, 5] = float("nan")
+    status = torch.zeros(4, dtype=torch.int32, device=DEV)
+    lp, g = mp.logpost_grad(x, status=status)
+    st = status.cpu().numpy()
+    assert st[2] & 1 and st[0] == 0 and st[1] == 0 and st[3] == 0
+    assert np.isfinite(lp.cpu().numpy()[[0, 1, 3]]).all()
+
+
+def mp_x_true():
+    return inputs.make_problem("small")["x_true"]
+
+
+def test_ray_shards_sum_to_whole(gpu, problems):
+    prob = problems("small")
+    R = len(prob["ray_det"])
+    cfg = inputs.CONFIGS["small"]
+    whole = gpu("small", max_chains=8)
+    parts = [Problem(prob, device=0, max_chains=8, ray_lo=lo, ray_hi=hi)
+             for lo, hi in ((0, 5000), (5000, 11111), (11111, R))]
+    x = torch.from_numpy(inputs.chain_states(prob["x_true"], 8, cfg.seed)).to(DEV)
+    lp, g = whole.logpost_grad(x)
+    lps, gs = zip(*[p.logpost_grad(x) for p in parts])
+    assert np.allclose(sum(l.cpu().numpy() for l in lps), lp.cpu().numpy(), rtol=1e-6)
+    gsum = sum(v.cpu().numpy().astype(np.float64) for v in gs)
+    for c in range(8):
+        assert rel_l2(gsum[c], g.cpu().numpy()[c].astype(np.float64)) < 1e-5
