@@ -1,0 +1,293 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: chain-sharded HMC on the Medium geometry.
+
+One STEP = one HMC iteration over this rank's chains:
+Philox momenta, L = 10 fused leapfrog steps (each = one log-posterior+gradient
+evaluation over chains x rays: trace K2 + finish K3), Metropolis accept, the
+a9 statistics (fixed-point acceptance sums, all-reduced over ranks for the
+dual-averaging step size).  Metric = chain x ray log-posterior+gradient
+evaluations per second, whole job: N * C * R * L * K / max-over-ranks time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mt|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...       (N > 1, one rank per GPU)
+
+Scaling is weak: each rank runs --chains-per-gpu chains (default 1024 =
+BASELINE configs[2] Medium), so N = 8 is configs[3]'s 8,192 chains.  L2 is
+flushed (256 MiB write) between timed steps, outside the event pairs.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "log-posterior+grad chain×ray evals/s"
+UNIT = "chain×ray evals/s"
+FP32_PEAK_NOMINAL = 148 * 128 * 2 * 1.965e9 / 1e12   # TFLOP/s: SMs x FP32 lanes x FMA x max clock
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="mt", choices=["mt", "reference"])
+    ap.add_argument("--chains-per-gpu", type=int, default=1024)
+    ap.add_argument("--leapfrog", type=int, default=10)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self, gpu_index=None):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            v = [t.strip() for t in line.split(",")]
+            if len(v) < 9:
+                continue
+            if gpu_index is not None and v[0] != str(gpu_index):
+                continue
+            rows.append(v)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].strip() == "Active"})
+        load = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_baseline(seconds: float, chains: int = 4):
+    """The fp64 oracle, as it stands, on this host's cores: Medium, `chains`
+    chains x all 262,144 rays per evaluation, repeated for ~`seconds`."""
+    import numpy as np
+
+    import oracle
+    from paper_2603_28907_b200 import inputs
+    prob = inputs.make_problem("medium")
+    op = oracle.Problem(prob)
+    x = inputs.chain_states(prob["x_true"], chains, inputs.CONFIGS["medium"].seed).astype(np.float64)
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        op.logpost_grad(x)
+        n += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": n * chains * op.R / dt, "unit": UNIT, "cores": oracle.num_threads(),
+            "kind": "oracle",
+            "sample": f"medium geometry, {chains} near-posterior chains x {op.R} rays per evaluation, "
+                      f"{n} evaluations ({n * chains * op.R:.3g} chain-ray pairs) in {dt:.1f} s, fp64"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle's HMC iteration (fp64 CPU) on a bounded sample."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle
+    from paper_2603_28907_b200 import inputs
+    cfg = inputs.CONFIGS["chain_sharded"]
+    prob = inputs.make_problem("medium")
+    op = oracle.Problem(prob)
+    Cs = 2
+    x = inputs.chain_states(prob["x_true"], Cs, cfg.seed, super_size=8).astype(np.float64)
+    seed = inputs.philox_key(cfg)
+    lg = lambda xx: (lambda o: (o["logp"], o["grad"]))(op.logpost_grad(xx))  # noqa: E731
+    L = args.leapfrog
+    for it in range(args.warmup):
+        x, *_ = oracle.hmc_step(x, cfg.eps, L, lg, seed, it)
+    times = []
+    for it in range(args.steps):
+        t0 = time.perf_counter()
+        x, *_ = oracle.hmc_step(x, cfg.eps, L, lg, seed, args.warmup + it)
+        times.append(time.perf_counter() - t0)
+    T = sum(times)
+    units = Cs * op.R * (L + 1) * args.steps   # L leapfrog evaluations + the initial one
+    v = units / T
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+            "data": "synthetic (seeded Medium geometry; counts = Poisson of the oracle's truth)",
+            "config": {"workload": "chain_sharded HMC iteration (Medium geometry)", "chains": Cs,
+                       "rays": op.R, "leapfrog_steps": L, "params": op.P,
+                       "sample": f"{Cs} chains of the {args.chains_per_gpu}-chain per-GPU shard"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                             "sample": f"{Cs} chains x {op.R} rays x {L} leapfrog steps per HMC iteration"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+
+    from paper_2603_28907_b200 import Problem, inputs
+    from paper_2603_28907_b200.hmc import ChainShard
+
+    ws, rank, local = dist_env()
+    if ws != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}: launch N>1 with torchrun")
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = torch.device(f"cuda:{local}")
+
+    cfg = inputs.CONFIGS["chain_sharded"]
+    prob = inputs.make_problem("medium")
+    C, L = args.chains_per_gpu, args.leapfrog
+    offset = rank * C
+    x0 = inputs.chain_states(prob["x_true"], C, cfg.seed, chain_offset=offset, super_size=8)
+    pb = Problem(prob, device=local, max_chains=C)
+    R, P = pb.R, pb.P
+    shard = ChainShard(pb, x0, seed=inputs.philox_key(cfg), L=L, eps0=cfg.eps, chain_offset=offset,
+                       n_chains_total=C * ws)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MiB > 126 MB L2
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        shard.step(adapt=True)
+    barrier()
+    clocks = ClockSampler() if rank == 0 else None
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    pb.timing_start(args.steps * L + 8)
+    wall0 = time.perf_counter()
+    for k in range(args.steps):
+        flush.zero_()
+        ev[k][0].record()
+        shard.step(adapt=True)
+        ev[k][1].record()
+    barrier()
+    wall = time.perf_counter() - wall0
+    ck = clocks.stop(gpu_index=None) if clocks else None
+    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    tm = pb.timing_read()
+    t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_ms = float(t.item())
+    units = ws * C * R * L * args.steps
+    value = units / (t_ms * 1e-3)
+
+    # dominant kernel (K2 trace): algorithmic FP32 flops per launch / measured launch duration
+    work = json.load(open(os.path.join(ROOT, "data", "work_counts.json")))["medium"]
+    F = work["flops_per_pair"]
+    avg_trace_ms = tm["trace_ms"] / max(tm["trace_launches"], 1)
+    achieved = F * C * R / (avg_trace_ms * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "trace_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get("bytes_per_launch")
+    roofline = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_NOMINAL, "unit": "TFLOP/s",
+                "frac": achieved / FP32_PEAK_NOMINAL, "traffic": traffic,
+                "kernel": "k_trace (K2)", "flops_per_pair": F,
+                "trace_share_of_step": tm["trace_ms"] / t_ms if ws == 1 else None,
+                "avg_trace_launch_ms": avg_trace_ms,
+                "peak_note": "FP32 peak derived: 148 SMs x 128 lanes x 2 x 1.965 GHz (B200_PROFILING.md); "
+                             "F = algorithmic flops per chain x ray from the oracle's work counters "
+                             "(tools/count_work.py, DESIGN.md Roofline)"}
+
+    e2e = None
+    if not args.no_e2e:
+        # same metric through the public API with host buffers: per step, pinned H2D of the
+        # chain states and D2H of (logp, accept_prob).
+        xh = torch.from_numpy(x0).pin_memory()
+        lph = torch.empty(C, dtype=torch.float64).pin_memory()
+        aph = torch.empty(C, dtype=torch.float32).pin_memory()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for k in range(args.steps):
+            shard.x.copy_(xh, non_blocking=True)
+            shard.step(adapt=True)
+            lph.copy_(shard.logp, non_blocking=True)
+            aph.copy_(shard.acc_prob, non_blocking=True)
+        e1.record()
+        barrier()
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if dist is not None:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": units / (float(te.item()) * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": C * P * 4, "d2h_bytes_per_step": C * (8 + 4)}
+
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    base = None
+    if ws == 1 and not args.no_cpu_baseline:
+        base = cpu_baseline(args.cpu_seconds)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded Medium geometry; counts = Poisson of the oracle's truth; "
+                    "near-posterior chain states)",
+            "config": {"workload": "chain_sharded HMC iteration (BASELINE configs[3] geometry = configs[2] Medium)",
+                       "chains_per_gpu": C, "global_chains": C * ws, "rays": R, "params": P,
+                       "leapfrog_steps": L, "parallelism": f"chain-sharded x{ws}",
+                       "l2": "flushed between timed steps (256 MiB write, outside the events)"},
+            "roofline": roofline, "cpu_baseline": base, "e2e": e2e, "clocks": ck,
+            "gpu_launches": tm["all_launches"],
+            "leapfrog_steps_per_s_per_chain": L * args.steps / (t_ms * 1e-3),
+            "wall_s_timed_region": wall}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -141,6 +141,23 @@ int mt_hmc_step(mt_problem *p, int32_t C, float *x, double *logp, float *grad, c
                 int32_t L, uint64_t seed, uint64_t iter, uint64_t chain_offset, float *accept_prob,
                 int32_t *accepted, int32_t *status, mt_stream stream);
 
+/* Per-iteration sampler statistics (step-size adaptation and R-hat, P:652-653,
+ * P:671-687; readings R20/R21).  Any of the three groups may be skipped by
+ * passing NULL:
+ *   accept_prob [C] + acc_fixed [2] (device uint64): acc_fixed[0] +=
+ *     Σ_c round(accept_prob_c · 2^32), acc_fixed[1] += C — exact integer sums,
+ *     so a cross-rank SUM is order-independent;
+ *   x [C][P] + mean, m2 [C][P] (device fp32): Welford update with count
+ *     n_prev + 1 (mean/m2 zero before the first sampling iteration). */
+int mt_stats_update(mt_problem *p, int32_t C, const float *x, const float *accept_prob,
+                    int32_t n_prev, float *mean, float *m2, uint64_t *acc_fixed, mt_stream stream);
+
+/* R-hat partial sums over this rank's C chains after n Welford updates:
+ * out [3][P] (device double) = (Σ_c mean_c, Σ_c mean_c², Σ_c m2_c/(n-1)).
+ * A SUM over ranks gives the global between/within-chain statistics. */
+int mt_rhat_partials(mt_problem *p, int32_t C, const float *mean, const float *m2, int32_t n,
+                     double *out, mt_stream stream);
+
 /* ---- parity / debug entry points (not on the hot path) ---------------- */
 
 /* Heights map of x (device [C][P] -> device H [C][2][n_x][n_y]). */

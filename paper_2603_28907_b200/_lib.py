@@ -41,7 +41,7 @@ class _Desc(ct.Structure):
 EXPORTS = [
     "mt_problem_create", "mt_problem_destroy", "mt_num_params", "mt_num_rays", "mt_loglik_offset",
     "mt_prior_constants", "mt_logpost_grad", "mt_leapfrog", "mt_draw_momenta", "mt_hmc_step",
-    "mt_heights", "mt_loglik_heights", "mt_path_lengths", "mt_debug_traversal", "mt_philox",
+    "mt_stats_update", "mt_rhat_partials", "mt_heights", "mt_loglik_heights", "mt_path_lengths", "mt_debug_traversal", "mt_philox",
     "mt_philox_curand", "mt_timing_start", "mt_timing_read", "mt_measure_fp32_peak", "mt_last_error",
 ]
 
@@ -66,6 +66,8 @@ def lib():
             "mt_leapfrog": ([vp, i32, vp, vp, vp, vp, vp, i32, vp], ct.c_int),
             "mt_draw_momenta": ([vp, i32, vp, u64, u64, u64, vp], ct.c_int),
             "mt_hmc_step": ([vp, i32, vp, vp, vp, vp, i32, u64, u64, u64, vp, vp, vp, vp], ct.c_int),
+            "mt_stats_update": ([vp, i32, vp, vp, i32, vp, vp, vp, vp], ct.c_int),
+            "mt_rhat_partials": ([vp, i32, vp, vp, i32, vp, vp], ct.c_int),
             "mt_heights": ([vp, i32, vp, vp, vp], ct.c_int),
             "mt_loglik_heights": ([vp, i32, vp, vp, vp, vp], ct.c_int),
             "mt_path_lengths": ([vp, i32, vp, vp, vp, vp], ct.c_int),
@@ -223,6 +225,20 @@ class Problem:
                                  chain_offset, _ptr(accept_prob), _ptr(accepted), _ptr(status),
                                  _stream(stream)), "mt_hmc_step")
         return accept_prob, accepted
+
+    def stats_update(self, C: int, x=None, accept_prob=None, n_prev: int = 0, mean=None, m2=None,
+                     acc_fixed=None, stream=None):
+        """a9: fixed-point acceptance sums (int64 [2]) and Welford mean/M2 of x."""
+        _check(lib().mt_stats_update(self.h, C, _ptr(x), _ptr(accept_prob), n_prev, _ptr(mean), _ptr(m2),
+                                     _ptr(acc_fixed), _stream(stream)), "mt_stats_update")
+
+    def rhat_partials(self, C: int, mean, m2, n: int, out=None, stream=None):
+        import torch
+        if out is None:
+            out = torch.empty((3, self.P), dtype=torch.float64, device=mean.device)
+        _check(lib().mt_rhat_partials(self.h, C, _ptr(mean), _ptr(m2), n, _ptr(out), _stream(stream)),
+               "mt_rhat_partials")
+        return out
 
     # -- parity / debug ------------------------------------------------------
     def heights(self, x, stream=None):

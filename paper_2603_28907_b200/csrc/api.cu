@@ -78,7 +78,7 @@ int check_chains(const mt_problem *p, int32_t C) {
 }
 
 void free_all(mt_problem *p) {
-  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_H, p->d_G,
+  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_trav_off, p->d_trav, p->d_H, p->d_G,
                   p->d_band, p->d_ll, p->d_x0, p->d_g0, p->d_mom, p->d_kin0, p->d_kin1, p->d_lp0};
   for (void *b : bufs)
     if (b) cudaFree(b);
@@ -194,6 +194,8 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   // ---- device buffers ----
   size_t R = (size_t)(p->R > 0 ? p->R : 1), MC = (size_t)(p->max_chains > 0 ? p->max_chains : 1);
   size_t P = p->P;
+  size_t MC32 = (MC + 31) / 32 * 32;   // chain-interleaved workspaces hold whole groups of 32
+  if (const char *e = getenv("MT_SMEMH_LIMIT")) p->smemh_limit = atoi(e);
   cudaError_t e = cudaSuccess;
 #define ALLOC(ptr, bytes)                                        \
   if (e == cudaSuccess) e = cudaMalloc((void **)&(ptr), (bytes));
@@ -202,8 +204,8 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   ALLOC(p->d_ray_a, sizeof(float4) * R);
   ALLOC(p->d_ray_b, sizeof(float4) * R);
   ALLOC(p->d_obase, sizeof(float) * R);
-  ALLOC(p->d_H, sizeof(float) * MC * P);
-  ALLOC(p->d_G, sizeof(float) * MC * P);
+  ALLOC(p->d_H, sizeof(float) * MC32 * P);
+  ALLOC(p->d_G, sizeof(float) * MC32 * P);
   ALLOC(p->d_band, sizeof(float4) * MC);
   ALLOC(p->d_ll, sizeof(double) * MC);
   ALLOC(p->d_x0, sizeof(float) * MC * P);
@@ -224,13 +226,15 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   if (e == cudaSuccess && p->R > 0) e = cudaMemcpy(p->d_ray_a, ra.data(), sizeof(float4) * p->R, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && p->R > 0) e = cudaMemcpy(p->d_ray_b, rb.data(), sizeof(float4) * p->R, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && p->R > 0) e = cudaMemcpy(p->d_obase, ob.data(), sizeof(float) * p->R, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemset(p->d_G, 0, sizeof(float) * MC * P);
+  if (e == cudaSuccess) e = cudaMemset(p->d_G, 0, sizeof(float) * MC32 * P);
+  if (e == cudaSuccess) e = cudaMemset(p->d_H, 0, sizeof(float) * MC32 * P);
   if (e == cudaSuccess) e = cudaMemset(p->d_ll, 0, sizeof(double) * MC);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = build_traversal(p);   // a2, once per problem (exact predicates)
   if (e != cudaSuccess) {
     free_all(p);
     delete p;
-    return cuda_err(e, "mt_problem_create upload");
+    return cuda_err(e, "mt_problem_create upload/traversal");
   }
   *out = p;
   return MT_OK;
@@ -319,12 +323,37 @@ int mt_hmc_step(mt_problem *p, int32_t C, float *x, double *logp, float *grad, c
   return MT_OK;
 }
 
+int mt_stats_update(mt_problem *p, int32_t C, const float *x, const float *accept_prob,
+                    int32_t n_prev, float *mean, float *m2, uint64_t *acc_fixed, mt_stream stream) {
+  if (int r = check_chains(p, C)) return r;
+  if (n_prev < 0) return set_err(MT_EINVAL, "n_prev < 0");
+  if ((x || mean || m2) && !(x && mean && m2)) return set_err(MT_EINVAL, "x, mean, m2 must all be given");
+  if ((accept_prob != nullptr) != (acc_fixed != nullptr))
+    return set_err(MT_EINVAL, "accept_prob and acc_fixed must both be given");
+  DevGuard g(p->device);
+  CK(launch_stats(p, C, x, accept_prob, n_prev, mean, m2,
+                  reinterpret_cast<unsigned long long *>(acc_fixed), (cudaStream_t)stream));
+  return MT_OK;
+}
+
+int mt_rhat_partials(mt_problem *p, int32_t C, const float *mean, const float *m2, int32_t n,
+                     double *out, mt_stream stream) {
+  if (int r = check_chains(p, C)) return r;
+  if (check_ptr(mean, "mean") || check_ptr(m2, "m2") || check_ptr(out, "out")) return MT_EINVAL;
+  if (n < 2) return set_err(MT_EINVAL, "n = %d < 2", n);
+  DevGuard g(p->device);
+  CK(launch_rhat_partials(p, C, mean, m2, n, out, (cudaStream_t)stream));
+  return MT_OK;
+}
+
 int mt_heights(mt_problem *p, int32_t C, const float *x, float *H, mt_stream stream) {
   if (int r = check_chains(p, C)) return r;
   if (C == 0) return MT_OK;
   if (check_ptr(x, "x") || check_ptr(H, "H")) return MT_EINVAL;
   DevGuard g(p->device);
-  CK(launch_heights(p, C, x, H, p->d_band, (cudaStream_t)stream));
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(launch_heights(p, C, x, p->d_H, p->d_band, s));
+  CK(launch_tile(p, C, p->d_H, H, 0, s));
   return MT_OK;
 }
 
@@ -360,8 +389,10 @@ int mt_loglik_heights(mt_problem *p, int32_t C, const float *H, double *ll, floa
   p->all_launches++;
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(ll, 0, sizeof(double) * C, s));
-  CK(cudaMemsetAsync(dldH, 0, sizeof(float) * (size_t)C * p->P, s));
-  CK(launch_trace(p, TRACE_LL, C, H, p->d_band, dldH, ll, nullptr, nullptr, s));
+  CK(launch_tile(p, C, H, p->d_H, 1, s));
+  CK(launch_trace(p, TRACE_LL, C, p->d_H, p->d_band, p->d_G, ll, nullptr, nullptr, s));
+  CK(launch_tile(p, C, p->d_G, dldH, 0, s));
+  CK(cudaMemsetAsync(p->d_G, 0, sizeof(float) * (size_t)(C + 31) / 32 * 32 * p->P, s));
   return MT_OK;
 }
 
@@ -374,7 +405,8 @@ int mt_path_lengths(mt_problem *p, int32_t C, const float *H, float *L, float *O
   k_band_of<<<C, 256, 0, s>>>(H, p->N, p->d_band);
   p->all_launches++;
   CK(cudaGetLastError());
-  CK(launch_trace(p, TRACE_PATH, C, H, p->d_band, nullptr, nullptr, L, O, s));
+  CK(launch_tile(p, C, H, p->d_H, 1, s));
+  CK(launch_trace(p, TRACE_PATH, C, p->d_H, p->d_band, nullptr, nullptr, L, O, s));
   return MT_OK;
 }
 
@@ -384,22 +416,25 @@ int mt_debug_traversal(mt_problem *p, int64_t ray, int32_t *ij, float *s_in, flo
   if (ray < 0 || ray >= p->R) return set_err(MT_EINVAL, "ray %lld out of range", (long long)ray);
   if (cap < 0 || !n || (cap > 0 && (!ij || !s_in || !s_out))) return set_err(MT_EINVAL, "bad output buffers");
   DevGuard g(p->device);
-  int c = cap > 0 ? cap : 1;
-  int32_t *d_ij = nullptr, *d_n = nullptr;
-  float *d_si = nullptr, *d_so = nullptr;
-  CK(cudaMalloc(&d_ij, sizeof(int32_t) * 2 * c));
-  CK(cudaMalloc(&d_si, sizeof(float) * c));
-  CK(cudaMalloc(&d_so, sizeof(float) * c));
-  CK(cudaMalloc(&d_n, sizeof(int32_t)));
-  cudaError_t e = launch_debug_traversal(p, ray, d_ij, d_si, d_so, cap, d_n);
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
-  if (e == cudaSuccess) e = cudaMemcpy(n, d_n, sizeof(int32_t), cudaMemcpyDeviceToHost);
-  int m = (e == cudaSuccess) ? (*n < cap ? *n : cap) : 0;
-  if (e == cudaSuccess && m > 0) e = cudaMemcpy(ij, d_ij, sizeof(int32_t) * 2 * m, cudaMemcpyDeviceToHost);
-  if (e == cudaSuccess && m > 0) e = cudaMemcpy(s_in, d_si, sizeof(float) * m, cudaMemcpyDeviceToHost);
-  if (e == cudaSuccess && m > 0) e = cudaMemcpy(s_out, d_so, sizeof(float) * m, cudaMemcpyDeviceToHost);
-  cudaFree(d_ij); cudaFree(d_si); cudaFree(d_so); cudaFree(d_n);
-  if (e != cudaSuccess) return cuda_err(e, "mt_debug_traversal");
+  // the stored traversal the trace kernels read (built by the exact device DDA)
+  int32_t off[2];
+  CK(cudaMemcpy(off, p->d_trav_off + ray, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost));
+  *n = (int32_t)(off[1] - off[0]);
+  int m = *n < cap ? *n : cap;
+  if (m > 0) {
+    std::vector<int2> cells(m);
+    CK(cudaMemcpy(cells.data(), p->d_trav + off[0], sizeof(int2) * m, cudaMemcpyDeviceToHost));
+    float prev = 0.f;
+    for (int k = 0; k < m; k++) {
+      ij[2 * k] = cells[k].x & 0xffff;
+      ij[2 * k + 1] = cells[k].x >> 16;
+      float so;
+      memcpy(&so, &cells[k].y, sizeof so);
+      s_in[k] = prev;
+      s_out[k] = so;
+      prev = so;
+    }
+  }
   return MT_OK;
 }
 

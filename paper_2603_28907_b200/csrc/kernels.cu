@@ -131,12 +131,11 @@ __device__ __forceinline__ void momenta4(uint64_t seed, uint64_t iter, uint64_t 
 __global__ void __launch_bounds__(MT_THREADS) k_heights(FinishArgs a, const float *x) {
   int c = blockIdx.x;
   const float *xc = x + (size_t)c * a.P;
-  float *Hc = a.H + (size_t)c * 2 * a.N;
   BlockRed v = {3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f, 0.0, 0.0, 0};
   for (int k = threadIdx.x; k < a.N; k += blockDim.x) {
     NodeH h = node_heights(xc[k], xc[a.N + k], a.inv_sigma[0], a.inv_sigma[1], a.z_top, false);
-    Hc[k] = h.H0;
-    Hc[a.N + k] = h.H1;
+    a.H[tix(c, 0, k, a.N)] = h.H0;
+    a.H[tix(c, 1, k, a.N)] = h.H1;
     v.mn0 = fminf(v.mn0, h.H0); v.mx0 = fmaxf(v.mx0, h.H0);
     v.mn1 = fminf(v.mn1, h.H1); v.mx1 = fmaxf(v.mx1, h.H1);
   }
@@ -156,19 +155,19 @@ __global__ void __launch_bounds__(MT_THREADS) k_finish(FinishArgs a) {
   float *xc = a.x + (size_t)c * a.P;
   for (int k = threadIdx.x; k < a.P; k += blockDim.x) xs[k] = xc[k];
   __syncthreads();
-  float *Gc = const_cast<float *>(a.G) + (size_t)c * 2 * N;
+  float *Gt = const_cast<float *>(a.G);
   float *gc = a.grad + (size_t)c * a.P;
   float *pc = MODE != FIN_PLAIN ? a.mom + (size_t)c * a.P : nullptr;
-  float *Hc = a.H + (size_t)c * 2 * N;
   const float eps = MODE != FIN_PLAIN ? a.eps[c] : 0.f;
   BlockRed v = {3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f, 0.0, 0.0, 0};
   for (int k = threadIdx.x; k < N; k += blockDim.x) {
     const int i = k / ny, j = k - i * ny;
     float x0 = xs[k], x1 = xs[N + k];
     NodeH h = node_heights(x0, x1, a.inv_sigma[0], a.inv_sigma[1], a.z_top, true);
-    float G0 = Gc[k], G1 = Gc[N + k];
-    Gc[k] = 0.f;
-    Gc[N + k] = 0.f;
+    const size_t t0 = tix(c, 0, k, N), t1 = tix(c, 1, k, N);
+    float G0 = Gt[t0], G1 = Gt[t1];
+    Gt[t0] = 0.f;
+    Gt[t1] = 0.f;
     double gx0 = (double)G0 * h.J0 + (double)G1 * h.J10;
     double gx1 = (double)G1 * h.J11;
     if (a.prior_on) {
@@ -195,8 +194,8 @@ __global__ void __launch_bounds__(MT_THREADS) k_finish(FinishArgs a) {
       xc[k] = xn0;
       xc[N + k] = xn1;
       NodeH hn = node_heights(xn0, xn1, a.inv_sigma[0], a.inv_sigma[1], a.z_top, false);
-      Hc[k] = hn.H0;
-      Hc[N + k] = hn.H1;
+      a.H[t0] = hn.H0;
+      a.H[t1] = hn.H1;
       v.mn0 = fminf(v.mn0, hn.H0); v.mx0 = fmaxf(v.mx0, hn.H0);
       v.mn1 = fminf(v.mn1, hn.H1); v.mx1 = fmaxf(v.mx1, hn.H1);
     } else if (MODE == FIN_LAST) {  // final half kick
@@ -223,7 +222,6 @@ __global__ void __launch_bounds__(MT_THREADS) k_kick_drift(FinishArgs a) {
   const int c = blockIdx.x, N = a.N;
   float *xc = a.x + (size_t)c * a.P, *pc = a.mom + (size_t)c * a.P;
   const float *gc = a.grad + (size_t)c * a.P;
-  float *Hc = a.H + (size_t)c * 2 * N;
   const float eps = a.eps[c];
   BlockRed v = {3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f, 0.0, 0.0, 0};
   for (int k = threadIdx.x; k < N; k += blockDim.x) {
@@ -234,8 +232,8 @@ __global__ void __launch_bounds__(MT_THREADS) k_kick_drift(FinishArgs a) {
     xc[k] = x0;
     xc[N + k] = x1;
     NodeH h = node_heights(x0, x1, a.inv_sigma[0], a.inv_sigma[1], a.z_top, false);
-    Hc[k] = h.H0;
-    Hc[N + k] = h.H1;
+    a.H[tix(c, 0, k, N)] = h.H0;
+    a.H[tix(c, 1, k, N)] = h.H1;
     v.mn0 = fminf(v.mn0, h.H0); v.mx0 = fmaxf(v.mx0, h.H0);
     v.mn1 = fminf(v.mn1, h.H1); v.mx1 = fmaxf(v.mx1, h.H1);
   }
@@ -252,7 +250,6 @@ __global__ void __launch_bounds__(MT_THREADS) k_hmc_begin(FinishArgs a, const do
   const int c = blockIdx.x, N = a.N, P = a.P;
   float *xc = a.x + (size_t)c * P, *pc = a.mom + (size_t)c * P;
   const float *gc = a.grad + (size_t)c * P;
-  float *Hc = a.H + (size_t)c * 2 * N;
   const float eps = a.eps[c];
   const int nq = (P + 3) / 4;
   BlockRed v = {3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f, 0.0, 0.0, 0};
@@ -277,8 +274,8 @@ __global__ void __launch_bounds__(MT_THREADS) k_hmc_begin(FinishArgs a, const do
   __syncthreads();
   for (int k = threadIdx.x; k < N; k += blockDim.x) {
     NodeH h = node_heights(xc[k], xc[N + k], a.inv_sigma[0], a.inv_sigma[1], a.z_top, false);
-    Hc[k] = h.H0;
-    Hc[N + k] = h.H1;
+    a.H[tix(c, 0, k, N)] = h.H0;
+    a.H[tix(c, 1, k, N)] = h.H1;
     v.mn0 = fminf(v.mn0, h.H0); v.mx0 = fmaxf(v.mx0, h.H0);
     v.mn1 = fminf(v.mn1, h.H1); v.mx1 = fmaxf(v.mx1, h.H1);
   }
@@ -465,6 +462,25 @@ cudaError_t launch_philox(const uint32_t *ctr, uint32_t k0, uint32_t k1, uint32_
   k_philox<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(reinterpret_cast<const uint4 *>(ctr),
                                                        make_uint2(k0, k1),
                                                        reinterpret_cast<uint4 *>(out), n, use_curand);
+  return cudaGetLastError();
+}
+
+// [C][2][N] <-> chain-interleaved [C/32][2][N][32]
+__global__ void k_tile(int C, int N, const float *src, float *dst, int to_tiled) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)C * 2 * N) return;
+  int c = (int)(t / (2 * N)), m = (int)(t - (int64_t)c * 2 * N);
+  size_t ti = tix(c, m / N, m % N, N);
+  if (to_tiled) dst[ti] = src[t];
+  else dst[t] = src[ti];
+}
+
+cudaError_t launch_tile(mt_problem *p, int C, const float *src, float *dst, int to_tiled,
+                        cudaStream_t s) {
+  if (C <= 0) return cudaSuccess;
+  int64_t n = (int64_t)C * 2 * p->N;
+  k_tile<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(C, p->N, src, dst, to_tiled);
+  p->all_launches++;
   return cudaGetLastError();
 }
 

@@ -13,6 +13,13 @@
 #define MT_MAX_NODES 4096
 #define MT_THREADS 256
 
+// Index of node k of surface l of chain c in the chain-interleaved layout
+// [group = c/32][l][node][c % 32] used for the heights and ∂ℓ/∂H workspaces
+// (a warp of 32 chains reads one 128-B line per node).
+__host__ __device__ __forceinline__ size_t tix(int c, int l, int k, int N) {
+  return ((size_t)(c >> 5) * 2 * N + (size_t)l * N + k) * 32 + (c & 31);
+}
+
 // Per-problem constants every trace launch needs (passed by value).
 struct TraceConsts {
   int nx, ny, N;     // nodes per axis, nodes per surface
@@ -31,6 +38,8 @@ struct TraceArgs {
   const float *X, *Y;           // node coordinates
   const float4 *ray_a, *ray_b;
   const float *obase;           // ρ_rock s_exit + ρ_ext L_ext (path-length export only)
+  const int32_t *trav_off;      // [R+1] CSR offsets of each ray's stored traversal
+  const int2 *trav;             // {i | j << 16, s_out bits} per cell, in ray order (a2)
   int64_t R;                    // rays in the shard
   int64_t rays_per_block;
   int C;                        // chains in this call
@@ -80,6 +89,9 @@ struct mt_problem {
   float *d_X = nullptr, *d_Y = nullptr;
   float4 *d_ray_a = nullptr, *d_ray_b = nullptr;
   float *d_obase = nullptr;
+  int32_t *d_trav_off = nullptr;
+  int2 *d_trav = nullptr;
+  int64_t trav_cells = 0;
   float *d_H = nullptr, *d_G = nullptr;
   float4 *d_band = nullptr;
   double *d_ll = nullptr;
@@ -89,6 +101,7 @@ struct mt_problem {
   // trace launch shape
   int trace_k = 0;              // chains per block (0 = auto)
   int trace_s = 0;              // ray splits (0 = auto)
+  int smemh_limit = 100 * 1024; // stage a 32-chain height tile in smem when it fits
   // measurement
   bool timing = false;
   std::vector<cudaEvent_t> ev_a, ev_b;
@@ -115,8 +128,13 @@ cudaError_t launch_hmc_end(mt_problem *p, int C, float *x, double *logp, float *
                            int32_t *accepted, int32_t *status, cudaStream_t s);
 cudaError_t launch_momenta(mt_problem *p, int C, float *mom, uint64_t seed, uint64_t iter,
                            uint64_t chain_offset, cudaStream_t s);
-cudaError_t launch_debug_traversal(mt_problem *p, int64_t ray, int32_t *d_ij, float *d_si,
-                                   float *d_so, int cap, int32_t *d_n);
+cudaError_t build_traversal(mt_problem *p);
 cudaError_t launch_philox(const uint32_t *ctr, uint32_t k0, uint32_t k1, uint32_t *out,
                           int64_t n, int use_curand, cudaStream_t s);
 cudaError_t run_fp32_peak(int device, double *tflops, double *mhz);
+cudaError_t launch_stats(mt_problem *p, int C, const float *x, const float *acc, int32_t n_prev,
+                         float *mean, float *m2, unsigned long long *acc_fixed, cudaStream_t s);
+cudaError_t launch_tile(mt_problem *p, int C, const float *src, float *dst, int to_tiled,
+                        cudaStream_t s);
+cudaError_t launch_rhat_partials(mt_problem *p, int C, const float *mean, const float *m2,
+                                 int32_t n, double *out, cudaStream_t s);

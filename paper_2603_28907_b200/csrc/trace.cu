@@ -1,6 +1,6 @@
 // trace.cu — K2: ray x chain trace through the bilinear height fields, fused
 // opacity -> flux -> Poisson log-likelihood epilogue and adjoint scatter of
-// ∂ℓ/∂H into per-chain shared-memory gradient tiles (B200, sm_100a).
+// ∂ℓ/∂H (B200, sm_100a).
 //
 // Method: opacity O = ∫ρ du along the sensor ray with the
 // Heaviside layer map evaluated exactly on bilinear surfaces (R1,
@@ -8,19 +8,25 @@
 // Gradient: reverse mode by hand: a crossing of surface l at
 // (u_c, v_c) with slope g' contributes φ_node(u_c, v_c)/|g'| to ∂B_l/∂h_node.
 //
-// Mapping: grid = (ray chunks, chain groups of K); block of
-// 256 threads; thread = one ray at a time, processing the K chains of its block
-// in turn.  The K chains' height fields and gradient tiles live in shared
-// memory; ray descriptors are two coalesced float4 loads per ray, shared by
-// the K chains; the exact traversal start (DDA state at the band entry) is
-// computed once per ray and reused by the K chains.
+// The traversal (ordered cells of each ray, a2) does not depend on the
+// geometry, so it is computed ONCE per problem by k_build_trav with exact
+// predicates (HP3) and stored as a CSR list; the hot kernels only read it.
+//
+// Two mappings:
+//  * chain lanes (C >= 16, the hot configuration): warp = one ray x 32 chains,
+//    lane = chain.  Ray, traversal and control flow are warp-uniform; heights
+//    are coalesced 128-B lines of the chain-interleaved layout (shared memory
+//    when a 32-chain tile fits, else L1-cached global loads); the adjoint is a
+//    coalesced RED.ADD.F32 into the interleaved ∂ℓ/∂H buffer (no CAS loops, no
+//    intra-warp contention).
+//  * ray lanes (small C, e.g. the single-chain ray-sharded config): block = K
+//    chains with shared-memory height and gradient tiles, thread = ray.
 #include <math.h>
 
 #include "mt_internal.cuh"
 
 namespace {
 
-constexpr int MAXREC = 4;       // crossing records kept in registers per chain x ray
 constexpr float GTHR = 0.1f;    // |g'| below which a crossing is re-solved in fp64
 constexpr float ZTHR = 1e-3f;   // near-tangent band (m) re-solved in fp64
 
@@ -38,8 +44,6 @@ __device__ __forceinline__ int cmp_prod(float a, float b, float c, float d) {
 
 struct Ray {
   float ox, oy, dx, dy, dz, s_exit, tb, cnt;
-  float adx, ady, iadx, iady;
-  int sx, sy;
 };
 
 __device__ __forceinline__ Ray load_ray(const float4 *__restrict__ A, const float4 *__restrict__ B,
@@ -48,69 +52,71 @@ __device__ __forceinline__ Ray load_ray(const float4 *__restrict__ A, const floa
   Ray y;
   y.ox = a.x; y.oy = a.y; y.dx = a.z; y.dy = a.w;
   y.dz = b.x; y.s_exit = b.y; y.tb = b.z; y.cnt = b.w;
-  y.adx = fabsf(y.dx); y.ady = fabsf(y.dy);
-  y.iadx = y.adx > 0.f ? 1.f / y.adx : 0.f;
-  y.iady = y.ady > 0.f ? 1.f / y.ady : 0.f;
-  y.sx = y.dx > 0.f ? 1 : (y.dx < 0.f ? -1 : 0);
-  y.sy = y.dy > 0.f ? 1 : (y.dy < 0.f ? -1 : 0);
   return y;
 }
 
-// Next traversal event of the ray in cell (i, j): bit 1 = crosses an x-line,
-// bit 2 = a y-line, bit 4 = leaves the box (top, or a wall line).  Events are
-// ordered by exact comparisons; ties step both indices (R16).  s_ev = parameter
-// of the event (fp32).  Shared by the hot kernel and the debug export.
-__device__ __forceinline__ int dda_next(const Ray &r, int i, int j, const float *Xs,
+// ---------------------------------------------------------------------------
+// exact traversal (a2): used only by the per-problem builder
+// ---------------------------------------------------------------------------
+struct DdaRay {
+  Ray r;
+  float adx, ady, iadx, iady;
+  int sx, sy;
+};
+
+__device__ __forceinline__ DdaRay dda_ray(const Ray &r) {
+  DdaRay y;
+  y.r = r;
+  y.adx = fabsf(r.dx); y.ady = fabsf(r.dy);
+  y.iadx = y.adx > 0.f ? 1.f / y.adx : 0.f;
+  y.iady = y.ady > 0.f ? 1.f / y.ady : 0.f;
+  y.sx = r.dx > 0.f ? 1 : (r.dx < 0.f ? -1 : 0);
+  y.sy = r.dy > 0.f ? 1 : (r.dy < 0.f ? -1 : 0);
+  return y;
+}
+
+// Next event of the ray in cell (i, j): bit 1 = crosses an x-line, bit 2 = a
+// y-line, bit 4 = leaves the box (top, or a wall line).  Events are ordered by
+// exact comparisons; ties step both indices (R16).  s_ev = event parameter.
+__device__ __forceinline__ int dda_next(const DdaRay &q, int i, int j, const float *Xs,
                                         const float *Ys, int nx, int ny, float z_top,
                                         float &s_ev) {
-  float bn = z_top, bd = r.dz;  // top exit z_top/d_z (detectors at z = 0)
+  float bn = z_top, bd = q.r.dz;  // top exit z_top/d_z (detectors at z = 0)
   float numx = 0.f, numy = 0.f;
   int ev = 4;
-  if (r.sx) {
-    numx = r.sx > 0 ? Xs[i + 1] - r.ox : r.ox - Xs[i];  // exact (HP3)
-    int c = cmp_prod(numx, bd, bn, r.adx);               // numx/adx vs bn/bd
-    if (c < 0) { bn = numx; bd = r.adx; ev = 1; }
+  if (q.sx) {
+    numx = q.sx > 0 ? Xs[i + 1] - q.r.ox : q.r.ox - Xs[i];  // exact (HP3)
+    int c = cmp_prod(numx, bd, bn, q.adx);                   // numx/adx vs bn/bd
+    if (c < 0) { bn = numx; bd = q.adx; ev = 1; }
     else if (c == 0) ev |= 1;
   }
-  if (r.sy) {
-    numy = r.sy > 0 ? Ys[j + 1] - r.oy : r.oy - Ys[j];
-    int c = cmp_prod(numy, bd, bn, r.ady);
+  if (q.sy) {
+    numy = q.sy > 0 ? Ys[j + 1] - q.r.oy : q.r.oy - Ys[j];
+    int c = cmp_prod(numy, bd, bn, q.ady);
     if (c < 0) { ev = 2; }
     else if (c == 0) ev |= 2;
   }
-  if (ev & 4) s_ev = r.s_exit;
-  else if (ev & 1) s_ev = numx * r.iadx;
-  else s_ev = numy * r.iady;
-  if ((ev & 1) && ((r.sx > 0 && i + 1 == nx - 1) || (r.sx < 0 && i == 0))) ev |= 4;
-  if ((ev & 2) && ((r.sy > 0 && j + 1 == ny - 1) || (r.sy < 0 && j == 0))) ev |= 4;
+  if (ev & 4) s_ev = q.r.s_exit;
+  else if (ev & 1) s_ev = numx * q.iadx;
+  else s_ev = numy * q.iady;
+  if ((ev & 1) && ((q.sx > 0 && i + 1 == nx - 1) || (q.sx < 0 && i == 0))) ev |= 4;
+  if ((ev & 2) && ((q.sy > 0 && j + 1 == ny - 1) || (q.sy < 0 && j == 0))) ev |= 4;
   return ev;
 }
 
-// Cell index along one axis at ray parameter s: the largest i in [0, n-2]
-// with X_i <= x(s) (d >= 0) or X_i < x(s) (d < 0), i.e. the cell the ray is in
-// (entering side on ties, R16).  Exact predicate in fp64.
-__device__ __forceinline__ int locate_axis(const float *Xs, int n, float o, float d, float s,
-                                           float x0, float inv_mean) {
-  float xs = fmaf(s, d, o);
-  int i = (int)floorf((xs - x0) * inv_mean);
-  i = max(0, min(n - 2, i));
-  double sd = (double)s * (double)d;
-  auto reached = [&](int k) -> bool {
-    double dxk = (double)(Xs[k] - o);
-    return d < 0.f ? (dxk < sd) : (dxk <= sd);
-  };
-  while (i < n - 2 && reached(i + 1)) i++;
-  while (i > 0 && !reached(i)) i--;
+// Cell index along one axis at the ray origin: the largest i in [0, n-2] with
+// X_i <= o (d >= 0) or X_i < o (d < 0), i.e. the cell in the direction of
+// travel when o lies on a line (R16).
+__device__ __forceinline__ int start_axis(const float *Xs, int n, float o, float d) {
+  int i = 0;
+  for (int k = 0; k < n - 1; k++)
+    if (d < 0.f ? (Xs[k] < o) : (Xs[k] <= o)) i = k;
   return i;
 }
 
-struct Rec {
-  int cell;       // (l << 16) | (i*ny + j)
-  float u, v, ig; // crossing position in the cell, 1/|g'|
-};
-
-// Below-surface length of the ray inside one cell of one surface and the
-// crossings (sign changes of g), in precision T.  g(τ) = g0 + g1 τ + g2 τ².
+// ---------------------------------------------------------------------------
+// per-cell analytic solve (a3)
+// ---------------------------------------------------------------------------
 template <typename T>
 struct CellSol {
   T below;
@@ -118,29 +124,21 @@ struct CellSol {
   T tc[2], gp[2];
 };
 
+// Split [0, L] at the real roots of g0 + g1 τ + g2 τ² (stable quadratic form;
+// g2 = 0 gives the linear root through the second formula) and add the pieces
+// with g > 0 at their midpoint (strict, R17); crossings = sign changes.
 template <typename T>
-__device__ __forceinline__ CellSol<T> solve_roots(T g0, T g1, T g2, T L) {
+__device__ __forceinline__ CellSol<T> classify(T g0, T g1, T g2, T L, T t1, T t2, bool two) {
   CellSol<T> o;
   o.n = 0;
   T rt[2];
   int nr = 0;
-  T disc = g1 * g1 - T(4) * g2 * g0;
-  if (g2 == T(0)) {
-    if (g1 != T(0)) {
-      T t = -g0 / g1;
-      if (t > T(0) && t < L) rt[nr++] = t;
-    }
-  } else if (disc > T(0)) {
-    T sq = sqrt(disc);
-    T q = T(-0.5) * (g1 + (g1 >= T(0) ? sq : -sq));
-    T t1 = q / g2, t2 = g0 / q;
+  if (two) {
     if (t1 > t2) { T tmp = t1; t1 = t2; t2 = tmp; }
     if (t1 > T(0) && t1 < L) rt[nr++] = t1;
     if (t2 > T(0) && t2 < L && t2 != t1) rt[nr++] = t2;
   }
-  // split [0, L] at the roots; sign of g at piece midpoints (strict >, R17)
-  T below = T(0);
-  T e0 = T(0);
+  T below = T(0), e0 = T(0);
   int prev = 0;
   for (int k = 0; k <= nr; k++) {
     T e1 = k < nr ? rt[k] : L;
@@ -160,24 +158,7 @@ __device__ __forceinline__ CellSol<T> solve_roots(T g0, T g1, T g2, T L) {
   return o;
 }
 
-// Cell-local quadratic g(τ) = h(u(τ), v(τ)) - z(τ), τ = s' - s (R2): with
-// h = a + b u + c v + e u v, u = u0 + α τ, v = v0 + β τ, z = d_z (s + τ).
-__device__ __forceinline__ void cell_coeffs(float h00, float h10, float h01, float h11, float Xi,
-                                            float Yj, float idx, float idy, const Ray &r, float s,
-                                            float &u0, float &v0, float &al, float &be, float &g0,
-                                            float &g1, float &g2) {
-  u0 = (fmaf(s, r.dx, r.ox) - Xi) * idx;
-  v0 = (fmaf(s, r.dy, r.oy) - Yj) * idy;
-  float z0 = s * r.dz;
-  al = r.dx * idx;
-  be = r.dy * idy;
-  float b = h10 - h00, c = h01 - h00, e = (h11 - h10) - (h01 - h00);
-  g0 = (h00 - z0) + u0 * (b + e * v0) + c * v0;
-  g1 = b * al + c * be + e * (u0 * be + v0 * al) - r.dz;
-  g2 = e * al * be;
-}
-
-// fp64 re-solve: coefficients from the exact cell spacing.
+// fp64 re-solve from the same fp32 inputs, exact cell spacing (HP2 lever 1).
 __device__ __noinline__ CellSol<double> solve_cell_f64(float h00, float h10, float h01, float h11,
                                                        float Xi, float Xi1, float Yj, float Yj1,
                                                        const Ray &r, float s, float s1,
@@ -193,228 +174,471 @@ __device__ __noinline__ CellSol<double> solve_cell_f64(float h00, float h10, flo
   double g0 = ((double)h00 - z0) + u0 * (b + e * v0) + c * v0;
   double g1 = b * al + c * be + e * (u0 * be + v0 * al) - (double)r.dz;
   double g2 = e * al * be;
-  return solve_roots<double>(g0, g1, g2, (double)s1 - (double)s);
+  double L = (double)s1 - (double)s;
+  double disc = g1 * g1 - 4.0 * g2 * g0, t1 = 0, t2 = 0;
+  bool two = disc > 0.0;
+  if (two) {
+    double q = -0.5 * (g1 + (g1 >= 0.0 ? sqrt(disc) : -sqrt(disc)));
+    t1 = q / g2;   // ±inf when g2 = 0: out of range
+    t2 = g0 / q;
+  }
+  return classify<double>(g0, g1, g2, L, t1, t2, two);
 }
 
 struct Geo {
   const float *Xs, *Ys, *idx, *idy;
   int nx, ny, N;
-  float z_top;
 };
 
-// Process one cell [s, s1] of surface l for one chain: adds the below length
-// to B; records (or, SCAT, scatters with factor f) the crossings.
-template <bool SCAT>
-__device__ __forceinline__ void do_cell(const Geo &g, const Ray &r, const float *Hl, float *Gl,
-                                        int l, int i, int j, float s, float s1, float zmin,
-                                        float zmax, float &B, Rec *rec, int &nrec, bool &ovf,
-                                        float f) {
-  float za = s * r.dz, zb = s1 * r.dz;
-  if (zb <= zmin) { B += s1 - s; return; }     // whole cell below the surface's lowest node
-  if (za >= zmax) return;                       // whole cell above its highest node
-  int base = i * g.ny + j;
-  float h00 = Hl[base], h10 = Hl[base + g.ny], h01 = Hl[base + 1], h11 = Hl[base + g.ny + 1];
-  float cmin = fminf(fminf(h00, h10), fminf(h01, h11));
-  float cmax = fmaxf(fmaxf(h00, h10), fmaxf(h01, h11));
-  if (zb <= cmin) { B += s1 - s; return; }     // bilinear min is at a corner
-  if (za >= cmax) return;
-  float u0, v0, al, be, g0, g1, g2;
-  cell_coeffs(h00, h10, h01, h11, g.Xs[i], g.Ys[j], g.idx[i], g.idy[j], r, s, u0, v0, al,
-                     be, g0, g1, g2);
-  float L = s1 - s;
-  CellSol<float> so = solve_roots<float>(g0, g1, g2, L);
-  bool bad = false;
-  for (int k = 0; k < so.n; k++) bad |= fabsf(so.gp[k]) < GTHR;
-  if (!bad && g2 != 0.f) {  // near-tangent: vertex inside with |g(vertex)| small
-    float tv = -g1 / (2.f * g2);
-    float disc = g1 * g1 - 4.f * g2 * g0;
-    if (tv > 0.f && tv < L && fabsf(disc) < 4.f * fabsf(g2) * ZTHR) bad = true;
-  }
-  float below;
-  int ncr;
-  float uc[2], vc[2], igc[2];
-  if (!bad) {
-    below = so.below;
-    ncr = so.n;
-    for (int k = 0; k < 2; k++) {
-      if (k < ncr) {
-        uc[k] = u0 + al * so.tc[k];
-        vc[k] = v0 + be * so.tc[k];
-        igc[k] = 1.f / fabsf(so.gp[k]);
-      }
-    }
+// Crossing records of one chain x ray: up to RCAP per surface, kept in shared
+// memory at slot [(l*RCAP + m)*blockDim + tid] (conflict-free: consecutive
+// threads, consecutive words); more set the overflow flag (handled by a
+// scattering re-walk).
+constexpr int RCAP = 4;
+struct Recs {
+  float4 *buf;   // {base bits, u, v, 1/|g'|}
+  int stride;    // blockDim.x
+  int n[2];
+};
+
+template <int L>
+__device__ __forceinline__ void rec_push(Recs &R, bool &ovf, int base, float u, float v, float ig) {
+  if (R.n[L] < RCAP) R.buf[(L * RCAP + R.n[L]) * R.stride] = make_float4(__int_as_float(base), u, v, ig);
+  else ovf = true;
+  R.n[L]++;
+}
+
+template <int STRIDE, bool LDG>
+__device__ __forceinline__ void load4(const float *Hl, int base, int ny, float &h00, float &h10,
+                                      float &h01, float &h11) {
+  const float *p = Hl + base * STRIDE;   // one address; the other corners are fixed offsets
+  const int oy = ny * STRIDE;
+  if (LDG) {
+    h00 = __ldg(p); h10 = __ldg(p + oy); h01 = __ldg(p + STRIDE); h11 = __ldg(p + oy + STRIDE);
   } else {
-    double du0, dv0, dal, dbe;
-    CellSol<double> sd = solve_cell_f64(h00, h10, h01, h11, g.Xs[i], g.Xs[i + 1], g.Ys[j],
-                                        g.Ys[j + 1], r, s, s1, du0, dv0, dal, dbe);
-    below = (float)sd.below;
-    ncr = sd.n;
-    for (int k = 0; k < 2; k++) {
-      if (k < ncr) {
-        uc[k] = (float)(du0 + dal * sd.tc[k]);
-        vc[k] = (float)(dv0 + dbe * sd.tc[k]);
-        igc[k] = (float)(1.0 / fabs(sd.gp[k]));
+    h00 = p[0]; h10 = p[oy]; h01 = p[STRIDE]; h11 = p[oy + STRIDE];
+  }
+}
+
+__device__ __forceinline__ void scatter4(float *Gl, int STRIDE, int base, int ny, float w, float u,
+                                         float v) {
+  atomicAdd(Gl + base * STRIDE, w * (1.f - u) * (1.f - v));
+  atomicAdd(Gl + (base + ny) * STRIDE, w * u * (1.f - v));
+  atomicAdd(Gl + (base + 1) * STRIDE, w * (1.f - u) * v);
+  atomicAdd(Gl + (base + ny + 1) * STRIDE, w * u * v);
+}
+
+// fp64 re-solve of one ill-conditioned cell (HP2 lever 1): same fp32 inputs,
+// exact cell spacing, oracle-style midpoint classification.  Rare; noinline so
+// its double-precision registers stay out of the hot loop.
+template <int L, int STRIDE, bool SCAT>
+__device__ __noinline__ void fix64(const Geo &g, const Ray &r, float *Gl, int base, int i, int j,
+                                   float s, float s1, float h00, float h10, float h01, float h11,
+                                   float &B, Recs &R, bool &ovf, float f) {
+  double u0, v0, al, be;
+  CellSol<double> sd = solve_cell_f64(h00, h10, h01, h11, g.Xs[i], g.Xs[i + 1], g.Ys[j],
+                                      g.Ys[j + 1], r, s, s1, u0, v0, al, be);
+  B += (float)sd.below;
+  for (int k = 0; k < sd.n; k++) {
+    float uc = (float)(u0 + al * sd.tc[k]), vc = (float)(v0 + be * sd.tc[k]);
+    float ig = (float)(1.0 / fabs(sd.gp[k]));
+    if (SCAT) scatter4(Gl, STRIDE, base, g.ny, f * ig, uc, vc);
+    else rec_push<L>(R, ovf, base, uc, vc, ig);
+  }
+}
+
+// One cell [s, s1] of surface L for one chain, fp32 (a3).  g(τ) = h(u0+ατ,
+// v0+βτ) - d_z(s+τ) = g0 + g1 τ + g2 τ² (R2).  With g(0) and g(Δs) of
+// different sign there is exactly one crossing; with equal signs there are
+// two iff the vertex lies inside and g(vertex) = -disc/(4 g2) has the other
+// sign.  Ill-conditioned cells (|g'| < GTHR at a crossing, or a near-tangent
+// vertex) set `redo`: the chain x ray is then re-traced in fp64.
+template <int L, int STRIDE, bool LDG, bool SCAT>
+__device__ __forceinline__ void cell32(const Geo &g, const Ray &r, const float *Hl, float *Gl,
+                                       int i, int j, float s, float s1, float zmin, float zmax,
+                                       float &B, Recs &R, bool &ovf, bool &redo, float f) {
+  const float za = s * r.dz, zb = s1 * r.dz, Ls = s1 - s;
+  if (zb <= zmin) { B += Ls; return; }          // below the surface's lowest node
+  if (za >= zmax) return;                       // above its highest node
+  const int base = i * g.ny + j;
+  float h00, h10, h01, h11;
+  load4<STRIDE, LDG>(Hl, base, g.ny, h00, h10, h01, h11);
+  if (zb <= fminf(fminf(h00, h10), fminf(h01, h11))) { B += Ls; return; }  // bilinear min at a corner
+  if (za >= fmaxf(fmaxf(h00, h10), fmaxf(h01, h11))) return;
+  const float idx = g.idx[i], idy = g.idy[j];
+  const float u0 = (fmaf(s, r.dx, r.ox) - g.Xs[i]) * idx;
+  const float v0 = (fmaf(s, r.dy, r.oy) - g.Ys[j]) * idy;
+  const float al = r.dx * idx, be = r.dy * idy;
+  const float b = h10 - h00, c = h01 - h00, e = (h11 - h10) - (h01 - h00);
+  const float g0 = (h00 - za) + u0 * (b + e * v0) + c * v0;
+  const float g1 = b * al + c * be + e * (u0 * be + v0 * al) - r.dz;
+  const float g2 = e * al * be;
+  const float gL = g0 + Ls * (g1 + Ls * g2);
+  const float disc = fmaf(g1, g1, -4.f * g2 * g0);
+  const bool p0 = g0 > 0.f;
+  const float a2 = 2.f * g2;
+  const bool vin = -g1 * a2 > 0.f && fabsf(g1) < Ls * fabsf(a2);   // vertex inside (0, Δs)
+  float q = 0.f;
+  if (disc > 0.f) q = -0.5f * (g1 + copysignf(disc * rsqrtf(disc), g1));
+  float ta = __fdividef(g0, q), tb = __fdividef(q, g2);             // the two roots (tb = ±inf if g2 = 0)
+  if (p0 != (gL > 0.f)) {                       // exactly one crossing
+    float t = (ta > 0.f && ta < Ls) ? ta : tb;
+    t = fminf(fmaxf(t, 0.f), Ls);
+    const float gp = g1 + a2 * t;
+    if (fabsf(gp) < GTHR || !(disc > 0.f)) { fix64<L, STRIDE, SCAT>(g, r, Gl, base, i, j, s, s1, h00, h10, h01, h11, B, R, ovf, f); return; }
+    B += p0 ? t : Ls - t;
+    const float ig = __frcp_rn(fabsf(gp)), uc = u0 + al * t, vc = v0 + be * t;
+    if (SCAT) scatter4(Gl, STRIDE, base, g.ny, f * ig, uc, vc);
+    else rec_push<L>(R, ovf, base, uc, vc, ig);
+  } else if (disc > 0.f && vin && ((g2 > 0.f) == p0)) {   // two crossings
+    float t1 = fminf(ta, tb), t2 = fmaxf(ta, tb);
+    const float gp1 = g1 + a2 * t1, gp2 = g1 + a2 * t2;
+    if (fabsf(gp1) < GTHR || fabsf(gp2) < GTHR) { fix64<L, STRIDE, SCAT>(g, r, Gl, base, i, j, s, s1, h00, h10, h01, h11, B, R, ovf, f); return; }
+    B += p0 ? Ls - (t2 - t1) : (t2 - t1);
+    const float ig1 = __frcp_rn(fabsf(gp1)), ig2 = __frcp_rn(fabsf(gp2));
+    if (SCAT) {
+      scatter4(Gl, STRIDE, base, g.ny, f * ig1, u0 + al * t1, v0 + be * t1);
+      scatter4(Gl, STRIDE, base, g.ny, f * ig2, u0 + al * t2, v0 + be * t2);
+    } else {
+      rec_push<L>(R, ovf, base, u0 + al * t1, v0 + be * t1, ig1);
+      rec_push<L>(R, ovf, base, u0 + al * t2, v0 + be * t2, ig2);
+    }
+  } else {                                      // no crossing
+    if (vin && fabsf(disc) < 2.f * fabsf(a2) * ZTHR) { fix64<L, STRIDE, SCAT>(g, r, Gl, base, i, j, s, s1, h00, h10, h01, h11, B, R, ovf, f); return; }  // near-tangent
+    if (p0) B += Ls;
+  }
+}
+
+// The same cell entirely in fp64 from the same fp32 inputs (HP2 lever 1), with
+// the oracle-style midpoint classification.
+template <int L, int STRIDE, bool LDG, bool SCAT>
+__device__ __forceinline__ void cell64(const Geo &g, const Ray &r, const float *Hl, float *Gl,
+                                       int i, int j, float s, float s1, float zmin, float zmax,
+                                       float &B, Recs &R, bool &ovf, float f) {
+  const float za = s * r.dz, zb = s1 * r.dz;
+  if (zb <= zmin) { B += s1 - s; return; }
+  if (za >= zmax) return;
+  const int base = i * g.ny + j;
+  float h00, h10, h01, h11;
+  load4<STRIDE, LDG>(Hl, base, g.ny, h00, h10, h01, h11);
+  if (zb <= fminf(fminf(h00, h10), fminf(h01, h11))) { B += s1 - s; return; }
+  if (za >= fmaxf(fmaxf(h00, h10), fmaxf(h01, h11))) return;
+  double u0, v0, al, be;
+  CellSol<double> sd = solve_cell_f64(h00, h10, h01, h11, g.Xs[i], g.Xs[i + 1], g.Ys[j],
+                                      g.Ys[j + 1], r, s, s1, u0, v0, al, be);
+  B += (float)sd.below;
+  for (int k = 0; k < sd.n; k++) {
+    float uc = (float)(u0 + al * sd.tc[k]), vc = (float)(v0 + be * sd.tc[k]);
+    float ig = (float)(1.0 / fabs(sd.gp[k]));
+    if (SCAT) scatter4(Gl, STRIDE, base, g.ny, f * ig, uc, vc);
+    else rec_push<L>(R, ovf, base, uc, vc, ig);
+  }
+}
+
+// First stored cell of the ray whose s_out exceeds s (binary search; the last
+// cell's s_out is s_exit > s).
+__device__ __forceinline__ int band_entry(const int2 *__restrict__ cells, int lo, int hi, float s) {
+  hi -= 1;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (__int_as_float(__ldg(&cells[mid].y)) > s) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+
+// Same, warp-cooperative (chain lanes, all 32 lanes converged, uniform
+// arguments): one coalesced load of 32 cells and a ballot per round.
+__device__ __forceinline__ int band_entry_warp(const int2 *__restrict__ cells, int lo, int hi, float s) {
+  const int lane = threadIdx.x & 31;
+  for (int b = lo; b < hi; b += 32) {
+    const int k = b + lane;
+    const bool gt = k < hi && __int_as_float(__ldg(&cells[k].y)) > s;
+    const unsigned m = __ballot_sync(0xffffffffu, gt);
+    if (m) return b + __ffs(m) - 1;
+  }
+  return hi - 1;
+}
+
+// Walk the stored cells from index k (containing s0) until s_hi, both surfaces.
+// F64: every straddling cell in fp64 (re-trace of an ill-conditioned chain x ray).
+template <int STRIDE, bool LDG, bool SCAT, bool F64>
+__device__ __forceinline__ void walk(const Geo &g, const Ray &r, const int2 *__restrict__ cells,
+                                     int k, int kend, float s0, float s_hi, const float *Hk,
+                                     float *Gk, float4 bd, float &B0, float &B1, Recs &R,
+                                     bool &ovf, bool &redo, float f0, float f1) {
+  float s = s0;
+  const int sN = g.N * STRIDE;
+  for (; k < kend; k++) {
+    // chain lanes, recording walk: the loop is warp-uniform; reconverge the
+    // lanes that left a cell early so every cell is one warp instruction
+    // stream.  (The SCAT re-walk runs on a divergent subset: no full-warp sync.)
+    if (STRIDE == 32 && !SCAT) __syncwarp();
+    const int2 e = __ldg(cells + k);
+    const float s1 = __int_as_float(e.y);
+    const int i = e.x & 0xffff, j = e.x >> 16;
+    if (s1 > s) {
+      if (F64) {
+        cell64<0, STRIDE, LDG, SCAT>(g, r, Hk, Gk, i, j, s, s1, bd.x, bd.y, B0, R, ovf, f0);
+        cell64<1, STRIDE, LDG, SCAT>(g, r, Hk + sN, Gk + sN, i, j, s, s1, bd.z, bd.w, B1, R, ovf, f1);
+      } else {
+        cell32<0, STRIDE, LDG, SCAT>(g, r, Hk, Gk, i, j, s, s1, bd.x, bd.y, B0, R, ovf, redo, f0);
+        cell32<1, STRIDE, LDG, SCAT>(g, r, Hk + sN, Gk + sN, i, j, s, s1, bd.z, bd.w, B1, R, ovf,
+                                     redo, f1);
       }
     }
+    if (s1 >= s_hi) break;
+    s = s1;
   }
-  B += below;
-  for (int k = 0; k < 2; k++) {
-    if (k < ncr) {
-      if (SCAT) {
-        float w = f * igc[k], u = uc[k], v = vc[k];
-        atomicAdd(Gl + base, w * (1.f - u) * (1.f - v));
-        atomicAdd(Gl + base + g.ny, w * u * (1.f - v));
-        atomicAdd(Gl + base + 1, w * (1.f - u) * v);
-        atomicAdd(Gl + base + g.ny + 1, w * u * v);
-      } else {
-        Rec rc;
-        rc.cell = (l << 16) | base;
-        rc.u = uc[k]; rc.v = vc[k]; rc.ig = igc[k];
+}
+
+// Scatter recorded crossings: G_l[node] += f_l · φ_node(u, v)/|g'|  (a6).
+template <int STRIDE>
+__device__ __forceinline__ void scatter(const Recs &R, float *Gk, int N, int ny, float f0, float f1) {
 #pragma unroll
-        for (int m = 0; m < MAXREC; m++)
-          if (m == nrec) rec[m] = rc;
-        if (nrec < MAXREC) nrec++;
-        else ovf = true;
-      }
+  for (int l = 0; l < 2; l++) {
+    for (int m = 0; m < R.n[l]; m++) {
+      const float4 q = R.buf[(l * RCAP + m) * R.stride];
+      scatter4(Gk + l * N * STRIDE, STRIDE, __float_as_int(q.x), ny, (l ? f1 : f0) * q.w, q.y, q.z);
     }
   }
 }
 
-// Walk the cells of the band [s0, s_hi] for one chain from DDA state (i0, j0).
-template <bool SCAT>
-__device__ __forceinline__ void walk(const Geo &g, const Ray &r, int i0, int j0, float s0,
-                                     float s_hi, const float *Hk, float *Gk, float4 bd, float &B0,
-                                     float &B1, Rec *rec, int &nrec, bool &ovf, float f0,
-                                     float f1) {
-  int i = i0, j = j0;
-  float s = s0;
-  for (int guard = 0; guard < 4 * (MT_MAX_AXIS + 2); guard++) {
-    float s_ev;
-    int ev = dda_next(r, i, j, g.Xs, g.Ys, g.nx, g.ny, g.z_top, s_ev);
-    float s1 = fminf(s_ev, r.s_exit);
-    if (s1 > s) {
-      do_cell<SCAT>(g, r, Hk, Gk, 0, i, j, s, s1, bd.x, bd.y, B0, rec, nrec, ovf, f0);
-      do_cell<SCAT>(g, r, Hk + g.N, Gk + g.N, 1, i, j, s, s1, bd.z, bd.w, B1, rec, nrec, ovf, f1);
-    }
-    if ((ev & 4) || s1 >= s_hi) break;
-    if (ev & 1) i += r.sx;
-    if (ev & 2) j += r.sy;
-    s = s1;
+// Trace one chain x ray from the band entry: fp32 with deferred fp64 re-trace
+// (redo) and the overflow re-walk, returning B0, B1 and the crossing records.
+template <int STRIDE, bool LDG>
+__device__ __forceinline__ void trace_pair(const Geo &g, const Ray &r, const int2 *__restrict__ cells,
+                                           int k0, int kend, float s_lo, float s_hi,
+                                           const float *Hk, float *Gk, float4 bd, float &B0,
+                                           float &B1, Recs &R, bool &ovf) {
+  bool redo = false;   // unused: ill-conditioned cells are re-solved in place (fix64)
+  R.n[0] = R.n[1] = 0;
+  walk<STRIDE, LDG, false, false>(g, r, cells, k0, kend, s_lo, s_hi, Hk, Gk, bd, B0, B1, R, ovf,
+                                  redo, 0.f, 0.f);
+}
+
+// Overflow (more than RCAP crossings of one surface): scatter every crossing of
+// the chain x ray directly, through the same fp32 cell code (and its fp64
+// fixes) as the recording walk, so the crossings are identical.
+template <int STRIDE, bool LDG>
+__device__ __noinline__ void rewalk_scatter(const Geo &g, const Ray &r, const int2 *__restrict__ cells,
+                                            int k0, int kend, float s_lo, float s_hi,
+                                            const float *Hk, float *Gk, float4 bd, float f0,
+                                            float f1) {
+  float d0 = s_lo, d1 = s_lo;
+  Recs R;
+  R.buf = nullptr;
+  R.stride = 0;
+  R.n[0] = R.n[1] = 0;
+  bool ovf = false, redo = false;
+  walk<STRIDE, LDG, true, false>(g, r, cells, k0, kend, s_lo, s_hi, Hk, Gk, bd, d0, d1, R, ovf,
+                                 redo, f0, f1);
+}
+
+// Fused epilogue (a4-a5): t = ln(λ/C) (C > 0) or ln λ (C = 0) from the
+// per-ray constant t_base (HP4, R15); returns ℓ_p, sets ∂ℓ/∂O = (λ - C)/Λ.
+__device__ __forceinline__ float epilogue(const Ray &r, const TraceConsts &tc, float B0, float B1,
+                                          float &dldO) {
+  float t = r.tb - (tc.k0 * B0 + tc.k1 * B1) * tc.inv_att;
+  if (r.cnt > 0.f) {
+    // ℓ = -C (e^t - 1 - t); e^t - 1 - t by its series when |t| < 0.1 (truncation
+    // < 2e-10 relative), expm1f otherwise
+    float d;
+    if (fabsf(t) < 0.1f)
+      d = t * t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.f / 720.f, 1.f / 120.f), 1.f / 24.f), 1.f / 6.f), 0.5f);
+    else
+      d = expm1f(t) - t;
+    dldO = r.cnt * (d + t) * tc.inv_att;
+    return -r.cnt * d;
+  }
+  float lam = __expf(t);
+  dldO = lam * tc.inv_att;
+  return -lam;
+}
+
+__device__ __forceinline__ void load_geometry(const TraceArgs &a, float *Xs, float *Ys, float *idx,
+                                              float *idy) {
+  const int nx = a.tc.nx, ny = a.tc.ny;
+  for (int k = threadIdx.x; k < nx; k += blockDim.x) {
+    Xs[k] = a.X[k];
+    idx[k] = k < nx - 1 ? 1.f / (a.X[k + 1] - a.X[k]) : 0.f;
+  }
+  for (int k = threadIdx.x; k < ny; k += blockDim.x) {
+    Ys[k] = a.Y[k];
+    idy[k] = k < ny - 1 ? 1.f / (a.Y[k + 1] - a.Y[k]) : 0.f;
   }
 }
 
 }  // namespace
 
-template <int K, int MODE>
-__global__ void __launch_bounds__(MT_THREADS) k_trace(TraceArgs a) {
+// ---------------------------------------------------------------------------
+// traversal builder (create time): thread = ray; count pass then write pass
+// ---------------------------------------------------------------------------
+__global__ void k_build_trav(TraceArgs a, const int32_t *off, int32_t *count, int2 *cells) {
+  __shared__ float Xs[MT_MAX_AXIS], Ys[MT_MAX_AXIS];
+  const int nx = a.tc.nx, ny = a.tc.ny;
+  for (int k = threadIdx.x; k < nx; k += blockDim.x) Xs[k] = a.X[k];
+  for (int k = threadIdx.x; k < ny; k += blockDim.x) Ys[k] = a.Y[k];
+  __syncthreads();
+  int64_t rr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (rr >= a.R) return;
+  DdaRay q = dda_ray(load_ray(a.ray_a, a.ray_b, rr));
+  int i = start_axis(Xs, nx, q.r.ox, q.r.dx), j = start_axis(Ys, ny, q.r.oy, q.r.dy);
+  float s = 0.f;
+  int n = 0;
+  for (int guard = 0; guard < 4 * (MT_MAX_AXIS + 2); guard++) {
+    float s_ev;
+    int ev = dda_next(q, i, j, Xs, Ys, nx, ny, a.tc.z_top, s_ev);
+    float s1 = fminf(s_ev, q.r.s_exit);
+    if (cells) cells[off[rr] + n] = make_int2(i | (j << 16), __float_as_int(fmaxf(s1, s)));
+    n++;
+    if (ev & 4) break;
+    if (ev & 1) i += q.sx;
+    if (ev & 2) j += q.sy;
+    s = s1;
+  }
+  if (count) count[rr] = n;
+}
+
+// ---------------------------------------------------------------------------
+// K2, chain lanes
+// ---------------------------------------------------------------------------
+template <int MODE, bool SMEMH>
+__global__ void __launch_bounds__(MT_THREADS, 3) k_trace_cl(TraceArgs a) {
   extern __shared__ __align__(16) float smem[];
   const int nx = a.tc.nx, ny = a.tc.ny, N = a.tc.N;
   float *Xs = smem, *Ys = Xs + nx, *idx = Ys + ny, *idy = idx + nx;
-  int geo_words = (2 * nx + 2 * ny + 3) & ~3;
+  const int geo_words = (2 * nx + 2 * ny + 3) & ~3;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int grp = blockIdx.y, c = grp * 32 + lane;
+  const bool act = c < a.C;
+  load_geometry(a, Xs, Ys, idx, idy);
+  const float *Hg = a.H + (size_t)grp * 2 * N * 32;
+  if (SMEMH) {
+    float4 *d4 = reinterpret_cast<float4 *>(smem + geo_words);
+    const float4 *s4 = reinterpret_cast<const float4 *>(Hg);
+    for (int k = threadIdx.x; k < 2 * N * 8; k += blockDim.x) d4[k] = __ldg(s4 + k);
+    Hg = smem + geo_words;
+  }
+  float4 *recbuf = reinterpret_cast<float4 *>(smem + geo_words + (SMEMH ? 2 * N * 32 : 0));
+  __syncthreads();
+  // this lane's chain band; the warp walks the union band of its 32 chains
+  float4 bd = act ? a.band[c] : make_float4(3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f);
+  float zlo = bd.x, zhi = bd.w;
+  for (int o = 16; o > 0; o >>= 1) {
+    zlo = fminf(zlo, __shfl_xor_sync(0xffffffffu, zlo, o));
+    zhi = fmaxf(zhi, __shfl_xor_sync(0xffffffffu, zhi, o));
+  }
+  if (!act) bd = make_float4(-3.0e38f, -3.0e38f, -3.0e38f, -3.0e38f);  // "above": no loads
+  Geo g;
+  g.Xs = Xs; g.Ys = Ys; g.idx = idx; g.idy = idy; g.nx = nx; g.ny = ny; g.N = N;
+  const float *Hk = Hg + lane;
+  float *Gk = a.G + (size_t)grp * 2 * N * 32 + lane;
+  float llacc = 0.f;
+
+  const int64_t r_begin = (int64_t)blockIdx.x * a.rays_per_block;
+  const int64_t r_end = min(a.R, r_begin + a.rays_per_block);
+  for (int64_t rr = r_begin + warp; rr < r_end; rr += nwarp) {
+    __syncwarp();
+    const Ray r = load_ray(a.ray_a, a.ray_b, rr);      // same address in every lane: broadcast
+    // band bounds, widened by 1e-6 so fast division can only walk more cells
+    const float s_lo = fminf(__fdividef(zlo, r.dz) * (1.f - 1e-6f), r.s_exit);
+    const float s_hi = fminf(__fdividef(zhi, r.dz) * (1.f + 1e-6f), r.s_exit);
+    float B0 = s_lo, B1 = s_lo;                        // below both surfaces before s_lo
+    Recs R;
+    R.buf = recbuf + threadIdx.x;
+    R.stride = blockDim.x;
+    R.n[0] = R.n[1] = 0;
+    bool ovf = false;
+    int k0 = 0;
+    const int kend = __ldg(a.trav_off + rr + 1);
+    if (s_lo < r.s_exit) {                             // warp-uniform
+      k0 = band_entry_warp(a.trav, __ldg(a.trav_off + rr), kend, s_lo);
+      trace_pair<32, !SMEMH>(g, r, a.trav, k0, kend, s_lo, s_hi, Hk, Gk, bd, B0, B1, R, ovf);
+    }
+    if (MODE == TRACE_LL) {
+      float dldO;
+      const float ll = epilogue(r, a.tc, B0, B1, dldO);
+      if (act) {
+        llacc += ll;
+        const float f0 = dldO * a.tc.k0, f1 = dldO * a.tc.k1;
+        if (!ovf) scatter<32>(R, Gk, N, ny, f0, f1);
+        else rewalk_scatter<32, !SMEMH>(g, r, a.trav, k0, kend, s_lo, s_hi, Hk, Gk, bd, f0, f1);
+      }
+    } else if (act) {
+      const int64_t o = (int64_t)c * a.R + rr;
+      a.Lout[3 * o + 0] = B0;
+      a.Lout[3 * o + 1] = B1 - B0;
+      a.Lout[3 * o + 2] = r.s_exit - B1;
+      a.Oout[o] = a.tc.k0 * B0 + a.tc.k1 * B1 + a.obase[rr];
+    }
+  }
+  if (MODE == TRACE_LL && act) atomicAdd(a.ll + c, (double)llacc);
+}
+
+// ---------------------------------------------------------------------------
+// K2, ray lanes (small C)
+// ---------------------------------------------------------------------------
+template <int K, int MODE>
+__global__ void __launch_bounds__(MT_THREADS) k_trace_rl(TraceArgs a) {
+  extern __shared__ __align__(16) float smem[];
+  const int nx = a.tc.nx, ny = a.tc.ny, N = a.tc.N;
+  float *Xs = smem, *Ys = Xs + nx, *idx = Ys + ny, *idy = idx + nx;
+  const int geo_words = (2 * nx + 2 * ny + 3) & ~3;
   float *Hs = smem + geo_words;                       // [K][2N]
   float *Gs = Hs + K * 2 * N;                         // [K][2N] (TRACE_LL)
+  float4 *recbuf = reinterpret_cast<float4 *>(
+      smem + geo_words + ((K * 2 * N * (MODE == TRACE_LL ? 2 : 1) + 3) & ~3));
   __shared__ double red[MT_THREADS / 32][K];
-
+  __shared__ float4 bds[K];
+  __shared__ float llacc[K][MT_THREADS];
   const int tid = threadIdx.x;
   const int c0 = blockIdx.y * K;
   const int nk = min(K, a.C - c0);
-  for (int k = tid; k < nx; k += blockDim.x) {
-    Xs[k] = a.X[k];
-    idx[k] = k < nx - 1 ? 1.f / (a.X[k + 1] - a.X[k]) : 0.f;
+  load_geometry(a, Xs, Ys, idx, idy);
+  for (int k = tid; k < nk * 2 * N; k += blockDim.x) {
+    int kc = k / (2 * N), m = k - kc * 2 * N;
+    Hs[k] = __ldg(a.H + tix(c0 + kc, m / N, m % N, N));
   }
-  for (int k = tid; k < ny; k += blockDim.x) {
-    Ys[k] = a.Y[k];
-    idy[k] = k < ny - 1 ? 1.f / (a.Y[k + 1] - a.Y[k]) : 0.f;
-  }
-  {
-    const float *src = a.H + (size_t)c0 * 2 * N;
-    const int nh = nk * 2 * N;
-    if ((N & 1) == 0) {  // 2N % 4 == 0: float4 path (rows stay 16-B aligned)
-      const float4 *s4 = reinterpret_cast<const float4 *>(src);
-      float4 *d4 = reinterpret_cast<float4 *>(Hs);
-      for (int k = tid; k < nh / 4; k += blockDim.x) d4[k] = __ldg(s4 + k);
-    } else {
-      for (int k = tid; k < nh; k += blockDim.x) Hs[k] = __ldg(src + k);
-    }
-    if (MODE == TRACE_LL)
-      for (int k = tid; k < K * 2 * N; k += blockDim.x) Gs[k] = 0.f;
-  }
-  __shared__ float4 bds[K];
-  __shared__ float llacc[K][MT_THREADS];
+  if (MODE == TRACE_LL)
+    for (int k = tid; k < K * 2 * N; k += blockDim.x) Gs[k] = 0.f;
   if (tid < K) bds[tid] = tid < nk ? a.band[c0 + tid] : make_float4(0.f, 0.f, 0.f, 0.f);
   for (int k = 0; k < K; k++) llacc[k][tid] = 0.f;
   __syncthreads();
   float zlo = 3.0e38f;
   for (int k = 0; k < nk; k++) zlo = fminf(zlo, bds[k].x);
-
   Geo g;
   g.Xs = Xs; g.Ys = Ys; g.idx = idx; g.idy = idy; g.nx = nx; g.ny = ny; g.N = N;
-  g.z_top = a.tc.z_top;
-  const float x0 = Xs[0], y0 = Ys[0];
-  const float inv_mx = (float)(nx - 1) / (Xs[nx - 1] - Xs[0]);
-  const float inv_my = (float)(ny - 1) / (Ys[ny - 1] - Ys[0]);
 
   const int64_t r_begin = (int64_t)blockIdx.x * a.rays_per_block;
   const int64_t r_end = min(a.R, r_begin + a.rays_per_block);
   for (int64_t rr = r_begin + tid; rr < r_end; rr += blockDim.x) {
-    Ray r = load_ray(a.ray_a, a.ray_b, rr);
-    // union band of the block's chains: the ray is below every surface before s_lo
-    float s_lo = fminf(zlo / r.dz, r.s_exit);
-    bool walkable = s_lo < r.s_exit;
-    int i0 = 0, j0 = 0;
-    if (walkable) {
-      i0 = locate_axis(Xs, nx, r.ox, r.dx, s_lo, x0, inv_mx);
-      j0 = locate_axis(Ys, ny, r.oy, r.dy, s_lo, y0, inv_my);
-    }
+    const Ray r = load_ray(a.ray_a, a.ray_b, rr);
+    const float s_lo = fminf(zlo / r.dz, r.s_exit);
+    const bool walkable = s_lo < r.s_exit;
+    const int kend = __ldg(a.trav_off + rr + 1);
+    const int k0 = walkable ? band_entry(a.trav, __ldg(a.trav_off + rr), kend, s_lo) : 0;
 #pragma unroll 1
     for (int k = 0; k < nk; k++) {
       const float *Hk = Hs + k * 2 * N;
       float *Gk = Gs + k * 2 * N;
       const float4 bd = bds[k];
       float B0 = s_lo, B1 = s_lo;
-      Rec rec[MAXREC];
-      int nrec = 0;
+      Recs R;
+      R.buf = recbuf + tid;
+      R.stride = blockDim.x;
+      R.n[0] = R.n[1] = 0;
       bool ovf = false;
-      float s_hi = fminf(bd.w / r.dz, r.s_exit);
-      if (walkable)
-        walk<false>(g, r, i0, j0, s_lo, s_hi, Hk, Gk, bd, B0, B1, rec, nrec, ovf, 0.f, 0.f);
+      const float s_hi = fminf(bd.w / r.dz, r.s_exit);
+      if (walkable) trace_pair<1, false>(g, r, a.trav, k0, kend, s_lo, s_hi, Hk, Gk, bd, B0, B1, R, ovf);
       if (MODE == TRACE_LL) {
-        // fused epilogue: t = ln(λ/C) (C > 0) or ln λ (C = 0)  (HP4, R15)
-        float t = r.tb - (a.tc.k0 * B0 + a.tc.k1 * B1) * a.tc.inv_att;
-        float ll, dldO;
-        if (r.cnt > 0.f) {
-          float em1 = expm1f(t);
-          ll = -r.cnt * (em1 - t);
-          dldO = r.cnt * em1 * a.tc.inv_att;      // (λ - C)/Λ
-        } else {
-          float lam = expf(t);
-          ll = -lam;
-          dldO = lam * a.tc.inv_att;
-        }
-        llacc[k][tid] += ll;
-        float f0 = dldO * a.tc.k0, f1 = dldO * a.tc.k1;
-        if (!ovf) {
-#pragma unroll
-          for (int m = 0; m < MAXREC; m++) {
-            if (m < nrec) {
-              Rec rc = rec[m];
-              int l = rc.cell >> 16, base = rc.cell & 0xffff;
-              float w = (l ? f1 : f0) * rc.ig, u = rc.u, v = rc.v;
-              float *Gl = Gk + l * N;
-              atomicAdd(Gl + base, w * (1.f - u) * (1.f - v));
-              atomicAdd(Gl + base + ny, w * u * (1.f - v));
-              atomicAdd(Gl + base + 1, w * (1.f - u) * v);
-              atomicAdd(Gl + base + ny + 1, w * u * v);
-            }
-          }
-        } else {  // rare: more crossings than registers hold -> scattering re-walk
-          float d0 = 0.f, d1 = 0.f;
-          int dn = 0;
-          bool dov = false;
-          walk<true>(g, r, i0, j0, s_lo, s_hi, Hk, Gk, bd, d0, d1, rec, dn, dov, f0, f1);
-        }
+        float dldO;
+        llacc[k][tid] += epilogue(r, a.tc, B0, B1, dldO);
+        const float f0 = dldO * a.tc.k0, f1 = dldO * a.tc.k1;
+        if (!ovf) scatter<1>(R, Gk, N, ny, f0, f1);
+        else rewalk_scatter<1, false>(g, r, a.trav, k0, kend, s_lo, s_hi, Hk, Gk, bd, f0, f1);
       } else {
-        int64_t o = (int64_t)(c0 + k) * a.R + rr;
+        const int64_t o = (int64_t)(c0 + k) * a.R + rr;
         a.Lout[3 * o + 0] = B0;
         a.Lout[3 * o + 1] = B1 - B0;
         a.Lout[3 * o + 2] = r.s_exit - B1;
@@ -422,7 +646,6 @@ __global__ void __launch_bounds__(MT_THREADS) k_trace(TraceArgs a) {
       }
     }
   }
-
   if (MODE == TRACE_LL) {
     const int lane = tid & 31, wid = tid >> 5;
     for (int k = 0; k < nk; k++) {
@@ -438,63 +661,90 @@ __global__ void __launch_bounds__(MT_THREADS) k_trace(TraceArgs a) {
     }
     for (int k = tid; k < nk * 2 * N; k += blockDim.x) {
       float v = Gs[k];
-      if (v != 0.f) atomicAdd(a.G + (size_t)c0 * 2 * N + k, v);
+      int kc = k / (2 * N), m = k - kc * 2 * N;
+      if (v != 0.f) atomicAdd(a.G + tix(c0 + kc, m / N, m % N, N), v);
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// debug traversal: the exact DDA from s = 0 with the same device functions
-// ---------------------------------------------------------------------------
-__global__ void k_debug_traversal(TraceArgs a, int64_t ray, int32_t *ij, float *si, float *so,
-                                  int cap, int32_t *n_out) {
-  __shared__ float Xs[MT_MAX_AXIS], Ys[MT_MAX_AXIS];
-  const int nx = a.tc.nx, ny = a.tc.ny;
-  for (int k = threadIdx.x; k < nx; k += blockDim.x) Xs[k] = a.X[k];
-  for (int k = threadIdx.x; k < ny; k += blockDim.x) Ys[k] = a.Y[k];
-  __syncthreads();
-  if (threadIdx.x) return;
-  Ray r = load_ray(a.ray_a, a.ray_b, ray);
-  const float inv_mx = (float)(nx - 1) / (Xs[nx - 1] - Xs[0]);
-  const float inv_my = (float)(ny - 1) / (Ys[ny - 1] - Ys[0]);
-  int i = locate_axis(Xs, nx, r.ox, r.dx, 0.f, Xs[0], inv_mx);
-  int j = locate_axis(Ys, ny, r.oy, r.dy, 0.f, Ys[0], inv_my);
-  float s = 0.f;
-  int n = 0;
-  for (int guard = 0; guard < 4 * (MT_MAX_AXIS + 2); guard++) {
-    float s_ev;
-    int ev = dda_next(r, i, j, Xs, Ys, nx, ny, a.tc.z_top, s_ev);
-    float s1 = fminf(s_ev, r.s_exit);
-    if (n < cap) { ij[2 * n] = i; ij[2 * n + 1] = j; si[n] = s; so[n] = s1; }
-    n++;
-    if (ev & 4) break;
-    if (ev & 1) i += r.sx;
-    if (ev & 2) j += r.sy;
-    s = s1;
-  }
-  *n_out = n;
-}
-
-// ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
-template <int K, int MODE>
-static cudaError_t launch_k(const TraceArgs &a, dim3 grid, size_t smem, cudaStream_t s) {
-  static size_t smem_set[16] = {0};
+static TraceArgs base_trace_args(mt_problem *p) {
+  TraceArgs a{};
+  a.tc = p->tc;
+  a.X = p->d_X; a.Y = p->d_Y;
+  a.ray_a = p->d_ray_a; a.ray_b = p->d_ray_b; a.obase = p->d_obase;
+  a.trav_off = p->d_trav_off; a.trav = p->d_trav;
+  a.R = p->R;
+  return a;
+}
+
+cudaError_t build_traversal(mt_problem *p) {
+  if (p->R <= 0) return cudaSuccess;
+  TraceArgs a = base_trace_args(p);
+  int32_t *d_cnt = nullptr;
+  cudaError_t e = cudaMalloc(&d_cnt, sizeof(int32_t) * p->R);
+  if (e != cudaSuccess) return e;
+  unsigned nb = (unsigned)((p->R + 127) / 128);
+  k_build_trav<<<nb, 128>>>(a, nullptr, d_cnt, nullptr);
+  std::vector<int32_t> cnt(p->R);
+  e = cudaMemcpy(cnt.data(), d_cnt, sizeof(int32_t) * p->R, cudaMemcpyDeviceToHost);
+  cudaFree(d_cnt);
+  if (e != cudaSuccess) return e;
+  std::vector<int32_t> off(p->R + 1, 0);
+  int64_t tot = 0;
+  for (int64_t q = 0; q < p->R; q++) {
+    tot += cnt[q];
+    if (tot >= (int64_t)1 << 31) return cudaErrorInvalidValue;   // > 2^31 stored cells
+    off[q + 1] = (int32_t)tot;
+  }
+  p->trav_cells = tot;
+  e = cudaMalloc(&p->d_trav_off, sizeof(int32_t) * (p->R + 1));
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_trav, sizeof(int2) * (p->trav_cells > 0 ? p->trav_cells : 1));
+  if (e == cudaSuccess)
+    e = cudaMemcpy(p->d_trav_off, off.data(), sizeof(int32_t) * (p->R + 1), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return e;
+  a.trav_off = p->d_trav_off;
+  a.trav = p->d_trav;
+  k_build_trav<<<nb, 128>>>(a, p->d_trav_off, nullptr, p->d_trav);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  return e;
+}
+
+template <typename Kern>
+static cudaError_t set_smem(Kern k, size_t smem, size_t *done) {
   int dev = 0;
   cudaGetDevice(&dev);
-  if (smem > 48 * 1024 && smem_set[dev & 15] < smem) {
-    cudaError_t e = cudaFuncSetAttribute(k_trace<K, MODE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (smem > 48 * 1024 && done[dev & 15] < smem) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    smem_set[dev & 15] = smem;
+    done[dev & 15] = smem;
   }
-  k_trace<K, MODE><<<grid, MT_THREADS, smem, s>>>(a);
+  return cudaSuccess;
+}
+
+template <int MODE, bool SMEMH>
+static cudaError_t launch_cl(const TraceArgs &a, dim3 grid, size_t smem, cudaStream_t s) {
+  static size_t done[16] = {0};
+  cudaError_t e = set_smem(k_trace_cl<MODE, SMEMH>, smem, done);
+  if (e != cudaSuccess) return e;
+  k_trace_cl<MODE, SMEMH><<<grid, MT_THREADS, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int K, int MODE>
+static cudaError_t launch_rl(const TraceArgs &a, dim3 grid, size_t smem, cudaStream_t s) {
+  static size_t done[16] = {0};
+  cudaError_t e = set_smem(k_trace_rl<K, MODE>, smem, done);
+  if (e != cudaSuccess) return e;
+  k_trace_rl<K, MODE><<<grid, MT_THREADS, smem, s>>>(a);
   return cudaGetLastError();
 }
 
 static int pick_k(const mt_problem *p, int C) {
-  if (p->trace_k > 0) return p->trace_k;
+  if (p->trace_k > 0 && p->trace_k <= 8) return p->trace_k;
   size_t per_chain = (size_t)16 * p->N;   // H + G tiles, fp32
   int k = 8;
   while (k > 1 && (size_t)k * per_chain > 40 * 1024) k >>= 1;
@@ -502,62 +752,64 @@ static int pick_k(const mt_problem *p, int C) {
   return k;
 }
 
+static int64_t pick_splits(const mt_problem *p, int64_t groups, int64_t blocks_per_sm) {
+  if (p->trace_s > 0) return p->trace_s;
+  int64_t target = (int64_t)p->num_sms * blocks_per_sm * 4;   // ~4 waves of resident blocks
+  int64_t S = (target + groups - 1) / groups;
+  int64_t max_s = (p->R + 63) / 64;
+  return S < 1 ? 1 : (S > max_s ? max_s : S);
+}
+
 cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const float4 *band,
                          float *G, double *ll, float *L, float *O, cudaStream_t s) {
   if (C <= 0 || p->R <= 0) return cudaSuccess;
-  TraceArgs a;
-  a.tc = p->tc;
-  a.X = p->d_X; a.Y = p->d_Y;
-  a.ray_a = p->d_ray_a; a.ray_b = p->d_ray_b; a.obase = p->d_obase;
-  a.R = p->R;
+  TraceArgs a = base_trace_args(p);
   a.C = C;
   a.H = H; a.band = band; a.G = G; a.ll = ll; a.Lout = L; a.Oout = O;
-  int K = pick_k(p, C);
-  int groups = (C + K - 1) / K;
-  int64_t S;
-  if (p->trace_s > 0) S = p->trace_s;
-  else {
-    int64_t target = (int64_t)p->num_sms * 8;  // ~8 resident-block slots per SM
-    S = (target + groups - 1) / groups;
-    int64_t max_s = (p->R + MT_THREADS - 1) / MT_THREADS;
-    if (S > max_s) S = max_s;
-    if (S < 1) S = 1;
-  }
-  a.rays_per_block = (p->R + S - 1) / S;
-  S = (p->R + a.rays_per_block - 1) / a.rays_per_block;
-  dim3 grid((unsigned)S, (unsigned)groups);
-  int geo_words = (2 * p->nx + 2 * p->ny + 3) & ~3;
-  size_t smem = (size_t)4 * (geo_words + (size_t)K * 2 * p->N * (mode == TRACE_LL ? 2 : 1));
+  const int geo_words = (2 * p->nx + 2 * p->ny + 3) & ~3;
+  const bool chain_lanes = p->trace_k == 0 ? C >= 16 : p->trace_k == 32;
   cudaError_t e = cudaSuccess;
   bool rec = p->timing && p->n_rec < (int)p->ev_a.size();
   if (rec) cudaEventRecord(p->ev_a[p->n_rec], s);
+  if (chain_lanes) {
+    int groups = (C + 31) / 32;
+    size_t tile = (size_t)4 * 2 * p->N * 32;
+    bool smemh = tile <= (size_t)p->smemh_limit;
+    int64_t S = pick_splits(p, groups, 2);
+    a.rays_per_block = (p->R + S - 1) / S;
+    S = (p->R + a.rays_per_block - 1) / a.rays_per_block;
+    dim3 grid((unsigned)S, (unsigned)groups);
+    size_t smem = (size_t)4 * geo_words + (smemh ? tile : 0) + (size_t)16 * 2 * RCAP * MT_THREADS;
+    if (mode == TRACE_LL) e = smemh ? launch_cl<TRACE_LL, true>(a, grid, smem, s)
+                                    : launch_cl<TRACE_LL, false>(a, grid, smem, s);
+    else e = smemh ? launch_cl<TRACE_PATH, true>(a, grid, smem, s)
+                   : launch_cl<TRACE_PATH, false>(a, grid, smem, s);
+  } else {
+    int K = pick_k(p, C);
+    int groups = (C + K - 1) / K;
+    int64_t S = pick_splits(p, groups, 2);
+    a.rays_per_block = (p->R + S - 1) / S;
+    S = (p->R + a.rays_per_block - 1) / a.rays_per_block;
+    dim3 grid((unsigned)S, (unsigned)groups);
+    size_t smem = (size_t)4 * (geo_words + (((size_t)K * 2 * p->N * (mode == TRACE_LL ? 2 : 1) + 3) & ~(size_t)3)) +
+                  (size_t)16 * 2 * RCAP * MT_THREADS;
 #define MT_DISPATCH(KK)                                                         \
   case KK:                                                                      \
-    e = mode == TRACE_LL ? launch_k<KK, TRACE_LL>(a, grid, smem, s)          \
-                         : launch_k<KK, TRACE_PATH>(a, grid, smem, s);       \
+    e = mode == TRACE_LL ? launch_rl<KK, TRACE_LL>(a, grid, smem, s)            \
+                         : launch_rl<KK, TRACE_PATH>(a, grid, smem, s);         \
     break;
-  switch (K) {
-    MT_DISPATCH(1)
-    MT_DISPATCH(2)
-    MT_DISPATCH(4)
-    MT_DISPATCH(8)
-    default: return cudaErrorInvalidValue;
-  }
+    switch (K) {
+      MT_DISPATCH(1)
+      MT_DISPATCH(2)
+      MT_DISPATCH(4)
+      MT_DISPATCH(8)
+      default: e = cudaErrorInvalidValue;
+    }
 #undef MT_DISPATCH
+  }
   if (rec) { cudaEventRecord(p->ev_b[p->n_rec], s); p->n_rec++; }
   p->all_launches++;
   p->trace_launches++;
   p->pairs += (double)C * (double)p->R;
   return e;
-}
-
-cudaError_t launch_debug_traversal(mt_problem *p, int64_t ray, int32_t *d_ij, float *d_si,
-                                   float *d_so, int cap, int32_t *d_n) {
-  TraceArgs a;
-  a.tc = p->tc;
-  a.X = p->d_X; a.Y = p->d_Y;
-  a.ray_a = p->d_ray_a; a.ray_b = p->d_ray_b;
-  k_debug_traversal<<<1, 128>>>(a, ray, d_ij, d_si, d_so, cap, d_n);
-  p->all_launches++;
-  return cudaGetLastError();
 }

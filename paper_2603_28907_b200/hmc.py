@@ -1,0 +1,143 @@
+"""HMC driver over the C ABI: one chain shard per process/GPU.
+
+Host-side logic only (scalars): step-size adaptation by dual averaging
+(Hoffman & Gelman 2014, Alg. 5 — the "robust adaptation procedure" of
+P:652-653, reading R20) on ONE global log ε driven by the all-chain mean
+acceptance probability, and the R-hat assembly from per-rank partial sums
+(reading R21).  All per-chain work (momenta, leapfrog, Metropolis,
+acceptance sums, Welford) runs in libmt kernels.
+
+Chain sharding: chains are split contiguously over ranks,
+Philox streams are keyed by the GLOBAL chain id and acceptance sums are exact
+int64 fixed-point, so every rank computes the same ε and per-chain results do
+not depend on the number of GPUs.  The only collectives are an all-reduce of
+two int64 per warm-up iteration and of 3P doubles for R-hat at the end.
+"""
+from __future__ import annotations
+
+import math
+from typing import Optional
+
+import numpy as np
+
+
+class DualAveraging:
+    """Nesterov dual averaging of log ε towards a target acceptance δ."""
+
+    def __init__(self, eps0: float, target: float = 0.8, gamma: float = 0.05, t0: float = 10.0,
+                 kappa: float = 0.75):
+        self.mu = math.log(10.0 * eps0)
+        self.target, self.gamma, self.t0, self.kappa = target, gamma, t0, kappa
+        self.m = 0
+        self.hbar = 0.0
+        self.log_eps = math.log(eps0)
+        self.log_eps_bar = 0.0
+
+    def update(self, alpha: float) -> float:
+        self.m += 1
+        m = self.m
+        w = 1.0 / (m + self.t0)
+        self.hbar = (1.0 - w) * self.hbar + w * (self.target - alpha)
+        self.log_eps = self.mu - math.sqrt(m) / self.gamma * self.hbar
+        mk = m ** (-self.kappa)
+        self.log_eps_bar = mk * self.log_eps + (1.0 - mk) * self.log_eps_bar
+        return math.exp(self.log_eps)
+
+    def final(self) -> float:
+        return math.exp(self.log_eps_bar)
+
+
+def rhat_from_partials(part: np.ndarray, n_chains: int, n: int) -> np.ndarray:
+    """Classic R-hat per parameter from Σ m̄_c, Σ m̄_c², Σ s²_c over all chains."""
+    s1, s2, sv = part
+    mean = s1 / n_chains
+    B_over_n = (s2 - n_chains * mean ** 2) / (n_chains - 1)   # variance of chain means
+    W = sv / n_chains
+    var_plus = (n - 1) / n * W + B_over_n
+    return np.sqrt(var_plus / W)
+
+
+class ChainShard:
+    """Device state of this rank's chains and the HMC loop."""
+
+    def __init__(self, problem, x0: np.ndarray, seed: int, L: int, eps0: float,
+                 chain_offset: int = 0, n_chains_total: Optional[int] = None, group=None,
+                 stream=None):
+        import torch
+        self.torch = torch
+        self.pb = problem
+        self.dev = torch.device(f"cuda:{problem.device}")
+        self.C, self.P = x0.shape
+        self.seed, self.L = seed, L
+        self.chain_offset = chain_offset
+        self.n_total = n_chains_total or self.C
+        self.group = group
+        self.stream = stream
+        t = lambda *s, dt=torch.float32: torch.zeros(s, dtype=dt, device=self.dev)  # noqa: E731
+        self.x = torch.from_numpy(np.ascontiguousarray(x0, np.float32)).to(self.dev)
+        self.logp = t(self.C, dt=torch.float64)
+        self.grad = t(self.C, self.P)
+        self.eps = torch.full((self.C,), eps0, dtype=torch.float32, device=self.dev)
+        self.acc_prob = t(self.C)
+        self.accepted = t(self.C, dt=torch.int32)
+        self.status = t(self.C, dt=torch.int32)
+        self.acc_fixed = t(2, dt=torch.int64)
+        self.mean = t(self.C, self.P)
+        self.m2 = t(self.C, self.P)
+        self.n_samples = 0
+        self.da = DualAveraging(eps0)
+        self.it = 0
+        problem.logpost_grad(self.x, self.logp, self.grad, self.status, stream=stream)
+
+    def _allreduce(self, t, op="sum"):
+        if self.group is not None or self._dist():
+            import torch.distributed as dist
+            dist.all_reduce(t, op=dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX, group=self.group)
+        return t
+
+    @staticmethod
+    def _dist() -> bool:
+        try:
+            import torch.distributed as dist
+            return dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
+        except Exception:
+            return False
+
+    def step(self, adapt: bool = True, sample: bool = False) -> float:
+        """One HMC iteration (a1-a9).  Returns the global mean acceptance probability
+        (only when adapting: it needs the all-rank sum on the host)."""
+        pb = self.pb
+        pb.hmc_step(self.x, self.logp, self.grad, self.eps, self.L, self.seed, self.it,
+                    self.chain_offset, self.acc_prob, self.accepted, self.status, stream=self.stream)
+        alpha = float("nan")
+        if adapt:
+            self.acc_fixed.zero_()
+            pb.stats_update(self.C, accept_prob=self.acc_prob, acc_fixed=self.acc_fixed, stream=self.stream)
+        if sample:
+            pb.stats_update(self.C, x=self.x, n_prev=self.n_samples, mean=self.mean, m2=self.m2,
+                            stream=self.stream)
+            self.n_samples += 1
+        if adapt:
+            self._allreduce(self.acc_fixed)
+            s, n = (int(v) for v in self.acc_fixed.cpu().tolist())
+            alpha = s / 4294967296.0 / max(n, 1)
+            self.eps.fill_(self.da.update(alpha))
+        self.it += 1
+        return alpha
+
+    def end_warmup(self):
+        self.eps.fill_(self.da.final())
+
+    def rhat(self) -> np.ndarray:
+        part = self.pb.rhat_partials(self.C, self.mean, self.m2, self.n_samples, stream=self.stream)
+        self._allreduce(part)
+        return rhat_from_partials(part.cpu().numpy(), self.n_total, self.n_samples)
+
+    def run(self, n_warmup: int, n_sample: int):
+        accs = []
+        for _ in range(n_warmup):
+            accs.append(self.step(adapt=True))
+        self.end_warmup()
+        for _ in range(n_sample):
+            self.step(adapt=False, sample=True)
+        return dict(warmup_accept=accs, eps=float(self.eps[0]), rhat=self.rhat() if n_sample > 1 else None)

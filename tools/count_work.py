@@ -1,0 +1,51 @@
+"""Algorithmic work per chain x ray for the roofline.
+
+Runs the ORACLE's instrumentation (§c.1 step 13) on each config's own
+near-posterior chain states and writes data/work_counts.json:
+  n_inbox  cells of the in-box traversal
+  n_band   cells whose z-range meets the chain's band [min H0, max H1]
+  n_solve  surface-cells not resolved by the corner-bound test (a quadratic solve)
+  n_cross  surface crossings (adjoint scatters of 4 nodes)
+per chain x ray, and the algorithmic FP32 flop count per chain x ray
+  F = F_CELL*n_band + F_SOLVE*n_solve + F_CROSS*n_cross + F_EPI
+with the op counts of the minimal formulas (add/mul = 1,
+FMA = 2, div/sqrt/exp = 1):
+  F_CELL = 14   DDA event choice + parameter, z-range, per-surface band test, length add
+  F_SOLVE = 57  cell coefficients (34), roots (8), piece classification (15)
+  F_CROSS = 18  crossing position, 1/|g'|, four bilinear adjoint weights
+  F_EPI = 14    t = ln(λ/C), expm1, ℓ_p, ∂ℓ/∂O, per-surface factors, accumulate
+Usage: python tools/count_work.py [config ...]
+"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import oracle  # noqa: E402
+from paper_2603_28907_b200 import inputs  # noqa: E402
+
+F_CELL, F_SOLVE, F_CROSS, F_EPI = 14, 57, 18, 14
+
+
+def count(name: str, n_chains: int = 4):
+    cfg = inputs.CONFIGS[name]
+    prob = inputs.make_problem(name)
+    op = oracle.Problem(prob)
+    x = inputs.chain_states(prob["x_true"], n_chains, cfg.seed)
+    out = op.logpost_grad(x.astype("float64"))
+    c = out["counters"] / float(n_chains * op.R)
+    n_inbox, n_band, n_solve, n_cross = (float(v) for v in c)
+    F = F_CELL * n_band + F_SOLVE * n_solve + F_CROSS * n_cross + F_EPI
+    return dict(n_inbox=n_inbox, n_band=n_band, n_solve=n_solve, n_cross=n_cross,
+                flops_per_pair=F, chains_sampled=n_chains, rays=op.R,
+                weights=dict(F_CELL=F_CELL, F_SOLVE=F_SOLVE, F_CROSS=F_CROSS, F_EPI=F_EPI))
+
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or ["tiny", "small", "medium", "ray_sharded"]
+    path = os.path.join(inputs.DATA_DIR, "work_counts.json")
+    data = json.load(open(path)) if os.path.exists(path) else {}
+    for n in names:
+        data[inputs.DATA_NAME[n]] = count(n, 1 if n == "ray_sharded" else 4)
+        print(n, json.dumps(data[inputs.DATA_NAME[n]]))
+    json.dump(data, open(path, "w"), indent=1, sort_keys=True)
