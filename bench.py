@@ -187,7 +187,11 @@ def main():
     x0 = inputs.chain_states(prob["x_true"], C, cfg.seed, chain_offset=offset, super_size=8)
     pb = Problem(prob, device=local, max_chains=C)
     R, P = pb.R, pb.P
-    shard = ChainShard(pb, x0, seed=inputs.philox_key(cfg), L=L, eps0=cfg.eps, chain_offset=offset,
+    # sampling-phase step size from the dual-averaging warm-up (tools/tune_eps.py)
+    tpath = os.path.join(ROOT, "data", "tuned_eps.json")
+    tuned = json.load(open(tpath)).get("medium") if os.path.exists(tpath) else None
+    eps = tuned["eps"] if tuned else cfg.eps
+    shard = ChainShard(pb, x0, seed=inputs.philox_key(cfg), L=L, eps0=eps, chain_offset=offset,
                        n_chains_total=C * ws)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MiB > 126 MB L2
 
@@ -198,7 +202,7 @@ def main():
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        shard.step(adapt=True)
+        shard.step(adapt=False, sample=True, monitor=True)
     barrier()
     clocks = ClockSampler() if rank == 0 else None
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -207,7 +211,7 @@ def main():
     for k in range(args.steps):
         flush.zero_()
         ev[k][0].record()
-        shard.step(adapt=True)
+        shard.step(adapt=False, sample=True, monitor=True)
         ev[k][1].record()
     barrier()
     wall = time.perf_counter() - wall0
@@ -251,7 +255,7 @@ def main():
         e0.record()
         for k in range(args.steps):
             shard.x.copy_(xh, non_blocking=True)
-            shard.step(adapt=True)
+            shard.step(adapt=False, sample=True, monitor=True)
             lph.copy_(shard.logp, non_blocking=True)
             aph.copy_(shard.acc_prob, non_blocking=True)
         e1.record()
@@ -278,6 +282,9 @@ def main():
             "config": {"workload": "chain_sharded HMC iteration (BASELINE configs[3] geometry = configs[2] Medium)",
                        "chains_per_gpu": C, "global_chains": C * ws, "rays": R, "params": P,
                        "leapfrog_steps": L, "parallelism": f"chain-sharded x{ws}",
+                       "phase": "sampling (fixed eps from the 100-iteration dual-averaging warm-up, "
+                                "tools/tune_eps.py; Welford + all-reduced acceptance sums each step)",
+                       "eps": eps,
                        "l2": "flushed between timed steps (256 MiB write, outside the events)"},
             "roofline": roofline, "cpu_baseline": base, "e2e": e2e, "clocks": ck,
             "gpu_launches": tm["all_launches"],

@@ -103,25 +103,26 @@ class ChainShard:
         except Exception:
             return False
 
-    def step(self, adapt: bool = True, sample: bool = False) -> float:
+    def step(self, adapt: bool = True, sample: bool = False, monitor: bool = False) -> float:
         """One HMC iteration (a1-a9).  Returns the global mean acceptance probability
-        (only when adapting: it needs the all-rank sum on the host)."""
+        when adapting or monitoring (it needs the all-rank sum on the host)."""
         pb = self.pb
         pb.hmc_step(self.x, self.logp, self.grad, self.eps, self.L, self.seed, self.it,
                     self.chain_offset, self.acc_prob, self.accepted, self.status, stream=self.stream)
         alpha = float("nan")
-        if adapt:
+        if adapt or monitor:
             self.acc_fixed.zero_()
             pb.stats_update(self.C, accept_prob=self.acc_prob, acc_fixed=self.acc_fixed, stream=self.stream)
         if sample:
             pb.stats_update(self.C, x=self.x, n_prev=self.n_samples, mean=self.mean, m2=self.m2,
                             stream=self.stream)
             self.n_samples += 1
-        if adapt:
+        if adapt or monitor:
             self._allreduce(self.acc_fixed)
             s, n = (int(v) for v in self.acc_fixed.cpu().tolist())
             alpha = s / 4294967296.0 / max(n, 1)
-            self.eps.fill_(self.da.update(alpha))
+            if adapt:
+                self.eps.fill_(self.da.update(alpha))
         self.it += 1
         return alpha
 

@@ -1,0 +1,134 @@
+"""Multi-process host logic of chain sharding, on CPU with gloo (world_size 2).
+
+What the N-GPU bench relies on, checked without GPUs:
+  * the global chain ids a rank owns give exactly the chain states of the
+    unsharded run (Philox streams and initial states keyed by global id);
+  * the fixed-point acceptance sums all-reduced over ranks give the SAME mean
+    acceptance, hence the same dual-averaging step size, on every rank and as
+    an unsharded run (order-independent integer sums, HP9);
+  * R-hat partial sums all-reduced over ranks equal the single-process R-hat
+    computed from all chains at once.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2603_28907_b200 import inputs
+from paper_2603_28907_b200.hmc import DualAveraging, rhat_from_partials
+
+WS = 2
+C_PER = 8
+P = 16
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def fixed_point(acc):
+    """Host mirror of k_accept_sum: Σ round(a·2^32) and the count, int64."""
+    return np.array([np.sum(np.rint(np.asarray(acc, np.float64) * 4294967296.0).astype(np.int64)),
+                     len(acc)], np.int64)
+
+
+def welford(xs):
+    n = len(xs)
+    mean = np.zeros_like(xs[0])
+    m2 = np.zeros_like(xs[0])
+    for k, x in enumerate(xs, 1):
+        d = x - mean
+        mean = mean + d / k
+        m2 = m2 + d * (x - mean)
+    return mean, m2, n
+
+
+def make_draws(n_iter, n_chains):
+    rng = np.random.default_rng(123)
+    return rng.standard_normal((n_iter, n_chains, P)) * 0.7 + rng.standard_normal((1, n_chains, P)) * 0.2
+
+
+def worker(rank, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WS)
+    try:
+        res = {}
+        # 1. chain partition
+        cfg = inputs.CONFIGS["small"]
+        xt = inputs.make_problem("small")["x_true"]
+        res["x0"] = inputs.chain_states(xt, C_PER, cfg.seed, chain_offset=rank * C_PER, super_size=8)
+        # 2. dual averaging driven by all-reduced fixed-point acceptance sums
+        rng = np.random.default_rng(7)
+        acc_all = rng.uniform(0, 1, size=(20, WS * C_PER))
+        da = DualAveraging(1e-3)
+        eps = []
+        for it in range(20):
+            t = torch.from_numpy(fixed_point(acc_all[it, rank * C_PER:(rank + 1) * C_PER]))
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            s, n = (int(v) for v in t.tolist())
+            eps.append(da.update(s / 4294967296.0 / n))
+        res["eps"] = eps
+        # 3. R-hat partials
+        draws = make_draws(30, WS * C_PER)[:, rank * C_PER:(rank + 1) * C_PER]
+        mean, m2, n = welford(list(draws))
+        part = np.stack([mean.sum(0), (mean ** 2).sum(0), (m2 / (n - 1)).sum(0)])
+        t = torch.from_numpy(part)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        res["rhat"] = rhat_from_partials(t.numpy(), WS * C_PER, n)
+        out[rank] = res
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.fixture(scope="module")
+def results():
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    out = mgr.dict()
+    port = free_port()
+    procs = [ctx.Process(target=worker, args=(r, port, out)) for r in range(WS)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+        assert p.exitcode == 0
+    return dict(out)
+
+
+def test_chain_partition_matches_unsharded(results):
+    cfg = inputs.CONFIGS["small"]
+    xt = inputs.make_problem("small")["x_true"]
+    whole = inputs.chain_states(xt, WS * C_PER, cfg.seed, super_size=8)
+    got = np.concatenate([results[r]["x0"] for r in range(WS)])
+    assert np.array_equal(got, whole)
+
+
+def test_step_size_identical_on_all_ranks_and_unsharded(results):
+    assert results[0]["eps"] == results[1]["eps"]
+    rng = np.random.default_rng(7)
+    acc_all = rng.uniform(0, 1, size=(20, WS * C_PER))
+    da = DualAveraging(1e-3)
+    ref = []
+    for it in range(20):
+        s, n = fixed_point(acc_all[it])
+        ref.append(da.update(int(s) / 4294967296.0 / int(n)))
+    assert results[0]["eps"] == ref          # bit-identical: integer sums are order-free
+
+
+def test_rhat_from_allreduced_partials(results):
+    draws = make_draws(30, WS * C_PER)            # [iter][chain][param]
+    n, m = draws.shape[0], draws.shape[1]
+    cm = draws.mean(0)
+    B = n * cm.var(0, ddof=1)
+    W = draws.var(0, ddof=1).mean(0)
+    ref = np.sqrt(((n - 1) / n * W + B / n) / W)  # Gelman-Rubin (P:684-687 cites the nested form)
+    assert np.allclose(results[0]["rhat"], ref, rtol=1e-10)
+    assert np.allclose(results[1]["rhat"], ref, rtol=1e-10)

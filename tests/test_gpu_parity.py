@@ -279,3 +279,46 @@ def test_ray_shards_sum_to_whole(gpu, problems):
     gsum = sum(v.cpu().numpy().astype(np.float64) for v in gs)
     for c in range(8):
         assert rel_l2(gsum[c], g.cpu().numpy()[c].astype(np.float64)) < 1e-5
+
+
+# ---------------------------------------------------------------------------
+# a9 statistics kernels against plain numpy
+# ---------------------------------------------------------------------------
+def test_stats_kernels_match_numpy(gpu):
+    mp = gpu("small", max_chains=64)
+    C, P = 64, mp.P
+    rng = np.random.default_rng(4)
+    draws = rng.standard_normal((12, C, P)).astype(np.float32)
+    acc = rng.uniform(0, 1, (12, C)).astype(np.float32)
+    mean = torch.zeros((C, P), device=DEV)
+    m2 = torch.zeros((C, P), device=DEV)
+    accf = torch.zeros(2, dtype=torch.int64, device=DEV)
+    for it in range(12):
+        mp.stats_update(C, x=torch.from_numpy(draws[it]).to(DEV), accept_prob=torch.from_numpy(acc[it]).to(DEV),
+                        n_prev=it, mean=mean, m2=m2, acc_fixed=accf)
+    torch.cuda.synchronize()
+    assert np.allclose(mean.cpu().numpy(), draws.mean(0), atol=1e-5)
+    assert np.allclose(m2.cpu().numpy() / 11, draws.var(0, ddof=1), rtol=1e-4, atol=1e-5)
+    s, n = accf.cpu().tolist()
+    ref = int(np.sum(np.rint(acc.astype(np.float64) * 4294967296.0).astype(np.int64)))
+    assert s == ref and n == 12 * C            # exact integer sums
+    part = mp.rhat_partials(C, mean, m2, 12).cpu().numpy()
+    cm = draws.astype(np.float64).mean(0)
+    assert np.allclose(part[0], cm.sum(0), rtol=1e-5, atol=1e-4)
+    assert np.allclose(part[1], (cm ** 2).sum(0), rtol=1e-5, atol=1e-4)
+    assert np.allclose(part[2], draws.astype(np.float64).var(0, ddof=1).sum(0), rtol=1e-4)
+
+
+def test_hmc_driver_runs_and_adapts(gpu, problems):
+    """ChainShard: dual-averaging warm-up then sampling on Small; acceptance
+    near the 0.8 target, finite R-hat, chains stay finite."""
+    from paper_2603_28907_b200.hmc import ChainShard
+    prob = problems("small")
+    cfg = inputs.CONFIGS["small"]
+    mp = gpu("small", max_chains=64)
+    x0 = inputs.chain_states(prob["x_true"], 64, cfg.seed, super_size=8)
+    sh = ChainShard(mp, x0, seed=inputs.philox_key(cfg), L=10, eps0=cfg.eps)
+    out = sh.run(60, 20)
+    assert 0.55 < np.mean(out["warmup_accept"][-10:]) < 0.95
+    assert np.all(np.isfinite(out["rhat"])) and out["rhat"].min() > 0.9
+    assert torch.isfinite(sh.x).all() and torch.isfinite(sh.logp).all()
