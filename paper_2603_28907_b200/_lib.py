@@ -12,7 +12,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libmt.so")
+SO_PATH = os.environ.get("MT_LIB") or os.path.join(_HERE, "libmt.so")   # MT_LIB: tuning variants
 
 MT_STATUS_NONFINITE = 1
 MT_STATUS_DIVERGENT = 2

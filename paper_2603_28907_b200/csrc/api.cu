@@ -6,6 +6,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <new>
 #include <string>
 #include <vector>
@@ -78,7 +79,7 @@ int check_chains(const mt_problem *p, int32_t C) {
 }
 
 void free_all(mt_problem *p) {
-  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_trav_off, p->d_trav, p->d_H, p->d_G,
+  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_H, p->d_G,
                   p->d_band, p->d_ll, p->d_x0, p->d_g0, p->d_mom, p->d_kin0, p->d_kin1, p->d_lp0};
   for (void *b : bufs)
     if (b) cudaFree(b);
@@ -191,6 +192,37 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   }
   p->loglik_offset = off;
 
+  // ---- internal ray order (performance only; results are order-independent
+  // and per-ray outputs are mapped back): Morton order of the cell where the
+  // ray reaches mid-height z_top/2, so rays processed together by a block
+  // traverse the same band cells and their corner lines stay in L1.
+  p->perm.resize(p->R);
+  for (int64_t q = 0; q < p->R; q++) p->perm[q] = (int32_t)q;
+  const char *ord = getenv("MT_RAY_ORDER");
+  if (!(ord && atoi(ord) == 0)) {
+    std::vector<uint64_t> key(p->R);
+    for (int64_t q = 0; q < p->R; q++) {
+      double sm = fmin(0.5 * (double)d->z_top / rb[q].x, (double)rb[q].y);
+      double px = ra[q].x + sm * ra[q].z, py = ra[q].y + sm * ra[q].w;
+      int ci = (int)floor((px - X0) / ((double)X1 - X0) * (p->nx - 1));
+      int cj = (int)floor((py - Y0) / ((double)Y1 - Y0) * (p->ny - 1));
+      ci = ci < 0 ? 0 : (ci > p->nx - 2 ? p->nx - 2 : ci);
+      cj = cj < 0 ? 0 : (cj > p->ny - 2 ? p->ny - 2 : cj);
+      uint64_t m = 0;
+      for (int b = 0; b < 16; b++) m |= (uint64_t)((ci >> b) & 1) << (2 * b) | (uint64_t)((cj >> b) & 1) << (2 * b + 1);
+      key[q] = (m << 32) | (uint64_t)q;
+    }
+    std::sort(p->perm.begin(), p->perm.end(), [&](int32_t a, int32_t b) { return key[a] < key[b]; });
+    std::vector<float4> ra2(p->R), rb2(p->R);
+    std::vector<float> ob2(p->R);
+    for (int64_t k = 0; k < p->R; k++) {
+      ra2[k] = ra[p->perm[k]]; rb2[k] = rb[p->perm[k]]; ob2[k] = ob[p->perm[k]];
+    }
+    ra.swap(ra2); rb.swap(rb2); ob.swap(ob2);
+  }
+  p->inv_perm.resize(p->R);
+  for (int64_t k = 0; k < p->R; k++) p->inv_perm[p->perm[k]] = (int32_t)k;
+
   // ---- device buffers ----
   size_t R = (size_t)(p->R > 0 ? p->R : 1), MC = (size_t)(p->max_chains > 0 ? p->max_chains : 1);
   size_t P = p->P;
@@ -204,6 +236,7 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   ALLOC(p->d_ray_a, sizeof(float4) * R);
   ALLOC(p->d_ray_b, sizeof(float4) * R);
   ALLOC(p->d_obase, sizeof(float) * R);
+  ALLOC(p->d_perm, sizeof(int32_t) * R);
   ALLOC(p->d_H, sizeof(float) * MC32 * P);
   ALLOC(p->d_G, sizeof(float) * MC32 * P);
   ALLOC(p->d_band, sizeof(float4) * MC);
@@ -226,6 +259,7 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   if (e == cudaSuccess && p->R > 0) e = cudaMemcpy(p->d_ray_a, ra.data(), sizeof(float4) * p->R, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && p->R > 0) e = cudaMemcpy(p->d_ray_b, rb.data(), sizeof(float4) * p->R, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && p->R > 0) e = cudaMemcpy(p->d_obase, ob.data(), sizeof(float) * p->R, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && p->R > 0) e = cudaMemcpy(p->d_perm, p->perm.data(), sizeof(int32_t) * p->R, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemset(p->d_G, 0, sizeof(float) * MC32 * P);
   if (e == cudaSuccess) e = cudaMemset(p->d_H, 0, sizeof(float) * MC32 * P);
   if (e == cudaSuccess) e = cudaMemset(p->d_ll, 0, sizeof(double) * MC);
@@ -418,7 +452,7 @@ int mt_debug_traversal(mt_problem *p, int64_t ray, int32_t *ij, float *s_in, flo
   DevGuard g(p->device);
   // the stored traversal the trace kernels read (built by the exact device DDA)
   int32_t off[2];
-  CK(cudaMemcpy(off, p->d_trav_off + ray, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(off, p->d_trav_off + p->inv_perm[ray], sizeof(int32_t) * 2, cudaMemcpyDeviceToHost));
   *n = (int32_t)(off[1] - off[0]);
   int m = *n < cap ? *n : cap;
   if (m > 0) {

@@ -40,6 +40,7 @@ struct TraceArgs {
   const float *obase;           // ρ_rock s_exit + ρ_ext L_ext (path-length export only)
   const int32_t *trav_off;      // [R+1] CSR offsets of each ray's stored traversal
   const int2 *trav;             // {i | j << 16, s_out bits} per cell, in ray order (a2)
+  const int32_t *perm;          // internal ray index -> caller's ray index
   int64_t R;                    // rays in the shard
   int64_t rays_per_block;
   int C;                        // chains in this call
@@ -90,6 +91,8 @@ struct mt_problem {
   float4 *d_ray_a = nullptr, *d_ray_b = nullptr;
   float *d_obase = nullptr;
   int32_t *d_trav_off = nullptr;
+  int32_t *d_perm = nullptr;
+  std::vector<int32_t> perm, inv_perm;   // internal <-> caller ray order (host)
   int2 *d_trav = nullptr;
   int64_t trav_cells = 0;
   float *d_H = nullptr, *d_G = nullptr;
