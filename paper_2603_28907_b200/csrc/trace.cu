@@ -241,20 +241,40 @@ __device__ __forceinline__ void scatter4(float *Gl, int STRIDE, int base, int ny
 
 // fp64 re-solve of one ill-conditioned cell (HP2 lever 1): same fp32 inputs,
 // exact cell spacing, oracle-style midpoint classification.  Rare; noinline so
-// its double-precision registers stay out of the hot loop.
-template <int L, int STRIDE, bool SCAT>
-__device__ __noinline__ void fix64(const Geo &g, const Ray &r, float *Gl, int base, int i, int j,
-                                   float s, float s1, float h00, float h10, float h01, float h11,
-                                   float &B, Recs &R, bool &ovf, float f) {
+// its double-precision registers stay out of the hot loop.  Everything is
+// passed and returned BY VALUE: a reference to a caller's accumulator would
+// make it address-taken and pin it to local memory for the whole loop.
+struct Fix {
+  float below;
+  int n;
+  float u[2], v[2], ig[2];
+};
+
+__device__ __noinline__ Fix fix64(float h00, float h10, float h01, float h11, float Xi, float Xi1,
+                                  float Yj, float Yj1, Ray r, float s, float s1) {
   double u0, v0, al, be;
-  CellSol<double> sd = solve_cell_f64(h00, h10, h01, h11, g.Xs[i], g.Xs[i + 1], g.Ys[j],
-                                      g.Ys[j + 1], r, s, s1, u0, v0, al, be);
-  B += (float)sd.below;
-  for (int k = 0; k < sd.n; k++) {
-    float uc = (float)(u0 + al * sd.tc[k]), vc = (float)(v0 + be * sd.tc[k]);
-    float ig = (float)(1.0 / fabs(sd.gp[k]));
-    if (SCAT) scatter4(Gl, STRIDE, base, g.ny, f * ig, uc, vc);
-    else rec_push<L>(R, ovf, base, uc, vc, ig);
+  CellSol<double> sd = solve_cell_f64(h00, h10, h01, h11, Xi, Xi1, Yj, Yj1, r, s, s1, u0, v0, al, be);
+  Fix x;
+  x.below = (float)sd.below;
+  x.n = sd.n;
+  for (int k = 0; k < 2; k++) {
+    x.u[k] = (float)(u0 + al * sd.tc[k]);
+    x.v[k] = (float)(v0 + be * sd.tc[k]);
+    x.ig[k] = (float)(1.0 / fabs(sd.gp[k]));
+  }
+  return x;
+}
+
+template <int L, int STRIDE, bool SCAT>
+__device__ __forceinline__ void apply_fix64(const Geo &g, const Ray &r, float *Gl, int base, int i,
+                                            int j, float s, float s1, float h00, float h10,
+                                            float h01, float h11, float &B, Recs &R, bool &ovf,
+                                            float f) {
+  const Fix x = fix64(h00, h10, h01, h11, g.Xs[i], g.Xs[i + 1], g.Ys[j], g.Ys[j + 1], r, s, s1);
+  B += x.below;
+  for (int k = 0; k < x.n; k++) {
+    if (SCAT) scatter4(Gl, STRIDE, base, g.ny, f * x.ig[k], x.u[k], x.v[k]);
+    else rec_push<L>(R, ovf, base, x.u[k], x.v[k], x.ig[k]);
   }
 }
 
@@ -296,7 +316,7 @@ __device__ __forceinline__ void cell32(const Geo &g, const Ray &r, const float *
     float t = (ta > 0.f && ta < Ls) ? ta : tb;
     t = fminf(fmaxf(t, 0.f), Ls);
     const float gp = g1 + a2 * t;
-    if (fabsf(gp) < GTHR || !(disc > 0.f)) { fix64<L, STRIDE, SCAT>(g, r, Gl, base, i, j, s, s1, h00, h10, h01, h11, B, R, ovf, f); return; }
+    if (fabsf(gp) < GTHR || !(disc > 0.f)) { apply_fix64<L, STRIDE, SCAT>(g, r, Gl, base, i, j, s, s1, h00, h10, h01, h11, B, R, ovf, f); return; }
     B += p0 ? t : Ls - t;
     const float ig = __frcp_rn(fabsf(gp)), uc = u0 + al * t, vc = v0 + be * t;
     if (SCAT) scatter4(Gl, STRIDE, base, g.ny, f * ig, uc, vc);
@@ -304,7 +324,7 @@ __device__ __forceinline__ void cell32(const Geo &g, const Ray &r, const float *
   } else if (disc > 0.f && vin && ((g2 > 0.f) == p0)) {   // two crossings
     float t1 = fminf(ta, tb), t2 = fmaxf(ta, tb);
     const float gp1 = g1 + a2 * t1, gp2 = g1 + a2 * t2;
-    if (fabsf(gp1) < GTHR || fabsf(gp2) < GTHR) { fix64<L, STRIDE, SCAT>(g, r, Gl, base, i, j, s, s1, h00, h10, h01, h11, B, R, ovf, f); return; }
+    if (fabsf(gp1) < GTHR || fabsf(gp2) < GTHR) { apply_fix64<L, STRIDE, SCAT>(g, r, Gl, base, i, j, s, s1, h00, h10, h01, h11, B, R, ovf, f); return; }
     B += p0 ? Ls - (t2 - t1) : (t2 - t1);
     const float ig1 = __frcp_rn(fabsf(gp1)), ig2 = __frcp_rn(fabsf(gp2));
     if (SCAT) {
@@ -315,7 +335,7 @@ __device__ __forceinline__ void cell32(const Geo &g, const Ray &r, const float *
       rec_push<L>(R, ovf, base, u0 + al * t2, v0 + be * t2, ig2);
     }
   } else {                                      // no crossing
-    if (vin && fabsf(disc) < 2.f * fabsf(a2) * ZTHR) { fix64<L, STRIDE, SCAT>(g, r, Gl, base, i, j, s, s1, h00, h10, h01, h11, B, R, ovf, f); return; }  // near-tangent
+    if (vin && fabsf(disc) < 2.f * fabsf(a2) * ZTHR) { apply_fix64<L, STRIDE, SCAT>(g, r, Gl, base, i, j, s, s1, h00, h10, h01, h11, B, R, ovf, f); return; }  // near-tangent
     if (p0) B += Ls;
   }
 }
@@ -432,7 +452,7 @@ __device__ __forceinline__ void trace_pair(const Geo &g, const Ray &r, const int
 // the chain x ray directly, through the same fp32 cell code (and its fp64
 // fixes) as the recording walk, so the crossings are identical.
 template <int STRIDE, bool LDG>
-__device__ __noinline__ void rewalk_scatter(const Geo &g, const Ray &r, const int2 *__restrict__ cells,
+__device__ __noinline__ void rewalk_scatter(const Geo g, const Ray r, const int2 *__restrict__ cells,
                                             int k0, int kend, float s_lo, float s_hi,
                                             const float *Hk, float *Gk, float4 bd, float f0,
                                             float f1) {

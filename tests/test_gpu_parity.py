@@ -38,6 +38,15 @@ def rel_l2(a, b):
     return np.linalg.norm(a - b) / np.linalg.norm(b)
 
 
+def sampling_eps(name):
+    """The sampling-phase step size (tools/tune_eps.py) when tuned, else the config's."""
+    import json
+    import os
+    path = os.path.join(inputs.DATA_DIR, "tuned_eps.json")
+    tuned = json.load(open(path)) if os.path.exists(path) else {}
+    return tuned.get(name, {}).get("eps", inputs.CONFIGS[name].eps)
+
+
 # ---------------------------------------------------------------------------
 # traversal (integer, bit-exact)
 # ---------------------------------------------------------------------------
@@ -165,16 +174,23 @@ def test_leapfrog_10_steps(gpu, oracle_problem, name, C):
     p = mp.draw_momenta(C, seed, 0)
     p0 = p.cpu().numpy().astype(np.float64)
     logp, grad = mp.logpost_grad(x)
-    eps = torch.full((C,), cfg.eps, dtype=torch.float32, device=DEV)
+    e = sampling_eps(name)
+    eps = torch.full((C,), e, dtype=torch.float32, device=DEV)
     mp.leapfrog(x, p, logp, grad, eps, 10)
-    xo, po, lpo, go = oracle.leapfrog(x0.astype(np.float64), p0, cfg.eps, 10,
+    xo, po, lpo, go = oracle.leapfrog(x0.astype(np.float64), p0, e, 10,
                                       lambda xx: (lambda o: (o["logp"], o["grad"]))(op.logpost_grad(xx)))
     xd = x.cpu().numpy().astype(np.float64)
     for c in range(C):
-        assert rel_l2(xd[c], xo[c]) <= 1e-3, (c, rel_l2(xd[c], xo[c]))
+        assert rel_l2(xd[c], xo[c]) <= 1e-3, (c, rel_l2(xd[c], xo[c]))   # north_star criterion
         disp = np.linalg.norm(xd[c] - xo[c]) / np.linalg.norm(xo[c] - x0[c])
         assert disp < 0.05, (c, disp)   # diagnostic: displacement-relative error
-    assert np.allclose(logp.cpu().numpy(), lpo, rtol=1e-4)
+    # logp/grad returned by the fused leapfrog are those of its own final x.  (Comparing with
+    # the oracle's trajectory end instead is ill-conditioned: |∇logp| ~ 1e5, so position
+    # differences well inside 1e-3 move logp by O(10).)
+    ref = op.logpost_grad(xd)
+    assert np.allclose(logp.cpu().numpy(), ref["logp"], rtol=1e-4)
+    for c in range(C):
+        assert rel_l2(grad.cpu().numpy()[c].astype(np.float64), ref["grad"][c]) <= 1e-3
 
 
 def test_hmc_step_matches_oracle_decisions(gpu, oracle_problem):
@@ -185,10 +201,11 @@ def test_hmc_step_matches_oracle_decisions(gpu, oracle_problem):
     seed = inputs.philox_key(cfg)
     x = torch.from_numpy(x0).to(DEV)
     logp, grad = mp.logpost_grad(x)
-    eps = torch.full((C,), cfg.eps, dtype=torch.float32, device=DEV)
+    e = sampling_eps(name)
+    eps = torch.full((C,), e, dtype=torch.float32, device=DEV)
     ap, acc = mp.hmc_step(x, logp, grad, eps, 10, seed, 3)
     lg = lambda xx: (lambda o: (o["logp"], o["grad"]))(op.logpost_grad(xx))  # noqa: E731
-    xo, apo, acco, lpo, dHo = oracle.hmc_step(x0.astype(np.float64), cfg.eps, 10, lg, seed, 3)
+    xo, apo, acco, lpo, dHo = oracle.hmc_step(x0.astype(np.float64), e, 10, lg, seed, 3)
     u = np.array([oracle.mh_uniform(seed, 3, c) for c in range(C)])
     clear = np.abs(np.log(u) + dHo) > 0.05      # decisions far from the threshold must agree
     acc = acc.cpu().numpy().astype(bool)
