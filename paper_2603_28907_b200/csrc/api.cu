@@ -79,7 +79,7 @@ int check_chains(const mt_problem *p, int32_t C) {
 }
 
 void free_all(mt_problem *p) {
-  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_H, p->d_G,
+  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_ovf_q, p->d_ovf_n, p->d_H, p->d_G,
                   p->d_band, p->d_ll, p->d_x0, p->d_g0, p->d_mom, p->d_kin0, p->d_kin1, p->d_lp0};
   for (void *b : bufs)
     if (b) cudaFree(b);
@@ -247,6 +247,8 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   ALLOC(p->d_kin0, sizeof(float) * MC);
   ALLOC(p->d_kin1, sizeof(float) * MC);
   ALLOC(p->d_lp0, sizeof(double) * MC);
+  ALLOC(p->d_ovf_q, sizeof(float4) * (size_t)p->ovf_cap);
+  ALLOC(p->d_ovf_n, sizeof(int) * 2);
 #undef ALLOC
   if (e != cudaSuccess) {
     free_all(p);
@@ -263,6 +265,7 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   if (e == cudaSuccess) e = cudaMemset(p->d_G, 0, sizeof(float) * MC32 * P);
   if (e == cudaSuccess) e = cudaMemset(p->d_H, 0, sizeof(float) * MC32 * P);
   if (e == cudaSuccess) e = cudaMemset(p->d_ll, 0, sizeof(double) * MC);
+  if (e == cudaSuccess) e = cudaMemset(p->d_ovf_n, 0, sizeof(int) * 2);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e == cudaSuccess) e = build_traversal(p);   // a2, once per problem (exact predicates)
   if (e != cudaSuccess) {

@@ -49,6 +49,9 @@ struct TraceArgs {
   float *G;                     // [C][2][N] ∂ℓ/∂H accumulator (atomic adds)
   double *ll;                   // [C] deviance-centred log-likelihood accumulator
   float *Lout, *Oout;           // path-length export: [C][R][3], [C][R]
+  float4 *ovf_q;                // chain lanes: deferred pairs {c, ray, s_lo, s_hi} (an ill-
+  int *ovf_n, *ovf_done;        //   conditioned cell or > RCAP crossings), done by k_trace_defer
+  int ovf_cap;
 };
 
 enum { TRACE_LL = 0, TRACE_PATH = 1 };
@@ -94,6 +97,9 @@ struct mt_problem {
   int32_t *d_perm = nullptr;
   std::vector<int32_t> perm, inv_perm;   // internal <-> caller ray order (host)
   int2 *d_trav = nullptr;
+  float4 *d_ovf_q = nullptr;    // deferred-pair queue of the chain-lanes trace (see TraceArgs)
+  int *d_ovf_n = nullptr;       // [2]: count, blocks done
+  int ovf_cap = 1 << 22;
   int64_t trav_cells = 0;
   float *d_H = nullptr, *d_G = nullptr;
   float4 *d_band = nullptr;

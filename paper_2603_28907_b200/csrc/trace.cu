@@ -161,7 +161,7 @@ __device__ __forceinline__ CellSol<T> classify(T g0, T g1, T g2, T L, T t1, T t2
 }
 
 // fp64 re-solve from the same fp32 inputs, exact cell spacing (HP2 lever 1).
-__device__ __noinline__ CellSol<double> solve_cell_f64(float h00, float h10, float h01, float h11,
+__device__ __forceinline__ CellSol<double> solve_cell_f64(float h00, float h10, float h01, float h11,
                                                        float Xi, float Xi1, float Yj, float Yj1,
                                                        const Ray &r, float s, float s1,
                                                        double &u0, double &v0, double &al,
@@ -200,7 +200,7 @@ struct Geo {
 #define MT_RCAP 4
 #endif
 #ifndef MT_CL_MINB
-#define MT_CL_MINB 3
+#define MT_CL_MINB 4
 #endif
 #ifndef MT_CARVEOUT
 #define MT_CARVEOUT -1
@@ -246,7 +246,7 @@ __device__ __forceinline__ void scatter4(float *Gl, int STRIDE, int base, int ny
 // make it address-taken and pin it to local memory for the whole loop.
 struct Fix {
   float below;
-  int n;
+  int n, base;
   float u[2], v[2], ig[2];
 };
 
@@ -401,10 +401,6 @@ __device__ __forceinline__ void walk(const Geo &g, const Ray &r, const int2 *__r
   float s = s0;
   const int sN = g.N * STRIDE;
   for (; k < kend; k++) {
-    // chain lanes, recording walk: the loop is warp-uniform; reconverge the
-    // lanes that left a cell early so every cell is one warp instruction
-    // stream.  (The SCAT re-walk runs on a divergent subset: no full-warp sync.)
-    if (STRIDE == 32 && !SCAT) __syncwarp();
     const int2 e = __ldg(cells + k);
     const float s1 = __int_as_float(e.y);
     const int i = e.x & 0xffff, j = e.x >> 16;
@@ -487,6 +483,69 @@ __device__ __forceinline__ float epilogue(const Ray &r, const TraceConsts &tc, f
   return -lam;
 }
 
+// ---------------------------------------------------------------------------
+// chain lanes: one surface of one stored cell for this lane's chain (a3).
+// Warp-uniform inputs: the cell (i, j, base node), its piece [s, s1] of the
+// ray, za = s d_z, zb = s1 d_z.  Per lane: the chain's heights (column of the
+// chain-interleaved layout), its band [zmin, zmax] of this surface, B.  The
+// arithmetic of the solve is cell32's.  An ill-conditioned cell (|g'| < GTHR
+// at a crossing, or a near-tangent vertex) sets `defer`: the whole chain x ray
+// pair is then handed to k_trace_defer, which re-traces it with the same fp32
+// cell code plus in-place fp64 re-solves (rare).  So the hot kernel holds no
+// double-precision code and makes no calls (a call forces the ABI's spills
+// into the loop).
+// ---------------------------------------------------------------------------
+template <int L, int NY>
+__device__ __forceinline__ void cw_surface(const Geo &g, const Ray &r, const float *__restrict__ Hl,
+                                           int i, int j, int base, float s, float za, float zb,
+                                           float Ls, float zmin, float zmax, float &B, int &n,
+                                           bool &defer, float4 *rec) {
+  if (zb <= zmin) { B += Ls; return; }            // below the chain's lowest node of this surface
+  if (za >= zmax) return;                         // above its highest node
+  const int oy = (NY ? NY : g.ny) * 32;
+  const float *p = Hl + base * 32;
+  const float h00 = __ldg(p), h01 = __ldg(p + 32), h10 = __ldg(p + oy), h11 = __ldg(p + oy + 32);
+  if (zb <= fminf(fminf(h00, h10), fminf(h01, h11))) { B += Ls; return; }   // bilinear min at a corner
+  if (za >= fmaxf(fmaxf(h00, h10), fmaxf(h01, h11))) return;
+  const float idx = g.idx[i], idy = g.idy[j];
+  const float u0 = (fmaf(s, r.dx, r.ox) - g.Xs[i]) * idx;
+  const float v0 = (fmaf(s, r.dy, r.oy) - g.Ys[j]) * idy;
+  const float al = r.dx * idx, be = r.dy * idy;
+  const float b = h10 - h00, c = h01 - h00, e = (h11 - h10) - (h01 - h00);
+  const float g0 = (h00 - za) + u0 * (b + e * v0) + c * v0;
+  const float g1 = b * al + c * be + e * (u0 * be + v0 * al) - r.dz;
+  const float g2 = e * al * be;
+  const float gL = g0 + Ls * (g1 + Ls * g2);
+  const float disc = fmaf(g1, g1, -4.f * g2 * g0);
+  const bool p0 = g0 > 0.f;
+  const float a2 = 2.f * g2;
+  const bool vin = -g1 * a2 > 0.f && fabsf(g1) < Ls * fabsf(a2);   // vertex inside (0, Δs)
+  float q = 0.f;
+  if (disc > 0.f) q = -0.5f * (g1 + copysignf(disc * rsqrtf(disc), g1));
+  const float ta = __fdividef(g0, q), tb = __fdividef(q, g2);       // the two roots (tb = ±inf if g2 = 0)
+  if (p0 != (gL > 0.f)) {                         // exactly one crossing
+    float t = (ta > 0.f && ta < Ls) ? ta : tb;
+    t = fminf(fmaxf(t, 0.f), Ls);
+    const float gp = g1 + a2 * t;
+    if (fabsf(gp) < GTHR || !(disc > 0.f)) { defer = true; return; }
+    B += p0 ? t : Ls - t;
+    if (n < RCAP) rec[(L * RCAP + n) * MT_THREADS] = make_float4(__int_as_float(base), u0 + al * t, v0 + be * t, __fdividef(1.f, fabsf(gp)));
+    n++;
+  } else if (disc > 0.f && vin && ((g2 > 0.f) == p0)) {   // two crossings
+    const float t1 = fminf(ta, tb), t2 = fmaxf(ta, tb);
+    const float gp1 = g1 + a2 * t1, gp2 = g1 + a2 * t2;
+    if (fabsf(gp1) < GTHR || fabsf(gp2) < GTHR) { defer = true; return; }
+    B += p0 ? Ls - (t2 - t1) : (t2 - t1);
+    if (n < RCAP) rec[(L * RCAP + n) * MT_THREADS] = make_float4(__int_as_float(base), u0 + al * t1, v0 + be * t1, __fdividef(1.f, fabsf(gp1)));
+    n++;
+    if (n < RCAP) rec[(L * RCAP + n) * MT_THREADS] = make_float4(__int_as_float(base), u0 + al * t2, v0 + be * t2, __fdividef(1.f, fabsf(gp2)));
+    n++;
+  } else {                                        // no crossing
+    if (vin && fabsf(disc) < 2.f * fabsf(a2) * ZTHR) { defer = true; return; }   // near-tangent
+    if (p0) B += Ls;
+  }
+}
+
 __device__ __forceinline__ void load_geometry(const TraceArgs &a, float *Xs, float *Ys, float *idx,
                                               float *idy) {
   const int nx = a.tc.nx, ny = a.tc.ny;
@@ -532,69 +591,102 @@ __global__ void k_build_trav(TraceArgs a, const int32_t *off, int32_t *count, in
 }
 
 // ---------------------------------------------------------------------------
-// K2, chain lanes
+// K2, chain lanes: warp = one ray x 32 chains, lane = chain
 // ---------------------------------------------------------------------------
-template <int MODE, bool SMEMH>
+template <int MODE, int NY>
 __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a) {
-  extern __shared__ __align__(16) float smem[];
-  const int nx = a.tc.nx, ny = a.tc.ny, N = a.tc.N;
-  float *Xs = smem, *Ys = Xs + nx, *idx = Ys + ny, *idy = idx + nx;
-  const int geo_words = (2 * nx + 2 * ny + 3) & ~3;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  // geometry at static shared addresses (no pointer registers): X, Y, 1/ΔX, 1/ΔY
+  __shared__ float sgeo[4][MT_MAX_AXIS];
+  extern __shared__ __align__(16) float4 recs[];    // crossing records [2*RCAP][MT_THREADS]
+  const int nx = a.tc.nx, ny = NY ? NY : a.tc.ny, N = a.tc.N;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = blockIdx.y, c = grp * 32 + lane;
   const bool act = c < a.C;
-  load_geometry(a, Xs, Ys, idx, idy);
-  const float *Hg = a.H + (size_t)grp * 2 * N * 32;
-  if (SMEMH) {
-    float4 *d4 = reinterpret_cast<float4 *>(smem + geo_words);
-    const float4 *s4 = reinterpret_cast<const float4 *>(Hg);
-    for (int k = threadIdx.x; k < 2 * N * 8; k += blockDim.x) d4[k] = __ldg(s4 + k);
-    Hg = smem + geo_words;
-  }
-  float4 *recbuf = reinterpret_cast<float4 *>(smem + geo_words + (SMEMH ? 2 * N * 32 : 0));
+  load_geometry(a, sgeo[0], sgeo[1], sgeo[2], sgeo[3]);
+  float4 *rec = recs + threadIdx.x;
   __syncthreads();
-  // this lane's chain band; the warp walks the union band of its 32 chains
-  float4 bd = act ? a.band[c] : make_float4(3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f);
+  // this lane's chain band; the warp walks the union band of its 32 chains.
+  // Inactive lanes get a band that every cell lies "above" (no loads).
+  float4 bd = act ? __ldg(a.band + c) : make_float4(3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f);
   float zlo = bd.x, zhi = bd.w;
   for (int o = 16; o > 0; o >>= 1) {
     zlo = fminf(zlo, __shfl_xor_sync(0xffffffffu, zlo, o));
     zhi = fmaxf(zhi, __shfl_xor_sync(0xffffffffu, zhi, o));
   }
-  if (!act) bd = make_float4(-3.0e38f, -3.0e38f, -3.0e38f, -3.0e38f);  // "above": no loads
+  if (!act) bd = make_float4(-3.0e38f, -3.0e38f, -3.0e38f, -3.0e38f);
   Geo g;
-  g.Xs = Xs; g.Ys = Ys; g.idx = idx; g.idy = idy; g.nx = nx; g.ny = ny; g.N = N;
-  const float *Hk = Hg + lane;
-  float *Gk = a.G + (size_t)grp * 2 * N * 32 + lane;
+  g.Xs = sgeo[0]; g.Ys = sgeo[1]; g.idx = sgeo[2]; g.idy = sgeo[3]; g.nx = nx; g.ny = ny; g.N = N;
+  const float *H0 = a.H + (size_t)grp * 2 * N * 32 + lane;
   float llacc = 0.f;
 
-  const int64_t r_begin = (int64_t)blockIdx.x * a.rays_per_block;
-  const int64_t r_end = min(a.R, r_begin + a.rays_per_block);
-  for (int64_t rr = r_begin + warp; rr < r_end; rr += nwarp) {
-    __syncwarp();
-    const Ray r = load_ray(a.ray_a, a.ray_b, rr);      // same address in every lane: broadcast
+  const int r_begin = blockIdx.x * (int)a.rays_per_block;
+  const int r_end = min((int)a.R, r_begin + (int)a.rays_per_block);
+  for (int rr = r_begin + warp; rr < r_end; rr += MT_THREADS / 32) {
+    Ray r;
+    {
+      const float4 ra = __ldg(a.ray_a + rr);           // same address in every lane: broadcast
+      const float2 rb = __ldg(reinterpret_cast<const float2 *>(a.ray_b + rr));
+      r.ox = ra.x; r.oy = ra.y; r.dx = ra.z; r.dy = ra.w; r.dz = rb.x; r.s_exit = rb.y;
+    }
     // band bounds, widened by 1e-6 so fast division can only walk more cells
     const float s_lo = fminf(__fdividef(zlo, r.dz) * (1.f - 1e-6f), r.s_exit);
     const float s_hi = fminf(__fdividef(zhi, r.dz) * (1.f + 1e-6f), r.s_exit);
     float B0 = s_lo, B1 = s_lo;                        // below both surfaces before s_lo
-    Recs R;
-    R.buf = recbuf + threadIdx.x;
-    R.stride = blockDim.x;
-    R.n[0] = R.n[1] = 0;
-    bool ovf = false;
-    int k0 = 0;
-    const int kend = __ldg(a.trav_off + rr + 1);
+    int n0 = 0, n1 = 0;
+    bool defer = false;
     if (s_lo < r.s_exit) {                             // warp-uniform
-      k0 = band_entry_warp(a.trav, __ldg(a.trav_off + rr), kend, s_lo);
-      trace_pair<32, !SMEMH>(g, r, a.trav, k0, kend, s_lo, s_hi, Hk, Gk, bd, B0, B1, R, ovf);
+      const int kend = __ldg(a.trav_off + rr + 1);
+      const int k0 = band_entry_warp(a.trav, __ldg(a.trav_off + rr), kend, s_lo);
+      float s = s_lo, za = s_lo * r.dz;
+      for (int k = k0; k < kend; k++) {
+        const int2 e = __ldg(a.trav + k);
+        const float s1 = __int_as_float(e.y);
+        const int i = e.x & 0xffff, j = e.x >> 16, base = i * ny + j;
+        const float zb = s1 * r.dz;
+        if (s1 > s) {
+          const float Ls = s1 - s;
+          cw_surface<0, NY>(g, r, H0, i, j, base, s, za, zb, Ls, bd.x, bd.y, B0, n0, defer, rec);
+          cw_surface<1, NY>(g, r, H0 + N * 32, i, j, base, s, za, zb, Ls, bd.z, bd.w, B1, n1, defer, rec);
+        }
+        if (s1 >= s_hi) break;
+        s = s1;
+        za = zb;
+      }
+    }
+    if (defer || n0 > RCAP || n1 > RCAP) {             // rare: the whole pair goes to k_trace_defer
+      const int q = atomicAdd(a.ovf_n, 1);
+      if (q < a.ovf_cap) a.ovf_q[q] = make_float4(__int_as_float(c), __int_as_float(rr), s_lo, s_hi);
+      continue;
     }
     if (MODE == TRACE_LL) {
+      const float2 rb = __ldg(reinterpret_cast<const float2 *>(a.ray_b + rr) + 1);
+      r.tb = rb.x; r.cnt = rb.y;
       float dldO;
       const float ll = epilogue(r, a.tc, B0, B1, dldO);
       if (act) {
         llacc += ll;
         const float f0 = dldO * a.tc.k0, f1 = dldO * a.tc.k1;
-        if (!ovf) scatter<32>(R, Gk, N, ny, f0, f1);
-        else rewalk_scatter<32, !SMEMH>(g, r, a.trav, k0, kend, s_lo, s_hi, Hk, Gk, bd, f0, f1);
+        float *G0 = a.G + (size_t)grp * 2 * N * 32 + lane;
+        const int oy = ny * 32;
+        for (int m = 0; m < n0; m++) {
+          const float4 q = rec[m * MT_THREADS];
+          const float w = f0 * q.w, u = q.y, v = q.z;
+          float *pg = G0 + __float_as_int(q.x) * 32;
+          atomicAdd(pg, w * (1.f - u) * (1.f - v));
+          atomicAdd(pg + oy, w * u * (1.f - v));
+          atomicAdd(pg + 32, w * (1.f - u) * v);
+          atomicAdd(pg + oy + 32, w * u * v);
+        }
+        float *G1 = G0 + N * 32;
+        for (int m = 0; m < n1; m++) {
+          const float4 q = rec[(RCAP + m) * MT_THREADS];
+          const float w = f1 * q.w, u = q.y, v = q.z;
+          float *pg = G1 + __float_as_int(q.x) * 32;
+          atomicAdd(pg, w * (1.f - u) * (1.f - v));
+          atomicAdd(pg + oy, w * u * (1.f - v));
+          atomicAdd(pg + 32, w * (1.f - u) * v);
+          atomicAdd(pg + oy + 32, w * u * v);
+        }
       }
     } else if (act) {
       const int64_t o = (int64_t)c * a.R + __ldg(a.perm + rr);
@@ -605,6 +697,69 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a
     }
   }
   if (MODE == TRACE_LL && act) atomicAdd(a.ll + c, (double)llacc);
+}
+
+// The chain x ray pairs the chain-lanes kernel deferred (an ill-conditioned
+// cell, or more than RCAP crossings of a surface): thread = pair.  The same
+// walk from the same s_lo with the same fp32 cell code, ill-conditioned cells
+// re-solved in place in fp64 (HP2 lever 1), then the epilogue and the adjoint
+// scatter (or the path-length export).  The last block resets the queue.
+template <int MODE>
+__global__ void __launch_bounds__(MT_THREADS) k_trace_defer(TraceArgs a) {
+  __shared__ float sgeo[4][MT_MAX_AXIS];
+  extern __shared__ __align__(16) float4 recs[];    // [2*RCAP][MT_THREADS]
+  load_geometry(a, sgeo[0], sgeo[1], sgeo[2], sgeo[3]);
+  __syncthreads();
+  const int n = *(volatile int *)a.ovf_n;
+  const int N = a.tc.N;
+  Geo g;
+  g.Xs = sgeo[0]; g.Ys = sgeo[1]; g.idx = sgeo[2]; g.idy = sgeo[3];
+  g.nx = a.tc.nx; g.ny = a.tc.ny; g.N = N;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < min(n, a.ovf_cap); q += gridDim.x * blockDim.x) {
+    const float4 e0 = a.ovf_q[q];
+    const int c = __float_as_int(e0.x), rr = __float_as_int(e0.y);
+    const float s_lo = e0.z, s_hi = e0.w;
+    const Ray r = load_ray(a.ray_a, a.ray_b, rr);
+    const size_t off = (size_t)(c >> 5) * 2 * N * 32 + (c & 31);
+    const float4 bd = a.band[c];
+    float B0 = s_lo, B1 = s_lo;
+    Recs R;
+    R.buf = recs + threadIdx.x;
+    R.stride = MT_THREADS;
+    R.n[0] = R.n[1] = 0;
+    bool ovf = false;
+    int k0 = 0;
+    const int kend = a.trav_off[rr + 1];
+    if (s_lo < r.s_exit) {
+      k0 = band_entry(a.trav, a.trav_off[rr], kend, s_lo);
+      trace_pair<32, true>(g, r, a.trav, k0, kend, s_lo, s_hi, a.H + off, nullptr, bd, B0, B1, R, ovf);
+    }
+    if (MODE == TRACE_LL) {
+      float dldO;
+      const float ll = epilogue(r, a.tc, B0, B1, dldO);
+      atomicAdd(a.ll + c, (double)ll);
+      const float f0 = dldO * a.tc.k0, f1 = dldO * a.tc.k1;
+      if (!ovf) scatter<32>(R, a.G + off, N, g.ny, f0, f1);
+      else rewalk_scatter<32, true>(g, r, a.trav, k0, kend, s_lo, s_hi, a.H + off, a.G + off, bd, f0, f1);
+    } else {
+      const int64_t o = (int64_t)c * a.R + a.perm[rr];
+      a.Lout[3 * o + 0] = B0;
+      a.Lout[3 * o + 1] = B1 - B0;
+      a.Lout[3 * o + 2] = r.s_exit - B1;
+      a.Oout[o] = a.tc.k0 * B0 + a.tc.k1 * B1 + a.obase[rr];
+    }
+  }
+  if (n > a.ovf_cap)   // queue overflow: fail loudly (non-finite log-likelihood -> status bit)
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.C; c += gridDim.x * blockDim.x)
+      a.ll[c] = __longlong_as_double(0x7ff8000000000000ll);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(a.ovf_done, 1) == (int)gridDim.x - 1) {
+      *a.ovf_n = 0;
+      *a.ovf_done = 0;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -708,6 +863,7 @@ static TraceArgs base_trace_args(mt_problem *p) {
   a.ray_a = p->d_ray_a; a.ray_b = p->d_ray_b; a.obase = p->d_obase;
   a.trav_off = p->d_trav_off; a.trav = p->d_trav; a.perm = p->d_perm;
   a.R = p->R;
+  a.ovf_q = p->d_ovf_q; a.ovf_n = p->d_ovf_n; a.ovf_done = p->d_ovf_n + 1; a.ovf_cap = p->ovf_cap;
   return a;
 }
 
@@ -756,21 +912,24 @@ static cudaError_t set_smem(Kern k, size_t smem, size_t *done) {
   return cudaSuccess;
 }
 
-template <int MODE, bool SMEMH>
+template <int MODE, int NY>
 static cudaError_t launch_cl(const TraceArgs &a, dim3 grid, size_t smem, cudaStream_t s) {
   static size_t done[16] = {0};
-  cudaError_t e = set_smem(k_trace_cl<MODE, SMEMH>, smem, done);
+  cudaError_t e = set_smem(k_trace_cl<MODE, NY>, smem, done);
   if (e != cudaSuccess) return e;
-  if (MT_CARVEOUT >= 0) {
-    static bool once = false;
-    if (!once) {
-      cudaFuncSetAttribute(k_trace_cl<MODE, SMEMH>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                           MT_CARVEOUT);
-      once = true;
-    }
-  }
-  k_trace_cl<MODE, SMEMH><<<grid, MT_THREADS, smem, s>>>(a);
+  k_trace_cl<MODE, NY><<<grid, MT_THREADS, smem, s>>>(a);
   return cudaGetLastError();
+}
+
+template <int MODE>
+static cudaError_t launch_cl_ny(const TraceArgs &a, int ny, dim3 grid, size_t smem, cudaStream_t s) {
+  switch (ny) {
+    case 8: return launch_cl<MODE, 8>(a, grid, smem, s);
+    case 16: return launch_cl<MODE, 16>(a, grid, smem, s);
+    case 32: return launch_cl<MODE, 32>(a, grid, smem, s);
+    case 64: return launch_cl<MODE, 64>(a, grid, smem, s);
+    default: return launch_cl<MODE, 0>(a, grid, smem, s);
+  }
 }
 
 template <int K, int MODE>
@@ -812,20 +971,23 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
   if (rec) cudaEventRecord(p->ev_a[p->n_rec], s);
   if (chain_lanes) {
     int groups = (C + 31) / 32;
-    size_t tile = (size_t)4 * 2 * p->N * 32;
-    bool smemh = tile <= (size_t)p->smemh_limit;
     // small ray chunks (~512 rays = 64 per warp): compact, L1-friendly regions per
-    // block and many waves for load balance (measured: 13.2 ms -> 10.3 ms, Medium)
+    // block and many waves for load balance
     int64_t S = p->trace_s > 0 ? p->trace_s
                                : std::max(pick_splits(p, groups, 2), (p->R + 511) / 512);
     a.rays_per_block = (p->R + S - 1) / S;
     S = (p->R + a.rays_per_block - 1) / a.rays_per_block;
     dim3 grid((unsigned)S, (unsigned)groups);
-    size_t smem = (size_t)4 * geo_words + (smemh ? tile : 0) + (size_t)16 * 2 * RCAP * MT_THREADS;
-    if (mode == TRACE_LL) e = smemh ? launch_cl<TRACE_LL, true>(a, grid, smem, s)
-                                    : launch_cl<TRACE_LL, false>(a, grid, smem, s);
-    else e = smemh ? launch_cl<TRACE_PATH, true>(a, grid, smem, s)
-                   : launch_cl<TRACE_PATH, false>(a, grid, smem, s);
+    size_t smem = (size_t)16 * 2 * RCAP * MT_THREADS;   // crossing records (geometry is static)
+    e = mode == TRACE_LL ? launch_cl_ny<TRACE_LL>(a, p->ny, grid, smem, s)
+                         : launch_cl_ny<TRACE_PATH>(a, p->ny, grid, smem, s);
+    if (e == cudaSuccess) {   // deferred pairs (ill-conditioned or > RCAP crossings)
+      const size_t dsm = (size_t)16 * 2 * RCAP * MT_THREADS;
+      if (mode == TRACE_LL) k_trace_defer<TRACE_LL><<<2 * p->num_sms, MT_THREADS, dsm, s>>>(a);
+      else k_trace_defer<TRACE_PATH><<<2 * p->num_sms, MT_THREADS, dsm, s>>>(a);
+      e = cudaGetLastError();
+      p->all_launches++;
+    }
   } else {
     int K = pick_k(p, C);
     int groups = (C + K - 1) / K;
