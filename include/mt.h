@@ -197,6 +197,14 @@ int mt_timing_start(mt_problem *p, int32_t max_records);
 int mt_timing_read(mt_problem *p, double *trace_ms, int64_t *trace_launches, double *pairs,
                    int64_t *all_launches);
 
+/* Trace work counters since mt_problem_create (synchronous; debugging and
+ * bench reporting): `deferred` = chain x ray pairs the chain-lanes trace
+ * kernel handed to its fp64 follow-up kernel (an ill-conditioned crossing,
+ * SURVEY HP2, or more than 4 crossings of one surface); `defer_ms` = device
+ * time of those follow-up launches while timing is on (mt_timing_start), also
+ * included in mt_timing_read's trace_ms.  NULL outputs are skipped. */
+int mt_trace_counters(mt_problem *p, int64_t *deferred, double *defer_ms);
+
 /* FP32 FFMA throughput microbenchmark on `device` (TFLOP/s, FMA = 2 flops). */
 int mt_measure_fp32_peak(int32_t device, double *tflops, double *sm_clock_mhz);
 

@@ -42,7 +42,8 @@ EXPORTS = [
     "mt_problem_create", "mt_problem_destroy", "mt_num_params", "mt_num_rays", "mt_loglik_offset",
     "mt_prior_constants", "mt_logpost_grad", "mt_leapfrog", "mt_draw_momenta", "mt_hmc_step",
     "mt_stats_update", "mt_rhat_partials", "mt_heights", "mt_loglik_heights", "mt_path_lengths", "mt_debug_traversal", "mt_philox",
-    "mt_philox_curand", "mt_timing_start", "mt_timing_read", "mt_measure_fp32_peak", "mt_last_error",
+    "mt_philox_curand", "mt_timing_start", "mt_timing_read", "mt_trace_counters", "mt_measure_fp32_peak",
+    "mt_last_error",
 ]
 
 _lib = None
@@ -76,6 +77,7 @@ def lib():
             "mt_philox_curand": ([vp, u32, u32, vp, i64, vp], ct.c_int),
             "mt_timing_start": ([vp, i32], ct.c_int),
             "mt_timing_read": ([vp, vp, vp, vp, vp], ct.c_int),
+            "mt_trace_counters": ([vp, vp, vp], ct.c_int),
             "mt_measure_fp32_peak": ([i32, vp, vp], ct.c_int),
             "mt_last_error": ([], ct.c_char_p),
         }
@@ -292,6 +294,13 @@ class Problem:
         _check(lib().mt_timing_read(self.h, ct.byref(ms), ct.byref(n), ct.byref(pairs), ct.byref(alln)),
                "mt_timing_read")
         return dict(trace_ms=ms.value, trace_launches=n.value, pairs=pairs.value, all_launches=alln.value)
+
+    def trace_counters(self):
+        """Cumulative deferred chain x ray pairs (fp64 follow-up kernel) and the
+        device time of the follow-up launches in the last timed region (ms)."""
+        n, ms = ct.c_int64(), ct.c_double()
+        _check(lib().mt_trace_counters(self.h, ct.byref(n), ct.byref(ms)), "mt_trace_counters")
+        return dict(deferred=n.value, defer_ms=ms.value)
 
 
 def philox(ctr, key, use_curand: bool = False, stream=None):

@@ -79,12 +79,13 @@ int check_chains(const mt_problem *p, int32_t C) {
 }
 
 void free_all(mt_problem *p) {
-  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_ovf_q, p->d_ovf_n, p->d_H, p->d_G,
+  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_trav_geo, p->d_ovf_q, p->d_ovf_n, p->d_H, p->d_G,
                   p->d_band, p->d_ll, p->d_x0, p->d_g0, p->d_mom, p->d_kin0, p->d_kin1, p->d_lp0};
   for (void *b : bufs)
     if (b) cudaFree(b);
   for (auto e : p->ev_a) cudaEventDestroy(e);
   for (auto e : p->ev_b) cudaEventDestroy(e);
+  for (auto e : p->ev_m) cudaEventDestroy(e);
 }
 
 }  // namespace
@@ -248,7 +249,7 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   ALLOC(p->d_kin1, sizeof(float) * MC);
   ALLOC(p->d_lp0, sizeof(double) * MC);
   ALLOC(p->d_ovf_q, sizeof(float4) * (size_t)p->ovf_cap);
-  ALLOC(p->d_ovf_n, sizeof(int) * 2);
+  ALLOC(p->d_ovf_n, sizeof(int) * 4);
 #undef ALLOC
   if (e != cudaSuccess) {
     free_all(p);
@@ -265,7 +266,7 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   if (e == cudaSuccess) e = cudaMemset(p->d_G, 0, sizeof(float) * MC32 * P);
   if (e == cudaSuccess) e = cudaMemset(p->d_H, 0, sizeof(float) * MC32 * P);
   if (e == cudaSuccess) e = cudaMemset(p->d_ll, 0, sizeof(double) * MC);
-  if (e == cudaSuccess) e = cudaMemset(p->d_ovf_n, 0, sizeof(int) * 2);
+  if (e == cudaSuccess) e = cudaMemset(p->d_ovf_n, 0, sizeof(int) * 4);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e == cudaSuccess) e = build_traversal(p);   // a2, once per problem (exact predicates)
   if (e != cudaSuccess) {
@@ -463,8 +464,8 @@ int mt_debug_traversal(mt_problem *p, int64_t ray, int32_t *ij, float *s_in, flo
     CK(cudaMemcpy(cells.data(), p->d_trav + off[0], sizeof(int2) * m, cudaMemcpyDeviceToHost));
     float prev = 0.f;
     for (int k = 0; k < m; k++) {
-      ij[2 * k] = cells[k].x & 0xffff;
-      ij[2 * k + 1] = cells[k].x >> 16;
+      ij[2 * k] = cell_i(cells[k].x);
+      ij[2 * k + 1] = cell_j(cells[k].x);
       float so;
       memcpy(&so, &cells[k].y, sizeof so);
       s_in[k] = prev;
@@ -493,11 +494,13 @@ int mt_timing_start(mt_problem *p, int32_t max_records) {
   if (!p || max_records < 0) return set_err(MT_EINVAL, "bad timing arguments");
   DevGuard g(p->device);
   while ((int)p->ev_a.size() < max_records) {
-    cudaEvent_t a, b;
+    cudaEvent_t a, b, m;
     CK(cudaEventCreate(&a));
     CK(cudaEventCreate(&b));
+    CK(cudaEventCreate(&m));
     p->ev_a.push_back(a);
     p->ev_b.push_back(b);
+    p->ev_m.push_back(m);
   }
   p->n_rec = 0;
   p->trace_launches = 0;
@@ -511,18 +514,34 @@ int mt_timing_read(mt_problem *p, double *trace_ms, int64_t *trace_launches, dou
                    int64_t *all_launches) {
   if (!p) return set_err(MT_EINVAL, "problem is NULL");
   DevGuard g(p->device);
-  double tot = 0;
+  double tot = 0, def = 0;
   for (int k = 0; k < p->n_rec; k++) {
     CK(cudaEventSynchronize(p->ev_b[k]));
-    float ms = 0;
+    float ms = 0, md = 0;
     CK(cudaEventElapsedTime(&ms, p->ev_a[k], p->ev_b[k]));
+    CK(cudaEventElapsedTime(&md, p->ev_m[k], p->ev_b[k]));
     tot += ms;
+    def += md;
   }
+  p->defer_ms = def;
   if (trace_ms) *trace_ms = tot;
   if (trace_launches) *trace_launches = p->trace_launches;
   if (pairs) *pairs = p->pairs;
   if (all_launches) *all_launches = p->all_launches;
   p->timing = false;
+  return MT_OK;
+}
+
+int mt_trace_counters(mt_problem *p, int64_t *deferred, double *defer_ms) {
+  if (!p) return set_err(MT_EINVAL, "problem is NULL");
+  DevGuard g(p->device);
+  if (deferred) {
+    unsigned long long v = 0;
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(&v, p->d_ovf_n + 2, sizeof v, cudaMemcpyDeviceToHost));
+    *deferred = (int64_t)v;
+  }
+  if (defer_ms) *defer_ms = p->defer_ms;
   return MT_OK;
 }
 

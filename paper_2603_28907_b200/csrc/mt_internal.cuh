@@ -20,6 +20,16 @@ __host__ __device__ __forceinline__ size_t tix(int c, int l, int k, int N) {
   return ((size_t)(c >> 5) * 2 * N + (size_t)l * N + k) * 32 + (c & 31);
 }
 
+// Stored traversal cell word: the node offset (i n_y + j)·32 of the cell's
+// (i, j) corner in the chain-interleaved layout (bits 0-16; N <= 4096), i
+// (bits 17-23) and j (bits 24-30); MT_MAX_AXIS = 128.
+__host__ __device__ __forceinline__ int cell_pack(int i, int j, int ny) {
+  return ((i * ny + j) << 5) | (i << 17) | (j << 24);
+}
+__host__ __device__ __forceinline__ unsigned cell_off32(int w) { return (unsigned)w & 0x1ffffu; }
+__host__ __device__ __forceinline__ int cell_i(int w) { return (w >> 17) & 127; }
+__host__ __device__ __forceinline__ int cell_j(int w) { return (w >> 24) & 127; }
+
 // Per-problem constants every trace launch needs (passed by value).
 struct TraceConsts {
   int nx, ny, N;     // nodes per axis, nodes per surface
@@ -39,7 +49,8 @@ struct TraceArgs {
   const float4 *ray_a, *ray_b;
   const float *obase;           // ρ_rock s_exit + ρ_ext L_ext (path-length export only)
   const int32_t *trav_off;      // [R+1] CSR offsets of each ray's stored traversal
-  const int2 *trav;             // {i | j << 16, s_out bits} per cell, in ray order (a2)
+  const int2 *trav;             // {cell_pack(i, j), s_out bits} per cell, in ray order (a2)
+  const float4 *trav_geo;       // per cell {u, v, α, β} at its entry (cell-local coordinates, a0)
   const int32_t *perm;          // internal ray index -> caller's ray index
   int64_t R;                    // rays in the shard
   int64_t rays_per_block;
@@ -51,6 +62,7 @@ struct TraceArgs {
   float *Lout, *Oout;           // path-length export: [C][R][3], [C][R]
   float4 *ovf_q;                // chain lanes: deferred pairs {c, ray, s_lo, s_hi} (an ill-
   int *ovf_n, *ovf_done;        //   conditioned cell or > RCAP crossings), done by k_trace_defer
+  unsigned long long *ovf_total;   // cumulative deferred pairs
   int ovf_cap;
 };
 
@@ -97,8 +109,9 @@ struct mt_problem {
   int32_t *d_perm = nullptr;
   std::vector<int32_t> perm, inv_perm;   // internal <-> caller ray order (host)
   int2 *d_trav = nullptr;
+  float4 *d_trav_geo = nullptr;
   float4 *d_ovf_q = nullptr;    // deferred-pair queue of the chain-lanes trace (see TraceArgs)
-  int *d_ovf_n = nullptr;       // [2]: count, blocks done
+  int *d_ovf_n = nullptr;       // [4]: count, blocks done, 64-bit cumulative count
   int ovf_cap = 1 << 22;
   int64_t trav_cells = 0;
   float *d_H = nullptr, *d_G = nullptr;
@@ -113,8 +126,9 @@ struct mt_problem {
   int smemh_limit = 100 * 1024; // stage a 32-chain height tile in smem when it fits
   // measurement
   bool timing = false;
-  std::vector<cudaEvent_t> ev_a, ev_b;
+  std::vector<cudaEvent_t> ev_a, ev_b, ev_m;   // trace start, end, main-kernel end
   int n_rec = 0;
+  double defer_ms = 0;
   int64_t trace_launches = 0, all_launches = 0;
   double pairs = 0;
 };

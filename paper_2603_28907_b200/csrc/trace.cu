@@ -29,8 +29,14 @@
 
 namespace {
 
-constexpr float GTHR = 0.1f;    // |g'| below which a crossing is re-solved in fp64
-constexpr float ZTHR = 1e-3f;   // near-tangent band (m) re-solved in fp64
+#ifndef MT_GTHR
+#define MT_GTHR 0.05f
+#endif
+#ifndef MT_ZTHR
+#define MT_ZTHR 1e-3f
+#endif
+constexpr float GTHR = MT_GTHR;   // |g'| below which a crossing is re-solved in fp64
+constexpr float ZTHR = MT_ZTHR;   // near-tangent band (m) re-solved in fp64
 
 // sign(a*b - c*d) for a, c >= 0 and b, d > 0, EXACTLY: operands are fp32 values
 // with <= 24 significant bits, so the products are exact in fp64.  A filtered
@@ -160,100 +166,38 @@ __device__ __forceinline__ CellSol<T> classify(T g0, T g1, T g2, T L, T t1, T t2
   return o;
 }
 
-// fp64 re-solve from the same fp32 inputs, exact cell spacing (HP2 lever 1).
-__device__ __forceinline__ CellSol<double> solve_cell_f64(float h00, float h10, float h01, float h11,
-                                                       float Xi, float Xi1, float Yj, float Yj1,
-                                                       const Ray &r, float s, float s1,
-                                                       double &u0, double &v0, double &al,
-                                                       double &be) {
-  double ix = 1.0 / ((double)Xi1 - (double)Xi), iy = 1.0 / ((double)Yj1 - (double)Yj);
-  u0 = ((double)r.ox + (double)s * (double)r.dx - (double)Xi) * ix;
-  v0 = ((double)r.oy + (double)s * (double)r.dy - (double)Yj) * iy;
-  double z0 = (double)s * (double)r.dz;
-  al = (double)r.dx * ix;
-  be = (double)r.dy * iy;
-  double b = (double)h10 - h00, c = (double)h01 - h00, e = ((double)h11 - h10) - ((double)h01 - h00);
-  double g0 = ((double)h00 - z0) + u0 * (b + e * v0) + c * v0;
-  double g1 = b * al + c * be + e * (u0 * be + v0 * al) - (double)r.dz;
-  double g2 = e * al * be;
-  double L = (double)s1 - (double)s;
-  double disc = g1 * g1 - 4.0 * g2 * g0, t1 = 0, t2 = 0;
-  bool two = disc > 0.0;
-  if (two) {
-    double q = -0.5 * (g1 + (g1 >= 0.0 ? sqrt(disc) : -sqrt(disc)));
-    t1 = q / g2;   // ±inf when g2 = 0: out of range
-    t2 = g0 / q;
-  }
-  return classify<double>(g0, g1, g2, L, t1, t2, two);
-}
-
-struct Geo {
-  const float *Xs, *Ys, *idx, *idy;
-  int nx, ny, N;
-};
-
-// Crossing records of one chain x ray: up to RCAP per surface, kept in shared
-// memory at slot [(l*RCAP + m)*blockDim + tid] (conflict-free: consecutive
-// threads, consecutive words); more set the overflow flag (handled by a
-// scattering re-walk).
-#ifndef MT_RCAP
-#define MT_RCAP 4
-#endif
-#ifndef MT_CL_MINB
-#define MT_CL_MINB 4
-#endif
-#ifndef MT_CARVEOUT
-#define MT_CARVEOUT -1
-#endif
-constexpr int RCAP = MT_RCAP;
-struct Recs {
-  float4 *buf;   // {base bits, u, v, 1/|g'|}
-  int stride;    // blockDim.x
-  int n[2];
-};
-
-template <int L>
-__device__ __forceinline__ void rec_push(Recs &R, bool &ovf, int base, float u, float v, float ig) {
-  if (R.n[L] < RCAP) R.buf[(L * RCAP + R.n[L]) * R.stride] = make_float4(__int_as_float(base), u, v, ig);
-  else ovf = true;
-  R.n[L]++;
-}
-
-template <int STRIDE, bool LDG>
-__device__ __forceinline__ void load4(const float *Hl, int base, int ny, float &h00, float &h10,
-                                      float &h01, float &h11) {
-  const float *p = Hl + base * STRIDE;   // one address; the other corners are fixed offsets
-  const int oy = ny * STRIDE;
-  if (LDG) {
-    h00 = __ldg(p); h10 = __ldg(p + oy); h01 = __ldg(p + STRIDE); h11 = __ldg(p + oy + STRIDE);
-  } else {
-    h00 = p[0]; h10 = p[oy]; h01 = p[STRIDE]; h11 = p[oy + STRIDE];
-  }
-}
-
-__device__ __forceinline__ void scatter4(float *Gl, int STRIDE, int base, int ny, float w, float u,
-                                         float v) {
-  atomicAdd(Gl + base * STRIDE, w * (1.f - u) * (1.f - v));
-  atomicAdd(Gl + (base + ny) * STRIDE, w * u * (1.f - v));
-  atomicAdd(Gl + (base + 1) * STRIDE, w * (1.f - u) * v);
-  atomicAdd(Gl + (base + ny + 1) * STRIDE, w * u * v);
-}
-
-// fp64 re-solve of one ill-conditioned cell (HP2 lever 1): same fp32 inputs,
-// exact cell spacing, oracle-style midpoint classification.  Rare; noinline so
-// its double-precision registers stay out of the hot loop.  Everything is
-// passed and returned BY VALUE: a reference to a caller's accumulator would
-// make it address-taken and pin it to local memory for the whole loop.
+// fp64 re-solve of one cell from the same fp32 inputs, exact cell spacing
+// (HP2 lever 1), with the oracle-style midpoint classification.  Rare;
+// noinline so its double-precision registers stay out of the callers' loops,
+// and everything is passed and returned BY VALUE (a reference to a caller's
+// accumulator would pin it to local memory).
 struct Fix {
   float below;
-  int n, base;
+  int n;
   float u[2], v[2], ig[2];
 };
 
 __device__ __noinline__ Fix fix64(float h00, float h10, float h01, float h11, float Xi, float Xi1,
                                   float Yj, float Yj1, Ray r, float s, float s1) {
-  double u0, v0, al, be;
-  CellSol<double> sd = solve_cell_f64(h00, h10, h01, h11, Xi, Xi1, Yj, Yj1, r, s, s1, u0, v0, al, be);
+  const double ix = 1.0 / ((double)Xi1 - (double)Xi), iy = 1.0 / ((double)Yj1 - (double)Yj);
+  const double u0 = ((double)r.ox + (double)s * (double)r.dx - (double)Xi) * ix;
+  const double v0 = ((double)r.oy + (double)s * (double)r.dy - (double)Yj) * iy;
+  const double z0 = (double)s * (double)r.dz;
+  const double al = (double)r.dx * ix, be = (double)r.dy * iy;
+  const double b = (double)h10 - h00, c = (double)h01 - h00, e = ((double)h11 - h10) - ((double)h01 - h00);
+  const double g0 = ((double)h00 - z0) + u0 * (b + e * v0) + c * v0;
+  const double g1 = b * al + c * be + e * (u0 * be + v0 * al) - (double)r.dz;
+  const double g2 = e * al * be;
+  const double L = (double)s1 - (double)s;
+  const double disc = g1 * g1 - 4.0 * g2 * g0;
+  double t1 = 0, t2 = 0;
+  const bool two = disc > 0.0;
+  if (two) {
+    const double q = -0.5 * (g1 + (g1 >= 0.0 ? sqrt(disc) : -sqrt(disc)));
+    t1 = q / g2;   // ±inf when g2 = 0: out of range
+    t2 = g0 / q;
+  }
+  const CellSol<double> sd = classify<double>(g0, g1, g2, L, t1, t2, two);
   Fix x;
   x.below = (float)sd.below;
   x.n = sd.n;
@@ -265,255 +209,23 @@ __device__ __noinline__ Fix fix64(float h00, float h10, float h01, float h11, fl
   return x;
 }
 
-template <int L, int STRIDE, bool SCAT>
-__device__ __forceinline__ void apply_fix64(const Geo &g, const Ray &r, float *Gl, int base, int i,
-                                            int j, float s, float s1, float h00, float h10,
-                                            float h01, float h11, float &B, Recs &R, bool &ovf,
-                                            float f) {
-  const Fix x = fix64(h00, h10, h01, h11, g.Xs[i], g.Xs[i + 1], g.Ys[j], g.Ys[j + 1], r, s, s1);
-  B += x.below;
-  for (int k = 0; k < x.n; k++) {
-    if (SCAT) scatter4(Gl, STRIDE, base, g.ny, f * x.ig[k], x.u[k], x.v[k]);
-    else rec_push<L>(R, ovf, base, x.u[k], x.v[k], x.ig[k]);
-  }
-}
-
-// One cell [s, s1] of surface L for one chain, fp32 (a3).  g(τ) = h(u0+ατ,
-// v0+βτ) - d_z(s+τ) = g0 + g1 τ + g2 τ² (R2).  With g(0) and g(Δs) of
+// One surface over one cell piece [s, s1] of a ray, fp32 (a3).  In cell-local
+// coordinates u = (x - X_i)/ΔX_i, v = (y - Y_j)/ΔY_j the ray is (u0 + α τ,
+// v0 + β τ) for τ ∈ [0, Δs] (cg = {u0, v0, α, β}, from the stored per-cell
+// geometry, a0) and the bilinear surface h = a + b u + c v + e u v (R2), so
+// g(τ) = h - d_z (s + τ) = g0 + g1 τ + g2 τ².  With g(0) and g(Δs) of
 // different sign there is exactly one crossing; with equal signs there are
 // two iff the vertex lies inside and g(vertex) = -disc/(4 g2) has the other
-// sign.  Ill-conditioned cells (|g'| < GTHR at a crossing, or a near-tangent
-// vertex) set `redo`: the chain x ray is then re-traced in fp64.
-template <int L, int STRIDE, bool LDG, bool SCAT>
-__device__ __forceinline__ void cell32(const Geo &g, const Ray &r, const float *Hl, float *Gl,
-                                       int i, int j, float s, float s1, float zmin, float zmax,
-                                       float &B, Recs &R, bool &ovf, bool &redo, float f) {
-  const float za = s * r.dz, zb = s1 * r.dz, Ls = s1 - s;
-  if (zb <= zmin) { B += Ls; return; }          // below the surface's lowest node
-  if (za >= zmax) return;                       // above its highest node
-  const int base = i * g.ny + j;
-  float h00, h10, h01, h11;
-  load4<STRIDE, LDG>(Hl, base, g.ny, h00, h10, h01, h11);
-  if (zb <= fminf(fminf(h00, h10), fminf(h01, h11))) { B += Ls; return; }  // bilinear min at a corner
-  if (za >= fmaxf(fmaxf(h00, h10), fmaxf(h01, h11))) return;
-  const float idx = g.idx[i], idy = g.idy[j];
-  const float u0 = (fmaf(s, r.dx, r.ox) - g.Xs[i]) * idx;
-  const float v0 = (fmaf(s, r.dy, r.oy) - g.Ys[j]) * idy;
-  const float al = r.dx * idx, be = r.dy * idy;
+// sign.  Adds the below-surface length to B, calls emit(u_c, v_c, 1/|g'|)
+// per crossing, and returns false (adding nothing) for an ill-conditioned
+// cell: |g'| < GTHR at a crossing or a near-tangent vertex (HP2).
+template <class Emit>
+__device__ __forceinline__ bool solve32(float h00, float h10, float h01, float h11, float4 cg,
+                                        float za, float Ls, float dz, float &B, Emit &&emit) {
+  const float u0 = cg.x, v0 = cg.y, al = cg.z, be = cg.w;
   const float b = h10 - h00, c = h01 - h00, e = (h11 - h10) - (h01 - h00);
   const float g0 = (h00 - za) + u0 * (b + e * v0) + c * v0;
-  const float g1 = b * al + c * be + e * (u0 * be + v0 * al) - r.dz;
-  const float g2 = e * al * be;
-  const float gL = g0 + Ls * (g1 + Ls * g2);
-  const float disc = fmaf(g1, g1, -4.f * g2 * g0);
-  const bool p0 = g0 > 0.f;
-  const float a2 = 2.f * g2;
-  const bool vin = -g1 * a2 > 0.f && fabsf(g1) < Ls * fabsf(a2);   // vertex inside (0, Δs)
-  float q = 0.f;
-  if (disc > 0.f) q = -0.5f * (g1 + copysignf(disc * rsqrtf(disc), g1));
-  float ta = __fdividef(g0, q), tb = __fdividef(q, g2);             // the two roots (tb = ±inf if g2 = 0)
-  if (p0 != (gL > 0.f)) {                       // exactly one crossing
-    float t = (ta > 0.f && ta < Ls) ? ta : tb;
-    t = fminf(fmaxf(t, 0.f), Ls);
-    const float gp = g1 + a2 * t;
-    if (fabsf(gp) < GTHR || !(disc > 0.f)) { apply_fix64<L, STRIDE, SCAT>(g, r, Gl, base, i, j, s, s1, h00, h10, h01, h11, B, R, ovf, f); return; }
-    B += p0 ? t : Ls - t;
-    const float ig = __frcp_rn(fabsf(gp)), uc = u0 + al * t, vc = v0 + be * t;
-    if (SCAT) scatter4(Gl, STRIDE, base, g.ny, f * ig, uc, vc);
-    else rec_push<L>(R, ovf, base, uc, vc, ig);
-  } else if (disc > 0.f && vin && ((g2 > 0.f) == p0)) {   // two crossings
-    float t1 = fminf(ta, tb), t2 = fmaxf(ta, tb);
-    const float gp1 = g1 + a2 * t1, gp2 = g1 + a2 * t2;
-    if (fabsf(gp1) < GTHR || fabsf(gp2) < GTHR) { apply_fix64<L, STRIDE, SCAT>(g, r, Gl, base, i, j, s, s1, h00, h10, h01, h11, B, R, ovf, f); return; }
-    B += p0 ? Ls - (t2 - t1) : (t2 - t1);
-    const float ig1 = __frcp_rn(fabsf(gp1)), ig2 = __frcp_rn(fabsf(gp2));
-    if (SCAT) {
-      scatter4(Gl, STRIDE, base, g.ny, f * ig1, u0 + al * t1, v0 + be * t1);
-      scatter4(Gl, STRIDE, base, g.ny, f * ig2, u0 + al * t2, v0 + be * t2);
-    } else {
-      rec_push<L>(R, ovf, base, u0 + al * t1, v0 + be * t1, ig1);
-      rec_push<L>(R, ovf, base, u0 + al * t2, v0 + be * t2, ig2);
-    }
-  } else {                                      // no crossing
-    if (vin && fabsf(disc) < 2.f * fabsf(a2) * ZTHR) { apply_fix64<L, STRIDE, SCAT>(g, r, Gl, base, i, j, s, s1, h00, h10, h01, h11, B, R, ovf, f); return; }  // near-tangent
-    if (p0) B += Ls;
-  }
-}
-
-// The same cell entirely in fp64 from the same fp32 inputs (HP2 lever 1), with
-// the oracle-style midpoint classification.
-template <int L, int STRIDE, bool LDG, bool SCAT>
-__device__ __forceinline__ void cell64(const Geo &g, const Ray &r, const float *Hl, float *Gl,
-                                       int i, int j, float s, float s1, float zmin, float zmax,
-                                       float &B, Recs &R, bool &ovf, float f) {
-  const float za = s * r.dz, zb = s1 * r.dz;
-  if (zb <= zmin) { B += s1 - s; return; }
-  if (za >= zmax) return;
-  const int base = i * g.ny + j;
-  float h00, h10, h01, h11;
-  load4<STRIDE, LDG>(Hl, base, g.ny, h00, h10, h01, h11);
-  if (zb <= fminf(fminf(h00, h10), fminf(h01, h11))) { B += s1 - s; return; }
-  if (za >= fmaxf(fmaxf(h00, h10), fmaxf(h01, h11))) return;
-  double u0, v0, al, be;
-  CellSol<double> sd = solve_cell_f64(h00, h10, h01, h11, g.Xs[i], g.Xs[i + 1], g.Ys[j],
-                                      g.Ys[j + 1], r, s, s1, u0, v0, al, be);
-  B += (float)sd.below;
-  for (int k = 0; k < sd.n; k++) {
-    float uc = (float)(u0 + al * sd.tc[k]), vc = (float)(v0 + be * sd.tc[k]);
-    float ig = (float)(1.0 / fabs(sd.gp[k]));
-    if (SCAT) scatter4(Gl, STRIDE, base, g.ny, f * ig, uc, vc);
-    else rec_push<L>(R, ovf, base, uc, vc, ig);
-  }
-}
-
-// First stored cell of the ray whose s_out exceeds s (binary search; the last
-// cell's s_out is s_exit > s).
-__device__ __forceinline__ int band_entry(const int2 *__restrict__ cells, int lo, int hi, float s) {
-  hi -= 1;
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (__int_as_float(__ldg(&cells[mid].y)) > s) hi = mid;
-    else lo = mid + 1;
-  }
-  return lo;
-}
-
-// Same, warp-cooperative (chain lanes, all 32 lanes converged, uniform
-// arguments): one coalesced load of 32 cells and a ballot per round.
-__device__ __forceinline__ int band_entry_warp(const int2 *__restrict__ cells, int lo, int hi, float s) {
-  const int lane = threadIdx.x & 31;
-  for (int b = lo; b < hi; b += 32) {
-    const int k = b + lane;
-    const bool gt = k < hi && __int_as_float(__ldg(&cells[k].y)) > s;
-    const unsigned m = __ballot_sync(0xffffffffu, gt);
-    if (m) return b + __ffs(m) - 1;
-  }
-  return hi - 1;
-}
-
-// Walk the stored cells from index k (containing s0) until s_hi, both surfaces.
-// F64: every straddling cell in fp64 (re-trace of an ill-conditioned chain x ray).
-template <int STRIDE, bool LDG, bool SCAT, bool F64>
-__device__ __forceinline__ void walk(const Geo &g, const Ray &r, const int2 *__restrict__ cells,
-                                     int k, int kend, float s0, float s_hi, const float *Hk,
-                                     float *Gk, float4 bd, float &B0, float &B1, Recs &R,
-                                     bool &ovf, bool &redo, float f0, float f1) {
-  float s = s0;
-  const int sN = g.N * STRIDE;
-  for (; k < kend; k++) {
-    const int2 e = __ldg(cells + k);
-    const float s1 = __int_as_float(e.y);
-    const int i = e.x & 0xffff, j = e.x >> 16;
-    if (s1 > s) {
-      if (F64) {
-        cell64<0, STRIDE, LDG, SCAT>(g, r, Hk, Gk, i, j, s, s1, bd.x, bd.y, B0, R, ovf, f0);
-        cell64<1, STRIDE, LDG, SCAT>(g, r, Hk + sN, Gk + sN, i, j, s, s1, bd.z, bd.w, B1, R, ovf, f1);
-      } else {
-        cell32<0, STRIDE, LDG, SCAT>(g, r, Hk, Gk, i, j, s, s1, bd.x, bd.y, B0, R, ovf, redo, f0);
-        cell32<1, STRIDE, LDG, SCAT>(g, r, Hk + sN, Gk + sN, i, j, s, s1, bd.z, bd.w, B1, R, ovf,
-                                     redo, f1);
-      }
-    }
-    if (s1 >= s_hi) break;
-    s = s1;
-  }
-}
-
-// Scatter recorded crossings: G_l[node] += f_l · φ_node(u, v)/|g'|  (a6).
-template <int STRIDE>
-__device__ __forceinline__ void scatter(const Recs &R, float *Gk, int N, int ny, float f0, float f1) {
-#pragma unroll
-  for (int l = 0; l < 2; l++) {
-    for (int m = 0; m < R.n[l]; m++) {
-      const float4 q = R.buf[(l * RCAP + m) * R.stride];
-      scatter4(Gk + l * N * STRIDE, STRIDE, __float_as_int(q.x), ny, (l ? f1 : f0) * q.w, q.y, q.z);
-    }
-  }
-}
-
-// Trace one chain x ray from the band entry: fp32 with deferred fp64 re-trace
-// (redo) and the overflow re-walk, returning B0, B1 and the crossing records.
-template <int STRIDE, bool LDG>
-__device__ __forceinline__ void trace_pair(const Geo &g, const Ray &r, const int2 *__restrict__ cells,
-                                           int k0, int kend, float s_lo, float s_hi,
-                                           const float *Hk, float *Gk, float4 bd, float &B0,
-                                           float &B1, Recs &R, bool &ovf) {
-  bool redo = false;   // unused: ill-conditioned cells are re-solved in place (fix64)
-  R.n[0] = R.n[1] = 0;
-  walk<STRIDE, LDG, false, false>(g, r, cells, k0, kend, s_lo, s_hi, Hk, Gk, bd, B0, B1, R, ovf,
-                                  redo, 0.f, 0.f);
-}
-
-// Overflow (more than RCAP crossings of one surface): scatter every crossing of
-// the chain x ray directly, through the same fp32 cell code (and its fp64
-// fixes) as the recording walk, so the crossings are identical.
-template <int STRIDE, bool LDG>
-__device__ __noinline__ void rewalk_scatter(const Geo g, const Ray r, const int2 *__restrict__ cells,
-                                            int k0, int kend, float s_lo, float s_hi,
-                                            const float *Hk, float *Gk, float4 bd, float f0,
-                                            float f1) {
-  float d0 = s_lo, d1 = s_lo;
-  Recs R;
-  R.buf = nullptr;
-  R.stride = 0;
-  R.n[0] = R.n[1] = 0;
-  bool ovf = false, redo = false;
-  walk<STRIDE, LDG, true, false>(g, r, cells, k0, kend, s_lo, s_hi, Hk, Gk, bd, d0, d1, R, ovf,
-                                 redo, f0, f1);
-}
-
-// Fused epilogue (a4-a5): t = ln(λ/C) (C > 0) or ln λ (C = 0) from the
-// per-ray constant t_base (HP4, R15); returns ℓ_p, sets ∂ℓ/∂O = (λ - C)/Λ.
-__device__ __forceinline__ float epilogue(const Ray &r, const TraceConsts &tc, float B0, float B1,
-                                          float &dldO) {
-  float t = r.tb - (tc.k0 * B0 + tc.k1 * B1) * tc.inv_att;
-  if (r.cnt > 0.f) {
-    // ℓ = -C (e^t - 1 - t); e^t - 1 - t by its series when |t| < 0.1 (truncation
-    // < 2e-10 relative), expm1f otherwise
-    float d;
-    if (fabsf(t) < 0.1f)
-      d = t * t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.f / 720.f, 1.f / 120.f), 1.f / 24.f), 1.f / 6.f), 0.5f);
-    else
-      d = expm1f(t) - t;
-    dldO = r.cnt * (d + t) * tc.inv_att;
-    return -r.cnt * d;
-  }
-  float lam = __expf(t);
-  dldO = lam * tc.inv_att;
-  return -lam;
-}
-
-// ---------------------------------------------------------------------------
-// chain lanes: one surface of one stored cell for this lane's chain (a3).
-// Warp-uniform inputs: the cell (i, j, base node), its piece [s, s1] of the
-// ray, za = s d_z, zb = s1 d_z.  Per lane: the chain's heights (column of the
-// chain-interleaved layout), its band [zmin, zmax] of this surface, B.  The
-// arithmetic of the solve is cell32's.  An ill-conditioned cell (|g'| < GTHR
-// at a crossing, or a near-tangent vertex) sets `defer`: the whole chain x ray
-// pair is then handed to k_trace_defer, which re-traces it with the same fp32
-// cell code plus in-place fp64 re-solves (rare).  So the hot kernel holds no
-// double-precision code and makes no calls (a call forces the ABI's spills
-// into the loop).
-// ---------------------------------------------------------------------------
-template <int L, int NY>
-__device__ __forceinline__ void cw_surface(const Geo &g, const Ray &r, const float *__restrict__ Hl,
-                                           int i, int j, int base, float s, float za, float zb,
-                                           float Ls, float zmin, float zmax, float &B, int &n,
-                                           bool &defer, float4 *rec) {
-  if (zb <= zmin) { B += Ls; return; }            // below the chain's lowest node of this surface
-  if (za >= zmax) return;                         // above its highest node
-  const int oy = (NY ? NY : g.ny) * 32;
-  const float *p = Hl + base * 32;
-  const float h00 = __ldg(p), h01 = __ldg(p + 32), h10 = __ldg(p + oy), h11 = __ldg(p + oy + 32);
-  if (zb <= fminf(fminf(h00, h10), fminf(h01, h11))) { B += Ls; return; }   // bilinear min at a corner
-  if (za >= fmaxf(fmaxf(h00, h10), fmaxf(h01, h11))) return;
-  const float idx = g.idx[i], idy = g.idy[j];
-  const float u0 = (fmaf(s, r.dx, r.ox) - g.Xs[i]) * idx;
-  const float v0 = (fmaf(s, r.dy, r.oy) - g.Ys[j]) * idy;
-  const float al = r.dx * idx, be = r.dy * idy;
-  const float b = h10 - h00, c = h01 - h00, e = (h11 - h10) - (h01 - h00);
-  const float g0 = (h00 - za) + u0 * (b + e * v0) + c * v0;
-  const float g1 = b * al + c * be + e * (u0 * be + v0 * al) - r.dz;
+  const float g1 = b * al + c * be + e * (u0 * be + v0 * al) - dz;
   const float g2 = e * al * be;
   const float gL = g0 + Ls * (g1 + Ls * g2);
   const float disc = fmaf(g1, g1, -4.f * g2 * g0);
@@ -527,23 +239,190 @@ __device__ __forceinline__ void cw_surface(const Geo &g, const Ray &r, const flo
     float t = (ta > 0.f && ta < Ls) ? ta : tb;
     t = fminf(fmaxf(t, 0.f), Ls);
     const float gp = g1 + a2 * t;
-    if (fabsf(gp) < GTHR || !(disc > 0.f)) { defer = true; return; }
+    if (fabsf(gp) < GTHR || !(disc > 0.f)) return false;
     B += p0 ? t : Ls - t;
-    if (n < RCAP) rec[(L * RCAP + n) * MT_THREADS] = make_float4(__int_as_float(base), u0 + al * t, v0 + be * t, __fdividef(1.f, fabsf(gp)));
-    n++;
+    emit(u0 + al * t, v0 + be * t, __fdividef(1.f, fabsf(gp)));
   } else if (disc > 0.f && vin && ((g2 > 0.f) == p0)) {   // two crossings
     const float t1 = fminf(ta, tb), t2 = fmaxf(ta, tb);
     const float gp1 = g1 + a2 * t1, gp2 = g1 + a2 * t2;
-    if (fabsf(gp1) < GTHR || fabsf(gp2) < GTHR) { defer = true; return; }
+    if (fabsf(gp1) < GTHR || fabsf(gp2) < GTHR) return false;
     B += p0 ? Ls - (t2 - t1) : (t2 - t1);
-    if (n < RCAP) rec[(L * RCAP + n) * MT_THREADS] = make_float4(__int_as_float(base), u0 + al * t1, v0 + be * t1, __fdividef(1.f, fabsf(gp1)));
-    n++;
-    if (n < RCAP) rec[(L * RCAP + n) * MT_THREADS] = make_float4(__int_as_float(base), u0 + al * t2, v0 + be * t2, __fdividef(1.f, fabsf(gp2)));
-    n++;
+    emit(u0 + al * t1, v0 + be * t1, __fdividef(1.f, fabsf(gp1)));
+    emit(u0 + al * t2, v0 + be * t2, __fdividef(1.f, fabsf(gp2)));
   } else {                                        // no crossing
-    if (vin && fabsf(disc) < 2.f * fabsf(a2) * ZTHR) { defer = true; return; }   // near-tangent
+    if (vin && fabsf(disc) < 2.f * fabsf(a2) * ZTHR) return false;   // near-tangent
     if (p0) B += Ls;
   }
+  return true;
+}
+
+// Stored per-cell geometry {u, v, α, β} is taken at the cell's entry s_in; a
+// walk that starts inside the cell (at the band entry s_lo) moves it by
+// ds = s_lo - s_in.  For every later cell ds = 0 exactly.
+__device__ __forceinline__ float4 shift_geo(float4 cg, float ds) {
+  cg.x = fmaf(cg.z, ds, cg.x);
+  cg.y = fmaf(cg.w, ds, cg.y);
+  return cg;
+}
+
+struct Geo {
+  const float *Xs, *Ys, *idx, *idy;
+  int nx, ny, N;
+};
+
+// Node coordinates and inverse spacings, at static shared addresses (indexed
+// directly: no pointer registers, no address setup in the hot loops).
+__shared__ float sgeo[4][MT_MAX_AXIS];   // X, Y, 1/ΔX, 1/ΔY
+
+// Crossing records of one chain x ray: up to RCAP per surface, kept in shared
+// memory at slot [(l*RCAP + m)*MT_THREADS + tid] (conflict-free: consecutive
+// threads, consecutive 16-B words).
+#ifndef MT_RCAP
+#define MT_RCAP 4
+#endif
+#ifndef MT_CL_MINB
+#define MT_CL_MINB 4
+#endif
+constexpr int RCAP = MT_RCAP;
+
+__device__ __forceinline__ void scatter4(float *Gl, int STRIDE, int base, int ny, float w, float u,
+                                         float v) {
+  atomicAdd(Gl + base * STRIDE, w * (1.f - u) * (1.f - v));
+  atomicAdd(Gl + (base + ny) * STRIDE, w * u * (1.f - v));
+  atomicAdd(Gl + (base + 1) * STRIDE, w * (1.f - u) * v);
+  atomicAdd(Gl + (base + ny + 1) * STRIDE, w * u * v);
+}
+
+// ---------------------------------------------------------------------------
+// generic walk (ray lanes, deferred pairs): one chain x ray, thread-serial.
+// Heights of the chain at Hk with node stride STRIDE (1: a shared-memory tile,
+// 32: the chain-interleaved global layout).  Ill-conditioned cells are
+// re-solved in place in fp64.  SCAT: scatter f_l φ/|g'| directly into Gk;
+// else record crossings (n[l] counts all, the first RCAP are stored).
+// ---------------------------------------------------------------------------
+template <int STRIDE, bool SCAT>
+__device__ __forceinline__ void walk(const Ray &r, const int2 *__restrict__ cells,
+                                     const float4 *__restrict__ cgeo, int k, int kend, float s0,
+                                     float s_in0, float s_hi, int ny, int N, const float *Hk,
+                                     float *Gk, float4 bd, float &B0, float &B1, float4 *rec,
+                                     int *n, float f0, float f1) {
+  float s = s0, ds = s0 - s_in0;
+  for (; k < kend; k++) {
+    const int2 w = __ldg(cells + k);
+    const float s1 = __int_as_float(w.y);
+    const float4 cg = shift_geo(__ldg(cgeo + k), ds);
+    const int i = cell_i(w.x), j = cell_j(w.x), base = i * ny + j;
+    const float za = s * r.dz, zb = s1 * r.dz, Ls = s1 - s;
+#pragma unroll
+    for (int l = 0; l < 2; l++) {
+      const float zmin = l ? bd.z : bd.x, zmax = l ? bd.w : bd.y;
+      float &B = l ? B1 : B0;
+      if (zb <= zmin) { B += Ls; continue; }
+      if (za >= zmax) continue;
+      const float *p = Hk + (size_t)l * N * STRIDE + base * STRIDE;
+      const float h00 = p[0], h10 = p[ny * STRIDE], h01 = p[STRIDE], h11 = p[ny * STRIDE + STRIDE];
+      if (zb <= fminf(fminf(h00, h10), fminf(h01, h11))) { B += Ls; continue; }
+      if (za >= fmaxf(fmaxf(h00, h10), fmaxf(h01, h11))) continue;
+      float *Gl = SCAT ? Gk + (size_t)l * N * STRIDE : nullptr;
+      const float f = l ? f1 : f0;
+      auto emit = [&](float u, float v, float ig) {
+        if (SCAT) {
+          scatter4(Gl, STRIDE, base, ny, f * ig, u, v);
+        } else {
+          if (n[l] < RCAP) rec[(l * RCAP + n[l]) * MT_THREADS] = make_float4(__int_as_float(base), u, v, ig);
+          n[l]++;
+        }
+      };
+      if (!solve32(h00, h10, h01, h11, cg, za, Ls, r.dz, B, emit)) {
+        const Fix x = fix64(h00, h10, h01, h11, sgeo[0][i], sgeo[0][i + 1], sgeo[1][j], sgeo[1][j + 1], r, s, s1);
+        B += x.below;
+        for (int m = 0; m < x.n; m++) emit(x.u[m], x.v[m], x.ig[m]);
+      }
+    }
+    if (s1 >= s_hi) break;
+    s = s1;
+    ds = 0.f;
+  }
+}
+
+// Scatter recorded crossings: G_l[node] += f_l · φ_node(u, v)/|g'|  (a6).
+template <int STRIDE>
+__device__ __forceinline__ void scatter_recs(const float4 *rec, const int *n, float *Gk, int N, int ny,
+                                             float f0, float f1) {
+#pragma unroll
+  for (int l = 0; l < 2; l++) {
+    for (int m = 0; m < n[l]; m++) {
+      const float4 q = rec[(l * RCAP + m) * MT_THREADS];
+      scatter4(Gk + (size_t)l * N * STRIDE, STRIDE, __float_as_int(q.x), ny, (l ? f1 : f0) * q.w, q.y, q.z);
+    }
+  }
+}
+
+// Trace one chain x ray (generic walk) from its band [s_lo, s_hi]: B0, B1 and,
+// in TRACE_LL mode, the adjoint scatter; returns ℓ_p (or writes the path
+// lengths in TRACE_PATH mode).  The scatter uses the records, or a second,
+// scattering walk when a surface had more than RCAP crossings.
+struct PairOut {
+  float B0, B1;
+};
+
+// First stored cell of the ray whose s_out exceeds s (binary search; the last
+// cell's s_out is s_exit > s), and the entry s_in of that cell.
+__device__ __forceinline__ int band_entry(const int2 *__restrict__ cells, int lo, int hi, float s,
+                                          float &s_in) {
+  const int first = lo;
+  hi -= 1;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (__int_as_float(__ldg(&cells[mid].y)) > s) hi = mid;
+    else lo = mid + 1;
+  }
+  s_in = lo > first ? __int_as_float(__ldg(&cells[lo - 1].y)) : 0.f;
+  return lo;
+}
+
+// Same, warp-cooperative (chain lanes, all 32 lanes converged, uniform
+// arguments): one coalesced load of 32 cells and a ballot per round.
+__device__ __forceinline__ int band_entry_warp(const int2 *__restrict__ cells, int lo, int hi, float s,
+                                               float &s_in) {
+  const int lane = threadIdx.x & 31;
+  float prev = 0.f;   // s_out of the cell before this round (0 before the first cell)
+  for (int b = lo; b < hi; b += 32) {
+    const int k = b + lane;
+    const float so = k < hi ? __int_as_float(__ldg(&cells[k].y)) : 3.0e38f;
+    const unsigned m = __ballot_sync(0xffffffffu, so > s);
+    const float before = __shfl_up_sync(0xffffffffu, so, 1);
+    if (m) {
+      const int f = __ffs(m) - 1;
+      const float sb = __shfl_sync(0xffffffffu, before, f);
+      s_in = f > 0 ? sb : prev;
+      return b + f;
+    }
+    prev = __shfl_sync(0xffffffffu, so, 31);
+  }
+  s_in = prev;
+  return hi - 1;
+}
+
+// Fused epilogue (a4-a5): t = ln(λ/C) (C > 0) or ln λ (C = 0) from the
+// per-ray constant t_base (HP4, R15); returns ℓ_p, sets ∂ℓ/∂O = (λ - C)/Λ.
+__device__ __forceinline__ float epilogue(float tb, float cnt, const TraceConsts &tc, float B0,
+                                          float B1, float &dldO) {
+  const float t = tb - (tc.k0 * B0 + tc.k1 * B1) * tc.inv_att;
+  if (cnt > 0.f) {
+    // ℓ = -C (e^t - 1 - t); e^t - 1 - t by its series when |t| < 0.1 (truncation
+    // < 2e-10 relative), expm1f otherwise
+    float d;
+    if (fabsf(t) < 0.1f)
+      d = t * t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.f / 720.f, 1.f / 120.f), 1.f / 24.f), 1.f / 6.f), 0.5f);
+    else
+      d = expm1f(t) - t;
+    dldO = cnt * (d + t) * tc.inv_att;
+    return -cnt * d;
+  }
+  const float lam = __expf(t);
+  dldO = lam * tc.inv_att;
+  return -lam;
 }
 
 __device__ __forceinline__ void load_geometry(const TraceArgs &a, float *Xs, float *Ys, float *idx,
@@ -564,7 +443,7 @@ __device__ __forceinline__ void load_geometry(const TraceArgs &a, float *Xs, flo
 // ---------------------------------------------------------------------------
 // traversal builder (create time): thread = ray; count pass then write pass
 // ---------------------------------------------------------------------------
-__global__ void k_build_trav(TraceArgs a, const int32_t *off, int32_t *count, int2 *cells) {
+__global__ void k_build_trav(TraceArgs a, const int32_t *off, int32_t *count, int2 *cells, float4 *cgeo) {
   __shared__ float Xs[MT_MAX_AXIS], Ys[MT_MAX_AXIS];
   const int nx = a.tc.nx, ny = a.tc.ny;
   for (int k = threadIdx.x; k < nx; k += blockDim.x) Xs[k] = a.X[k];
@@ -574,13 +453,23 @@ __global__ void k_build_trav(TraceArgs a, const int32_t *off, int32_t *count, in
   if (rr >= a.R) return;
   DdaRay q = dda_ray(load_ray(a.ray_a, a.ray_b, rr));
   int i = start_axis(Xs, nx, q.r.ox, q.r.dx), j = start_axis(Ys, ny, q.r.oy, q.r.dy);
-  float s = 0.f;
+  float s = 0.f, s_in = 0.f;   // s_in: the previous STORED s_out (what the walks carry)
   int n = 0;
   for (int guard = 0; guard < 4 * (MT_MAX_AXIS + 2); guard++) {
     float s_ev;
     int ev = dda_next(q, i, j, Xs, Ys, nx, ny, a.tc.z_top, s_ev);
     float s1 = fminf(s_ev, q.r.s_exit);
-    if (cells) cells[off[rr] + n] = make_int2(i | (j << 16), __float_as_int(fmaxf(s1, s)));
+    const float so = fmaxf(s1, s);
+    if (cells) {
+      cells[off[rr] + n] = make_int2(cell_pack(i, j, ny), __float_as_int(so));
+      // cell-local entry point and rates (a0), fp64 from the exact fp32 inputs
+      const double ix = 1.0 / ((double)Xs[i + 1] - (double)Xs[i]);
+      const double iy = 1.0 / ((double)Ys[j + 1] - (double)Ys[j]);
+      const double u = ((double)q.r.ox + (double)s_in * (double)q.r.dx - (double)Xs[i]) * ix;
+      const double v = ((double)q.r.oy + (double)s_in * (double)q.r.dy - (double)Ys[j]) * iy;
+      cgeo[off[rr] + n] = make_float4((float)u, (float)v, (float)((double)q.r.dx * ix), (float)((double)q.r.dy * iy));
+    }
+    s_in = so;
     n++;
     if (ev & 4) break;
     if (ev & 1) i += q.sx;
@@ -593,18 +482,40 @@ __global__ void k_build_trav(TraceArgs a, const int32_t *off, int32_t *count, in
 // ---------------------------------------------------------------------------
 // K2, chain lanes: warp = one ray x 32 chains, lane = chain
 // ---------------------------------------------------------------------------
+// One surface of one stored cell for this lane's chain.  Warp-uniform inputs:
+// the cell word w (node offset, i, j), its geometry cg, the piece [s, s1] of
+// the ray (za = s d_z, zb = s1 d_z).  Per lane: the chain's heights (column of
+// the chain-interleaved layout), its band [zmin, zmax] of this surface, B.  An
+// ill-conditioned cell sets `defer`: the whole chain x ray pair is then handed
+// to k_trace_defer (same fp32 cell code plus in-place fp64 re-solves), so the
+// hot kernel holds no double-precision code and makes no calls (a call forces
+// the ABI's spills into the loop).
+template <int L>
+__device__ __forceinline__ void cw_surface(const float *__restrict__ Hl, int w, int oy, float4 cg,
+                                           float za, float zb, float Ls, float dz, float zmin,
+                                           float zmax, float &B, int &n, int &defer, float4 *rec) {
+  if (zb <= zmin) { B += Ls; return; }            // below the chain's lowest node of this surface
+  if (za >= zmax) return;                         // above its highest node
+  const float *p = Hl + cell_off32(w);
+  const float h00 = __ldg(p), h01 = __ldg(p + 32), h10 = __ldg(p + oy), h11 = __ldg(p + oy + 32);
+  if (zb <= fminf(fminf(h00, h10), fminf(h01, h11))) { B += Ls; return; }   // bilinear min at a corner
+  if (za >= fmaxf(fmaxf(h00, h10), fmaxf(h01, h11))) return;
+  const float wbase = __int_as_float(cell_off32(w) >> 5);
+  auto emit = [&](float u, float v, float ig) {
+    if (n < RCAP) rec[(L * RCAP + n) * MT_THREADS] = make_float4(wbase, u, v, ig);
+    n++;
+  };
+  if (!solve32(h00, h10, h01, h11, cg, za, Ls, dz, B, emit)) defer = 1;
+}
+
 template <int MODE, int NY>
 __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a) {
-  // geometry at static shared addresses (no pointer registers): X, Y, 1/ΔX, 1/ΔY
-  __shared__ float sgeo[4][MT_MAX_AXIS];
   extern __shared__ __align__(16) float4 recs[];    // crossing records [2*RCAP][MT_THREADS]
-  const int nx = a.tc.nx, ny = NY ? NY : a.tc.ny, N = a.tc.N;
+  const int ny = NY ? NY : a.tc.ny, N = a.tc.N;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = blockIdx.y, c = grp * 32 + lane;
   const bool act = c < a.C;
-  load_geometry(a, sgeo[0], sgeo[1], sgeo[2], sgeo[3]);
   float4 *rec = recs + threadIdx.x;
-  __syncthreads();
   // this lane's chain band; the warp walks the union band of its 32 chains.
   // Inactive lanes get a band that every cell lies "above" (no loads).
   float4 bd = act ? __ldg(a.band + c) : make_float4(3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f);
@@ -614,43 +525,41 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a
     zhi = fmaxf(zhi, __shfl_xor_sync(0xffffffffu, zhi, o));
   }
   if (!act) bd = make_float4(-3.0e38f, -3.0e38f, -3.0e38f, -3.0e38f);
-  Geo g;
-  g.Xs = sgeo[0]; g.Ys = sgeo[1]; g.idx = sgeo[2]; g.idy = sgeo[3]; g.nx = nx; g.ny = ny; g.N = N;
-  const float *H0 = a.H + (size_t)grp * 2 * N * 32 + lane;
+  const int oy = ny * 32;
+  const float *H0 = a.H + (size_t)grp * 2 * N * 32 + lane, *H1 = H0 + N * 32;
   float llacc = 0.f;
 
   const int r_begin = blockIdx.x * (int)a.rays_per_block;
   const int r_end = min((int)a.R, r_begin + (int)a.rays_per_block);
   for (int rr = r_begin + warp; rr < r_end; rr += MT_THREADS / 32) {
-    Ray r;
+    float dz, s_exit;
     {
-      const float4 ra = __ldg(a.ray_a + rr);           // same address in every lane: broadcast
-      const float2 rb = __ldg(reinterpret_cast<const float2 *>(a.ray_b + rr));
-      r.ox = ra.x; r.oy = ra.y; r.dx = ra.z; r.dy = ra.w; r.dz = rb.x; r.s_exit = rb.y;
+      const float2 rb = __ldg(reinterpret_cast<const float2 *>(a.ray_b + rr));   // broadcast
+      dz = rb.x; s_exit = rb.y;
     }
     // band bounds, widened by 1e-6 so fast division can only walk more cells
-    const float s_lo = fminf(__fdividef(zlo, r.dz) * (1.f - 1e-6f), r.s_exit);
-    const float s_hi = fminf(__fdividef(zhi, r.dz) * (1.f + 1e-6f), r.s_exit);
+    const float s_lo = fminf(__fdividef(zlo, dz) * (1.f - 1e-6f), s_exit);
+    const float s_hi = fminf(__fdividef(zhi, dz) * (1.f + 1e-6f), s_exit);
     float B0 = s_lo, B1 = s_lo;                        // below both surfaces before s_lo
-    int n0 = 0, n1 = 0;
-    bool defer = false;
-    if (s_lo < r.s_exit) {                             // warp-uniform
+    int n0 = 0, n1 = 0, defer = 0;
+    if (s_lo < s_exit) {                               // warp-uniform
       const int kend = __ldg(a.trav_off + rr + 1);
-      const int k0 = band_entry_warp(a.trav, __ldg(a.trav_off + rr), kend, s_lo);
-      float s = s_lo, za = s_lo * r.dz;
+      float s_in0;
+      const int k0 = band_entry_warp(a.trav, __ldg(a.trav_off + rr), kend, s_lo, s_in0);
+      float s = s_lo, za = s_lo * dz, ds = s_lo - s_in0;
       for (int k = k0; k < kend; k++) {
-        const int2 e = __ldg(a.trav + k);
-        const float s1 = __int_as_float(e.y);
-        const int i = e.x & 0xffff, j = e.x >> 16, base = i * ny + j;
-        const float zb = s1 * r.dz;
-        if (s1 > s) {
-          const float Ls = s1 - s;
-          cw_surface<0, NY>(g, r, H0, i, j, base, s, za, zb, Ls, bd.x, bd.y, B0, n0, defer, rec);
-          cw_surface<1, NY>(g, r, H0 + N * 32, i, j, base, s, za, zb, Ls, bd.z, bd.w, B1, n1, defer, rec);
-        }
+        // (a zero-length stored cell, possible only through fp32 event rounding
+        // in the builder, adds nothing: no crossing, B += 0)
+        const int2 w = __ldg(a.trav + k);
+        const float4 cg = shift_geo(__ldg(a.trav_geo + k), ds);
+        const float s1 = __int_as_float(w.y);
+        const float zb = s1 * dz, Ls = s1 - s;
+        cw_surface<0>(H0, w.x, oy, cg, za, zb, Ls, dz, bd.x, bd.y, B0, n0, defer, rec);
+        cw_surface<1>(H1, w.x, oy, cg, za, zb, Ls, dz, bd.z, bd.w, B1, n1, defer, rec);
         if (s1 >= s_hi) break;
         s = s1;
         za = zb;
+        ds = 0.f;
       }
     }
     if (defer || n0 > RCAP || n1 > RCAP) {             // rare: the whole pair goes to k_trace_defer
@@ -660,18 +569,16 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a
     }
     if (MODE == TRACE_LL) {
       const float2 rb = __ldg(reinterpret_cast<const float2 *>(a.ray_b + rr) + 1);
-      r.tb = rb.x; r.cnt = rb.y;
       float dldO;
-      const float ll = epilogue(r, a.tc, B0, B1, dldO);
+      const float ll = epilogue(rb.x, rb.y, a.tc, B0, B1, dldO);
       if (act) {
         llacc += ll;
         const float f0 = dldO * a.tc.k0, f1 = dldO * a.tc.k1;
         float *G0 = a.G + (size_t)grp * 2 * N * 32 + lane;
-        const int oy = ny * 32;
         for (int m = 0; m < n0; m++) {
           const float4 q = rec[m * MT_THREADS];
           const float w = f0 * q.w, u = q.y, v = q.z;
-          float *pg = G0 + __float_as_int(q.x) * 32;
+          float *pg = G0 + ((unsigned)__float_as_int(q.x) << 5);
           atomicAdd(pg, w * (1.f - u) * (1.f - v));
           atomicAdd(pg + oy, w * u * (1.f - v));
           atomicAdd(pg + 32, w * (1.f - u) * v);
@@ -681,7 +588,7 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a
         for (int m = 0; m < n1; m++) {
           const float4 q = rec[(RCAP + m) * MT_THREADS];
           const float w = f1 * q.w, u = q.y, v = q.z;
-          float *pg = G1 + __float_as_int(q.x) * 32;
+          float *pg = G1 + ((unsigned)__float_as_int(q.x) << 5);
           atomicAdd(pg, w * (1.f - u) * (1.f - v));
           atomicAdd(pg + oy, w * u * (1.f - v));
           atomicAdd(pg + 32, w * (1.f - u) * v);
@@ -692,7 +599,7 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a
       const int64_t o = (int64_t)c * a.R + __ldg(a.perm + rr);
       a.Lout[3 * o + 0] = B0;
       a.Lout[3 * o + 1] = B1 - B0;
-      a.Lout[3 * o + 2] = r.s_exit - B1;
+      a.Lout[3 * o + 2] = s_exit - B1;
       a.Oout[o] = a.tc.k0 * B0 + a.tc.k1 * B1 + a.obase[rr];
     }
   }
@@ -706,15 +613,11 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a
 // scatter (or the path-length export).  The last block resets the queue.
 template <int MODE>
 __global__ void __launch_bounds__(MT_THREADS) k_trace_defer(TraceArgs a) {
-  __shared__ float sgeo[4][MT_MAX_AXIS];
   extern __shared__ __align__(16) float4 recs[];    // [2*RCAP][MT_THREADS]
   load_geometry(a, sgeo[0], sgeo[1], sgeo[2], sgeo[3]);
   __syncthreads();
   const int n = *(volatile int *)a.ovf_n;
-  const int N = a.tc.N;
-  Geo g;
-  g.Xs = sgeo[0]; g.Ys = sgeo[1]; g.idx = sgeo[2]; g.idy = sgeo[3];
-  g.nx = a.tc.nx; g.ny = a.tc.ny; g.N = N;
+  const int N = a.tc.N, ny = a.tc.ny;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < min(n, a.ovf_cap); q += gridDim.x * blockDim.x) {
     const float4 e0 = a.ovf_q[q];
     const int c = __float_as_int(e0.x), rr = __float_as_int(e0.y);
@@ -723,24 +626,27 @@ __global__ void __launch_bounds__(MT_THREADS) k_trace_defer(TraceArgs a) {
     const size_t off = (size_t)(c >> 5) * 2 * N * 32 + (c & 31);
     const float4 bd = a.band[c];
     float B0 = s_lo, B1 = s_lo;
-    Recs R;
-    R.buf = recs + threadIdx.x;
-    R.stride = MT_THREADS;
-    R.n[0] = R.n[1] = 0;
-    bool ovf = false;
+    int nrec[2] = {0, 0};
     int k0 = 0;
+    float s_in0 = 0.f;
     const int kend = a.trav_off[rr + 1];
     if (s_lo < r.s_exit) {
-      k0 = band_entry(a.trav, a.trav_off[rr], kend, s_lo);
-      trace_pair<32, true>(g, r, a.trav, k0, kend, s_lo, s_hi, a.H + off, nullptr, bd, B0, B1, R, ovf);
+      k0 = band_entry(a.trav, a.trav_off[rr], kend, s_lo, s_in0);
+      walk<32, false>(r, a.trav, a.trav_geo, k0, kend, s_lo, s_in0, s_hi, ny, N, a.H + off, nullptr, bd,
+                      B0, B1, recs + threadIdx.x, nrec, 0.f, 0.f);
     }
     if (MODE == TRACE_LL) {
       float dldO;
-      const float ll = epilogue(r, a.tc, B0, B1, dldO);
+      const float ll = epilogue(r.tb, r.cnt, a.tc, B0, B1, dldO);
       atomicAdd(a.ll + c, (double)ll);
       const float f0 = dldO * a.tc.k0, f1 = dldO * a.tc.k1;
-      if (!ovf) scatter<32>(R, a.G + off, N, g.ny, f0, f1);
-      else rewalk_scatter<32, true>(g, r, a.trav, k0, kend, s_lo, s_hi, a.H + off, a.G + off, bd, f0, f1);
+      if (nrec[0] <= RCAP && nrec[1] <= RCAP) {
+        scatter_recs<32>(recs + threadIdx.x, nrec, a.G + off, N, ny, f0, f1);
+      } else {
+        float d0 = s_lo, d1 = s_lo;
+        walk<32, true>(r, a.trav, a.trav_geo, k0, kend, s_lo, s_in0, s_hi, ny, N, a.H + off, a.G + off, bd,
+                       d0, d1, nullptr, nrec, f0, f1);
+      }
     } else {
       const int64_t o = (int64_t)c * a.R + a.perm[rr];
       a.Lout[3 * o + 0] = B0;
@@ -756,6 +662,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_trace_defer(TraceArgs a) {
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(a.ovf_done, 1) == (int)gridDim.x - 1) {
+      *a.ovf_total += (unsigned long long)n;
       *a.ovf_n = 0;
       *a.ovf_done = 0;
     }
@@ -763,25 +670,23 @@ __global__ void __launch_bounds__(MT_THREADS) k_trace_defer(TraceArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// K2, ray lanes (small C)
+// K2, ray lanes (small C): block = K chains whose height and gradient tiles
+// sit in shared memory, thread = ray
 // ---------------------------------------------------------------------------
 template <int K, int MODE>
 __global__ void __launch_bounds__(MT_THREADS) k_trace_rl(TraceArgs a) {
   extern __shared__ __align__(16) float smem[];
-  const int nx = a.tc.nx, ny = a.tc.ny, N = a.tc.N;
-  float *Xs = smem, *Ys = Xs + nx, *idx = Ys + ny, *idy = idx + nx;
-  const int geo_words = (2 * nx + 2 * ny + 3) & ~3;
-  float *Hs = smem + geo_words;                       // [K][2N]
+  const int ny = a.tc.ny, N = a.tc.N;
+  float *Hs = smem;                                   // [K][2N]
   float *Gs = Hs + K * 2 * N;                         // [K][2N] (TRACE_LL)
-  float4 *recbuf = reinterpret_cast<float4 *>(
-      smem + geo_words + ((K * 2 * N * (MODE == TRACE_LL ? 2 : 1) + 3) & ~3));
+  float4 *recbuf = reinterpret_cast<float4 *>(smem + ((K * 2 * N * (MODE == TRACE_LL ? 2 : 1) + 3) & ~3));
   __shared__ double red[MT_THREADS / 32][K];
   __shared__ float4 bds[K];
   __shared__ float llacc[K][MT_THREADS];
   const int tid = threadIdx.x;
   const int c0 = blockIdx.y * K;
   const int nk = min(K, a.C - c0);
-  load_geometry(a, Xs, Ys, idx, idy);
+  load_geometry(a, sgeo[0], sgeo[1], sgeo[2], sgeo[3]);
   for (int k = tid; k < nk * 2 * N; k += blockDim.x) {
     int kc = k / (2 * N), m = k - kc * 2 * N;
     Hs[k] = __ldg(a.H + tix(c0 + kc, m / N, m % N, N));
@@ -793,8 +698,6 @@ __global__ void __launch_bounds__(MT_THREADS) k_trace_rl(TraceArgs a) {
   __syncthreads();
   float zlo = 3.0e38f;
   for (int k = 0; k < nk; k++) zlo = fminf(zlo, bds[k].x);
-  Geo g;
-  g.Xs = Xs; g.Ys = Ys; g.idx = idx; g.idy = idy; g.nx = nx; g.ny = ny; g.N = N;
 
   const int64_t r_begin = (int64_t)blockIdx.x * a.rays_per_block;
   const int64_t r_end = min(a.R, r_begin + a.rays_per_block);
@@ -803,26 +706,30 @@ __global__ void __launch_bounds__(MT_THREADS) k_trace_rl(TraceArgs a) {
     const float s_lo = fminf(zlo / r.dz, r.s_exit);
     const bool walkable = s_lo < r.s_exit;
     const int kend = __ldg(a.trav_off + rr + 1);
-    const int k0 = walkable ? band_entry(a.trav, __ldg(a.trav_off + rr), kend, s_lo) : 0;
+    float s_in0 = 0.f;
+    const int k0 = walkable ? band_entry(a.trav, __ldg(a.trav_off + rr), kend, s_lo, s_in0) : 0;
 #pragma unroll 1
     for (int k = 0; k < nk; k++) {
       const float *Hk = Hs + k * 2 * N;
       float *Gk = Gs + k * 2 * N;
       const float4 bd = bds[k];
       float B0 = s_lo, B1 = s_lo;
-      Recs R;
-      R.buf = recbuf + tid;
-      R.stride = blockDim.x;
-      R.n[0] = R.n[1] = 0;
-      bool ovf = false;
+      int nrec[2] = {0, 0};
       const float s_hi = fminf(bd.w / r.dz, r.s_exit);
-      if (walkable) trace_pair<1, false>(g, r, a.trav, k0, kend, s_lo, s_hi, Hk, Gk, bd, B0, B1, R, ovf);
+      if (walkable)
+        walk<1, false>(r, a.trav, a.trav_geo, k0, kend, s_lo, s_in0, s_hi, ny, N, Hk, nullptr, bd, B0, B1,
+                       recbuf + tid, nrec, 0.f, 0.f);
       if (MODE == TRACE_LL) {
         float dldO;
-        llacc[k][tid] += epilogue(r, a.tc, B0, B1, dldO);
+        llacc[k][tid] += epilogue(r.tb, r.cnt, a.tc, B0, B1, dldO);
         const float f0 = dldO * a.tc.k0, f1 = dldO * a.tc.k1;
-        if (!ovf) scatter<1>(R, Gk, N, ny, f0, f1);
-        else rewalk_scatter<1, false>(g, r, a.trav, k0, kend, s_lo, s_hi, Hk, Gk, bd, f0, f1);
+        if (nrec[0] <= RCAP && nrec[1] <= RCAP) {
+          scatter_recs<1>(recbuf + tid, nrec, Gk, N, ny, f0, f1);
+        } else {
+          float d0 = s_lo, d1 = s_lo;
+          walk<1, true>(r, a.trav, a.trav_geo, k0, kend, s_lo, s_in0, s_hi, ny, N, Hk, Gk, bd, d0, d1,
+                        nullptr, nrec, f0, f1);
+        }
       } else {
         const int64_t o = (int64_t)(c0 + k) * a.R + __ldg(a.perm + rr);
         a.Lout[3 * o + 0] = B0;
@@ -861,9 +768,10 @@ static TraceArgs base_trace_args(mt_problem *p) {
   a.tc = p->tc;
   a.X = p->d_X; a.Y = p->d_Y;
   a.ray_a = p->d_ray_a; a.ray_b = p->d_ray_b; a.obase = p->d_obase;
-  a.trav_off = p->d_trav_off; a.trav = p->d_trav; a.perm = p->d_perm;
+  a.trav_off = p->d_trav_off; a.trav = p->d_trav; a.trav_geo = p->d_trav_geo; a.perm = p->d_perm;
   a.R = p->R;
   a.ovf_q = p->d_ovf_q; a.ovf_n = p->d_ovf_n; a.ovf_done = p->d_ovf_n + 1; a.ovf_cap = p->ovf_cap;
+  a.ovf_total = reinterpret_cast<unsigned long long *>(p->d_ovf_n + 2);
   return a;
 }
 
@@ -874,7 +782,7 @@ cudaError_t build_traversal(mt_problem *p) {
   cudaError_t e = cudaMalloc(&d_cnt, sizeof(int32_t) * p->R);
   if (e != cudaSuccess) return e;
   unsigned nb = (unsigned)((p->R + 127) / 128);
-  k_build_trav<<<nb, 128>>>(a, nullptr, d_cnt, nullptr);
+  k_build_trav<<<nb, 128>>>(a, nullptr, d_cnt, nullptr, nullptr);
   std::vector<int32_t> cnt(p->R);
   e = cudaMemcpy(cnt.data(), d_cnt, sizeof(int32_t) * p->R, cudaMemcpyDeviceToHost);
   cudaFree(d_cnt);
@@ -889,12 +797,14 @@ cudaError_t build_traversal(mt_problem *p) {
   p->trav_cells = tot;
   e = cudaMalloc(&p->d_trav_off, sizeof(int32_t) * (p->R + 1));
   if (e == cudaSuccess) e = cudaMalloc(&p->d_trav, sizeof(int2) * (p->trav_cells > 0 ? p->trav_cells : 1));
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_trav_geo, sizeof(float4) * (p->trav_cells > 0 ? p->trav_cells : 1));
   if (e == cudaSuccess)
     e = cudaMemcpy(p->d_trav_off, off.data(), sizeof(int32_t) * (p->R + 1), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return e;
   a.trav_off = p->d_trav_off;
   a.trav = p->d_trav;
-  k_build_trav<<<nb, 128>>>(a, p->d_trav_off, nullptr, p->d_trav);
+  a.trav_geo = p->d_trav_geo;
+  k_build_trav<<<nb, 128>>>(a, p->d_trav_off, nullptr, p->d_trav, p->d_trav_geo);
   e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   return e;
@@ -904,7 +814,7 @@ template <typename Kern>
 static cudaError_t set_smem(Kern k, size_t smem, size_t *done) {
   int dev = 0;
   cudaGetDevice(&dev);
-  if (smem > 48 * 1024 && done[dev & 15] < smem) {
+  if (smem > 32 * 1024 && done[dev & 15] < smem) {   // (dynamic + static must fit the attribute)
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     done[dev & 15] = smem;
@@ -964,7 +874,6 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
   TraceArgs a = base_trace_args(p);
   a.C = C;
   a.H = H; a.band = band; a.G = G; a.ll = ll; a.Lout = L; a.Oout = O;
-  const int geo_words = (2 * p->nx + 2 * p->ny + 3) & ~3;
   const bool chain_lanes = p->trace_k == 0 ? C >= 16 : p->trace_k == 32;
   cudaError_t e = cudaSuccess;
   bool rec = p->timing && p->n_rec < (int)p->ev_a.size();
@@ -981,6 +890,7 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
     size_t smem = (size_t)16 * 2 * RCAP * MT_THREADS;   // crossing records (geometry is static)
     e = mode == TRACE_LL ? launch_cl_ny<TRACE_LL>(a, p->ny, grid, smem, s)
                          : launch_cl_ny<TRACE_PATH>(a, p->ny, grid, smem, s);
+    if (rec) cudaEventRecord(p->ev_m[p->n_rec], s);
     if (e == cudaSuccess) {   // deferred pairs (ill-conditioned or > RCAP crossings)
       const size_t dsm = (size_t)16 * 2 * RCAP * MT_THREADS;
       if (mode == TRACE_LL) k_trace_defer<TRACE_LL><<<2 * p->num_sms, MT_THREADS, dsm, s>>>(a);
@@ -995,7 +905,7 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
     a.rays_per_block = (p->R + S - 1) / S;
     S = (p->R + a.rays_per_block - 1) / a.rays_per_block;
     dim3 grid((unsigned)S, (unsigned)groups);
-    size_t smem = (size_t)4 * (geo_words + (((size_t)K * 2 * p->N * (mode == TRACE_LL ? 2 : 1) + 3) & ~(size_t)3)) +
+    size_t smem = (size_t)4 * (((size_t)K * 2 * p->N * (mode == TRACE_LL ? 2 : 1) + 3) & ~(size_t)3) +
                   (size_t)16 * 2 * RCAP * MT_THREADS;
 #define MT_DISPATCH(KK)                                                         \
   case KK:                                                                      \
@@ -1011,6 +921,7 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
     }
 #undef MT_DISPATCH
   }
+  if (rec && !chain_lanes) cudaEventRecord(p->ev_m[p->n_rec], s);
   if (rec) { cudaEventRecord(p->ev_b[p->n_rec], s); p->n_rec++; }
   p->all_launches++;
   p->trace_launches++;

@@ -41,13 +41,15 @@ def main():
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.reps
     tm = pb.timing_read()
+    cnt = pb.trace_counters()
     tr = tm["trace_ms"] / tm["trace_launches"]
     work = json.load(open(os.path.join(ROOT, "data", "work_counts.json")))[inputs.DATA_NAME[a.config]]
     F = work["flops_per_pair"]
     pairs = C * pb.R
     print(json.dumps({"config": a.config, "C": C, "R": pb.R, "K": os.environ.get("MT_TRACE_K", "auto"),
                       "S": os.environ.get("MT_TRACE_S", "auto"), "ms_per_eval": ms, "trace_ms": tr,
-                      "trace_share": tr / ms, "evals_per_s": pairs / (ms * 1e-3),
+                      "trace_share": tr / ms, "defer_ms": cnt["defer_ms"] / a.reps,
+                      "deferred_per_eval": cnt["deferred"] / (a.reps + 4), "lib": os.environ.get("MT_LIB", "default"), "evals_per_s": pairs / (ms * 1e-3),
                       "trace_alg_tflops": F * pairs / (tr * 1e-3) / 1e12}))
 
 
