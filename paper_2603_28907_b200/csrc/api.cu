@@ -79,7 +79,7 @@ int check_chains(const mt_problem *p, int32_t C) {
 }
 
 void free_all(mt_problem *p) {
-  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_trav_geo, p->d_ovf_q, p->d_ovf_n, p->d_H, p->d_G,
+  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_trav_geo, p->d_ovf_q, p->d_ovf_n, p->d_H, p->d_Hlo, p->d_G,
                   p->d_band, p->d_ll, p->d_x0, p->d_g0, p->d_mom, p->d_kin0, p->d_kin1, p->d_lp0};
   for (void *b : bufs)
     if (b) cudaFree(b);
@@ -166,6 +166,7 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   p->tc.inv_att = (float)(1.0 / (double)d->att_len);
   if (const char *e = getenv("MT_TRACE_K")) p->trace_k = atoi(e);
   if (const char *e = getenv("MT_TRACE_S")) p->trace_s = atoi(e);
+  if (const char *e = getenv("MT_CHUNK")) p->chunk = atoi(e);
 
   // ---- per-ray constants in double (a0) ----
   std::vector<float4> ra(p->R), rb(p->R);
@@ -202,8 +203,10 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   const char *ord = getenv("MT_RAY_ORDER");
   if (!(ord && atoi(ord) == 0)) {
     std::vector<uint64_t> key(p->R);
+    double zf = 0.5;   // reference height of the order, as a fraction of z_top
+    if (const char *e = getenv("MT_ORDER_Z")) zf = atof(e);
     for (int64_t q = 0; q < p->R; q++) {
-      double sm = fmin(0.5 * (double)d->z_top / rb[q].x, (double)rb[q].y);
+      double sm = fmin(zf * (double)d->z_top / rb[q].x, (double)rb[q].y);
       double px = ra[q].x + sm * ra[q].z, py = ra[q].y + sm * ra[q].w;
       int ci = (int)floor((px - X0) / ((double)X1 - X0) * (p->nx - 1));
       int cj = (int)floor((py - Y0) / ((double)Y1 - Y0) * (p->ny - 1));
@@ -239,6 +242,7 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   ALLOC(p->d_obase, sizeof(float) * R);
   ALLOC(p->d_perm, sizeof(int32_t) * R);
   ALLOC(p->d_H, sizeof(float) * MC32 * P);
+  ALLOC(p->d_Hlo, sizeof(float) * MC32 * P);
   ALLOC(p->d_G, sizeof(float) * MC32 * P);
   ALLOC(p->d_band, sizeof(float4) * MC);
   ALLOC(p->d_ll, sizeof(double) * MC);
@@ -265,6 +269,7 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   if (e == cudaSuccess && p->R > 0) e = cudaMemcpy(p->d_perm, p->perm.data(), sizeof(int32_t) * p->R, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemset(p->d_G, 0, sizeof(float) * MC32 * P);
   if (e == cudaSuccess) e = cudaMemset(p->d_H, 0, sizeof(float) * MC32 * P);
+  if (e == cudaSuccess) e = cudaMemset(p->d_Hlo, 0, sizeof(float) * MC32 * P);
   if (e == cudaSuccess) e = cudaMemset(p->d_ll, 0, sizeof(double) * MC);
   if (e == cudaSuccess) e = cudaMemset(p->d_ovf_n, 0, sizeof(int) * 4);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -428,6 +433,7 @@ int mt_loglik_heights(mt_problem *p, int32_t C, const float *H, double *ll, floa
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(ll, 0, sizeof(double) * C, s));
   CK(launch_tile(p, C, H, p->d_H, 1, s));
+  CK(cudaMemsetAsync(p->d_Hlo, 0, sizeof(float) * (size_t)(C + 31) / 32 * 32 * p->P, s));   // exact fp32 heights
   CK(launch_trace(p, TRACE_LL, C, p->d_H, p->d_band, p->d_G, ll, nullptr, nullptr, s));
   CK(launch_tile(p, C, p->d_G, dldH, 0, s));
   CK(cudaMemsetAsync(p->d_G, 0, sizeof(float) * (size_t)(C + 31) / 32 * 32 * p->P, s));
@@ -444,6 +450,7 @@ int mt_path_lengths(mt_problem *p, int32_t C, const float *H, float *L, float *O
   p->all_launches++;
   CK(cudaGetLastError());
   CK(launch_tile(p, C, H, p->d_H, 1, s));
+  CK(cudaMemsetAsync(p->d_Hlo, 0, sizeof(float) * (size_t)(C + 31) / 32 * 32 * p->P, s));   // exact fp32 heights
   CK(launch_trace(p, TRACE_PATH, C, p->d_H, p->d_band, nullptr, nullptr, L, O, s));
   return MT_OK;
 }

@@ -17,6 +17,7 @@ constexpr double kTClamp = 10.0;  // R18
 
 struct NodeH {
   float H0, H1;      // heights (fp32, computed in fp64)
+  float L0, L1;      // fp32 residuals: H + L = the fp64 heights to ~1e-14 (HP2)
   double J0, J10, J11;  // ∂H0/∂x0, ∂H1/∂x0, ∂H1/∂x1
 };
 
@@ -34,6 +35,8 @@ __device__ __forceinline__ NodeH node_heights(float x0, float x1, double is0, do
   double h0 = u0 * zt, h1 = h0 + u1 * (zt - h0);
   o.H0 = (float)h0;
   o.H1 = (float)h1;
+  o.L0 = (float)(h0 - (double)o.H0);
+  o.L1 = (float)(h1 - (double)o.H1);
   if (want_jac) {
     const double inv_sqrt_2pi = 0.39894228040143267794;
     double d0 = c0 ? 0.0 : exp(-0.5 * t0 * t0) * inv_sqrt_2pi * is0;
@@ -136,6 +139,8 @@ __global__ void __launch_bounds__(MT_THREADS) k_heights(FinishArgs a, const floa
     NodeH h = node_heights(xc[k], xc[a.N + k], a.inv_sigma[0], a.inv_sigma[1], a.z_top, false);
     a.H[tix(c, 0, k, a.N)] = h.H0;
     a.H[tix(c, 1, k, a.N)] = h.H1;
+    a.Hlo[tix(c, 0, k, a.N)] = h.L0;
+    a.Hlo[tix(c, 1, k, a.N)] = h.L1;
     v.mn0 = fminf(v.mn0, h.H0); v.mx0 = fmaxf(v.mx0, h.H0);
     v.mn1 = fminf(v.mn1, h.H1); v.mx1 = fmaxf(v.mx1, h.H1);
   }
@@ -196,6 +201,8 @@ __global__ void __launch_bounds__(MT_THREADS) k_finish(FinishArgs a) {
       NodeH hn = node_heights(xn0, xn1, a.inv_sigma[0], a.inv_sigma[1], a.z_top, false);
       a.H[t0] = hn.H0;
       a.H[t1] = hn.H1;
+      a.Hlo[t0] = hn.L0;
+      a.Hlo[t1] = hn.L1;
       v.mn0 = fminf(v.mn0, hn.H0); v.mx0 = fmaxf(v.mx0, hn.H0);
       v.mn1 = fminf(v.mn1, hn.H1); v.mx1 = fmaxf(v.mx1, hn.H1);
     } else if (MODE == FIN_LAST) {  // final half kick
@@ -234,6 +241,8 @@ __global__ void __launch_bounds__(MT_THREADS) k_kick_drift(FinishArgs a) {
     NodeH h = node_heights(x0, x1, a.inv_sigma[0], a.inv_sigma[1], a.z_top, false);
     a.H[tix(c, 0, k, N)] = h.H0;
     a.H[tix(c, 1, k, N)] = h.H1;
+    a.Hlo[tix(c, 0, k, N)] = h.L0;
+    a.Hlo[tix(c, 1, k, N)] = h.L1;
     v.mn0 = fminf(v.mn0, h.H0); v.mx0 = fmaxf(v.mx0, h.H0);
     v.mn1 = fminf(v.mn1, h.H1); v.mx1 = fmaxf(v.mx1, h.H1);
   }
@@ -276,6 +285,8 @@ __global__ void __launch_bounds__(MT_THREADS) k_hmc_begin(FinishArgs a, const do
     NodeH h = node_heights(xc[k], xc[N + k], a.inv_sigma[0], a.inv_sigma[1], a.z_top, false);
     a.H[tix(c, 0, k, N)] = h.H0;
     a.H[tix(c, 1, k, N)] = h.H1;
+    a.Hlo[tix(c, 0, k, N)] = h.L0;
+    a.Hlo[tix(c, 1, k, N)] = h.L1;
     v.mn0 = fminf(v.mn0, h.H0); v.mx0 = fmaxf(v.mx0, h.H0);
     v.mn1 = fminf(v.mn1, h.H1); v.mx1 = fmaxf(v.mx1, h.H1);
   }
@@ -376,6 +387,7 @@ static FinishArgs base_args(mt_problem *p, int C) {
   a.G = p->d_G;
   a.ll = p->d_ll;
   a.H = p->d_H;
+  a.Hlo = p->d_Hlo;
   a.band = p->d_band;
   return a;
 }
@@ -385,6 +397,7 @@ cudaError_t launch_heights(mt_problem *p, int C, const float *x, float *H, float
   if (C <= 0) return cudaSuccess;
   FinishArgs a = base_args(p, C);
   a.H = H;
+  a.Hlo = p->d_Hlo;
   a.band = band;
   k_heights<<<C, MT_THREADS, 0, s>>>(a, x);
   p->all_launches++;

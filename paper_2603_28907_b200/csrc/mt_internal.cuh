@@ -56,6 +56,8 @@ struct TraceArgs {
   int64_t rays_per_block;
   int C;                        // chains in this call
   const float *H;               // [C][2][N] heights
+  const float *Hlo;             // fp32 residuals of the fp64 heights (0 for caller heights): the
+                                //   fp64 re-solves of ill-conditioned cells use H + Hlo (HP2)
   const float4 *band;           // [C] (min H0, max H0, min H1, max H1)
   float *G;                     // [C][2][N] ∂ℓ/∂H accumulator (atomic adds)
   double *ll;                   // [C] deviance-centred log-likelihood accumulator
@@ -84,6 +86,7 @@ struct FinishArgs {
   float *mom;                   // [C][P] leapfrog momenta
   const float *eps;             // [C]
   float *H;                     // [C][2N] heights of the updated x (leapfrog)
+  float *Hlo;                   // their fp32 residuals (H + Hlo = fp64 heights)
   float4 *band;                 // [C]
   float *kin;                   // [C] 1/2 |p|^2 after the last half kick
 };
@@ -114,7 +117,7 @@ struct mt_problem {
   int *d_ovf_n = nullptr;       // [4]: count, blocks done, 64-bit cumulative count
   int ovf_cap = 1 << 22;
   int64_t trav_cells = 0;
-  float *d_H = nullptr, *d_G = nullptr;
+  float *d_H = nullptr, *d_G = nullptr, *d_Hlo = nullptr;
   float4 *d_band = nullptr;
   double *d_ll = nullptr;
   // HMC workspace
@@ -123,6 +126,7 @@ struct mt_problem {
   // trace launch shape
   int trace_k = 0;              // chains per block (0 = auto)
   int trace_s = 0;              // ray splits (0 = auto)
+  int chunk = 512;              // chain lanes: rays per block (a Morton-ordered chunk)
   int smemh_limit = 100 * 1024; // stage a 32-chain height tile in smem when it fits
   // measurement
   bool timing = false;

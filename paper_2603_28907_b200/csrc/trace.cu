@@ -177,15 +177,15 @@ struct Fix {
   float u[2], v[2], ig[2];
 };
 
-__device__ __noinline__ Fix fix64(float h00, float h10, float h01, float h11, float Xi, float Xi1,
+__device__ __noinline__ Fix fix64(double h00, double h10, double h01, double h11, float Xi, float Xi1,
                                   float Yj, float Yj1, Ray r, float s, float s1) {
   const double ix = 1.0 / ((double)Xi1 - (double)Xi), iy = 1.0 / ((double)Yj1 - (double)Yj);
   const double u0 = ((double)r.ox + (double)s * (double)r.dx - (double)Xi) * ix;
   const double v0 = ((double)r.oy + (double)s * (double)r.dy - (double)Yj) * iy;
   const double z0 = (double)s * (double)r.dz;
   const double al = (double)r.dx * ix, be = (double)r.dy * iy;
-  const double b = (double)h10 - h00, c = (double)h01 - h00, e = ((double)h11 - h10) - ((double)h01 - h00);
-  const double g0 = ((double)h00 - z0) + u0 * (b + e * v0) + c * v0;
+  const double b = h10 - h00, c = h01 - h00, e = (h11 - h10) - (h01 - h00);
+  const double g0 = (h00 - z0) + u0 * (b + e * v0) + c * v0;
   const double g1 = b * al + c * be + e * (u0 * be + v0 * al) - (double)r.dz;
   const double g2 = e * al * be;
   const double L = (double)s1 - (double)s;
@@ -236,8 +236,10 @@ __device__ __forceinline__ bool solve32(float h00, float h10, float h01, float h
   if (disc > 0.f) q = -0.5f * (g1 + copysignf(disc * rsqrtf(disc), g1));
   const float ta = __fdividef(g0, q), tb = __fdividef(q, g2);       // the two roots (tb = ±inf if g2 = 0)
   if (p0 != (gL > 0.f)) {                         // exactly one crossing
-    float t = (ta > 0.f && ta < Ls) ? ta : tb;
-    t = fminf(fmaxf(t, 0.f), Ls);
+    // the root in [0, Δs]: of the two, the one nearer the interval (rounding
+    // can put the true root just outside when it sits at a cell edge)
+    const float ca = fminf(fmaxf(ta, 0.f), Ls), cb = fminf(fmaxf(tb, 0.f), Ls);
+    const float t = fabsf(ta - ca) <= fabsf(tb - cb) ? ca : cb;
     const float gp = g1 + a2 * t;
     if (fabsf(gp) < GTHR || !(disc > 0.f)) return false;
     B += p0 ? t : Ls - t;
@@ -278,7 +280,7 @@ __shared__ float sgeo[4][MT_MAX_AXIS];   // X, Y, 1/ΔX, 1/ΔY
 // memory at slot [(l*RCAP + m)*MT_THREADS + tid] (conflict-free: consecutive
 // threads, consecutive 16-B words).
 #ifndef MT_RCAP
-#define MT_RCAP 4
+#define MT_RCAP 3
 #endif
 #ifndef MT_CL_MINB
 #define MT_CL_MINB 4
@@ -304,8 +306,8 @@ template <int STRIDE, bool SCAT>
 __device__ __forceinline__ void walk(const Ray &r, const int2 *__restrict__ cells,
                                      const float4 *__restrict__ cgeo, int k, int kend, float s0,
                                      float s_in0, float s_hi, int ny, int N, const float *Hk,
-                                     float *Gk, float4 bd, float &B0, float &B1, float4 *rec,
-                                     int *n, float f0, float f1) {
+                                     const float *Hlo, float *Gk, float4 bd, float &B0, float &B1,
+                                     float4 *rec, int *n, float f0, float f1) {
   float s = s0, ds = s0 - s_in0;
   for (; k < kend; k++) {
     const int2 w = __ldg(cells + k);
@@ -334,7 +336,11 @@ __device__ __forceinline__ void walk(const Ray &r, const int2 *__restrict__ cell
         }
       };
       if (!solve32(h00, h10, h01, h11, cg, za, Ls, r.dz, B, emit)) {
-        const Fix x = fix64(h00, h10, h01, h11, sgeo[0][i], sgeo[0][i + 1], sgeo[1][j], sgeo[1][j + 1], r, s, s1);
+        // fp64 heights = fp32 value + stored residual (chain-interleaved column, stride 32)
+        const float *pl = Hlo + ((size_t)l * N + base) * 32;
+        const Fix x = fix64((double)h00 + pl[0], (double)h10 + pl[ny * 32], (double)h01 + pl[32],
+                            (double)h11 + pl[ny * 32 + 32], sgeo[0][i], sgeo[0][i + 1], sgeo[1][j],
+                            sgeo[1][j + 1], r, s, s1);
         B += x.below;
         for (int m = 0; m < x.n; m++) emit(x.u[m], x.v[m], x.ig[m]);
       }
@@ -632,8 +638,8 @@ __global__ void __launch_bounds__(MT_THREADS) k_trace_defer(TraceArgs a) {
     const int kend = a.trav_off[rr + 1];
     if (s_lo < r.s_exit) {
       k0 = band_entry(a.trav, a.trav_off[rr], kend, s_lo, s_in0);
-      walk<32, false>(r, a.trav, a.trav_geo, k0, kend, s_lo, s_in0, s_hi, ny, N, a.H + off, nullptr, bd,
-                      B0, B1, recs + threadIdx.x, nrec, 0.f, 0.f);
+      walk<32, false>(r, a.trav, a.trav_geo, k0, kend, s_lo, s_in0, s_hi, ny, N, a.H + off, a.Hlo + off,
+                      nullptr, bd, B0, B1, recs + threadIdx.x, nrec, 0.f, 0.f);
     }
     if (MODE == TRACE_LL) {
       float dldO;
@@ -644,8 +650,8 @@ __global__ void __launch_bounds__(MT_THREADS) k_trace_defer(TraceArgs a) {
         scatter_recs<32>(recs + threadIdx.x, nrec, a.G + off, N, ny, f0, f1);
       } else {
         float d0 = s_lo, d1 = s_lo;
-        walk<32, true>(r, a.trav, a.trav_geo, k0, kend, s_lo, s_in0, s_hi, ny, N, a.H + off, a.G + off, bd,
-                       d0, d1, nullptr, nrec, f0, f1);
+        walk<32, true>(r, a.trav, a.trav_geo, k0, kend, s_lo, s_in0, s_hi, ny, N, a.H + off, a.Hlo + off,
+                       a.G + off, bd, d0, d1, nullptr, nrec, f0, f1);
       }
     } else {
       const int64_t o = (int64_t)c * a.R + a.perm[rr];
@@ -716,9 +722,10 @@ __global__ void __launch_bounds__(MT_THREADS) k_trace_rl(TraceArgs a) {
       float B0 = s_lo, B1 = s_lo;
       int nrec[2] = {0, 0};
       const float s_hi = fminf(bd.w / r.dz, r.s_exit);
+      const float *Hlok = a.Hlo + ((size_t)((c0 + k) >> 5) * 2 * N * 32 + ((c0 + k) & 31));
       if (walkable)
-        walk<1, false>(r, a.trav, a.trav_geo, k0, kend, s_lo, s_in0, s_hi, ny, N, Hk, nullptr, bd, B0, B1,
-                       recbuf + tid, nrec, 0.f, 0.f);
+        walk<1, false>(r, a.trav, a.trav_geo, k0, kend, s_lo, s_in0, s_hi, ny, N, Hk, Hlok, nullptr, bd, B0,
+                       B1, recbuf + tid, nrec, 0.f, 0.f);
       if (MODE == TRACE_LL) {
         float dldO;
         llacc[k][tid] += epilogue(r.tb, r.cnt, a.tc, B0, B1, dldO);
@@ -727,8 +734,8 @@ __global__ void __launch_bounds__(MT_THREADS) k_trace_rl(TraceArgs a) {
           scatter_recs<1>(recbuf + tid, nrec, Gk, N, ny, f0, f1);
         } else {
           float d0 = s_lo, d1 = s_lo;
-          walk<1, true>(r, a.trav, a.trav_geo, k0, kend, s_lo, s_in0, s_hi, ny, N, Hk, Gk, bd, d0, d1,
-                        nullptr, nrec, f0, f1);
+          walk<1, true>(r, a.trav, a.trav_geo, k0, kend, s_lo, s_in0, s_hi, ny, N, Hk, Hlok, Gk, bd, d0,
+                        d1, nullptr, nrec, f0, f1);
         }
       } else {
         const int64_t o = (int64_t)(c0 + k) * a.R + __ldg(a.perm + rr);
@@ -873,7 +880,7 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
   if (C <= 0 || p->R <= 0) return cudaSuccess;
   TraceArgs a = base_trace_args(p);
   a.C = C;
-  a.H = H; a.band = band; a.G = G; a.ll = ll; a.Lout = L; a.Oout = O;
+  a.H = H; a.Hlo = p->d_Hlo; a.band = band; a.G = G; a.ll = ll; a.Lout = L; a.Oout = O;
   const bool chain_lanes = p->trace_k == 0 ? C >= 16 : p->trace_k == 32;
   cudaError_t e = cudaSuccess;
   bool rec = p->timing && p->n_rec < (int)p->ev_a.size();
@@ -883,7 +890,7 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
     // small ray chunks (~512 rays = 64 per warp): compact, L1-friendly regions per
     // block and many waves for load balance
     int64_t S = p->trace_s > 0 ? p->trace_s
-                               : std::max(pick_splits(p, groups, 2), (p->R + 511) / 512);
+                               : std::max(pick_splits(p, groups, 2), (p->R + p->chunk - 1) / p->chunk);
     a.rays_per_block = (p->R + S - 1) / S;
     S = (p->R + a.rays_per_block - 1) / a.rays_per_block;
     dim3 grid((unsigned)S, (unsigned)groups);
