@@ -11,9 +11,11 @@ evaluations per second, whole job: N * C * R * L * K / max-over-ranks time.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mt|reference]
   torchrun --nproc-per-node N bench.py --gpus N ...       (N > 1, one rank per GPU)
 
-Scaling is weak: each rank runs --chains-per-gpu chains (default 1024 =
-BASELINE configs[2] Medium), so N = 8 is configs[3]'s 8,192 chains.  L2 is
-flushed (256 MiB write) between timed steps, outside the event pairs.
+Workload = BASELINE configs[3] exactly: the Medium geometry and rays with
+8,192 chains split evenly over the N GPUs (strong scaling: 8,192 chains on
+one GPU at N = 1, 1,024 per GPU at N = 8).  --chains-total changes the total;
+--weak keeps --chains-per-gpu fixed instead.  L2 is flushed (256 MiB write)
+between timed steps, outside the event pairs.
 """
 import argparse
 import json
@@ -38,6 +40,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mt", choices=["mt", "reference"])
+    ap.add_argument("--chains-total", type=int, default=8192)     # configs[3]
+    ap.add_argument("--weak", action="store_true", help="fixed --chains-per-gpu per rank instead")
     ap.add_argument("--chains-per-gpu", type=int, default=1024)
     ap.add_argument("--leapfrog", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
@@ -149,11 +153,11 @@ def run_reference(args):
     v = units / T
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+            "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64", "impl": "reference",
             "data": "synthetic (seeded Medium geometry; counts = Poisson of the oracle's truth)",
             "config": {"workload": "chain_sharded HMC iteration (Medium geometry)", "chains": Cs,
                        "rays": op.R, "leapfrog_steps": L, "params": op.P,
-                       "sample": f"{Cs} chains of the {args.chains_per_gpu}-chain per-GPU shard"},
+                       "sample": f"{Cs} of the {args.chains_total} chains"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
                              "sample": f"{Cs} chains x {op.R} rays x {L} leapfrog steps per HMC iteration"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -182,7 +186,13 @@ def main():
 
     cfg = inputs.CONFIGS["chain_sharded"]
     prob = inputs.make_problem("medium")
-    C, L = args.chains_per_gpu, args.leapfrog
+    if args.weak:
+        C = args.chains_per_gpu
+    else:
+        if args.chains_total % (8 * ws):
+            raise SystemExit(f"--chains-total {args.chains_total} must split into super-chains of 8 per rank")
+        C = args.chains_total // ws
+    L = args.leapfrog
     offset = rank * C
     x0 = inputs.chain_states(prob["x_true"], C, cfg.seed, chain_offset=offset, super_size=8)
     pb = Problem(prob, device=local, max_chains=C)
@@ -207,6 +217,7 @@ def main():
     clocks = ClockSampler() if rank == 0 else None
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     pb.timing_start(args.steps * L + 8)
+    d0 = pb.trace_counters()["deferred"]
     wall0 = time.perf_counter()
     for k in range(args.steps):
         flush.zero_()
@@ -218,6 +229,7 @@ def main():
     ck = clocks.stop(gpu_index=None) if clocks else None
     t_ms = sum(a.elapsed_time(b) for a, b in ev)
     tm = pb.timing_read()
+    cnt = pb.trace_counters()
     t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -228,7 +240,8 @@ def main():
     # dominant kernel (K2 trace): algorithmic FP32 flops per launch / measured launch duration
     work = json.load(open(os.path.join(ROOT, "data", "work_counts.json")))["medium"]
     F = work["flops_per_pair"]
-    avg_trace_ms = tm["trace_ms"] / max(tm["trace_launches"], 1)
+    avg_trace_ms = tm["trace_ms"] / max(tm["trace_launches"], 1)       # K2 main + fp64 follow-up
+    avg_defer_ms = cnt["defer_ms"] / max(tm["trace_launches"], 1)
     achieved = F * C * R / (avg_trace_ms * 1e-3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "trace_traffic.json")
@@ -236,7 +249,10 @@ def main():
         traffic = json.load(open(tpath)).get("bytes_per_launch")
     roofline = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_NOMINAL, "unit": "TFLOP/s",
                 "frac": achieved / FP32_PEAK_NOMINAL, "traffic": traffic,
-                "kernel": "k_trace (K2)", "flops_per_pair": F,
+                "kernel": "K2 = k_trace_cl (chain lanes) + k_trace_defer (fp64 follow-up), per launch pair",
+                "flops_per_pair": F,
+                "defer_share_of_trace": avg_defer_ms / avg_trace_ms,
+                "deferred_pairs_per_launch": (cnt["deferred"] - d0) / max(tm["trace_launches"], 1),
                 "trace_share_of_step": tm["trace_ms"] / t_ms if ws == 1 else None,
                 "avg_trace_launch_ms": avg_trace_ms,
                 "peak_note": "FP32 peak derived: 148 SMs x 128 lanes x 2 x 1.965 GHz (B200_PROFILING.md); "
@@ -276,10 +292,11 @@ def main():
         base = cpu_baseline(args.cpu_seconds)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded Medium geometry; counts = Poisson of the oracle's truth; "
                     "near-posterior chain states)",
-            "config": {"workload": "chain_sharded HMC iteration (BASELINE configs[3] geometry = configs[2] Medium)",
+            "config": {"workload": "chain_sharded HMC iteration (BASELINE configs[3]: Medium geometry and rays, "
+                                   f"{C * ws} chains over {ws} GPU(s))",
                        "chains_per_gpu": C, "global_chains": C * ws, "rays": R, "params": P,
                        "leapfrog_steps": L, "parallelism": f"chain-sharded x{ws}",
                        "phase": "sampling (fixed eps from the 100-iteration dual-averaging warm-up, "

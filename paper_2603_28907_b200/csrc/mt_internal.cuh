@@ -118,6 +118,7 @@ struct mt_problem {
   int ovf_cap = 1 << 22;
   int64_t trav_cells = 0;
   float *d_H = nullptr, *d_G = nullptr, *d_Hlo = nullptr;
+  float *d_Hc = nullptr;        // [min(max_chains, 16)][2N] contiguous heights for the ray-lanes trace
   float4 *d_band = nullptr;
   double *d_ll = nullptr;
   // HMC workspace

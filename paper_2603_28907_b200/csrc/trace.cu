@@ -497,13 +497,9 @@ __global__ void k_build_trav(TraceArgs a, const int32_t *off, int32_t *count, in
 // hot kernel holds no double-precision code and makes no calls (a call forces
 // the ABI's spills into the loop).
 template <int L>
-__device__ __forceinline__ void cw_surface(const float *__restrict__ Hl, int w, int oy, float4 cg,
-                                           float za, float zb, float Ls, float dz, float zmin,
-                                           float zmax, float &B, int &n, int &defer, float4 *rec) {
-  if (zb <= zmin) { B += Ls; return; }            // below the chain's lowest node of this surface
-  if (za >= zmax) return;                         // above its highest node
-  const float *p = Hl + cell_off32(w);
-  const float h00 = __ldg(p), h01 = __ldg(p + 32), h10 = __ldg(p + oy), h11 = __ldg(p + oy + 32);
+__device__ __forceinline__ void cw_solve(float4 h, int w, float4 cg, float za, float zb, float Ls,
+                                         float dz, float &B, int &n, int &defer, float4 *rec) {
+  const float h00 = h.x, h01 = h.y, h10 = h.z, h11 = h.w;
   if (zb <= fminf(fminf(h00, h10), fminf(h01, h11))) { B += Ls; return; }   // bilinear min at a corner
   if (za >= fmaxf(fmaxf(h00, h10), fmaxf(h01, h11))) return;
   const float wbase = __int_as_float(cell_off32(w) >> 5);
@@ -512,6 +508,17 @@ __device__ __forceinline__ void cw_surface(const float *__restrict__ Hl, int w, 
     n++;
   };
   if (!solve32(h00, h10, h01, h11, cg, za, Ls, dz, B, emit)) defer = 1;
+}
+
+template <int L>
+__device__ __forceinline__ void cw_surface(const float *__restrict__ Hl, int w, int oy, float4 cg,
+                                           float za, float zb, float Ls, float dz, float zmin,
+                                           float zmax, float &B, int &n, int &defer, float4 *rec) {
+  if (zb <= zmin) { B += Ls; return; }            // below the chain's lowest node of this surface
+  if (za >= zmax) return;                         // above its highest node
+  const float *p = Hl + cell_off32(w);
+  cw_solve<L>(make_float4(__ldg(p), __ldg(p + 32), __ldg(p + oy), __ldg(p + oy + 32)), w, cg, za, zb, Ls,
+              dz, B, n, defer, rec);
 }
 
 template <int MODE, int NY>
@@ -624,41 +631,61 @@ __global__ void __launch_bounds__(MT_THREADS) k_trace_defer(TraceArgs a) {
   __syncthreads();
   const int n = *(volatile int *)a.ovf_n;
   const int N = a.tc.N, ny = a.tc.ny;
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < min(n, a.ovf_cap); q += gridDim.x * blockDim.x) {
-    const float4 e0 = a.ovf_q[q];
-    const int c = __float_as_int(e0.x), rr = __float_as_int(e0.y);
-    const float s_lo = e0.z, s_hi = e0.w;
-    const Ray r = load_ray(a.ray_a, a.ray_b, rr);
-    const size_t off = (size_t)(c >> 5) * 2 * N * 32 + (c & 31);
-    const float4 bd = a.band[c];
-    float B0 = s_lo, B1 = s_lo;
-    int nrec[2] = {0, 0};
-    int k0 = 0;
-    float s_in0 = 0.f;
-    const int kend = a.trav_off[rr + 1];
-    if (s_lo < r.s_exit) {
-      k0 = band_entry(a.trav, a.trav_off[rr], kend, s_lo, s_in0);
-      walk<32, false>(r, a.trav, a.trav_geo, k0, kend, s_lo, s_in0, s_hi, ny, N, a.H + off, a.Hlo + off,
-                      nullptr, bd, B0, B1, recs + threadIdx.x, nrec, 0.f, 0.f);
-    }
-    if (MODE == TRACE_LL) {
-      float dldO;
-      const float ll = epilogue(r.tb, r.cnt, a.tc, B0, B1, dldO);
-      atomicAdd(a.ll + c, (double)ll);
-      const float f0 = dldO * a.tc.k0, f1 = dldO * a.tc.k1;
-      if (nrec[0] <= RCAP && nrec[1] <= RCAP) {
-        scatter_recs<32>(recs + threadIdx.x, nrec, a.G + off, N, ny, f0, f1);
-      } else {
-        float d0 = s_lo, d1 = s_lo;
-        walk<32, true>(r, a.trav, a.trav_geo, k0, kend, s_lo, s_in0, s_hi, ny, N, a.H + off, a.Hlo + off,
-                       a.G + off, bd, d0, d1, nullptr, nrec, f0, f1);
+  __shared__ double llw[MT_THREADS];
+  const int lane = threadIdx.x & 31, nq = min(n, a.ovf_cap);
+  // warp-uniform loop over 32-entry slices (the ll aggregation below needs the whole warp)
+  for (int q0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; q0 < nq; q0 += gridDim.x * blockDim.x) {
+    const int q = q0 + lane;
+    int c = -1;
+    double ll = 0.0;
+    if (q < nq) {
+      const float4 e0 = a.ovf_q[q];
+      c = __float_as_int(e0.x);
+      const int rr = __float_as_int(e0.y);
+      const float s_lo = e0.z, s_hi = e0.w;
+      const Ray r = load_ray(a.ray_a, a.ray_b, rr);
+      const size_t off = (size_t)(c >> 5) * 2 * N * 32 + (c & 31);
+      const float4 bd = a.band[c];
+      float B0 = s_lo, B1 = s_lo;
+      int nrec[2] = {0, 0};
+      int k0 = 0;
+      float s_in0 = 0.f;
+      const int kend = a.trav_off[rr + 1];
+      if (s_lo < r.s_exit) {
+        k0 = band_entry(a.trav, a.trav_off[rr], kend, s_lo, s_in0);
+        walk<32, false>(r, a.trav, a.trav_geo, k0, kend, s_lo, s_in0, s_hi, ny, N, a.H + off, a.Hlo + off,
+                        nullptr, bd, B0, B1, recs + threadIdx.x, nrec, 0.f, 0.f);
       }
-    } else {
-      const int64_t o = (int64_t)c * a.R + a.perm[rr];
-      a.Lout[3 * o + 0] = B0;
-      a.Lout[3 * o + 1] = B1 - B0;
-      a.Lout[3 * o + 2] = r.s_exit - B1;
-      a.Oout[o] = a.tc.k0 * B0 + a.tc.k1 * B1 + a.obase[rr];
+      if (MODE == TRACE_LL) {
+        float dldO;
+        ll = (double)epilogue(r.tb, r.cnt, a.tc, B0, B1, dldO);
+        const float f0 = dldO * a.tc.k0, f1 = dldO * a.tc.k1;
+        if (nrec[0] <= RCAP && nrec[1] <= RCAP) {
+          scatter_recs<32>(recs + threadIdx.x, nrec, a.G + off, N, ny, f0, f1);
+        } else {
+          float d0 = s_lo, d1 = s_lo;
+          walk<32, true>(r, a.trav, a.trav_geo, k0, kend, s_lo, s_in0, s_hi, ny, N, a.H + off, a.Hlo + off,
+                         a.G + off, bd, d0, d1, nullptr, nrec, f0, f1);
+        }
+      } else {
+        const int64_t o = (int64_t)c * a.R + a.perm[rr];
+        a.Lout[3 * o + 0] = B0;
+        a.Lout[3 * o + 1] = B1 - B0;
+        a.Lout[3 * o + 2] = r.s_exit - B1;
+        a.Oout[o] = a.tc.k0 * B0 + a.tc.k1 * B1 + a.obase[rr];
+      }
+    }
+    if (MODE == TRACE_LL) {   // one double atomic per distinct chain of the warp (a single chain's
+      __syncwarp();           // deferred pairs would otherwise serialise on one address)
+      const unsigned peers = __match_any_sync(0xffffffffu, c);
+      llw[threadIdx.x] = ll;
+      __syncwarp();
+      if (c >= 0 && lane == __ffs(peers) - 1) {
+        double t = 0.0;
+        for (unsigned m = peers; m; m &= m - 1) t += llw[(threadIdx.x & ~31) + __ffs(m) - 1];
+        atomicAdd(a.ll + c, t);
+      }
+      __syncwarp();
     }
   }
   if (n > a.ovf_cap)   // queue overflow: fail loudly (non-finite log-likelihood -> status bit)
@@ -676,93 +703,122 @@ __global__ void __launch_bounds__(MT_THREADS) k_trace_defer(TraceArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// K2, ray lanes (small C): block = K chains whose height and gradient tiles
-// sit in shared memory, thread = ray
+// K2, ray lanes (small C, e.g. the single-chain ray-sharded config): block row
+// = one chain whose heights ([2N] fp32, 32 KiB at n = 64) sit in shared
+// memory; thread = ray (rays Morton-ordered, so a warp's rays walk nearby
+// cells).  Same cell code as the chain lanes; ill-conditioned pairs and pairs
+// with more than RCAP crossings of a surface go to k_trace_defer; the adjoint
+// is a RED.ADD.F32 per corner into the chain's ∂ℓ/∂H column (shared-memory
+// fp32 atomics are CAS loops on sm_100a).
 // ---------------------------------------------------------------------------
-template <int K, int MODE>
-__global__ void __launch_bounds__(MT_THREADS) k_trace_rl(TraceArgs a) {
+template <int MODE, int NY>
+__global__ void __launch_bounds__(MT_THREADS, 4) k_trace_rl(TraceArgs a, const float *__restrict__ Hc) {
   extern __shared__ __align__(16) float smem[];
-  const int ny = a.tc.ny, N = a.tc.N;
-  float *Hs = smem;                                   // [K][2N]
-  float *Gs = Hs + K * 2 * N;                         // [K][2N] (TRACE_LL)
-  float4 *recbuf = reinterpret_cast<float4 *>(smem + ((K * 2 * N * (MODE == TRACE_LL ? 2 : 1) + 3) & ~3));
-  __shared__ double red[MT_THREADS / 32][K];
-  __shared__ float4 bds[K];
-  __shared__ float llacc[K][MT_THREADS];
-  const int tid = threadIdx.x;
-  const int c0 = blockIdx.y * K;
-  const int nk = min(K, a.C - c0);
-  load_geometry(a, sgeo[0], sgeo[1], sgeo[2], sgeo[3]);
-  for (int k = tid; k < nk * 2 * N; k += blockDim.x) {
-    int kc = k / (2 * N), m = k - kc * 2 * N;
-    Hs[k] = __ldg(a.H + tix(c0 + kc, m / N, m % N, N));
+  __shared__ double red[MT_THREADS / 32];
+  const int ny = NY ? NY : a.tc.ny, N = a.tc.N;
+  const int tid = threadIdx.x, c = blockIdx.y;
+  float *Hs = smem;                                                            // [2N]
+  float4 *rec = reinterpret_cast<float4 *>(smem + ((2 * N + 3) & ~3)) + tid;   // [2*RCAP][MT_THREADS]
+  {
+    const float *src = Hc + (size_t)c * 2 * N;
+    for (int k = tid; k < 2 * N; k += MT_THREADS) Hs[k] = __ldg(src + k);
   }
-  if (MODE == TRACE_LL)
-    for (int k = tid; k < K * 2 * N; k += blockDim.x) Gs[k] = 0.f;
-  if (tid < K) bds[tid] = tid < nk ? a.band[c0 + tid] : make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int k = 0; k < K; k++) llacc[k][tid] = 0.f;
+  load_geometry(a, sgeo[0], sgeo[1], sgeo[2], sgeo[3]);
+  const float4 bd = __ldg(a.band + c);
+  const size_t coff = (size_t)(c >> 5) * 2 * N * 32 + (c & 31);
+  float *G0 = a.G + coff, *G1 = G0 + (size_t)N * 32;
   __syncthreads();
-  float zlo = 3.0e38f;
-  for (int k = 0; k < nk; k++) zlo = fminf(zlo, bds[k].x);
-
-  const int64_t r_begin = (int64_t)blockIdx.x * a.rays_per_block;
-  const int64_t r_end = min(a.R, r_begin + a.rays_per_block);
-  for (int64_t rr = r_begin + tid; rr < r_end; rr += blockDim.x) {
-    const Ray r = load_ray(a.ray_a, a.ray_b, rr);
-    const float s_lo = fminf(zlo / r.dz, r.s_exit);
-    const bool walkable = s_lo < r.s_exit;
-    const int kend = __ldg(a.trav_off + rr + 1);
-    float s_in0 = 0.f;
-    const int k0 = walkable ? band_entry(a.trav, __ldg(a.trav_off + rr), kend, s_lo, s_in0) : 0;
-#pragma unroll 1
-    for (int k = 0; k < nk; k++) {
-      const float *Hk = Hs + k * 2 * N;
-      float *Gk = Gs + k * 2 * N;
-      const float4 bd = bds[k];
-      float B0 = s_lo, B1 = s_lo;
-      int nrec[2] = {0, 0};
-      const float s_hi = fminf(bd.w / r.dz, r.s_exit);
-      const float *Hlok = a.Hlo + ((size_t)((c0 + k) >> 5) * 2 * N * 32 + ((c0 + k) & 31));
-      if (walkable)
-        walk<1, false>(r, a.trav, a.trav_geo, k0, kend, s_lo, s_in0, s_hi, ny, N, Hk, Hlok, nullptr, bd, B0,
-                       B1, recbuf + tid, nrec, 0.f, 0.f);
-      if (MODE == TRACE_LL) {
-        float dldO;
-        llacc[k][tid] += epilogue(r.tb, r.cnt, a.tc, B0, B1, dldO);
-        const float f0 = dldO * a.tc.k0, f1 = dldO * a.tc.k1;
-        if (nrec[0] <= RCAP && nrec[1] <= RCAP) {
-          scatter_recs<1>(recbuf + tid, nrec, Gk, N, ny, f0, f1);
-        } else {
-          float d0 = s_lo, d1 = s_lo;
-          walk<1, true>(r, a.trav, a.trav_geo, k0, kend, s_lo, s_in0, s_hi, ny, N, Hk, Hlok, Gk, bd, d0,
-                        d1, nullptr, nrec, f0, f1);
+  float llacc = 0.f;
+  const int r_begin = blockIdx.x * (int)a.rays_per_block;
+  const int r_end = min((int)a.R, r_begin + (int)a.rays_per_block);
+  for (int rr = r_begin + tid; rr < r_end; rr += MT_THREADS) {
+    const float2 rb = __ldg(reinterpret_cast<const float2 *>(a.ray_b + rr));
+    const float dz = rb.x, s_exit = rb.y;
+    const float s_lo = fminf(__fdividef(bd.x, dz) * (1.f - 1e-6f), s_exit);
+    const float s_hi = fminf(__fdividef(bd.w, dz) * (1.f + 1e-6f), s_exit);
+    float B0 = s_lo, B1 = s_lo;
+    int n0 = 0, n1 = 0, defer = 0;
+    if (s_lo < s_exit) {
+      const int kend = __ldg(a.trav_off + rr + 1);
+      float s_in0;
+      const int k0 = band_entry(a.trav, __ldg(a.trav_off + rr), kend, s_lo, s_in0);
+      float s = s_lo, za = s_lo * dz;
+      // cell geometry on the fly (thread-private walks: the stored per-cell
+      // geometry would triple the uncoalesced per-cell traffic)
+      const float2 ro = __ldg(reinterpret_cast<const float2 *>(a.ray_a + rr));
+      const float2 rd = __ldg(reinterpret_cast<const float2 *>(a.ray_a + rr) + 1);
+      int2 w = __ldg(a.trav + k0);
+      for (int k = k0; k < kend; k++) {
+        const int2 wn = __ldg(a.trav + min(k + 1, kend - 1));   // prefetch the next stored cell
+        const int ci = cell_i(w.x), cj = cell_j(w.x);
+        const float ix = sgeo[2][ci], iy = sgeo[3][cj];
+        const float4 cg = make_float4((fmaf(s, rd.x, ro.x) - sgeo[0][ci]) * ix, (fmaf(s, rd.y, ro.y) - sgeo[1][cj]) * iy,
+                                      rd.x * ix, rd.y * iy);
+        const float s1 = __int_as_float(w.y);
+        const float zb = s1 * dz, Ls = s1 - s;
+        const int base = (int)(cell_off32(w.x) >> 5);
+        if (zb <= bd.x) B0 += Ls;
+        else if (za < bd.y) {
+          const float *p = Hs + base;
+          cw_solve<0>(make_float4(p[0], p[1], p[ny], p[ny + 1]), w.x, cg, za, zb, Ls, dz, B0, n0, defer, rec);
         }
-      } else {
-        const int64_t o = (int64_t)(c0 + k) * a.R + __ldg(a.perm + rr);
-        a.Lout[3 * o + 0] = B0;
-        a.Lout[3 * o + 1] = B1 - B0;
-        a.Lout[3 * o + 2] = r.s_exit - B1;
-        a.Oout[o] = a.tc.k0 * B0 + a.tc.k1 * B1 + a.obase[rr];
+        if (zb <= bd.z) B1 += Ls;
+        else if (za < bd.w) {
+          const float *p = Hs + N + base;
+          cw_solve<1>(make_float4(p[0], p[1], p[ny], p[ny + 1]), w.x, cg, za, zb, Ls, dz, B1, n1, defer, rec);
+        }
+        if (s1 >= s_hi) break;
+        s = s1;
+        za = zb;
+        w = wn;
       }
+    }
+    if (defer || n0 > RCAP || n1 > RCAP) {             // rare: the whole pair goes to k_trace_defer
+      const int q = atomicAdd(a.ovf_n, 1);
+      if (q < a.ovf_cap) a.ovf_q[q] = make_float4(__int_as_float(c), __int_as_float(rr), s_lo, s_hi);
+      continue;
+    }
+    if (MODE == TRACE_LL) {
+      const float2 rt = __ldg(reinterpret_cast<const float2 *>(a.ray_b + rr) + 1);
+      float dldO;
+      llacc += epilogue(rt.x, rt.y, a.tc, B0, B1, dldO);
+      const float f0 = dldO * a.tc.k0, f1 = dldO * a.tc.k1;
+      const int oy = ny * 32;
+      for (int m = 0; m < n0; m++) {
+        const float4 q = rec[m * MT_THREADS];
+        const float w = f0 * q.w, u = q.y, v = q.z;
+        float *pg = G0 + ((unsigned)__float_as_int(q.x) << 5);
+        atomicAdd(pg, w * (1.f - u) * (1.f - v));
+        atomicAdd(pg + oy, w * u * (1.f - v));
+        atomicAdd(pg + 32, w * (1.f - u) * v);
+        atomicAdd(pg + oy + 32, w * u * v);
+      }
+      for (int m = 0; m < n1; m++) {
+        const float4 q = rec[(RCAP + m) * MT_THREADS];
+        const float w = f1 * q.w, u = q.y, v = q.z;
+        float *pg = G1 + ((unsigned)__float_as_int(q.x) << 5);
+        atomicAdd(pg, w * (1.f - u) * (1.f - v));
+        atomicAdd(pg + oy, w * u * (1.f - v));
+        atomicAdd(pg + 32, w * (1.f - u) * v);
+        atomicAdd(pg + oy + 32, w * u * v);
+      }
+    } else {
+      const int64_t o = (int64_t)c * a.R + __ldg(a.perm + rr);
+      a.Lout[3 * o + 0] = B0;
+      a.Lout[3 * o + 1] = B1 - B0;
+      a.Lout[3 * o + 2] = s_exit - B1;
+      a.Oout[o] = a.tc.k0 * B0 + a.tc.k1 * B1 + a.obase[rr];
     }
   }
   if (MODE == TRACE_LL) {
-    const int lane = tid & 31, wid = tid >> 5;
-    for (int k = 0; k < nk; k++) {
-      float v = llacc[k][tid];
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) red[wid][k] = (double)v;
-    }
+    double v = (double)llacc;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((tid & 31) == 0) red[tid >> 5] = v;
     __syncthreads();
-    if (tid < nk) {
-      double s = 0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += red[w][tid];
-      atomicAdd(a.ll + c0 + tid, s);
-    }
-    for (int k = tid; k < nk * 2 * N; k += blockDim.x) {
-      float v = Gs[k];
-      int kc = k / (2 * N), m = k - kc * 2 * N;
-      if (v != 0.f) atomicAdd(a.G + tix(c0 + kc, m / N, m % N, N), v);
+    if (tid == 0) {
+      double t = 0;
+      for (int w = 0; w < MT_THREADS / 32; w++) t += red[w];
+      atomicAdd(a.ll + c, t);
     }
   }
 }
@@ -849,22 +905,25 @@ static cudaError_t launch_cl_ny(const TraceArgs &a, int ny, dim3 grid, size_t sm
   }
 }
 
-template <int K, int MODE>
-static cudaError_t launch_rl(const TraceArgs &a, dim3 grid, size_t smem, cudaStream_t s) {
+template <int MODE, int NY>
+static cudaError_t launch_rl(const TraceArgs &a, const float *Hc, dim3 grid, size_t smem, cudaStream_t s) {
   static size_t done[16] = {0};
-  cudaError_t e = set_smem(k_trace_rl<K, MODE>, smem, done);
+  cudaError_t e = set_smem(k_trace_rl<MODE, NY>, smem, done);
   if (e != cudaSuccess) return e;
-  k_trace_rl<K, MODE><<<grid, MT_THREADS, smem, s>>>(a);
+  k_trace_rl<MODE, NY><<<grid, MT_THREADS, smem, s>>>(a, Hc);
   return cudaGetLastError();
 }
 
-static int pick_k(const mt_problem *p, int C) {
-  if (p->trace_k > 0 && p->trace_k <= 8) return p->trace_k;
-  size_t per_chain = (size_t)16 * p->N;   // H + G tiles, fp32
-  int k = 8;
-  while (k > 1 && (size_t)k * per_chain > 40 * 1024) k >>= 1;
-  while (k > 1 && (C + k - 1) / k < p->num_sms) k >>= 1;
-  return k;
+template <int MODE>
+static cudaError_t launch_rl_ny(const TraceArgs &a, const float *Hc, int ny, dim3 grid, size_t smem,
+                                cudaStream_t s) {
+  switch (ny) {
+    case 8: return launch_rl<MODE, 8>(a, Hc, grid, smem, s);
+    case 16: return launch_rl<MODE, 16>(a, Hc, grid, smem, s);
+    case 32: return launch_rl<MODE, 32>(a, Hc, grid, smem, s);
+    case 64: return launch_rl<MODE, 64>(a, Hc, grid, smem, s);
+    default: return launch_rl<MODE, 0>(a, Hc, grid, smem, s);
+  }
 }
 
 static int64_t pick_splits(const mt_problem *p, int64_t groups, int64_t blocks_per_sm) {
@@ -906,29 +965,26 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
       p->all_launches++;
     }
   } else {
-    int K = pick_k(p, C);
-    int groups = (C + K - 1) / K;
-    int64_t S = pick_splits(p, groups, 2);
+    // contiguous [C][2N] copy of the chains' heights for the shared-memory tiles
+    e = launch_tile(p, C, H, p->d_Hc, 0, s);
+    int64_t S = p->trace_s > 0 ? p->trace_s : std::max<int64_t>(1, (int64_t)p->num_sms * 4 * 4 / C);
+    S = std::min<int64_t>(S, (p->R + 255) / 256);
     a.rays_per_block = (p->R + S - 1) / S;
     S = (p->R + a.rays_per_block - 1) / a.rays_per_block;
-    dim3 grid((unsigned)S, (unsigned)groups);
-    size_t smem = (size_t)4 * (((size_t)K * 2 * p->N * (mode == TRACE_LL ? 2 : 1) + 3) & ~(size_t)3) +
-                  (size_t)16 * 2 * RCAP * MT_THREADS;
-#define MT_DISPATCH(KK)                                                         \
-  case KK:                                                                      \
-    e = mode == TRACE_LL ? launch_rl<KK, TRACE_LL>(a, grid, smem, s)            \
-                         : launch_rl<KK, TRACE_PATH>(a, grid, smem, s);         \
-    break;
-    switch (K) {
-      MT_DISPATCH(1)
-      MT_DISPATCH(2)
-      MT_DISPATCH(4)
-      MT_DISPATCH(8)
-      default: e = cudaErrorInvalidValue;
+    dim3 grid((unsigned)S, (unsigned)C);
+    size_t smem = (size_t)4 * ((2 * p->N + 3) & ~3) + (size_t)16 * 2 * RCAP * MT_THREADS;
+    if (e == cudaSuccess)
+      e = mode == TRACE_LL ? launch_rl_ny<TRACE_LL>(a, p->d_Hc, p->ny, grid, smem, s)
+                           : launch_rl_ny<TRACE_PATH>(a, p->d_Hc, p->ny, grid, smem, s);
+    if (rec) cudaEventRecord(p->ev_m[p->n_rec], s);
+    if (e == cudaSuccess) {
+      const size_t dsm = (size_t)16 * 2 * RCAP * MT_THREADS;
+      if (mode == TRACE_LL) k_trace_defer<TRACE_LL><<<p->num_sms, MT_THREADS, dsm, s>>>(a);
+      else k_trace_defer<TRACE_PATH><<<p->num_sms, MT_THREADS, dsm, s>>>(a);
+      e = cudaGetLastError();
+      p->all_launches += 2;
     }
-#undef MT_DISPATCH
   }
-  if (rec && !chain_lanes) cudaEventRecord(p->ev_m[p->n_rec], s);
   if (rec) { cudaEventRecord(p->ev_b[p->n_rec], s); p->n_rec++; }
   p->all_launches++;
   p->trace_launches++;

@@ -50,7 +50,8 @@ def sampling_eps(name):
 # ---------------------------------------------------------------------------
 # traversal (integer, bit-exact)
 # ---------------------------------------------------------------------------
-@pytest.mark.parametrize("name,nsample", [("tiny", None), ("small", 3000), ("medium", 2000)])
+@pytest.mark.parametrize("name,nsample", [("tiny", None), ("small", 3000), ("medium", 2000),
+                                          ("ray_sharded", 1500)])
 def test_traversal_bit_exact(gpu, oracle_problem, name, nsample):
     mp, op = gpu(name), oracle_problem(name)
     rays = range(op.R) if nsample is None else np.random.default_rng(7).choice(op.R, nsample, replace=False)
@@ -69,7 +70,7 @@ def identical_heights(prob, C, seed, scale=2.0):
     return inputs.perturbed_heights(prob["H_true"], C, seed, scale=scale)
 
 
-@pytest.mark.parametrize("name,C", [("tiny", 4), ("small", 8), ("medium", 2)])
+@pytest.mark.parametrize("name,C", [("tiny", 4), ("small", 8), ("medium", 2), ("ray_sharded", 1)])
 def test_path_lengths_identical_heights(gpu, oracle_problem, name, C):
     mp, op = gpu(name), oracle_problem(name)
     H = identical_heights(op.prob, C, 100 + C)
@@ -82,7 +83,7 @@ def test_path_lengths_identical_heights(gpu, oracle_problem, name, C):
     assert np.allclose(O_d.cpu().numpy(), O_o, rtol=2e-5)
 
 
-@pytest.mark.parametrize("name,C", [("tiny", 4), ("small", 8), ("medium", 2)])
+@pytest.mark.parametrize("name,C", [("tiny", 4), ("small", 8), ("medium", 2), ("ray_sharded", 1)])
 def test_loglik_and_adjoint_identical_heights(gpu, oracle_problem, name, C):
     mp, op = gpu(name), oracle_problem(name)
     H = identical_heights(op.prob, C, 200 + C, scale=1.0)
@@ -125,6 +126,19 @@ def test_logpost_grad_end_to_end(gpu, oracle_problem, name):
     x = inputs.chain_states(op.prob["x_true"], cfg.chains, cfg.seed)
     logp, grad = mp.logpost_grad(torch.from_numpy(x).to(DEV))
     fails = e2e_check(mp, op, x, np.arange(cfg.chains), logp.cpu().numpy(), grad.cpu().numpy())
+    assert not fails, fails
+
+
+def test_logpost_grad_ray_sharded_full_size(gpu, oracle_problem):
+    """configs[4] at full size (4,194,304 rays, 8,192 params, one chain): the
+    single-chain ray-lanes path.  This chain has crossings with |g'| ~ 1e-5, where
+    ∇ₓ moves by 1.2e-2 (relative) between fp64 and fp32-rounded heights
+    (tools/e2e_diag.py): the fp64 re-solves must use the fp64 heights (HP2)."""
+    mp, op = gpu("ray_sharded"), oracle_problem("ray_sharded")
+    cfg = inputs.CONFIGS["ray_sharded"]
+    x = inputs.chain_states(op.prob["x_true"], cfg.chains, cfg.seed)
+    logp, grad = mp.logpost_grad(torch.from_numpy(x).to(DEV))
+    fails = e2e_check(mp, op, x, np.array([0]), logp.cpu().numpy(), grad.cpu().numpy())
     assert not fails, fails
 
 
