@@ -46,7 +46,7 @@ enum {
   MT_EINVAL = 1, /* bad descriptor / argument (message says which) */
   MT_ENOMEM = 2, /* device or host allocation failed */
   MT_ECUDA = 3,  /* CUDA runtime error (message holds cudaGetErrorString) */
-  MT_ENCCL = 4,  /* reserved: in-library collectives */
+  MT_ENCCL = 4,  /* NCCL error in the in-library communicator (message holds ncclGetErrorString) */
   MT_ESTATE = 5  /* call not valid in the current state */
 };
 
@@ -140,6 +140,27 @@ int mt_draw_momenta(mt_problem *p, int32_t C, float *mom, uint64_t seed, uint64_
 int mt_hmc_step(mt_problem *p, int32_t C, float *x, double *logp, float *grad, const float *eps,
                 int32_t L, uint64_t seed, uint64_t iter, uint64_t chain_offset, float *accept_prob,
                 int32_t *accepted, int32_t *status, mt_stream stream);
+
+/* ---- ray sharding over GPUs (BASELINE configs[4]) ---------
+ * Rays are independent given a chain's heights, so a problem created with a
+ * ray shard computes partial sums; with a communicator attached, every
+ * per-evaluation call (mt_logpost_grad, and each of the L evaluations inside
+ * mt_leapfrog / mt_hmc_step) all-reduces (SUM) the per-chain [logp, grad]
+ * in-stream with NCCL over NVLink before the kick that consumes them, so all
+ * ranks hold identical (replicated) chain states and trajectories.  The prior
+ * term is added by the shard with ray_lo == 0 only.
+ *
+ * mt_comm_unique_id: an NCCL unique id (128 bytes, host) on one rank; the
+ *   caller broadcasts it (e.g. torch.distributed.broadcast_object_list).
+ * mt_attach_comm: every rank (one process per GPU, the problem's device)
+ *   creates the communicator of `world` ranks from that id (collective,
+ *   synchronous; NCCL is loaded from the already-loaded libnccl.so.2 of the
+ *   process, else the system one).  Replaces any attached communicator.
+ * mt_detach_comm: destroy it (also done by mt_problem_destroy).
+ * Errors: MT_EINVAL, MT_ENCCL (NCCL missing or failing). */
+int mt_comm_unique_id(void *uid128);
+int mt_attach_comm(mt_problem *p, const void *uid128, int32_t rank, int32_t world);
+int mt_detach_comm(mt_problem *p);
 
 /* Per-iteration sampler statistics (step-size adaptation and R-hat, P:652-653,
  * P:671-687; readings R20/R21).  Any of the three groups may be skipped by

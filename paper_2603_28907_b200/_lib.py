@@ -43,7 +43,7 @@ EXPORTS = [
     "mt_prior_constants", "mt_logpost_grad", "mt_leapfrog", "mt_draw_momenta", "mt_hmc_step",
     "mt_stats_update", "mt_rhat_partials", "mt_heights", "mt_loglik_heights", "mt_path_lengths", "mt_debug_traversal", "mt_philox",
     "mt_philox_curand", "mt_timing_start", "mt_timing_read", "mt_trace_counters", "mt_measure_fp32_peak",
-    "mt_last_error",
+    "mt_last_error", "mt_comm_unique_id", "mt_attach_comm", "mt_detach_comm",
 ]
 
 _lib = None
@@ -78,6 +78,9 @@ def lib():
             "mt_timing_start": ([vp, i32], ct.c_int),
             "mt_timing_read": ([vp, vp, vp, vp, vp], ct.c_int),
             "mt_trace_counters": ([vp, vp, vp], ct.c_int),
+            "mt_comm_unique_id": ([vp], ct.c_int),
+            "mt_attach_comm": ([vp, vp, i32, i32], ct.c_int),
+            "mt_detach_comm": ([vp], ct.c_int),
             "mt_measure_fp32_peak": ([i32, vp, vp], ct.c_int),
             "mt_last_error": ([], ct.c_char_p),
         }
@@ -295,12 +298,30 @@ class Problem:
                "mt_timing_read")
         return dict(trace_ms=ms.value, trace_launches=n.value, pairs=pairs.value, all_launches=alln.value)
 
+    def attach_comm(self, uid: bytes, rank: int, world: int):
+        """Create the in-library NCCL communicator for ray sharding (collective over
+        `world` ranks; uid from comm_unique_id() on one rank, broadcast by the caller)."""
+        if len(uid) != 128:
+            raise MTError("NCCL unique id must be 128 bytes")
+        buf = ct.create_string_buffer(uid, 128)
+        _check(lib().mt_attach_comm(self.h, buf, rank, world), "mt_attach_comm")
+
+    def detach_comm(self):
+        _check(lib().mt_detach_comm(self.h), "mt_detach_comm")
+
     def trace_counters(self):
         """Cumulative deferred chain x ray pairs (fp64 follow-up kernel) and the
         device time of the follow-up launches in the last timed region (ms)."""
         n, ms = ct.c_int64(), ct.c_double()
         _check(lib().mt_trace_counters(self.h, ct.byref(n), ct.byref(ms)), "mt_trace_counters")
         return dict(deferred=n.value, defer_ms=ms.value)
+
+
+def comm_unique_id() -> bytes:
+    """An NCCL unique id (128 bytes) for Problem.attach_comm."""
+    buf = ct.create_string_buffer(128)
+    _check(lib().mt_comm_unique_id(buf), "mt_comm_unique_id")
+    return buf.raw
 
 
 def philox(ctr, key, use_curand: bool = False, stream=None):

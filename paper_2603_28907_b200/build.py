@@ -29,7 +29,7 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return SO
-    cmd = [NVCC, *FLAGS, "-shared", "-o", SO, *sources(), "-lcudart"]
+    cmd = [NVCC, *FLAGS, "-shared", "-o", SO, *sources(), "-lcudart", "-ldl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))

@@ -288,6 +288,7 @@ int mt_problem_destroy(mt_problem *p) {
   if (!p) return MT_OK;
   DevGuard g(p->device);
   cudaDeviceSynchronize();
+  comm_detach(p);
   free_all(p);
   delete p;
   return MT_OK;
@@ -303,6 +304,19 @@ int mt_prior_constants(const mt_problem *p, double sigma[2], double logdetQ[2]) 
   return MT_OK;
 }
 
+// Ray sharding with an attached communicator: one evaluation = trace of this
+// shard + chain rule / prior (shard 0) -> partial [logp, grad] -> in-stream
+// NCCL SUM all-reduce -> full [logp, grad] on every rank.
+static int eval_sharded(mt_problem *p, int C, float *x, double *logp, float *grad, int32_t *status,
+                        cudaStream_t s) {
+  CK(launch_trace(p, TRACE_LL, C, p->d_H, p->d_band, p->d_G, p->d_ll, nullptr, nullptr, s));
+  CK(launch_finish(p, FIN_PLAIN, C, x, grad, logp, status, nullptr, nullptr, nullptr, s));
+  std::string why;
+  if (comm_allreduce_logp_grad(p, C, logp, grad, s, why) != cudaSuccess)
+    return set_err(MT_ENCCL, "ncclAllReduce: %s", why.c_str());
+  return MT_OK;
+}
+
 int mt_logpost_grad(mt_problem *p, int32_t C, const float *x, double *logp, float *grad,
                     int32_t *status, mt_stream stream) {
   if (int r = check_chains(p, C)) return r;
@@ -311,9 +325,22 @@ int mt_logpost_grad(mt_problem *p, int32_t C, const float *x, double *logp, floa
   DevGuard g(p->device);
   cudaStream_t s = (cudaStream_t)stream;
   CK(launch_heights(p, C, x, p->d_H, p->d_band, s));
+  if (p->comm) return eval_sharded(p, C, const_cast<float *>(x), logp, grad, status, s);
   CK(launch_trace(p, TRACE_LL, C, p->d_H, p->d_band, p->d_G, p->d_ll, nullptr, nullptr, s));
   CK(launch_finish(p, FIN_PLAIN, C, const_cast<float *>(x), grad, logp, status, nullptr, nullptr,
                    nullptr, s));
+  return MT_OK;
+}
+
+// L leapfrog evaluations with all-reduced gradients (x, mom already carry the
+// first half kick + drift and d_H the heights of the drifted x).
+static int leapfrog_sharded(mt_problem *p, int C, float *x, float *mom, double *logp, float *grad,
+                            int32_t *status, const float *eps, int L, cudaStream_t s) {
+  for (int step = 1; step <= L; step++) {
+    if (int r = eval_sharded(p, C, x, logp, grad, status, s)) return r;
+    if (step < L) CK(launch_kick(p, KICK_FULL_DRIFT, C, x, mom, grad, eps, nullptr, s));
+    else CK(launch_kick(p, KICK_HALF_LAST, C, x, mom, grad, eps, p->d_kin1, s));
+  }
   return MT_OK;
 }
 
@@ -328,6 +355,7 @@ int mt_leapfrog(mt_problem *p, int32_t C, float *x, float *mom, double *logp, fl
   DevGuard g(p->device);
   cudaStream_t s = (cudaStream_t)stream;
   CK(launch_kick_drift(p, C, x, mom, grad, eps, s));
+  if (p->comm) return leapfrog_sharded(p, C, x, mom, logp, grad, nullptr, eps, L, s);
   for (int step = 1; step <= L; step++) {
     CK(launch_trace(p, TRACE_LL, C, p->d_H, p->d_band, p->d_G, p->d_ll, nullptr, nullptr, s));
     CK(launch_finish(p, step < L ? FIN_STEP : FIN_LAST, C, x, grad, logp, nullptr, mom, eps,
@@ -358,12 +386,41 @@ int mt_hmc_step(mt_problem *p, int32_t C, float *x, double *logp, float *grad, c
   DevGuard g(p->device);
   cudaStream_t s = (cudaStream_t)stream;
   CK(launch_hmc_begin(p, C, x, logp, grad, eps, seed, iter, chain_offset, s));
+  if (p->comm) {
+    if (int r = leapfrog_sharded(p, C, x, p->d_mom, logp, grad, status, eps, L, s)) return r;
+    CK(launch_hmc_end(p, C, x, logp, grad, seed, iter, chain_offset, accept_prob, accepted, status, s));
+    return MT_OK;
+  }
   for (int step = 1; step <= L; step++) {
     CK(launch_trace(p, TRACE_LL, C, p->d_H, p->d_band, p->d_G, p->d_ll, nullptr, nullptr, s));
     CK(launch_finish(p, step < L ? FIN_STEP : FIN_LAST, C, x, grad, logp, status, p->d_mom, eps,
                      p->d_kin1, s));
   }
   CK(launch_hmc_end(p, C, x, logp, grad, seed, iter, chain_offset, accept_prob, accepted, status, s));
+  return MT_OK;
+}
+
+int mt_comm_unique_id(void *uid128) {
+  if (!uid128) return set_err(MT_EINVAL, "uid buffer is NULL");
+  std::string why;
+  if (!comm_unique_id(uid128, why)) return set_err(MT_ENCCL, "ncclGetUniqueId: %s", why.c_str());
+  return MT_OK;
+}
+
+int mt_attach_comm(mt_problem *p, const void *uid128, int32_t rank, int32_t world) {
+  if (!p || !uid128) return set_err(MT_EINVAL, "NULL argument");
+  if (world < 1 || rank < 0 || rank >= world) return set_err(MT_EINVAL, "rank %d / world %d", rank, world);
+  DevGuard g(p->device);
+  std::string why;
+  if (!comm_attach(p, uid128, rank, world, why)) return set_err(MT_ENCCL, "ncclCommInitRank: %s", why.c_str());
+  return MT_OK;
+}
+
+int mt_detach_comm(mt_problem *p) {
+  if (!p) return set_err(MT_EINVAL, "problem is NULL");
+  DevGuard g(p->device);
+  cudaDeviceSynchronize();
+  comm_detach(p);
   return MT_OK;
 }
 

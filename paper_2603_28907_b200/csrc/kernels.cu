@@ -224,17 +224,28 @@ __global__ void __launch_bounds__(MT_THREADS) k_finish(FinishArgs a) {
   }
 }
 
-// first half kick + drift + heights: p += ε/2 g; x += ε p; H(x)
-__global__ void __launch_bounds__(MT_THREADS) k_kick_drift(FinishArgs a) {
+// Leapfrog kicks from a stored gradient (R19):
+//   KICK_HALF_DRIFT  p += ε/2 g; x += ε p; H(x)   (first step of mt_leapfrog)
+//   KICK_FULL_DRIFT  p += ε g;   x += ε p; H(x)   (ray sharding: after the all-reduce)
+//   KICK_HALF_LAST   p += ε/2 g; kinetic ½|p|²     (ray sharding: last step)
+// The arithmetic is k_finish<FIN_STEP / FIN_LAST>'s, so a one-rank
+// communicator reproduces the unsharded trajectory exactly.
+template <int MODE>
+__global__ void __launch_bounds__(MT_THREADS) k_kick(FinishArgs a) {
   const int c = blockIdx.x, N = a.N;
   float *xc = a.x + (size_t)c * a.P, *pc = a.mom + (size_t)c * a.P;
   const float *gc = a.grad + (size_t)c * a.P;
   const float eps = a.eps[c];
+  const float f = MODE == KICK_FULL_DRIFT ? eps : 0.5f * eps;
   BlockRed v = {3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f, 0.0, 0.0, 0};
   for (int k = threadIdx.x; k < N; k += blockDim.x) {
-    float p0 = pc[k] + 0.5f * eps * gc[k], p1 = pc[N + k] + 0.5f * eps * gc[N + k];
+    float p0 = pc[k] + f * gc[k], p1 = pc[N + k] + f * gc[N + k];
     pc[k] = p0;
     pc[N + k] = p1;
+    if (MODE == KICK_HALF_LAST) {
+      v.s1 += 0.5 * ((double)p0 * p0 + (double)p1 * p1);
+      continue;
+    }
     float x0 = xc[k] + eps * p0, x1 = xc[N + k] + eps * p1;
     xc[k] = x0;
     xc[N + k] = x1;
@@ -247,7 +258,10 @@ __global__ void __launch_bounds__(MT_THREADS) k_kick_drift(FinishArgs a) {
     v.mn1 = fminf(v.mn1, h.H1); v.mx1 = fmaxf(v.mx1, h.H1);
   }
   BlockRed r = block_reduce(v);
-  if (threadIdx.x == 0) a.band[c] = make_float4(r.mn0, r.mx0, r.mn1, r.mx1);
+  if (threadIdx.x == 0) {
+    if (MODE == KICK_HALF_LAST) a.kin[c] = (float)r.s1;
+    else a.band[c] = make_float4(r.mn0, r.mx0, r.mn1, r.mx1);
+  }
 }
 
 // HMC begin: Philox momenta, kinetic energy, save (x, grad, logp), first
@@ -428,14 +442,21 @@ cudaError_t launch_finish(mt_problem *p, int mode, int C, float *x, float *grad,
   return cudaGetLastError();
 }
 
-cudaError_t launch_kick_drift(mt_problem *p, int C, float *x, float *mom, const float *grad,
-                              const float *eps, cudaStream_t s) {
+cudaError_t launch_kick(mt_problem *p, int mode, int C, float *x, float *mom, const float *grad,
+                        const float *eps, float *kin, cudaStream_t s) {
   if (C <= 0) return cudaSuccess;
   FinishArgs a = base_args(p, C);
-  a.x = x; a.mom = mom; a.grad = const_cast<float *>(grad); a.eps = eps;
-  k_kick_drift<<<C, MT_THREADS, 0, s>>>(a);
+  a.x = x; a.mom = mom; a.grad = const_cast<float *>(grad); a.eps = eps; a.kin = kin;
+  if (mode == KICK_HALF_DRIFT) k_kick<KICK_HALF_DRIFT><<<C, MT_THREADS, 0, s>>>(a);
+  else if (mode == KICK_FULL_DRIFT) k_kick<KICK_FULL_DRIFT><<<C, MT_THREADS, 0, s>>>(a);
+  else k_kick<KICK_HALF_LAST><<<C, MT_THREADS, 0, s>>>(a);
   p->all_launches++;
   return cudaGetLastError();
+}
+
+cudaError_t launch_kick_drift(mt_problem *p, int C, float *x, float *mom, const float *grad,
+                              const float *eps, cudaStream_t s) {
+  return launch_kick(p, KICK_HALF_DRIFT, C, x, mom, grad, eps, nullptr, s);
 }
 
 cudaError_t launch_hmc_begin(mt_problem *p, int C, float *x, const double *logp,

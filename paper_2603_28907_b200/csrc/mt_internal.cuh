@@ -129,6 +129,9 @@ struct mt_problem {
   int trace_s = 0;              // ray splits (0 = auto)
   int chunk = 512;              // chain lanes: rays per block (a Morton-ordered chunk)
   int smemh_limit = 100 * 1024; // stage a 32-chain height tile in smem when it fits
+  // in-library NCCL communicator (ray sharding; comm.cu)
+  void *comm = nullptr;
+  int comm_rank = 0, comm_world = 1;
   // measurement
   bool timing = false;
   std::vector<cudaEvent_t> ev_a, ev_b, ev_m;   // trace start, end, main-kernel end
@@ -157,6 +160,15 @@ cudaError_t launch_hmc_end(mt_problem *p, int C, float *x, double *logp, float *
 cudaError_t launch_momenta(mt_problem *p, int C, float *mom, uint64_t seed, uint64_t iter,
                            uint64_t chain_offset, cudaStream_t s);
 cudaError_t build_traversal(mt_problem *p);
+cudaError_t launch_kick(mt_problem *p, int mode, int C, float *x, float *mom, const float *grad,
+                        const float *eps, float *kin, cudaStream_t s);
+enum { KICK_HALF_DRIFT = 0, KICK_FULL_DRIFT = 1, KICK_HALF_LAST = 2 };
+// comm.cu
+bool comm_unique_id(void *uid, std::string &why);
+bool comm_attach(mt_problem *p, const void *uid, int rank, int world, std::string &why);
+void comm_detach(mt_problem *p);
+cudaError_t comm_allreduce_logp_grad(mt_problem *p, int C, double *logp, float *grad, cudaStream_t s,
+                                     std::string &why);
 cudaError_t launch_philox(const uint32_t *ctr, uint32_t k0, uint32_t k1, uint32_t *out,
                           int64_t n, int use_curand, cudaStream_t s);
 cudaError_t run_fp32_peak(int device, double *tflops, double *mhz);

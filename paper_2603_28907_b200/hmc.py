@@ -12,6 +12,13 @@ Philox streams are keyed by the GLOBAL chain id and acceptance sums are exact
 int64 fixed-point, so every rank computes the same ε and per-chain results do
 not depend on the number of GPUs.  The only collectives are an all-reduce of
 two int64 per warm-up iteration and of 3P doubles for R-hat at the end.
+
+Ray sharding (BASELINE configs[4]): the rays are split into contiguous ranges,
+one per rank (ray_shards); every rank holds the same chains (replicated) and
+its problem computes the shard's partial log-likelihood and gradient; the
+library's in-stream NCCL all-reduce (Problem.attach_comm, include/mt.h) sums
+them before every kick, so all ranks follow identical trajectories and no
+sampler statistic needs a cross-rank reduction (ChainShard(replicated=True)).
 """
 from __future__ import annotations
 
@@ -57,12 +64,45 @@ def rhat_from_partials(part: np.ndarray, n_chains: int, n: int) -> np.ndarray:
     return np.sqrt(var_plus / W)
 
 
+def ray_shards(R: int, world: int):
+    """Contiguous ray ranges [lo, hi) of the caller's ray order, one per rank,
+    sizes differing by at most one."""
+    if world < 1 or R < 0:
+        raise ValueError("bad ray sharding")
+    q, r = divmod(R, world)
+    out, lo = [], 0
+    for k in range(world):
+        hi = lo + q + (1 if k < r else 0)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+def ray_sharded_problem(prob: dict, rank: int, world: int, device: int, max_chains: int, group=None):
+    """This rank's Problem over its ray shard with the in-library NCCL
+    communicator attached (rank 0 creates the NCCL id; broadcast over the
+    torch.distributed group)."""
+    from ._lib import Problem, comm_unique_id
+    lo, hi = ray_shards(len(prob["ray_det"]), world)[rank]
+    pb = Problem(prob, device=device, max_chains=max_chains, ray_lo=lo, ray_hi=hi)
+    if world > 1:
+        import torch.distributed as dist
+        obj = [comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        pb.attach_comm(obj[0], rank, world)
+    return pb
+
+
 class ChainShard:
-    """Device state of this rank's chains and the HMC loop."""
+    """Device state of this rank's chains and the HMC loop.
+
+    replicated=True: every rank holds the same chains (ray sharding) — the
+    library all-reduces each evaluation, so acceptance and Welford statistics
+    are already global and are not reduced again."""
 
     def __init__(self, problem, x0: np.ndarray, seed: int, L: int, eps0: float,
                  chain_offset: int = 0, n_chains_total: Optional[int] = None, group=None,
-                 stream=None):
+                 stream=None, replicated: bool = False):
         import torch
         self.torch = torch
         self.pb = problem
@@ -73,6 +113,7 @@ class ChainShard:
         self.n_total = n_chains_total or self.C
         self.group = group
         self.stream = stream
+        self.replicated = replicated
         t = lambda *s, dt=torch.float32: torch.zeros(s, dtype=dt, device=self.dev)  # noqa: E731
         self.x = torch.from_numpy(np.ascontiguousarray(x0, np.float32)).to(self.dev)
         self.logp = t(self.C, dt=torch.float64)
@@ -90,6 +131,8 @@ class ChainShard:
         problem.logpost_grad(self.x, self.logp, self.grad, self.status, stream=stream)
 
     def _allreduce(self, t, op="sum"):
+        if self.replicated:
+            return t
         if self.group is not None or self._dist():
             import torch.distributed as dist
             dist.all_reduce(t, op=dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX, group=self.group)

@@ -7,7 +7,11 @@ What the N-GPU bench relies on, checked without GPUs:
     acceptance, hence the same dual-averaging step size, on every rank and as
     an unsharded run (order-independent integer sums, HP9);
   * R-hat partial sums all-reduced over ranks equal the single-process R-hat
-    computed from all chains at once.
+    computed from all chains at once;
+  * ray sharding (configs[4] logic): hmc.ray_shards partitions the rays, each
+    rank's partial log-posterior/gradient (likelihood of its shard, prior on
+    shard 0 only — here computed by the oracle, test infrastructure) summed by
+    all_reduce equals the unsharded result, identically on every rank.
 """
 import os
 import socket
@@ -19,7 +23,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2603_28907_b200 import inputs
-from paper_2603_28907_b200.hmc import DualAveraging, rhat_from_partials
+from paper_2603_28907_b200.hmc import DualAveraging, ray_shards, rhat_from_partials
 
 WS = 2
 C_PER = 8
@@ -56,6 +60,30 @@ def make_draws(n_iter, n_chains):
     return rng.standard_normal((n_iter, n_chains, P)) * 0.7 + rng.standard_normal((1, n_chains, P)) * 0.2
 
 
+def shard_problem(prob, lo, hi):
+    keys = ("ray_det", "ray_dir", "ray_w", "counts")
+    return dict(prob, **{k: np.asarray(prob[k])[lo:hi] for k in keys})
+
+
+def ray_shard_partial_sum(rank):
+    import oracle
+    prob = inputs.make_problem("tiny")
+    x = inputs.chain_states(prob["x_true"], 2, inputs.CONFIGS["tiny"].seed).astype(np.float64)
+    lo, hi = ray_shards(len(prob["ray_det"]), WS)[rank]
+    o = oracle.Problem(shard_problem(prob, lo, hi)).logpost_grad(x)
+    logp = o["logp"] - (0.0 if rank == 0 else o["prior"])      # prior on shard 0 only
+    grad = o["grad"].copy()
+    if rank != 0:                                               # remove the prior gradient
+        n = int(np.sqrt(x.shape[1] // 2))
+        for c in range(2):
+            for l in range(2):
+                _, gp = oracle.prior_surface(x[c].reshape(2, n, n)[l], prob["car_r"][l])
+                grad[c].reshape(2, n, n)[l] -= gp
+    t = torch.from_numpy(np.concatenate([logp, grad.ravel()]))
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t.numpy()
+
+
 def worker(rank, port, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=WS)
@@ -83,6 +111,8 @@ def worker(rank, port, out):
         t = torch.from_numpy(part)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         res["rhat"] = rhat_from_partials(t.numpy(), WS * C_PER, n)
+        # 4. ray sharding: partial [logp, grad] of this rank's ray shard, all-reduced
+        res["ray"] = ray_shard_partial_sum(rank)
         out[rank] = res
     finally:
         dist.destroy_process_group()
@@ -132,3 +162,13 @@ def test_rhat_from_allreduced_partials(results):
     ref = np.sqrt(((n - 1) / n * W + B / n) / W)  # Gelman-Rubin (P:684-687 cites the nested form)
     assert np.allclose(results[0]["rhat"], ref, rtol=1e-10)
     assert np.allclose(results[1]["rhat"], ref, rtol=1e-10)
+
+
+def test_ray_sharded_partials_sum_to_unsharded(results):
+    import oracle
+    prob = inputs.make_problem("tiny")
+    x = inputs.chain_states(prob["x_true"], 2, inputs.CONFIGS["tiny"].seed).astype(np.float64)
+    ref = oracle.Problem(prob).logpost_grad(x)
+    want = np.concatenate([ref["logp"], ref["grad"].ravel()])
+    assert np.array_equal(results[0]["ray"], results[1]["ray"])      # identical on every rank
+    assert np.allclose(results[0]["ray"], want, rtol=1e-10, atol=1e-8)

@@ -353,3 +353,57 @@ def test_hmc_driver_runs_and_adapts(gpu, problems):
     assert 0.55 < np.mean(out["warmup_accept"][-10:]) < 0.95
     assert np.all(np.isfinite(out["rhat"])) and out["rhat"].min() > 0.9
     assert torch.isfinite(sh.x).all() and torch.isfinite(sh.logp).all()
+
+
+# ---------------------------------------------------------------------------
+# ray sharding with the in-library NCCL communicator (one GPU: a one-rank
+# communicator runs the all-reduce code path; multi-rank logic: test_dist_cpu)
+# ---------------------------------------------------------------------------
+def test_one_rank_communicator_reproduces_unsharded_hmc(gpu, problems):
+    from paper_2603_28907_b200 import comm_unique_id
+    from paper_2603_28907_b200.hmc import ray_sharded_problem
+    name, C = "small", 8
+    prob = problems(name)
+    cfg = inputs.CONFIGS[name]
+    plain = Problem(prob, device=0, max_chains=C)
+    shard = ray_sharded_problem(prob, 0, 1, 0, C)       # world 1: no communicator
+    shard.attach_comm(comm_unique_id(), 0, 1)             # ... attach one explicitly
+    x0 = torch.from_numpy(inputs.chain_states(prob["x_true"], C, cfg.seed)).to(DEV)
+    out = []
+    for pb in (plain, shard):
+        x = x0.clone()
+        logp, grad = pb.logpost_grad(x)
+        eps = torch.full((C,), sampling_eps(name), dtype=torch.float32, device=DEV)
+        ap, acc = pb.hmc_step(x, logp, grad, eps, 10, inputs.philox_key(cfg), 5)
+        torch.cuda.synchronize()
+        out.append((x.cpu().numpy(), logp.cpu().numpy(), grad.cpu().numpy(), ap.cpu().numpy()))
+    # (not bit-identical: the adjoint's float atomics sum in run-dependent order)
+    (x1, lp1, g1, a1), (x2, lp2, g2, a2) = out
+    for c in range(C):
+        assert rel_l2(x2[c].astype(np.float64), x1[c].astype(np.float64)) < 1e-5
+        assert rel_l2(g2[c].astype(np.float64), g1[c].astype(np.float64)) < 1e-4
+    assert np.allclose(lp2, lp1, rtol=1e-7)
+    assert np.allclose(a2, a1, atol=1e-3)
+    shard.detach_comm()
+
+
+def test_ray_shards_partition_and_sum_ray_sharded_config(gpu, problems):
+    """configs[4] split as for 4 GPUs (hmc.ray_shards): the shards' partial
+    log-posteriors and gradients (prior on shard 0 only) sum to the whole."""
+    from paper_2603_28907_b200.hmc import ray_shards
+    prob = problems("ray_sharded")
+    R = len(prob["ray_det"])
+    sh = ray_shards(R, 4)
+    assert sh[0][0] == 0 and sh[-1][1] == R and all(a[1] == b[0] for a, b in zip(sh, sh[1:]))
+    whole = gpu("ray_sharded")
+    x = torch.from_numpy(inputs.chain_states(prob["x_true"], 1, inputs.CONFIGS["ray_sharded"].seed)).to(DEV)
+    lp, g = whole.logpost_grad(x)
+    lps, gs = [], []
+    for lo, hi in sh:
+        part = Problem(prob, device=0, max_chains=1, ray_lo=lo, ray_hi=hi)
+        a, b = part.logpost_grad(x)
+        lps.append(a.cpu().numpy())
+        gs.append(b.cpu().numpy().astype(np.float64))
+        del part
+    assert np.allclose(sum(lps), lp.cpu().numpy(), rtol=1e-7)
+    assert rel_l2(sum(gs)[0], g.cpu().numpy()[0].astype(np.float64)) < 1e-5
