@@ -40,6 +40,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mt", choices=["mt", "reference"])
+    ap.add_argument("--workload", default="chain_sharded", choices=["chain_sharded", "ray_sharded"],
+                    help="configs[3] (default, the headline) or configs[4] (one chain, rays over the GPUs)")
     ap.add_argument("--chains-total", type=int, default=8192)     # configs[3]
     ap.add_argument("--weak", action="store_true", help="fixed --chains-per-gpu per rank instead")
     ap.add_argument("--chains-per-gpu", type=int, default=1024)
@@ -100,16 +102,16 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
 
 
-def cpu_baseline(seconds: float, chains: int = 4):
-    """The fp64 oracle, as it stands, on this host's cores: Medium, `chains`
-    chains x all 262,144 rays per evaluation, repeated for ~`seconds`."""
+def cpu_baseline(seconds: float, chains: int = 4, name: str = "chain_sharded"):
+    """The fp64 oracle, as it stands, on this host's cores: the workload's
+    geometry, `chains` chains x all its rays per evaluation, repeated for ~`seconds`."""
     import numpy as np
 
     import oracle
     from paper_2603_28907_b200 import inputs
-    prob = inputs.make_problem("medium")
+    prob = inputs.make_problem(name)
     op = oracle.Problem(prob)
-    x = inputs.chain_states(prob["x_true"], chains, inputs.CONFIGS["medium"].seed).astype(np.float64)
+    x = inputs.chain_states(prob["x_true"], chains, inputs.CONFIGS[name].seed).astype(np.float64)
     t0 = time.perf_counter()
     n = 0
     while True:
@@ -120,7 +122,7 @@ def cpu_baseline(seconds: float, chains: int = 4):
     dt = time.perf_counter() - t0
     return {"value": n * chains * op.R / dt, "unit": UNIT, "cores": oracle.num_threads(),
             "kind": "oracle",
-            "sample": f"medium geometry, {chains} near-posterior chains x {op.R} rays per evaluation, "
+            "sample": f"{name} geometry, {chains} near-posterior chain(s) x {op.R} rays per evaluation, "
                       f"{n} evaluations ({n * chains * op.R:.3g} chain-ray pairs) in {dt:.1f} s, fp64"}
 
 
@@ -184,25 +186,37 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     dev = torch.device(f"cuda:{local}")
 
-    cfg = inputs.CONFIGS["chain_sharded"]
-    prob = inputs.make_problem("medium")
-    if args.weak:
-        C = args.chains_per_gpu
-    else:
-        if args.chains_total % (8 * ws):
-            raise SystemExit(f"--chains-total {args.chains_total} must split into super-chains of 8 per rank")
-        C = args.chains_total // ws
+    ray = args.workload == "ray_sharded"
+    cfg = inputs.CONFIGS[args.workload]
+    dname = inputs.DATA_NAME[args.workload]
+    prob = inputs.make_problem(args.workload)
     L = args.leapfrog
-    offset = rank * C
-    x0 = inputs.chain_states(prob["x_true"], C, cfg.seed, chain_offset=offset, super_size=8)
-    pb = Problem(prob, device=local, max_chains=C)
-    R, P = pb.R, pb.P
-    # sampling-phase step size from the dual-averaging warm-up (tools/tune_eps.py)
     tpath = os.path.join(ROOT, "data", "tuned_eps.json")
-    tuned = json.load(open(tpath)).get("medium") if os.path.exists(tpath) else None
-    eps = tuned["eps"] if tuned else cfg.eps
-    shard = ChainShard(pb, x0, seed=inputs.philox_key(cfg), L=L, eps0=eps, chain_offset=offset,
-                       n_chains_total=C * ws)
+    tuned = json.load(open(tpath)).get(dname) if os.path.exists(tpath) else None
+    eps = tuned["eps"] if tuned else cfg.eps   # sampling-phase ε from the warm-up (tools/tune_eps.py)
+    if ray:
+        # configs[4]: one chain, its 4,194,304 rays split over the ranks, in-library NCCL
+        # all-reduce of [logp, grad] per evaluation; chains replicated on every rank
+        from paper_2603_28907_b200.hmc import ray_sharded_problem
+        C, offset = 1, 0
+        x0 = inputs.chain_states(prob["x_true"], C, cfg.seed)
+        pb = ray_sharded_problem(prob, rank, ws, local, max_chains=C)
+        R_total = len(prob["ray_det"])
+        shard = ChainShard(pb, x0, seed=inputs.philox_key(cfg), L=L, eps0=eps, replicated=True)
+    else:
+        if args.weak:
+            C = args.chains_per_gpu
+        else:
+            if args.chains_total % (8 * ws):
+                raise SystemExit(f"--chains-total {args.chains_total} must split into super-chains of 8 per rank")
+            C = args.chains_total // ws
+        offset = rank * C
+        x0 = inputs.chain_states(prob["x_true"], C, cfg.seed, chain_offset=offset, super_size=8)
+        pb = Problem(prob, device=local, max_chains=C)
+        R_total = pb.R * ws   # (chain sharding: every rank traces all rays of its chains)
+        shard = ChainShard(pb, x0, seed=inputs.philox_key(cfg), L=L, eps0=eps, chain_offset=offset,
+                           n_chains_total=C * ws)
+    R, P = pb.R, pb.P
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MiB > 126 MB L2
 
     def barrier():
@@ -234,11 +248,11 @@ def main():
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_ms = float(t.item())
-    units = ws * C * R * L * args.steps
+    units = (R_total * C if ray else ws * C * R) * L * args.steps
     value = units / (t_ms * 1e-3)
 
     # dominant kernel (K2 trace): algorithmic FP32 flops per launch / measured launch duration
-    work = json.load(open(os.path.join(ROOT, "data", "work_counts.json")))["medium"]
+    work = json.load(open(os.path.join(ROOT, "data", "work_counts.json")))[dname]
     F = work["flops_per_pair"]
     avg_trace_ms = tm["trace_ms"] / max(tm["trace_launches"], 1)       # K2 main + fp64 follow-up
     avg_defer_ms = cnt["defer_ms"] / max(tm["trace_launches"], 1)
@@ -246,10 +260,12 @@ def main():
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "trace_traffic.json")
     if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get("bytes_per_launch")
+        tr = json.load(open(tpath)).get(args.workload)
+        traffic = tr.get("bytes_per_launch") if tr and tr.get("chains") == C else None
     roofline = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_NOMINAL, "unit": "TFLOP/s",
                 "frac": achieved / FP32_PEAK_NOMINAL, "traffic": traffic,
-                "kernel": "K2 = k_trace_cl (chain lanes) + k_trace_defer (fp64 follow-up), per launch pair",
+                "kernel": ("K2 = k_trace_rl (ray lanes)" if ray else "K2 = k_trace_cl (chain lanes)")
+                          + " + k_trace_defer (fp64 follow-up), per launch pair",
                 "flops_per_pair": F,
                 "defer_share_of_trace": avg_defer_ms / avg_trace_ms,
                 "deferred_pairs_per_launch": (cnt["deferred"] - d0) / max(tm["trace_launches"], 1),
@@ -289,16 +305,19 @@ def main():
         return
     base = None
     if ws == 1 and not args.no_cpu_baseline:
-        base = cpu_baseline(args.cpu_seconds)
+        base = cpu_baseline(args.cpu_seconds, chains=1 if ray else 4, name=args.workload)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded Medium geometry; counts = Poisson of the oracle's truth; "
-                    "near-posterior chain states)",
-            "config": {"workload": "chain_sharded HMC iteration (BASELINE configs[3]: Medium geometry and rays, "
-                                   f"{C * ws} chains over {ws} GPU(s))",
-                       "chains_per_gpu": C, "global_chains": C * ws, "rays": R, "params": P,
-                       "leapfrog_steps": L, "parallelism": f"chain-sharded x{ws}",
+            "data": f"synthetic (seeded {'configs[4] 800 m' if ray else 'Medium'} geometry; counts = Poisson of the "
+                    "oracle's truth; near-posterior chain states)",
+            "config": {"workload": (f"ray_sharded HMC iteration (BASELINE configs[4]: one chain, {R_total} rays "
+                                    f"over {ws} GPU(s))") if ray else
+                                   ("chain_sharded HMC iteration (BASELINE configs[3]: Medium geometry and rays, "
+                                    f"{C * ws} chains over {ws} GPU(s))"),
+                       "chains_per_gpu": C, "global_chains": C if ray else C * ws, "rays": R_total if ray else R,
+                       "rays_per_gpu": R, "params": P,
+                       "leapfrog_steps": L, "parallelism": (f"ray-sharded x{ws}" if ray else f"chain-sharded x{ws}"),
                        "phase": "sampling (fixed eps from the 100-iteration dual-averaging warm-up, "
                                 "tools/tune_eps.py; Welford + all-reduced acceptance sums each step)",
                        "eps": eps,

@@ -1,3 +1,3 @@
-timeout 600 python bench.py > gpurun_out/bench_r1c.log 2>&1; echo "rc $?" >> gpurun_out/bench_r1c.log
-timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_short_r1c.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r1c.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch_r1c.log 2>&1
-timeout 300 python tools/trace_bench.py medium --chains 8192 --reps 2 > gpurun_out/tb8192.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_trace -s 3 -c 2 -o gpurun_out/prof_r1c_8192 python tools/trace_bench.py medium --chains 8192 --reps 2 > gpurun_out/ncu_full_r1c.log 2>&1
+timeout 600 python tools/tune_eps.py ray_sharded --chains 1 > gpurun_out/tune_ray.log 2>&1
+cp data/tuned_eps.json gpurun_out/tuned_eps.json
+timeout 600 python bench.py --workload ray_sharded > gpurun_out/bench_ray.log 2>&1
