@@ -283,7 +283,7 @@ __shared__ float sgeo[4][MT_MAX_AXIS];   // X, Y, 1/ΔX, 1/ΔY
 #define MT_RCAP 3
 #endif
 #ifndef MT_CL_MINB
-#define MT_CL_MINB 4
+#define MT_CL_MINB 5
 #endif
 constexpr int RCAP = MT_RCAP;
 

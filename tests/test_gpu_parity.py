@@ -142,6 +142,19 @@ def test_logpost_grad_ray_sharded_full_size(gpu, oracle_problem):
     assert not fails, fails
 
 
+def test_logpost_grad_chain_sharded_8192(gpu, oracle_problem):
+    """configs[3] in the launch configuration bench.py times at N = 1: all 8,192
+    chains (super-chains of 8 share a start) on one device, compared on sampled
+    chains the oracle computes one by one."""
+    mp, op = gpu("medium", max_chains=8192), oracle_problem("medium")
+    cfg = inputs.CONFIGS["chain_sharded"]
+    x = inputs.chain_states(op.prob["x_true"], 8192, cfg.seed, super_size=8)
+    logp, grad = mp.logpost_grad(torch.from_numpy(x).to(DEV))
+    chains = np.array([0, 4095, 4100, 8191])
+    fails = e2e_check(mp, op, x, chains, logp.cpu().numpy(), grad.cpu().numpy())
+    assert not fails, fails
+
+
 def test_logpost_grad_medium_bench_launch(gpu, oracle_problem):
     """Full Medium size, in the launch configuration bench.py times (1024 chains),
     compared on sampled chains the oracle computes one by one."""
@@ -178,7 +191,7 @@ def test_momenta_match_oracle(gpu, oracle_problem):
         assert np.allclose(p_d[c], oracle.momenta(P, seed, it, off + c), rtol=1e-6, atol=1e-6)
 
 
-@pytest.mark.parametrize("name,C", [("tiny", 4), ("small", 16)])
+@pytest.mark.parametrize("name,C", [("tiny", 4), ("small", 16), ("medium", 2), ("ray_sharded", 1)])
 def test_leapfrog_10_steps(gpu, oracle_problem, name, C):
     mp, op = gpu(name), oracle_problem(name)
     cfg = inputs.CONFIGS[name]

@@ -1,3 +1,4 @@
-timeout 600 python tools/tune_eps.py ray_sharded --chains 1 > gpurun_out/tune_ray.log 2>&1
-cp data/tuned_eps.json gpurun_out/tuned_eps.json
-timeout 600 python bench.py --workload ray_sharded > gpurun_out/bench_ray.log 2>&1
+for v in default mb5 mb6; do
+  if [ $v = default ]; then unset MT_LIB; else export MT_LIB=$PWD/variants/libmt_$v.so; fi
+  timeout 300 python tools/trace_bench.py medium >> gpurun_out/tb_v18.log 2>&1
+done
