@@ -387,6 +387,35 @@ __device__ __forceinline__ int band_entry(const int2 *__restrict__ cells, int lo
   return lo;
 }
 
+// Band entry from an estimate (ray lanes: thread-private walks, where a binary
+// search costs ~log2(cells) dependent uncoalesced loads).  Each stored cell
+// after the first steps i, j or both, so the cell containing s is (almost)
+// entry |i(s) - i0| + |j(s) - j0| of the list (fewer by the vertex steps);
+// the estimate is then verified against the stored s_out and moved (rarely)
+// until it is the first cell with s_out > s.  rc = {off, end, first cell word}.
+__device__ __forceinline__ int band_entry_est(const int2 *__restrict__ cells, int4 rc, float ox, float oy,
+                                              float dx, float dy, float s, int nx, int ny, float &s_in) {
+  const float x = fmaf(s, dx, ox), y = fmaf(s, dy, oy);
+  const int i0 = cell_i(rc.z), j0 = cell_j(rc.z);
+  // the cell column / row holding (x, y): from the mean spacing, then corrected
+  int i = min(max((int)((x - sgeo[0][0]) * ((float)(nx - 1) / (sgeo[0][nx - 1] - sgeo[0][0]))), 0), nx - 2);
+  int j = min(max((int)((y - sgeo[1][0]) * ((float)(ny - 1) / (sgeo[1][ny - 1] - sgeo[1][0]))), 0), ny - 2);
+  while (i < nx - 2 && sgeo[0][i + 1] <= x) i++;
+  while (i > 0 && sgeo[0][i] > x) i--;
+  while (j < ny - 2 && sgeo[1][j + 1] <= y) j++;
+  while (j > 0 && sgeo[1][j] > y) j--;
+  int k = min(rc.x + abs(i - i0) + abs(j - j0), rc.y - 1);
+  for (int guard = 0; guard < 64; guard++) {
+    const float so = __int_as_float(__ldg(&cells[k].y));
+    const float sp = k > rc.x ? __int_as_float(__ldg(&cells[k - 1].y)) : 0.f;
+    if (so <= s && k < rc.y - 1) { k++; continue; }
+    if (sp > s && k > rc.x) { k--; continue; }
+    s_in = sp;
+    return k;
+  }
+  return band_entry(cells, rc.x, rc.y, s, s_in);   // not reached in practice
+}
+
 // Same, warp-cooperative (chain lanes, all 32 lanes converged, uniform
 // arguments): one coalesced load of 32 cells and a ballot per round.
 __device__ __forceinline__ int band_entry_warp(const int2 *__restrict__ cells, int lo, int hi, float s,
@@ -449,7 +478,8 @@ __device__ __forceinline__ void load_geometry(const TraceArgs &a, float *Xs, flo
 // ---------------------------------------------------------------------------
 // traversal builder (create time): thread = ray; count pass then write pass
 // ---------------------------------------------------------------------------
-__global__ void k_build_trav(TraceArgs a, const int32_t *off, int32_t *count, int2 *cells, float4 *cgeo) {
+__global__ void k_build_trav(TraceArgs a, const int32_t *off, int32_t *count, int2 *cells, float4 *cgeo,
+                             int4 *ray_c) {
   __shared__ float Xs[MT_MAX_AXIS], Ys[MT_MAX_AXIS];
   const int nx = a.tc.nx, ny = a.tc.ny;
   for (int k = threadIdx.x; k < nx; k += blockDim.x) Xs[k] = a.X[k];
@@ -461,6 +491,7 @@ __global__ void k_build_trav(TraceArgs a, const int32_t *off, int32_t *count, in
   int i = start_axis(Xs, nx, q.r.ox, q.r.dx), j = start_axis(Ys, ny, q.r.oy, q.r.dy);
   float s = 0.f, s_in = 0.f;   // s_in: the previous STORED s_out (what the walks carry)
   int n = 0;
+  if (ray_c) ray_c[rr] = make_int4(off[rr], off[rr + 1], cell_pack(i, j, ny), 0);
   for (int guard = 0; guard < 4 * (MT_MAX_AXIS + 2); guard++) {
     float s_ev;
     int ev = dda_next(q, i, j, Xs, Ys, nx, ny, a.tc.z_top, s_ev);
@@ -619,75 +650,140 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a
   if (MODE == TRACE_LL && act) atomicAdd(a.ll + c, (double)llacc);
 }
 
-// The chain x ray pairs the chain-lanes kernel deferred (an ill-conditioned
-// cell, or more than RCAP crossings of a surface): thread = pair.  The same
-// walk from the same s_lo with the same fp32 cell code, ill-conditioned cells
-// re-solved in place in fp64 (HP2 lever 1), then the epilogue and the adjoint
-// scatter (or the path-length export).  The last block resets the queue.
+// The chain x ray pairs the trace kernels deferred (an ill-conditioned cell,
+// or more than RCAP crossings of a surface).  A group of DG = 8 lanes takes
+// one pair, lane = one stored cell of its band (8 cells per round): the same fp32 cell code with
+// the same cell pieces as the serial walk, ill-conditioned cells re-solved in
+// place in fp64 from H + Hlo (HP2 lever 1), the lengths summed over the lanes,
+// then the epilogue and each lane's adjoint scatter (or the path-length
+// export).  A pair's latency is a few dependent loads, not a serial march.
+// The last block resets the queue.
 template <int MODE>
 __global__ void __launch_bounds__(MT_THREADS) k_trace_defer(TraceArgs a) {
-  extern __shared__ __align__(16) float4 recs[];    // [2*RCAP][MT_THREADS]
+  __shared__ float4 wrec[MT_THREADS][4];   // per lane: up to 2 crossings per surface of its cell
   load_geometry(a, sgeo[0], sgeo[1], sgeo[2], sgeo[3]);
   __syncthreads();
   const int n = *(volatile int *)a.ovf_n;
   const int N = a.tc.N, ny = a.tc.ny;
-  __shared__ double llw[MT_THREADS];
-  const int lane = threadIdx.x & 31, nq = min(n, a.ovf_cap);
-  // warp-uniform loop over 32-entry slices (the ll aggregation below needs the whole warp)
-  for (int q0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; q0 < nq; q0 += gridDim.x * blockDim.x) {
-    const int q = q0 + lane;
-    int c = -1;
-    double ll = 0.0;
-    if (q < nq) {
-      const float4 e0 = a.ovf_q[q];
-      c = __float_as_int(e0.x);
-      const int rr = __float_as_int(e0.y);
-      const float s_lo = e0.z, s_hi = e0.w;
-      const Ray r = load_ray(a.ray_a, a.ray_b, rr);
-      const size_t off = (size_t)(c >> 5) * 2 * N * 32 + (c & 31);
-      const float4 bd = a.band[c];
-      float B0 = s_lo, B1 = s_lo;
-      int nrec[2] = {0, 0};
-      int k0 = 0;
-      float s_in0 = 0.f;
+  constexpr int DG = 8;
+  const int lane = threadIdx.x & (DG - 1), nq = min(n, a.ovf_cap);
+  const unsigned gmask = 0xffu << (threadIdx.x & 31 & ~(DG - 1));   // this group's lanes
+  const int grp_g = (blockIdx.x * blockDim.x + threadIdx.x) / DG, ngrp = (gridDim.x * blockDim.x) / DG;
+  int c_acc = -1;
+  double ll_acc = 0.0;
+  // group-uniform loop (the whole warp keeps iterating until all its groups are done,
+  // so the full-warp shuffles below see every lane)
+  const int iters = (nq + ngrp - 1) / ngrp;
+  for (int it = 0; it < iters; it++) {
+    const int q = grp_g + it * ngrp;
+    if (q >= nq) continue;
+    const float4 e0 = a.ovf_q[q];
+    const int c = __float_as_int(e0.x), rr = __float_as_int(e0.y);
+    const float s_lo = e0.z, s_hi = e0.w;
+    const Ray r = load_ray(a.ray_a, a.ray_b, rr);
+    const size_t off = (size_t)(c >> 5) * 2 * N * 32 + (c & 31);
+    const float *Hk = a.H + off, *Hl = a.Hlo + off;
+    const float4 bd = a.band[c];
+    float B0 = 0.f, B1 = 0.f;                          // this lane's cells' contributions
+    int nr0 = 0, nr1 = 0, ovf = 0;
+    if (s_lo < r.s_exit) {
       const int kend = a.trav_off[rr + 1];
-      if (s_lo < r.s_exit) {
-        k0 = band_entry(a.trav, a.trav_off[rr], kend, s_lo, s_in0);
-        walk<32, false>(r, a.trav, a.trav_geo, k0, kend, s_lo, s_in0, s_hi, ny, N, a.H + off, a.Hlo + off,
-                        nullptr, bd, B0, B1, recs + threadIdx.x, nrec, 0.f, 0.f);
-      }
-      if (MODE == TRACE_LL) {
-        float dldO;
-        ll = (double)epilogue(r.tb, r.cnt, a.tc, B0, B1, dldO);
-        const float f0 = dldO * a.tc.k0, f1 = dldO * a.tc.k1;
-        if (nrec[0] <= RCAP && nrec[1] <= RCAP) {
-          scatter_recs<32>(recs + threadIdx.x, nrec, a.G + off, N, ny, f0, f1);
-        } else {
-          float d0 = s_lo, d1 = s_lo;
-          walk<32, true>(r, a.trav, a.trav_geo, k0, kend, s_lo, s_in0, s_hi, ny, N, a.H + off, a.Hlo + off,
-                         a.G + off, bd, d0, d1, nullptr, nrec, f0, f1);
+      float s_in0;
+      const int k0 = band_entry(a.trav, a.trav_off[rr], kend, s_lo, s_in0);
+      float s_prev = s_lo;                             // s_out before this round's first cell
+      for (int kb = k0; kb < kend; kb += DG) {
+        const int k = kb + lane;
+        const int2 w = k < kend ? __ldg(a.trav + k) : make_int2(0, __float_as_int(3.0e38f));
+        const float s1 = __int_as_float(w.y);
+        const float sp = __shfl_up_sync(gmask, s1, 1, DG);
+        const float s = lane == 0 ? s_prev : sp;       // the piece [s, s1] of the serial walk
+        const bool act = k < kend && s < s_hi;         // the walk stops after the cell reaching s_hi
+        if (act) {
+          const float4 cg = shift_geo(__ldg(a.trav_geo + k), k == k0 ? s_lo - s_in0 : 0.f);
+          const int i = cell_i(w.x), j = cell_j(w.x), base = i * ny + j;
+          const float za = s * r.dz, zb = s1 * r.dz, Ls = s1 - s;
+#pragma unroll
+          for (int l = 0; l < 2; l++) {
+            const float zmin = l ? bd.z : bd.x, zmax = l ? bd.w : bd.y;
+            float &B = l ? B1 : B0;
+            int &nr = l ? nr1 : nr0;
+            if (zb <= zmin) { B += Ls; continue; }
+            if (za >= zmax) continue;
+            const float *p = Hk + ((size_t)l * N + base) * 32;
+            const float h00 = __ldg(p), h10 = __ldg(p + ny * 32), h01 = __ldg(p + 32), h11 = __ldg(p + ny * 32 + 32);
+            if (zb <= fminf(fminf(h00, h10), fminf(h01, h11))) { B += Ls; continue; }
+            if (za >= fmaxf(fmaxf(h00, h10), fmaxf(h01, h11))) continue;
+            auto emit = [&](float u, float v, float ig) {
+              if (nr < 2) wrec[threadIdx.x][2 * l + nr] = make_float4(__int_as_float(base), u, v, ig);
+              else ovf = 1;
+              nr++;
+            };
+            if (!solve32(h00, h10, h01, h11, cg, za, Ls, r.dz, B, emit)) {
+              const float *pl = Hl + ((size_t)l * N + base) * 32;
+              const Fix x = fix64((double)h00 + pl[0], (double)h10 + pl[ny * 32], (double)h01 + pl[32],
+                                  (double)h11 + pl[ny * 32 + 32], sgeo[0][i], sgeo[0][i + 1], sgeo[1][j],
+                                  sgeo[1][j + 1], r, s, s1);
+              B += x.below;
+              for (int m = 0; m < x.n; m++) emit(x.u[m], x.v[m], x.ig[m]);
+            }
+          }
         }
-      } else {
-        const int64_t o = (int64_t)c * a.R + a.perm[rr];
-        a.Lout[3 * o + 0] = B0;
-        a.Lout[3 * o + 1] = B1 - B0;
-        a.Lout[3 * o + 2] = r.s_exit - B1;
-        a.Oout[o] = a.tc.k0 * B0 + a.tc.k1 * B1 + a.obase[rr];
+        // continue while this round's last cell ends below s_hi
+        const float last = __shfl_sync(gmask, s1, DG - 1, DG);
+        if (__ballot_sync(gmask, k < kend && s1 >= s_hi) || kb + DG >= kend) break;
+        s_prev = last;   // (records accumulate over rounds: at most 2 per surface per lane, else ovf)
       }
     }
-    if (MODE == TRACE_LL) {   // one double atomic per distinct chain of the warp (a single chain's
-      __syncwarp();           // deferred pairs would otherwise serialise on one address)
-      const unsigned peers = __match_any_sync(0xffffffffu, c);
-      llw[threadIdx.x] = ll;
-      __syncwarp();
-      if (c >= 0 && lane == __ffs(peers) - 1) {
-        double t = 0.0;
-        for (unsigned m = peers; m; m &= m - 1) t += llw[(threadIdx.x & ~31) + __ffs(m) - 1];
-        atomicAdd(a.ll + c, t);
+    // pair totals
+    float T0 = B0, T1 = B1;
+    for (int o = DG / 2; o > 0; o >>= 1) {
+      T0 += __shfl_xor_sync(gmask, T0, o, DG);
+      T1 += __shfl_xor_sync(gmask, T1, o, DG);
+    }
+    T0 += s_lo;
+    T1 += s_lo;
+    const bool anyovf = __ballot_sync(gmask, ovf) != 0;
+    if (MODE == TRACE_LL) {
+      float dldO;
+      const float ll = epilogue(r.tb, r.cnt, a.tc, T0, T1, dldO);
+      if (lane == 0) {
+        if (c != c_acc) {
+          if (c_acc >= 0) atomicAdd(a.ll + c_acc, ll_acc);
+          c_acc = c;
+          ll_acc = 0.0;
+        }
+        ll_acc += (double)ll;
       }
-      __syncwarp();
+      const float f0 = dldO * a.tc.k0, f1 = dldO * a.tc.k1;
+      if (!anyovf) {
+        float *G0 = a.G + off;
+        for (int m = 0; m < nr0; m++) {
+          const float4 t = wrec[threadIdx.x][m];
+          scatter4(G0, 32, __float_as_int(t.x), ny, f0 * t.w, t.y, t.z);
+        }
+        for (int m = 0; m < nr1; m++) {
+          const float4 t = wrec[threadIdx.x][2 + m];
+          scatter4(G0 + (size_t)N * 32, 32, __float_as_int(t.x), ny, f1 * t.w, t.y, t.z);
+        }
+      } else if (lane == 0 && s_lo < r.s_exit) {
+        // rare: a lane with more than 2 crossings of a surface over its cells (bands of
+        // more than DG cells): one lane re-walks and scatters directly
+        float s_in0, d0 = s_lo, d1 = s_lo;
+        int nrec[2] = {0, 0};
+        const int kend = a.trav_off[rr + 1];
+        const int k0 = band_entry(a.trav, a.trav_off[rr], kend, s_lo, s_in0);
+        walk<32, true>(r, a.trav, a.trav_geo, k0, kend, s_lo, s_in0, s_hi, ny, N, Hk, Hl, a.G + off, bd,
+                       d0, d1, nullptr, nrec, f0, f1);
+      }
+    } else if (lane == 0) {
+      const int64_t o = (int64_t)c * a.R + a.perm[rr];
+      a.Lout[3 * o + 0] = T0;
+      a.Lout[3 * o + 1] = T1 - T0;
+      a.Lout[3 * o + 2] = r.s_exit - T1;
+      a.Oout[o] = a.tc.k0 * T0 + a.tc.k1 * T1 + a.obase[rr];
     }
   }
+  if (MODE == TRACE_LL && lane == 0 && c_acc >= 0) atomicAdd(a.ll + c_acc, ll_acc);
   if (n > a.ovf_cap)   // queue overflow: fail loudly (non-finite log-likelihood -> status bit)
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.C; c += gridDim.x * blockDim.x)
       a.ll[c] = __longlong_as_double(0x7ff8000000000000ll);
@@ -727,11 +823,23 @@ __global__ void __launch_bounds__(MT_THREADS, 4) k_trace_rl(TraceArgs a, const f
   const float4 bd = __ldg(a.band + c);
   const size_t coff = (size_t)(c >> 5) * 2 * N * 32 + (c & 31);
   float *G0 = a.G + coff, *G1 = G0 + (size_t)N * 32;
-  __syncthreads();
-  float llacc = 0.f;
+  int2 *stage = reinterpret_cast<int2 *>(smem + ((2 * N + 3) & ~3) + 8 * RCAP * MT_THREADS) + tid;  // [8][MT_THREADS]
+  __shared__ int next_ray;
   const int r_begin = blockIdx.x * (int)a.rays_per_block;
   const int r_end = min((int)a.R, r_begin + (int)a.rays_per_block);
-  for (int rr = r_begin + tid; rr < r_end; rr += MT_THREADS) {
+  if (tid == 0) next_ray = r_begin;
+  __syncthreads();
+  float llacc = 0.f;
+  const int lane = tid & 31;
+  // warps take 32 consecutive (Morton-adjacent) rays at a time from the block's range:
+  // thread-serial walks vary in length, and a static split left warps idle at the end
+  for (;;) {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(&next_ray, 32);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= r_end) break;
+    const int rr = base + lane;
+    if (rr >= r_end) continue;
     const float2 rb = __ldg(reinterpret_cast<const float2 *>(a.ray_b + rr));
     const float dz = rb.x, s_exit = rb.y;
     const float s_lo = fminf(__fdividef(bd.x, dz) * (1.f - 1e-6f), s_exit);
@@ -739,17 +847,27 @@ __global__ void __launch_bounds__(MT_THREADS, 4) k_trace_rl(TraceArgs a, const f
     float B0 = s_lo, B1 = s_lo;
     int n0 = 0, n1 = 0, defer = 0;
     if (s_lo < s_exit) {
-      const int kend = __ldg(a.trav_off + rr + 1);
-      float s_in0;
-      const int k0 = band_entry(a.trav, __ldg(a.trav_off + rr), kend, s_lo, s_in0);
-      float s = s_lo, za = s_lo * dz;
+      const int4 rc = __ldg(a.ray_c + rr);
+      const int kend = rc.y;
       // cell geometry on the fly (thread-private walks: the stored per-cell
       // geometry would triple the uncoalesced per-cell traffic)
       const float2 ro = __ldg(reinterpret_cast<const float2 *>(a.ray_a + rr));
       const float2 rd = __ldg(reinterpret_cast<const float2 *>(a.ray_a + rr) + 1);
-      int2 w = __ldg(a.trav + k0);
+      float s_in0;
+      const int k0 = band_entry_est(a.trav, rc, ro.x, ro.y, rd.x, rd.y, s_lo, a.tc.nx, ny, s_in0);
+      float s = s_lo, za = s_lo * dz;
       for (int k = k0; k < kend; k++) {
-        const int2 wn = __ldg(a.trav + min(k + 1, kend - 1));   // prefetch the next stored cell
+        // the stored cells in batches of 8: eight independent loads in flight, then
+        // shared-memory reads (thread-private lists do not coalesce)
+        const int m = (k - k0) & 7;
+        if (m == 0) {
+          int2 v[8];
+#pragma unroll
+          for (int q = 0; q < 8; q++) v[q] = k + q < kend ? __ldg(a.trav + k + q) : make_int2(0, 0);
+#pragma unroll
+          for (int q = 0; q < 8; q++) stage[q * MT_THREADS] = v[q];
+        }
+        const int2 w = stage[m * MT_THREADS];
         const int ci = cell_i(w.x), cj = cell_j(w.x);
         const float ix = sgeo[2][ci], iy = sgeo[3][cj];
         const float4 cg = make_float4((fmaf(s, rd.x, ro.x) - sgeo[0][ci]) * ix, (fmaf(s, rd.y, ro.y) - sgeo[1][cj]) * iy,
@@ -770,7 +888,6 @@ __global__ void __launch_bounds__(MT_THREADS, 4) k_trace_rl(TraceArgs a, const f
         if (s1 >= s_hi) break;
         s = s1;
         za = zb;
-        w = wn;
       }
     }
     if (defer || n0 > RCAP || n1 > RCAP) {             // rare: the whole pair goes to k_trace_defer
@@ -831,7 +948,8 @@ static TraceArgs base_trace_args(mt_problem *p) {
   a.tc = p->tc;
   a.X = p->d_X; a.Y = p->d_Y;
   a.ray_a = p->d_ray_a; a.ray_b = p->d_ray_b; a.obase = p->d_obase;
-  a.trav_off = p->d_trav_off; a.trav = p->d_trav; a.trav_geo = p->d_trav_geo; a.perm = p->d_perm;
+  a.trav_off = p->d_trav_off; a.trav = p->d_trav; a.trav_geo = p->d_trav_geo; a.ray_c = p->d_ray_c;
+  a.perm = p->d_perm;
   a.R = p->R;
   a.ovf_q = p->d_ovf_q; a.ovf_n = p->d_ovf_n; a.ovf_done = p->d_ovf_n + 1; a.ovf_cap = p->ovf_cap;
   a.ovf_total = reinterpret_cast<unsigned long long *>(p->d_ovf_n + 2);
@@ -845,7 +963,7 @@ cudaError_t build_traversal(mt_problem *p) {
   cudaError_t e = cudaMalloc(&d_cnt, sizeof(int32_t) * p->R);
   if (e != cudaSuccess) return e;
   unsigned nb = (unsigned)((p->R + 127) / 128);
-  k_build_trav<<<nb, 128>>>(a, nullptr, d_cnt, nullptr, nullptr);
+  k_build_trav<<<nb, 128>>>(a, nullptr, d_cnt, nullptr, nullptr, nullptr);
   std::vector<int32_t> cnt(p->R);
   e = cudaMemcpy(cnt.data(), d_cnt, sizeof(int32_t) * p->R, cudaMemcpyDeviceToHost);
   cudaFree(d_cnt);
@@ -861,13 +979,14 @@ cudaError_t build_traversal(mt_problem *p) {
   e = cudaMalloc(&p->d_trav_off, sizeof(int32_t) * (p->R + 1));
   if (e == cudaSuccess) e = cudaMalloc(&p->d_trav, sizeof(int2) * (p->trav_cells > 0 ? p->trav_cells : 1));
   if (e == cudaSuccess) e = cudaMalloc(&p->d_trav_geo, sizeof(float4) * (p->trav_cells > 0 ? p->trav_cells : 1));
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_ray_c, sizeof(int4) * p->R);
   if (e == cudaSuccess)
     e = cudaMemcpy(p->d_trav_off, off.data(), sizeof(int32_t) * (p->R + 1), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return e;
   a.trav_off = p->d_trav_off;
   a.trav = p->d_trav;
   a.trav_geo = p->d_trav_geo;
-  k_build_trav<<<nb, 128>>>(a, p->d_trav_off, nullptr, p->d_trav, p->d_trav_geo);
+  k_build_trav<<<nb, 128>>>(a, p->d_trav_off, nullptr, p->d_trav, p->d_trav_geo, p->d_ray_c);
   e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   return e;
@@ -958,9 +1077,8 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
                          : launch_cl_ny<TRACE_PATH>(a, p->ny, grid, smem, s);
     if (rec) cudaEventRecord(p->ev_m[p->n_rec], s);
     if (e == cudaSuccess) {   // deferred pairs (ill-conditioned or > RCAP crossings)
-      const size_t dsm = (size_t)16 * 2 * RCAP * MT_THREADS;
-      if (mode == TRACE_LL) k_trace_defer<TRACE_LL><<<2 * p->num_sms, MT_THREADS, dsm, s>>>(a);
-      else k_trace_defer<TRACE_PATH><<<2 * p->num_sms, MT_THREADS, dsm, s>>>(a);
+      if (mode == TRACE_LL) k_trace_defer<TRACE_LL><<<2 * p->num_sms, MT_THREADS, 0, s>>>(a);
+      else k_trace_defer<TRACE_PATH><<<2 * p->num_sms, MT_THREADS, 0, s>>>(a);
       e = cudaGetLastError();
       p->all_launches++;
     }
@@ -972,15 +1090,14 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
     a.rays_per_block = (p->R + S - 1) / S;
     S = (p->R + a.rays_per_block - 1) / a.rays_per_block;
     dim3 grid((unsigned)S, (unsigned)C);
-    size_t smem = (size_t)4 * ((2 * p->N + 3) & ~3) + (size_t)16 * 2 * RCAP * MT_THREADS;
+    size_t smem = (size_t)4 * ((2 * p->N + 3) & ~3) + (size_t)16 * 2 * RCAP * MT_THREADS + (size_t)8 * 8 * MT_THREADS;
     if (e == cudaSuccess)
       e = mode == TRACE_LL ? launch_rl_ny<TRACE_LL>(a, p->d_Hc, p->ny, grid, smem, s)
                            : launch_rl_ny<TRACE_PATH>(a, p->d_Hc, p->ny, grid, smem, s);
     if (rec) cudaEventRecord(p->ev_m[p->n_rec], s);
     if (e == cudaSuccess) {
-      const size_t dsm = (size_t)16 * 2 * RCAP * MT_THREADS;
-      if (mode == TRACE_LL) k_trace_defer<TRACE_LL><<<p->num_sms, MT_THREADS, dsm, s>>>(a);
-      else k_trace_defer<TRACE_PATH><<<p->num_sms, MT_THREADS, dsm, s>>>(a);
+      if (mode == TRACE_LL) k_trace_defer<TRACE_LL><<<2 * p->num_sms, MT_THREADS, 0, s>>>(a);
+      else k_trace_defer<TRACE_PATH><<<2 * p->num_sms, MT_THREADS, 0, s>>>(a);
       e = cudaGetLastError();
       p->all_launches += 2;
     }

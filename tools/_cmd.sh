@@ -1,4 +1,4 @@
-for v in default mb5 mb6; do
-  if [ $v = default ]; then unset MT_LIB; else export MT_LIB=$PWD/variants/libmt_$v.so; fi
-  timeout 300 python tools/trace_bench.py medium >> gpurun_out/tb_v18.log 2>&1
-done
+timeout 300 python tools/trace_bench.py ray_sharded > gpurun_out/tb_v24.log 2>&1
+timeout 300 python tools/trace_bench.py medium >> gpurun_out/tb_v24.log 2>&1
+timeout 900 python tools/parity_margin.py ray_sharded medium > gpurun_out/pm_v24.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_v24.log 2>&1
