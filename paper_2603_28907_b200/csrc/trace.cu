@@ -542,12 +542,12 @@ __device__ __forceinline__ void cw_solve(float4 h, int w, float4 cg, float za, f
 }
 
 template <int L>
-__device__ __forceinline__ void cw_surface(const float *__restrict__ Hl, int w, int oy, float4 cg,
-                                           float za, float zb, float Ls, float dz, float zmin,
+__device__ __forceinline__ void cw_surface(const float *__restrict__ Hg, unsigned off, int w, int oy,
+                                           float4 cg, float za, float zb, float Ls, float dz, float zmin,
                                            float zmax, float &B, int &n, int &defer, float4 *rec) {
   if (zb <= zmin) { B += Ls; return; }            // below the chain's lowest node of this surface
   if (za >= zmax) return;                         // above its highest node
-  const float *p = Hl + cell_off32(w);
+  const float *p = Hg + off;   // Hg: the heights array (kernel parameter); off: 32-bit element index
   cw_solve<L>(make_float4(__ldg(p), __ldg(p + 32), __ldg(p + oy), __ldg(p + oy + 32)), w, cg, za, zb, Ls,
               dz, B, n, defer, rec);
 }
@@ -570,7 +570,7 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a
   }
   if (!act) bd = make_float4(-3.0e38f, -3.0e38f, -3.0e38f, -3.0e38f);
   const int oy = ny * 32;
-  const float *H0 = a.H + (size_t)grp * 2 * N * 32 + lane, *H1 = H0 + N * 32;
+  const unsigned gbase = (unsigned)grp * 2 * N * 32 + lane;   // this lane's column of the group tile
   float llacc = 0.f;
 
   const int r_begin = blockIdx.x * (int)a.rays_per_block;
@@ -598,8 +598,9 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a
         const float4 cg = shift_geo(__ldg(a.trav_geo + k), ds);
         const float s1 = __int_as_float(w.y);
         const float zb = s1 * dz, Ls = s1 - s;
-        cw_surface<0>(H0, w.x, oy, cg, za, zb, Ls, dz, bd.x, bd.y, B0, n0, defer, rec);
-        cw_surface<1>(H1, w.x, oy, cg, za, zb, Ls, dz, bd.z, bd.w, B1, n1, defer, rec);
+        const unsigned off = cell_off32(w.x) + gbase;   // 32-bit element index (C·P < 2^32)
+        cw_surface<0>(a.H, off, w.x, oy, cg, za, zb, Ls, dz, bd.x, bd.y, B0, n0, defer, rec);
+        cw_surface<1>(a.H, off + N * 32, w.x, oy, cg, za, zb, Ls, dz, bd.z, bd.w, B1, n1, defer, rec);
         if (s1 >= s_hi) break;
         s = s1;
         za = zb;
