@@ -90,7 +90,7 @@ def full(rep, out, traffic=None):
                     return val * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
                 b = to_b(d["dram__bytes_read.sum"]) + to_b(d["dram__bytes_write.sum"])
                 json.dump({"kernel": d["_name"], "bytes_per_launch": b, "source": rep.split("/")[-1]},
-                          open(traffic, "w"), indent=1)
+                          open(traffic, "w"), indent=1)   # (profiles/trace_traffic.json nests these per workload)
                 print("traffic", b)
                 break
 
