@@ -491,10 +491,10 @@ int mt_loglik_heights(mt_problem *p, int32_t C, const float *H, double *ll, floa
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(ll, 0, sizeof(double) * C, s));
   CK(launch_tile(p, C, H, p->d_H, 1, s));
-  CK(cudaMemsetAsync(p->d_Hlo, 0, sizeof(float) * (size_t)(C + 31) / 32 * 32 * p->P, s));   // exact fp32 heights
+  CK(cudaMemsetAsync(p->d_Hlo, 0, sizeof(float) * ((size_t)(C + 31) / 32 * 32) * p->P, s));   // exact fp32 heights
   CK(launch_trace(p, TRACE_LL, C, p->d_H, p->d_band, p->d_G, ll, nullptr, nullptr, s));
   CK(launch_tile(p, C, p->d_G, dldH, 0, s));
-  CK(cudaMemsetAsync(p->d_G, 0, sizeof(float) * (size_t)(C + 31) / 32 * 32 * p->P, s));
+  CK(cudaMemsetAsync(p->d_G, 0, sizeof(float) * ((size_t)(C + 31) / 32 * 32) * p->P, s));
   return MT_OK;
 }
 
@@ -508,7 +508,7 @@ int mt_path_lengths(mt_problem *p, int32_t C, const float *H, float *L, float *O
   p->all_launches++;
   CK(cudaGetLastError());
   CK(launch_tile(p, C, H, p->d_H, 1, s));
-  CK(cudaMemsetAsync(p->d_Hlo, 0, sizeof(float) * (size_t)(C + 31) / 32 * 32 * p->P, s));   // exact fp32 heights
+  CK(cudaMemsetAsync(p->d_Hlo, 0, sizeof(float) * ((size_t)(C + 31) / 32 * 32) * p->P, s));   // exact fp32 heights
   CK(launch_trace(p, TRACE_PATH, C, p->d_H, p->d_band, nullptr, nullptr, L, O, s));
   return MT_OK;
 }

@@ -96,6 +96,24 @@ def test_loglik_and_adjoint_identical_heights(gpu, oracle_problem, name, C):
         assert rel_l2(G_d[c], out["dldH"][c]) <= 1e-3, (c, rel_l2(G_d[c], out["dldH"][c]))
 
 
+def test_caller_heights_at_full_chain_count(gpu, oracle_problem):
+    """mt_path_lengths / mt_loglik_heights with C = max_chains (64): every workspace
+    clear covers whole 32-chain groups (a precedence bug once cleared too much)."""
+    mp, op = gpu("small"), oracle_problem("small")
+    C = mp.max_chains
+    H = identical_heights(op.prob, C, 300, scale=1.0)
+    L_d, _ = mp.path_lengths(torch.from_numpy(H).to(DEV))
+    ll_d, G_d = mp.loglik_heights(torch.from_numpy(H).to(DEV))
+    sel = [0, 31, 32, C - 1]
+    L_o, _ = op.path_lengths(H[sel].astype(np.float64))
+    out = op.loglik_grad_H(H[sel].astype(np.float64))
+    L_d = L_d.cpu().numpy()[sel].astype(np.float64)
+    assert np.all(np.abs(L_d - L_o).max(2) <= 1e-5 * L_o.sum(2))
+    for k, c in enumerate(sel):
+        assert abs(ll_d.cpu().numpy()[c] - out["ll_dev"][k]) <= 1e-4 * abs(out["ll_dev"][k])
+        assert rel_l2(G_d.cpu().numpy()[c].astype(np.float64), out["dldH"][k]) <= 1e-3
+
+
 def test_heights_map(gpu, oracle_problem):
     mp, op = gpu("small"), oracle_problem("small")
     x = inputs.chain_states(op.prob["x_true"], 8, 2, scale=0.3)
