@@ -79,7 +79,7 @@ int check_chains(const mt_problem *p, int32_t C) {
 }
 
 void free_all(mt_problem *p) {
-  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_trav_geo, p->d_ray_c, p->d_ovf_q, p->d_ovf_n, p->d_H, p->d_Hlo, p->d_Hc, p->d_G,
+  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_trav_geo, p->d_rl_head, p->d_rl_code, p->d_rl_ovf, p->d_ovf_q, p->d_ovf_n, p->d_H, p->d_Hlo, p->d_Hc, p->d_G,
                   p->d_band, p->d_ll, p->d_x0, p->d_g0, p->d_mom, p->d_kin0, p->d_kin1, p->d_lp0};
   for (void *b : bufs)
     if (b) cudaFree(b);

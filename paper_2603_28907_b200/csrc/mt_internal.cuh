@@ -51,7 +51,12 @@ struct TraceArgs {
   const int32_t *trav_off;      // [R+1] CSR offsets of each ray's stored traversal
   const int2 *trav;             // {cell_pack(i, j), s_out bits} per cell, in ray order (a2)
   const float4 *trav_geo;       // per cell {u, v, α, β} at its entry (cell-local coordinates, a0)
-  const int4 *ray_c;            // per ray {first cell, end, cell word of the first cell, 0}
+  // ray-lane traversal replay (k_trace_rl): per ray {n | i0 << 8 | j0 << 15, overflow word},
+  // 2-bit exit codes of its cells (0 top, 1 x-line, 2 y-line, 3 vertex) for cells 0..63
+  // and the code words of cells >= 64; the exit parameters are recomputed bit-exactly
+  const int2 *rl_head;
+  const uint4 *rl_code;
+  const uint32_t *rl_ovf;
   const int32_t *perm;          // internal ray index -> caller's ray index
   int64_t R;                    // rays in the shard
   int64_t rays_per_block;
@@ -114,7 +119,9 @@ struct mt_problem {
   std::vector<int32_t> perm, inv_perm;   // internal <-> caller ray order (host)
   int2 *d_trav = nullptr;
   float4 *d_trav_geo = nullptr;
-  int4 *d_ray_c = nullptr;
+  int2 *d_rl_head = nullptr;
+  uint4 *d_rl_code = nullptr;
+  uint32_t *d_rl_ovf = nullptr;
   float4 *d_ovf_q = nullptr;    // deferred-pair queue of the chain-lanes trace (see TraceArgs)
   int *d_ovf_n = nullptr;       // [4]: count, blocks done, 64-bit cumulative count
   int ovf_cap = 1 << 22;

@@ -88,7 +88,7 @@ __device__ __forceinline__ DdaRay dda_ray(const Ray &r) {
 // exact comparisons; ties step both indices (R16).  s_ev = event parameter.
 __device__ __forceinline__ int dda_next(const DdaRay &q, int i, int j, const float *Xs,
                                         const float *Ys, int nx, int ny, float z_top,
-                                        float &s_ev) {
+                                        float &s_ev, int *fcode = nullptr) {
   float bn = z_top, bd = q.r.dz;  // top exit z_top/d_z (detectors at z = 0)
   float numx = 0.f, numy = 0.f;
   int ev = 4;
@@ -107,6 +107,7 @@ __device__ __forceinline__ int dda_next(const DdaRay &q, int i, int j, const flo
   if (ev & 4) s_ev = q.r.s_exit;
   else if (ev & 1) s_ev = numx * q.iadx;
   else s_ev = numy * q.iady;
+  if (fcode) *fcode = (ev & 4) ? 0 : (ev & 3);   // which formula gave s_ev (ray-lane step codes)
   if ((ev & 1) && ((q.sx > 0 && i + 1 == nx - 1) || (q.sx < 0 && i == 0))) ev |= 4;
   if ((ev & 2) && ((q.sy > 0 && j + 1 == ny - 1) || (q.sy < 0 && j == 0))) ev |= 4;
   return ev;
@@ -387,35 +388,6 @@ __device__ __forceinline__ int band_entry(const int2 *__restrict__ cells, int lo
   return lo;
 }
 
-// Band entry from an estimate (ray lanes: thread-private walks, where a binary
-// search costs ~log2(cells) dependent uncoalesced loads).  Each stored cell
-// after the first steps i, j or both, so the cell containing s is (almost)
-// entry |i(s) - i0| + |j(s) - j0| of the list (fewer by the vertex steps);
-// the estimate is then verified against the stored s_out and moved (rarely)
-// until it is the first cell with s_out > s.  rc = {off, end, first cell word}.
-__device__ __forceinline__ int band_entry_est(const int2 *__restrict__ cells, int4 rc, float ox, float oy,
-                                              float dx, float dy, float s, int nx, int ny, float &s_in) {
-  const float x = fmaf(s, dx, ox), y = fmaf(s, dy, oy);
-  const int i0 = cell_i(rc.z), j0 = cell_j(rc.z);
-  // the cell column / row holding (x, y): from the mean spacing, then corrected
-  int i = min(max((int)((x - sgeo[0][0]) * ((float)(nx - 1) / (sgeo[0][nx - 1] - sgeo[0][0]))), 0), nx - 2);
-  int j = min(max((int)((y - sgeo[1][0]) * ((float)(ny - 1) / (sgeo[1][ny - 1] - sgeo[1][0]))), 0), ny - 2);
-  while (i < nx - 2 && sgeo[0][i + 1] <= x) i++;
-  while (i > 0 && sgeo[0][i] > x) i--;
-  while (j < ny - 2 && sgeo[1][j + 1] <= y) j++;
-  while (j > 0 && sgeo[1][j] > y) j--;
-  int k = min(rc.x + abs(i - i0) + abs(j - j0), rc.y - 1);
-  for (int guard = 0; guard < 64; guard++) {
-    const float so = __int_as_float(__ldg(&cells[k].y));
-    const float sp = k > rc.x ? __int_as_float(__ldg(&cells[k - 1].y)) : 0.f;
-    if (so <= s && k < rc.y - 1) { k++; continue; }
-    if (sp > s && k > rc.x) { k--; continue; }
-    s_in = sp;
-    return k;
-  }
-  return band_entry(cells, rc.x, rc.y, s, s_in);   // not reached in practice
-}
-
 // Same, warp-cooperative (chain lanes, all 32 lanes converged, uniform
 // arguments): one coalesced load of 32 cells and a ballot per round.
 __device__ __forceinline__ int band_entry_warp(const int2 *__restrict__ cells, int lo, int hi, float s,
@@ -479,7 +451,8 @@ __device__ __forceinline__ void load_geometry(const TraceArgs &a, float *Xs, flo
 // traversal builder (create time): thread = ray; count pass then write pass
 // ---------------------------------------------------------------------------
 __global__ void k_build_trav(TraceArgs a, const int32_t *off, int32_t *count, int2 *cells, float4 *cgeo,
-                             int4 *ray_c) {
+                             int2 *rl_head, uint4 *rl_code, uint32_t *rl_ovf,
+                             const int32_t *ovf_off) {
   __shared__ float Xs[MT_MAX_AXIS], Ys[MT_MAX_AXIS];
   const int nx = a.tc.nx, ny = a.tc.ny;
   for (int k = threadIdx.x; k < nx; k += blockDim.x) Xs[k] = a.X[k];
@@ -491,10 +464,16 @@ __global__ void k_build_trav(TraceArgs a, const int32_t *off, int32_t *count, in
   int i = start_axis(Xs, nx, q.r.ox, q.r.dx), j = start_axis(Ys, ny, q.r.oy, q.r.dy);
   float s = 0.f, s_in = 0.f;   // s_in: the previous STORED s_out (what the walks carry)
   int n = 0;
-  if (ray_c) ray_c[rr] = make_int4(off[rr], off[rr + 1], cell_pack(i, j, ny), 0);
+  if (rl_head) rl_head[rr] = make_int2((off[rr + 1] - off[rr]) | (i << 8) | (j << 15), ovf_off[rr]);
+  uint32_t cw[4] = {0u, 0u, 0u, 0u};
   for (int guard = 0; guard < 4 * (MT_MAX_AXIS + 2); guard++) {
     float s_ev;
-    int ev = dda_next(q, i, j, Xs, Ys, nx, ny, a.tc.z_top, s_ev);
+    int fc;
+    int ev = dda_next(q, i, j, Xs, Ys, nx, ny, a.tc.z_top, s_ev, &fc);
+    if (rl_code) {   // 2-bit exit code of cell n: 0 top (s_exit), 1 x-line, 2 y-line, 3 vertex
+      if (n < 64) cw[n >> 4] |= (uint32_t)fc << (2 * (n & 15));
+      else atomicOr(rl_ovf + ovf_off[rr] + ((n - 64) >> 4), (uint32_t)fc << (2 * (n & 15)));
+    }
     float s1 = fminf(s_ev, q.r.s_exit);
     const float so = fmaxf(s1, s);
     if (cells) {
@@ -514,6 +493,7 @@ __global__ void k_build_trav(TraceArgs a, const int32_t *off, int32_t *count, in
     s = s1;
   }
   if (count) count[rr] = n;
+  if (rl_code) rl_code[rr] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
 }
 
 // ---------------------------------------------------------------------------
@@ -824,7 +804,6 @@ __global__ void __launch_bounds__(MT_THREADS, 4) k_trace_rl(TraceArgs a, const f
   const float4 bd = __ldg(a.band + c);
   const size_t coff = (size_t)(c >> 5) * 2 * N * 32 + (c & 31);
   float *G0 = a.G + coff, *G1 = G0 + (size_t)N * 32;
-  int2 *stage = reinterpret_cast<int2 *>(smem + ((2 * N + 3) & ~3) + 8 * RCAP * MT_THREADS) + tid;  // [8][MT_THREADS]
   __shared__ int next_ray;
   const int r_begin = blockIdx.x * (int)a.rays_per_block;
   const int r_end = min((int)a.R, r_begin + (int)a.rays_per_block);
@@ -848,47 +827,99 @@ __global__ void __launch_bounds__(MT_THREADS, 4) k_trace_rl(TraceArgs a, const f
     float B0 = s_lo, B1 = s_lo;
     int n0 = 0, n1 = 0, defer = 0;
     if (s_lo < s_exit) {
-      const int4 rc = __ldg(a.ray_c + rr);
-      const int kend = rc.y;
-      // cell geometry on the fly (thread-private walks: the stored per-cell
-      // geometry would triple the uncoalesced per-cell traffic)
+      // replay of the exact traversal from 2-bit exit codes (a2): the exit parameter
+      // of each cell is recomputed with the builder's fp32 operations, so the cells
+      // and their pieces are bit-identical to the stored traversal, from 16 B/ray
+      // of coalesced, L2-resident codes instead of 8 B/cell of scattered lists
+      const int2 hd = __ldg(a.rl_head + rr);
+      const uint4 cw = __ldg(a.rl_code + rr);
+      const int ncell = hd.x & 255;
+      int i = (hd.x >> 8) & 127, j = (hd.x >> 15) & 127;
       const float2 ro = __ldg(reinterpret_cast<const float2 *>(a.ray_a + rr));
       const float2 rd = __ldg(reinterpret_cast<const float2 *>(a.ray_a + rr) + 1);
-      float s_in0;
-      const int k0 = band_entry_est(a.trav, rc, ro.x, ro.y, rd.x, rd.y, s_lo, a.tc.nx, ny, s_in0);
-      float s = s_lo, za = s_lo * dz;
-      for (int k = k0; k < kend; k++) {
-        // the stored cells in batches of 8: eight independent loads in flight, then
-        // shared-memory reads (thread-private lists do not coalesce)
-        const int m = (k - k0) & 7;
-        if (m == 0) {
-          int2 v[8];
+      const int sx = rd.x > 0.f ? 1 : (rd.x < 0.f ? -1 : 0), sy = rd.y > 0.f ? 1 : (rd.y < 0.f ? -1 : 0);
+      const float adx = fabsf(rd.x), ady = fabsf(rd.y);
+      const float iadx = adx > 0.f ? 1.f / adx : 0.f, iady = ady > 0.f ? 1.f / ady : 0.f;
+      float s_prev = 0.f, s = s_lo, za = s_lo * dz;
+      int k = 0;
+      // jump to the band: the cell holding s_lo is (i, j) -> list entry |Δi| + |Δj| when no
+      // vertex step precedes it; checked against the codes (x/y step counts) and the
+      // recomputed exit parameters, else the replay simply starts from the first cell
+      if (ncell <= 64) {
+        const float x = fmaf(s_lo, rd.x, ro.x), y = fmaf(s_lo, rd.y, ro.y);
+        const int nx = a.tc.nx;
+        int ie = min(max((int)((x - sgeo[0][0]) * ((float)(nx - 1) / (sgeo[0][nx - 1] - sgeo[0][0]))), 0), nx - 2);
+        int je = min(max((int)((y - sgeo[1][0]) * ((float)(ny - 1) / (sgeo[1][ny - 1] - sgeo[1][0]))), 0), ny - 2);
+        while (ie < nx - 2 && sgeo[0][ie + 1] <= x) ie++;
+        while (ie > 0 && sgeo[0][ie] > x) ie--;
+        while (je < ny - 2 && sgeo[1][je + 1] <= y) je++;
+        while (je > 0 && sgeo[1][je] > y) je--;
+        const int ke = abs(ie - i) + abs(je - j);
+        if (ke > 1 && ke < ncell) {
+          // x and y steps among the exits of cells 0 .. ke-2 (the ones before cell ke-1)
+          const int m = ke - 1;
+          int nxs = 0, nys = 0;
 #pragma unroll
-          for (int q = 0; q < 8; q++) v[q] = k + q < kend ? __ldg(a.trav + k + q) : make_int2(0, 0);
-#pragma unroll
-          for (int q = 0; q < 8; q++) stage[q * MT_THREADS] = v[q];
+          for (int q = 0; q < 4; q++) {
+            const uint32_t wq = q == 0 ? cw.x : (q == 1 ? cw.y : (q == 2 ? cw.z : cw.w));
+            const int lo = 16 * q, cnt = min(max(m - lo, 0), 16);
+            const uint32_t mask = cnt >= 16 ? 0xffffffffu : ((1u << (2 * cnt)) - 1u);
+            nxs += __popc(wq & mask & 0x55555555u);
+            nys += __popc(wq & mask & 0xaaaaaaaau);
+          }
+          const int ip = i + sx * nxs, jp = j + sy * nys;    // cell ke-1
+          if (nxs + nys == m) {                               // no vertex step before it
+            const uint32_t wp = m - 1 < 16 ? cw.x : (m - 1 < 32 ? cw.y : (m - 1 < 48 ? cw.z : cw.w));
+            const int cp = (wp >> (2 * ((m - 1) & 15))) & 3;   // exit code of cell ke-2
+            // exit parameter of cell ke-2 (its stored s_out) needs that cell's (i, j)
+            const int i2 = ip - ((cp & 1) ? sx : 0), j2 = jp - ((cp & 2) ? sy : 0);
+            float e2;
+            if (cp == 0) e2 = s_exit;
+            else if (cp & 1) e2 = __fmul_rn(sx > 0 ? __fsub_rn(sgeo[0][i2 + 1], ro.x) : __fsub_rn(ro.x, sgeo[0][i2]), iadx);
+            else e2 = __fmul_rn(sy > 0 ? __fsub_rn(sgeo[1][j2 + 1], ro.y) : __fsub_rn(ro.y, sgeo[1][j2]), iady);
+            const float sp2 = fminf(e2, s_exit);
+            if (sp2 <= s_lo) {   // cells before ke-1 end at or below s_lo: start the replay at ke-1
+              k = m;
+              i = ip;
+              j = jp;
+              s_prev = sp2;      // (monotone s_out: max with earlier values is a no-op here)
+            }
+          }
         }
-        const int2 w = stage[m * MT_THREADS];
-        const int ci = cell_i(w.x), cj = cell_j(w.x);
-        const float ix = sgeo[2][ci], iy = sgeo[3][cj];
-        const float4 cg = make_float4((fmaf(s, rd.x, ro.x) - sgeo[0][ci]) * ix, (fmaf(s, rd.y, ro.y) - sgeo[1][cj]) * iy,
-                                      rd.x * ix, rd.y * iy);
-        const float s1 = __int_as_float(w.y);
-        const float zb = s1 * dz, Ls = s1 - s;
-        const int base = (int)(cell_off32(w.x) >> 5);
-        if (zb <= bd.x) B0 += Ls;
-        else if (za < bd.y) {
-          const float *p = Hs + base;
-          cw_solve<0>(make_float4(p[0], p[1], p[ny], p[ny + 1]), w.x, cg, za, zb, Ls, dz, B0, n0, defer, rec);
+      }
+      for (; k < ncell; k++) {
+        uint32_t word;
+        if (k < 64) word = k < 32 ? (k < 16 ? cw.x : cw.y) : (k < 48 ? cw.z : cw.w);
+        else word = __ldg(a.rl_ovf + hd.y + ((k - 64) >> 4));
+        const int code = (word >> (2 * (k & 15))) & 3;
+        float s_ev;
+        if (code == 0) s_ev = s_exit;
+        else if (code & 1) s_ev = __fmul_rn(sx > 0 ? __fsub_rn(sgeo[0][i + 1], ro.x) : __fsub_rn(ro.x, sgeo[0][i]), iadx);
+        else s_ev = __fmul_rn(sy > 0 ? __fsub_rn(sgeo[1][j + 1], ro.y) : __fsub_rn(ro.y, sgeo[1][j]), iady);
+        const float s1 = fmaxf(fminf(s_ev, s_exit), s_prev);   // the stored s_out
+        if (s1 > s_lo) {                                         // in the band (from its entry cell on)
+          const float ix = sgeo[2][i], iy = sgeo[3][j];
+          const float4 cg = make_float4((fmaf(s, rd.x, ro.x) - sgeo[0][i]) * ix,
+                                        (fmaf(s, rd.y, ro.y) - sgeo[1][j]) * iy, rd.x * ix, rd.y * iy);
+          const float zb = s1 * dz, Ls = s1 - s;
+          const int base = i * ny + j, w = base << 5;
+          if (zb <= bd.x) B0 += Ls;
+          else if (za < bd.y) {
+            const float *p = Hs + base;
+            cw_solve<0>(make_float4(p[0], p[1], p[ny], p[ny + 1]), w, cg, za, zb, Ls, dz, B0, n0, defer, rec);
+          }
+          if (zb <= bd.z) B1 += Ls;
+          else if (za < bd.w) {
+            const float *p = Hs + N + base;
+            cw_solve<1>(make_float4(p[0], p[1], p[ny], p[ny + 1]), w, cg, za, zb, Ls, dz, B1, n1, defer, rec);
+          }
+          if (s1 >= s_hi) break;
+          s = s1;
+          za = zb;
         }
-        if (zb <= bd.z) B1 += Ls;
-        else if (za < bd.w) {
-          const float *p = Hs + N + base;
-          cw_solve<1>(make_float4(p[0], p[1], p[ny], p[ny + 1]), w.x, cg, za, zb, Ls, dz, B1, n1, defer, rec);
-        }
-        if (s1 >= s_hi) break;
-        s = s1;
-        za = zb;
+        if (code & 1) i += sx;
+        if (code & 2) j += sy;
+        s_prev = s1;
       }
     }
     if (defer || n0 > RCAP || n1 > RCAP) {             // rare: the whole pair goes to k_trace_defer
@@ -949,7 +980,8 @@ static TraceArgs base_trace_args(mt_problem *p) {
   a.tc = p->tc;
   a.X = p->d_X; a.Y = p->d_Y;
   a.ray_a = p->d_ray_a; a.ray_b = p->d_ray_b; a.obase = p->d_obase;
-  a.trav_off = p->d_trav_off; a.trav = p->d_trav; a.trav_geo = p->d_trav_geo; a.ray_c = p->d_ray_c;
+  a.trav_off = p->d_trav_off; a.trav = p->d_trav; a.trav_geo = p->d_trav_geo;
+  a.rl_head = p->d_rl_head; a.rl_code = p->d_rl_code; a.rl_ovf = p->d_rl_ovf;
   a.perm = p->d_perm;
   a.R = p->R;
   a.ovf_q = p->d_ovf_q; a.ovf_n = p->d_ovf_n; a.ovf_done = p->d_ovf_n + 1; a.ovf_cap = p->ovf_cap;
@@ -964,32 +996,42 @@ cudaError_t build_traversal(mt_problem *p) {
   cudaError_t e = cudaMalloc(&d_cnt, sizeof(int32_t) * p->R);
   if (e != cudaSuccess) return e;
   unsigned nb = (unsigned)((p->R + 127) / 128);
-  k_build_trav<<<nb, 128>>>(a, nullptr, d_cnt, nullptr, nullptr, nullptr);
+  k_build_trav<<<nb, 128>>>(a, nullptr, d_cnt, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
   std::vector<int32_t> cnt(p->R);
   e = cudaMemcpy(cnt.data(), d_cnt, sizeof(int32_t) * p->R, cudaMemcpyDeviceToHost);
   cudaFree(d_cnt);
   if (e != cudaSuccess) return e;
-  std::vector<int32_t> off(p->R + 1, 0);
+  std::vector<int32_t> off(p->R + 1, 0), ovf(p->R + 1, 0);
   int64_t tot = 0;
   for (int64_t q = 0; q < p->R; q++) {
     tot += cnt[q];
     if (tot >= (int64_t)1 << 31) return cudaErrorInvalidValue;   // > 2^31 stored cells
     off[q + 1] = (int32_t)tot;
+    ovf[q + 1] = ovf[q] + (cnt[q] > 64 ? (cnt[q] - 64 + 15) / 16 : 0);   // step-code words past 64 cells
   }
   p->trav_cells = tot;
   e = cudaMalloc(&p->d_trav_off, sizeof(int32_t) * (p->R + 1));
   if (e == cudaSuccess) e = cudaMalloc(&p->d_trav, sizeof(int2) * (p->trav_cells > 0 ? p->trav_cells : 1));
   if (e == cudaSuccess) e = cudaMalloc(&p->d_trav_geo, sizeof(float4) * (p->trav_cells > 0 ? p->trav_cells : 1));
-  if (e == cudaSuccess) e = cudaMalloc(&p->d_ray_c, sizeof(int4) * p->R);
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_rl_head, sizeof(int2) * p->R);
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_rl_code, sizeof(uint4) * p->R);
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_rl_ovf, sizeof(uint32_t) * (ovf[p->R] > 0 ? ovf[p->R] : 1));
+  int32_t *d_ovfoff = nullptr;
+  if (e == cudaSuccess) e = cudaMalloc(&d_ovfoff, sizeof(int32_t) * (p->R + 1));
+  if (e == cudaSuccess) e = cudaMemcpy(d_ovfoff, ovf.data(), sizeof(int32_t) * (p->R + 1), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(p->d_rl_ovf, 0, sizeof(uint32_t) * (ovf[p->R] > 0 ? ovf[p->R] : 1));
   if (e == cudaSuccess)
     e = cudaMemcpy(p->d_trav_off, off.data(), sizeof(int32_t) * (p->R + 1), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return e;
   a.trav_off = p->d_trav_off;
   a.trav = p->d_trav;
   a.trav_geo = p->d_trav_geo;
-  k_build_trav<<<nb, 128>>>(a, p->d_trav_off, nullptr, p->d_trav, p->d_trav_geo, p->d_ray_c);
-  e = cudaGetLastError();
+  if (e == cudaSuccess)
+    k_build_trav<<<nb, 128>>>(a, p->d_trav_off, nullptr, p->d_trav, p->d_trav_geo, p->d_rl_head,
+                              p->d_rl_code, p->d_rl_ovf, d_ovfoff);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  cudaFree(d_ovfoff);
   return e;
 }
 
@@ -1091,7 +1133,7 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
     a.rays_per_block = (p->R + S - 1) / S;
     S = (p->R + a.rays_per_block - 1) / a.rays_per_block;
     dim3 grid((unsigned)S, (unsigned)C);
-    size_t smem = (size_t)4 * ((2 * p->N + 3) & ~3) + (size_t)16 * 2 * RCAP * MT_THREADS + (size_t)8 * 8 * MT_THREADS;
+    size_t smem = (size_t)4 * ((2 * p->N + 3) & ~3) + (size_t)16 * 2 * RCAP * MT_THREADS;
     if (e == cudaSuccess)
       e = mode == TRACE_LL ? launch_rl_ny<TRACE_LL>(a, p->d_Hc, p->ny, grid, smem, s)
                            : launch_rl_ny<TRACE_PATH>(a, p->d_Hc, p->ny, grid, smem, s);

@@ -1,5 +1,4 @@
-timeout 600 python bench.py > gpurun_out/bench_r1d.log 2>&1; echo "rc $?" >> gpurun_out/bench_r1d.log
-timeout 600 python bench.py --workload ray_sharded > gpurun_out/bench_ray_r1d.log 2>&1
-timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_short_r1d.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r1d.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch_r1d.log 2>&1
-timeout 300 python tools/trace_bench.py medium --chains 8192 --reps 2 > gpurun_out/tb8192d.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_trace -s 3 -c 2 -o gpurun_out/prof_r1d_8192 python tools/trace_bench.py medium --chains 8192 --reps 2 > gpurun_out/ncu_full_r1d.log 2>&1
-timeout 300 python tools/trace_bench.py ray_sharded --reps 3 > gpurun_out/tbray_d.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_trace -s 4 -c 2 -o gpurun_out/prof_r1d_ray python tools/trace_bench.py ray_sharded --reps 3 > gpurun_out/ncu_full_ray_r1d.log 2>&1
+timeout 300 python tools/trace_bench.py ray_sharded > gpurun_out/tb_v30.log 2>&1
+timeout 300 python tools/trace_bench.py small >> gpurun_out/tb_v30.log 2>&1
+timeout 600 python tools/parity_margin.py ray_sharded > gpurun_out/pm_v30.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_v30.log 2>&1
