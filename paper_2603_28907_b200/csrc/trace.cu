@@ -887,15 +887,21 @@ __global__ void __launch_bounds__(MT_THREADS, 4) k_trace_rl(TraceArgs a, const f
           }
         }
       }
+      // branch-free exit parameter: next x-line X[i + px] (px = [d_x > 0]) at distance
+      // sx·(X - o_x) (exact, HP3) over |d_x|; likewise y; code 0 = the top exit
+      const int px = sx > 0, py = sy > 0;
+      const float sxf = (float)sx, syf = (float)sy;
+      uint32_t word = k < 64 ? (k < 32 ? (k < 16 ? cw.x : cw.y) : (k < 48 ? cw.z : cw.w))
+                             : __ldg(a.rl_ovf + hd.y + ((k - 64) >> 4));
+      word >>= 2 * (k & 15);
       for (; k < ncell; k++) {
-        uint32_t word;
-        if (k < 64) word = k < 32 ? (k < 16 ? cw.x : cw.y) : (k < 48 ? cw.z : cw.w);
-        else word = __ldg(a.rl_ovf + hd.y + ((k - 64) >> 4));
-        const int code = (word >> (2 * (k & 15))) & 3;
-        float s_ev;
-        if (code == 0) s_ev = s_exit;
-        else if (code & 1) s_ev = __fmul_rn(sx > 0 ? __fsub_rn(sgeo[0][i + 1], ro.x) : __fsub_rn(ro.x, sgeo[0][i]), iadx);
-        else s_ev = __fmul_rn(sy > 0 ? __fsub_rn(sgeo[1][j + 1], ro.y) : __fsub_rn(ro.y, sgeo[1][j]), iady);
+        if (k > 0 && (k & 15) == 0)
+          word = k < 64 ? (k == 16 ? cw.y : (k == 32 ? cw.z : cw.w)) : __ldg(a.rl_ovf + hd.y + ((k - 64) >> 4));
+        const int code = word & 3;
+        word >>= 2;
+        const float numx = __fmul_rn(__fsub_rn(sgeo[0][i + px], ro.x), sxf);
+        const float numy = __fmul_rn(__fsub_rn(sgeo[1][j + py], ro.y), syf);
+        const float s_ev = code == 0 ? s_exit : __fmul_rn((code & 1) ? numx : numy, (code & 1) ? iadx : iady);
         const float s1 = fmaxf(fminf(s_ev, s_exit), s_prev);   // the stored s_out
         if (s1 > s_lo) {                                         // in the band (from its entry cell on)
           const float ix = sgeo[2][i], iy = sgeo[3][j];
