@@ -63,6 +63,8 @@ def lib():
         L.or_loglik_grad_H.argtypes = [ct.c_void_p, ct.c_int, _dp, _dp, _dp, _dp, ct.c_void_p, _lp]
         L.or_logpost_grad.argtypes = [ct.c_void_p, ct.c_int, _dp, _dp, _dp, _dp, _dp, _dp,
                                       ct.c_void_p, _lp]
+        L.or_torus_spectrum_dr.argtypes = [ct.c_int, ct.c_int, ct.c_double] + [ct.POINTER(ct.c_double)] * 4
+        L.or_logpost_grad_r.argtypes = [ct.c_void_p, ct.c_int, _dp, _dp, _dp, _dp, _dp]
         L.or_philox4x32_10.argtypes = [_up, _up, _up]
         L.or_momenta.argtypes = [ct.c_int, ct.c_uint64, ct.c_uint64, ct.c_uint64, _dp]
         L.or_mh_uniform.restype = ct.c_double
@@ -81,6 +83,13 @@ def torus_spectrum(nx: int, ny: int, r: float):
     s, ld = ct.c_double(), ct.c_double()
     lib().or_torus_spectrum(nx, ny, r, ct.byref(s), ct.byref(ld))
     return s.value, ld.value
+
+
+def torus_spectrum_dr(nx: int, ny: int, r: float):
+    """(σ, dσ/dr, ln det Q, d ln det Q/dr) of the torus CAR precision Q(r) = 4I - rA."""
+    out = [ct.c_double() for _ in range(4)]
+    lib().or_torus_spectrum_dr(nx, ny, r, *[ct.byref(o) for o in out])
+    return tuple(o.value for o in out)
 
 
 def prior_surface(x: np.ndarray, r: float):
@@ -203,6 +212,16 @@ class Problem:
         cnt = np.zeros(4, np.int64)
         lib().or_logpost_grad(self.h, C, x, logp, g, ll, lls, pr, sens.ctypes.data, cnt)
         return dict(logp=logp, grad=g, ll_dev=ll, ll_std=lls, prior=pr, sens=sens, counters=cnt)
+
+    def logpost_grad_r(self, v: np.ndarray):
+        """Sampled r_l (f2): v [C][2N+2] = (x_0, x_1, ρ_0, ρ_1), r_l = logistic(ρ_l)
+        -> dict(logp [C], grad [C][2N+2], ll_dev, prior)."""
+        v = np.ascontiguousarray(v, np.float64).reshape(-1, self.P + 2)
+        C = v.shape[0]
+        logp, ll, pr = np.zeros(C), np.zeros(C), np.zeros(C)
+        g = np.zeros_like(v)
+        lib().or_logpost_grad_r(self.h, C, v, logp, g, ll, pr)
+        return dict(logp=logp, grad=g, ll_dev=ll, prior=pr)
 
     def loglik_offset(self) -> float:
         """Σ_p (C ln C - C - ln Γ(C+1)): ll_std - ll_dev (R15)."""

@@ -518,6 +518,123 @@ void or_logpost_grad(const or_problem *p, int C, const double *x, double *logp, 
 }
 
 /* ------------------------------------------------------------------ */
+/* Hierarchical r_l (readings R13b/R13c)    */
+/* ------------------------------------------------------------------ */
+
+/* The torus spectrum of Q(r) = 4I - rA and its r-derivatives: eigenvalues
+ * λ_ab = 4 - r c_ab with c_ab = 2(cos 2πa/n_x + cos 2πb/n_y), so
+ *   σ² = N⁻¹ Σ 1/λ,  dσ²/dr = N⁻¹ Σ c/λ²,  ln det Q = Σ ln λ,  d ln det Q/dr = -Σ c/λ. */
+void or_torus_spectrum_dr(int nx, int ny, double r, double *sigma, double *dsigma, double *logdet,
+                          double *dlogdet) {
+  double s = 0.0, ds = 0.0, ld = 0.0, dld = 0.0;
+  for (int a = 0; a < nx; a++)
+    for (int b = 0; b < ny; b++) {
+      double c = 2.0 * (cos(2.0 * OR_PI * a / nx) + cos(2.0 * OR_PI * b / ny));
+      double lam = 4.0 - r * c;
+      s += 1.0 / lam;
+      ds += c / (lam * lam);
+      ld += log(lam);
+      dld -= c / lam;
+    }
+  double N = (double)nx * ny;
+  *sigma = sqrt(s / N);
+  *dsigma = (ds / N) / (2.0 * *sigma);
+  *logdet = ld;
+  *dlogdet = dld;
+}
+
+/* Log-posterior and gradient with the CAR dependence parameters sampled:
+ * v [C][2N + 2] = (x_0, x_1, ρ_0, ρ_1) with r_l = 1/(1 + e^{-ρ_l}) (R13b: the
+ * unconstrained coordinate of r_l ~ Unif(0,1), prior density of ρ_l
+ * = r_l (1 - r_l) by the change of variables), x_l | r_l ~ N(0, Q(r_l)^-1)
+ * (R13c: centred), heights ǔ = Φ(x/σ(r)):
+ *   logp = ll + Σ_l [-½ x_lᵀQ(r_l)x_l + ½ ln det Q(r_l) - (N/2) ln 2π + ln r_l + ln(1 - r_l)].
+ * ∂logp/∂ρ_l = r_l(1 - r_l) [½ x_lᵀ A x_l + ½ d ln det Q/dr + (∂ll/∂σ_l) dσ_l/dr] + 1 - 2 r_l,
+ * with ∂t/∂σ = -t/σ for t = x/σ inside the clamp (R18), so ∂ǔ/∂σ = -t φ(t)/σ. */
+void or_logpost_grad_r(const or_problem *p, int C, const double *v, double *logp, double *grad,
+                       double *ll_out, double *prior_out) {
+  int N = p->nx * p->ny, P = 2 * N + 2;
+  double *H = (double *)malloc(sizeof(double) * (size_t)C * 2 * N);
+  double *aux = (double *)malloc(sizeof(double) * (size_t)C * 5 * N);   /* dH/dx (3N), dH/dσ (2N) */
+  double *G = (double *)malloc(sizeof(double) * (size_t)C * 2 * N);
+  double *ll = (double *)malloc(sizeof(double) * C);
+  double *rr = (double *)malloc(sizeof(double) * C * 2), *sg = (double *)malloc(sizeof(double) * C * 2);
+  double *dsg = (double *)malloc(sizeof(double) * C * 2), *ld = (double *)malloc(sizeof(double) * C * 2);
+  double *dld = (double *)malloc(sizeof(double) * C * 2);
+  for (int c = 0; c < C; c++) {
+    const double *vc = v + (long)c * P;
+    for (int l = 0; l < 2; l++) {
+      double r = 1.0 / (1.0 + exp(-vc[2 * N + l]));
+      rr[2 * c + l] = r;
+      or_torus_spectrum_dr(p->nx, p->ny, r, &sg[2 * c + l], &dsg[2 * c + l], &ld[2 * c + l], &dld[2 * c + l]);
+    }
+    double *Hc = H + (long)c * 2 * N, *dx = aux + (long)c * 5 * N, *ds = dx + 3 * N;
+    for (int k = 0; k < N; k++) {
+      double t[2], u[2], dudx[2], duds[2];
+      for (int l = 0; l < 2; l++) {
+        double s = sg[2 * c + l];
+        double tt = vc[l * N + k] / s;
+        int clamped = 0;
+        if (tt > OR_TCLAMP) { tt = OR_TCLAMP; clamped = 1; }
+        if (tt < -OR_TCLAMP) { tt = -OR_TCLAMP; clamped = 1; }
+        t[l] = tt;
+        u[l] = 0.5 * erfc(-tt / sqrt(2.0));
+        double phi = clamped ? 0.0 : exp(-0.5 * tt * tt) / sqrt(2.0 * OR_PI);
+        dudx[l] = phi / s;
+        duds[l] = -tt * phi / s;
+      }
+      double H0 = u[0] * p->z_top, H1 = (1.0 - u[1]) * H0 + u[1] * p->z_top;
+      Hc[k] = H0;
+      Hc[N + k] = H1;
+      dx[k] = p->z_top * dudx[0];
+      dx[N + k] = (1.0 - u[1]) * p->z_top * dudx[0];
+      dx[2 * N + k] = (p->z_top - H0) * dudx[1];
+      ds[k] = p->z_top * duds[0];                         /* ∂H0/∂σ0 (∂H1/∂σ0 = (1-ǔ1)·this) */
+      ds[N + k] = (p->z_top - H0) * duds[1];              /* ∂H1/∂σ1 */
+      (void)t;
+    }
+  }
+  or_loglik_grad_H(p, C, H, ll, NULL, G, NULL, NULL);
+  for (int c = 0; c < C; c++) {
+    const double *vc = v + (long)c * P, *Gc = G + (long)c * 2 * N;
+    const double *dx = aux + (long)c * 5 * N, *ds = dx + 3 * N, *Hc = H + (long)c * 2 * N;
+    double *gc = grad + (long)c * P;
+    double pr = 0.0;
+    double dll_ds[2] = {0.0, 0.0};
+    for (int k = 0; k < N; k++) {
+      double u1 = (Hc[N + k] - Hc[k]) / (p->z_top - Hc[k]);   /* ǔ1 from H0, H1 */
+      dll_ds[0] += Gc[k] * ds[k] + Gc[N + k] * (1.0 - u1) * ds[k];
+      dll_ds[1] += Gc[N + k] * ds[N + k];
+    }
+    for (int l = 0; l < 2; l++) {
+      double r = rr[2 * c + l];
+      const double *x = vc + l * N;
+      double quad = 0.0, xAx = 0.0;
+      for (int i = 0; i < p->nx; i++)
+        for (int j = 0; j < p->ny; j++) {
+          int ip = (i + 1) % p->nx, im = (i - 1 + p->nx) % p->nx, jp = (j + 1) % p->ny, jm = (j - 1 + p->ny) % p->ny;
+          double nb = x[ip * p->ny + j] + x[im * p->ny + j] + x[i * p->ny + jp] + x[i * p->ny + jm];
+          double Qx = 4.0 * x[i * p->ny + j] - r * nb;
+          quad += x[i * p->ny + j] * Qx;
+          xAx += x[i * p->ny + j] * nb;
+          gc[l * N + i * p->ny + j] = -Qx;
+        }
+      pr += -0.5 * quad + 0.5 * ld[2 * c + l] - 0.5 * N * log(2.0 * OR_PI) + log(r) + log(1.0 - r);
+      gc[2 * N + l] = r * (1.0 - r) * (0.5 * xAx + 0.5 * dld[2 * c + l] + dll_ds[l] * dsg[2 * c + l])
+                      + 1.0 - 2.0 * r;
+    }
+    for (int k = 0; k < N; k++) {
+      gc[k] += Gc[k] * dx[k] + Gc[N + k] * dx[N + k];
+      gc[N + k] += Gc[N + k] * dx[2 * N + k];
+    }
+    logp[c] = ll[c] + pr;
+    if (ll_out) ll_out[c] = ll[c];
+    if (prior_out) prior_out[c] = pr;
+  }
+  free(H); free(aux); free(G); free(ll); free(rr); free(sg); free(dsg); free(ld); free(dld);
+}
+
+/* ------------------------------------------------------------------ */
 /* Philox4x32-10 (Salmon et al., SC'11) and momenta (R22, reading c.1.12) */
 /* ------------------------------------------------------------------ */
 void or_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
