@@ -82,6 +82,10 @@ typedef struct {
   int64_t ray_lo, ray_hi;    /* this rank's ray shard [ray_lo, ray_hi); (0, n_rays) unsharded */
   int32_t device;            /* CUDA device ordinal */
   int32_t max_chains;        /* capacity of the per-chain workspace */
+  int32_t sample_r;          /* 0: r_l = car_r[l] fixed (R13, the hot path).  1: hierarchical r_l
+                                (SURVEY §8(f) f2): each chain's state gains two
+                                parameters ρ_0, ρ_1 with r_l = 1/(1+e^{-ρ_l}) ~ Unif(0,1); the
+                                prior, σ_l and ln det Q_l then follow each chain's r_l (car_r unused) */
 } mt_problem_desc;
 
 /* Validate the description, precompute per-ray constants (in-box extent,
@@ -93,7 +97,7 @@ int mt_problem_create(const mt_problem_desc *desc, mt_problem **out);
 /* Free everything the problem owns.  NULL-safe.  Synchronous. */
 int mt_problem_destroy(mt_problem *p);
 
-/* P = 2*n_x*n_y parameters per chain; rays in this shard. */
+/* P = 2*n_x*n_y (+ 2 with sample_r: ρ_0, ρ_1 last) parameters per chain; rays in this shard. */
 int32_t mt_num_params(const mt_problem *p);
 int64_t mt_num_rays(const mt_problem *p);
 

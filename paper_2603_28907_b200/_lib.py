@@ -34,7 +34,7 @@ class _Desc(ct.Structure):
         ("n_rays", ct.c_int64), ("ray_det", ct.c_void_p), ("ray_dir", ct.c_void_p),
         ("ray_w", ct.c_void_p), ("counts", ct.c_void_p),
         ("ray_lo", ct.c_int64), ("ray_hi", ct.c_int64),
-        ("device", ct.c_int32), ("max_chains", ct.c_int32),
+        ("device", ct.c_int32), ("max_chains", ct.c_int32), ("sample_r", ct.c_int32),
     ]
 
 
@@ -127,7 +127,7 @@ class Problem:
     """A canonical problem bound to one CUDA device (mt_problem_create)."""
 
     def __init__(self, prob: dict, device: int = 0, max_chains: int = 1,
-                 ray_lo: int = 0, ray_hi: Optional[int] = None):
+                 ray_lo: int = 0, ray_hi: Optional[int] = None, sample_r: bool = False):
         self._keep = {
             "node_x": np.ascontiguousarray(prob["node_x"], np.float32),
             "node_y": np.ascontiguousarray(prob["node_y"], np.float32),
@@ -156,6 +156,7 @@ class Problem:
         d.ray_hi = R if ray_hi is None else ray_hi
         d.device = device
         d.max_chains = max_chains
+        d.sample_r = 1 if sample_r else 0
         h = ct.c_void_p()
         _check(lib().mt_problem_create(ct.byref(d), ct.byref(h)), "mt_problem_create")
         self.h = h
@@ -250,15 +251,16 @@ class Problem:
         import torch
         C = x.shape[0]
         _dev_tensor(x, torch.float32, (C, self.P), self.device, "x")
-        H = torch.empty_like(x)
+        H = torch.empty((C, 2 * self.nx * self.ny), dtype=torch.float32, device=x.device)
         _check(lib().mt_heights(self.h, C, _ptr(x), _ptr(H), _stream(stream)), "mt_heights")
         return H.view(C, 2, self.nx, self.ny)
 
     def loglik_heights(self, H, stream=None):
         import torch
         C = H.shape[0]
-        H = H.reshape(C, self.P)
-        _dev_tensor(H, torch.float32, (C, self.P), self.device, "H")
+        NH = 2 * self.nx * self.ny
+        H = H.reshape(C, NH)
+        _dev_tensor(H, torch.float32, (C, NH), self.device, "H")
         ll = torch.empty(C, dtype=torch.float64, device=H.device)
         G = torch.empty_like(H)
         _check(lib().mt_loglik_heights(self.h, C, _ptr(H), _ptr(ll), _ptr(G), _stream(stream)),
@@ -268,8 +270,9 @@ class Problem:
     def path_lengths(self, H, stream=None):
         import torch
         C = H.shape[0]
-        H = H.reshape(C, self.P)
-        _dev_tensor(H, torch.float32, (C, self.P), self.device, "H")
+        NH = 2 * self.nx * self.ny
+        H = H.reshape(C, NH)
+        _dev_tensor(H, torch.float32, (C, NH), self.device, "H")
         L = torch.empty((C, self.R, 3), dtype=torch.float32, device=H.device)
         O = torch.empty((C, self.R), dtype=torch.float32, device=H.device)
         _check(lib().mt_path_lengths(self.h, C, _ptr(H), _ptr(L), _ptr(O), _stream(stream)),

@@ -79,7 +79,7 @@ int check_chains(const mt_problem *p, int32_t C) {
 }
 
 void free_all(mt_problem *p) {
-  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_trav_geo, p->d_rl_head, p->d_rl_code, p->d_rl_ovf, p->d_ovf_q, p->d_ovf_n, p->d_H, p->d_Hlo, p->d_Hc, p->d_G,
+  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_trav_geo, p->d_rl_head, p->d_rl_code, p->d_rl_ovf, p->d_ovf_q, p->d_ovf_n, p->d_H, p->d_Hlo, p->d_Hc, p->d_cs, p->d_G,
                   p->d_band, p->d_ll, p->d_x0, p->d_g0, p->d_mom, p->d_kin0, p->d_kin1, p->d_lp0};
   for (void *b : bufs)
     if (b) cudaFree(b);
@@ -151,7 +151,8 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   DevGuard g(d->device);
   p->device = d->device;
   cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, d->device);
-  p->nx = d->n_x; p->ny = d->n_y; p->N = d->n_x * d->n_y; p->P = 2 * p->N;
+  p->sample_r = d->sample_r ? 1 : 0;
+  p->nx = d->n_x; p->ny = d->n_y; p->N = d->n_x * d->n_y; p->P = 2 * p->N + 2 * p->sample_r;
   p->R = d->ray_hi - d->ray_lo;
   p->ray_lo = d->ray_lo;
   p->max_chains = d->max_chains;
@@ -255,6 +256,7 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   ALLOC(p->d_lp0, sizeof(double) * MC);
   ALLOC(p->d_ovf_q, sizeof(float4) * (size_t)p->ovf_cap);
   ALLOC(p->d_ovf_n, sizeof(int) * 4);
+  ALLOC(p->d_cs, sizeof(double) * p->N);
 #undef ALLOC
   if (e != cudaSuccess) {
     free_all(p);
@@ -273,6 +275,13 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   if (e == cudaSuccess) e = cudaMemset(p->d_Hlo, 0, sizeof(float) * MC32 * P);
   if (e == cudaSuccess) e = cudaMemset(p->d_ll, 0, sizeof(double) * MC);
   if (e == cudaSuccess) e = cudaMemset(p->d_ovf_n, 0, sizeof(int) * 4);
+  if (e == cudaSuccess) {   // torus spectrum table c_ab = 2(cos 2πa/n_x + cos 2πb/n_y) (sample_r)
+    std::vector<double> cs(p->N);
+    for (int a = 0; a < p->nx; a++)
+      for (int b = 0; b < p->ny; b++)
+        cs[a * p->ny + b] = 2.0 * (cos(2.0 * M_PI * a / p->nx) + cos(2.0 * M_PI * b / p->ny));
+    e = cudaMemcpy(p->d_cs, cs.data(), sizeof(double) * p->N, cudaMemcpyHostToDevice);
+  }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e == cudaSuccess) e = build_traversal(p);   // a2, once per problem (exact predicates)
   if (e != cudaSuccess) {

@@ -19,6 +19,7 @@ struct NodeH {
   float H0, H1;      // heights (fp32, computed in fp64)
   float L0, L1;      // fp32 residuals: H + L = the fp64 heights to ~1e-14 (HP2)
   double J0, J10, J11;  // ∂H0/∂x0, ∂H1/∂x0, ∂H1/∂x1
+  double t0, t1;        // x/σ (clamped): ∂H/∂σ = -t·∂H/∂x (sampled r, f2)
 };
 
 // Gaussian copula + stick-breaking: ǔ = Φ(clamp(x/σ)),
@@ -37,6 +38,8 @@ __device__ __forceinline__ NodeH node_heights(float x0, float x1, double is0, do
   o.H1 = (float)h1;
   o.L0 = (float)(h0 - (double)o.H0);
   o.L1 = (float)(h1 - (double)o.H1);
+  o.t0 = t0;
+  o.t1 = t1;
   if (want_jac) {
     const double inv_sqrt_2pi = 0.39894228040143267794;
     double d0 = c0 ? 0.0 : exp(-0.5 * t0 * t0) * inv_sqrt_2pi * is0;
@@ -124,6 +127,67 @@ __device__ __forceinline__ void momenta4(uint64_t seed, uint64_t iter, uint64_t 
     z[2 * h] = rad * cs;
     z[2 * h + 1] = rad * sn;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Sampled r_l (readings R13b/R13c): state per chain
+// (x_0, x_1, ρ_0, ρ_1), r_l = logistic(ρ_l).  Every per-chain kernel first
+// evaluates the torus spectrum of Q(r_l) = 4I - r_l A for its chain (a block
+// reduction over the N eigenvalues λ = 4 - r c_ab, c_ab = 2(cos 2πa/n_x +
+// cos 2πb/n_y)): σ_l (the copula scale), dσ_l/dr, ln det Q(r_l)
+// and its derivative.
+// ---------------------------------------------------------------------------
+// In-place block sum of K doubles (all threads get the totals).
+template <int K>
+__device__ __forceinline__ void block_sum(double *v) {
+  __shared__ double sh[K][MT_THREADS / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int q = 0; q < K; q++) v[q] = warp_sum(v[q]);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < K; q++) sh[q][w] = v[q];
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < K; q++) {
+    double t = 0.0;
+    for (int k = 0; k < nw; k++) t += sh[q][k];
+    v[q] = t;
+  }
+  __syncthreads();
+}
+
+struct Spec {
+  double r[2], inv_sigma[2], dsig[2], ld[2], dld[2];
+};
+
+__device__ __forceinline__ Spec block_spectrum(const double *cs, int N, float rho0, float rho1, bool logs) {
+  Spec o;
+  o.r[0] = 1.0 / (1.0 + exp(-(double)rho0));
+  o.r[1] = 1.0 / (1.0 + exp(-(double)rho1));
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    const double c = cs[k];
+#pragma unroll
+    for (int l = 0; l < 2; l++) {
+      const double lam = 4.0 - o.r[l] * c, il = 1.0 / lam;
+      acc[4 * l] += il;
+      acc[4 * l + 1] += c * il * il;
+      if (logs) acc[4 * l + 2] += log(lam);
+      acc[4 * l + 3] -= c * il;
+    }
+  }
+  block_sum<8>(acc);
+#pragma unroll
+  for (int l = 0; l < 2; l++) {
+    const double sg = sqrt(acc[4 * l] / N);
+    o.inv_sigma[l] = 1.0 / sg;
+    o.dsig[l] = (acc[4 * l + 1] / N) / (2.0 * sg);
+    o.ld[l] = acc[4 * l + 2];
+    o.dld[l] = acc[4 * l + 3];
+  }
+  return o;
 }
 
 }  // namespace
@@ -295,8 +359,14 @@ __global__ void __launch_bounds__(MT_THREADS) k_hmc_begin(FinishArgs a, const do
     }
   }
   __syncthreads();
+  double is0 = a.inv_sigma[0], is1 = a.inv_sigma[1];
+  if (a.sample_r) {   // σ of the drifted ρ (f2)
+    const Spec sp = block_spectrum(a.cs, N, xc[2 * N], xc[2 * N + 1], false);
+    is0 = sp.inv_sigma[0];
+    is1 = sp.inv_sigma[1];
+  }
   for (int k = threadIdx.x; k < N; k += blockDim.x) {
-    NodeH h = node_heights(xc[k], xc[N + k], a.inv_sigma[0], a.inv_sigma[1], a.z_top, false);
+    NodeH h = node_heights(xc[k], xc[N + k], is0, is1, a.z_top, false);
     a.H[tix(c, 0, k, N)] = h.H0;
     a.H[tix(c, 1, k, N)] = h.H1;
     a.Hlo[tix(c, 0, k, N)] = h.L0;
@@ -385,6 +455,197 @@ __global__ void k_ffma(float *out, int iters, float a, float b, long long *cycle
 }
 
 // ---------------------------------------------------------------------------
+// sampled-r variants of K1 / K3 / kicks (f2).  The fixed-r kernels above stay
+// single-pass; here a leapfrog step needs σ(r) of the DRIFTED ρ before the next
+// heights, so the update is split: ρ first (one thread), then the spectrum, then
+// the nodes.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void heights_nodes_r(const FinishArgs &a, int c, const float *xc, const Spec &sp) {
+  BlockRed v = {3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f, 0.0, 0.0, 0};
+  for (int k = threadIdx.x; k < a.N; k += blockDim.x) {
+    NodeH h = node_heights(xc[k], xc[a.N + k], sp.inv_sigma[0], sp.inv_sigma[1], a.z_top, false);
+    a.H[tix(c, 0, k, a.N)] = h.H0;
+    a.H[tix(c, 1, k, a.N)] = h.H1;
+    a.Hlo[tix(c, 0, k, a.N)] = h.L0;
+    a.Hlo[tix(c, 1, k, a.N)] = h.L1;
+    v.mn0 = fminf(v.mn0, h.H0); v.mx0 = fmaxf(v.mx0, h.H0);
+    v.mn1 = fminf(v.mn1, h.H1); v.mx1 = fmaxf(v.mx1, h.H1);
+  }
+  BlockRed r = block_reduce(v);
+  if (threadIdx.x == 0) a.band[c] = make_float4(r.mn0, r.mx0, r.mn1, r.mx1);
+}
+
+__global__ void __launch_bounds__(MT_THREADS) k_heights_r(FinishArgs a, const float *x) {
+  const int c = blockIdx.x;
+  const float *xc = x + (size_t)c * a.P;
+  const Spec sp = block_spectrum(a.cs, a.N, xc[2 * a.N], xc[2 * a.N + 1], false);
+  heights_nodes_r(a, c, xc, sp);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(MT_THREADS) k_finish_r(FinishArgs a) {
+  extern __shared__ float xs[];  // [P] current state of this chain
+  __shared__ float s_new[2];
+  const int c = blockIdx.x, N = a.N, ny = a.ny, nx = a.nx;
+  float *xc = a.x + (size_t)c * a.P;
+  for (int k = threadIdx.x; k < a.P; k += blockDim.x) xs[k] = xc[k];
+  __syncthreads();
+  const Spec sp = block_spectrum(a.cs, N, xs[2 * N], xs[2 * N + 1], a.prior_on != 0);
+  float *Gt = const_cast<float *>(a.G);
+  float *gc = a.grad + (size_t)c * a.P;
+  float *pc = MODE != FIN_PLAIN ? a.mom + (size_t)c * a.P : nullptr;
+  const float eps = MODE != FIN_PLAIN ? a.eps[c] : 0.f;
+  // quad_l = x_lᵀQx_l, xAx_l = x_lᵀAx_l, tg_l = Σ t·∂ll/∂x_l (= -∂ll/∂σ_l), kinetic, bad
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    const int i = k / ny, j = k - i * ny;
+    const float x0 = xs[k], x1 = xs[N + k];
+    const NodeH h = node_heights(x0, x1, sp.inv_sigma[0], sp.inv_sigma[1], a.z_top, true);
+    const size_t t0 = tix(c, 0, k, N), t1 = tix(c, 1, k, N);
+    const float G0 = Gt[t0], G1 = Gt[t1];
+    Gt[t0] = 0.f;
+    Gt[t1] = 0.f;
+    double gx0 = (double)G0 * h.J0 + (double)G1 * h.J10;
+    double gx1 = (double)G1 * h.J11;
+    acc[4] += h.t0 * gx0;
+    acc[5] += h.t1 * gx1;
+    if (a.prior_on) {
+      const int ip = (i + 1 == nx ? 0 : i + 1) * ny + j, im = (i == 0 ? nx - 1 : i - 1) * ny + j;
+      const int jp = i * ny + (j + 1 == ny ? 0 : j + 1), jm = i * ny + (j == 0 ? ny - 1 : j - 1);
+#pragma unroll
+      for (int l = 0; l < 2; l++) {
+        const float *xl = xs + l * N;
+        const double xv = xl[k], nb = (double)xl[ip] + xl[im] + xl[jp] + xl[jm];
+        const double Qx = 4.0 * xv - sp.r[l] * nb;
+        acc[l] += xv * Qx;
+        acc[2 + l] += xv * nb;
+        if (l == 0) gx0 -= Qx; else gx1 -= Qx;
+      }
+    }
+    const float g0f = (float)gx0, g1f = (float)gx1;
+    gc[k] = g0f;
+    gc[N + k] = g1f;
+    if (!(isfinite(g0f) && isfinite(g1f))) acc[7] = 1.0;
+    if (MODE == FIN_LAST) {
+      const float p0 = pc[k] + 0.5f * eps * g0f, p1 = pc[N + k] + 0.5f * eps * g1f;
+      pc[k] = p0;
+      pc[N + k] = p1;
+      acc[6] += 0.5 * ((double)p0 * p0 + (double)p1 * p1);
+    }
+  }
+  block_sum<8>(acc);
+  if (threadIdx.x == 0) {
+    double lp = a.ll[c];
+    float gr[2];
+#pragma unroll
+    for (int l = 0; l < 2; l++) {
+      const double r = sp.r[l], drdrho = r * (1.0 - r);
+      double g = drdrho * (-acc[4 + l]) * sp.dsig[l];   // ∂ll/∂σ = -Σ t ∂ll/∂x (∂H/∂σ = -t ∂H/∂x)
+      if (a.prior_on) {
+        g += drdrho * (0.5 * acc[2 + l] + 0.5 * sp.dld[l]) + 1.0 - 2.0 * r;
+        lp += -0.5 * acc[l] + 0.5 * sp.ld[l] - 0.5 * N * log(2.0 * M_PI) + log(r) + log(1.0 - r);
+      }
+      gr[l] = (float)g;
+      gc[2 * N + l] = gr[l];
+    }
+    a.ll[c] = 0.0;
+    a.logp[c] = lp;
+    const int bad = acc[7] != 0.0 || !isfinite(lp) || !isfinite(gr[0]) || !isfinite(gr[1]);
+    if (a.status) a.status[c] = bad ? MT_STATUS_NONFINITE : 0;
+    if (MODE == FIN_LAST) {
+      double kin = acc[6];
+      for (int l = 0; l < 2; l++) {
+        const float pr = pc[2 * N + l] + 0.5f * eps * gr[l];
+        pc[2 * N + l] = pr;
+        kin += 0.5 * (double)pr * pr;
+      }
+      if (a.kin) a.kin[c] = (float)kin;
+    }
+    if (MODE == FIN_STEP) {   // close this step's half kick, open the next: p += ε g; ρ += ε p
+      for (int l = 0; l < 2; l++) {
+        const float pr = pc[2 * N + l] + eps * gr[l];
+        pc[2 * N + l] = pr;
+        s_new[l] = xs[2 * N + l] + eps * pr;
+        xc[2 * N + l] = s_new[l];
+      }
+    }
+  }
+  if (MODE == FIN_STEP) {
+    __syncthreads();
+    const Spec sn = block_spectrum(a.cs, N, s_new[0], s_new[1], false);
+    BlockRed v = {3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f, 0.0, 0.0, 0};
+    for (int k = threadIdx.x; k < N; k += blockDim.x) {
+      const float p0 = pc[k] + eps * gc[k], p1 = pc[N + k] + eps * gc[N + k];
+      pc[k] = p0;
+      pc[N + k] = p1;
+      const float xn0 = xs[k] + eps * p0, xn1 = xs[N + k] + eps * p1;
+      xc[k] = xn0;
+      xc[N + k] = xn1;
+      const NodeH hn = node_heights(xn0, xn1, sn.inv_sigma[0], sn.inv_sigma[1], a.z_top, false);
+      const size_t t0 = tix(c, 0, k, N), t1 = tix(c, 1, k, N);
+      a.H[t0] = hn.H0;
+      a.H[t1] = hn.H1;
+      a.Hlo[t0] = hn.L0;
+      a.Hlo[t1] = hn.L1;
+      v.mn0 = fminf(v.mn0, hn.H0); v.mx0 = fmaxf(v.mx0, hn.H0);
+      v.mn1 = fminf(v.mn1, hn.H1); v.mx1 = fmaxf(v.mx1, hn.H1);
+    }
+    BlockRed r = block_reduce(v);
+    if (threadIdx.x == 0) a.band[c] = make_float4(r.mn0, r.mx0, r.mn1, r.mx1);
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(MT_THREADS) k_kick_r(FinishArgs a) {
+  __shared__ float s_new[2];
+  __shared__ double s_kin;
+  const int c = blockIdx.x, N = a.N;
+  float *xc = a.x + (size_t)c * a.P, *pc = a.mom + (size_t)c * a.P;
+  const float *gc = a.grad + (size_t)c * a.P;
+  const float eps = a.eps[c];
+  const float f = MODE == KICK_FULL_DRIFT ? eps : 0.5f * eps;
+  if (threadIdx.x == 0) {
+    double kin = 0.0;
+    for (int l = 0; l < 2; l++) {
+      const float pr = pc[2 * N + l] + f * gc[2 * N + l];
+      pc[2 * N + l] = pr;
+      kin += 0.5 * (double)pr * pr;
+      if (MODE != KICK_HALF_LAST) xc[2 * N + l] += eps * pr;
+      s_new[l] = xc[2 * N + l];
+    }
+    s_kin = kin;
+  }
+  __syncthreads();
+  Spec sp{};
+  if (MODE != KICK_HALF_LAST) sp = block_spectrum(a.cs, N, s_new[0], s_new[1], false);
+  BlockRed v = {3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f, 0.0, 0.0, 0};
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    const float p0 = pc[k] + f * gc[k], p1 = pc[N + k] + f * gc[N + k];
+    pc[k] = p0;
+    pc[N + k] = p1;
+    if (MODE == KICK_HALF_LAST) {
+      v.s1 += 0.5 * ((double)p0 * p0 + (double)p1 * p1);
+      continue;
+    }
+    const float x0 = xc[k] + eps * p0, x1 = xc[N + k] + eps * p1;
+    xc[k] = x0;
+    xc[N + k] = x1;
+    const NodeH h = node_heights(x0, x1, sp.inv_sigma[0], sp.inv_sigma[1], a.z_top, false);
+    a.H[tix(c, 0, k, N)] = h.H0;
+    a.H[tix(c, 1, k, N)] = h.H1;
+    a.Hlo[tix(c, 0, k, N)] = h.L0;
+    a.Hlo[tix(c, 1, k, N)] = h.L1;
+    v.mn0 = fminf(v.mn0, h.H0); v.mx0 = fmaxf(v.mx0, h.H0);
+    v.mn1 = fminf(v.mn1, h.H1); v.mx1 = fmaxf(v.mx1, h.H1);
+  }
+  BlockRed r = block_reduce(v);
+  if (threadIdx.x == 0) {
+    if (MODE == KICK_HALF_LAST) a.kin[c] = (float)(r.s1 + s_kin);
+    else a.band[c] = make_float4(r.mn0, r.mx0, r.mn1, r.mx1);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
 static FinishArgs base_args(mt_problem *p, int C) {
@@ -403,6 +664,8 @@ static FinishArgs base_args(mt_problem *p, int C) {
   a.H = p->d_H;
   a.Hlo = p->d_Hlo;
   a.band = p->d_band;
+  a.sample_r = p->sample_r;
+  a.cs = p->d_cs;
   return a;
 }
 
@@ -413,7 +676,8 @@ cudaError_t launch_heights(mt_problem *p, int C, const float *x, float *H, float
   a.H = H;
   a.Hlo = p->d_Hlo;
   a.band = band;
-  k_heights<<<C, MT_THREADS, 0, s>>>(a, x);
+  if (p->sample_r) k_heights_r<<<C, MT_THREADS, 0, s>>>(a, x);
+  else k_heights<<<C, MT_THREADS, 0, s>>>(a, x);
   p->all_launches++;
   return cudaGetLastError();
 }
@@ -435,7 +699,21 @@ cudaError_t launch_finish(mt_problem *p, int mode, int C, float *x, float *grad,
       cudaFuncSetAttribute(k_finish<FIN_LAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     attr[mode] = true;
   }
-  if (mode == FIN_PLAIN) k_finish<FIN_PLAIN><<<C, MT_THREADS, smem, s>>>(a);
+  if (p->sample_r) {
+    static bool attr_r[3] = {false, false, false};
+    if (smem > 48 * 1024 && !attr_r[mode]) {
+      if (mode == FIN_PLAIN)
+        cudaFuncSetAttribute(k_finish_r<FIN_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      if (mode == FIN_STEP)
+        cudaFuncSetAttribute(k_finish_r<FIN_STEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      if (mode == FIN_LAST)
+        cudaFuncSetAttribute(k_finish_r<FIN_LAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      attr_r[mode] = true;
+    }
+    if (mode == FIN_PLAIN) k_finish_r<FIN_PLAIN><<<C, MT_THREADS, smem, s>>>(a);
+    else if (mode == FIN_STEP) k_finish_r<FIN_STEP><<<C, MT_THREADS, smem, s>>>(a);
+    else k_finish_r<FIN_LAST><<<C, MT_THREADS, smem, s>>>(a);
+  } else if (mode == FIN_PLAIN) k_finish<FIN_PLAIN><<<C, MT_THREADS, smem, s>>>(a);
   else if (mode == FIN_STEP) k_finish<FIN_STEP><<<C, MT_THREADS, smem, s>>>(a);
   else k_finish<FIN_LAST><<<C, MT_THREADS, smem, s>>>(a);
   p->all_launches++;
@@ -447,7 +725,11 @@ cudaError_t launch_kick(mt_problem *p, int mode, int C, float *x, float *mom, co
   if (C <= 0) return cudaSuccess;
   FinishArgs a = base_args(p, C);
   a.x = x; a.mom = mom; a.grad = const_cast<float *>(grad); a.eps = eps; a.kin = kin;
-  if (mode == KICK_HALF_DRIFT) k_kick<KICK_HALF_DRIFT><<<C, MT_THREADS, 0, s>>>(a);
+  if (p->sample_r) {
+    if (mode == KICK_HALF_DRIFT) k_kick_r<KICK_HALF_DRIFT><<<C, MT_THREADS, 0, s>>>(a);
+    else if (mode == KICK_FULL_DRIFT) k_kick_r<KICK_FULL_DRIFT><<<C, MT_THREADS, 0, s>>>(a);
+    else k_kick_r<KICK_HALF_LAST><<<C, MT_THREADS, 0, s>>>(a);
+  } else if (mode == KICK_HALF_DRIFT) k_kick<KICK_HALF_DRIFT><<<C, MT_THREADS, 0, s>>>(a);
   else if (mode == KICK_FULL_DRIFT) k_kick<KICK_FULL_DRIFT><<<C, MT_THREADS, 0, s>>>(a);
   else k_kick<KICK_HALF_LAST><<<C, MT_THREADS, 0, s>>>(a);
   p->all_launches++;

@@ -95,6 +95,8 @@ struct FinishArgs {
   float *Hlo;                   // their fp32 residuals (H + Hlo = fp64 heights)
   float4 *band;                 // [C]
   float *kin;                   // [C] 1/2 |p|^2 after the last half kick
+  int sample_r;                 // f2: state (x_0, x_1, ρ_0, ρ_1), r_l = logistic(ρ_l)
+  const double *cs;             // [N] c_ab = 2(cos 2πa/n_x + cos 2πb/n_y) (torus spectrum)
 };
 
 enum { FIN_PLAIN = 0, FIN_STEP = 1, FIN_LAST = 2 };
@@ -110,6 +112,8 @@ struct mt_problem {
   double sigma[2] = {0, 0}, logdetQ[2] = {0, 0};
   double loglik_offset = 0;
   int prior_on = 1;
+  int sample_r = 0;             // f2: the CAR r_l are sampled (two more parameters per chain)
+  double *d_cs = nullptr;       // [N] torus spectrum table (sample_r)
   TraceConsts tc{};
   float *d_X = nullptr, *d_Y = nullptr;
   float4 *d_ray_a = nullptr, *d_ray_b = nullptr;
