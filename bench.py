@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--impl", default="mt", choices=["mt", "reference"])
     ap.add_argument("--workload", default="chain_sharded", choices=["chain_sharded", "ray_sharded"],
                     help="configs[3] (default, the headline) or configs[4] (one chain, rays over the GPUs)")
+    ap.add_argument("--sample-r", action="store_true",
+                    help="hierarchical CAR r_l (SURVEY §8(f) f2): two more parameters per chain")
     ap.add_argument("--chains-total", type=int, default=8192)     # configs[3]
     ap.add_argument("--weak", action="store_true", help="fixed --chains-per-gpu per rank instead")
     ap.add_argument("--chains-per-gpu", type=int, default=1024)
@@ -212,7 +214,10 @@ def main():
             C = args.chains_total // ws
         offset = rank * C
         x0 = inputs.chain_states(prob["x_true"], C, cfg.seed, chain_offset=offset, super_size=8)
-        pb = Problem(prob, device=local, max_chains=C)
+        if args.sample_r:   # ρ_l = logit(r_l) started at the fixed-r value
+            rho = np.log(np.asarray(cfg.car_r) / (1.0 - np.asarray(cfg.car_r)))
+            x0 = np.concatenate([x0, np.broadcast_to(rho, (C, 2))], axis=1).astype(np.float32)
+        pb = Problem(prob, device=local, max_chains=C, sample_r=args.sample_r)
         R_total = pb.R * ws   # (chain sharding: every rank traces all rays of its chains)
         shard = ChainShard(pb, x0, seed=inputs.philox_key(cfg), L=L, eps0=eps, chain_offset=offset,
                            n_chains_total=C * ws)
@@ -318,6 +323,7 @@ def main():
                        "chains_per_gpu": C, "global_chains": C if ray else C * ws, "rays": R_total if ray else R,
                        "rays_per_gpu": R, "params": P,
                        "leapfrog_steps": L, "parallelism": (f"ray-sharded x{ws}" if ray else f"chain-sharded x{ws}"),
+                       "car_r": "sampled (f2)" if args.sample_r else "fixed",
                        "phase": "sampling (fixed eps from the 100-iteration dual-averaging warm-up, "
                                 "tools/tune_eps.py; Welford + all-reduced acceptance sums each step)",
                        "eps": eps,
