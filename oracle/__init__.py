@@ -283,3 +283,109 @@ def hmc_step(x, eps, L, logp_grad, seed, it, chain_offset=0):
     x_new = np.where(accepted[:, None], x1, x)
     lp_new = np.where(accepted, lp1, lp0)
     return x_new, acc_prob, accepted, lp_new, dH
+
+
+# ---------------------------------------------------------------------------
+# No-U-Turn Sampler (NUTS of Hoffman & Gelman as run by NumPyro,
+# trajectory capped at 2^max_depth leapfrog steps).  Plain Python,
+# one chain at a time, in the order of the algorithm (reading R26 in DESIGN.md):
+#   momenta p ~ N(0, I); the trajectory doubles max_depth times at most; at
+#   depth j a direction v_j = ±1 is drawn and a subtree of 2^j leapfrog steps
+#   is integrated from the tree's edge on that side with step v_j·ε;
+#   within the subtree a leaf replaces the subtree proposal with probability
+#   w_leaf / W_subtree (progressive multinomial sampling, w = e^{-ΔH});
+#   the subtree is rejected (and the tree stops) on a divergence (ΔH > 1000
+#   or non-finite) or a U-turn of any aligned sub-subtree (iterative checks
+#   against checkpoints); a valid subtree's proposal replaces the tree's with
+#   probability min(1, W_subtree / W_tree) (biased progressive sampling), then
+#   the whole tree is checked for a U-turn between its two edge momenta;
+#   U-turn(p⁻, p⁺, ρ): p⁻·(ρ - (p⁻+p⁺)/2) <= 0 or p⁺·(ρ - (p⁻+p⁺)/2) <= 0,
+#   ρ = Σ momenta of the (sub)tree, identity mass.
+# Random numbers: Philox4x32-10 word 0, counter (q, chain, iter, stream):
+#   stream 2: direction at depth q (u >= 1/2 -> +1); stream 3: leaf q of the
+#   iteration (within-subtree choice); stream 4: merge at depth q.
+# ---------------------------------------------------------------------------
+
+def philox_uniform(seed: int, it: int, chain: int, stream: int, q: int) -> float:
+    w = philox4x32_10([q & 0xffffffff, chain & 0xffffffff, it & 0xffffffff, stream],
+                      [seed & 0xffffffff, (seed >> 32) & 0xffffffff])
+    return (float(w[0]) + 0.5) * 2.0 ** -32
+
+
+def leaf_ckpt_idxs(n: int):
+    """Checkpoint range for leaf n of a subtree: idx_max = popcount(n >> 1),
+    idx_min = idx_max - (trailing ones of n) + 1."""
+    idx_max = bin(n >> 1).count("1")
+    t = 0
+    while (n >> t) & 1:
+        t += 1
+    return idx_max - t + 1, idx_max
+
+
+def is_turning(p_left, p_right, rho):
+    rs = rho - 0.5 * (p_left + p_right)
+    return float(np.dot(p_left, rs)) <= 0.0 or float(np.dot(p_right, rs)) <= 0.0
+
+
+def nuts_step(x, lp, g, eps, logp_grad1, seed, it, chain, max_depth=8):
+    """One NUTS transition of one chain.  logp_grad1(x [P]) -> (logp, grad [P]).
+    Returns dict(x, logp, grad, depth, n_leaves, accept_stat, diverging)."""
+    x = np.array(x, np.float64)
+    P = x.size
+    p = momenta(P, seed, it, chain)
+    H0 = -lp + 0.5 * float(p @ p)
+    left = right = (x, p, g, lp)                 # (θ, p, ∇, logp) of the two edges
+    prop = (x, lp, g)
+    logW = 0.0                                   # log Σ e^{-ΔH} over the tree (initial leaf: ΔH = 0)
+    rho = p.copy()
+    n_leaf, acc_sum, diverging, depth = 0, 0.0, False, 0
+    for j in range(max_depth):
+        v = 1 if philox_uniform(seed, it, chain, 2, j) >= 0.5 else -1
+        th, pp, gg, ll = right if v > 0 else left
+        logWs, rhos, props = -math.inf, np.zeros(P), None
+        r_ck = [None] * (max_depth + 1)
+        rs_ck = [None] * (max_depth + 1)
+        ok = True
+        for n in range(2 ** j):
+            e = v * eps
+            pp = pp + 0.5 * e * gg
+            th = th + e * pp
+            ll, gg = logp_grad1(th)
+            pp = pp + 0.5 * e * gg
+            dH = (-ll + 0.5 * float(pp @ pp)) - H0
+            acc_sum += min(1.0, math.exp(-dH)) if math.isfinite(dH) else 0.0
+            n_leaf += 1
+            if not math.isfinite(dH) or dH > 1000.0:
+                ok, diverging = False, True
+                break
+            logWs_new = np.logaddexp(logWs, -dH)
+            u = philox_uniform(seed, it, chain, 3, n_leaf - 1)
+            if math.log(u) < -dH - logWs_new:
+                props = (th, ll, gg)
+            logWs = logWs_new
+            rhos = rhos + pp
+            lo, hi = leaf_ckpt_idxs(n)
+            if n % 2 == 0:
+                r_ck[hi], rs_ck[hi] = pp, rhos.copy()
+            else:
+                for i in range(hi, lo - 1, -1):
+                    if is_turning(r_ck[i], pp, rhos - rs_ck[i] + r_ck[i]):
+                        ok = False
+                        break
+                if not ok:
+                    break
+        depth = j + 1
+        if not ok:
+            break
+        if math.log(philox_uniform(seed, it, chain, 4, j)) < logWs - logW:
+            prop = props
+        logW = np.logaddexp(logW, logWs)
+        if v > 0:
+            right = (th, pp, gg, ll)
+        else:
+            left = (th, pp, gg, ll)
+        rho = rho + rhos
+        if is_turning(left[1], right[1], rho):
+            break
+    return dict(x=prop[0], logp=prop[1], grad=prop[2], depth=depth, n_leaves=n_leaf,
+                accept_stat=acc_sum / max(n_leaf, 1), diverging=diverging)
