@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--impl", default="mt", choices=["mt", "reference"])
     ap.add_argument("--workload", default="chain_sharded", choices=["chain_sharded", "ray_sharded"],
                     help="configs[3] (default, the headline) or configs[4] (one chain, rays over the GPUs)")
+    ap.add_argument("--sampler", default="hmc", choices=["hmc", "nuts"],
+                    help="fixed-L HMC (configs[3], default) or NUTS (SURVEY §8(f) f1; --max-depth)")
+    ap.add_argument("--max-depth", type=int, default=8, help="NUTS: 2^max_depth leaves cap (P:662-669)")
     ap.add_argument("--sample-r", action="store_true",
                     help="hierarchical CAR r_l (SURVEY §8(f) f2): two more parameters per chain")
     ap.add_argument("--chains-total", type=int, default=8192)     # configs[3]
@@ -220,7 +223,7 @@ def main():
         pb = Problem(prob, device=local, max_chains=C, sample_r=args.sample_r)
         R_total = pb.R * ws   # (chain sharding: every rank traces all rays of its chains)
         shard = ChainShard(pb, x0, seed=inputs.philox_key(cfg), L=L, eps0=eps, chain_offset=offset,
-                           n_chains_total=C * ws)
+                           n_chains_total=C * ws, sampler=args.sampler, max_depth=args.max_depth)
     R, P = pb.R, pb.P
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MiB > 126 MB L2
 
@@ -235,7 +238,7 @@ def main():
     barrier()
     clocks = ClockSampler() if rank == 0 else None
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    pb.timing_start(args.steps * L + 8)
+    pb.timing_start(args.steps * (L if args.sampler == "hmc" else 2 ** args.max_depth) + 8)
     d0 = pb.trace_counters()["deferred"]
     wall0 = time.perf_counter()
     for k in range(args.steps):
@@ -253,7 +256,10 @@ def main():
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_ms = float(t.item())
-    units = (R_total * C if ray else ws * C * R) * L * args.steps
+    # evaluations of all chains x all rays (the trace launches: L per HMC step; one per
+    # lockstep NUTS leaf, idle chains included)
+    evals = tm["trace_launches"]
+    units = (R_total * C if ray else ws * C * R) * evals
     value = units / (t_ms * 1e-3)
 
     # dominant kernel (K2 trace): algorithmic FP32 flops per launch / measured launch duration
@@ -282,26 +288,36 @@ def main():
 
     e2e = None
     if not args.no_e2e:
-        # same metric through the public API with host buffers: per step, pinned H2D of the
-        # chain states and D2H of (logp, accept_prob).
-        xh = torch.from_numpy(x0).pin_memory()
-        lph = torch.empty(C, dtype=torch.float64).pin_memory()
+        # the same metric through the public API with the chain state held in pinned host
+        # memory: every step copies (x, logp, grad) host -> device, runs the step, and
+        # copies (x, logp, grad, acceptance) device -> host
+        xh = shard.x.cpu().pin_memory()
+        gh = shard.grad.cpu().pin_memory()
+        lph = shard.logp.cpu().pin_memory()
         aph = torch.empty(C, dtype=torch.float32).pin_memory()
         barrier()
+        pb.timing_start(args.steps * (L if args.sampler == "hmc" else 2 ** args.max_depth) + 8)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for k in range(args.steps):
             shard.x.copy_(xh, non_blocking=True)
+            shard.grad.copy_(gh, non_blocking=True)
+            shard.logp.copy_(lph, non_blocking=True)
             shard.step(adapt=False, sample=True, monitor=True)
+            xh.copy_(shard.x, non_blocking=True)
+            gh.copy_(shard.grad, non_blocking=True)
             lph.copy_(shard.logp, non_blocking=True)
             aph.copy_(shard.acc_prob, non_blocking=True)
         e1.record()
         barrier()
+        evals_e2e = pb.timing_read()["trace_launches"]
         te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
         if dist is not None:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": units / (float(te.item()) * 1e-3), "unit": UNIT,
-               "h2d_bytes_per_step": C * P * 4, "d2h_bytes_per_step": C * (8 + 4)}
+        units_e2e = (R_total * C if ray else ws * C * R) * evals_e2e
+        state_bytes = C * (2 * P * 4 + 8)
+        e2e = {"value": units_e2e / (float(te.item()) * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": state_bytes, "d2h_bytes_per_step": state_bytes + C * 4}
 
     if rank != 0:
         if dist is not None:
@@ -330,7 +346,8 @@ def main():
                        "l2": "flushed between timed steps (256 MiB write, outside the events)"},
             "roofline": roofline, "cpu_baseline": base, "e2e": e2e, "clocks": ck,
             "gpu_launches": tm["all_launches"],
-            "leapfrog_steps_per_s_per_chain": L * args.steps / (t_ms * 1e-3),
+            "leapfrog_steps_per_s_per_chain": evals / (t_ms * 1e-3),
+            "sampler": args.sampler if args.sampler == "hmc" else f"nuts (max_depth {args.max_depth})",
             "wall_s_timed_region": wall}
     print(json.dumps(line), flush=True)
     if dist is not None:

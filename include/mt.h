@@ -166,6 +166,28 @@ int mt_comm_unique_id(void *uid128);
 int mt_attach_comm(mt_problem *p, const void *uid128, int32_t rank, int32_t world);
 int mt_detach_comm(mt_problem *p);
 
+/* One No-U-Turn transition per chain (trajectory
+ * capped at 2^max_depth leapfrog steps; reading R26 in DESIGN.md):
+ * momenta as mt_draw_momenta; the trajectory doubles up to max_depth times in
+ * Philox-drawn directions (counter (depth, chain, iter, 2)); leaves are chosen
+ * by progressive multinomial sampling (counters (leaf, chain, iter, 3) and
+ * (depth, chain, iter, 4)); subtrees stop on a U-turn of any aligned
+ * sub-trajectory or a divergence (ΔH > 1000 / non-finite).  All chains advance
+ * in lockstep, one leaf (one log-posterior+gradient evaluation of all C
+ * chains) per step; finished chains idle.
+ *   x, logp, grad (in/out): on entry the current state with its logp/grad, on
+ *     return the selected state with its logp/grad;
+ *   accept_stat [C] float: mean min(1, e^{-ΔH}) over the leaves (step-size
+ *     adaptation); depth, n_leaves [C] int32 or NULL; status [C] or NULL
+ *     (bit 2 = divergent trajectory).
+ * 1 <= max_depth <= 10.  Synchronous (the doubling loop reads one flag per
+ * depth), not graph-capturable; the first call allocates the tree workspace
+ * ((16 + 20) x max_chains x P floats).  With a ray-shard communicator every
+ * leaf is all-reduced like mt_leapfrog. */
+int mt_nuts_step(mt_problem *p, int32_t C, float *x, double *logp, float *grad, const float *eps,
+                 int32_t max_depth, uint64_t seed, uint64_t iter, uint64_t chain_offset, float *accept_stat,
+                 int32_t *depth, int32_t *n_leaves, int32_t *status, mt_stream stream);
+
 /* Per-iteration sampler statistics (step-size adaptation and R-hat, P:652-653,
  * P:671-687; readings R20/R21).  Any of the three groups may be skipped by
  * passing NULL:

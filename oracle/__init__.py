@@ -327,9 +327,11 @@ def is_turning(p_left, p_right, rho):
     return float(np.dot(p_left, rs)) <= 0.0 or float(np.dot(p_right, rs)) <= 0.0
 
 
-def nuts_step(x, lp, g, eps, logp_grad1, seed, it, chain, max_depth=8):
+def nuts_step(x, lp, g, eps, logp_grad1, seed, it, chain, max_depth=8, trace=None):
     """One NUTS transition of one chain.  logp_grad1(x [P]) -> (logp, grad [P]).
-    Returns dict(x, logp, grad, depth, n_leaves, accept_stat, diverging)."""
+    Returns dict(x, logp, grad, depth, n_leaves, accept_stat, diverging).
+    trace (a list, optional) receives (kind, margin, x) for every random choice:
+    the distance of log u from its threshold (debugging threshold flips)."""
     x = np.array(x, np.float64)
     P = x.size
     p = momenta(P, seed, it, chain)
@@ -360,6 +362,8 @@ def nuts_step(x, lp, g, eps, logp_grad1, seed, it, chain, max_depth=8):
                 break
             logWs_new = np.logaddexp(logWs, -dH)
             u = philox_uniform(seed, it, chain, 3, n_leaf - 1)
+            if trace is not None:
+                trace.append(("leaf", math.log(u) - (-dH - logWs_new), th))
             if math.log(u) < -dH - logWs_new:
                 props = (th, ll, gg)
             logWs = logWs_new
@@ -377,6 +381,8 @@ def nuts_step(x, lp, g, eps, logp_grad1, seed, it, chain, max_depth=8):
         depth = j + 1
         if not ok:
             break
+        if trace is not None:
+            trace.append(("merge", math.log(philox_uniform(seed, it, chain, 4, j)) - (logWs - logW), props[0]))
         if math.log(philox_uniform(seed, it, chain, 4, j)) < logWs - logW:
             prop = props
         logW = np.logaddexp(logW, logWs)

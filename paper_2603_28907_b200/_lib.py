@@ -43,7 +43,7 @@ EXPORTS = [
     "mt_prior_constants", "mt_logpost_grad", "mt_leapfrog", "mt_draw_momenta", "mt_hmc_step",
     "mt_stats_update", "mt_rhat_partials", "mt_heights", "mt_loglik_heights", "mt_path_lengths", "mt_debug_traversal", "mt_philox",
     "mt_philox_curand", "mt_timing_start", "mt_timing_read", "mt_trace_counters", "mt_measure_fp32_peak",
-    "mt_last_error", "mt_comm_unique_id", "mt_attach_comm", "mt_detach_comm",
+    "mt_last_error", "mt_comm_unique_id", "mt_attach_comm", "mt_detach_comm", "mt_nuts_step",
 ]
 
 _lib = None
@@ -79,6 +79,7 @@ def lib():
             "mt_timing_read": ([vp, vp, vp, vp, vp], ct.c_int),
             "mt_trace_counters": ([vp, vp, vp], ct.c_int),
             "mt_comm_unique_id": ([vp], ct.c_int),
+            "mt_nuts_step": ([vp, i32, vp, vp, vp, vp, i32, u64, u64, u64, vp, vp, vp, vp, vp], ct.c_int),
             "mt_attach_comm": ([vp, vp, i32, i32], ct.c_int),
             "mt_detach_comm": ([vp], ct.c_int),
             "mt_measure_fp32_peak": ([i32, vp, vp], ct.c_int),
@@ -231,6 +232,26 @@ class Problem:
                                  chain_offset, _ptr(accept_prob), _ptr(accepted), _ptr(status),
                                  _stream(stream)), "mt_hmc_step")
         return accept_prob, accepted
+
+    def nuts_step(self, x, logp, grad, eps, max_depth: int, seed: int, it: int, chain_offset: int = 0,
+                  accept_stat=None, depth=None, n_leaves=None, status=None, stream=None):
+        """One NUTS transition per chain (mt_nuts_step); returns (accept_stat, depth, n_leaves)."""
+        import torch
+        C = x.shape[0]
+        dev = x.device
+        if accept_stat is None:
+            accept_stat = torch.empty(C, dtype=torch.float32, device=dev)
+        if depth is None:
+            depth = torch.empty(C, dtype=torch.int32, device=dev)
+        if n_leaves is None:
+            n_leaves = torch.empty(C, dtype=torch.int32, device=dev)
+        for t, n, dt, sh in ((x, "x", torch.float32, (C, self.P)), (logp, "logp", torch.float64, (C,)),
+                             (grad, "grad", torch.float32, (C, self.P)), (eps, "eps", torch.float32, (C,))):
+            _dev_tensor(t, dt, sh, self.device, n)
+        _check(lib().mt_nuts_step(self.h, C, _ptr(x), _ptr(logp), _ptr(grad), _ptr(eps), max_depth, seed, it,
+                                  chain_offset, _ptr(accept_stat), _ptr(depth), _ptr(n_leaves), _ptr(status),
+                                  _stream(stream)), "mt_nuts_step")
+        return accept_stat, depth, n_leaves
 
     def stats_update(self, C: int, x=None, accept_prob=None, n_prev: int = 0, mean=None, m2=None,
                      acc_fixed=None, stream=None):

@@ -83,6 +83,10 @@ void free_all(mt_problem *p) {
                   p->d_band, p->d_ll, p->d_x0, p->d_g0, p->d_mom, p->d_kin0, p->d_kin1, p->d_lp0};
   for (void *b : bufs)
     if (b) cudaFree(b);
+  void *nb[] = {p->nuts_ws, p->nuts_lp, p->nuts_st, p->nuts_flags};
+  for (void *b : nb)
+    if (b) cudaFree(b);
+  if (p->nuts_hflags) cudaFreeHost(p->nuts_hflags);
   for (auto e : p->ev_a) cudaEventDestroy(e);
   for (auto e : p->ev_b) cudaEventDestroy(e);
   for (auto e : p->ev_m) cudaEventDestroy(e);
@@ -406,6 +410,26 @@ int mt_hmc_step(mt_problem *p, int32_t C, float *x, double *logp, float *grad, c
                      p->d_kin1, s));
   }
   CK(launch_hmc_end(p, C, x, logp, grad, seed, iter, chain_offset, accept_prob, accepted, status, s));
+  return MT_OK;
+}
+
+int mt_nuts_step(mt_problem *p, int32_t C, float *x, double *logp, float *grad, const float *eps,
+                 int32_t max_depth, uint64_t seed, uint64_t iter, uint64_t chain_offset, float *accept_stat,
+                 int32_t *depth, int32_t *n_leaves, int32_t *status, mt_stream stream) {
+  if (int r = check_chains(p, C)) return r;
+  if (max_depth < 1 || max_depth > MT_NUTS_MAX_DEPTH)
+    return set_err(MT_EINVAL, "max_depth = %d not in [1, %d]", max_depth, MT_NUTS_MAX_DEPTH);
+  if (C == 0) return MT_OK;
+  if (check_ptr(x, "x") || check_ptr(logp, "logp") || check_ptr(grad, "grad") || check_ptr(eps, "eps") ||
+      check_ptr(accept_stat, "accept_stat"))
+    return MT_EINVAL;
+  DevGuard g(p->device);
+  std::string why;
+  cudaError_t e = run_nuts(p, C, x, logp, grad, eps, max_depth, seed, iter, chain_offset, accept_stat, depth,
+                           n_leaves, status, (cudaStream_t)stream, why);
+  if (!why.empty()) return set_err(MT_ENCCL, "ncclAllReduce: %s", why.c_str());
+  if (e == cudaErrorMemoryAllocation) return set_err(MT_ENOMEM, "NUTS workspace: %s", cudaGetErrorString(e));
+  CK(e);
   return MT_OK;
 }
 

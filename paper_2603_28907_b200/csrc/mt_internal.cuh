@@ -101,6 +101,23 @@ struct FinishArgs {
 
 enum { FIN_PLAIN = 0, FIN_STEP = 1, FIN_LAST = 2 };
 
+// batched NUTS (kernels.cu, f1): per-chain tree state and workspace views
+#define MT_NUTS_MAX_DEPTH 10
+struct NutsChain {
+  double H0, logW, logWs, lpL, lpR, lpw, lps, acc_sum;
+  int dir, active, sub_ok, depth, n_leaf, diverging;
+};
+struct NutsArgs {
+  float *thL, *pL, *gL, *thR, *pR, *gR;   // tree edges
+  float *thw, *pw, *gw;                   // working state (the leaf being built)
+  float *ths, *gs;                        // subtree proposal
+  float *rho, *rhos, *tmp;                // momentum sums of the tree / subtree
+  float *rck, *rsck;                      // U-turn checkpoints [depth][C][P]
+  double *lpw_out;                        // logp of the working state (K3 output)
+  NutsChain *st;
+  int *any_active, *any_sub;
+};
+
 struct mt_problem {
   int device = 0;
   int num_sms = 148;
@@ -142,6 +159,11 @@ struct mt_problem {
   int trace_s = 0;              // ray splits (0 = auto)
   int chunk = 512;              // chain lanes: rays per block (a Morton-ordered chunk)
   int smemh_limit = 100 * 1024; // stage a 32-chain height tile in smem when it fits
+  // batched NUTS workspace (allocated by the first mt_nuts_step)
+  float *nuts_ws = nullptr;
+  double *nuts_lp = nullptr;
+  NutsChain *nuts_st = nullptr;
+  int *nuts_flags = nullptr, *nuts_hflags = nullptr;
   // in-library NCCL communicator (ray sharding; comm.cu)
   void *comm = nullptr;
   int comm_rank = 0, comm_world = 1;
@@ -176,6 +198,9 @@ cudaError_t build_traversal(mt_problem *p);
 cudaError_t launch_kick(mt_problem *p, int mode, int C, float *x, float *mom, const float *grad,
                         const float *eps, float *kin, cudaStream_t s);
 enum { KICK_HALF_DRIFT = 0, KICK_FULL_DRIFT = 1, KICK_HALF_LAST = 2 };
+cudaError_t run_nuts(mt_problem *p, int C, float *x, double *logp, float *grad, const float *eps, int max_depth,
+                     uint64_t seed, uint64_t iter, uint64_t chain_offset, float *accept_stat, int32_t *depth,
+                     int32_t *n_leaves, int32_t *status, cudaStream_t s, std::string &why);
 // comm.cu
 bool comm_unique_id(void *uid, std::string &why);
 bool comm_attach(mt_problem *p, const void *uid, int rank, int world, std::string &why);

@@ -102,7 +102,7 @@ class ChainShard:
 
     def __init__(self, problem, x0: np.ndarray, seed: int, L: int, eps0: float,
                  chain_offset: int = 0, n_chains_total: Optional[int] = None, group=None,
-                 stream=None, replicated: bool = False):
+                 stream=None, replicated: bool = False, sampler: str = "hmc", max_depth: int = 8):
         import torch
         self.torch = torch
         self.pb = problem
@@ -114,6 +114,9 @@ class ChainShard:
         self.group = group
         self.stream = stream
         self.replicated = replicated
+        if sampler not in ("hmc", "nuts"):
+            raise ValueError(f"sampler {sampler!r}")
+        self.sampler, self.max_depth = sampler, max_depth   # NUTS: 2^max_depth leaves cap
         t = lambda *s, dt=torch.float32: torch.zeros(s, dtype=dt, device=self.dev)  # noqa: E731
         self.x = torch.from_numpy(np.ascontiguousarray(x0, np.float32)).to(self.dev)
         self.logp = t(self.C, dt=torch.float64)
@@ -121,6 +124,7 @@ class ChainShard:
         self.eps = torch.full((self.C,), eps0, dtype=torch.float32, device=self.dev)
         self.acc_prob = t(self.C)
         self.accepted = t(self.C, dt=torch.int32)
+        self.depth = t(self.C, dt=torch.int32)
         self.status = t(self.C, dt=torch.int32)
         self.acc_fixed = t(2, dt=torch.int64)
         self.mean = t(self.C, self.P)
@@ -150,8 +154,13 @@ class ChainShard:
         """One HMC iteration (a1-a9).  Returns the global mean acceptance probability
         when adapting or monitoring (it needs the all-rank sum on the host)."""
         pb = self.pb
-        pb.hmc_step(self.x, self.logp, self.grad, self.eps, self.L, self.seed, self.it,
-                    self.chain_offset, self.acc_prob, self.accepted, self.status, stream=self.stream)
+        if self.sampler == "nuts":   # acc_prob <- the NUTS acceptance statistic
+            pb.nuts_step(self.x, self.logp, self.grad, self.eps, self.max_depth, self.seed, self.it,
+                         self.chain_offset, self.acc_prob, self.depth, self.accepted, self.status,
+                         stream=self.stream)
+        else:
+            pb.hmc_step(self.x, self.logp, self.grad, self.eps, self.L, self.seed, self.it,
+                        self.chain_offset, self.acc_prob, self.accepted, self.status, stream=self.stream)
         alpha = float("nan")
         if adapt or monitor:
             self.acc_fixed.zero_()

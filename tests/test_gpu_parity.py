@@ -520,3 +520,59 @@ def test_sampled_r_hmc_step_with_and_without_communicator(gpu, oracle_problem, p
     assert np.all((a1 >= 0) & (a1 <= 1)) and np.allclose(a1, a2, atol=1e-3)
     ref = op.logpost_grad_r(x1)
     assert np.allclose(lp1, ref["logp"], rtol=1e-4)
+
+
+# ---------------------------------------------------------------------------
+# batched NUTS against the oracle's one-chain NUTS
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name,C,max_depth", [("tiny", 4, 5), ("small", 16, 4)])
+def test_nuts_step_matches_oracle(gpu, oracle_problem, name, C, max_depth):
+    """Kernel NUTS vs the oracle's NUTS from the same state with the same Philox
+    streams.  Long trajectories amplify the fp32/fp64 evaluation differences
+    exponentially (tools/nuts_debug.py: |Δθ| grows 1e-6 -> 1e-3 over ~20 leaves at
+    2x the tuned ε and then flips a multinomial choice), so trees are kept to
+    2^max_depth <= 32 leaves at the tuned ε; chains whose tree decisions agree must
+    land on the same state."""
+    mp, op = gpu(name), oracle_problem(name)
+    cfg = inputs.CONFIGS[name]
+    x0 = inputs.chain_states(op.prob["x_true"], C, cfg.seed)
+    seed, it = inputs.philox_key(cfg), 11
+    e = sampling_eps(name)
+    x = torch.from_numpy(x0).to(DEV)
+    logp, grad = mp.logpost_grad(x)
+    eps = torch.full((C,), e, dtype=torch.float32, device=DEV)
+    acc, depth, nl = mp.nuts_step(x, logp, grad, eps, max_depth, seed, it)
+    torch.cuda.synchronize()
+    xd, depth, nl, acc = x.cpu().numpy().astype(np.float64), depth.cpu().numpy(), nl.cpu().numpy(), acc.cpu().numpy()
+    lg1 = lambda th: (lambda o: (o["logp"][0], o["grad"][0]))(op.logpost_grad(th[None]))  # noqa: E731
+    agree = 0
+    for c in range(C):
+        lp0, g0 = lg1(x0[c].astype(np.float64))
+        ref = oracle.nuts_step(x0[c], lp0, g0, e, lg1, seed, it, c, max_depth=max_depth)
+        if ref["depth"] == depth[c] and ref["n_leaves"] == nl[c]:
+            agree += 1
+            assert rel_l2(xd[c], ref["x"]) <= 1e-3, (c, rel_l2(xd[c], ref["x"]))
+            assert acc[c] == pytest.approx(ref["accept_stat"], abs=2e-3)
+    # the tree decisions compare fp32 against fp64 quantities: allow the rare
+    # chain whose U-turn or selection sits on a threshold to differ
+    assert agree >= max(C - 1, int(0.75 * C)), (agree, C)
+    ref_lp = op.logpost_grad(xd)
+    assert np.allclose(logp.cpu().numpy(), ref_lp["logp"], rtol=1e-4)   # returned logp is that of x
+
+
+def test_nuts_driver_runs_and_adapts(gpu, problems):
+    """ChainShard(sampler="nuts") on Small: dual averaging on the NUTS acceptance
+    statistic reaches the 0.8 target neighbourhood, trees stay under the cap,
+    chains stay finite."""
+    from paper_2603_28907_b200.hmc import ChainShard
+    prob = problems("small")
+    cfg = inputs.CONFIGS["small"]
+    mp = gpu("small", max_chains=64)
+    x0 = inputs.chain_states(prob["x_true"], 64, cfg.seed, super_size=8)
+    sh = ChainShard(mp, x0, seed=inputs.philox_key(cfg), L=10, eps0=sampling_eps("small"), sampler="nuts",
+                    max_depth=5)
+    out = sh.run(30, 5)
+    assert 0.5 < np.mean(out["warmup_accept"][-10:]) < 0.98
+    d = sh.depth.cpu().numpy()
+    assert d.min() >= 1 and d.max() <= 5
+    assert torch.isfinite(sh.x).all() and torch.isfinite(sh.logp).all()
