@@ -205,6 +205,17 @@ int mt_stats_update(mt_problem *p, int32_t C, const float *x, const float *accep
 int mt_rhat_partials(mt_problem *p, int32_t C, const float *mean, const float *m2, int32_t n,
                      double *out, mt_stream stream);
 
+/* Nested R̂ partial sums (n_super super-chains of M chains that share
+ * their start, Margossian et al.; reading R21b): chains [kM, (k+1)M) of this
+ * rank form super-chain k (C % M == 0; super-chains never straddle ranks).
+ * After n >= 1 Welford updates (n = 1: the paper's keep-last protocol), out
+ * [3][P] (device double) = (Σ_k m_k, Σ_k m_k², Σ_k W_k) with m_k the
+ * super-chain mean and W_k its pooled variance (mean within-chain variance +
+ * variance of its chain means).  A SUM over ranks gives B = var_k m_k
+ * (unbiased), W = mean_k W_k and nested R̂ = sqrt(1 + B/W) per parameter. */
+int mt_nested_rhat_partials(mt_problem *p, int32_t C, int32_t M, const float *mean, const float *m2, int32_t n,
+                            double *out, mt_stream stream);
+
 /* ---- parity / debug entry points (not on the hot path) ---------------- */
 
 /* Heights map of x (device [C][P] -> device H [C][2][n_x][n_y]). */

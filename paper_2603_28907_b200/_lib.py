@@ -44,6 +44,7 @@ EXPORTS = [
     "mt_stats_update", "mt_rhat_partials", "mt_heights", "mt_loglik_heights", "mt_path_lengths", "mt_debug_traversal", "mt_philox",
     "mt_philox_curand", "mt_timing_start", "mt_timing_read", "mt_trace_counters", "mt_measure_fp32_peak",
     "mt_last_error", "mt_comm_unique_id", "mt_attach_comm", "mt_detach_comm", "mt_nuts_step",
+    "mt_nested_rhat_partials",
 ]
 
 _lib = None
@@ -69,6 +70,7 @@ def lib():
             "mt_hmc_step": ([vp, i32, vp, vp, vp, vp, i32, u64, u64, u64, vp, vp, vp, vp], ct.c_int),
             "mt_stats_update": ([vp, i32, vp, vp, i32, vp, vp, vp, vp], ct.c_int),
             "mt_rhat_partials": ([vp, i32, vp, vp, i32, vp, vp], ct.c_int),
+            "mt_nested_rhat_partials": ([vp, i32, i32, vp, vp, i32, vp, vp], ct.c_int),
             "mt_heights": ([vp, i32, vp, vp, vp], ct.c_int),
             "mt_loglik_heights": ([vp, i32, vp, vp, vp, vp], ct.c_int),
             "mt_path_lengths": ([vp, i32, vp, vp, vp, vp], ct.c_int),
@@ -265,6 +267,14 @@ class Problem:
             out = torch.empty((3, self.P), dtype=torch.float64, device=mean.device)
         _check(lib().mt_rhat_partials(self.h, C, _ptr(mean), _ptr(m2), n, _ptr(out), _stream(stream)),
                "mt_rhat_partials")
+        return out
+
+    def nested_rhat_partials(self, C: int, M: int, mean, m2, n: int, out=None, stream=None):
+        import torch
+        if out is None:
+            out = torch.empty((3, self.P), dtype=torch.float64, device=mean.device)
+        _check(lib().mt_nested_rhat_partials(self.h, C, M, _ptr(mean), _ptr(m2), n, _ptr(out), _stream(stream)),
+               "mt_nested_rhat_partials")
         return out
 
     # -- parity / debug ------------------------------------------------------

@@ -480,6 +480,17 @@ int mt_rhat_partials(mt_problem *p, int32_t C, const float *mean, const float *m
   return MT_OK;
 }
 
+int mt_nested_rhat_partials(mt_problem *p, int32_t C, int32_t M, const float *mean, const float *m2, int32_t n,
+                            double *out, mt_stream stream) {
+  if (int r = check_chains(p, C)) return r;
+  if (check_ptr(mean, "mean") || check_ptr(m2, "m2") || check_ptr(out, "out")) return MT_EINVAL;
+  if (M < 1 || C % M) return set_err(MT_EINVAL, "C = %d not a multiple of the super-chain size M = %d", C, M);
+  if (n < 1) return set_err(MT_EINVAL, "n = %d < 1", n);
+  DevGuard g(p->device);
+  CK(launch_nested_rhat_partials(p, C, M, mean, m2, n, out, (cudaStream_t)stream));
+  return MT_OK;
+}
+
 int mt_heights(mt_problem *p, int32_t C, const float *x, float *H, mt_stream stream) {
   if (int r = check_chains(p, C)) return r;
   if (C == 0) return MT_OK;

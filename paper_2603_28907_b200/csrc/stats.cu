@@ -63,6 +63,52 @@ __global__ void k_rhat_partials(int C, int P, const float *mean, const float *m2
   out[2 * P + k] = sv;
 }
 
+// nested R̂ partial sums (Margossian et al.'s super-chains; reading
+// R21b): chains [kM, (k+1)M) form super-chain k (same start).  Per
+// parameter and super-chain: m_k = mean of its chain means; W_k = W̃_k + B̃_k,
+// the mean within-chain variance (m2/(n-1); 0 for one draw per chain, the
+// paper's keep-last protocol) plus the variance of its chain means (M-1 in the
+// denominator).  out [3][P] = (Σ_k m_k, Σ_k m_k², Σ_k W_k) over this rank's
+// super-chains; a SUM over ranks and the host give B = var_k m_k, W = mean_k W_k,
+// nested R̂ = sqrt(1 + B/W).
+__global__ void k_nested_rhat_partials(int C, int P, int M, const float *mean, const float *m2,
+                                       double inv_nm1, double *out) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= P) return;
+  double s1 = 0, s2 = 0, sw = 0;
+  for (int c0 = 0; c0 + M <= C; c0 += M) {
+    double mk = 0, wt = 0;
+    for (int c = c0; c < c0 + M; c++) {
+      mk += mean[(size_t)c * P + k];
+      wt += (double)m2[(size_t)c * P + k] * inv_nm1;
+    }
+    mk /= M;
+    wt /= M;
+    double bt = 0;
+    if (M > 1) {
+      for (int c = c0; c < c0 + M; c++) {
+        const double d = mean[(size_t)c * P + k] - mk;
+        bt += d * d;
+      }
+      bt /= (M - 1);
+    }
+    s1 += mk;
+    s2 += mk * mk;
+    sw += wt + bt;
+  }
+  out[k] = s1;
+  out[P + k] = s2;
+  out[2 * P + k] = sw;
+}
+
+cudaError_t launch_nested_rhat_partials(mt_problem *p, int C, int M, const float *mean, const float *m2,
+                                        int32_t n, double *out, cudaStream_t s) {
+  double inv = n > 1 ? 1.0 / (n - 1) : 0.0;
+  k_nested_rhat_partials<<<(p->P + 255) / 256, 256, 0, s>>>(C, p->P, M, mean, m2, inv, out);
+  p->all_launches++;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_stats(mt_problem *p, int C, const float *x, const float *acc, int32_t n_prev,
                          float *mean, float *m2, unsigned long long *acc_fixed, cudaStream_t s) {
   if (C <= 0) return cudaSuccess;

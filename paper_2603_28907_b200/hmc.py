@@ -93,6 +93,18 @@ def ray_sharded_problem(prob: dict, rank: int, world: int, device: int, max_chai
     return pb
 
 
+def nested_rhat_from_partials(part: np.ndarray, n_super: int) -> np.ndarray:
+    """Nested R̂ = sqrt(1 + B/W) per parameter from Σ m_k, Σ m_k², Σ W_k over all
+    super-chains (mt_nested_rhat_partials summed over ranks)."""
+    s1, s2, sw = part
+    mean = s1 / n_super
+    B = (s2 - n_super * mean ** 2) / (n_super - 1)
+    W = sw / n_super
+    with np.errstate(divide="ignore", invalid="ignore"):
+        r = np.sqrt(1.0 + B / W)
+    return np.where((W == 0) & (B <= 0), 1.0, r)
+
+
 class ChainShard:
     """Device state of this rank's chains and the HMC loop.
 
@@ -180,6 +192,13 @@ class ChainShard:
 
     def end_warmup(self):
         self.eps.fill_(self.da.final())
+
+    def nested_rhat(self, M: int = 8) -> np.ndarray:
+        """Nested R̂ over super-chains of M contiguous chains."""
+        part = self.pb.nested_rhat_partials(self.C, M, self.mean, self.m2, max(self.n_samples, 1),
+                                            stream=self.stream)
+        self._allreduce(part)
+        return nested_rhat_from_partials(part.cpu().numpy(), self.n_total // M)
 
     def rhat(self) -> np.ndarray:
         part = self.pb.rhat_partials(self.C, self.mean, self.m2, self.n_samples, stream=self.stream)

@@ -23,7 +23,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2603_28907_b200 import inputs
-from paper_2603_28907_b200.hmc import DualAveraging, ray_shards, rhat_from_partials
+from paper_2603_28907_b200.hmc import DualAveraging, nested_rhat_from_partials, ray_shards, rhat_from_partials
 
 WS = 2
 C_PER = 8
@@ -111,6 +111,12 @@ def worker(rank, port, out):
         t = torch.from_numpy(part)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         res["rhat"] = rhat_from_partials(t.numpy(), WS * C_PER, n)
+        # 3b. nested R-hat partials (super-chains of 8 never straddle ranks)
+        from test_nested_rhat import partials_numpy
+        part_n, Kr = partials_numpy(draws, 8)
+        t = torch.from_numpy(part_n)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        res["nested"] = nested_rhat_from_partials(t.numpy(), WS * C_PER // 8)
         # 4. ray sharding: partial [logp, grad] of this rank's ray shard, all-reduced
         res["ray"] = ray_shard_partial_sum(rank)
         out[rank] = res
@@ -172,3 +178,11 @@ def test_ray_sharded_partials_sum_to_unsharded(results):
     want = np.concatenate([ref["logp"], ref["grad"].ravel()])
     assert np.array_equal(results[0]["ray"], results[1]["ray"])      # identical on every rank
     assert np.allclose(results[0]["ray"], want, rtol=1e-10, atol=1e-8)
+
+
+def test_nested_rhat_from_allreduced_partials(results):
+    from test_nested_rhat import nested_rhat_direct
+    draws = make_draws(30, WS * C_PER)
+    want = nested_rhat_direct(draws, 8)
+    for r in range(WS):
+        assert np.allclose(results[r]["nested"], want, rtol=1e-10)
