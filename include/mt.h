@@ -216,6 +216,21 @@ int mt_rhat_partials(mt_problem *p, int32_t C, const float *mean, const float *m
 int mt_nested_rhat_partials(mt_problem *p, int32_t C, int32_t M, const float *mean, const float *m2, int32_t n,
                             double *out, mt_stream stream);
 
+/* Posterior summaries (reading R27), accumulated
+ * over draws (call once per kept draw set, e.g. each sampling iteration, or once
+ * with the last draws of the keep-last protocol):
+ *   acc (device double, zeroed by the caller), size 1 + 3N + 6 N nz:
+ *     [0] number of draws; [1, 1+2N) Σ heights (mean heights);
+ *     [1+2N, 1+3N) #draws with air thickness H1 - H0 > gap (m);
+ *     then Σ D and Σ D² of the smooth layer indicators D^(l) (l = muck, air,
+ *     rock, γ = 1 m) on voxel columns at the nodes, z_k = k z_top/nz,
+ *     laid out [sum|sum²][l][node][k] (indicator-std tomography).
+ *   map_x [P] / map_logp [1] (device, optional, map_logp initialised to -inf):
+ *     replaced by the highest-logp draw among x when higher (MAP).
+ * Uses (and overwrites) the problem's height workspace. */
+int mt_summary_update(mt_problem *p, int32_t C, const float *x, const double *logp, int32_t nz, float gap,
+                      double *acc, float *map_x, double *map_logp, mt_stream stream);
+
 /* ---- parity / debug entry points (not on the hot path) ---------------- */
 
 /* Heights map of x (device [C][P] -> device H [C][2][n_x][n_y]). */

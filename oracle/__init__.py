@@ -395,3 +395,37 @@ def nuts_step(x, lp, g, eps, logp_grad1, seed, it, chain, max_depth=8, trace=Non
             break
     return dict(x=prop[0], logp=prop[1], grad=prop[2], depth=depth, n_leaves=n_leaf,
                 accept_stat=acc_sum / max(n_leaf, 1), diverging=diverging)
+
+
+# ---------------------------------------------------------------------------
+# Posterior summaries (reading R27 in DESIGN.md): plain numpy over a
+# list of draw sets, each [C][P] with its log-posteriors [C].
+# ---------------------------------------------------------------------------
+def sigmoid(u, gamma=1.0):
+    """ς_γ(u) = 1/(1 + e^{-u/γ}) (P:349-352)."""
+    return 1.0 / (1.0 + np.exp(-np.asarray(u, np.float64) / gamma))
+
+
+def layer_indicators(H0, H1, z_top, nz):
+    """D^(l)_{ijk} = ς(H_l - kΔz) - ς(H_{l-1} - kΔz) for l = muck (H_{-1} = 0),
+    air, rock (H_2 = z_top), voxel columns at the nodes, Δz = z_top/nz -> [3][nx][ny][nz]."""
+    z = np.arange(nz) * (z_top / nz)
+    b = [np.zeros_like(H0), H0, H1, np.full_like(H0, z_top)]
+    s = [sigmoid(h[..., None] - z) for h in b]
+    return np.stack([s[1] - s[0], s[2] - s[1], s[3] - s[2]])
+
+
+def posterior_summaries(op, draws, logps, nz, gap):
+    """MAP draw, mean heights, air-thickness exceedance
+    probability, std across draws of the layer indicators."""
+    Hs, Ds, best = [], [], (-math.inf, None)
+    for xs, lps in zip(draws, logps):
+        for x, lp in zip(np.asarray(xs, np.float64), lps):
+            H = op.heights(x[:op.P])[0]
+            Hs.append(H)
+            Ds.append(layer_indicators(H[0], H[1], op.z_top, nz))
+            if lp > best[0]:
+                best = (float(lp), x)
+    Hs, Ds = np.array(Hs), np.array(Ds)
+    return dict(mean_heights=Hs.mean(0), gap_probability=((Hs[:, 1] - Hs[:, 0]) > gap).mean(0),
+                indicator_std=Ds.std(0), map_logp=best[0], map_x=best[1], draws=len(Hs))

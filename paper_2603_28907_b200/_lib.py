@@ -44,7 +44,7 @@ EXPORTS = [
     "mt_stats_update", "mt_rhat_partials", "mt_heights", "mt_loglik_heights", "mt_path_lengths", "mt_debug_traversal", "mt_philox",
     "mt_philox_curand", "mt_timing_start", "mt_timing_read", "mt_trace_counters", "mt_measure_fp32_peak",
     "mt_last_error", "mt_comm_unique_id", "mt_attach_comm", "mt_detach_comm", "mt_nuts_step",
-    "mt_nested_rhat_partials",
+    "mt_nested_rhat_partials", "mt_summary_update",
 ]
 
 _lib = None
@@ -71,6 +71,7 @@ def lib():
             "mt_stats_update": ([vp, i32, vp, vp, i32, vp, vp, vp, vp], ct.c_int),
             "mt_rhat_partials": ([vp, i32, vp, vp, i32, vp, vp], ct.c_int),
             "mt_nested_rhat_partials": ([vp, i32, i32, vp, vp, i32, vp, vp], ct.c_int),
+            "mt_summary_update": ([vp, i32, vp, vp, i32, ct.c_float, vp, vp, vp, vp], ct.c_int),
             "mt_heights": ([vp, i32, vp, vp, vp], ct.c_int),
             "mt_loglik_heights": ([vp, i32, vp, vp, vp, vp], ct.c_int),
             "mt_path_lengths": ([vp, i32, vp, vp, vp, vp], ct.c_int),
@@ -276,6 +277,33 @@ class Problem:
         _check(lib().mt_nested_rhat_partials(self.h, C, M, _ptr(mean), _ptr(m2), n, _ptr(out), _stream(stream)),
                "mt_nested_rhat_partials")
         return out
+
+    def summary_update(self, x, logp, acc, nz: int, gap: float, map_x=None, map_logp=None, stream=None):
+        """f4 posterior-summary accumulators (mt_summary_update); acc from summary_buffers()."""
+        C = x.shape[0]
+        _check(lib().mt_summary_update(self.h, C, _ptr(x), _ptr(logp), nz, gap, _ptr(acc), _ptr(map_x),
+                                       _ptr(map_logp), _stream(stream)), "mt_summary_update")
+
+    def summary_buffers(self, nz: int):
+        import torch
+        N = self.nx * self.ny
+        dev = f"cuda:{self.device}"
+        acc = torch.zeros(1 + 3 * N + 6 * N * nz, dtype=torch.float64, device=dev)
+        return acc, torch.zeros(self.P, dtype=torch.float32, device=dev), \
+            torch.full((1,), float("-inf"), dtype=torch.float64, device=dev)
+
+    def summaries(self, acc, nz: int):
+        """Host assembly: mean heights [2][nx][ny], air-gap exceedance probability
+        [nx][ny], indicator std [3][nx][ny][nz]."""
+        a = acc.cpu().numpy()
+        N = self.nx * self.ny
+        n = a[0]
+        meanH = (a[1:1 + 2 * N] / n).reshape(2, self.nx, self.ny)
+        gap = (a[1 + 2 * N:1 + 3 * N] / n).reshape(self.nx, self.ny)
+        sd = a[1 + 3 * N:1 + 3 * N + 3 * N * nz] / n
+        sd2 = a[1 + 3 * N + 3 * N * nz:] / n
+        std = np.sqrt(np.maximum(sd2 - sd * sd, 0.0)).reshape(3, self.nx, self.ny, nz)
+        return dict(mean_heights=meanH, gap_probability=gap, indicator_std=std, draws=int(n))
 
     # -- parity / debug ------------------------------------------------------
     def heights(self, x, stream=None):

@@ -491,6 +491,19 @@ int mt_nested_rhat_partials(mt_problem *p, int32_t C, int32_t M, const float *me
   return MT_OK;
 }
 
+int mt_summary_update(mt_problem *p, int32_t C, const float *x, const double *logp, int32_t nz, float gap,
+                      double *acc, float *map_x, double *map_logp, mt_stream stream) {
+  if (int r = check_chains(p, C)) return r;
+  if (C == 0) return MT_OK;
+  if (nz < 1) return set_err(MT_EINVAL, "nz = %d < 1", nz);
+  if (check_ptr(x, "x") || check_ptr(acc, "acc")) return MT_EINVAL;
+  if ((map_x != nullptr) != (map_logp != nullptr) || (map_x && !logp))
+    return set_err(MT_EINVAL, "map_x, map_logp and logp go together");
+  DevGuard g(p->device);
+  CK(launch_summary(p, C, x, logp, nz, gap, acc, map_x, map_logp, (cudaStream_t)stream));
+  return MT_OK;
+}
+
 int mt_heights(mt_problem *p, int32_t C, const float *x, float *H, mt_stream stream) {
   if (int r = check_chains(p, C)) return r;
   if (C == 0) return MT_OK;

@@ -214,6 +214,8 @@ cudaError_t launch_stats(mt_problem *p, int C, const float *x, const float *acc,
                          float *mean, float *m2, unsigned long long *acc_fixed, cudaStream_t s);
 cudaError_t launch_tile(mt_problem *p, int C, const float *src, float *dst, int to_tiled,
                         cudaStream_t s);
+cudaError_t launch_summary(mt_problem *p, int C, const float *x, const double *logp, int nz, float gap,
+                           double *acc, float *map_x, double *map_logp, cudaStream_t s);
 cudaError_t launch_nested_rhat_partials(mt_problem *p, int C, int M, const float *mean, const float *m2,
                                         int32_t n, double *out, cudaStream_t s);
 cudaError_t launch_rhat_partials(mt_problem *p, int C, const float *mean, const float *m2,

@@ -109,6 +109,93 @@ cudaError_t launch_nested_rhat_partials(mt_problem *p, int C, int M, const float
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// posterior summaries (reading R27): from the
+// current draws x [C][P] and their heights H (chain-interleaved, from K1):
+//   acc[0]                      number of draws accumulated
+//   acc[1 .. 2N]                Σ H_l(node)              -> posterior-mean heights
+//   acc[1+2N .. 1+3N)           #draws with H1 - H0 > gap (air-gap thickness exceedance)
+//   then Σ D, Σ D² per layer l in {muck, air, rock}, node, voxel k (layer-indicator
+//   tomography): D^(l) = ς(H_l - z_k) - ς(H_{l-1} - z_k) with
+//   ς(u) = 1/(1+e^{-u/γ}), γ = 1 m, H_{-1} = 0 (floor), H_2 = z_top, voxel
+//   columns at the nodes, z_k = k Δz, Δz = z_top/n_z.
+// Block = one node; thread = one voxel of its column; loop over chains.
+__global__ void k_summary_update(int C, int N, int nz, float z_top, float gap, const float *H,
+                                 double *acc) {
+  const int n = blockIdx.x;
+  const double dz = (double)z_top / nz;
+  double sH0 = 0, sH1 = 0, sgap = 0;
+  for (int k = threadIdx.x; k < nz; k += blockDim.x) {
+    const double z = k * dz;
+    double sd[3] = {0, 0, 0}, sd2[3] = {0, 0, 0};
+    for (int c = 0; c < C; c++) {
+      const double h0 = H[tix(c, 0, n, N)], h1 = H[tix(c, 1, n, N)];
+      const double sf = 1.0 / (1.0 + exp(z)), s0 = 1.0 / (1.0 + exp(-(h0 - z)));
+      const double s1 = 1.0 / (1.0 + exp(-(h1 - z))), st = 1.0 / (1.0 + exp(-((double)z_top - z)));
+      const double D[3] = {s0 - sf, s1 - s0, st - s1};
+#pragma unroll
+      for (int l = 0; l < 3; l++) {
+        sd[l] += D[l];
+        sd2[l] += D[l] * D[l];
+      }
+      if (k == 0) {
+        sH0 += h0;
+        sH1 += h1;
+        sgap += (h1 - h0) > gap ? 1.0 : 0.0;
+      }
+    }
+    double *accD = acc + 1 + 3 * (size_t)N;
+#pragma unroll
+    for (int l = 0; l < 3; l++) {
+      accD[((size_t)l * N + n) * nz + k] += sd[l];
+      accD[(3 * (size_t)N + (size_t)l * N + n) * nz + k] += sd2[l];
+    }
+  }
+  if (threadIdx.x == 0) {
+    acc[1 + n] += sH0;
+    acc[1 + N + n] += sH1;
+    acc[1 + 2 * N + n] += sgap;
+    if (n == 0) acc[0] += C;
+  }
+}
+
+// MAP draw: the highest log-posterior among the C current draws
+// replaces map_x / map_logp when higher (ties keep the first).
+__global__ void k_map_update(int C, int P, const float *x, const double *logp, float *map_x, double *map_logp) {
+  __shared__ double bv[MT_THREADS];
+  __shared__ int bi[MT_THREADS];
+  double v = -INFINITY;
+  int idx = -1;
+  for (int c = threadIdx.x; c < C; c += blockDim.x)
+    if (logp[c] > v) { v = logp[c]; idx = c; }
+  bv[threadIdx.x] = v;
+  bi[threadIdx.x] = idx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int t = 1; t < (int)blockDim.x; t++)
+      if (bv[t] > v || (bv[t] == v && bi[t] >= 0 && (idx < 0 || bi[t] < idx))) { v = bv[t]; idx = bi[t]; }
+    bi[0] = (idx >= 0 && v > *map_logp) ? idx : -1;
+    if (bi[0] >= 0) *map_logp = v;
+  }
+  __syncthreads();
+  const int best = bi[0];
+  if (best >= 0)
+    for (int k = threadIdx.x; k < P; k += blockDim.x) map_x[k] = x[(size_t)best * P + k];
+}
+
+cudaError_t launch_summary(mt_problem *p, int C, const float *x, const double *logp, int nz, float gap,
+                           double *acc, float *map_x, double *map_logp, cudaStream_t s) {
+  cudaError_t e = launch_heights(p, C, x, p->d_H, p->d_band, s);
+  if (e != cudaSuccess) return e;
+  k_summary_update<<<p->N, 64, 0, s>>>(C, p->N, nz, p->z_top, gap, p->d_H, acc);
+  p->all_launches++;
+  if (map_x && map_logp && logp) {
+    k_map_update<<<1, MT_THREADS, 0, s>>>(C, p->P, x, logp, map_x, map_logp);
+    p->all_launches++;
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_stats(mt_problem *p, int C, const float *x, const float *acc, int32_t n_prev,
                          float *mean, float *m2, unsigned long long *acc_fixed, cudaStream_t s) {
   if (C <= 0) return cudaSuccess;

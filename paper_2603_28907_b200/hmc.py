@@ -193,6 +193,22 @@ class ChainShard:
     def end_warmup(self):
         self.eps.fill_(self.da.final())
 
+    def summary_update(self, nz: int = 60, gap: float = 10.0):
+        """Accumulate the f4 posterior summaries of the current draws (mt_summary_update)."""
+        if getattr(self, "_sum", None) is None:
+            self._sum = (nz, gap) + tuple(self.pb.summary_buffers(nz))
+        nz, gap, acc, mx, ml = self._sum
+        self.pb.summary_update(self.x, self.logp, acc, nz, gap, mx, ml, stream=self.stream)
+
+    def summaries(self):
+        """Mean heights, air-gap probability, indicator-std tomography (all ranks'
+        draws, all-reduced) and this rank's MAP draw."""
+        nz, gap, acc, mx, ml = self._sum
+        acc = self._allreduce(acc.clone())
+        out = self.pb.summaries(acc, nz)
+        out.update(map_x=mx.cpu().numpy(), map_logp=float(ml.cpu()[0]), gap_threshold=gap)
+        return out
+
     def nested_rhat(self, M: int = 8) -> np.ndarray:
         """Nested R̂ over super-chains of M contiguous chains."""
         part = self.pb.nested_rhat_partials(self.C, M, self.mean, self.m2, max(self.n_samples, 1),
