@@ -65,6 +65,15 @@ def lib():
                                       ct.c_void_p, _lp]
         L.or_torus_spectrum_dr.argtypes = [ct.c_int, ct.c_int, ct.c_double] + [ct.POINTER(ct.c_double)] * 4
         L.or_logpost_grad_r.argtypes = [ct.c_void_p, ct.c_int, _dp, _dp, _dp, _dp, _dp]
+        L.or_voxel_path.restype = ct.c_int
+        L.or_voxel_path.argtypes = [ct.c_void_p, ct.c_int, ct.c_long, _ip, _dp, ct.c_int]
+        L.or_voxel_rhat.argtypes = [ct.c_void_p, ct.c_int, ct.c_double, _dp, ct.c_void_p, _dp]
+        L.or_voxel_lambda.argtypes = [ct.c_void_p, ct.c_int, _dp, _dp]
+        L.or_voxel_G_row.restype = ct.c_int
+        L.or_voxel_G_row.argtypes = [ct.c_void_p, ct.c_int, _dp, ct.c_long, _ip, _dp, ct.c_int,
+                                     ct.POINTER(ct.c_double)]
+        L.or_voxel_logpost_grad.argtypes = [ct.c_void_p, ct.c_int, ct.c_double, ct.c_double, _dp,
+                                            ct.c_int, _dp, _dp, _dp, _dp, _dp]
         L.or_philox4x32_10.argtypes = [_up, _up, _up]
         L.or_momenta.argtypes = [ct.c_int, ct.c_uint64, ct.c_uint64, ct.c_uint64, _dp]
         L.or_mh_uniform.restype = ct.c_double
@@ -221,6 +230,54 @@ class Problem:
         logp, ll, pr = np.zeros(C), np.zeros(C), np.zeros(C)
         g = np.zeros_like(v)
         lib().or_logpost_grad_r(self.h, C, v, logp, g, ll, pr)
+        return dict(logp=logp, grad=g, ll_dev=ll, prior=pr)
+
+    # -- the paper's voxel / sigmoid / linearised model (f3, R28/R29)
+    def voxel_path(self, nz: int, q: int):
+        """Voxel ids and lengths of ray q's in-box segment."""
+        cap = self.nx + self.ny + nz + 8
+        vox = np.zeros(cap, np.int32)
+        ln = np.zeros(cap)
+        n = lib().or_voxel_path(self.h, nz, q, vox, ln, cap)
+        assert n <= cap
+        return vox[:n], ln[:n]
+
+    def voxel_rhat(self, H: np.ndarray, nz: int, gamma: float = 1.0, with_weights: bool = False):
+        """H [2][nx][ny] -> R̂ [n_grid] (, W [3][n_grid]) (P:363-383)."""
+        H = np.ascontiguousarray(H, np.float64).reshape(-1)
+        ng = self.N * nz
+        Rh = np.zeros(ng)
+        W = np.zeros(3 * ng) if with_weights else None
+        lib().or_voxel_rhat(self.h, nz, gamma, H, W.ctypes.data if with_weights else None, Rh)
+        return (Rh, W.reshape(3, ng)) if with_weights else Rh
+
+    def voxel_lambda(self, R: np.ndarray, nz: int):
+        """λ_p(R) for every ray, R [n_grid] piecewise constant."""
+        lam = np.zeros(self.R)
+        lib().or_voxel_lambda(self.h, nz, np.ascontiguousarray(R, np.float64), lam)
+        return lam
+
+    def voxel_G_row(self, R0: np.ndarray, nz: int, q: int):
+        """(voxel ids, G_pv, λ_p(R0)) of row q of G = ∂λ/∂R at R0."""
+        cap = self.nx + self.ny + nz + 8
+        vox = np.zeros(cap, np.int32)
+        g = np.zeros(cap)
+        lam0 = ct.c_double()
+        n = lib().or_voxel_G_row(self.h, nz, np.ascontiguousarray(R0, np.float64), q, vox, g, cap,
+                                 ct.byref(lam0))
+        return vox[:n], g[:n], lam0.value
+
+    def voxel_logpost_grad(self, x: np.ndarray, Href: np.ndarray, nz: int, gamma: float = 1.0,
+                           tau: float = 1e-3):
+        """Linearised smooth model λ̂ = λ(R0) + G(R̂(H) - R0), R0 = R̂(H_ref) (P:293-294,
+        P:386-390) -> dict(logp, grad, ll_dev, prior)."""
+        x = np.ascontiguousarray(x, np.float64).reshape(-1, self.P)
+        C = x.shape[0]
+        logp, ll, pr = np.zeros(C), np.zeros(C), np.zeros(C)
+        g = np.zeros_like(x)
+        lib().or_voxel_logpost_grad(self.h, nz, gamma, tau,
+                                    np.ascontiguousarray(Href, np.float64).reshape(-1), C, x, logp, g,
+                                    ll, pr)
         return dict(logp=logp, grad=g, ll_dev=ll, prior=pr)
 
     def loglik_offset(self) -> float:

@@ -635,6 +635,232 @@ void or_logpost_grad_r(const or_problem *p, int C, const double *v, double *logp
 }
 
 /* ------------------------------------------------------------------ */
+/* The paper's voxel / sigmoid / linearised forward model (P:242-390,  */
+/* SURVEY §8(f) f3; reading R28 in DESIGN.md)                          */
+/* ------------------------------------------------------------------ */
+
+/* Voxel grid (R28): column (i,j) belongs to layer-grid node (i,j) (the map
+ * (i,j) -> (x(i),y(j)) of P:248-250 is the identity) and spans
+ * [e_i, e_{i+1}] x [f_j, f_{j+1}] with e_0 = X_0, e_i = (X_{i-1}+X_i)/2,
+ * e_nx = X_{nx-1} (likewise f for y); layer k spans [kΔz, (k+1)Δz) with
+ * Δz = z_top/nz.  Linear index v = (i*ny + j)*nz + k, the right-most index
+ * fastest. */
+static double col_edge(const double *X, int n, int i) {
+  if (i <= 0) return X[0];
+  if (i >= n) return X[n - 1];
+  return 0.5 * (X[i - 1] + X[i]);
+}
+
+static int cmp_double(const void *a, const void *b) {
+  double x = *(const double *)a, y = *(const double *)b;
+  return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+/* Voxels met by the in-box segment [0, s_exit] of ray q and the length in each
+ * (the L_pv of the piecewise-constant restriction λ_p(R)): every
+ * x-edge, y-edge and z-plane crossing in (0, s_exit) is a breakpoint; after
+ * sorting, each piece of positive length lies in one voxel, found from its
+ * midpoint.  Returns the number of pieces (writes at most cap). */
+int or_voxel_path(const or_problem *p, int nz, long q, int *vox, double *len, int cap) {
+  const double *o = p->det + 3 * p->rdet[q], *d = p->dir + 3 * q;
+  double s_exit, L_ext;
+  or_ray_extent(p, q, &s_exit, &L_ext);
+  int nb_max = (p->nx + 1) + (p->ny + 1) + (nz + 1) + 2;
+  double *bp = (double *)malloc(sizeof(double) * nb_max);
+  int nb = 0;
+  bp[nb++] = 0.0;
+  bp[nb++] = s_exit;
+  for (int i = 0; i <= p->nx; i++)
+    if (d[0] != 0.0) {
+      double s = (col_edge(p->X, p->nx, i) - o[0]) / d[0];
+      if (s > 0.0 && s < s_exit) bp[nb++] = s;
+    }
+  for (int j = 0; j <= p->ny; j++)
+    if (d[1] != 0.0) {
+      double s = (col_edge(p->Y, p->ny, j) - o[1]) / d[1];
+      if (s > 0.0 && s < s_exit) bp[nb++] = s;
+    }
+  double dz = p->z_top / nz;
+  for (int k = 1; k <= nz; k++) {
+    double s = (k * dz - o[2]) / d[2];
+    if (s > 0.0 && s < s_exit) bp[nb++] = s;
+  }
+  qsort(bp, nb, sizeof(double), cmp_double);
+  int n = 0;
+  for (int m = 0; m + 1 < nb; m++) {
+    double l = bp[m + 1] - bp[m];
+    if (!(l > 0.0)) continue;
+    double sm = 0.5 * (bp[m] + bp[m + 1]);
+    double xm = o[0] + sm * d[0], ym = o[1] + sm * d[1], zm = o[2] + sm * d[2];
+    int i = 0, j = 0;
+    while (i < p->nx - 1 && xm >= col_edge(p->X, p->nx, i + 1)) i++;
+    while (j < p->ny - 1 && ym >= col_edge(p->Y, p->ny, j + 1)) j++;
+    int k = (int)floor(zm / dz);
+    if (k < 0) k = 0;
+    if (k > nz - 1) k = nz - 1;
+    if (n < cap) { vox[n] = (i * p->ny + j) * nz + k; len[n] = l; }
+    n++;
+  }
+  free(bp);
+  return n;
+}
+
+/* Smooth layer indicators D^(l) with ς_γ(u) = 1/(1+e^{-u/γ})
+ * (P:349-352), three units muck / air / rock (H_{-1} = 0, H_0 muck top,
+ * H_1 cave back, H_2 = z_top; R27/R28), partition-of-unity weights
+ * W^(l) = D^(l)/Σ_l' D^(l') and R̂ = Σ_l W^(l) R^(l) with
+ * R^(l) = (ρ_m, ρ_a, ρ_r).  H: [2][nx][ny]; W [3][n_grid]
+ * (optional), Rhat [n_grid]. */
+static double sigm(double u, double gamma) { return 1.0 / (1.0 + exp(-u / gamma)); }
+
+void or_voxel_rhat(const or_problem *p, int nz, double gamma, const double *H, double *W, double *Rhat) {
+  int N = p->nx * p->ny;
+  double dz = p->z_top / nz, rho[3] = {p->rho_m, p->rho_a, p->rho_r};
+  for (int node = 0; node < N; node++)
+    for (int k = 0; k < nz; k++) {
+      double z = k * dz;
+      double b[4] = {0.0, H[node], H[N + node], p->z_top};
+      double D[3], S = 0.0;
+      for (int l = 0; l < 3; l++) { D[l] = sigm(b[l + 1] - z, gamma) - sigm(b[l] - z, gamma); S += D[l]; }
+      long v = (long)node * nz + k;
+      double R = 0.0;
+      for (int l = 0; l < 3; l++) {
+        double w = D[l] / S;
+        if (W) W[(long)l * N * nz + v] = w;
+        R += w * rho[l];
+      }
+      Rhat[v] = R;
+    }
+}
+
+/* λ_p(R) = w_p exp(-(Σ_v L_pv R_v + ρ_e L_ext)/Λ) for every ray: the restriction
+ * of eq:expected_counts to piecewise-constant fields, the rock
+ * beyond a side exit as in the exact model (R7). */
+void or_voxel_lambda(const or_problem *p, int nz, const double *R, double *lam) {
+  int cap = (p->nx + p->ny + nz) + 8;
+#pragma omp parallel
+  {
+    int *vox = (int *)malloc(sizeof(int) * cap);
+    double *len = (double *)malloc(sizeof(double) * cap);
+#pragma omp for schedule(dynamic, 256)
+    for (long q = 0; q < p->nray; q++) {
+      int n = or_voxel_path(p, nz, q, vox, len, cap);
+      double s_exit, L_ext, O = 0.0;
+      or_ray_extent(p, q, &s_exit, &L_ext);
+      for (int m = 0; m < n; m++) O += len[m] * R[vox[m]];
+      O += p->rho_e * L_ext;
+      lam[q] = p->w[q] * exp(-O / p->Lambda);
+    }
+    free(vox); free(len);
+  }
+}
+
+/* Row p of the sensitivity matrix G = ∂λ/∂R at R0:
+ * G_pv = -λ_p(R0) L_pv / Λ for the voxels on the ray (0 elsewhere).
+ * Writes the voxel ids / values of the row and returns their number; lam0_out
+ * receives λ_p(R0). */
+int or_voxel_G_row(const or_problem *p, int nz, const double *R0, long q, int *vox, double *G, int cap,
+                   double *lam0_out) {
+  int n = or_voxel_path(p, nz, q, vox, G, cap);
+  if (n > cap) n = cap;
+  double s_exit, L_ext, O = 0.0;
+  or_ray_extent(p, q, &s_exit, &L_ext);
+  for (int m = 0; m < n; m++) O += G[m] * R0[vox[m]];
+  O += p->rho_e * L_ext;
+  double lam0 = p->w[q] * exp(-O / p->Lambda);
+  for (int m = 0; m < n; m++) G[m] = -lam0 * G[m] / p->Lambda;
+  if (lam0_out) *lam0_out = lam0;
+  return n;
+}
+
+/* Log-posterior and gradient under the linearised smooth model
+ * λ̂(R̂(H)) = λ(R0) + G(R̂(H) - R0) with
+ * R0 = R̂(H_ref) for a reference geometry H_ref [2][nx][ny] (R28), the Poisson
+ * deviance likelihood of the exact model (R15) and the floor
+ * λ̂ <- max(λ̂, τ λ_p(R0)) with zero derivative below it (R29):
+ *   ℓ = Σ_p C(ln λ̂ - ln C) - λ̂ + C,   ∂ℓ/∂λ̂_p = C/λ̂ - 1,
+ *   ∂ℓ/∂R̂_v = Σ_p G_pv ∂ℓ/∂λ̂_p,
+ *   ∂R̂_v/∂H_0 = ς'(H_0 - z_k)(ρ_m - ρ_a)/S_k,  ∂R̂_v/∂H_1 = ς'(H_1 - z_k)(ρ_a - ρ_r)/S_k,
+ * S_k = Σ_l D^(l) = ς(z_top - z_k) - ς(-z_k) (the indicators telescope), then the
+ * heights chain rule and the CAR prior exactly as or_logpost_grad.
+ * x: [C][2N]; outputs as or_logpost_grad. */
+void or_voxel_logpost_grad(const or_problem *p, int nz, double gamma, double tau, const double *Href, int C,
+                           const double *x, double *logp, double *grad, double *ll_out, double *prior_out) {
+  int N = p->nx * p->ny;
+  long ng = (long)N * nz;
+  long R = p->nray;
+  int cap = (p->nx + p->ny + nz) + 8;
+  double dz = p->z_top / nz;
+  double *R0 = (double *)malloc(sizeof(double) * ng);
+  or_voxel_rhat(p, nz, gamma, Href, NULL, R0);
+  /* G rows at R0, once */
+  long *row = (long *)malloc(sizeof(long) * (R + 1));
+  double *lam0 = (double *)malloc(sizeof(double) * R);
+  row[0] = 0;
+  {
+    int *vox = (int *)malloc(sizeof(int) * cap);
+    double *len = (double *)malloc(sizeof(double) * cap);
+    for (long q = 0; q < R; q++) {
+      int n = or_voxel_path(p, nz, q, vox, len, cap);
+      row[q + 1] = row[q] + (n < cap ? n : cap);
+    }
+    free(vox); free(len);
+  }
+  int *gv = (int *)malloc(sizeof(int) * (row[R] > 0 ? row[R] : 1));
+  double *gx = (double *)malloc(sizeof(double) * (row[R] > 0 ? row[R] : 1));
+#pragma omp parallel for schedule(dynamic, 256)
+  for (long q = 0; q < R; q++) or_voxel_G_row(p, nz, R0, q, gv + row[q], gx + row[q], cap, &lam0[q]);
+#pragma omp parallel
+  {
+    double *H = (double *)malloc(sizeof(double) * 2 * N), *dH = (double *)malloc(sizeof(double) * 3 * N);
+    double *Rh = (double *)malloc(sizeof(double) * ng), *gR = (double *)malloc(sizeof(double) * ng);
+    double *GH = (double *)malloc(sizeof(double) * 2 * N);
+#pragma omp for schedule(dynamic, 1)
+    for (int c = 0; c < C; c++) {
+      const double *xc = x + (long)c * 2 * N;
+      or_heights(p, xc, H, dH);
+      or_voxel_rhat(p, nz, gamma, H, NULL, Rh);
+      memset(gR, 0, sizeof(double) * ng);
+      double ll = 0.0;
+      for (long q = 0; q < R; q++) {
+        double lam = lam0[q];
+        for (long m = row[q]; m < row[q + 1]; m++) lam += gx[m] * (Rh[gv[m]] - R0[gv[m]]);
+        double dl = 0.0;
+        if (lam < tau * lam0[q]) lam = tau * lam0[q];
+        else dl = p->cnt[q] / lam - 1.0;
+        double Cq = p->cnt[q];
+        ll += (Cq > 0 ? Cq * (log(lam) - log(Cq)) : 0.0) - lam + Cq;
+        for (long m = row[q]; m < row[q + 1]; m++) gR[gv[m]] += gx[m] * dl;
+      }
+      for (int node = 0; node < N; node++) {
+        double g0 = 0.0, g1 = 0.0;
+        for (int k = 0; k < nz; k++) {
+          double z = k * dz, S = sigm(p->z_top - z, gamma) - sigm(-z, gamma);
+          double s0 = sigm(H[node] - z, gamma), s1 = sigm(H[N + node] - z, gamma);
+          double gv_ = gR[(long)node * nz + k];
+          g0 += gv_ * s0 * (1.0 - s0) / gamma * (p->rho_m - p->rho_a) / S;
+          g1 += gv_ * s1 * (1.0 - s1) / gamma * (p->rho_a - p->rho_r) / S;
+        }
+        GH[node] = g0;
+        GH[N + node] = g1;
+      }
+      double *gc = grad + (long)c * 2 * N;
+      double pr = 0.0;
+      for (int l = 0; l < 2; l++) pr += or_prior_surface(p->nx, p->ny, p->r[l], xc + l * N, gc + l * N);
+      for (int k = 0; k < N; k++) {
+        gc[k] += GH[k] * dH[k] + GH[N + k] * dH[N + k];
+        gc[N + k] += GH[N + k] * dH[2 * N + k];
+      }
+      logp[c] = ll + pr;
+      if (ll_out) ll_out[c] = ll;
+      if (prior_out) prior_out[c] = pr;
+    }
+    free(H); free(dH); free(Rh); free(gR); free(GH);
+  }
+  free(R0); free(row); free(lam0); free(gv); free(gx);
+}
+
+/* ------------------------------------------------------------------ */
 /* Philox4x32-10 (Salmon et al., SC'11) and momenta (R22, reading c.1.12) */
 /* ------------------------------------------------------------------ */
 void or_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
