@@ -231,6 +231,36 @@ int mt_nested_rhat_partials(mt_problem *p, int32_t C, int32_t M, const float *me
 int mt_summary_update(mt_problem *p, int32_t C, const float *x, const double *logp, int32_t nz, float gap,
                       double *acc, float *map_x, double *map_logp, mt_stream stream);
 
+/* ---- the paper's voxel / sigmoid / linearised forward model (f3) -------- */
+
+/* Switch the problem's likelihood to the paper's own approximate forward
+ * model (readings R28/R29):
+ *   voxel grid: column (i,j) at layer-grid node (i,j) between the midpoints of
+ *     neighbouring nodes, n_z layers [kΔz, (k+1)Δz), Δz = z_top/n_z,
+ *     v = (i n_y + j) n_z + k;
+ *   R̂_v(H) = Σ_l W_v^(l) ρ_l, W = D/ΣD, D^(l) = ς_γ(H_l − kΔz) − ς_γ(H_{l−1} − kΔz)
+ *     (P:344-383), three units muck/air/rock;
+ *   λ̂(H) = λ(R0) + G (R̂(H) − R0), G = ∂λ/∂R at R0 = R̂(H_ref),
+ *     floored at τ λ(R0) with zero derivative below (R29);
+ *   ℓ = Σ_p C_p (ln λ̂_p − ln C_p) − λ̂_p + C_p (the exact model's deviance form).
+ * After the call mt_logpost_grad, mt_leapfrog, mt_hmc_step, mt_nuts_step and
+ * mt_loglik_heights evaluate this model (the prior, heights map, samplers and
+ * communicator are unchanged); mt_path_lengths stays the exact tracer's.
+ *   n_z      layers (1..4096); 0 switches back to the exact model and frees
+ *            the voxel buffers (gamma, tau, H_ref ignored).
+ *   gamma    sigmoid scale γ (> 0, metres; the paper's value is 1).
+ *   tau      floor fraction τ in [0, 1) (R29; 1e-3 in the tests and bench).
+ *   H_ref    HOST [2][n_x][n_y] fp32 reference geometry (muck top, cave back).
+ * Setup builds G (CSR by ray and CSC by voxel, fp32 values) on the host in
+ * double and uploads it: one synchronous call, O(nnz) host work and device
+ * memory 16 B per non-zero + 4·(n_grid + R)·⌈max_chains/32⌉·32 B of
+ * workspace.  Errors: MT_EINVAL (arguments), MT_ENOMEM, MT_ECUDA; on error the
+ * exact model is active. */
+int mt_voxel_model(mt_problem *p, int32_t n_z, float gamma, float tau, const float *H_ref);
+
+/* Active voxel model: n_z (0 = exact model), non-zeros of G, n_grid. */
+int mt_voxel_info(const mt_problem *p, int32_t *n_z, int64_t *nnz, int64_t *n_grid);
+
 /* ---- parity / debug entry points (not on the hot path) ---------------- */
 
 /* Heights map of x (device [C][P] -> device H [C][2][n_x][n_y]). */

@@ -44,7 +44,7 @@ EXPORTS = [
     "mt_stats_update", "mt_rhat_partials", "mt_heights", "mt_loglik_heights", "mt_path_lengths", "mt_debug_traversal", "mt_philox",
     "mt_philox_curand", "mt_timing_start", "mt_timing_read", "mt_trace_counters", "mt_measure_fp32_peak",
     "mt_last_error", "mt_comm_unique_id", "mt_attach_comm", "mt_detach_comm", "mt_nuts_step",
-    "mt_nested_rhat_partials", "mt_summary_update",
+    "mt_nested_rhat_partials", "mt_summary_update", "mt_voxel_model", "mt_voxel_info",
 ]
 
 _lib = None
@@ -86,6 +86,8 @@ def lib():
             "mt_attach_comm": ([vp, vp, i32, i32], ct.c_int),
             "mt_detach_comm": ([vp], ct.c_int),
             "mt_measure_fp32_peak": ([i32, vp, vp], ct.c_int),
+            "mt_voxel_model": ([vp, i32, ct.c_float, ct.c_float, vp], ct.c_int),
+            "mt_voxel_info": ([vp, vp, vp, vp], ct.c_int),
             "mt_last_error": ([], ct.c_char_p),
         }
         for name, (args, res) in sig.items():
@@ -370,6 +372,21 @@ class Problem:
 
     def detach_comm(self):
         _check(lib().mt_detach_comm(self.h), "mt_detach_comm")
+
+    def voxel_model(self, n_z: int, H_ref=None, gamma: float = 1.0, tau: float = 1e-3):
+        """Switch to the paper's voxel / sigmoid / linearised model (mt_voxel_model,
+        P:242-390) around R0 = R̂(H_ref), H_ref host [2][nx][ny]; n_z = 0 switches back."""
+        import numpy as np
+        if n_z == 0:
+            _check(lib().mt_voxel_model(self.h, 0, 1.0, 0.0, None), "mt_voxel_model")
+            return
+        Hr = np.ascontiguousarray(np.asarray(H_ref, np.float32).reshape(2 * self.nx * self.ny))
+        _check(lib().mt_voxel_model(self.h, n_z, gamma, tau, Hr.ctypes.data), "mt_voxel_model")
+
+    def voxel_info(self):
+        nz, nnz, ng = ct.c_int32(), ct.c_int64(), ct.c_int64()
+        _check(lib().mt_voxel_info(self.h, ct.byref(nz), ct.byref(nnz), ct.byref(ng)), "mt_voxel_info")
+        return dict(n_z=nz.value, nnz=nnz.value, n_grid=ng.value)
 
     def trace_counters(self):
         """Cumulative deferred chain x ray pairs (fp64 follow-up kernel) and the

@@ -79,6 +79,7 @@ int check_chains(const mt_problem *p, int32_t C) {
 }
 
 void free_all(mt_problem *p) {
+  voxel_free(p);
   void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_trav_geo, p->d_rl_head, p->d_rl_code, p->d_rl_ovf, p->d_ovf_q, p->d_ovf_n, p->d_H, p->d_Hlo, p->d_Hc, p->d_cs, p->d_G,
                   p->d_band, p->d_ll, p->d_x0, p->d_g0, p->d_mom, p->d_kin0, p->d_kin1, p->d_lp0};
   for (void *b : bufs)
@@ -198,6 +199,10 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
     off += (C > 0 ? C * log(C) : 0.0) - C - lgamma(C + 1.0);
   }
   p->loglik_offset = off;
+  p->rho[0] = d->rho_muck; p->rho[1] = d->rho_air; p->rho[2] = d->rho_rock; p->rho[3] = d->rho_ext;
+  p->att_len = d->att_len;
+  p->hX.assign(d->node_x, d->node_x + p->nx);
+  p->hY.assign(d->node_y, d->node_y + p->ny);
 
   // ---- internal ray order (performance only; results are order-independent
   // and per-ray outputs are mapped back): Morton order of the cell where the
@@ -229,6 +234,10 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
     }
     ra.swap(ra2); rb.swap(rb2); ob.swap(ob2);
   }
+  p->h_ra = ra;
+  p->h_rb = rb;
+  p->h_w.resize(p->R);
+  for (int64_t k = 0; k < p->R; k++) p->h_w[k] = d->ray_w[d->ray_lo + p->perm[k]];
   p->inv_perm.resize(p->R);
   for (int64_t k = 0; k < p->R; k++) p->inv_perm[p->perm[k]] = (int32_t)k;
 
@@ -664,6 +673,33 @@ int mt_trace_counters(mt_problem *p, int64_t *deferred, double *defer_ms) {
     *deferred = (int64_t)v;
   }
   if (defer_ms) *defer_ms = p->defer_ms;
+  return MT_OK;
+}
+
+int mt_voxel_model(mt_problem *p, int32_t n_z, float gamma, float tau, const float *H_ref) {
+  if (!p) return set_err(MT_EINVAL, "problem is NULL");
+  if (n_z < 0 || n_z > 4096) return set_err(MT_EINVAL, "n_z = %d not in [0, 4096]", n_z);
+  if (n_z > 0) {
+    if (!(gamma > 0.f) || !isfinite(gamma)) return set_err(MT_EINVAL, "gamma must be > 0");
+    if (!(tau >= 0.f && tau < 1.f)) return set_err(MT_EINVAL, "tau not in [0, 1)");
+    if (check_ptr(H_ref, "H_ref")) return MT_EINVAL;
+    for (int k = 0; k < 2 * p->N; k++)
+      if (!isfinite(H_ref[k])) return set_err(MT_EINVAL, "H_ref[%d] not finite", k);
+    if ((int64_t)p->N * n_z >= ((int64_t)1 << 31)) return set_err(MT_EINVAL, "n_grid too large");
+  }
+  DevGuard g(p->device);
+  CK(cudaDeviceSynchronize());
+  cudaError_t e = voxel_setup(p, n_z, gamma, tau, H_ref);
+  if (e == cudaErrorMemoryAllocation) return set_err(MT_ENOMEM, "voxel model: cudaMalloc failed");
+  if (e != cudaSuccess) return cuda_err(e, "voxel_setup");
+  return MT_OK;
+}
+
+int mt_voxel_info(const mt_problem *p, int32_t *n_z, int64_t *nnz, int64_t *n_grid) {
+  if (!p) return set_err(MT_EINVAL, "problem is NULL");
+  if (n_z) *n_z = p->vx.nz;
+  if (nnz) *nnz = p->vx.nnz;
+  if (n_grid) *n_grid = p->vx.ng;
   return MT_OK;
 }
 

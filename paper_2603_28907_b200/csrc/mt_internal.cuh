@@ -118,6 +118,22 @@ struct NutsArgs {
   int *any_active, *any_sub;
 };
 
+struct VxItem { int node, kb; long long eb, ee; };   // Gᵀ work item (voxel.cu)
+
+// f3 voxel / linearised model state (voxel.cu); nz == 0: the exact model is active
+struct VoxelState {
+  int nz = 0;
+  float gamma = 1.f, tau = 1e-3f;
+  int64_t nnz = 0, ng = 0;
+  int64_t *rowptr = nullptr, *colptr = nullptr;
+  int2 *csr = nullptr, *csc = nullptr;
+  float2 *lc = nullptr;
+  float *R0 = nullptr, *dR = nullptr, *r = nullptr;
+  VxItem *items = nullptr;
+  int64_t n_items = 0;
+  float href_lo = 0, href_hi = 0;
+};
+
 struct mt_problem {
   int device = 0;
   int num_sms = 148;
@@ -128,6 +144,11 @@ struct mt_problem {
   float car_r[2] = {0, 0};
   double sigma[2] = {0, 0}, logdetQ[2] = {0, 0};
   double loglik_offset = 0;
+  float rho[4] = {0, 0, 0, 0};  // muck, air, rock, exterior
+  float att_len = 0;
+  std::vector<float> hX, hY, h_w;          // host copies for the voxel-model setup (internal ray order)
+  std::vector<float4> h_ra, h_rb;
+  VoxelState vx;
   int prior_on = 1;
   int sample_r = 0;             // f2: the CAR r_l are sampled (two more parameters per chain)
   double *d_cs = nullptr;       // [N] torus spectrum table (sample_r)
@@ -195,6 +216,11 @@ cudaError_t launch_hmc_end(mt_problem *p, int C, float *x, double *logp, float *
 cudaError_t launch_momenta(mt_problem *p, int C, float *mom, uint64_t seed, uint64_t iter,
                            uint64_t chain_offset, cudaStream_t s);
 cudaError_t build_traversal(mt_problem *p);
+// voxel.cu (f3)
+cudaError_t voxel_setup(mt_problem *p, int nz, float gamma, float tau, const float *Href);
+void voxel_free(mt_problem *p);
+cudaError_t launch_voxel(mt_problem *p, int C, const float *H, const float4 *band, float *G, double *ll,
+                         cudaStream_t s);
 cudaError_t launch_kick(mt_problem *p, int mode, int C, float *x, float *mom, const float *grad,
                         const float *eps, float *kin, cudaStream_t s);
 enum { KICK_HALF_DRIFT = 0, KICK_FULL_DRIFT = 1, KICK_HALF_LAST = 2 };

@@ -1105,6 +1105,7 @@ static int64_t pick_splits(const mt_problem *p, int64_t groups, int64_t blocks_p
 cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const float4 *band,
                          float *G, double *ll, float *L, float *O, cudaStream_t s) {
   if (C <= 0 || p->R <= 0) return cudaSuccess;
+  if (mode == TRACE_LL && p->vx.nz > 0) return launch_voxel(p, C, H, band, G, ll, s);   // f3 model active
   TraceArgs a = base_trace_args(p);
   a.C = C;
   a.H = H; a.Hlo = p->d_Hlo; a.band = band; a.G = G; a.ll = ll; a.Lout = L; a.Oout = O;

@@ -22,11 +22,17 @@ def main():
     ap.add_argument("config", nargs="?", default="medium")
     ap.add_argument("--chains", type=int, default=None)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--voxel", type=int, default=0, help="n_z > 0: time the f3 voxel / linearised model")
     a = ap.parse_args()
     cfg = inputs.CONFIGS[a.config]
     C = a.chains or cfg.chains
     prob = inputs.make_problem(a.config)
     pb = Problem(prob, device=0, max_chains=C)
+    if a.voxel:
+        import time
+        t0 = time.time()
+        pb.voxel_model(a.voxel, prob["H_true"])
+        print("voxel setup", pb.voxel_info(), f"{time.time() - t0:.2f} s", flush=True)
     x = torch.from_numpy(inputs.chain_states(prob["x_true"], C, cfg.seed)).cuda()
     lp, g = pb.logpost_grad(x)
     for _ in range(3):
