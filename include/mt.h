@@ -254,7 +254,8 @@ int mt_summary_update(mt_problem *p, int32_t C, const float *x, const double *lo
  * Setup builds G (CSR by ray and CSC by voxel, fp32 values) on the host in
  * double and uploads it: one synchronous call, O(nnz) host work and device
  * memory 16 B per non-zero + 4·(n_grid + R)·⌈max_chains/32⌉·32 B of
- * workspace.  Errors: MT_EINVAL (arguments), MT_ENOMEM, MT_ECUDA; on error the
+ * workspace.  Limits: n_x n_y n_z <= 2^23 voxels and <= 2^23 rays per shard.
+ * Errors: MT_EINVAL (arguments, limits), MT_ENOMEM, MT_ECUDA; on error the
  * exact model is active. */
 int mt_voxel_model(mt_problem *p, int32_t n_z, float gamma, float tau, const float *H_ref);
 

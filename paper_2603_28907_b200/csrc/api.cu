@@ -685,7 +685,8 @@ int mt_voxel_model(mt_problem *p, int32_t n_z, float gamma, float tau, const flo
     if (check_ptr(H_ref, "H_ref")) return MT_EINVAL;
     for (int k = 0; k < 2 * p->N; k++)
       if (!isfinite(H_ref[k])) return set_err(MT_EINVAL, "H_ref[%d] not finite", k);
-    if ((int64_t)p->N * n_z >= ((int64_t)1 << 31)) return set_err(MT_EINVAL, "n_grid too large");
+    if ((int64_t)p->N * n_z > ((int64_t)1 << 23) || p->R > ((int64_t)1 << 23))
+      return set_err(MT_EINVAL, "voxel model: at most 2^23 voxels and 2^23 rays per shard");
   }
   DevGuard g(p->device);
   CK(cudaDeviceSynchronize());

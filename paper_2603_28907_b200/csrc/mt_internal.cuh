@@ -132,6 +132,8 @@ struct VoxelState {
   VxItem *items = nullptr;
   int64_t n_items = 0;
   float href_lo = 0, href_hi = 0;
+  int rpw_cl = 4, rpw_rl = 16;   // rays per warp of V2 (MT_VX_RPW overrides)
+  int vec = 0;                   // chains per lane of the chain-lanes kernels (0 = by C; MT_VX_VEC)
 };
 
 struct mt_problem {

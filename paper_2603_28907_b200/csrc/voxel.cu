@@ -24,6 +24,7 @@
 // (blockIdx.y = chain group), so one group's ΔR (n_grid·128 B) and r (R·128 B)
 // stay in L2 while its blocks run.
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -59,6 +60,7 @@ struct VoxArgs {
   const float4 *band;      // per chain {min H0, max H0, min H1, max H1}
   float href_lo, href_hi;  // min H_ref,0 and max H_ref,1
   float zc;                // band margin (VX_ZC γ)
+  int rpw;                 // rays per warp in V2
   float *G;                // ∂ℓ/∂H out (tix layout)
   double *ll;              // [C] += Σ_p ℓ_p
 };
@@ -100,38 +102,94 @@ __device__ __forceinline__ float loglik(float lam, float lam0, float cnt, float 
 }
 
 // ---- chain lanes ---------------------------------------------------------
-__global__ void __launch_bounds__(MT_THREADS) k_vx_rhat_cl(VoxArgs a) {
-  const int lane = threadIdx.x & 31, node = blockIdx.x * VX_WARPS + (threadIdx.x >> 5), grp = blockIdx.y;
-  if (node >= a.N) return;
-  const int c = grp * 32 + lane;
-  const float H0 = a.H[tix(c, 0, node, a.N)], H1 = a.H[tix(c, 1, node, a.N)];
-  float *out = a.dR + ((size_t)grp * a.ng + (size_t)node * a.nz) * 32 + lane;
-  const float *r0 = a.R0 + (size_t)node * a.nz;
-  for (int k = 0; k < a.nz; k++) out[(size_t)k * 32] = rhat(a, H0, H1, k * a.dz) - r0[k];
+// A group of W = 32·VEC chains: lane l holds chains g·W + 32u + l (u < VEC), so
+// the heights / ∂ℓ/∂H of each u are the coalesced 32-chain lines of the tix
+// layout, while ΔR and r store the VEC values of a lane contiguously
+// ([g][voxel | ray][lane][u]) and one gather of a G entry is a VEC-wide
+// vector load: VEC x fewer instructions per chain and entry.
+__device__ __forceinline__ int chain_of(int g, int VEC, int u, int lane) { return g * 32 * VEC + 32 * u + lane; }
+
+template <int VEC>
+__device__ __forceinline__ void ldv(const char *p, float (&d)[VEC]) {
+  if constexpr (VEC == 1) {
+    d[0] = __ldg((const float *)p);
+  } else if constexpr (VEC == 2) {
+    const float2 v = __ldg((const float2 *)p);
+    d[0] = v.x; d[1] = v.y;
+  } else {
+    const float4 v = __ldg((const float4 *)p);
+    d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+  }
 }
 
-// Σ_j val_j · src[idx_j·32 + lane] over one CSR/CSC segment: the lanes load 32
-// entries at a time (one 256-B read), then every lane walks them via shuffles.
-__device__ __forceinline__ float seg_dot_cl(const int2 *e, int64_t beg, int64_t end, const float *src, int lane) {
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int64_t j0 = beg; j0 < end; j0 += 32) {
-    const int n = end - j0 < 32 ? (int)(end - j0) : 32;
-    const int2 my = lane < n ? e[j0 + lane] : make_int2(0, 0);   // padding: G = 0 at voxel 0
-    const int n4 = (n + 3) & ~3;
-#pragma unroll 2
-    for (int t = 0; t < n4; t += 4) {
-      float v[4], d[4];
+template <int VEC>
+__device__ __forceinline__ void stv(float *p, const float (&d)[VEC]) {
+  if constexpr (VEC == 1) *p = d[0];
+  else if constexpr (VEC == 2) *(float2 *)p = make_float2(d[0], d[1]);
+  else *(float4 *)p = make_float4(d[0], d[1], d[2], d[3]);
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(MT_THREADS) k_vx_rhat_cl(VoxArgs a) {
+  const int lane = threadIdx.x & 31, node = blockIdx.x * VX_WARPS + (threadIdx.x >> 5), g = blockIdx.y;
+  if (node >= a.N) return;
+  float H0[VEC], H1[VEC];
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const int i = __shfl_sync(0xffffffffu, my.x, t + u);
-        v[u] = __int_as_float(__shfl_sync(0xffffffffu, my.y, t + u));
-        d[u] = __ldg(src + (size_t)i * 32 + lane);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; u++) acc[u] = fmaf(v[u], d[u], acc[u]);
-    }
+  for (int u = 0; u < VEC; u++) {
+    const int c = chain_of(g, VEC, u, lane);
+    H0[u] = c < a.C ? a.H[tix(c, 0, node, a.N)] : 0.f;
+    H1[u] = c < a.C ? a.H[tix(c, 1, node, a.N)] : 0.f;
   }
-  return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  float *out = a.dR + (((size_t)g * a.ng + (size_t)node * a.nz) * 32 + lane) * VEC;
+  const float *r0 = a.R0 + (size_t)node * a.nz;
+  for (int k = 0; k < a.nz; k++) {
+    const float z = k * a.dz, rk = r0[k];
+    float d[VEC];
+#pragma unroll
+    for (int u = 0; u < VEC; u++) d[u] = rhat(a, H0[u], H1[u], z) - rk;
+    stv<VEC>(out + (size_t)k * 32 * VEC, d);
+  }
+}
+
+// acc[u] += Σ_j val_j · src_lane[idx_j][u] over one CSR / CSC segment.  Each
+// chunk of 32 entries is loaded coalesced; the entries kept (all, or the
+// in-band ones for BAND) are compacted into a per-warp shared list as
+// {byte offset, value} (ballot + popc), zero-padded to a multiple of 4, and
+// read back two at a time by broadcast LDS.128.
+template <int VEC, bool BAND>
+__device__ __forceinline__ void gather_dot(const int2 *e, int64_t beg, int64_t end, const char *src_lane, int lane,
+                                           int nz, int k_lo, int k_hi, int4 *buf, float (&acc)[VEC]) {
+  int2 *b2 = reinterpret_cast<int2 *>(buf);
+  for (int64_t j0 = beg; j0 < end; j0 += 32) {
+    const bool in = j0 + lane < end;
+    const int2 my = in ? e[j0 + lane] : make_int2(0, 0);
+    bool keep = in;
+    if (BAND) {
+      const int k = my.x % nz;
+      keep = keep && k >= k_lo && k <= k_hi;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    const int n = __popc(m), n4 = (n + 3) & ~3;
+    if (keep) b2[__popc(m & ((1u << lane) - 1u))] = make_int2((int)((unsigned)my.x * (128u * VEC)), my.y);
+    if (lane >= n && lane < n4) b2[lane] = make_int2(0, 0);
+    __syncwarp();
+    for (int t = 0; t < n4; t += 4) {
+      const int4 q0 = buf[t >> 1], q1 = buf[(t >> 1) + 1];
+      float d0[VEC], d1[VEC], d2[VEC], d3[VEC];
+      ldv<VEC>(src_lane + (unsigned)q0.x, d0);
+      ldv<VEC>(src_lane + (unsigned)q0.z, d1);
+      ldv<VEC>(src_lane + (unsigned)q1.x, d2);
+      ldv<VEC>(src_lane + (unsigned)q1.z, d3);
+#pragma unroll
+      for (int u = 0; u < VEC; u++) {
+        acc[u] = fmaf(__int_as_float(q0.y), d0[u], acc[u]);
+        acc[u] = fmaf(__int_as_float(q0.w), d1[u], acc[u]);
+        acc[u] = fmaf(__int_as_float(q1.y), d2[u], acc[u]);
+        acc[u] = fmaf(__int_as_float(q1.w), d3[u], acc[u]);
+      }
+    }
+    __syncwarp();
+  }
 }
 
 // Layers k whose ΔR_v or ∂R̂_v/∂H can exceed e^{-VX_ZC} (relative) for any chain
@@ -161,69 +219,50 @@ __device__ __forceinline__ void vx_band(const VoxArgs &a, int c0, int c1, int la
   }
 }
 
-// Σ over the in-band entries of one CSR row of val_j · src[idx_j·32 + lane]:
-// each chunk of 32 entries is loaded coalesced, its in-band entries compacted
-// into a per-warp shared-memory list (ballot + popc), then broadcast-read.
-__device__ __forceinline__ float row_dot_band(const int2 *e, int64_t beg, int64_t end, const float *src, int lane,
-                                              int nz, int k_lo, int k_hi, int2 *buf) {
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int64_t j0 = beg; j0 < end; j0 += 32) {
-    const bool in = j0 + lane < end;
-    const int2 my = in ? e[j0 + lane] : make_int2(0, 0);
-    const int k = my.x % nz;
-    const bool keep = in && k >= k_lo && k <= k_hi;
-    const unsigned m = __ballot_sync(0xffffffffu, keep);
-    if (keep) buf[__popc(m & ((1u << lane) - 1u))] = my;
-    __syncwarp();
-    const int n = __popc(m);
-    for (int t = 0; t < n; t += 4) {
-      float v[4], d[4];
+// Block-sum the per-lane log-likelihood partials and add them to ll[c].
+template <int VEC>
+__device__ __forceinline__ void flush_ll(const double (&mine)[VEC], int lane, int g, int C, double *ll) {
+  __shared__ double sh[VX_WARPS][VEC][32];
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const int2 x = t + u < n ? buf[t + u] : make_int2(0, 0);
-        v[u] = __int_as_float(x.y);
-        d[u] = __ldg(src + (size_t)x.x * 32 + lane);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; u++) acc[u] = fmaf(v[u], d[u], acc[u]);
-    }
-    __syncwarp();
-  }
-  return (acc[0] + acc[1]) + (acc[2] + acc[3]);
-}
-
-__device__ __forceinline__ void flush_ll(double mine, int lane, int c, int C, double *ll) {
-  __shared__ double sh[VX_WARPS][32];
-  sh[threadIdx.x >> 5][lane] = mine;
+  for (int u = 0; u < VEC; u++) sh[threadIdx.x >> 5][u][lane] = mine[u];
   __syncthreads();
-  if (threadIdx.x < 32) {
+  if (threadIdx.x < 32 * VEC) {
+    const int u = threadIdx.x >> 5, l = threadIdx.x & 31;
     double s = 0.0;
 #pragma unroll
-    for (int w = 0; w < VX_WARPS; w++) s += sh[w][threadIdx.x];
+    for (int w = 0; w < VX_WARPS; w++) s += sh[w][u][l];
+    const int c = chain_of(g, VEC, u, l);
     if (c < C) atomicAdd(ll + c, s);
   }
 }
 
+template <int VEC>
 __global__ void __launch_bounds__(MT_THREADS) k_vx_fwd_cl(VoxArgs a) {
-  const int lane = threadIdx.x & 31, grp = blockIdx.y, c = grp * 32 + lane;
-  const int64_t p0 = ((int64_t)blockIdx.x * VX_WARPS + (threadIdx.x >> 5)) * VX_RPW_CL;
-  const float *dR = a.dR + (size_t)grp * a.ng * 32;
-  float *rout = a.r + (size_t)grp * a.R * 32 + lane;
-  __shared__ int2 bufs[VX_WARPS][32];
+  const int lane = threadIdx.x & 31, g = blockIdx.y;
+  const int64_t p0 = ((int64_t)blockIdx.x * VX_WARPS + (threadIdx.x >> 5)) * a.rpw;
+  const char *src = (const char *)(a.dR + ((size_t)g * a.ng * 32 + lane) * VEC);
+  float *rout = a.r + ((size_t)g * a.R * 32 + lane) * VEC;
+  __shared__ int4 bufs[VX_WARPS][16];
   int k_lo, k_hi;
-  vx_band(a, grp * 32, min(a.C, grp * 32 + 32), lane, k_lo, k_hi);
-  double mine = 0.0;
-  for (int m = 0; m < VX_RPW_CL; m++) {
+  vx_band(a, g * 32 * VEC, min(a.C, (g + 1) * 32 * VEC), lane, k_lo, k_hi);
+  double mine[VEC];
+#pragma unroll
+  for (int u = 0; u < VEC; u++) mine[u] = 0.0;
+  for (int m = 0; m < a.rpw; m++) {
     const int64_t p = p0 + m;
     if (p >= a.R) break;
-    const float acc = row_dot_band(a.csr, a.rowptr[p], a.rowptr[p + 1], dR, lane, a.nz, k_lo, k_hi,
-                                   bufs[threadIdx.x >> 5]);
+    float acc[VEC];
+#pragma unroll
+    for (int u = 0; u < VEC; u++) acc[u] = 0.f;
+    gather_dot<VEC, true>(a.csr, a.rowptr[p], a.rowptr[p + 1], src, lane, a.nz, k_lo, k_hi,
+                          bufs[threadIdx.x >> 5], acc);
     const float2 lc = a.lc[p];
-    float dl;
-    mine += loglik(lc.x + acc, lc.x, lc.y, a.tau, dl);
-    rout[(size_t)p * 32] = dl;
+    float dl[VEC];
+#pragma unroll
+    for (int u = 0; u < VEC; u++) mine[u] += loglik(lc.x + acc[u], lc.x, lc.y, a.tau, dl[u]);
+    stv<VEC>(rout + (size_t)p * 32 * VEC, dl);
   }
-  flush_ll(mine, lane, c, a.C, a.ll);
+  flush_ll<VEC>(mine, lane, g, a.C, a.ll);
 }
 
 // Gᵀ pass: one warp per work item = a run of <= VX_CH consecutive CSC entries
@@ -237,32 +276,49 @@ __device__ __forceinline__ void vx_factors(const VoxArgs &a, float H0, float H1,
   f1 = s1 * (1.f - s1) * (a.rho_a - a.rho_r) * iS;
 }
 
+template <int VEC>
 __global__ void __launch_bounds__(MT_THREADS) k_vx_bwd_cl(VoxArgs a) {
-  const int lane = threadIdx.x & 31, grp = blockIdx.y;
+  const int lane = threadIdx.x & 31, g = blockIdx.y;
   const int64_t w = (int64_t)blockIdx.x * VX_WARPS + (threadIdx.x >> 5);
+  __shared__ int4 bufs[VX_WARPS][16];
   if (w >= a.n_items) return;
   const VxItem it = a.items[w];
-  const int c = grp * 32 + lane;
-  const float H0 = a.H[tix(c, 0, it.node, a.N)], H1 = a.H[tix(c, 1, it.node, a.N)];
-  const float *r = a.r + (size_t)grp * a.R * 32;
+  float H0[VEC], H1[VEC], g0[VEC], g1[VEC];
+#pragma unroll
+  for (int u = 0; u < VEC; u++) {
+    const int c = chain_of(g, VEC, u, lane);
+    H0[u] = c < a.C ? a.H[tix(c, 0, it.node, a.N)] : 0.f;
+    H1[u] = c < a.C ? a.H[tix(c, 1, it.node, a.N)] : 0.f;
+    g0[u] = g1[u] = 0.f;
+  }
+  const char *src = (const char *)(a.r + ((size_t)g * a.R * 32 + lane) * VEC);
   int k_lo, k_hi;
-  vx_band(a, grp * 32, min(a.C, grp * 32 + 32), lane, k_lo, k_hi);
-  float g0 = 0.f, g1 = 0.f;
+  vx_band(a, g * 32 * VEC, min(a.C, (g + 1) * 32 * VEC), lane, k_lo, k_hi);
   int64_t pos = it.eb, v = (int64_t)it.node * a.nz + it.kb;
   for (int k = it.kb; pos < it.ee && k <= k_hi; k++, v++) {
     const int64_t cv = a.colptr[v + 1], vend = cv < (int64_t)it.ee ? cv : (int64_t)it.ee;
     if (vend <= pos) continue;
     if (k < k_lo) { pos = vend; continue; }
-    const float gR = seg_dot_cl(a.csc, pos, vend, r, lane);   // (Gᵀ r)_v, this item's share
-    float f0, f1;
-    vx_factors(a, H0, H1, k, f0, f1);
-    g0 = fmaf(gR, f0, g0);
-    g1 = fmaf(gR, f1, g1);
+    float gR[VEC];   // (Gᵀ r)_v, this item's share
+#pragma unroll
+    for (int u = 0; u < VEC; u++) gR[u] = 0.f;
+    gather_dot<VEC, false>(a.csc, pos, vend, src, lane, a.nz, 0, 0, bufs[threadIdx.x >> 5], gR);
+#pragma unroll
+    for (int u = 0; u < VEC; u++) {
+      float f0, f1;
+      vx_factors(a, H0[u], H1[u], k, f0, f1);
+      g0[u] = fmaf(gR[u], f0, g0[u]);
+      g1[u] = fmaf(gR[u], f1, g1[u]);
+    }
     pos = vend;
   }
-  if (c < a.C) {   // G is zero on entry (K3 clears what it reads)
-    atomicAdd(a.G + tix(c, 0, it.node, a.N), g0);
-    atomicAdd(a.G + tix(c, 1, it.node, a.N), g1);
+#pragma unroll
+  for (int u = 0; u < VEC; u++) {
+    const int c = chain_of(g, VEC, u, lane);
+    if (c < a.C) {   // G is zero on entry (K3 clears what it reads)
+      atomicAdd(a.G + tix(c, 0, it.node, a.N), g0[u]);
+      atomicAdd(a.G + tix(c, 1, it.node, a.N), g1[u]);
+    }
   }
 }
 
@@ -316,11 +372,11 @@ __device__ __forceinline__ float row_part_rl_band(const int2 *e, int64_t beg, in
 
 __global__ void __launch_bounds__(MT_THREADS) k_vx_fwd_rl(VoxArgs a) {
   const int lane = threadIdx.x & 31;
-  const int64_t p0 = ((int64_t)blockIdx.x * VX_WARPS + (threadIdx.x >> 5)) * VX_RPW_RL;
+  const int64_t p0 = ((int64_t)blockIdx.x * VX_WARPS + (threadIdx.x >> 5)) * a.rpw;
   int k_lo, k_hi;
   vx_band(a, 0, a.C, lane, k_lo, k_hi);
   double mine = 0.0;   // lane c: chain c's partial
-  for (int m = 0; m < VX_RPW_RL; m++) {
+  for (int m = 0; m < a.rpw; m++) {
     const int64_t p = p0 + m;
     if (p >= a.R) break;
     const int64_t beg = a.rowptr[p], end = a.rowptr[p + 1];
@@ -332,7 +388,8 @@ __global__ void __launch_bounds__(MT_THREADS) k_vx_fwd_rl(VoxArgs a) {
       if (lane == c) { mine += l; a.r[(size_t)c * a.R + p] = dl; }
     }
   }
-  flush_ll(mine, lane, lane, a.C, a.ll);
+  const double mine1[1] = {mine};
+  flush_ll<1>(mine1, lane, 0, a.C, a.ll);
 }
 
 __global__ void __launch_bounds__(MT_THREADS) k_vx_bwd_rl(VoxArgs a) {
@@ -512,12 +569,14 @@ cudaError_t voxel_setup(mt_problem *p, int nz, float gamma, float tau, const flo
   }
   // Gᵀ work items: runs of <= VX_CH entries inside one node column
   std::vector<VxItem> items;
+  int ch = VX_CH;
+  if (const char *ev = getenv("MT_VX_CH")) ch = std::max(32, atoi(ev));
   for (int node = 0; node < N; node++) {
     int64_t e0 = colptr[(int64_t)node * nz], e1 = colptr[(int64_t)(node + 1) * nz];
     int k = 0;
     for (int64_t e = e0; e < e1;) {
       while (colptr[(int64_t)node * nz + k + 1] <= e) k++;
-      const int64_t ee = std::min<int64_t>(e + VX_CH, e1);
+      const int64_t ee = std::min<int64_t>(e + ch, e1);
       items.push_back(VxItem{node, k, e, ee});
       e = ee;
     }
@@ -527,9 +586,14 @@ cudaError_t voxel_setup(mt_problem *p, int nz, float gamma, float tau, const flo
   // device
   VoxelState &s = p->vx;
   s.nz = nz; s.gamma = gamma; s.tau = tau; s.nnz = nnz; s.ng = ng;
+  s.rpw_cl = VX_RPW_CL;
+  s.vec = 0;
+  if (const char *ev = getenv("MT_VX_VEC")) s.vec = atoi(ev) >= 4 ? 4 : (atoi(ev) >= 2 ? 2 : 1);
+  s.rpw_rl = VX_RPW_RL;
+  if (const char *ev = getenv("MT_VX_RPW")) s.rpw_cl = s.rpw_rl = std::max(1, atoi(ev));
   s.href_lo = *std::min_element(Href, Href + N);
   s.href_hi = *std::max_element(Href + N, Href + 2 * N);
-  const size_t MC32 = (size_t)(p->max_chains > 0 ? (p->max_chains + 31) / 32 * 32 : 32);
+  const size_t MC32 = (size_t)(p->max_chains > 0 ? (p->max_chains + 127) / 128 * 128 : 128);   // whole groups of up to 128
   cudaError_t e = cudaSuccess;
 #define VALLOC(ptr, bytes) \
   if (e == cudaSuccess) e = cudaMalloc((void **)&(ptr), (bytes));
@@ -579,16 +643,24 @@ cudaError_t launch_voxel(mt_problem *p, int C, const float *H, const float4 *ban
   const unsigned nb_bwd = (unsigned)std::max<int64_t>(1, (v.n_items + VX_WARPS - 1) / VX_WARPS);
   if (rec) cudaEventRecord(p->ev_a[p->n_rec], s);
   if (C >= 16) {
-    const unsigned groups = (unsigned)((C + 31) / 32);
-    k_vx_rhat_cl<<<dim3(nb_nodes, groups), MT_THREADS, 0, s>>>(a);
-    const int64_t rpb = (int64_t)VX_WARPS * VX_RPW_CL;
-    if (p->R > 0) k_vx_fwd_cl<<<dim3((unsigned)((p->R + rpb - 1) / rpb), groups), MT_THREADS, 0, s>>>(a);
-    if (rec) cudaEventRecord(p->ev_m[p->n_rec], s);
-    k_vx_bwd_cl<<<dim3(nb_bwd, groups), MT_THREADS, 0, s>>>(a);
+    // chains per lane: 4 once the 128-chain groups are mostly full (MT_VX_VEC overrides)
+    const int vec = p->vx.vec > 0 ? p->vx.vec : (C >= 96 ? 4 : (C >= 48 ? 2 : 1));
+    const unsigned groups = (unsigned)((C + 32 * vec - 1) / (32 * vec));
+    a.rpw = p->vx.rpw_cl;
+    const int64_t rpb = (int64_t)VX_WARPS * a.rpw;
+    const unsigned nb_rays = (unsigned)((p->R + rpb - 1) / rpb);
+#define VX_LAUNCH_CL(V)                                                                      \
+    k_vx_rhat_cl<V><<<dim3(nb_nodes, groups), MT_THREADS, 0, s>>>(a);                       \
+    if (p->R > 0) k_vx_fwd_cl<V><<<dim3(nb_rays, groups), MT_THREADS, 0, s>>>(a);          \
+    if (rec) cudaEventRecord(p->ev_m[p->n_rec], s);                                          \
+    k_vx_bwd_cl<V><<<dim3(nb_bwd, groups), MT_THREADS, 0, s>>>(a);
+    if (vec == 4) { VX_LAUNCH_CL(4) } else if (vec == 2) { VX_LAUNCH_CL(2) } else { VX_LAUNCH_CL(1) }
+#undef VX_LAUNCH_CL
   } else {
     const int64_t n = (int64_t)C * v.ng;
     k_vx_rhat_rl<<<(unsigned)((n + MT_THREADS - 1) / MT_THREADS), MT_THREADS, 0, s>>>(a);
-    const int64_t rpb = (int64_t)VX_WARPS * VX_RPW_RL;
+    a.rpw = p->vx.rpw_rl;
+    const int64_t rpb = (int64_t)VX_WARPS * a.rpw;
     if (p->R > 0) k_vx_fwd_rl<<<(unsigned)((p->R + rpb - 1) / rpb), MT_THREADS, 0, s>>>(a);
     if (rec) cudaEventRecord(p->ev_m[p->n_rec], s);
     k_vx_bwd_rl<<<nb_bwd, MT_THREADS, 0, s>>>(a);
