@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--sampler", default="hmc", choices=["hmc", "nuts"],
                     help="fixed-L HMC (configs[3], default) or NUTS (SURVEY §8(f) f1; --max-depth)")
     ap.add_argument("--max-depth", type=int, default=8, help="NUTS: 2^max_depth leaves cap (P:662-669)")
+    ap.add_argument("--model", default="exact", choices=["exact", "voxel"],
+                    help="exact bilinear tracing (north_star) or the paper's voxel/linearised model (f3)")
+    ap.add_argument("--nz", type=int, default=60, help="voxel model: layers (Δz = z_top/nz, reading R28)")
     ap.add_argument("--sample-r", action="store_true",
                     help="hierarchical CAR r_l (SURVEY §8(f) f2): two more parameters per chain")
     ap.add_argument("--chains-total", type=int, default=8192)     # configs[3]
@@ -224,6 +227,10 @@ def main():
         R_total = pb.R * ws   # (chain sharding: every rank traces all rays of its chains)
         shard = ChainShard(pb, x0, seed=inputs.philox_key(cfg), L=L, eps0=eps, chain_offset=offset,
                            n_chains_total=C * ws, sampler=args.sampler, max_depth=args.max_depth)
+    voxel = args.model == "voxel"
+    if voxel:   # R0 = R̂(H_ref), H_ref = the synthetic truth (stand-in for the expert model, R28)
+        pb.voxel_model(args.nz, prob["H_true"])
+        shard.refresh()
     R, P = pb.R, pb.P
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MiB > 126 MB L2
 
@@ -236,10 +243,16 @@ def main():
     for _ in range(args.warmup):
         shard.step(adapt=False, sample=True, monitor=True)
     barrier()
+    l2_peak = None
+    if voxel:
+        from paper_2603_28907_b200 import measure_l2_gather
+        l2_peak = measure_l2_gather(local, 32 << 20)
+        barrier()
     clocks = ClockSampler() if rank == 0 else None
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     pb.timing_start(args.steps * (L if args.sampler == "hmc" else 2 ** args.max_depth) + 8)
     d0 = pb.trace_counters()["deferred"]
+    g0 = pb.voxel_gathered_bytes() if voxel else 0
     wall0 = time.perf_counter()
     for k in range(args.steps):
         flush.zero_()
@@ -252,6 +265,7 @@ def main():
     t_ms = sum(a.elapsed_time(b) for a, b in ev)
     tm = pb.timing_read()
     cnt = pb.trace_counters()
+    gathered = (pb.voxel_gathered_bytes() - g0) if voxel else 0
     t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -285,6 +299,35 @@ def main():
                 "peak_note": "FP32 peak derived: 148 SMs x 128 lanes x 2 x 1.965 GHz (B200_PROFILING.md); "
                              "F = algorithmic flops per chain x ray from the oracle's work counters "
                              "(tools/count_work.py, DESIGN.md Roofline)"}
+
+    if voxel:
+        # V2 (λ̂ SpMV) + V3 (Gᵀ pass) are bound by L2-resident gathers of ΔR / r: 4 B per
+        # chain and in-band G entry each (the V2 count, counted by the kernel; V3 gathers
+        # the same entries), against the measured L2 gather bandwidth
+        avg_vx_ms = tm["trace_ms"] / max(tm["trace_launches"], 1)
+        ach = 2.0 * gathered / max(tm["trace_launches"], 1) / (avg_vx_ms * 1e-3) / 1e9
+        vtraffic = None
+        tpath = os.path.join(ROOT, "profiles", "voxel_traffic.json")
+        if os.path.exists(tpath):
+            tr = json.load(open(tpath)).get(args.workload)
+            vtraffic = tr.get("bytes_per_launch") if tr and tr.get("chains") == C else None
+        info = pb.voxel_info()
+        roofline = {"bound": "l2", "achieved": ach, "peak": l2_peak, "unit": "GB/s", "frac": ach / l2_peak,
+                    "traffic": vtraffic,
+                    "kernel": "V1 k_vx_rhat + V2 k_vx_fwd + V3 k_vx_bwd per evaluation (voxel model)",
+                    "gathered_bytes_per_launch": 2.0 * gathered / max(tm["trace_launches"], 1),
+                    "trace_share_of_step": tm["trace_ms"] / t_ms if ws == 1 else None,
+                    "avg_eval_ms": avg_vx_ms, "nnz": info["nnz"], "n_grid": info["n_grid"],
+                    "peak_note": "peak = mt_measure_l2_gather on this device (512-B rows at hashed indices of "
+                                 "a 32 MiB L2-resident buffer, best of 10); achieved = algorithmic gather bytes "
+                                 "(kernel-counted) / measured V1+V2+V3 time (DESIGN.md §7 voxel model)"}
+        if C < 16:   # row lanes (one chain): the G stream (CSR + CSC, 8 B per entry each) from HBM binds
+            hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+            gb = 16.0 * info["nnz"] / (avg_vx_ms * 1e-3) / 1e9
+            roofline.update({"bound": "hbm", "achieved": gb, "peak": hbm, "frac": gb / hbm,
+                             "peak_note": "peak = MEASURED_PEAKS.json hbm_gbs (copy bandwidth); achieved = G bytes "
+                                          "(CSR + CSC, 16 B per non-zero; the in-band skip reads less) / "
+                                          "measured V1+V2+V3 time (DESIGN.md §7 voxel model)"})
 
     e2e = None
     if not args.no_e2e:
@@ -340,6 +383,8 @@ def main():
                        "rays_per_gpu": R, "params": P,
                        "leapfrog_steps": L, "parallelism": (f"ray-sharded x{ws}" if ray else f"chain-sharded x{ws}"),
                        "car_r": "sampled (f2)" if args.sample_r else "fixed",
+                       "forward_model": (f"voxel/sigmoid/linearised (f3, P:242-390): n_z={args.nz}, gamma=1 m, "
+                                         "R0 = R-hat(truth)") if voxel else "exact bilinear tracing (north_star)",
                        "phase": "sampling (fixed eps from the 100-iteration dual-averaging warm-up, "
                                 "tools/tune_eps.py; Welford + all-reduced acceptance sums each step)",
                        "eps": eps,

@@ -262,6 +262,17 @@ int mt_voxel_model(mt_problem *p, int32_t n_z, float gamma, float tau, const flo
 /* Active voxel model: n_z (0 = exact model), non-zeros of G, n_grid. */
 int mt_voxel_info(const mt_problem *p, int32_t *n_z, int64_t *nnz, int64_t *n_grid);
 
+/* Cumulative ΔR bytes the λ̂ kernel gathered while timing was on
+ * (mt_timing_start .. mt_timing_read): 4 B per chain and in-band G entry, the
+ * algorithmic gather traffic of the voxel model's roofline.
+ * Synchronises the device. */
+int mt_voxel_counters(mt_problem *p, uint64_t *gathered_bytes);
+
+/* Measured roofline denominator for the voxel kernels: the best of 10 runs of
+ * a gather kernel reading 512-B rows at hashed indices of an L2-resident
+ * buffer of `bytes` (>= 1 MiB; 32 MiB in bench.py), in GB/s. */
+int mt_measure_l2_gather(int32_t device, int64_t bytes, double *gbs);
+
 /* ---- parity / debug entry points (not on the hot path) ---------------- */
 
 /* Heights map of x (device [C][P] -> device H [C][2][n_x][n_y]). */

@@ -45,6 +45,7 @@ EXPORTS = [
     "mt_philox_curand", "mt_timing_start", "mt_timing_read", "mt_trace_counters", "mt_measure_fp32_peak",
     "mt_last_error", "mt_comm_unique_id", "mt_attach_comm", "mt_detach_comm", "mt_nuts_step",
     "mt_nested_rhat_partials", "mt_summary_update", "mt_voxel_model", "mt_voxel_info",
+    "mt_voxel_counters", "mt_measure_l2_gather",
 ]
 
 _lib = None
@@ -88,6 +89,8 @@ def lib():
             "mt_measure_fp32_peak": ([i32, vp, vp], ct.c_int),
             "mt_voxel_model": ([vp, i32, ct.c_float, ct.c_float, vp], ct.c_int),
             "mt_voxel_info": ([vp, vp, vp, vp], ct.c_int),
+            "mt_voxel_counters": ([vp, vp], ct.c_int),
+            "mt_measure_l2_gather": ([i32, i64, vp], ct.c_int),
             "mt_last_error": ([], ct.c_char_p),
         }
         for name, (args, res) in sig.items():
@@ -388,6 +391,11 @@ class Problem:
         _check(lib().mt_voxel_info(self.h, ct.byref(nz), ct.byref(nnz), ct.byref(ng)), "mt_voxel_info")
         return dict(n_z=nz.value, nnz=nnz.value, n_grid=ng.value)
 
+    def voxel_gathered_bytes(self) -> int:
+        v = ct.c_uint64()
+        _check(lib().mt_voxel_counters(self.h, ct.byref(v)), "mt_voxel_counters")
+        return v.value
+
     def trace_counters(self):
         """Cumulative deferred chain x ray pairs (fp64 follow-up kernel) and the
         device time of the follow-up launches in the last timed region (ms)."""
@@ -417,3 +425,10 @@ def measure_fp32_peak(device: int = 0):
     tf, mhz = ct.c_double(), ct.c_double()
     _check(lib().mt_measure_fp32_peak(device, ct.byref(tf), ct.byref(mhz)), "mt_measure_fp32_peak")
     return tf.value, mhz.value
+
+
+def measure_l2_gather(device: int = 0, nbytes: int = 32 << 20) -> float:
+    """Measured L2-resident 512-B-row gather bandwidth (GB/s), the voxel kernels' roofline."""
+    v = ct.c_double()
+    _check(lib().mt_measure_l2_gather(device, nbytes, ct.byref(v)), "mt_measure_l2_gather")
+    return v.value

@@ -704,6 +704,25 @@ int mt_voxel_info(const mt_problem *p, int32_t *n_z, int64_t *nnz, int64_t *n_gr
   return MT_OK;
 }
 
+int mt_voxel_counters(mt_problem *p, uint64_t *gathered_bytes) {
+  if (!p || !gathered_bytes) return set_err(MT_EINVAL, "NULL argument");
+  *gathered_bytes = 0;
+  if (!p->vx.gathered) return MT_OK;
+  DevGuard g(p->device);
+  CK(cudaDeviceSynchronize());
+  unsigned long long v = 0;
+  CK(cudaMemcpy(&v, p->vx.gathered, sizeof v, cudaMemcpyDeviceToHost));
+  *gathered_bytes = v;
+  return MT_OK;
+}
+
+int mt_measure_l2_gather(int32_t device, int64_t bytes, double *gbs) {
+  if (!gbs || bytes < (1 << 20)) return set_err(MT_EINVAL, "gbs NULL or bytes < 1 MiB");
+  DevGuard g(device);
+  CK(run_l2_gather_peak(device, (size_t)bytes, gbs));
+  return MT_OK;
+}
+
 int mt_measure_fp32_peak(int32_t device, double *tflops, double *sm_clock_mhz) {
   if (!tflops || !sm_clock_mhz) return set_err(MT_EINVAL, "NULL argument");
   DevGuard g(device);

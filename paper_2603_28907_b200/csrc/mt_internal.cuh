@@ -133,6 +133,9 @@ struct VoxelState {
   int64_t n_items = 0;
   float href_lo = 0, href_hi = 0;
   int rpw_cl = 4, rpw_rl = 16;   // rays per warp of V2 (MT_VX_RPW overrides)
+  unsigned long long *gathered = nullptr;   // V2 gather-byte counter (while timing)
+  uint4 *kofs = nullptr;         // per-row layer-bucket offsets
+  int kb = 1;
   int vec = 0;                   // chains per lane of the chain-lanes kernels (0 = by C; MT_VX_VEC)
 };
 
@@ -238,6 +241,7 @@ cudaError_t comm_allreduce_logp_grad(mt_problem *p, int C, double *logp, float *
 cudaError_t launch_philox(const uint32_t *ctr, uint32_t k0, uint32_t k1, uint32_t *out,
                           int64_t n, int use_curand, cudaStream_t s);
 cudaError_t run_fp32_peak(int device, double *tflops, double *mhz);
+cudaError_t run_l2_gather_peak(int device, size_t bytes, double *gbs);
 cudaError_t launch_stats(mt_problem *p, int C, const float *x, const float *acc, int32_t n_prev,
                          float *mean, float *m2, unsigned long long *acc_fixed, cudaStream_t s);
 cudaError_t launch_tile(mt_problem *p, int C, const float *src, float *dst, int to_tiled,

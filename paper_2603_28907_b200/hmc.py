@@ -146,6 +146,10 @@ class ChainShard:
         self.it = 0
         problem.logpost_grad(self.x, self.logp, self.grad, self.status, stream=stream)
 
+    def refresh(self):
+        """Re-evaluate logp / grad at the current x (after the problem's model changed)."""
+        self.pb.logpost_grad(self.x, self.logp, self.grad, self.status, stream=self.stream)
+
     def _allreduce(self, t, op="sum"):
         if self.replicated:
             return t
