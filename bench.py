@@ -110,9 +110,11 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
 
 
-def cpu_baseline(seconds: float, chains: int = 4, name: str = "chain_sharded"):
+def cpu_baseline(seconds: float, chains: int = 4, name: str = "chain_sharded", nz: int = 0):
     """The fp64 oracle, as it stands, on this host's cores: the workload's
-    geometry, `chains` chains x all its rays per evaluation, repeated for ~`seconds`."""
+    geometry, `chains` chains x all its rays per evaluation, repeated for ~`seconds`
+    (nz > 0: the voxel / linearised model's oracle, G rebuilt by every call as the
+    oracle does)."""
     import numpy as np
 
     import oracle
@@ -123,14 +125,18 @@ def cpu_baseline(seconds: float, chains: int = 4, name: str = "chain_sharded"):
     t0 = time.perf_counter()
     n = 0
     while True:
-        op.logpost_grad(x)
+        if nz:
+            op.voxel_logpost_grad(x, np.asarray(prob["H_true"], np.float32).astype(np.float64), nz)
+        else:
+            op.logpost_grad(x)
         n += 1
         if time.perf_counter() - t0 >= seconds:
             break
     dt = time.perf_counter() - t0
     return {"value": n * chains * op.R / dt, "unit": UNIT, "cores": oracle.num_threads(),
             "kind": "oracle",
-            "sample": f"{name} geometry, {chains} near-posterior chain(s) x {op.R} rays per evaluation, "
+            "sample": f"{name} geometry{' (voxel model, n_z=%d)' % nz if nz else ''}, {chains} near-posterior "
+                      f"chain(s) x {op.R} rays per evaluation, "
                       f"{n} evaluations ({n * chains * op.R:.3g} chain-ray pairs) in {dt:.1f} s, fp64"}
 
 
@@ -369,7 +375,8 @@ def main():
         return
     base = None
     if ws == 1 and not args.no_cpu_baseline:
-        base = cpu_baseline(args.cpu_seconds, chains=1 if ray else 4, name=args.workload)
+        base = cpu_baseline(args.cpu_seconds, chains=1 if ray else 4, name=args.workload,
+                            nz=args.nz if voxel else 0)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f32",

@@ -136,6 +136,7 @@ struct VoxelState {
   unsigned long long *gathered = nullptr;   // V2 gather-byte counter (while timing)
   uint4 *kofs = nullptr;         // per-row layer-bucket offsets
   int kb = 1;
+  int gchunk = 0;                // chain groups per V1-V3 launch triple (0 = all; MT_VX_GCHUNK)
   int vec = 0;                   // chains per lane of the chain-lanes kernels (0 = by C; MT_VX_VEC)
 };
 

@@ -63,6 +63,7 @@ struct VoxArgs {
   float href_lo, href_hi;  // min H_ref,0 and max H_ref,1
   float zc;                // band margin (VX_ZC γ)
   int rpw;                 // rays per warp in V2
+  int g0;                  // first chain group of this launch (blockIdx.y + g0)
   unsigned long long *gathered;   // optional: += ΔR bytes gathered by V2 (valid chains × 4 B per kept entry)
   float *G;                // ∂ℓ/∂H out (tix layout)
   double *ll;              // [C] += Σ_p ℓ_p
@@ -132,10 +133,39 @@ __device__ __forceinline__ void stv(float *p, const float (&d)[VEC]) {
   else *(float4 *)p = make_float4(d[0], d[1], d[2], d[3]);
 }
 
+// Layers k whose ΔR_v or ∂R̂_v/∂H can exceed e^{-VX_ZC} (relative) for any chain
+// c in [c0, c1): z_k within VX_ZC γ of [min(H0, H_ref,0), max(H1, H_ref,1)].
+// Outside it both R̂(H) and R0 equal the unit density to within
+// 4 ρ_max e^{-24} (the sigmoids saturate), so their G ΔR terms sum to
+// < 1e-9 λ_p(R0), below fp32 resolution of λ̂, and are skipped.
+__device__ __forceinline__ void vx_band(const VoxArgs &a, int c0, int c1, int lane, int &k_lo, int &k_hi) {
+  float lo = 3.0e38f, hi = -3.0e38f;
+  for (int c = c0 + lane; c < c1; c += 32) {
+    const float4 b = a.band[c];
+    lo = fminf(lo, b.x);
+    hi = fmaxf(hi, b.w);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  lo = fminf(lo, a.href_lo) - a.zc;
+  hi = fmaxf(hi, a.href_hi) + a.zc;
+  k_lo = 0;
+  k_hi = a.nz - 1;
+  if (lo == lo && hi == hi) {   // NaN heights: no skipping
+    k_lo = max(0, (int)floorf(lo / a.dz));
+    k_hi = min(a.nz - 1, (int)fminf(ceilf(hi / a.dz), 1.0e9f));
+  }
+}
+
 template <int VEC>
 __global__ void __launch_bounds__(MT_THREADS) k_vx_rhat_cl(VoxArgs a) {
-  const int lane = threadIdx.x & 31, node = blockIdx.x * VX_WARPS + (threadIdx.x >> 5), g = blockIdx.y;
+  const int lane = threadIdx.x & 31, node = blockIdx.x * VX_WARPS + (threadIdx.x >> 5), g = blockIdx.y + a.g0;
   if (node >= a.N) return;
+  int k_lo, k_hi;   // only the layers V2 / V3 read (vx_band)
+  vx_band(a, g * 32 * VEC, min(a.C, (g + 1) * 32 * VEC), lane, k_lo, k_hi);
   float H0[VEC], H1[VEC];
 #pragma unroll
   for (int u = 0; u < VEC; u++) {
@@ -145,7 +175,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_vx_rhat_cl(VoxArgs a) {
   }
   float *out = a.dR + (((size_t)g * a.ng + (size_t)node * a.nz) * 32 + lane) * VEC;
   const float *r0 = a.R0 + (size_t)node * a.nz;
-  for (int k = 0; k < a.nz; k++) {
+  for (int k = k_lo; k <= k_hi; k++) {
     const float z = k * a.dz, rk = r0[k];
     float d[VEC];
 #pragma unroll
@@ -198,33 +228,6 @@ __device__ __forceinline__ int gather_dot(const int2 *e, int64_t beg, int64_t en
   return kept;
 }
 
-// Layers k whose ΔR_v or ∂R̂_v/∂H can exceed e^{-VX_ZC} (relative) for any chain
-// c in [c0, c1): z_k within VX_ZC γ of [min(H0, H_ref,0), max(H1, H_ref,1)].
-// Outside it both R̂(H) and R0 equal the unit density to within
-// 4 ρ_max e^{-24} (the sigmoids saturate), so their G ΔR terms sum to
-// < 1e-9 λ_p(R0), below fp32 resolution of λ̂, and are skipped.
-__device__ __forceinline__ void vx_band(const VoxArgs &a, int c0, int c1, int lane, int &k_lo, int &k_hi) {
-  float lo = 3.0e38f, hi = -3.0e38f;
-  for (int c = c0 + lane; c < c1; c += 32) {
-    const float4 b = a.band[c];
-    lo = fminf(lo, b.x);
-    hi = fmaxf(hi, b.w);
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-    hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-  }
-  lo = fminf(lo, a.href_lo) - a.zc;
-  hi = fmaxf(hi, a.href_hi) + a.zc;
-  k_lo = 0;
-  k_hi = a.nz - 1;
-  if (lo == lo && hi == hi) {   // NaN heights: no skipping
-    k_lo = max(0, (int)floorf(lo / a.dz));
-    k_hi = min(a.nz - 1, (int)fminf(ceilf(hi / a.dz), 1.0e9f));
-  }
-}
-
 // The sub-range of row p that can hold layers [k_lo, k_hi]: entries of a row
 // are in path order and z grows along every ray (d_z > 0), so its layers are
 // non-decreasing; the per-row bucket offsets bound the in-band run.
@@ -257,7 +260,7 @@ __device__ __forceinline__ void flush_ll(const double (&mine)[VEC], int lane, in
 
 template <int VEC>
 __global__ void __launch_bounds__(MT_THREADS) k_vx_fwd_cl(VoxArgs a) {
-  const int lane = threadIdx.x & 31, g = blockIdx.y;
+  const int lane = threadIdx.x & 31, g = blockIdx.y + a.g0;
   const int64_t p0 = ((int64_t)blockIdx.x * VX_WARPS + (threadIdx.x >> 5)) * a.rpw;
   const char *src = (const char *)(a.dR + ((size_t)g * a.ng * 32 + lane) * VEC);
   float *rout = a.r + ((size_t)g * a.R * 32 + lane) * VEC;
@@ -302,7 +305,7 @@ __device__ __forceinline__ void vx_factors(const VoxArgs &a, float H0, float H1,
 
 template <int VEC>
 __global__ void __launch_bounds__(MT_THREADS) k_vx_bwd_cl(VoxArgs a) {
-  const int lane = threadIdx.x & 31, g = blockIdx.y;
+  const int lane = threadIdx.x & 31, g = blockIdx.y + a.g0;
   const int64_t w = (int64_t)blockIdx.x * VX_WARPS + (threadIdx.x >> 5);
   __shared__ int4 bufs[VX_WARPS][16];
   if (w >= a.n_items) return;
@@ -639,6 +642,8 @@ cudaError_t voxel_setup(mt_problem *p, int nz, float gamma, float tau, const flo
   s.nz = nz; s.gamma = gamma; s.tau = tau; s.nnz = nnz; s.ng = ng;
   s.rpw_cl = VX_RPW_CL;
   s.vec = 0;
+  s.gchunk = 0;
+  if (const char *ev = getenv("MT_VX_GCHUNK")) s.gchunk = atoi(ev);
   if (const char *ev = getenv("MT_VX_VEC")) s.vec = atoi(ev) >= 4 ? 4 : (atoi(ev) >= 2 ? 2 : 1);
   s.rpw_rl = VX_RPW_RL;
   if (const char *ev = getenv("MT_VX_RPW")) s.rpw_cl = s.rpw_rl = std::max(1, atoi(ev));
@@ -696,6 +701,7 @@ cudaError_t launch_voxel(mt_problem *p, int C, const float *H, const float4 *ban
   a.href_lo = v.href_lo; a.href_hi = v.href_hi;
   a.zc = VX_ZC * v.gamma;
   a.gathered = p->timing ? v.gathered : nullptr;
+  a.g0 = 0;
   const bool rec = p->timing && p->n_rec < (int)p->ev_a.size();
   const unsigned nb_nodes = (unsigned)((p->N + VX_WARPS - 1) / VX_WARPS);
   const unsigned nb_bwd = (unsigned)std::max<int64_t>(1, (v.n_items + VX_WARPS - 1) / VX_WARPS);
@@ -707,11 +713,19 @@ cudaError_t launch_voxel(mt_problem *p, int C, const float *H, const float4 *ban
     a.rpw = p->vx.rpw_cl;
     const int64_t rpb = (int64_t)VX_WARPS * a.rpw;
     const unsigned nb_rays = (unsigned)((p->R + rpb - 1) / rpb);
-#define VX_LAUNCH_CL(V)                                                                      \
-    k_vx_rhat_cl<V><<<dim3(nb_nodes, groups), MT_THREADS, 0, s>>>(a);                       \
-    if (p->R > 0) k_vx_fwd_cl<V><<<dim3(nb_rays, groups), MT_THREADS, 0, s>>>(a);          \
-    if (rec) cudaEventRecord(p->ev_m[p->n_rec], s);                                          \
-    k_vx_bwd_cl<V><<<dim3(nb_bwd, groups), MT_THREADS, 0, s>>>(a);
+    // group chunks: V1-V3 of `gc` groups back to back, so a chunk's ΔR and r are
+    // still in L2 when V2 / V3 read them (gc = 0: all groups in one launch each)
+    const int gc = p->vx.gchunk > 0 ? p->vx.gchunk : (int)groups;
+#define VX_LAUNCH_CL(V)                                                                         \
+    for (int g0 = 0; g0 < (int)groups; g0 += gc) {                                              \
+      const unsigned ng_ = (unsigned)std::min(gc, (int)groups - g0);                            \
+      a.g0 = g0;                                                                                \
+      k_vx_rhat_cl<V><<<dim3(nb_nodes, ng_), MT_THREADS, 0, s>>>(a);                            \
+      if (p->R > 0) k_vx_fwd_cl<V><<<dim3(nb_rays, ng_), MT_THREADS, 0, s>>>(a);               \
+      k_vx_bwd_cl<V><<<dim3(nb_bwd, ng_), MT_THREADS, 0, s>>>(a);                               \
+      p->all_launches += 3;                                                                     \
+    }                                                                                           \
+    if (rec) cudaEventRecord(p->ev_m[p->n_rec], s);
     if (vec == 4) { VX_LAUNCH_CL(4) } else if (vec == 2) { VX_LAUNCH_CL(2) } else { VX_LAUNCH_CL(1) }
 #undef VX_LAUNCH_CL
   } else {
@@ -722,9 +736,9 @@ cudaError_t launch_voxel(mt_problem *p, int C, const float *H, const float4 *ban
     if (p->R > 0) k_vx_fwd_rl<<<(unsigned)((p->R + rpb - 1) / rpb), MT_THREADS, 0, s>>>(a);
     if (rec) cudaEventRecord(p->ev_m[p->n_rec], s);
     k_vx_bwd_rl<<<nb_bwd, MT_THREADS, 0, s>>>(a);
+    p->all_launches += 3;
   }
   if (rec) { cudaEventRecord(p->ev_b[p->n_rec], s); p->n_rec++; }
-  p->all_launches += 3;
   p->trace_launches++;
   p->pairs += (double)C * (double)p->R;
   return cudaGetLastError();
