@@ -109,6 +109,18 @@ def prior_surface(x: np.ndarray, r: float):
     return v, g
 
 
+def prior_draws(nx: int, ny: int, r: float, n: int, rng) -> np.ndarray:
+    """n draws of x ~ N(0, Q(r)^-1) on the n_x x n_y torus:
+    Q = F* diag(λ) F with λ_ab = 4 - 2r(cos 2πa/n_x + cos 2πb/n_y), so
+    x = Q^{-1/2} w = real(ifft2(fft2(w) / sqrt(λ))) for w ~ N(0, I).  -> [n][nx*ny]."""
+    a = np.arange(nx)[:, None]
+    b = np.arange(ny)[None, :]
+    lam = 4.0 - 2.0 * r * (np.cos(2 * math.pi * a / nx) + np.cos(2 * math.pi * b / ny))
+    w = rng.standard_normal((n, nx, ny))
+    x = np.real(np.fft.ifft2(np.fft.fft2(w) / np.sqrt(lam)))
+    return x.reshape(n, nx * ny)
+
+
 def philox4x32_10(ctr, key) -> np.ndarray:
     out = np.zeros(4, np.uint32)
     lib().or_philox4x32_10(np.asarray(ctr, np.uint32), np.asarray(key, np.uint32), out)

@@ -80,7 +80,7 @@ int check_chains(const mt_problem *p, int32_t C) {
 
 void free_all(mt_problem *p) {
   voxel_free(p);
-  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_trav_geo, p->d_rl_head, p->d_rl_code, p->d_rl_ovf, p->d_ovf_q, p->d_ovf_n, p->d_H, p->d_Hlo, p->d_Hc, p->d_cs, p->d_G,
+  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_trav_geo, p->d_rl_head, p->d_rl_code, p->d_rl_ovf, p->d_ovf_q, p->d_ovf_n, p->d_redo, p->d_H, p->d_Hlo, p->d_Hc, p->d_cs, p->d_G,
                   p->d_band, p->d_ll, p->d_x0, p->d_g0, p->d_mom, p->d_kin0, p->d_kin1, p->d_lp0};
   for (void *b : bufs)
     if (b) cudaFree(b);
@@ -173,6 +173,7 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   if (const char *e = getenv("MT_TRACE_K")) p->trace_k = atoi(e);
   if (const char *e = getenv("MT_TRACE_S")) p->trace_s = atoi(e);
   if (const char *e = getenv("MT_CHUNK")) p->chunk = atoi(e);
+  if (const char *e = getenv("MT_OVF_CAP")) p->ovf_cap = std::max(1, atoi(e));   // (tests: force the overflow path)
 
   // ---- per-ray constants in double (a0) ----
   std::vector<float4> ra(p->R), rb(p->R);
@@ -269,6 +270,8 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   ALLOC(p->d_lp0, sizeof(double) * MC);
   ALLOC(p->d_ovf_q, sizeof(float4) * (size_t)p->ovf_cap);
   ALLOC(p->d_ovf_n, sizeof(int) * 4);
+  const size_t redo_words = (MC * R + 31) / 32;
+  ALLOC(p->d_redo, sizeof(unsigned) * redo_words);
   ALLOC(p->d_cs, sizeof(double) * p->N);
 #undef ALLOC
   if (e != cudaSuccess) {
@@ -288,6 +291,7 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   if (e == cudaSuccess) e = cudaMemset(p->d_Hlo, 0, sizeof(float) * MC32 * P);
   if (e == cudaSuccess) e = cudaMemset(p->d_ll, 0, sizeof(double) * MC);
   if (e == cudaSuccess) e = cudaMemset(p->d_ovf_n, 0, sizeof(int) * 4);
+  if (e == cudaSuccess) e = cudaMemset(p->d_redo, 0, sizeof(unsigned) * redo_words);
   if (e == cudaSuccess) {   // torus spectrum table c_ab = 2(cos 2πa/n_x + cos 2πb/n_y) (sample_r)
     std::vector<double> cs(p->N);
     for (int a = 0; a < p->nx; a++)

@@ -72,6 +72,7 @@ struct TraceArgs {
   int *ovf_n, *ovf_done;        //   conditioned cell or > RCAP crossings), done by k_trace_defer
   unsigned long long *ovf_total;   // cumulative deferred pairs
   int ovf_cap;
+  unsigned *redo;               // [ceil(C R / 32)] pairs deferred after the queue filled
 };
 
 enum { TRACE_LL = 0, TRACE_PATH = 1 };
@@ -173,6 +174,7 @@ struct mt_problem {
   float4 *d_ovf_q = nullptr;    // deferred-pair queue of the chain-lanes trace (see TraceArgs)
   int *d_ovf_n = nullptr;       // [4]: count, blocks done, 64-bit cumulative count
   int ovf_cap = 1 << 22;
+  unsigned *d_redo = nullptr;   // (max_chains x R)-bit overflow bitmap of the deferred-pair queue
   int64_t trav_cells = 0;
   float *d_H = nullptr, *d_G = nullptr, *d_Hlo = nullptr;
   float *d_Hc = nullptr;        // [min(max_chains, 16)][2N] contiguous heights for the ray-lanes trace

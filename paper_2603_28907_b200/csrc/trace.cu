@@ -229,6 +229,12 @@ __device__ __forceinline__ bool solve32(float h00, float h10, float h01, float h
   const float g1 = b * al + c * be + e * (u0 * be + v0 * al) - dz;
   const float g2 = e * al * be;
   const float gL = g0 + Ls * (g1 + Ls * g2);
+  // |g| < 1 mm where the ray enters or leaves the cell: the surface passes within
+  // fp32 rounding of the cell edge, where the bilinear patches meet at a kink; the
+  // two cells' fp32 quadratics can then disagree on the sign there and invent (or
+  // lose) a crossing pair around a sliver of zero length whose adjoint terms add up.
+  // Decide it in fp64 (HP2), like a near-tangent vertex.
+  if (fabsf(g0) < ZTHR || fabsf(gL) < ZTHR) return false;
   const float disc = fmaf(g1, g1, -4.f * g2 * g0);
   const bool p0 = g0 > 0.f;
   const float a2 = 2.f * g2;
@@ -411,6 +417,12 @@ __device__ __forceinline__ int band_entry_warp(const int2 *__restrict__ cells, i
   return hi - 1;
 }
 
+// Queue overflow: mark pair (c, ray) in the (C x R)-bit redo bitmap.
+__device__ __forceinline__ void redo_mark(const TraceArgs &a, int c, int rr) {
+  const int64_t idx = (int64_t)c * a.R + rr;
+  atomicOr(a.redo + (idx >> 5), 1u << (idx & 31));
+}
+
 // Fused epilogue (a4-a5): t = ln(λ/C) (C > 0) or ln λ (C = 0) from the
 // per-ray constant t_base (HP4, R15); returns ℓ_p, sets ∂ℓ/∂O = (λ - C)/Λ.
 __device__ __forceinline__ float epilogue(float tb, float cnt, const TraceConsts &tc, float B0,
@@ -590,6 +602,7 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a
     if (defer || n0 > RCAP || n1 > RCAP) {             // rare: the whole pair goes to k_trace_defer
       const int q = atomicAdd(a.ovf_n, 1);
       if (q < a.ovf_cap) a.ovf_q[q] = make_float4(__int_as_float(c), __int_as_float(rr), s_lo, s_hi);
+      else redo_mark(a, c, rr);   // queue full: the follow-up kernel finds the pair in the bitmap
       continue;
     }
     if (MODE == TRACE_LL) {
@@ -652,15 +665,8 @@ __global__ void __launch_bounds__(MT_THREADS) k_trace_defer(TraceArgs a) {
   const int grp_g = (blockIdx.x * blockDim.x + threadIdx.x) / DG, ngrp = (gridDim.x * blockDim.x) / DG;
   int c_acc = -1;
   double ll_acc = 0.0;
-  // group-uniform loop (the whole warp keeps iterating until all its groups are done,
-  // so the full-warp shuffles below see every lane)
-  const int iters = (nq + ngrp - 1) / ngrp;
-  for (int it = 0; it < iters; it++) {
-    const int q = grp_g + it * ngrp;
-    if (q >= nq) continue;
-    const float4 e0 = a.ovf_q[q];
-    const int c = __float_as_int(e0.x), rr = __float_as_int(e0.y);
-    const float s_lo = e0.z, s_hi = e0.w;
+  // one pair per group of DG lanes (all shuffles / ballots below are group-masked)
+  auto process = [&](const int c, const int rr, const float s_lo, const float s_hi) {
     const Ray r = load_ray(a.ray_a, a.ray_b, rr);
     const size_t off = (size_t)(c >> 5) * 2 * N * 32 + (c & 31);
     const float *Hk = a.H + off, *Hl = a.Hlo + off;
@@ -763,11 +769,34 @@ __global__ void __launch_bounds__(MT_THREADS) k_trace_defer(TraceArgs a) {
       a.Lout[3 * o + 2] = r.s_exit - T1;
       a.Oout[o] = a.tc.k0 * T0 + a.tc.k1 * T1 + a.obase[rr];
     }
+  };
+  // the queued pairs (walk range as queued: the warp's union band)
+  for (int q = grp_g; q < nq; q += ngrp) {
+    const float4 e0 = a.ovf_q[q];
+    process(__float_as_int(e0.x), __float_as_int(e0.y), e0.z, e0.w);
+  }
+  // queue overflow: the pairs that did not fit are marked in the (C x R)-bit redo
+  // bitmap; walk range = the pair's own chain band (a subset of the union band
+  // the main kernel would have used: the same lengths up to rounding)
+  if (n > a.ovf_cap) {
+    const int64_t nw = ((int64_t)a.C * a.R + 31) / 32;
+    for (int64_t wi = grp_g; wi < nw; wi += ngrp) {
+      unsigned bits = a.redo[wi];
+      while (bits) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1u;
+        const int64_t idx = wi * 32 + b;
+        const int c = (int)(idx / a.R), rr = (int)(idx - (int64_t)c * a.R);
+        const float4 bd = a.band[c];
+        const float2 rb = __ldg(reinterpret_cast<const float2 *>(a.ray_b + rr));
+        process(c, rr, fminf(__fdividef(bd.x, rb.x) * (1.f - 1e-6f), rb.y),
+                fminf(__fdividef(bd.w, rb.x) * (1.f + 1e-6f), rb.y));
+      }
+      __syncwarp(gmask);
+      if (lane == 0 && a.redo[wi]) a.redo[wi] = 0u;
+    }
   }
   if (MODE == TRACE_LL && lane == 0 && c_acc >= 0) atomicAdd(a.ll + c_acc, ll_acc);
-  if (n > a.ovf_cap)   // queue overflow: fail loudly (non-finite log-likelihood -> status bit)
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.C; c += gridDim.x * blockDim.x)
-      a.ll[c] = __longlong_as_double(0x7ff8000000000000ll);
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -931,6 +960,7 @@ __global__ void __launch_bounds__(MT_THREADS, 4) k_trace_rl(TraceArgs a, const f
     if (defer || n0 > RCAP || n1 > RCAP) {             // rare: the whole pair goes to k_trace_defer
       const int q = atomicAdd(a.ovf_n, 1);
       if (q < a.ovf_cap) a.ovf_q[q] = make_float4(__int_as_float(c), __int_as_float(rr), s_lo, s_hi);
+      else redo_mark(a, c, rr);   // queue full: the follow-up kernel finds the pair in the bitmap
       continue;
     }
     if (MODE == TRACE_LL) {
@@ -991,6 +1021,7 @@ static TraceArgs base_trace_args(mt_problem *p) {
   a.perm = p->d_perm;
   a.R = p->R;
   a.ovf_q = p->d_ovf_q; a.ovf_n = p->d_ovf_n; a.ovf_done = p->d_ovf_n + 1; a.ovf_cap = p->ovf_cap;
+  a.redo = p->d_redo;
   a.ovf_total = reinterpret_cast<unsigned long long *>(p->d_ovf_n + 2);
   return a;
 }

@@ -225,6 +225,13 @@ def chain_states(x_true: np.ndarray, n_chains: int, seed: int, scale: float = 0.
     return (x_true.reshape(1, -1) + scale * xi[g]).astype(np.float32)
 
 
+def prior_states(name: str, n_chains: int) -> np.ndarray:
+    """fp32 [C][P] "prior-draw" chain states (wide active band, worst-case
+    work), tiled from data/<config>_prior.npz (written by tools/make_data.py via the oracle)."""
+    z = np.load(os.path.join(DATA_DIR, DATA_NAME[name] + "_prior.npz"))["x_prior"]
+    return np.ascontiguousarray(z[np.arange(n_chains) % len(z)], dtype=np.float32)
+
+
 def perturbed_heights(H: np.ndarray, n_chains: int, seed: int, scale: float = 1.0) -> np.ndarray:
     """fp32 height fields [C][2][n][n] = H + scale·N(0,1) m, kept ordered.
 

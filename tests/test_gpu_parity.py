@@ -173,6 +173,18 @@ def test_logpost_grad_chain_sharded_8192(gpu, oracle_problem):
     assert not fails, fails
 
 
+@pytest.mark.parametrize("name,C,chains", [("small", 64, None), ("medium", 1024, [0, 77, 1023])])
+def test_logpost_grad_prior_draw_states(gpu, oracle_problem, name, C, chains):
+    """The wide-band "prior-draw" chain states: heights spread over
+    the whole box, every in-box cell in the band, many crossings per ray."""
+    mp, op = gpu(name), oracle_problem(name)
+    x = inputs.prior_states(name, C)
+    logp, grad = mp.logpost_grad(torch.from_numpy(x).to(DEV))
+    sel = np.arange(C) if chains is None else np.array(chains)
+    fails = e2e_check(mp, op, x, sel, logp.cpu().numpy(), grad.cpu().numpy())
+    assert not fails, fails
+
+
 def test_logpost_grad_medium_bench_launch(gpu, oracle_problem):
     """Full Medium size, in the launch configuration bench.py times (1024 chains),
     compared on sampled chains the oracle computes one by one."""
@@ -576,3 +588,32 @@ def test_nuts_driver_runs_and_adapts(gpu, problems):
     d = sh.depth.cpu().numpy()
     assert d.min() >= 1 and d.max() <= 5
     assert torch.isfinite(sh.x).all() and torch.isfinite(sh.logp).all()
+
+
+def test_chain_shards_reproduce_the_unsharded_hmc_step(gpu, problems):
+    """Chain sharding (configs[3], §9): a rank's chains are a contiguous slice with
+    chain_offset = its first global id; Philox streams depend on the global id only,
+    so two 32-chain shards reproduce one 64-chain HMC step (up to the summation
+    order of the float atomics)."""
+    prob = problems("small")
+    cfg = inputs.CONFIGS["small"]
+    mp = gpu("small")
+    x0 = torch.from_numpy(inputs.chain_states(prob["x_true"], 64, cfg.seed)).to(DEV)
+    eps = torch.full((64,), sampling_eps("small"), dtype=torch.float32, device=DEV)
+    seed = inputs.philox_key(cfg)
+    xa = x0.clone()
+    lpa, ga = mp.logpost_grad(xa)
+    apa, acca = mp.hmc_step(xa, lpa, ga, eps, 10, seed, 3)
+    xb = x0.clone()
+    lpb, gb = mp.logpost_grad(xb)
+    aps, accs = [], []
+    for lo in (0, 32):
+        ap, acc = mp.hmc_step(xb[lo:lo + 32], lpb[lo:lo + 32], gb[lo:lo + 32], eps[lo:lo + 32], 10, seed, 3,
+                              chain_offset=lo)
+        aps.append(ap)
+        accs.append(acc)
+    apb, accb = torch.cat(aps), torch.cat(accs)
+    assert torch.allclose(apa, apb, rtol=0, atol=1e-3)
+    close = (apa - apb).abs() < 1e-4
+    assert torch.equal(acca[close], accb[close])
+    assert float((xa - xb).norm() / xa.norm()) < 1e-6

@@ -157,3 +157,18 @@ def test_heights_clamp_and_inverse(oracle_problem):
     H, _ = op.heights(xt)
     assert np.allclose(H, op.prob["H_true"], rtol=1e-12, atol=1e-9)
     assert np.allclose(op.latent_from_heights(H), xt, rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("nr,nc,r", [(4, 4, 0.8), (3, 5, 0.95)])
+def test_prior_draws_covariance(nr, nc, r):
+    """oracle.prior_draws (the prior-draw chain states of SURVEY §8(d.1)) has
+    covariance Q^-1 (dense numpy inverse of the definition) and E[xᵀQx] = N."""
+    rng = np.random.default_rng(17)
+    n = 200000
+    x = oracle.prior_draws(nr, nc, r, n, rng)
+    Qi = np.linalg.inv(dense_Q(nr, nc, r))
+    emp = x.T @ x / n
+    se = np.sqrt((Qi ** 2 + np.outer(np.diag(Qi), np.diag(Qi))) / n)   # MC s.e. of a Gaussian covariance
+    assert np.all(np.abs(emp - Qi) < 5 * se)
+    quad = np.einsum("ni,ij,nj->n", x, dense_Q(nr, nc, r), x)
+    assert abs(quad.mean() - nr * nc) < 5 * np.sqrt(2 * nr * nc / n)

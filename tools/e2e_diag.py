@@ -3,7 +3,7 @@ oracle from fp64 heights, and vs the oracle fed the fp32-rounded heights
 (the "heights are fp32 quantities" convention), to separate kernel error
 from the conditioning of fp32 height rounding (HP2).  Test infrastructure.
 
-  python tools/e2e_diag.py <config> [chain ...]
+  python tools/e2e_diag.py <config> [chain ...] [--prior]   (--prior: prior-draw states)
 """
 import json
 import os
@@ -25,12 +25,14 @@ def rel(a, b):
 
 def main():
     name = sys.argv[1]
-    chains = [int(c) for c in sys.argv[2:]] or [0]
+    prior = "--prior" in sys.argv
+    chains = [int(c) for c in sys.argv[2:] if c != "--prior"] or [0]
     cfg = inputs.CONFIGS[name]
     prob = inputs.make_problem(name)
     op = oracle.Problem(prob)
     mp = Problem(prob, device=0, max_chains=cfg.chains)
-    x = inputs.chain_states(prob["x_true"], cfg.chains, cfg.seed)
+    x = (inputs.prior_states(name, cfg.chains) if prior
+         else inputs.chain_states(prob["x_true"], cfg.chains, cfg.seed))
     lp, g = mp.logpost_grad(torch.from_numpy(x).cuda())
     g = g.cpu().numpy().astype(np.float64)
     ref = op.logpost_grad(x[chains].astype(np.float64))

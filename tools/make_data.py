@@ -42,7 +42,22 @@ def make(name: str):
           f"({os.path.getsize(out)} B)")
 
 
+def make_prior_states(name: str, n: int = 128):
+    """data/<config>_prior.npz: n chain states x = (x_0, x_1) drawn from the CAR prior
+    N(0, Q(r_l)^-1) by oracle.prior_draws — the wide-band "prior-draw" set of SURVEY
+    §8(d.1), used for worst-case work and parity far from the posterior."""
+    cfg = inputs.CONFIGS[name]
+    rng = np.random.default_rng(np.random.SeedSequence([cfg.seed, 99]))
+    x = np.concatenate([oracle.prior_draws(cfg.n, cfg.n, cfg.car_r[l], n, rng) for l in range(2)], axis=1)
+    out = os.path.join(inputs.DATA_DIR, name + "_prior.npz")
+    np.savez_compressed(out, x_prior=x.astype(np.float32))
+    print(f"{name}: {n} prior-draw states x[{x.min():.3f},{x.max():.3f}] -> {out} ({os.path.getsize(out)} B)")
+
+
 if __name__ == "__main__":
     names = sys.argv[1:] or ["tiny", "small", "medium", "ray_sharded"]
     for n in names:
-        make(n)
+        if n.endswith("_prior"):
+            make_prior_states(n[:-len("_prior")])
+        else:
+            make(n)

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("config", nargs="?", default="medium")
     ap.add_argument("--chains", type=int, default=None)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--prior", action="store_true", help="prior-draw chain states (worst-case band)")
     ap.add_argument("--voxel", type=int, default=0, help="n_z > 0: time the f3 voxel / linearised model")
     a = ap.parse_args()
     cfg = inputs.CONFIGS[a.config]
@@ -33,7 +34,8 @@ def main():
         t0 = time.time()
         pb.voxel_model(a.voxel, prob["H_true"])
         print("voxel setup", pb.voxel_info(), f"{time.time() - t0:.2f} s", flush=True)
-    x = torch.from_numpy(inputs.chain_states(prob["x_true"], C, cfg.seed)).cuda()
+    x = torch.from_numpy(inputs.prior_states(a.config, C) if a.prior
+                         else inputs.chain_states(prob["x_true"], C, cfg.seed)).cuda()
     lp, g = pb.logpost_grad(x)
     for _ in range(3):
         pb.logpost_grad(x, lp, g)
@@ -52,7 +54,7 @@ def main():
     work = json.load(open(os.path.join(ROOT, "data", "work_counts.json")))[inputs.DATA_NAME[a.config]]
     F = work["flops_per_pair"]
     pairs = C * pb.R
-    print(json.dumps({"config": a.config, "C": C, "R": pb.R, "K": os.environ.get("MT_TRACE_K", "auto"),
+    print(json.dumps({"config": a.config, "states": "prior" if a.prior else "near-posterior", "C": C, "R": pb.R, "K": os.environ.get("MT_TRACE_K", "auto"),
                       "S": os.environ.get("MT_TRACE_S", "auto"), "ms_per_eval": ms, "trace_ms": tr,
                       "trace_share": tr / ms, "defer_ms": cnt["defer_ms"] / a.reps,
                       "deferred_per_eval": cnt["deferred"] / (a.reps + 4), "lib": os.environ.get("MT_LIB", "default"), "evals_per_s": pairs / (ms * 1e-3),
