@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--max-depth", type=int, default=8, help="NUTS: 2^max_depth leaves cap (P:662-669)")
     ap.add_argument("--model", default="exact", choices=["exact", "voxel"],
                     help="exact bilinear tracing (north_star) or the paper's voxel/linearised model (f3)")
+    ap.add_argument("--states", default="posterior", choices=["posterior", "prior"],
+                    help="near-posterior chain starts (headline) or prior draws (wide band: worst-case work, "
+                         "SURVEY §8(d.1))")
     ap.add_argument("--nz", type=int, default=60, help="voxel model: layers (Δz = z_top/nz, reading R28)")
     ap.add_argument("--sample-r", action="store_true",
                     help="hierarchical CAR r_l (SURVEY §8(f) f2): two more parameters per chain")
@@ -226,6 +229,8 @@ def main():
             C = args.chains_total // ws
         offset = rank * C
         x0 = inputs.chain_states(prob["x_true"], C, cfg.seed, chain_offset=offset, super_size=8)
+        if args.states == "prior":
+            x0 = np.ascontiguousarray(np.roll(inputs.prior_states(args.workload, C + offset), -offset, axis=0)[:C])
         if args.sample_r:   # ρ_l = logit(r_l) started at the fixed-r value
             rho = np.log(np.asarray(cfg.car_r) / (1.0 - np.asarray(cfg.car_r)))
             x0 = np.concatenate([x0, np.broadcast_to(rho, (C, 2))], axis=1).astype(np.float32)
@@ -390,6 +395,8 @@ def main():
                        "rays_per_gpu": R, "params": P,
                        "leapfrog_steps": L, "parallelism": (f"ray-sharded x{ws}" if ray else f"chain-sharded x{ws}"),
                        "car_r": "sampled (f2)" if args.sample_r else "fixed",
+                       "states": ("prior draws (wide band, worst-case work)" if args.states == "prior"
+                                  else "near-posterior"),
                        "forward_model": (f"voxel/sigmoid/linearised (f3, P:242-390): n_z={args.nz}, gamma=1 m, "
                                          "R0 = R-hat(truth)") if voxel else "exact bilinear tracing (north_star)",
                        "phase": "sampling (fixed eps from the 100-iteration dual-averaging warm-up, "

@@ -533,6 +533,31 @@ __device__ __forceinline__ void cw_solve(float4 h, int w, float4 cg, float za, f
   if (!solve32(h00, h10, h01, h11, cg, za, Ls, dz, B, emit)) defer = 1;
 }
 
+// Second pass of a pair with more than RCAP crossings of a surface (dℓ/dO now
+// known): the same cell code, crossings m >= RCAP scattered directly (the
+// first RCAP were stored and scattered from the records).
+__device__ __forceinline__ void cw_scatter_surface(const float *__restrict__ Hg, unsigned off, int oy, float4 cg,
+                                                   float za, float zb, float Ls, float dz, float zmin, float zmax,
+                                                   float *Gp, float f, int &m) {
+  if (zb <= zmin || za >= zmax) return;
+  const float *p = Hg + off;
+  const float h00 = __ldg(p), h01 = __ldg(p + 32), h10 = __ldg(p + oy), h11 = __ldg(p + oy + 32);
+  if (zb <= fminf(fminf(h00, h10), fminf(h01, h11))) return;
+  if (za >= fmaxf(fmaxf(h00, h10), fmaxf(h01, h11))) return;
+  float Bd = 0.f;
+  auto emit = [&](float u, float v, float ig) {
+    if (m >= RCAP) {
+      const float wv = f * ig;
+      atomicAdd(Gp, wv * (1.f - u) * (1.f - v));
+      atomicAdd(Gp + oy, wv * u * (1.f - v));
+      atomicAdd(Gp + 32, wv * (1.f - u) * v);
+      atomicAdd(Gp + oy + 32, wv * u * v);
+    }
+    m++;
+  };
+  solve32(h00, h10, h01, h11, cg, za, Ls, dz, Bd, emit);
+}
+
 template <int L>
 __device__ __forceinline__ void cw_surface(const float *__restrict__ Hg, unsigned off, int w, int oy,
                                            float4 cg, float za, float zb, float Ls, float dz, float zmin,
@@ -599,21 +624,24 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a
         ds = 0.f;
       }
     }
-    if (defer || n0 > RCAP || n1 > RCAP) {             // rare: the whole pair goes to k_trace_defer
+    // an ill-conditioned cell: the whole pair goes to k_trace_defer (fp64 re-solve)
+    if (defer) {
       const int q = atomicAdd(a.ovf_n, 1);
       if (q < a.ovf_cap) a.ovf_q[q] = make_float4(__int_as_float(c), __int_as_float(rr), s_lo, s_hi);
       else redo_mark(a, c, rr);   // queue full: the follow-up kernel finds the pair in the bitmap
-      continue;
     }
     if (MODE == TRACE_LL) {
-      const float2 rb = __ldg(reinterpret_cast<const float2 *>(a.ray_b + rr) + 1);
-      float dldO;
-      const float ll = epilogue(rb.x, rb.y, a.tc, B0, B1, dldO);
-      if (act) {
+      const bool over = !defer && (n0 > RCAP || n1 > RCAP);   // more crossings than records
+      float f0 = 0.f, f1 = 0.f;
+      float *G0 = a.G + (size_t)grp * 2 * N * 32 + lane;
+      if (!defer && act) {
+        const float2 rb = __ldg(reinterpret_cast<const float2 *>(a.ray_b + rr) + 1);
+        float dldO;
+        const float ll = epilogue(rb.x, rb.y, a.tc, B0, B1, dldO);
         llacc += ll;
-        const float f0 = dldO * a.tc.k0, f1 = dldO * a.tc.k1;
-        float *G0 = a.G + (size_t)grp * 2 * N * 32 + lane;
-        for (int m = 0; m < n0; m++) {
+        f0 = dldO * a.tc.k0;
+        f1 = dldO * a.tc.k1;
+        for (int m = 0; m < min(n0, RCAP); m++) {
           const float4 q = rec[m * MT_THREADS];
           const float w = f0 * q.w, u = q.y, v = q.z;
           float *pg = G0 + ((unsigned)__float_as_int(q.x) << 5);
@@ -623,7 +651,7 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a
           atomicAdd(pg + oy + 32, w * u * v);
         }
         float *G1 = G0 + N * 32;
-        for (int m = 0; m < n1; m++) {
+        for (int m = 0; m < min(n1, RCAP); m++) {
           const float4 q = rec[(RCAP + m) * MT_THREADS];
           const float w = f1 * q.w, u = q.y, v = q.z;
           float *pg = G1 + ((unsigned)__float_as_int(q.x) << 5);
@@ -633,7 +661,31 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a
           atomicAdd(pg + oy + 32, w * u * v);
         }
       }
-    } else if (act) {
+      if (__any_sync(0xffffffffu, over)) {   // wide bands (e.g. prior draws): re-walk, scatter the rest
+        const int kend = __ldg(a.trav_off + rr + 1);
+        float s_in0;
+        const int k0 = band_entry_warp(a.trav, __ldg(a.trav_off + rr), kend, s_lo, s_in0);
+        float s = s_lo, za = s_lo * dz, ds = s_lo - s_in0;
+        int m0 = 0, m1 = 0;
+        for (int k = k0; k < kend; k++) {
+          const int2 w = __ldg(a.trav + k);
+          const float4 cg = shift_geo(__ldg(a.trav_geo + k), ds);
+          const float s1 = __int_as_float(w.y);
+          const float zb = s1 * dz, Ls = s1 - s;
+          if (over) {
+            const unsigned off = cell_off32(w.x) + gbase;
+            float *pg = G0 + ((unsigned)(cell_off32(w.x)));
+            if (n0 > RCAP) cw_scatter_surface(a.H, off, oy, cg, za, zb, Ls, dz, bd.x, bd.y, pg, f0, m0);
+            if (n1 > RCAP) cw_scatter_surface(a.H, off + N * 32, oy, cg, za, zb, Ls, dz, bd.z, bd.w,
+                                              pg + N * 32, f1, m1);
+          }
+          if (s1 >= s_hi) break;
+          s = s1;
+          za = zb;
+          ds = 0.f;
+        }
+      }
+    } else if (act && !defer) {
       const int64_t o = (int64_t)c * a.R + __ldg(a.perm + rr);
       a.Lout[3 * o + 0] = B0;
       a.Lout[3 * o + 1] = B1 - B0;
