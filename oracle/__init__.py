@@ -65,6 +65,8 @@ def lib():
                                       ct.c_void_p, _lp]
         L.or_torus_spectrum_dr.argtypes = [ct.c_int, ct.c_int, ct.c_double] + [ct.POINTER(ct.c_double)] * 4
         L.or_logpost_grad_r.argtypes = [ct.c_void_p, ct.c_int, _dp, _dp, _dp, _dp, _dp]
+        L.or_ncp_kernel.argtypes = [ct.c_int, ct.c_int, ct.c_double, _dp, _dp]
+        L.or_logpost_grad_ncp.argtypes = [ct.c_void_p, ct.c_int, _dp, _dp, _dp, _dp]
         L.or_voxel_path.restype = ct.c_int
         L.or_voxel_path.argtypes = [ct.c_void_p, ct.c_int, ct.c_long, _ip, _dp, ct.c_int]
         L.or_voxel_rhat.argtypes = [ct.c_void_p, ct.c_int, ct.c_double, _dp, ct.c_void_p, _dp]
@@ -119,6 +121,14 @@ def prior_draws(nx: int, ny: int, r: float, n: int, rng) -> np.ndarray:
     w = rng.standard_normal((n, nx, ny))
     x = np.real(np.fft.ifft2(np.fft.fft2(w) / np.sqrt(lam)))
     return x.reshape(n, nx * ny)
+
+
+def ncp_kernel(nx: int, ny: int, r: float):
+    """(k, dk/dr) [nx][ny]: kernels of the circulant U = Q(r)^{-1/2} and dU/dr."""
+    k = np.zeros(nx * ny)
+    dk = np.zeros(nx * ny)
+    lib().or_ncp_kernel(nx, ny, r, k, dk)
+    return k.reshape(nx, ny), dk.reshape(nx, ny)
 
 
 def philox4x32_10(ctr, key) -> np.ndarray:
@@ -291,6 +301,16 @@ class Problem:
                                     np.ascontiguousarray(Href, np.float64).reshape(-1), C, x, logp, g,
                                     ll, pr)
         return dict(logp=logp, grad=g, ll_dev=ll, prior=pr)
+
+    def logpost_grad_ncp(self, v: np.ndarray):
+        """Non-centred (f2): v [C][2N+2] = (z_0, z_1, ρ_0, ρ_1), x_l = U(r_l) z_l
+        -> dict(logp [C], grad [C][2N+2], ll_dev)."""
+        v = np.ascontiguousarray(v, np.float64).reshape(-1, self.P + 2)
+        C = v.shape[0]
+        logp, ll = np.zeros(C), np.zeros(C)
+        g = np.zeros_like(v)
+        lib().or_logpost_grad_ncp(self.h, C, v, logp, g, ll)
+        return dict(logp=logp, grad=g, ll_dev=ll)
 
     def loglik_offset(self) -> float:
         """Σ_p (C ln C - C - ln Γ(C+1)): ll_std - ll_dev (R15)."""

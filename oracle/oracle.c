@@ -635,6 +635,134 @@ void or_logpost_grad_r(const or_problem *p, int C, const double *v, double *logp
 }
 
 /* ------------------------------------------------------------------ */
+/* Non-centred CAR parameterisation x = U z (*/
+/* reading R13d in DESIGN.md)                                          */
+/* ------------------------------------------------------------------ */
+
+/* The square root U = Q(r)^{-1/2} of the torus CAR covariance: Q is circulant,
+ * Q = F* diag(λ) F with λ_ab = 4 - r c_ab, c_ab = 2(cos 2πa/n_x + cos 2πb/n_y), so
+ * U is the circulant with kernel k[d] = N^{-1} Σ_ab λ_ab^{-1/2} cos 2π(a d_i/n_x + b d_j/n_y)
+ * (x_i = Σ_j k[i - j] z_j; UUᵀ = U² = Q^{-1} = Σ, as P:576-582 require), and
+ * dk/dr the kernel of dU/dr (eigenvalues ½ c λ^{-3/2}).  Direct sums. */
+void or_ncp_kernel(int nx, int ny, double r, double *k, double *dk) {
+  int N = nx * ny;
+  for (int di = 0; di < nx; di++)
+    for (int dj = 0; dj < ny; dj++) {
+      double s = 0.0, ds = 0.0;
+      for (int a = 0; a < nx; a++)
+        for (int b = 0; b < ny; b++) {
+          double c = 2.0 * (cos(2.0 * OR_PI * a / nx) + cos(2.0 * OR_PI * b / ny));
+          double lam = 4.0 - r * c;
+          double ph = cos(2.0 * OR_PI * ((double)a * di / nx + (double)b * dj / ny));
+          s += ph / sqrt(lam);
+          ds += ph * 0.5 * c / (lam * sqrt(lam));
+        }
+      k[di * ny + dj] = s / N;
+      if (dk) dk[di * ny + dj] = ds / N;
+    }
+}
+
+/* y = (circulant with kernel k) v on the torus: y_i = Σ_j k[i - j] v_j. */
+static void circ_apply(int nx, int ny, const double *k, const double *v, double *y) {
+  for (int i = 0; i < nx; i++)
+    for (int j = 0; j < ny; j++) {
+      double s = 0.0;
+      for (int i2 = 0; i2 < nx; i2++)
+        for (int j2 = 0; j2 < ny; j2++) {
+          int di = (i - i2 + nx) % nx, dj = (j - j2 + ny) % ny;
+          s += k[di * ny + dj] * v[i2 * ny + j2];
+        }
+      y[i * ny + j] = s;
+    }
+}
+
+/* Log-posterior and gradient in the non-centred parameters v [C][2N + 2] =
+ * (z_0, z_1, ρ_0, ρ_1): z_l ~ N(0, I), r_l = logistic(ρ_l) with r_l ~ Unif(0,1)
+ * (R13b), x_l = U(r_l) z_l, heights ǔ = Φ(x/σ(r)):
+ *   logp = ll(H(x)) - ½ Σ_l |z_l|² - N ln 2π + Σ_l [ln r_l + ln(1 - r_l)],
+ *   ∂/∂z_l = -z_l + U ∂ll/∂x_l   (U symmetric),
+ *   ∂/∂ρ_l = r(1-r) [(∂ll/∂x_l)ᵀ (dU/dr) z_l + (∂ll/∂σ_l) dσ_l/dr] + 1 - 2r,
+ * with ∂ll/∂x the likelihood part only (the prior is the standard normal on z). */
+void or_logpost_grad_ncp(const or_problem *p, int C, const double *v, double *logp, double *grad,
+                         double *ll_out) {
+  int N = p->nx * p->ny, P = 2 * N + 2;
+  double *H = (double *)malloc(sizeof(double) * (size_t)C * 2 * N);
+  double *aux = (double *)malloc(sizeof(double) * (size_t)C * 5 * N);   /* dH/dx (3N), dH/dσ (2N) */
+  double *X = (double *)malloc(sizeof(double) * (size_t)C * 2 * N);
+  double *G = (double *)malloc(sizeof(double) * (size_t)C * 2 * N);
+  double *ll = (double *)malloc(sizeof(double) * C);
+  double *kk = (double *)malloc(sizeof(double) * (size_t)C * 4 * N);    /* k, dk per surface */
+  double *rr = (double *)malloc(sizeof(double) * C * 2), *dsg = (double *)malloc(sizeof(double) * C * 2);
+  for (int c = 0; c < C; c++) {
+    const double *vc = v + (long)c * P;
+    double sg[2];
+    for (int l = 0; l < 2; l++) {
+      double r = 1.0 / (1.0 + exp(-vc[2 * N + l])), ld, dld;
+      rr[2 * c + l] = r;
+      or_torus_spectrum_dr(p->nx, p->ny, r, &sg[l], &dsg[2 * c + l], &ld, &dld);
+      double *k = kk + (long)c * 4 * N + 2 * l * N;
+      or_ncp_kernel(p->nx, p->ny, r, k, k + N);
+      circ_apply(p->nx, p->ny, k, vc + l * N, X + (long)c * 2 * N + l * N);
+    }
+    const double *xc = X + (long)c * 2 * N;
+    double *Hc = H + (long)c * 2 * N, *dx = aux + (long)c * 5 * N, *ds = dx + 3 * N;
+    for (int q = 0; q < N; q++) {
+      double u[2], dudx[2], duds[2];
+      for (int l = 0; l < 2; l++) {
+        double tt = xc[l * N + q] / sg[l];
+        int clamped = 0;
+        if (tt > OR_TCLAMP) { tt = OR_TCLAMP; clamped = 1; }
+        if (tt < -OR_TCLAMP) { tt = -OR_TCLAMP; clamped = 1; }
+        u[l] = 0.5 * erfc(-tt / sqrt(2.0));
+        double phi = clamped ? 0.0 : exp(-0.5 * tt * tt) / sqrt(2.0 * OR_PI);
+        dudx[l] = phi / sg[l];
+        duds[l] = -tt * phi / sg[l];
+      }
+      double H0 = u[0] * p->z_top, H1 = (1.0 - u[1]) * H0 + u[1] * p->z_top;
+      Hc[q] = H0;
+      Hc[N + q] = H1;
+      dx[q] = p->z_top * dudx[0];
+      dx[N + q] = (1.0 - u[1]) * p->z_top * dudx[0];
+      dx[2 * N + q] = (p->z_top - H0) * dudx[1];
+      ds[q] = p->z_top * duds[0];
+      ds[N + q] = (p->z_top - H0) * duds[1];
+    }
+  }
+  or_loglik_grad_H(p, C, H, ll, NULL, G, NULL, NULL);
+  double *gx = (double *)malloc(sizeof(double) * 2 * N), *tmp = (double *)malloc(sizeof(double) * N);
+  for (int c = 0; c < C; c++) {
+    const double *vc = v + (long)c * P, *Gc = G + (long)c * 2 * N, *Hc = H + (long)c * 2 * N;
+    const double *dx = aux + (long)c * 5 * N, *ds = dx + 3 * N;
+    double *gc = grad + (long)c * P;
+    double dll_ds[2] = {0.0, 0.0}, zz = 0.0;
+    for (int q = 0; q < N; q++) {
+      gx[q] = Gc[q] * dx[q] + Gc[N + q] * dx[N + q];
+      gx[N + q] = Gc[N + q] * dx[2 * N + q];
+      double u1 = (Hc[N + q] - Hc[q]) / (p->z_top - Hc[q]);
+      dll_ds[0] += Gc[q] * ds[q] + Gc[N + q] * (1.0 - u1) * ds[q];
+      dll_ds[1] += Gc[N + q] * ds[N + q];
+    }
+    double lp = ll[c];
+    for (int l = 0; l < 2; l++) {
+      const double *k = kk + (long)c * 4 * N + 2 * l * N, *dk = k + N, *z = vc + l * N;
+      circ_apply(p->nx, p->ny, k, gx + l * N, tmp);                  /* U ∂ll/∂x */
+      for (int q = 0; q < N; q++) { gc[l * N + q] = -z[q] + tmp[q]; zz += z[q] * z[q]; }
+      circ_apply(p->nx, p->ny, dk, z, tmp);                          /* (dU/dr) z */
+      double s = 0.0;
+      for (int q = 0; q < N; q++) s += gx[l * N + q] * tmp[q];
+      double r = rr[2 * c + l];
+      gc[2 * N + l] = r * (1.0 - r) * (s + dll_ds[l] * dsg[2 * c + l]) + 1.0 - 2.0 * r;
+      lp += log(r) + log(1.0 - r);
+    }
+    lp += -0.5 * zz - N * log(2.0 * OR_PI);
+    logp[c] = lp;
+    if (ll_out) ll_out[c] = ll[c];
+  }
+  free(gx); free(tmp);
+  free(H); free(aux); free(X); free(G); free(ll); free(kk); free(rr); free(dsg);
+}
+
+/* ------------------------------------------------------------------ */
 /* The paper's voxel / sigmoid / linearised forward model (P:242-390,  */
 /* SURVEY §8(f) f3; reading R28 in DESIGN.md)                          */
 /* ------------------------------------------------------------------ */
