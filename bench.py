@@ -51,6 +51,8 @@ def parse():
                     help="near-posterior chain starts (headline) or prior draws (wide band: worst-case work, "
                          "SURVEY §8(d.1))")
     ap.add_argument("--nz", type=int, default=60, help="voxel model: layers (Δz = z_top/nz, reading R28)")
+    ap.add_argument("--noncentred", action="store_true",
+                    help="non-centred prior x = Q(r)^-1/2 z with sampled r (f2, P:570-584; implies --sample-r)")
     ap.add_argument("--sample-r", action="store_true",
                     help="hierarchical CAR r_l (SURVEY §8(f) f2): two more parameters per chain")
     ap.add_argument("--chains-total", type=int, default=8192)     # configs[3]
@@ -231,10 +233,13 @@ def main():
         x0 = inputs.chain_states(prob["x_true"], C, cfg.seed, chain_offset=offset, super_size=8)
         if args.states == "prior":
             x0 = np.ascontiguousarray(np.roll(inputs.prior_states(args.workload, C + offset), -offset, axis=0)[:C])
-        if args.sample_r:   # ρ_l = logit(r_l) started at the fixed-r value
-            rho = np.log(np.asarray(cfg.car_r) / (1.0 - np.asarray(cfg.car_r)))
+        rho = np.log(np.asarray(cfg.car_r) / (1.0 - np.asarray(cfg.car_r)))
+        if args.noncentred:   # z = Q(r)^{1/2} x at the fixed-r value of ρ
+            from paper_2603_28907_b200.hmc import noncentred_state
+            x0 = noncentred_state(x0, rho, cfg.n, cfg.n)
+        elif args.sample_r:   # ρ_l = logit(r_l) started at the fixed-r value
             x0 = np.concatenate([x0, np.broadcast_to(rho, (C, 2))], axis=1).astype(np.float32)
-        pb = Problem(prob, device=local, max_chains=C, sample_r=args.sample_r)
+        pb = Problem(prob, device=local, max_chains=C, sample_r=args.sample_r, noncentred=args.noncentred)
         R_total = pb.R * ws   # (chain sharding: every rank traces all rays of its chains)
         shard = ChainShard(pb, x0, seed=inputs.philox_key(cfg), L=L, eps0=eps, chain_offset=offset,
                            n_chains_total=C * ws, sampler=args.sampler, max_depth=args.max_depth)
@@ -394,7 +399,8 @@ def main():
                        "chains_per_gpu": C, "global_chains": C if ray else C * ws, "rays": R_total if ray else R,
                        "rays_per_gpu": R, "params": P,
                        "leapfrog_steps": L, "parallelism": (f"ray-sharded x{ws}" if ray else f"chain-sharded x{ws}"),
-                       "car_r": "sampled (f2)" if args.sample_r else "fixed",
+                       "car_r": ("sampled, non-centred x = Q(r)^-1/2 z (f2)" if args.noncentred
+                                 else "sampled (f2)" if args.sample_r else "fixed"),
                        "states": ("prior draws (wide band, worst-case work)" if args.states == "prior"
                                   else "near-posterior"),
                        "forward_model": (f"voxel/sigmoid/linearised (f3, P:242-390): n_z={args.nz}, gamma=1 m, "

@@ -86,6 +86,11 @@ typedef struct {
                                 (SURVEY §8(f) f2): each chain's state gains two
                                 parameters ρ_0, ρ_1 with r_l = 1/(1+e^{-ρ_l}) ~ Unif(0,1); the
                                 prior, σ_l and ln det Q_l then follow each chain's r_l (car_r unused) */
+  int32_t noncentred;        /* 1 (requires sample_r): the paper's non-centred parameterisation
+                                (R13d): the state is (z_0, z_1, ρ_0, ρ_1) with
+                                z_l ~ N(0, I) and x_l = Q(r_l)^{-1/2} z_l (the symmetric root, applied
+                                as a circulant by the 2-D DFT in fp64); logp = ll - ½|z|² - N ln 2π
+                                + Σ ln r_l(1-r_l).  mt_nuts_step is not available in this mode. */
 } mt_problem_desc;
 
 /* Validate the description, precompute per-ray constants (in-box extent,

@@ -35,6 +35,7 @@ class _Desc(ct.Structure):
         ("ray_w", ct.c_void_p), ("counts", ct.c_void_p),
         ("ray_lo", ct.c_int64), ("ray_hi", ct.c_int64),
         ("device", ct.c_int32), ("max_chains", ct.c_int32), ("sample_r", ct.c_int32),
+        ("noncentred", ct.c_int32),
     ]
 
 
@@ -136,7 +137,8 @@ class Problem:
     """A canonical problem bound to one CUDA device (mt_problem_create)."""
 
     def __init__(self, prob: dict, device: int = 0, max_chains: int = 1,
-                 ray_lo: int = 0, ray_hi: Optional[int] = None, sample_r: bool = False):
+                 ray_lo: int = 0, ray_hi: Optional[int] = None, sample_r: bool = False,
+                 noncentred: bool = False):
         self._keep = {
             "node_x": np.ascontiguousarray(prob["node_x"], np.float32),
             "node_y": np.ascontiguousarray(prob["node_y"], np.float32),
@@ -165,7 +167,8 @@ class Problem:
         d.ray_hi = R if ray_hi is None else ray_hi
         d.device = device
         d.max_chains = max_chains
-        d.sample_r = 1 if sample_r else 0
+        d.sample_r = 1 if (sample_r or noncentred) else 0
+        d.noncentred = 1 if noncentred else 0
         h = ct.c_void_p()
         _check(lib().mt_problem_create(ct.byref(d), ct.byref(h)), "mt_problem_create")
         self.h = h

@@ -80,7 +80,7 @@ int check_chains(const mt_problem *p, int32_t C) {
 
 void free_all(mt_problem *p) {
   voxel_free(p);
-  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_trav_geo, p->d_rl_head, p->d_rl_code, p->d_rl_ovf, p->d_ovf_q, p->d_ovf_n, p->d_redo, p->d_H, p->d_Hlo, p->d_Hc, p->d_cs, p->d_G,
+  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_trav_geo, p->d_rl_head, p->d_rl_code, p->d_rl_ovf, p->d_ovf_q, p->d_ovf_n, p->d_redo, p->d_H, p->d_Hlo, p->d_Hc, p->d_cs, p->d_xw, p->d_G,
                   p->d_band, p->d_ll, p->d_x0, p->d_g0, p->d_mom, p->d_kin0, p->d_kin1, p->d_lp0};
   for (void *b : bufs)
     if (b) cudaFree(b);
@@ -138,6 +138,7 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   if (d->ray_lo < 0 || d->ray_hi < d->ray_lo || d->ray_hi > d->n_rays)
     return set_err(MT_EINVAL, "ray shard [%lld, %lld) invalid", (long long)d->ray_lo, (long long)d->ray_hi);
   if (d->max_chains < 0) return set_err(MT_EINVAL, "max_chains < 0");
+  if (d->noncentred && !d->sample_r) return set_err(MT_EINVAL, "noncentred requires sample_r");
   for (int64_t q = d->ray_lo; q < d->ray_hi; q++) {
     if (d->ray_det[q] < 0 || d->ray_det[q] >= d->n_det) return set_err(MT_EINVAL, "ray_det[%lld] out of range", (long long)q);
     const float *v = d->ray_dir + 3 * q;
@@ -157,6 +158,7 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   p->device = d->device;
   cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, d->device);
   p->sample_r = d->sample_r ? 1 : 0;
+  p->ncp = d->noncentred ? 1 : 0;
   p->nx = d->n_x; p->ny = d->n_y; p->N = d->n_x * d->n_y; p->P = 2 * p->N + 2 * p->sample_r;
   p->R = d->ray_hi - d->ray_lo;
   p->ray_lo = d->ray_lo;
@@ -273,6 +275,7 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   const size_t redo_words = (MC * R + 31) / 32;
   ALLOC(p->d_redo, sizeof(unsigned) * redo_words);
   ALLOC(p->d_cs, sizeof(double) * p->N);
+  if (p->ncp) ALLOC(p->d_xw, sizeof(double) * MC * 2 * p->N);
 #undef ALLOC
   if (e != cudaSuccess) {
     free_all(p);
@@ -337,6 +340,7 @@ static int eval_sharded(mt_problem *p, int C, float *x, double *logp, float *gra
                         cudaStream_t s) {
   CK(launch_trace(p, TRACE_LL, C, p->d_H, p->d_band, p->d_G, p->d_ll, nullptr, nullptr, s));
   CK(launch_finish(p, FIN_PLAIN, C, x, grad, logp, status, nullptr, nullptr, nullptr, s));
+  if (!p->comm) return MT_OK;   // (the non-centred mode uses this unfused path on one shard too)
   std::string why;
   if (comm_allreduce_logp_grad(p, C, logp, grad, s, why) != cudaSuccess)
     return set_err(MT_ENCCL, "ncclAllReduce: %s", why.c_str());
@@ -351,7 +355,7 @@ int mt_logpost_grad(mt_problem *p, int32_t C, const float *x, double *logp, floa
   DevGuard g(p->device);
   cudaStream_t s = (cudaStream_t)stream;
   CK(launch_heights(p, C, x, p->d_H, p->d_band, s));
-  if (p->comm) return eval_sharded(p, C, const_cast<float *>(x), logp, grad, status, s);
+  if (p->comm || p->ncp) return eval_sharded(p, C, const_cast<float *>(x), logp, grad, status, s);
   CK(launch_trace(p, TRACE_LL, C, p->d_H, p->d_band, p->d_G, p->d_ll, nullptr, nullptr, s));
   CK(launch_finish(p, FIN_PLAIN, C, const_cast<float *>(x), grad, logp, status, nullptr, nullptr,
                    nullptr, s));
@@ -381,7 +385,7 @@ int mt_leapfrog(mt_problem *p, int32_t C, float *x, float *mom, double *logp, fl
   DevGuard g(p->device);
   cudaStream_t s = (cudaStream_t)stream;
   CK(launch_kick_drift(p, C, x, mom, grad, eps, s));
-  if (p->comm) return leapfrog_sharded(p, C, x, mom, logp, grad, nullptr, eps, L, s);
+  if (p->comm || p->ncp) return leapfrog_sharded(p, C, x, mom, logp, grad, nullptr, eps, L, s);
   for (int step = 1; step <= L; step++) {
     CK(launch_trace(p, TRACE_LL, C, p->d_H, p->d_band, p->d_G, p->d_ll, nullptr, nullptr, s));
     CK(launch_finish(p, step < L ? FIN_STEP : FIN_LAST, C, x, grad, logp, nullptr, mom, eps,
@@ -412,7 +416,7 @@ int mt_hmc_step(mt_problem *p, int32_t C, float *x, double *logp, float *grad, c
   DevGuard g(p->device);
   cudaStream_t s = (cudaStream_t)stream;
   CK(launch_hmc_begin(p, C, x, logp, grad, eps, seed, iter, chain_offset, s));
-  if (p->comm) {
+  if (p->comm || p->ncp) {
     if (int r = leapfrog_sharded(p, C, x, p->d_mom, logp, grad, status, eps, L, s)) return r;
     CK(launch_hmc_end(p, C, x, logp, grad, seed, iter, chain_offset, accept_prob, accepted, status, s));
     return MT_OK;
@@ -430,6 +434,7 @@ int mt_nuts_step(mt_problem *p, int32_t C, float *x, double *logp, float *grad, 
                  int32_t max_depth, uint64_t seed, uint64_t iter, uint64_t chain_offset, float *accept_stat,
                  int32_t *depth, int32_t *n_leaves, int32_t *status, mt_stream stream) {
   if (int r = check_chains(p, C)) return r;
+  if (p->ncp) return set_err(MT_EINVAL, "mt_nuts_step: not available with noncentred");
   if (max_depth < 1 || max_depth > MT_NUTS_MAX_DEPTH)
     return set_err(MT_EINVAL, "max_depth = %d not in [1, %d]", max_depth, MT_NUTS_MAX_DEPTH);
   if (C == 0) return MT_OK;

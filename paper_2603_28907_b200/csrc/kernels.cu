@@ -24,10 +24,10 @@ struct NodeH {
 
 // Gaussian copula + stick-breaking: ǔ = Φ(clamp(x/σ)),
 // H0 = ǔ0 z_top, H1 = H0 + ǔ1 (z_top - H0).  fp64 internally (HP2 lever 2).
-__device__ __forceinline__ NodeH node_heights(float x0, float x1, double is0, double is1,
+__device__ __forceinline__ NodeH node_heights(double x0, double x1, double is0, double is1,
                                               float z_top, bool want_jac) {
   NodeH o;
-  double t0 = (double)x0 * is0, t1 = (double)x1 * is1;
+  double t0 = x0 * is0, t1 = x1 * is1;
   bool c0 = fabs(t0) > kTClamp, c1 = fabs(t1) > kTClamp;
   t0 = fmin(fmax(t0, -kTClamp), kTClamp);
   t1 = fmin(fmax(t1, -kTClamp), kTClamp);
@@ -359,6 +359,14 @@ __global__ void __launch_bounds__(MT_THREADS) k_hmc_begin(FinishArgs a, const do
     }
   }
   __syncthreads();
+  if (a.ncp) {   // non-centred: k_ncp_heights follows
+    const BlockRed r = block_reduce(v);
+    if (threadIdx.x == 0) {
+      kin0[c] = (float)r.s0;
+      lp0[c] = logp[c];
+    }
+    return;
+  }
   double is0 = a.inv_sigma[0], is1 = a.inv_sigma[1];
   if (a.sample_r) {   // σ of the drifted ρ (f2)
     const Spec sp = block_spectrum(a.cs, N, xc[2 * N], xc[2 * N + 1], false);
@@ -925,8 +933,238 @@ __global__ void k_nuts_end(NutsArgs n, int C, float *accept_stat, int32_t *depth
 }
 
 // ---------------------------------------------------------------------------
+// Non-centred CAR prior (reading R13d): state
+// (z_0, z_1, ρ_0, ρ_1), x_l = U(r_l) z_l with U = Q(r_l)^{-1/2}, the symmetric
+// root of the torus CAR covariance, applied as a circulant by the 2-D DFT:
+// U = F⁻¹ diag(λ_ab^{-1/2}) F, dU/dr = F⁻¹ diag(½ c_ab λ_ab^{-3/2}) F,
+// λ_ab = 4 - r c_ab.  One block per chain; the DFT is separable (rows, then
+// columns), in fp64 (x feeds the heights map, HP2), with the twiddles and all
+// intermediates in shared memory: 4N doubles of work space.
+// ---------------------------------------------------------------------------
+struct Dft {
+  double *wre, *wim, *vre, *vim;    // [N] each
+  const double *tcx, *tsx, *tcy, *tsy;   // cos / sin (2π k / n) for the two axes
+  int nx, ny, N;
+};
+
+// y = S(v) for the circulant with eigenvalues s_ab = λ^{-1/2} (mode 0) or
+// ½ c λ^{-3/2} (mode 1); v(k) gives input element k (row-major [i][j]); the
+// result is left in d.vre (real part).  All threads of the block participate.
+template <class In>
+__device__ void circ_apply(const Dft &d, const double *cs, double r, int mode, In v) {
+  const int nx = d.nx, ny = d.ny, N = d.N;
+  for (int q = threadIdx.x; q < N; q += blockDim.x) {        // rows: T[i][b] = Σ_j v e^{-2πi bj/ny}
+    const int i = q / ny, b = q - i * ny;
+    double re = 0.0, im = 0.0;
+    int ph = 0;
+    for (int j = 0; j < ny; j++) {
+      const double x = v(i * ny + j);
+      re += x * d.tcy[ph];
+      im -= x * d.tsy[ph];
+      ph += b;
+      if (ph >= ny) ph -= ny;
+    }
+    d.wre[q] = re;
+    d.wim[q] = im;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < N; q += blockDim.x) {        // columns, scaled: V = s_ab Σ_i T e^{-2πi ai/nx}
+    const int a = q / ny, b = q - a * ny;
+    double re = 0.0, im = 0.0;
+    int ph = 0;
+    for (int i = 0; i < nx; i++) {
+      const double tr = d.wre[i * ny + b], ti = d.wim[i * ny + b], c = d.tcx[ph], s = d.tsx[ph];
+      re += tr * c + ti * s;
+      im += ti * c - tr * s;
+      ph += a;
+      if (ph >= nx) ph -= nx;
+    }
+    const double cab = cs[q], lam = 4.0 - r * cab;
+    const double sc = mode == 0 ? rsqrt(lam) : 0.5 * cab * rsqrt(lam) / lam;
+    d.vre[q] = re * sc;
+    d.vim[q] = im * sc;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < N; q += blockDim.x) {        // inverse columns
+    const int i = q / ny, b = q - i * ny;
+    double re = 0.0, im = 0.0;
+    int ph = 0;
+    for (int a = 0; a < nx; a++) {
+      const double vr = d.vre[a * ny + b], vi = d.vim[a * ny + b], c = d.tcx[ph], s = d.tsx[ph];
+      re += vr * c - vi * s;
+      im += vi * c + vr * s;
+      ph += i;
+      if (ph >= nx) ph -= nx;
+    }
+    d.wre[q] = re;
+    d.wim[q] = im;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < N; q += blockDim.x) {        // inverse rows, real part / N
+    const int i = q / ny, j = q - i * ny;
+    double re = 0.0;
+    int ph = 0;
+    for (int b = 0; b < ny; b++) {
+      re += d.wre[i * ny + b] * d.tcy[ph] - d.wim[i * ny + b] * d.tsy[ph];
+      ph += j;
+      if (ph >= ny) ph -= ny;
+    }
+    d.vre[q] = re / N;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ Dft dft_setup(double *sm, int nx, int ny) {
+  Dft d;
+  d.nx = nx; d.ny = ny; d.N = nx * ny;
+  d.wre = sm; d.wim = sm + d.N; d.vre = sm + 2 * d.N; d.vim = sm + 3 * d.N;
+  double *tw = sm + 4 * d.N;
+  for (int k = threadIdx.x; k < nx; k += blockDim.x) {
+    double sn, c;
+    sincospi(2.0 * k / nx, &sn, &c);
+    tw[k] = c;
+    tw[MT_MAX_AXIS + k] = sn;
+  }
+  for (int k = threadIdx.x; k < ny; k += blockDim.x) {
+    double sn, c;
+    sincospi(2.0 * k / ny, &sn, &c);
+    tw[2 * MT_MAX_AXIS + k] = c;
+    tw[3 * MT_MAX_AXIS + k] = sn;
+  }
+  d.tcx = tw; d.tsx = tw + MT_MAX_AXIS; d.tcy = tw + 2 * MT_MAX_AXIS; d.tsy = tw + 3 * MT_MAX_AXIS;
+  __syncthreads();
+  return d;
+}
+
+// K1 (non-centred): x_l = U(r_l) z_l (fp64, kept in a.xw for K3), heights, band.
+__global__ void __launch_bounds__(MT_THREADS) k_ncp_heights(FinishArgs a, const float *v) {
+  extern __shared__ double sm[];
+  const int c = blockIdx.x, N = a.N;
+  const float *vc = v + (size_t)c * a.P;
+  const Spec sp = block_spectrum(a.cs, N, vc[2 * N], vc[2 * N + 1], false);
+  const Dft d = dft_setup(sm, a.nx, a.ny);
+  double *xw = a.xw + (size_t)c * 2 * N;
+  for (int l = 0; l < 2; l++) {
+    const float *z = vc + l * N;
+    circ_apply(d, a.cs, sp.r[l], 0, [&](int k) { return (double)z[k]; });
+    for (int k = threadIdx.x; k < N; k += blockDim.x) xw[l * N + k] = d.vre[k];
+    __syncthreads();
+  }
+  BlockRed vr = {3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f, 0.0, 0.0, 0};
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    const NodeH h = node_heights(xw[k], xw[N + k], sp.inv_sigma[0], sp.inv_sigma[1], a.z_top, false);
+    a.H[tix(c, 0, k, N)] = h.H0;
+    a.H[tix(c, 1, k, N)] = h.H1;
+    a.Hlo[tix(c, 0, k, N)] = h.L0;
+    a.Hlo[tix(c, 1, k, N)] = h.L1;
+    vr.mn0 = fminf(vr.mn0, h.H0); vr.mx0 = fmaxf(vr.mx0, h.H0);
+    vr.mn1 = fminf(vr.mn1, h.H1); vr.mx1 = fmaxf(vr.mx1, h.H1);
+  }
+  const BlockRed r = block_reduce(vr);
+  if (threadIdx.x == 0) a.band[c] = make_float4(r.mn0, r.mx0, r.mn1, r.mx1);
+}
+
+// K3 (non-centred): ∂ll/∂x from ∂ll/∂H, then
+//   ∂/∂z_l = -z_l + U ∂ll/∂x_l,  ∂/∂ρ_l = r(1-r)[(∂ll/∂x_l)ᵀ (dU/dr) z_l + (∂ll/∂σ_l) dσ_l/dr] + 1 - 2r,
+//   logp = ll - ½|z|² - N ln 2π + Σ_l ln r_l(1 - r_l)   (prior terms on the prior-owning shard).
+__global__ void __launch_bounds__(MT_THREADS) k_ncp_finish(FinishArgs a) {
+  extern __shared__ double sm[];
+  const int c = blockIdx.x, N = a.N, P = a.P;
+  const float *vc = a.x + (size_t)c * P;
+  float *gc = a.grad + (size_t)c * P;
+  const Spec sp = block_spectrum(a.cs, N, vc[2 * N], vc[2 * N + 1], false);
+  double *gx = sm + 4 * N + 4 * MT_MAX_AXIS;   // [2N] ∂ll/∂x
+  const double *xw = a.xw + (size_t)c * 2 * N;
+  float *Gt = const_cast<float *>(a.G);
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};   // Σ t0 gx0, Σ t1 gx1, Σ z², bad
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    const NodeH h = node_heights(xw[k], xw[N + k], sp.inv_sigma[0], sp.inv_sigma[1], a.z_top, true);
+    const size_t t0 = tix(c, 0, k, N), t1 = tix(c, 1, k, N);
+    const double G0 = Gt[t0], G1 = Gt[t1];
+    Gt[t0] = 0.f;
+    Gt[t1] = 0.f;
+    const double gx0 = G0 * h.J0 + G1 * h.J10, gx1 = G1 * h.J11;
+    gx[k] = gx0;
+    gx[N + k] = gx1;
+    acc[0] += h.t0 * gx0;
+    acc[1] += h.t1 * gx1;
+    const double z0 = vc[k], z1 = vc[N + k];
+    acc[2] += z0 * z0 + z1 * z1;
+  }
+  block_sum<4>(acc);
+  const Dft d = dft_setup(sm, a.nx, a.ny);
+  double gr[2];
+  int bad = 0;
+  for (int l = 0; l < 2; l++) {
+    const double *g = gx + l * N;
+    circ_apply(d, a.cs, sp.r[l], 0, [&](int k) { return g[k]; });   // U ∂ll/∂x_l
+    for (int k = threadIdx.x; k < N; k += blockDim.x) {
+      const float gz = (float)((a.prior_on ? -(double)vc[l * N + k] : 0.0) + d.vre[k]);
+      gc[l * N + k] = gz;
+      bad |= !isfinite(gz);
+    }
+    __syncthreads();
+    const float *z = vc + l * N;
+    circ_apply(d, a.cs, sp.r[l], 1, [&](int k) { return (double)z[k]; });   // (dU/dr) z_l
+    double s[1] = {0.0};
+    for (int k = threadIdx.x; k < N; k += blockDim.x) s[0] += g[k] * d.vre[k];
+    block_sum<1>(s);
+    const double r = sp.r[l];
+    // ∂ll/∂σ_l = Σ ∂ll/∂H ∂H/∂σ = -Σ t_l ∂ll/∂x_l  (t = x/σ inside the clamp)
+    const double dll_ds = -acc[l];
+    gr[l] = r * (1.0 - r) * (s[0] + dll_ds * sp.dsig[l]) + (a.prior_on ? 1.0 - 2.0 * r : 0.0);
+  }
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    gc[2 * N] = (float)gr[0];
+    gc[2 * N + 1] = (float)gr[1];
+    double lp = a.ll[c];
+    if (a.prior_on)
+      lp += -0.5 * acc[2] - N * log(2.0 * M_PI) + log(sp.r[0]) + log1p(-sp.r[0]) + log(sp.r[1]) + log1p(-sp.r[1]);
+    a.ll[c] = 0.0;
+    a.logp[c] = lp;
+    if (a.status) a.status[c] = (bad || !isfinite(lp) || !isfinite(gr[0]) || !isfinite(gr[1])) ? MT_STATUS_NONFINITE : 0;
+  }
+}
+
+// Leapfrog kicks / drifts in the non-centred coordinates (heights follow in
+// k_ncp_heights): KICK_HALF_DRIFT p += ε/2 g, z += ε p; KICK_FULL_DRIFT p += ε g,
+// z += ε p; KICK_HALF_LAST p += ε/2 g and the kinetic energy ½|p|².
+template <int MODE>
+__global__ void __launch_bounds__(MT_THREADS) k_ncp_kick(FinishArgs a) {
+  const int c = blockIdx.x, P = a.P;
+  float *xc = a.x + (size_t)c * P, *pc = a.mom + (size_t)c * P;
+  const float *gc = a.grad + (size_t)c * P;
+  const float eps = a.eps[c], f = MODE == KICK_FULL_DRIFT ? eps : 0.5f * eps;
+  double kin[1] = {0.0};
+  for (int k = threadIdx.x; k < P; k += blockDim.x) {
+    const float p = pc[k] + f * gc[k];
+    pc[k] = p;
+    if (MODE != KICK_HALF_LAST) xc[k] = xc[k] + eps * p;
+    else kin[0] += 0.5 * (double)p * p;
+  }
+  if (MODE == KICK_HALF_LAST) {
+    block_sum<1>(kin);
+    if (threadIdx.x == 0 && a.kin) a.kin[c] = (float)kin[0];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
+// dynamic shared memory of the non-centred kernels: 4N doubles of DFT work + twiddles
+// (K3 adds 2N for ∂ll/∂x): up to 200 KiB at N = 4096, so opt in once
+static size_t ncp_smem(const mt_problem *p) {
+  static bool attr = false;
+  if (!attr) {
+    const int mx = (6 * MT_MAX_NODES + 4 * MT_MAX_AXIS) * (int)sizeof(double);
+    cudaFuncSetAttribute(k_ncp_heights, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_ncp_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    attr = true;
+  }
+  return (size_t)(4 * p->N + 4 * MT_MAX_AXIS) * sizeof(double);
+}
+
 static FinishArgs base_args(mt_problem *p, int C) {
   FinishArgs a{};
   a.nx = p->nx; a.ny = p->ny; a.N = p->N; a.P = p->P; a.C = C;
@@ -945,6 +1183,8 @@ static FinishArgs base_args(mt_problem *p, int C) {
   a.band = p->d_band;
   a.sample_r = p->sample_r;
   a.cs = p->d_cs;
+  a.ncp = p->ncp;
+  a.xw = p->d_xw;
   return a;
 }
 
@@ -955,7 +1195,8 @@ cudaError_t launch_heights(mt_problem *p, int C, const float *x, float *H, float
   a.H = H;
   a.Hlo = p->d_Hlo;
   a.band = band;
-  if (p->sample_r) k_heights_r<<<C, MT_THREADS, 0, s>>>(a, x);
+  if (p->ncp) k_ncp_heights<<<C, MT_THREADS, ncp_smem(p), s>>>(a, x);
+  else if (p->sample_r) k_heights_r<<<C, MT_THREADS, 0, s>>>(a, x);
   else k_heights<<<C, MT_THREADS, 0, s>>>(a, x);
   p->all_launches++;
   return cudaGetLastError();
@@ -967,6 +1208,12 @@ cudaError_t launch_finish(mt_problem *p, int mode, int C, float *x, float *grad,
   if (C <= 0) return cudaSuccess;
   FinishArgs a = base_args(p, C);
   a.x = x; a.grad = grad; a.logp = logp; a.status = status; a.mom = mom; a.eps = eps; a.kin = kin;
+  if (p->ncp) {   // unfused: the API drives kicks / drifts separately (k_ncp_kick)
+    if (mode != FIN_PLAIN) return cudaErrorInvalidValue;
+    k_ncp_finish<<<C, MT_THREADS, ncp_smem(p) + (size_t)2 * p->N * sizeof(double), s>>>(a);
+    p->all_launches++;
+    return cudaGetLastError();
+  }
   size_t smem = (size_t)p->P * sizeof(float);
   static bool attr[3] = {false, false, false};
   if (smem > 48 * 1024 && !attr[mode]) {
@@ -1004,6 +1251,17 @@ cudaError_t launch_kick(mt_problem *p, int mode, int C, float *x, float *mom, co
   if (C <= 0) return cudaSuccess;
   FinishArgs a = base_args(p, C);
   a.x = x; a.mom = mom; a.grad = const_cast<float *>(grad); a.eps = eps; a.kin = kin;
+  if (p->ncp) {
+    if (mode == KICK_HALF_DRIFT) k_ncp_kick<KICK_HALF_DRIFT><<<C, MT_THREADS, 0, s>>>(a);
+    else if (mode == KICK_FULL_DRIFT) k_ncp_kick<KICK_FULL_DRIFT><<<C, MT_THREADS, 0, s>>>(a);
+    else k_ncp_kick<KICK_HALF_LAST><<<C, MT_THREADS, 0, s>>>(a);
+    p->all_launches++;
+    if (mode != KICK_HALF_LAST) {
+      k_ncp_heights<<<C, MT_THREADS, ncp_smem(p), s>>>(a, x);
+      p->all_launches++;
+    }
+    return cudaGetLastError();
+  }
   if (p->sample_r) {
     if (mode == KICK_HALF_DRIFT) k_kick_r<KICK_HALF_DRIFT><<<C, MT_THREADS, 0, s>>>(a);
     else if (mode == KICK_FULL_DRIFT) k_kick_r<KICK_FULL_DRIFT><<<C, MT_THREADS, 0, s>>>(a);
@@ -1028,6 +1286,10 @@ cudaError_t launch_hmc_begin(mt_problem *p, int C, float *x, const double *logp,
   k_hmc_begin<<<C, MT_THREADS, 0, s>>>(a, logp, p->d_x0, p->d_g0, p->d_lp0, p->d_kin0, seed, iter,
                                        chain_offset);
   p->all_launches++;
+  if (p->ncp) {   // heights of the drifted z (k_hmc_begin skipped them)
+    k_ncp_heights<<<C, MT_THREADS, ncp_smem(p), s>>>(a, x);
+    p->all_launches++;
+  }
   return cudaGetLastError();
 }
 

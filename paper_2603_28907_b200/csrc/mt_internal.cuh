@@ -98,6 +98,8 @@ struct FinishArgs {
   float *kin;                   // [C] 1/2 |p|^2 after the last half kick
   int sample_r;                 // f2: state (x_0, x_1, ρ_0, ρ_1), r_l = logistic(ρ_l)
   const double *cs;             // [N] c_ab = 2(cos 2πa/n_x + cos 2πb/n_y) (torus spectrum)
+  int ncp;                      // f2 non-centred: state (z_0, z_1, ρ_0, ρ_1), x = U(r) z
+  double *xw;                   // [C][2N] fp64 x = U z of the current state (ncp)
 };
 
 enum { FIN_PLAIN = 0, FIN_STEP = 1, FIN_LAST = 2 };
@@ -159,6 +161,8 @@ struct mt_problem {
   int prior_on = 1;
   int sample_r = 0;             // f2: the CAR r_l are sampled (two more parameters per chain)
   double *d_cs = nullptr;       // [N] torus spectrum table (sample_r)
+  int ncp = 0;                  // f2 non-centred parameterisation (implies sample_r)
+  double *d_xw = nullptr;       // [max_chains][2N] fp64 x = U z (ncp)
   TraceConsts tc{};
   float *d_X = nullptr, *d_Y = nullptr;
   float4 *d_ray_a = nullptr, *d_ray_b = nullptr;

@@ -28,6 +28,25 @@ from typing import Optional
 import numpy as np
 
 
+def noncentred_state(x: np.ndarray, rho, nx: int, ny: int) -> np.ndarray:
+    """Host helper: the non-centred state (z_0, z_1, ρ_0, ρ_1) with U(r_l) z_l = x_l, i.e.
+    z_l = Q(r_l)^{1/2} x_l (numpy 2-D FFT on the torus), for starting non-centred chains
+    (Problem(noncentred=True)) from centred states x [C][2N].  Not on the hot path."""
+    x = np.asarray(x, np.float64)
+    C, N = x.shape[0], nx * ny
+    a = np.arange(nx)[:, None]
+    b = np.arange(ny)[None, :]
+    cab = 2.0 * (np.cos(2 * np.pi * a / nx) + np.cos(2 * np.pi * b / ny))
+    out = np.zeros((C, 2 * N + 2), np.float64)
+    for l in range(2):
+        r = 1.0 / (1.0 + np.exp(-float(rho[l])))
+        xl = x[:, l * N:(l + 1) * N].reshape(C, nx, ny)
+        zl = np.real(np.fft.ifft2(np.fft.fft2(xl) * np.sqrt(4.0 - r * cab)))
+        out[:, l * N:(l + 1) * N] = zl.reshape(C, N)
+        out[:, 2 * N + l] = rho[l]
+    return out.astype(np.float32)
+
+
 class DualAveraging:
     """Nesterov dual averaging of log ε towards a target acceptance δ."""
 

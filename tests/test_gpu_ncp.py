@@ -1,0 +1,114 @@
+"""GPU parity of the non-centred CAR parameterisation (f2, reading
+R13d): state (z_0, z_1, ρ_0, ρ_1), x = Q(r)^{-1/2} z applied by a 2-D DFT in
+fp64 on the device, against the oracle's direct circulant sums.  Tolerances as
+north_star's."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from paper_2603_28907_b200 import Problem, inputs  # noqa: E402
+from test_oracle_ncp import circulant  # noqa: E402
+
+DEV = "cuda:0"
+
+
+def rel_l2(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def ncp_states(prob, op, C, seed, rho=(2.5, 2.0), scale=0.01):
+    """z = U(r)^{-1} x for near-posterior centred states x (dense solve, test-side)."""
+    x = inputs.chain_states(prob["x_true"], C, seed, scale=scale).astype(np.float64)
+    v = np.zeros((C, op.P + 2))
+    for l in range(2):
+        r = 1.0 / (1.0 + np.exp(-rho[l]))
+        U = circulant(oracle.ncp_kernel(op.nx, op.ny, r)[0])
+        v[:, l * op.N:(l + 1) * op.N] = np.linalg.solve(U, x[:, l * op.N:(l + 1) * op.N].T).T
+        v[:, 2 * op.N + l] = rho[l]
+    return v.astype(np.float32)
+
+
+@pytest.mark.parametrize("name,C,chains", [("tiny", 4, None), ("small", 16, None), ("small", 40, None),
+                                           ("medium", 64, [0, 31, 63])])
+def test_ncp_logpost_grad(problems, oracle_problem, name, C, chains):
+    prob = problems(name)
+    op = oracle_problem(name)
+    v = ncp_states(prob, op, C, inputs.CONFIGS[name].seed)
+    mp = Problem(prob, device=0, max_chains=C, noncentred=True)
+    assert mp.P == op.P + 2
+    lp, g = mp.logpost_grad(torch.from_numpy(v).to(DEV))
+    sel = np.arange(C) if chains is None else np.array(chains)
+    ref = op.logpost_grad_ncp(v[sel].astype(np.float64))
+    lpd, gd = lp.cpu().numpy(), g.cpu().numpy().astype(np.float64)
+    for k, c in enumerate(sel):
+        assert abs(lpd[c] - ref["logp"][k]) <= 1e-4 * abs(ref["logp"][k]), (c, lpd[c], ref["logp"][k])
+        assert rel_l2(gd[c], ref["grad"][k]) <= 1e-3, (c, rel_l2(gd[c], ref["grad"][k]))
+        # the two hyper-parameter components on their own
+        assert np.allclose(gd[c, -2:], ref["grad"][k, -2:], rtol=1e-3, atol=1e-3 * np.abs(ref["grad"][k]).max())
+
+
+def test_ncp_ray_sharded_full_size(problems, oracle_problem):
+    """configs[4]: n = 64 (N = 4096 nodes per surface, the 200 KiB shared-memory DFT), 4.19M rays."""
+    prob = problems("ray_sharded")
+    op = oracle_problem("ray_sharded")
+    v = ncp_states(prob, op, 1, inputs.CONFIGS["ray_sharded"].seed)
+    mp = Problem(prob, device=0, max_chains=1, noncentred=True)
+    lp, g = mp.logpost_grad(torch.from_numpy(v).to(DEV))
+    ref = op.logpost_grad_ncp(v.astype(np.float64))
+    assert abs(lp[0].item() - ref["logp"][0]) <= 1e-4 * abs(ref["logp"][0])
+    assert rel_l2(g[0].cpu().numpy().astype(np.float64), ref["grad"][0]) <= 1e-3
+
+
+@pytest.mark.parametrize("name,C", [("tiny", 4), ("small", 16)])
+def test_ncp_leapfrog_10_steps(problems, oracle_problem, name, C):
+    prob = problems(name)
+    op = oracle_problem(name)
+    v0 = ncp_states(prob, op, C, inputs.CONFIGS[name].seed)
+    mp = Problem(prob, device=0, max_chains=C, noncentred=True)
+    p0 = np.random.default_rng(12).standard_normal(v0.shape).astype(np.float32)
+    e = 2e-4
+    x = torch.from_numpy(v0.copy()).to(DEV)
+    p = torch.from_numpy(p0.copy()).to(DEV)
+    lp, g = mp.logpost_grad(x)
+    mp.leapfrog(x, p, lp, g, torch.full((C,), e, dtype=torch.float32, device=DEV), 10)
+    lg = lambda vv: (lambda o: (o["logp"], o["grad"]))(op.logpost_grad_ncp(vv))  # noqa: E731
+    xo, po, lpo, _ = oracle.leapfrog(v0.astype(np.float64), p0.astype(np.float64), e, 10, lg)
+    xd = x.cpu().numpy().astype(np.float64)
+    for c in range(C):
+        assert rel_l2(xd[c], xo[c]) <= 1e-3, (c, rel_l2(xd[c], xo[c]))
+        assert np.linalg.norm(xd[c] - xo[c]) / np.linalg.norm(xo[c] - v0[c]) < 0.05
+    ref = op.logpost_grad_ncp(xd)
+    assert np.allclose(lp.cpu().numpy(), ref["logp"], rtol=1e-4)
+
+
+def test_ncp_hmc_step_heights_and_nuts_refusal(problems, oracle_problem):
+    prob = problems("small")
+    op = oracle_problem("small")
+    C = 32
+    v = torch.from_numpy(ncp_states(prob, op, C, 2)).to(DEV)
+    mp = Problem(prob, device=0, max_chains=C, noncentred=True)
+    lp, g = mp.logpost_grad(v)
+    eps = torch.full((C,), 2e-4, dtype=torch.float32, device=DEV)
+    ap, acc = mp.hmc_step(v, lp, g, eps, 10, seed=11, it=0)
+    assert torch.isfinite(lp).all() and torch.isfinite(v).all() and float(ap.mean()) > 0.3
+    # logp / grad returned by the step are those of the (accepted or restored) state
+    ref = op.logpost_grad_ncp(v.cpu().numpy().astype(np.float64))
+    assert np.allclose(lp.cpu().numpy(), ref["logp"], rtol=1e-4)
+    # heights of the state are those of x = U z
+    H = mp.heights(v[:2]).cpu().numpy().astype(np.float64)
+    zz = v[:2].cpu().numpy().astype(np.float64)
+    for c in range(2):
+        x = np.concatenate([circulant(oracle.ncp_kernel(op.nx, op.ny, 1 / (1 + np.exp(-zz[c, op.P + l])))[0])
+                            @ zz[c, l * op.N:(l + 1) * op.N] for l in range(2)])
+        sig = [oracle.torus_spectrum(op.nx, op.ny, 1 / (1 + np.exp(-zz[c, op.P + l])))[0] for l in range(2)]
+        from scipy.special import ndtr
+        u0, u1 = ndtr(x[:op.N] / sig[0]), ndtr(x[op.N:] / sig[1])
+        H0 = u0 * op.z_top
+        H1 = H0 + u1 * (op.z_top - H0)
+        assert np.allclose(H[c].reshape(2, -1), np.stack([H0, H1]), atol=2e-5 * op.z_top)
+    from paper_2603_28907_b200 import MTError
+    with pytest.raises(MTError):
+        mp.nuts_step(v, lp, g, eps, 4, seed=1, it=0)

@@ -84,3 +84,17 @@ def test_ncp_gradient_vs_fd(problems, oracle_problem):
             vm[c, k] -= h
             fd = (op.logpost_grad_ncp(vp[c:c + 1])["logp"][0] - op.logpost_grad_ncp(vm[c:c + 1])["logp"][0]) / (2 * h)
             assert out["grad"][c, k] == pytest.approx(fd, rel=2e-5, abs=1e-3)
+
+
+def test_noncentred_state_helper_inverts_U():
+    """hmc.noncentred_state (host helper for starting non-centred chains) gives
+    U(r) z = x with the oracle's U (dense circulant)."""
+    from paper_2603_28907_b200.hmc import noncentred_state
+    nx, ny, rho = 3, 4, (1.0, 2.0)
+    x = np.random.default_rng(0).standard_normal((2, 2 * nx * ny))
+    v = noncentred_state(x, rho, nx, ny).astype(np.float64)
+    N = nx * ny
+    for l in range(2):
+        U = circulant(oracle.ncp_kernel(nx, ny, 1 / (1 + np.exp(-rho[l])))[0])
+        assert np.allclose(v[:, l * N:(l + 1) * N] @ U.T, x[:, l * N:(l + 1) * N], atol=1e-6)
+        assert np.all(v[:, 2 * N + l] == np.float32(rho[l]))
