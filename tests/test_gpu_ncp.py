@@ -112,3 +112,22 @@ def test_ncp_hmc_step_heights_and_nuts_refusal(problems, oracle_problem):
     from paper_2603_28907_b200 import MTError
     with pytest.raises(MTError):
         mp.nuts_step(v, lp, g, eps, 4, seed=1, it=0)
+
+
+def test_ncp_ray_shards_sum_to_whole(problems, oracle_problem):
+    """Ray sharding (§9) in the non-centred mode: the prior terms (−½|z|², the ρ
+    hyperprior) on shard 0 only, the likelihood parts of ∂/∂z and ∂/∂ρ on every
+    shard; the partials sum to the unsharded result."""
+    prob = problems("small")
+    op = oracle_problem("small")
+    R = len(prob["ray_det"])
+    v = torch.from_numpy(ncp_states(prob, op, 20, 2)).to(DEV)
+    whole = Problem(prob, device=0, max_chains=20, noncentred=True)
+    lp, g = whole.logpost_grad(v)
+    parts = [Problem(prob, device=0, max_chains=20, ray_lo=lo, ray_hi=hi, noncentred=True)
+             for lo, hi in ((0, 9000), (9000, R))]
+    outs = [p.logpost_grad(v) for p in parts]
+    assert np.allclose(sum(o[0].cpu().numpy() for o in outs), lp.cpu().numpy(), rtol=1e-6)
+    gsum = sum(o[1].cpu().numpy().astype(np.float64) for o in outs)
+    for c in range(20):
+        assert rel_l2(gsum[c], g.cpu().numpy()[c].astype(np.float64)) < 1e-5

@@ -159,3 +159,26 @@ def test_voxel_hmc_step_and_switch_back(problems):
     lp2, g2 = mp.logpost_grad(x)
     assert torch.allclose(lp2, lp_exact, rtol=1e-9, atol=0)
     assert float((g2 - g_exact).norm() / g_exact.norm()) < 1e-5
+
+
+def test_voxel_ray_shards_sum_to_whole(problems):
+    """Ray sharding (§9) under the voxel model: each shard's problem builds G for
+    its rays; partial logp / grad (prior on shard 0) sum to the unsharded result."""
+    prob = problems("small")
+    R = len(prob["ray_det"])
+    cfg = inputs.CONFIGS["small"]
+    x = torch.from_numpy(inputs.chain_states(prob["x_true"], 40, cfg.seed)).to(DEV)
+    whole = Problem(prob, device=0, max_chains=40)
+    whole.voxel_model(NZ, href(prob))
+    lp, g = whole.logpost_grad(x)
+    lps, gs = [], []
+    for lo, hi in ((0, 7000), (7000, R)):
+        part = Problem(prob, device=0, max_chains=40, ray_lo=lo, ray_hi=hi)
+        part.voxel_model(NZ, href(prob))
+        a, b = part.logpost_grad(x)
+        lps.append(a.cpu().numpy())
+        gs.append(b.cpu().numpy().astype(np.float64))
+    assert np.allclose(sum(lps), lp.cpu().numpy(), rtol=1e-6)
+    gsum = sum(gs)
+    for c in range(40):
+        assert rel_l2(gsum[c], g.cpu().numpy()[c].astype(np.float64)) < 1e-5
