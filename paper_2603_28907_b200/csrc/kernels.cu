@@ -951,7 +951,7 @@ struct Dft {
 // ½ c λ^{-3/2} (mode 1); v(k) gives input element k (row-major [i][j]); the
 // result is left in d.vre (real part).  All threads of the block participate.
 template <class In>
-__device__ void circ_apply(const Dft &d, const double *cs, double r, int mode, In v) {
+__device__ void circ_apply_dft(const Dft &d, const double *cs, double r, int mode, In v) {
   const int nx = d.nx, ny = d.ny, N = d.N;
   for (int q = threadIdx.x; q < N; q += blockDim.x) {        // rows: T[i][b] = Σ_j v e^{-2πi bj/ny}
     const int i = q / ny, b = q - i * ny;
@@ -1012,6 +1012,80 @@ __device__ void circ_apply(const Dft &d, const double *cs, double r, int mode, I
     d.vre[q] = re / N;
   }
   __syncthreads();
+}
+
+__device__ __forceinline__ int bitrev(int v, int bits) { return (int)(__brev((unsigned)v) >> (32 - bits)); }
+
+// Power-of-two sizes: radix-2 FFTs in place on (vre, vim).  Forward: decimation
+// in frequency along rows then columns (natural order in, bit-reversed out);
+// the eigenvalue scaling reads c_ab at the bit-reversed frequency; inverse:
+// decimation in time (bit-reversed in, natural out).  N log2 N butterflies per
+// transform instead of the direct sums' N (n_x + n_y).
+template <class In>
+__device__ void circ_apply_fft(const Dft &d, const double *cs, double r, int mode, In v) {
+  const int nx = d.nx, ny = d.ny, N = d.N, bx = __ffs(nx) - 1, by = __ffs(ny) - 1;
+  double *re = d.vre, *im = d.vim;
+  for (int q = threadIdx.x; q < N; q += blockDim.x) { re[q] = v(q); im[q] = 0.0; }
+  __syncthreads();
+  // forward DIF along rows (length ny, stride 1) then columns (length nx, stride ny)
+  for (int pass = 0; pass < 2; pass++) {
+    const int n = pass ? nx : ny, ln = pass ? bx : by, st = pass ? ny : 1, lines = pass ? ny : nx;
+    const double *tc = pass ? d.tcx : d.tcy, *ts = pass ? d.tsx : d.tsy;
+    for (int lh = ln - 1; lh >= 0; lh--) {
+      const int h = 1 << lh, tstep = n >> (lh + 1);
+      for (int t = threadIdx.x; t < lines << (ln - 1); t += blockDim.x) {
+        const int line = t >> (ln - 1), bfly = t & ((n >> 1) - 1);
+        const int g = (bfly >> lh) << (lh + 1), k = bfly & (h - 1);
+        const int base = pass ? line : line * ny;
+        const int i0 = base + (g + k) * st, i1 = i0 + h * st;
+        const double ar = re[i0], ai = im[i0], br = re[i1], bi = im[i1];
+        const double dr = ar - br, di = ai - bi, c = tc[k * tstep], sn = ts[k * tstep];
+        re[i0] = ar + br;
+        im[i0] = ai + bi;
+        re[i1] = dr * c + di * sn;      // (a - b) e^{-iθ}
+        im[i1] = di * c - dr * sn;
+      }
+      __syncthreads();
+    }
+  }
+  for (int q = threadIdx.x; q < N; q += blockDim.x) {        // eigenvalues at bit-reversed frequencies
+    const int pi = q >> by, pj = q & (ny - 1);
+    const double cab = cs[bitrev(pi, bx) * ny + bitrev(pj, by)], lam = 4.0 - r * cab;
+    const double sc = (mode == 0 ? rsqrt(lam) : 0.5 * cab * rsqrt(lam) / lam) / N;
+    re[q] *= sc;
+    im[q] *= sc;
+  }
+  __syncthreads();
+  // inverse DIT along columns then rows
+  for (int pass = 0; pass < 2; pass++) {
+    const int n = pass ? ny : nx, ln = pass ? by : bx, st = pass ? 1 : ny, lines = pass ? nx : ny;
+    const double *tc = pass ? d.tcy : d.tcx, *ts = pass ? d.tsy : d.tsx;
+    for (int lh = 0; lh < ln; lh++) {
+      const int h = 1 << lh, tstep = n >> (lh + 1);
+      for (int t = threadIdx.x; t < lines << (ln - 1); t += blockDim.x) {
+        const int line = t >> (ln - 1), bfly = t & ((n >> 1) - 1);
+        const int g = (bfly >> lh) << (lh + 1), k = bfly & (h - 1);
+        const int base = pass ? line * ny : line;
+        const int i0 = base + (g + k) * st, i1 = i0 + h * st;
+        const double c = tc[k * tstep], sn = ts[k * tstep];
+        const double br = re[i1] * c - im[i1] * sn, bi = im[i1] * c + re[i1] * sn;   // b e^{+iθ}
+        const double ar = re[i0], ai = im[i0];
+        re[i0] = ar + br;
+        im[i0] = ai + bi;
+        re[i1] = ar - br;
+        im[i1] = ai - bi;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+template <class In>
+__device__ __forceinline__ void circ_apply(const Dft &d, const double *cs, double r, int mode, In v) {
+  // the FFT's 2 log2 N synchronised stages only pay off on large grids (measured:
+  // Medium n = 32 DFT 6.00 vs FFT 6.41 ms per evaluation; ray-sharded n = 64 DFT 1.50 vs FFT 1.31 ms)
+  if ((d.nx & (d.nx - 1)) == 0 && (d.ny & (d.ny - 1)) == 0 && d.N >= 2048) circ_apply_fft(d, cs, r, mode, v);
+  else circ_apply_dft(d, cs, r, mode, v);
 }
 
 __device__ __forceinline__ Dft dft_setup(double *sm, int nx, int ny) {

@@ -131,3 +131,22 @@ def test_ncp_ray_shards_sum_to_whole(problems, oracle_problem):
     gsum = sum(o[1].cpu().numpy().astype(np.float64) for o in outs)
     for c in range(20):
         assert rel_l2(gsum[c], g.cpu().numpy()[c].astype(np.float64)) < 1e-5
+
+
+def test_ncp_non_power_of_two_grid_uses_the_direct_dft(problems):
+    """A 12 x 12 grid (not a power of two: the direct-DFT branch of circ_apply,
+    the paper's own grids are 19 x 19 / 12 x 15) with zero counts and random z."""
+    import dataclasses
+    cfg = dataclasses.replace(inputs.CONFIGS["tiny"], name="ncp12", n=12)
+    prob = inputs.make_problem(cfg, data={"A": 1.0, "counts": np.zeros(cfg.n_rays, np.int32)})
+    op = oracle.Problem(prob)
+    C = 3
+    rng = np.random.default_rng(5)
+    v = np.concatenate([0.3 * rng.standard_normal((C, op.P)), np.tile([[2.0, 1.0]], (C, 1))], axis=1)
+    v = v.astype(np.float32)
+    mp = Problem(prob, device=0, max_chains=C, noncentred=True)
+    lp, g = mp.logpost_grad(torch.from_numpy(v).to(DEV))
+    ref = op.logpost_grad_ncp(v.astype(np.float64))
+    for c in range(C):
+        assert abs(lp[c].item() - ref["logp"][c]) <= 1e-4 * abs(ref["logp"][c])
+        assert rel_l2(g[c].cpu().numpy().astype(np.float64), ref["grad"][c]) <= 1e-3
