@@ -182,3 +182,28 @@ def test_voxel_ray_shards_sum_to_whole(problems):
     gsum = sum(gs)
     for c in range(40):
         assert rel_l2(gsum[c], g.cpu().numpy()[c].astype(np.float64)) < 1e-5
+
+
+def test_voxel_nuts_step_matches_oracle(vgpu, oracle_problem, problems):
+    """The batched NUTS transition (f1) on the voxel model (f3): same Philox
+    streams as the oracle's NUTS driven by the voxel oracle; trees of <= 16 leaves."""
+    prob = problems("tiny")
+    mp, op = vgpu("tiny"), oracle_problem("tiny")
+    cfg = inputs.CONFIGS["tiny"]
+    Hr = href(prob).astype(np.float64)
+    C, max_depth, e, seed, it = 4, 4, 2e-3, inputs.philox_key(cfg), 5
+    x0 = inputs.chain_states(prob["x_true"], C, cfg.seed)
+    x = torch.from_numpy(x0).to(DEV)
+    lp, g = mp.logpost_grad(x)
+    eps = torch.full((C,), e, dtype=torch.float32, device=DEV)
+    acc, depth, nl = mp.nuts_step(x, lp, g, eps, max_depth, seed, it)
+    xd = x.cpu().numpy().astype(np.float64)
+    lg1 = lambda th: (lambda o: (o["logp"][0], o["grad"][0]))(op.voxel_logpost_grad(th[None], Hr, NZ))  # noqa: E731
+    agree = 0
+    for c in range(C):
+        lp0, g0 = lg1(x0[c].astype(np.float64))
+        ref = oracle.nuts_step(x0[c], lp0, g0, e, lg1, seed, it, c, max_depth=max_depth)
+        if ref["depth"] == depth[c].item() and ref["n_leaves"] == nl[c].item():
+            agree += 1
+            assert rel_l2(xd[c], ref["x"]) <= 1e-3
+    assert agree >= C - 1, agree
