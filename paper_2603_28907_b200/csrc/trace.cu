@@ -289,6 +289,12 @@ __shared__ float sgeo[4][MT_MAX_AXIS];   // X, Y, 1/ΔX, 1/ΔY
 #ifndef MT_RCAP
 #define MT_RCAP 3
 #endif
+#ifndef MT_RL_GLOBAL_H
+#define MT_RL_GLOBAL_H 1
+#endif
+#ifndef MT_RL_MINB
+#define MT_RL_MINB 4
+#endif
 #ifndef MT_CL_MINB
 #define MT_CL_MINB 5
 #endif
@@ -870,17 +876,24 @@ __global__ void __launch_bounds__(MT_THREADS) k_trace_defer(TraceArgs a) {
 // fp32 atomics are CAS loops on sm_100a).
 // ---------------------------------------------------------------------------
 template <int MODE, int NY>
-__global__ void __launch_bounds__(MT_THREADS, 4) k_trace_rl(TraceArgs a, const float *__restrict__ Hc) {
+__global__ void __launch_bounds__(MT_THREADS, MT_RL_MINB) k_trace_rl(TraceArgs a, const float *__restrict__ Hc) {
   extern __shared__ __align__(16) float smem[];
   __shared__ double red[MT_THREADS / 32];
   const int ny = NY ? NY : a.tc.ny, N = a.tc.N;
   const int tid = threadIdx.x, c = blockIdx.y;
+#if MT_RL_GLOBAL_H
+  // the chain's heights straight from global memory (L1-resident: 2N floats);
+  // shared memory holds only the crossing records, so more blocks fit per SM
+  const float *__restrict__ Hs = Hc + (size_t)c * 2 * N;
+  float4 *rec = reinterpret_cast<float4 *>(smem) + tid;                        // [2*RCAP][MT_THREADS]
+#else
   float *Hs = smem;                                                            // [2N]
   float4 *rec = reinterpret_cast<float4 *>(smem + ((2 * N + 3) & ~3)) + tid;   // [2*RCAP][MT_THREADS]
   {
     const float *src = Hc + (size_t)c * 2 * N;
     for (int k = tid; k < 2 * N; k += MT_THREADS) Hs[k] = __ldg(src + k);
   }
+#endif
   load_geometry(a, sgeo[0], sgeo[1], sgeo[2], sgeo[3]);
   const float4 bd = __ldg(a.band + c);
   const size_t coff = (size_t)(c >> 5) * 2 * N * 32 + (c & 31);
@@ -1223,7 +1236,7 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
     a.rays_per_block = (p->R + S - 1) / S;
     S = (p->R + a.rays_per_block - 1) / a.rays_per_block;
     dim3 grid((unsigned)S, (unsigned)C);
-    size_t smem = (size_t)4 * ((2 * p->N + 3) & ~3) + (size_t)16 * 2 * RCAP * MT_THREADS;
+    size_t smem = (MT_RL_GLOBAL_H ? 0 : (size_t)4 * ((2 * p->N + 3) & ~3)) + (size_t)16 * 2 * RCAP * MT_THREADS;
     if (e == cudaSuccess)
       e = mode == TRACE_LL ? launch_rl_ny<TRACE_LL>(a, p->d_Hc, p->ny, grid, smem, s)
                            : launch_rl_ny<TRACE_PATH>(a, p->d_Hc, p->ny, grid, smem, s);
