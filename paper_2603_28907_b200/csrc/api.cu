@@ -80,7 +80,7 @@ int check_chains(const mt_problem *p, int32_t C) {
 
 void free_all(mt_problem *p) {
   voxel_free(p);
-  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_trav_geo, p->d_rl_head, p->d_rl_code, p->d_rl_ovf, p->d_ovf_q, p->d_ovf_n, p->d_redo, p->d_H, p->d_Hlo, p->d_Hc, p->d_cs, p->d_xw, p->d_G,
+  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_trav_geo, p->d_rl_head, p->d_rl_code, p->d_rl_ovf, p->d_ovf_q, p->d_ovf_n, p->d_redo, p->d_H, p->d_Hlo, p->d_Hc, p->d_cs, p->d_xw, p->mb_red, p->mb_band, p->mb_ticket, p->d_G,
                   p->d_band, p->d_ll, p->d_x0, p->d_g0, p->d_mom, p->d_kin0, p->d_kin1, p->d_lp0};
   for (void *b : bufs)
     if (b) cudaFree(b);
@@ -276,6 +276,11 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   ALLOC(p->d_redo, sizeof(unsigned) * redo_words);
   ALLOC(p->d_cs, sizeof(double) * p->N);
   if (p->ncp) ALLOC(p->d_xw, sizeof(double) * MC * 2 * p->N);
+  if (!getenv("MT_NO_MB")) {   // few-chain multi-block K3 / kick scratch (use_mb)
+    ALLOC(p->mb_red, sizeof(double) * 16 * 3);
+    ALLOC(p->mb_band, sizeof(unsigned) * 16 * 4);
+    ALLOC(p->mb_ticket, sizeof(unsigned) * 16);
+  }
 #undef ALLOC
   if (e != cudaSuccess) {
     free_all(p);
@@ -295,6 +300,13 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   if (e == cudaSuccess) e = cudaMemset(p->d_ll, 0, sizeof(double) * MC);
   if (e == cudaSuccess) e = cudaMemset(p->d_ovf_n, 0, sizeof(int) * 4);
   if (e == cudaSuccess) e = cudaMemset(p->d_redo, 0, sizeof(unsigned) * redo_words);
+  if (e == cudaSuccess && p->mb_red) {
+    std::vector<unsigned> b(64);
+    for (int k = 0; k < 16; k++) { b[4 * k] = b[4 * k + 2] = 0x7f7fffffu; b[4 * k + 1] = b[4 * k + 3] = 0u; }
+    e = cudaMemset(p->mb_red, 0, sizeof(double) * 48);
+    if (e == cudaSuccess) e = cudaMemset(p->mb_ticket, 0, sizeof(unsigned) * 16);
+    if (e == cudaSuccess) e = cudaMemcpy(p->mb_band, b.data(), sizeof(unsigned) * 64, cudaMemcpyHostToDevice);
+  }
   if (e == cudaSuccess) {   // torus spectrum table c_ab = 2(cos 2πa/n_x + cos 2πb/n_y) (sample_r)
     std::vector<double> cs(p->N);
     for (int a = 0; a < p->nx; a++)
@@ -355,7 +367,7 @@ int mt_logpost_grad(mt_problem *p, int32_t C, const float *x, double *logp, floa
   DevGuard g(p->device);
   cudaStream_t s = (cudaStream_t)stream;
   CK(launch_heights(p, C, x, p->d_H, p->d_band, s));
-  if (p->comm || p->ncp) return eval_sharded(p, C, const_cast<float *>(x), logp, grad, status, s);
+  if (p->comm || p->ncp || use_mb(p, C)) return eval_sharded(p, C, const_cast<float *>(x), logp, grad, status, s);
   CK(launch_trace(p, TRACE_LL, C, p->d_H, p->d_band, p->d_G, p->d_ll, nullptr, nullptr, s));
   CK(launch_finish(p, FIN_PLAIN, C, const_cast<float *>(x), grad, logp, status, nullptr, nullptr,
                    nullptr, s));
@@ -385,7 +397,7 @@ int mt_leapfrog(mt_problem *p, int32_t C, float *x, float *mom, double *logp, fl
   DevGuard g(p->device);
   cudaStream_t s = (cudaStream_t)stream;
   CK(launch_kick_drift(p, C, x, mom, grad, eps, s));
-  if (p->comm || p->ncp) return leapfrog_sharded(p, C, x, mom, logp, grad, nullptr, eps, L, s);
+  if (p->comm || p->ncp || use_mb(p, C)) return leapfrog_sharded(p, C, x, mom, logp, grad, nullptr, eps, L, s);
   for (int step = 1; step <= L; step++) {
     CK(launch_trace(p, TRACE_LL, C, p->d_H, p->d_band, p->d_G, p->d_ll, nullptr, nullptr, s));
     CK(launch_finish(p, step < L ? FIN_STEP : FIN_LAST, C, x, grad, logp, nullptr, mom, eps,
@@ -416,7 +428,7 @@ int mt_hmc_step(mt_problem *p, int32_t C, float *x, double *logp, float *grad, c
   DevGuard g(p->device);
   cudaStream_t s = (cudaStream_t)stream;
   CK(launch_hmc_begin(p, C, x, logp, grad, eps, seed, iter, chain_offset, s));
-  if (p->comm || p->ncp) {
+  if (p->comm || p->ncp || use_mb(p, C)) {
     if (int r = leapfrog_sharded(p, C, x, p->d_mom, logp, grad, status, eps, L, s)) return r;
     CK(launch_hmc_end(p, C, x, logp, grad, seed, iter, chain_offset, accept_prob, accepted, status, s));
     return MT_OK;

@@ -328,6 +328,136 @@ __global__ void __launch_bounds__(MT_THREADS) k_kick(FinishArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Few chains (C < 16, e.g. the one-chain ray-sharded config): one block per
+// chain leaves 147 of 148 SMs idle in K3 (68 µs of a 0.49 ms evaluation at
+// N = 4096).  These variants spread a chain's nodes over gridDim.y blocks;
+// the per-chain scalars go through fp64 atomics into a small scratch record,
+// and the last block of the chain (atomic ticket) finalises and resets it.
+// The leapfrog then runs unfused (K3 PLAIN + kick/drift), so no block reads a
+// neighbour's x while another block drifts it.
+// scratch per chain: red[0] Σ x·Qx, red[1] kinetic, red[2] non-finite flag,
+//   bandi[4] = (min H0, max H0, min H1, max H1) as ordered float bits (heights >= 0)
+// ---------------------------------------------------------------------------
+struct MbScratch {
+  double *red;          // [C][3]
+  unsigned *bandi;      // [C][4]
+  unsigned *ticket;     // [C]
+};
+
+__device__ __forceinline__ bool mb_last(unsigned *ticket, int c) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket + c, 1u) == gridDim.y - 1;
+  __syncthreads();
+  return last;
+}
+
+__global__ void __launch_bounds__(MT_THREADS) k_finish_mb(FinishArgs a, MbScratch m) {
+  const int c = blockIdx.x, N = a.N, ny = a.ny, nx = a.nx;
+  const float *xc = a.x + (size_t)c * a.P;
+  float *gc = a.grad + (size_t)c * a.P;
+  float *Gt = const_cast<float *>(a.G);
+  BlockRed v = {3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f, 0.0, 0.0, 0};
+  for (int k = blockIdx.y * blockDim.x + threadIdx.x; k < N; k += gridDim.y * blockDim.x) {
+    const int i = k / ny, j = k - i * ny;
+    const float x0 = xc[k], x1 = xc[N + k];
+    const NodeH h = node_heights(x0, x1, a.inv_sigma[0], a.inv_sigma[1], a.z_top, true);
+    const size_t t0 = tix(c, 0, k, N), t1 = tix(c, 1, k, N);
+    const float G0 = Gt[t0], G1 = Gt[t1];
+    Gt[t0] = 0.f;
+    Gt[t1] = 0.f;
+    double gx0 = (double)G0 * h.J0 + (double)G1 * h.J10;
+    double gx1 = (double)G1 * h.J11;
+    if (a.prior_on) {
+      const int ip = (i + 1 == nx ? 0 : i + 1) * ny + j, im = (i == 0 ? nx - 1 : i - 1) * ny + j;
+      const int jp = i * ny + (j + 1 == ny ? 0 : j + 1), jm = i * ny + (j == 0 ? ny - 1 : j - 1);
+#pragma unroll
+      for (int l = 0; l < 2; l++) {
+        const float *xl = xc + l * N;
+        const double xv = xl[k];
+        const double Qx = 4.0 * xv - (double)a.car_r[l] * ((double)xl[ip] + xl[im] + xl[jp] + xl[jm]);
+        v.s0 += xv * Qx;
+        if (l == 0) gx0 -= Qx; else gx1 -= Qx;
+      }
+    }
+    const float g0f = (float)gx0, g1f = (float)gx1;
+    gc[k] = g0f;
+    gc[N + k] = g1f;
+    v.bad |= !(isfinite(g0f) && isfinite(g1f));
+  }
+  const BlockRed r = block_reduce(v);
+  if (threadIdx.x == 0) {
+    atomicAdd(m.red + 3 * c, r.s0);
+    if (r.bad) atomicAdd(m.red + 3 * c + 2, 1.0);
+  }
+  if (mb_last(m.ticket, c) && threadIdx.x == 0) {
+    volatile double *rd = m.red + 3 * c;
+    const double lp = a.ll[c] + (a.prior_on ? -0.5 * rd[0] + a.prior_const : 0.0);
+    a.ll[c] = 0.0;
+    a.logp[c] = lp;
+    if (a.status) a.status[c] = (rd[2] != 0.0 || !isfinite(lp)) ? MT_STATUS_NONFINITE : 0;
+    rd[0] = 0.0;
+    rd[2] = 0.0;
+    m.ticket[c] = 0u;
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(MT_THREADS) k_kick_mb(FinishArgs a, MbScratch m) {
+  const int c = blockIdx.x, N = a.N;
+  float *xc = a.x + (size_t)c * a.P, *pc = a.mom + (size_t)c * a.P;
+  const float *gc = a.grad + (size_t)c * a.P;
+  const float eps = a.eps[c];
+  const float f = MODE == KICK_FULL_DRIFT ? eps : 0.5f * eps;
+  BlockRed v = {3.0e38f, 0.f, 3.0e38f, 0.f, 0.0, 0.0, 0};
+  for (int k = blockIdx.y * blockDim.x + threadIdx.x; k < N; k += gridDim.y * blockDim.x) {
+    const float p0 = pc[k] + f * gc[k], p1 = pc[N + k] + f * gc[N + k];
+    pc[k] = p0;
+    pc[N + k] = p1;
+    if (MODE == KICK_HALF_LAST) {
+      v.s1 += 0.5 * ((double)p0 * p0 + (double)p1 * p1);
+      continue;
+    }
+    const float x0 = xc[k] + eps * p0, x1 = xc[N + k] + eps * p1;
+    xc[k] = x0;
+    xc[N + k] = x1;
+    const NodeH h = node_heights(x0, x1, a.inv_sigma[0], a.inv_sigma[1], a.z_top, false);
+    a.H[tix(c, 0, k, N)] = h.H0;
+    a.H[tix(c, 1, k, N)] = h.H1;
+    a.Hlo[tix(c, 0, k, N)] = h.L0;
+    a.Hlo[tix(c, 1, k, N)] = h.L1;
+    v.mn0 = fminf(v.mn0, h.H0); v.mx0 = fmaxf(v.mx0, h.H0);
+    v.mn1 = fminf(v.mn1, h.H1); v.mx1 = fmaxf(v.mx1, h.H1);
+  }
+  const BlockRed r = block_reduce(v);
+  unsigned *bi = m.bandi + 4 * c;
+  if (threadIdx.x == 0) {
+    if (MODE == KICK_HALF_LAST) {
+      atomicAdd(m.red + 3 * c + 1, r.s1);
+    } else {   // non-negative floats order like their bit patterns
+      atomicMin(bi + 0, __float_as_uint(r.mn0));
+      atomicMax(bi + 1, __float_as_uint(r.mx0));
+      atomicMin(bi + 2, __float_as_uint(r.mn1));
+      atomicMax(bi + 3, __float_as_uint(r.mx1));
+    }
+  }
+  if (mb_last(m.ticket, c) && threadIdx.x == 0) {
+    if (MODE == KICK_HALF_LAST) {
+      volatile double *rd = m.red + 3 * c;
+      if (a.kin) a.kin[c] = (float)rd[1];
+      rd[1] = 0.0;
+    } else {
+      volatile unsigned *vb = bi;
+      a.band[c] = make_float4(__uint_as_float(vb[0]), __uint_as_float(vb[1]), __uint_as_float(vb[2]),
+                              __uint_as_float(vb[3]));
+      vb[0] = 0x7f7fffffu; vb[1] = 0u; vb[2] = 0x7f7fffffu; vb[3] = 0u;
+    }
+    m.ticket[c] = 0u;
+  }
+}
+
 // HMC begin: Philox momenta, kinetic energy, save (x, grad, logp), first
 // half kick + drift + heights.
 __global__ void __launch_bounds__(MT_THREADS) k_hmc_begin(FinishArgs a, const double *logp,
@@ -1226,6 +1356,24 @@ __global__ void __launch_bounds__(MT_THREADS) k_ncp_kick(FinishArgs a) {
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
+// few-chain multi-block K3 / kicks (fixed r, centred): blocks per chain so that
+// about 2 blocks per SM are in flight
+bool use_mb(const mt_problem *p, int C) {
+  return p->mb_red != nullptr && C < 16 && !p->sample_r && !p->ncp;
+}
+static int mb_blocks(const mt_problem *p, int C) {
+  int nb = (2 * p->num_sms + C - 1) / C;
+  const int cap = (p->N + MT_THREADS - 1) / MT_THREADS;
+  return nb < 1 ? 1 : (nb > cap ? cap : nb);
+}
+static MbScratch mb_scratch(mt_problem *p) {
+  MbScratch m;
+  m.red = p->mb_red;
+  m.bandi = p->mb_band;
+  m.ticket = p->mb_ticket;
+  return m;
+}
+
 // dynamic shared memory of the non-centred kernels: 4N doubles of DFT work + twiddles
 // (K3 adds 2N for ∂ll/∂x): up to 200 KiB at N = 4096, so opt in once
 static size_t ncp_smem(const mt_problem *p) {
@@ -1282,6 +1430,12 @@ cudaError_t launch_finish(mt_problem *p, int mode, int C, float *x, float *grad,
   if (C <= 0) return cudaSuccess;
   FinishArgs a = base_args(p, C);
   a.x = x; a.grad = grad; a.logp = logp; a.status = status; a.mom = mom; a.eps = eps; a.kin = kin;
+  if (use_mb(p, C)) {   // few chains: several blocks per chain (unfused leapfrog)
+    if (mode != FIN_PLAIN) return cudaErrorInvalidValue;
+    k_finish_mb<<<dim3(C, mb_blocks(p, C)), MT_THREADS, 0, s>>>(a, mb_scratch(p));
+    p->all_launches++;
+    return cudaGetLastError();
+  }
   if (p->ncp) {   // unfused: the API drives kicks / drifts separately (k_ncp_kick)
     if (mode != FIN_PLAIN) return cudaErrorInvalidValue;
     k_ncp_finish<<<C, MT_THREADS, ncp_smem(p) + (size_t)2 * p->N * sizeof(double), s>>>(a);
@@ -1325,6 +1479,14 @@ cudaError_t launch_kick(mt_problem *p, int mode, int C, float *x, float *mom, co
   if (C <= 0) return cudaSuccess;
   FinishArgs a = base_args(p, C);
   a.x = x; a.mom = mom; a.grad = const_cast<float *>(grad); a.eps = eps; a.kin = kin;
+  if (use_mb(p, C)) {
+    const dim3 g(C, mb_blocks(p, C));
+    if (mode == KICK_HALF_DRIFT) k_kick_mb<KICK_HALF_DRIFT><<<g, MT_THREADS, 0, s>>>(a, mb_scratch(p));
+    else if (mode == KICK_FULL_DRIFT) k_kick_mb<KICK_FULL_DRIFT><<<g, MT_THREADS, 0, s>>>(a, mb_scratch(p));
+    else k_kick_mb<KICK_HALF_LAST><<<g, MT_THREADS, 0, s>>>(a, mb_scratch(p));
+    p->all_launches++;
+    return cudaGetLastError();
+  }
   if (p->ncp) {
     if (mode == KICK_HALF_DRIFT) k_ncp_kick<KICK_HALF_DRIFT><<<C, MT_THREADS, 0, s>>>(a);
     else if (mode == KICK_FULL_DRIFT) k_ncp_kick<KICK_FULL_DRIFT><<<C, MT_THREADS, 0, s>>>(a);

@@ -162,6 +162,9 @@ struct mt_problem {
   int sample_r = 0;             // f2: the CAR r_l are sampled (two more parameters per chain)
   double *d_cs = nullptr;       // [N] torus spectrum table (sample_r)
   int ncp = 0;                  // f2 non-centred parameterisation (implies sample_r)
+  double *mb_red = nullptr;     // few-chain multi-block K3 scratch: [16][3] sums
+  unsigned *mb_band = nullptr;  //   [16][4] band as float bits
+  unsigned *mb_ticket = nullptr;   // [16] last-block tickets
   double *d_xw = nullptr;       // [max_chains][2N] fp64 x = U z (ncp)
   TraceConsts tc{};
   float *d_X = nullptr, *d_Y = nullptr;
@@ -217,6 +220,7 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
 cudaError_t launch_finish(mt_problem *p, int mode, int C, float *x, float *grad, double *logp,
                           int32_t *status, float *mom, const float *eps, float *kin,
                           cudaStream_t s);
+bool use_mb(const mt_problem *p, int C);   // few chains: multi-block K3 and kicks, unfused leapfrog
 cudaError_t launch_kick_drift(mt_problem *p, int C, float *x, float *mom, const float *grad,
                               const float *eps, cudaStream_t s);
 cudaError_t launch_hmc_begin(mt_problem *p, int C, float *x, const double *logp,
