@@ -150,3 +150,22 @@ def test_ncp_non_power_of_two_grid_uses_the_direct_dft(problems):
     for c in range(C):
         assert abs(lp[c].item() - ref["logp"][c]) <= 1e-4 * abs(ref["logp"][c])
         assert rel_l2(g[c].cpu().numpy().astype(np.float64), ref["grad"][c]) <= 1e-3
+
+
+def test_ncp_chain_sharded_8192_bench_launch(problems, oracle_problem):
+    """configs[3] in the non-centred mode, the launch `bench.py --noncentred`
+    times (8,192 chains), sampled chains."""
+    from paper_2603_28907_b200.hmc import noncentred_state
+    prob = problems("medium")
+    op = oracle_problem("medium")
+    cfg = inputs.CONFIGS["chain_sharded"]
+    x = inputs.chain_states(prob["x_true"], 8192, cfg.seed, super_size=8)
+    rho = np.log(np.asarray(cfg.car_r) / (1.0 - np.asarray(cfg.car_r)))
+    v = noncentred_state(x, rho, cfg.n, cfg.n)
+    mp = Problem(prob, device=0, max_chains=8192, noncentred=True)
+    lp, g = mp.logpost_grad(torch.from_numpy(v).to(DEV))
+    sel = np.array([0, 4100, 8191])
+    ref = op.logpost_grad_ncp(v[sel].astype(np.float64))
+    for k, c in enumerate(sel):
+        assert abs(lp[c].item() - ref["logp"][k]) <= 1e-4 * abs(ref["logp"][k])
+        assert rel_l2(g[c].cpu().numpy().astype(np.float64), ref["grad"][k]) <= 1e-3

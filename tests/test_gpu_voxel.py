@@ -207,3 +207,16 @@ def test_voxel_nuts_step_matches_oracle(vgpu, oracle_problem, problems):
             agree += 1
             assert rel_l2(xd[c], ref["x"]) <= 1e-3
     assert agree >= C - 1, agree
+
+
+def test_voxel_chain_sharded_8192_bench_launch(oracle_problem, problems):
+    """configs[3] under the voxel model in the launch configuration
+    `bench.py --model voxel` times (8,192 chains, 4 per lane), sampled chains."""
+    prob = problems("medium")
+    op = oracle_problem("medium")
+    mp = Problem(prob, device=0, max_chains=8192)
+    mp.voxel_model(NZ, href(prob))
+    x = inputs.chain_states(prob["x_true"], 8192, inputs.CONFIGS["chain_sharded"].seed, super_size=8)
+    logp, grad = mp.logpost_grad(torch.from_numpy(x).to(DEV))
+    fails = check(op, prob, x, np.array([0, 4095, 8191]), logp.cpu().numpy(), grad.cpu().numpy())
+    assert not fails, fails
