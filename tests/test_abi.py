@@ -5,6 +5,7 @@ import os
 import re
 import subprocess
 
+import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -61,3 +62,42 @@ def test_product_path_does_not_import_the_oracle():
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "oracle.c" not in txt and "liboracle" not in txt, f
+
+
+def test_widening_entry_points_validate_before_touching_the_device(so_path, problems):
+    """f2/f3 entry points reject bad arguments with MT_EINVAL (no GPU needed)."""
+    from paper_2603_28907_b200 import inputs
+    from paper_2603_28907_b200._lib import _Desc
+    L = ct.CDLL(so_path)
+    L.mt_last_error.restype = ct.c_char_p
+    L.mt_voxel_model.argtypes = [ct.c_void_p, ct.c_int32, ct.c_float, ct.c_float, ct.c_void_p]
+    L.mt_voxel_info.argtypes = [ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_void_p]
+    L.mt_voxel_counters.argtypes = [ct.c_void_p, ct.c_void_p]
+    L.mt_measure_l2_gather.argtypes = [ct.c_int32, ct.c_int64, ct.c_void_p]
+    assert L.mt_voxel_model(None, 60, 1.0, 1e-3, None) == 1
+    assert b"problem is NULL" in L.mt_last_error()
+    assert L.mt_voxel_info(None, None, None, None) == 1
+    assert L.mt_voxel_counters(None, None) == 1
+    v = ct.c_double()
+    assert L.mt_measure_l2_gather(0, 1024, ct.byref(v)) == 1
+    # noncentred without sample_r: a descriptor error, found before any device query
+    prob = problems("tiny")
+    keep = {k: np.ascontiguousarray(prob[k], dt) for k, dt in
+            (("node_x", np.float32), ("node_y", np.float32), ("det_xyz", np.float32), ("ray_det", np.int32),
+             ("ray_dir", np.float32), ("ray_w", np.float32), ("counts", np.int32))}
+    d = _Desc()
+    d.n_x = d.n_y = len(keep["node_x"])
+    d.node_x, d.node_y = keep["node_x"].ctypes.data, keep["node_y"].ctypes.data
+    d.z_top, d.rho_muck, d.rho_air, d.rho_rock, d.rho_ext, d.att_len = 300.0, 1.9, 0.0012, 2.65, 2.65, 250.0
+    d.car_r[0] = d.car_r[1] = 0.95
+    d.n_det, d.det_xyz = len(keep["det_xyz"]), keep["det_xyz"].ctypes.data
+    d.n_rays = len(keep["ray_det"])
+    d.ray_det, d.ray_dir = keep["ray_det"].ctypes.data, keep["ray_dir"].ctypes.data
+    d.ray_w, d.counts = keep["ray_w"].ctypes.data, keep["counts"].ctypes.data
+    d.ray_lo, d.ray_hi, d.max_chains = 0, d.n_rays, 4
+    d.sample_r, d.noncentred = 0, 1
+    L.mt_problem_create.argtypes = [ct.c_void_p, ct.c_void_p]
+    h = ct.c_void_p()
+    assert L.mt_problem_create(ct.byref(d), ct.byref(h)) == 1
+    assert b"noncentred requires sample_r" in L.mt_last_error()
+    assert inputs.CONFIGS["tiny"].n == d.n_x
