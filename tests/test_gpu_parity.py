@@ -617,3 +617,47 @@ def test_chain_shards_reproduce_the_unsharded_hmc_step(gpu, problems):
     close = (apa - apb).abs() < 1e-4
     assert torch.equal(acca[close], accb[close])
     assert float((xa - xb).norm() / xa.norm()) < 1e-6
+
+
+@pytest.mark.parametrize("mode", ["plain", "one_rank_comm", "few_chains"])
+def test_cuda_graph_capture_and_replay(gpu, problems, mode):
+    """The evaluation and leapfrog entry points are stream-ordered with no host
+    synchronisation, so they can be captured into a CUDA graph (with the
+    in-library NCCL all-reduce when a communicator is attached) and replayed:
+    a replayed 10-step leapfrog equals the eager one."""
+    from paper_2603_28907_b200 import comm_unique_id
+    prob = problems("small")
+    cfg = inputs.CONFIGS["small"]
+    C = 4 if mode == "few_chains" else 32
+    pb = Problem(prob, device=0, max_chains=C)
+    if mode == "one_rank_comm":
+        pb.attach_comm(comm_unique_id(), 0, 1)
+    x0 = torch.from_numpy(inputs.chain_states(prob["x_true"], C, cfg.seed)).to(DEV)
+    p0 = torch.from_numpy(np.random.default_rng(3).standard_normal((C, pb.P)).astype(np.float32)).to(DEV)
+    eps = torch.full((C,), sampling_eps("small"), dtype=torch.float32, device=DEV)
+    # eager reference
+    xe, pe = x0.clone(), p0.clone()
+    lpe, ge = pb.logpost_grad(xe)
+    pb.leapfrog(xe, pe, lpe, ge, eps, 10)
+    # static buffers, warm-up on a side stream, capture, replay
+    xs, ps = x0.clone(), p0.clone()
+    lps = torch.empty(C, dtype=torch.float64, device=DEV)
+    gs = torch.empty_like(xs)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        pb.logpost_grad(xs, lps, gs)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):      # (the binding launches on the current = capture stream)
+        pb.logpost_grad(xs, lps, gs)
+        pb.leapfrog(xs, ps, lps, gs, eps, 10)
+    xs.copy_(x0)
+    ps.copy_(p0)
+    graph.replay()
+    torch.cuda.synchronize()
+    assert float((xs - xe).norm() / xe.norm()) < 1e-5
+    assert np.allclose(lps.cpu().numpy(), lpe.cpu().numpy(), rtol=1e-6)
+    if mode == "one_rank_comm":
+        pb.detach_comm()
