@@ -335,35 +335,39 @@ class Problem:
 # identity mass (R19), accept iff ln u < -ΔH (Metropolis correction).
 # ---------------------------------------------------------------------------
 
-def leapfrog(x, p, eps, L, logp_grad):
+def leapfrog(x, p, eps, L, logp_grad, minv=None):
     """L kick-drift-kick steps.  logp_grad(x [C][P]) -> (logp [C], grad [C][P]).
 
-    eps: scalar or [C].  Returns (x, p, logp, grad) after L steps.
+    eps: scalar or [C].  minv: diagonal inverse mass [P] (None: identity; R19b):
+    drift x += ε M^-1 p.  Returns (x, p, logp, grad) after L steps.
     """
     x = np.array(x, np.float64)
     p = np.array(p, np.float64)
+    mi = 1.0 if minv is None else np.asarray(minv, np.float64)
     e = np.asarray(eps, np.float64).reshape(-1, 1) if np.ndim(eps) else float(eps)
     lp, g = logp_grad(x)
     for _ in range(L):
         p = p + 0.5 * e * g
-        x = x + e * p
+        x = x + e * mi * p
         lp, g = logp_grad(x)
         p = p + 0.5 * e * g
     return x, p, lp, g
 
 
-def hmc_step(x, eps, L, logp_grad, seed, it, chain_offset=0):
-    """One HMC transition per chain with Philox momenta and MH uniforms.
+def hmc_step(x, eps, L, logp_grad, seed, it, chain_offset=0, minv=None):
+    """One HMC transition per chain with Philox momenta and MH uniforms; minv the
+    diagonal inverse mass (p = z / sqrt(minv) ~ N(0, M), kinetic ½ pᵀ M^-1 p).
 
     Returns (x_new, accept_prob [C], accepted [C] bool, logp_new, dH [C]).
     """
     x = np.array(x, np.float64)
     C, P = x.shape
-    p0 = np.stack([momenta(P, seed, it, chain_offset + c) for c in range(C)])
+    mi = np.ones(P) if minv is None else np.asarray(minv, np.float64)
+    p0 = np.stack([momenta(P, seed, it, chain_offset + c) for c in range(C)]) / np.sqrt(mi)
     lp0, _ = logp_grad(x)
-    x1, p1, lp1, _ = leapfrog(x, p0, eps, L, logp_grad)
-    H0 = -lp0 + 0.5 * np.sum(p0 * p0, axis=1)
-    H1 = -lp1 + 0.5 * np.sum(p1 * p1, axis=1)
+    x1, p1, lp1, _ = leapfrog(x, p0, eps, L, logp_grad, minv)
+    H0 = -lp0 + 0.5 * np.sum(mi * p0 * p0, axis=1)
+    H1 = -lp1 + 0.5 * np.sum(mi * p1 * p1, axis=1)
     dH = H1 - H0
     u = np.array([mh_uniform(seed, it, chain_offset + c) for c in range(C)])
     with np.errstate(over="ignore", invalid="ignore"):
@@ -411,20 +415,22 @@ def leaf_ckpt_idxs(n: int):
     return idx_max - t + 1, idx_max
 
 
-def is_turning(p_left, p_right, rho):
+def is_turning(p_left, p_right, rho, minv=1.0):
+    """Generalised U-turn on the velocities M^-1 p of the two ends."""
     rs = rho - 0.5 * (p_left + p_right)
-    return float(np.dot(p_left, rs)) <= 0.0 or float(np.dot(p_right, rs)) <= 0.0
+    return float(np.dot(minv * p_left, rs)) <= 0.0 or float(np.dot(minv * p_right, rs)) <= 0.0
 
 
-def nuts_step(x, lp, g, eps, logp_grad1, seed, it, chain, max_depth=8, trace=None):
+def nuts_step(x, lp, g, eps, logp_grad1, seed, it, chain, max_depth=8, trace=None, minv=None):
     """One NUTS transition of one chain.  logp_grad1(x [P]) -> (logp, grad [P]).
     Returns dict(x, logp, grad, depth, n_leaves, accept_stat, diverging).
     trace (a list, optional) receives (kind, margin, x) for every random choice:
     the distance of log u from its threshold (debugging threshold flips)."""
     x = np.array(x, np.float64)
     P = x.size
-    p = momenta(P, seed, it, chain)
-    H0 = -lp + 0.5 * float(p @ p)
+    mi = np.ones(P) if minv is None else np.asarray(minv, np.float64)
+    p = momenta(P, seed, it, chain) / np.sqrt(mi)
+    H0 = -lp + 0.5 * float(p @ (mi * p))
     left = right = (x, p, g, lp)                 # (θ, p, ∇, logp) of the two edges
     prop = (x, lp, g)
     logW = 0.0                                   # log Σ e^{-ΔH} over the tree (initial leaf: ΔH = 0)
@@ -440,10 +446,10 @@ def nuts_step(x, lp, g, eps, logp_grad1, seed, it, chain, max_depth=8, trace=Non
         for n in range(2 ** j):
             e = v * eps
             pp = pp + 0.5 * e * gg
-            th = th + e * pp
+            th = th + e * mi * pp
             ll, gg = logp_grad1(th)
             pp = pp + 0.5 * e * gg
-            dH = (-ll + 0.5 * float(pp @ pp)) - H0
+            dH = (-ll + 0.5 * float(pp @ (mi * pp))) - H0
             acc_sum += min(1.0, math.exp(-dH)) if math.isfinite(dH) else 0.0
             n_leaf += 1
             if not math.isfinite(dH) or dH > 1000.0:
@@ -462,7 +468,7 @@ def nuts_step(x, lp, g, eps, logp_grad1, seed, it, chain, max_depth=8, trace=Non
                 r_ck[hi], rs_ck[hi] = pp, rhos.copy()
             else:
                 for i in range(hi, lo - 1, -1):
-                    if is_turning(r_ck[i], pp, rhos - rs_ck[i] + r_ck[i]):
+                    if is_turning(r_ck[i], pp, rhos - rs_ck[i] + r_ck[i], mi):
                         ok = False
                         break
                 if not ok:
@@ -480,7 +486,7 @@ def nuts_step(x, lp, g, eps, logp_grad1, seed, it, chain, max_depth=8, trace=Non
         else:
             left = (th, pp, gg, ll)
         rho = rho + rhos
-        if is_turning(left[1], right[1], rho):
+        if is_turning(left[1], right[1], rho, mi):
             break
     return dict(x=prop[0], logp=prop[1], grad=prop[2], depth=depth, n_leaves=n_leaf,
                 accept_stat=acc_sum / max(n_leaf, 1), diverging=diverging)

@@ -93,3 +93,47 @@ def test_momenta_are_standard_normal():
     # distinct streams per chain / iteration
     assert not np.allclose(oracle.momenta(8, 1, 0, 0), oracle.momenta(8, 1, 0, 1))
     assert not np.allclose(oracle.momenta(8, 1, 0, 0), oracle.momenta(8, 1, 1, 0))
+
+
+def test_diagonal_mass_is_a_change_of_variables():
+    """R19b: HMC / NUTS with diagonal inverse mass m on logp(x) equal the
+    identity-mass algorithms (pinned above by closed forms) on y = x / sqrt(m)
+    with target logp(sqrt(m) y): momenta q = p sqrt(m), ½ qᵀq = ½ pᵀ M^-1 p,
+    velocities M^-1 p in the U-turn criterion."""
+    import math
+    rng = np.random.default_rng(21)
+    P = 6
+    A = rng.standard_normal((P, P))
+    A = A @ A.T + P * np.eye(P)                       # a correlated Gaussian target
+    mu = rng.standard_normal(P)
+
+    def lg(x):
+        d = np.atleast_2d(x) - mu
+        return -0.5 * np.einsum("ci,ij,cj->c", d, A, d), -(d @ A)
+    m = np.array([0.3, 2.0, 1.0, 0.5, 4.0, 0.8])
+    sq = np.sqrt(m)
+
+    def lg_y(y):
+        lp, g = lg(np.atleast_2d(y) * sq)
+        return lp, g * sq
+    x0 = rng.standard_normal((3, P))
+    p0 = rng.standard_normal((3, P))
+    x1, p1, lp1, _ = oracle.leapfrog(x0, p0, 0.05, 7, lg, minv=m)
+    y1, q1, lpy, _ = oracle.leapfrog(x0 / sq, p0 * sq, 0.05, 7, lg_y)
+    assert np.allclose(x1, y1 * sq, atol=1e-12) and np.allclose(p1 * sq, q1, atol=1e-12)
+    seed = 12345
+    for it in range(3):
+        xa, aa, acca, lpa, dHa = oracle.hmc_step(x0, 0.1, 5, lg, seed, it, minv=m)
+        ya, ab, accb, lpb, dHb = oracle.hmc_step(x0 / sq, 0.1, 5, lg_y, seed, it)
+        assert np.allclose(xa, ya * sq, atol=1e-12) and np.allclose(dHa, dHb, atol=1e-10)
+        assert np.array_equal(acca, accb)
+    lg1 = lambda th: (lambda o: (o[0][0], o[1][0]))(lg(th[None]))      # noqa: E731
+    lg1y = lambda th: (lambda o: (o[0][0], o[1][0]))(lg_y(th[None]))   # noqa: E731
+    for c in range(3):
+        lp, g = lg1(x0[c])
+        a = oracle.nuts_step(x0[c], lp, g, 0.1, lg1, seed, 5, c, max_depth=5, minv=m)
+        lpy0, gy = lg1y(x0[c] / sq)
+        b = oracle.nuts_step(x0[c] / sq, lpy0, gy, 0.1, lg1y, seed, 5, c, max_depth=5)
+        assert a["depth"] == b["depth"] and a["n_leaves"] == b["n_leaves"]
+        assert np.allclose(a["x"], b["x"] * sq, atol=1e-10)
+        assert math.isclose(a["accept_stat"], b["accept_stat"], rel_tol=1e-9, abs_tol=1e-12)
