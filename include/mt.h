@@ -236,6 +236,18 @@ int mt_nested_rhat_partials(mt_problem *p, int32_t C, int32_t M, const float *me
 int mt_summary_update(mt_problem *p, int32_t C, const float *x, const double *logp, int32_t nz, float gap,
                       double *acc, float *map_x, double *map_logp, mt_stream stream);
 
+/* Diagonal inverse mass matrix M^-1 for HMC and NUTS (NumPyro's default
+ * adapted diagonal mass, the paper's sampler P:643-653; R19b):
+ * momenta p ~ N(0, M), drift x += ε M^-1 p, kinetic energy ½ pᵀ M^-1 p, the
+ * NUTS U-turn criterion on the velocities M^-1 p.  One vector shared by all
+ * chains of the problem (the driver adapts it from pooled warm-up variances).
+ *   minv   DEVICE [n] fp32, every entry finite and > 0; copied (synchronous).
+ *          NULL restores the identity.
+ *   n      must equal P (mt_num_params).
+ * Affects mt_draw_momenta, mt_leapfrog, mt_hmc_step, mt_nuts_step.
+ * Errors: MT_EINVAL (n, non-positive entries), MT_ENOMEM, MT_ECUDA. */
+int mt_set_inverse_mass(mt_problem *p, const float *minv, int32_t n);
+
 /* ---- the paper's voxel / sigmoid / linearised forward model (f3) -------- */
 
 /* Switch the problem's likelihood to the paper's own approximate forward

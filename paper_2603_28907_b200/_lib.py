@@ -46,7 +46,7 @@ EXPORTS = [
     "mt_philox_curand", "mt_timing_start", "mt_timing_read", "mt_trace_counters", "mt_measure_fp32_peak",
     "mt_last_error", "mt_comm_unique_id", "mt_attach_comm", "mt_detach_comm", "mt_nuts_step",
     "mt_nested_rhat_partials", "mt_summary_update", "mt_voxel_model", "mt_voxel_info",
-    "mt_voxel_counters", "mt_measure_l2_gather",
+    "mt_voxel_counters", "mt_measure_l2_gather", "mt_set_inverse_mass",
 ]
 
 _lib = None
@@ -91,6 +91,7 @@ def lib():
             "mt_voxel_model": ([vp, i32, ct.c_float, ct.c_float, vp], ct.c_int),
             "mt_voxel_info": ([vp, vp, vp, vp], ct.c_int),
             "mt_voxel_counters": ([vp, vp], ct.c_int),
+            "mt_set_inverse_mass": ([vp, vp, i32], ct.c_int),
             "mt_measure_l2_gather": ([i32, i64, vp], ct.c_int),
             "mt_last_error": ([], ct.c_char_p),
         }
@@ -393,6 +394,15 @@ class Problem:
         nz, nnz, ng = ct.c_int32(), ct.c_int64(), ct.c_int64()
         _check(lib().mt_voxel_info(self.h, ct.byref(nz), ct.byref(nnz), ct.byref(ng)), "mt_voxel_info")
         return dict(n_z=nz.value, nnz=nnz.value, n_grid=ng.value)
+
+    def set_inverse_mass(self, minv=None):
+        """Diagonal inverse mass M^-1 [P] (device fp32) for HMC / NUTS; None = identity."""
+        import torch
+        if minv is None:
+            _check(lib().mt_set_inverse_mass(self.h, None, 0), "mt_set_inverse_mass")
+            return
+        _dev_tensor(minv, torch.float32, (self.P,), self.device, "minv")
+        _check(lib().mt_set_inverse_mass(self.h, _ptr(minv), self.P), "mt_set_inverse_mass")
 
     def voxel_gathered_bytes(self) -> int:
         v = ct.c_uint64()

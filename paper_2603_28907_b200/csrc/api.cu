@@ -80,7 +80,7 @@ int check_chains(const mt_problem *p, int32_t C) {
 
 void free_all(mt_problem *p) {
   voxel_free(p);
-  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_trav_geo, p->d_rl_head, p->d_rl_code, p->d_rl_ovf, p->d_ovf_q, p->d_ovf_n, p->d_redo, p->d_H, p->d_Hlo, p->d_Hc, p->d_cs, p->d_xw, p->mb_red, p->mb_band, p->mb_ticket, p->d_G,
+  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_trav_geo, p->d_rl_head, p->d_rl_code, p->d_rl_ovf, p->d_ovf_q, p->d_ovf_n, p->d_redo, p->d_H, p->d_Hlo, p->d_Hc, p->d_cs, p->d_xw, p->d_minv, p->mb_red, p->mb_band, p->mb_ticket, p->d_G,
                   p->d_band, p->d_ll, p->d_x0, p->d_g0, p->d_mom, p->d_kin0, p->d_kin1, p->d_lp0};
   for (void *b : bufs)
     if (b) cudaFree(b);
@@ -694,6 +694,28 @@ int mt_trace_counters(mt_problem *p, int64_t *deferred, double *defer_ms) {
     *deferred = (int64_t)v;
   }
   if (defer_ms) *defer_ms = p->defer_ms;
+  return MT_OK;
+}
+
+int mt_set_inverse_mass(mt_problem *p, const float *minv, int32_t n) {
+  if (!p) return set_err(MT_EINVAL, "problem is NULL");
+  DevGuard g(p->device);
+  if (!minv) {   // back to the identity mass
+    CK(cudaDeviceSynchronize());
+    if (p->d_minv) cudaFree(p->d_minv);
+    p->d_minv = nullptr;
+    return MT_OK;
+  }
+  if (n != p->P) return set_err(MT_EINVAL, "n = %d != P = %d", n, p->P);
+  std::vector<float> h(p->P);
+  CK(cudaMemcpy(h.data(), minv, sizeof(float) * p->P, cudaMemcpyDeviceToHost));
+  for (int k = 0; k < p->P; k++)
+    if (!(h[k] > 0.f) || !isfinite(h[k])) return set_err(MT_EINVAL, "minv[%d] = %g must be finite and > 0", k, h[k]);
+  if (!p->d_minv) {
+    cudaError_t e = cudaMalloc((void **)&p->d_minv, sizeof(float) * p->P);
+    if (e != cudaSuccess) return set_err(MT_ENOMEM, "cudaMalloc: %s", cudaGetErrorString(e));
+  }
+  CK(cudaMemcpy(p->d_minv, h.data(), sizeof(float) * p->P, cudaMemcpyHostToDevice));
   return MT_OK;
 }
 

@@ -51,6 +51,10 @@ __device__ __forceinline__ NodeH node_heights(double x0, double x1, double is0, 
   return o;
 }
 
+// diagonal inverse mass M^-1 (mt_set_inverse_mass; identity when not set):
+// p ~ N(0, M), drift x += ε M^-1 p, kinetic ½ pᵀ M^-1 p (R19b)
+__device__ __forceinline__ float mi(const FinishArgs &a, int k) { return a.minv ? a.minv[k] : 1.f; }
+
 __device__ __forceinline__ float warp_min(float v) {
   for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
@@ -259,7 +263,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_finish(FinishArgs a) {
       float p0 = pc[k] + eps * g0f, p1 = pc[N + k] + eps * g1f;
       pc[k] = p0;
       pc[N + k] = p1;
-      float xn0 = x0 + eps * p0, xn1 = x1 + eps * p1;
+      float xn0 = x0 + eps * mi(a, k) * p0, xn1 = x1 + eps * mi(a, N + k) * p1;
       xc[k] = xn0;
       xc[N + k] = xn1;
       NodeH hn = node_heights(xn0, xn1, a.inv_sigma[0], a.inv_sigma[1], a.z_top, false);
@@ -273,7 +277,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_finish(FinishArgs a) {
       float p0 = pc[k] + 0.5f * eps * g0f, p1 = pc[N + k] + 0.5f * eps * g1f;
       pc[k] = p0;
       pc[N + k] = p1;
-      v.s1 += 0.5 * ((double)p0 * p0 + (double)p1 * p1);
+      v.s1 += 0.5 * ((double)mi(a, k) * p0 * p0 + (double)mi(a, N + k) * p1 * p1);
     }
   }
   BlockRed r = block_reduce(v);
@@ -307,10 +311,10 @@ __global__ void __launch_bounds__(MT_THREADS) k_kick(FinishArgs a) {
     pc[k] = p0;
     pc[N + k] = p1;
     if (MODE == KICK_HALF_LAST) {
-      v.s1 += 0.5 * ((double)p0 * p0 + (double)p1 * p1);
+      v.s1 += 0.5 * ((double)mi(a, k) * p0 * p0 + (double)mi(a, N + k) * p1 * p1);
       continue;
     }
-    float x0 = xc[k] + eps * p0, x1 = xc[N + k] + eps * p1;
+    float x0 = xc[k] + eps * mi(a, k) * p0, x1 = xc[N + k] + eps * mi(a, N + k) * p1;
     xc[k] = x0;
     xc[N + k] = x1;
     NodeH h = node_heights(x0, x1, a.inv_sigma[0], a.inv_sigma[1], a.z_top, false);
@@ -417,10 +421,10 @@ __global__ void __launch_bounds__(MT_THREADS) k_kick_mb(FinishArgs a, MbScratch 
     pc[k] = p0;
     pc[N + k] = p1;
     if (MODE == KICK_HALF_LAST) {
-      v.s1 += 0.5 * ((double)p0 * p0 + (double)p1 * p1);
+      v.s1 += 0.5 * ((double)mi(a, k) * p0 * p0 + (double)mi(a, N + k) * p1 * p1);
       continue;
     }
-    const float x0 = xc[k] + eps * p0, x1 = xc[N + k] + eps * p1;
+    const float x0 = xc[k] + eps * mi(a, k) * p0, x1 = xc[N + k] + eps * mi(a, N + k) * p1;
     xc[k] = x0;
     xc[N + k] = x1;
     const NodeH h = node_heights(x0, x1, a.inv_sigma[0], a.inv_sigma[1], a.z_top, false);
@@ -474,17 +478,18 @@ __global__ void __launch_bounds__(MT_THREADS) k_hmc_begin(FinishArgs a, const do
     double z[4];
     momenta4(seed, iter, chain_offset + c, q, z);
 #pragma unroll
-    for (int m = 0; m < 4; m++) {
-      int k = 4 * q + m;
+    for (int u = 0; u < 4; u++) {
+      int k = 4 * q + u;
       if (k < P) {
-        float pz = (float)z[m];
-        v.s0 += 0.5 * (double)pz * pz;
+        const float m = mi(a, k);
+        float pz = a.minv ? (float)(z[u] / sqrt((double)m)) : (float)z[u];
+        v.s0 += 0.5 * (double)m * pz * pz;
         float g = gc[k], xv = xc[k];
         x0s[(size_t)c * P + k] = xv;
         g0s[(size_t)c * P + k] = g;
         float ph = pz + 0.5f * eps * g;
         pc[k] = ph;
-        xc[k] = xv + eps * ph;
+        xc[k] = xv + eps * m * ph;
       }
     }
   }
@@ -556,7 +561,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_hmc_end(FinishArgs a, const floa
 }
 
 __global__ void k_momenta(int C, int P, float *mom, uint64_t seed, uint64_t iter,
-                          uint64_t chain_offset) {
+                          uint64_t chain_offset, const float *minv) {
   const int nq = (P + 3) / 4;
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)C * nq) return;
@@ -564,7 +569,8 @@ __global__ void k_momenta(int C, int P, float *mom, uint64_t seed, uint64_t iter
   double z[4];
   momenta4(seed, iter, chain_offset + c, q, z);
   for (int m = 0; m < 4; m++)
-    if (4 * q + m < P) mom[(size_t)c * P + 4 * q + m] = (float)z[m];
+    if (4 * q + m < P)
+      mom[(size_t)c * P + 4 * q + m] = minv ? (float)(z[m] / sqrt((double)minv[4 * q + m])) : (float)z[m];
 }
 
 __global__ void k_philox(const uint4 *ctr, uint2 key, uint4 *out, int64_t n, int use_curand) {
@@ -668,7 +674,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_finish_r(FinishArgs a) {
       const float p0 = pc[k] + 0.5f * eps * g0f, p1 = pc[N + k] + 0.5f * eps * g1f;
       pc[k] = p0;
       pc[N + k] = p1;
-      acc[6] += 0.5 * ((double)p0 * p0 + (double)p1 * p1);
+      acc[6] += 0.5 * ((double)mi(a, k) * p0 * p0 + (double)mi(a, N + k) * p1 * p1);
     }
   }
   block_sum<8>(acc);
@@ -695,7 +701,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_finish_r(FinishArgs a) {
       for (int l = 0; l < 2; l++) {
         const float pr = pc[2 * N + l] + 0.5f * eps * gr[l];
         pc[2 * N + l] = pr;
-        kin += 0.5 * (double)pr * pr;
+        kin += 0.5 * (double)mi(a, 2 * N + l) * pr * pr;
       }
       if (a.kin) a.kin[c] = (float)kin;
     }
@@ -703,7 +709,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_finish_r(FinishArgs a) {
       for (int l = 0; l < 2; l++) {
         const float pr = pc[2 * N + l] + eps * gr[l];
         pc[2 * N + l] = pr;
-        s_new[l] = xs[2 * N + l] + eps * pr;
+        s_new[l] = xs[2 * N + l] + eps * mi(a, 2 * N + l) * pr;
         xc[2 * N + l] = s_new[l];
       }
     }
@@ -716,7 +722,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_finish_r(FinishArgs a) {
       const float p0 = pc[k] + eps * gc[k], p1 = pc[N + k] + eps * gc[N + k];
       pc[k] = p0;
       pc[N + k] = p1;
-      const float xn0 = xs[k] + eps * p0, xn1 = xs[N + k] + eps * p1;
+      const float xn0 = xs[k] + eps * mi(a, k) * p0, xn1 = xs[N + k] + eps * mi(a, N + k) * p1;
       xc[k] = xn0;
       xc[N + k] = xn1;
       const NodeH hn = node_heights(xn0, xn1, sn.inv_sigma[0], sn.inv_sigma[1], a.z_top, false);
@@ -747,8 +753,8 @@ __global__ void __launch_bounds__(MT_THREADS) k_kick_r(FinishArgs a) {
     for (int l = 0; l < 2; l++) {
       const float pr = pc[2 * N + l] + f * gc[2 * N + l];
       pc[2 * N + l] = pr;
-      kin += 0.5 * (double)pr * pr;
-      if (MODE != KICK_HALF_LAST) xc[2 * N + l] += eps * pr;
+      kin += 0.5 * (double)mi(a, 2 * N + l) * pr * pr;
+      if (MODE != KICK_HALF_LAST) xc[2 * N + l] += eps * mi(a, 2 * N + l) * pr;
       s_new[l] = xc[2 * N + l];
     }
     s_kin = kin;
@@ -762,10 +768,10 @@ __global__ void __launch_bounds__(MT_THREADS) k_kick_r(FinishArgs a) {
     pc[k] = p0;
     pc[N + k] = p1;
     if (MODE == KICK_HALF_LAST) {
-      v.s1 += 0.5 * ((double)p0 * p0 + (double)p1 * p1);
+      v.s1 += 0.5 * ((double)mi(a, k) * p0 * p0 + (double)mi(a, N + k) * p1 * p1);
       continue;
     }
-    const float x0 = xc[k] + eps * p0, x1 = xc[N + k] + eps * p1;
+    const float x0 = xc[k] + eps * mi(a, k) * p0, x1 = xc[N + k] + eps * mi(a, N + k) * p1;
     xc[k] = x0;
     xc[N + k] = x1;
     const NodeH h = node_heights(x0, x1, sp.inv_sigma[0], sp.inv_sigma[1], a.z_top, false);
@@ -800,12 +806,15 @@ __device__ __forceinline__ double block_dot(const float *a, const float *b, int 
 }
 
 // U-turn(p⁻, p⁺, ρ): p⁻·(ρ - (p⁻+p⁺)/2) <= 0 or p⁺·(ρ - (p⁻+p⁺)/2) <= 0
-__device__ __forceinline__ bool block_turning(const float *pl, const float *pr, const float *rho, int n) {
+// generalised U-turn with the velocities p# = M^-1 p at both ends (identity: p)
+__device__ __forceinline__ bool block_turning(const float *pl, const float *pr, const float *rho, int n,
+                                              const float *minv) {
   double v[2] = {0.0, 0.0};
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
     const double rs = (double)rho[k] - 0.5 * ((double)pl[k] + pr[k]);
-    v[0] += (double)pl[k] * rs;
-    v[1] += (double)pr[k] * rs;
+    const double m = minv ? (double)minv[k] : 1.0;
+    v[0] += m * (double)pl[k] * rs;
+    v[1] += m * (double)pr[k] * rs;
   }
   block_sum<2>(v);
   return v[0] <= 0.0 || v[1] <= 0.0;
@@ -844,8 +853,9 @@ __global__ void __launch_bounds__(MT_THREADS) k_nuts_begin(FinishArgs a, NutsArg
     for (int m = 0; m < 4; m++) {
       const int k = 4 * q + m;
       if (k < P) {
-        const float pz = (float)z[m];
-        v[0] += 0.5 * (double)pz * pz;
+        const float mm = mi(a, k);
+        const float pz = a.minv ? (float)(z[m] / sqrt((double)mm)) : (float)z[m];
+        v[0] += 0.5 * (double)mm * pz * pz;
         n.pL[o + k] = pz;
         n.pR[o + k] = pz;
         n.rho[o + k] = pz;
@@ -903,7 +913,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_nuts_kick(FinishArgs a, NutsArgs
   for (int k = threadIdx.x; k < P; k += blockDim.x) {
     const float pk = pp[k] + 0.5f * e * gg[k];
     pp[k] = pk;
-    th[k] = th[k] + e * pk;
+    th[k] = th[k] + e * mi(a, k) * pk;
   }
   __syncthreads();
   double is0 = a.inv_sigma[0], is1 = a.inv_sigma[1];
@@ -944,7 +954,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_nuts_leaf(FinishArgs a, NutsArgs
   for (int k = threadIdx.x; k < P; k += blockDim.x) {
     const float pk = pp[k] + 0.5f * e * gg[k];
     pp[k] = pk;
-    v[0] += 0.5 * (double)pk * pk;
+    v[0] += 0.5 * (double)mi(a, k) * pk * pk;
   }
   block_sum<1>(v);
   if (threadIdx.x == 0) {
@@ -991,7 +1001,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_nuts_leaf(FinishArgs a, NutsArgs
       const float *rl = n.rck + i * cs + o, *rsl = n.rsck + i * cs + o;
       for (int k = threadIdx.x; k < P; k += blockDim.x) tmp[k] = rhos[k] - rsl[k] + rl[k];
       __syncthreads();
-      if (block_turning(rl, pp, tmp, P)) {
+      if (block_turning(rl, pp, tmp, P, n.minv)) {
         if (threadIdx.x == 0) s_turn = 1;
       }
       __syncthreads();
@@ -1043,7 +1053,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_nuts_merge(NutsArgs n, int P, in
   copyP((s.dir > 0 ? n.gR : n.gL) + o, n.gw + o, P);
   for (int k = threadIdx.x; k < P; k += blockDim.x) n.rho[o + k] += n.rhos[o + k];
   __syncthreads();
-  const bool turn = block_turning(n.pL + o, n.pR + o, n.rho + o, P);
+  const bool turn = block_turning(n.pL + o, n.pR + o, n.rho + o, P, n.minv);
   if (threadIdx.x == 0) {
     if (turn || j + 1 >= max_depth) s.active = 0;
     else atomicOr(n.any_active, 1);
@@ -1344,8 +1354,8 @@ __global__ void __launch_bounds__(MT_THREADS) k_ncp_kick(FinishArgs a) {
   for (int k = threadIdx.x; k < P; k += blockDim.x) {
     const float p = pc[k] + f * gc[k];
     pc[k] = p;
-    if (MODE != KICK_HALF_LAST) xc[k] = xc[k] + eps * p;
-    else kin[0] += 0.5 * (double)p * p;
+    if (MODE != KICK_HALF_LAST) xc[k] = xc[k] + eps * mi(a, k) * p;
+    else kin[0] += 0.5 * (double)mi(a, k) * p * p;
   }
   if (MODE == KICK_HALF_LAST) {
     block_sum<1>(kin);
@@ -1407,6 +1417,7 @@ static FinishArgs base_args(mt_problem *p, int C) {
   a.cs = p->d_cs;
   a.ncp = p->ncp;
   a.xw = p->d_xw;
+  a.minv = p->d_minv;
   return a;
 }
 
@@ -1544,7 +1555,7 @@ cudaError_t launch_momenta(mt_problem *p, int C, float *mom, uint64_t seed, uint
                            uint64_t chain_offset, cudaStream_t s) {
   if (C <= 0) return cudaSuccess;
   int64_t n = (int64_t)C * ((p->P + 3) / 4);
-  k_momenta<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(C, p->P, mom, seed, iter, chain_offset);
+  k_momenta<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(C, p->P, mom, seed, iter, chain_offset, p->d_minv);
   p->all_launches++;
   return cudaGetLastError();
 }
@@ -1641,6 +1652,7 @@ static NutsArgs nuts_args(mt_problem *p) {
   n.st = p->nuts_st;
   n.any_active = p->nuts_flags;
   n.any_sub = p->nuts_flags + 1;
+  n.minv = p->d_minv;
   return n;
 }
 

@@ -100,6 +100,7 @@ struct FinishArgs {
   const double *cs;             // [N] c_ab = 2(cos 2πa/n_x + cos 2πb/n_y) (torus spectrum)
   int ncp;                      // f2 non-centred: state (z_0, z_1, ρ_0, ρ_1), x = U(r) z
   double *xw;                   // [C][2N] fp64 x = U z of the current state (ncp)
+  const float *minv;            // [P] diagonal inverse mass (null: identity)
 };
 
 enum { FIN_PLAIN = 0, FIN_STEP = 1, FIN_LAST = 2 };
@@ -119,6 +120,7 @@ struct NutsArgs {
   double *lpw_out;                        // logp of the working state (K3 output)
   NutsChain *st;
   int *any_active, *any_sub;
+  const float *minv;                      // [P] diagonal inverse mass (null: identity)
 };
 
 struct VxItem { int node, kb; long long eb, ee; };   // Gᵀ work item (voxel.cu)
@@ -162,6 +164,7 @@ struct mt_problem {
   int sample_r = 0;             // f2: the CAR r_l are sampled (two more parameters per chain)
   double *d_cs = nullptr;       // [N] torus spectrum table (sample_r)
   int ncp = 0;                  // f2 non-centred parameterisation (implies sample_r)
+  float *d_minv = nullptr;      // [P] diagonal inverse mass (null until mt_set_inverse_mass)
   double *mb_red = nullptr;     // few-chain multi-block K3 scratch: [16][3] sums
   unsigned *mb_band = nullptr;  //   [16][4] band as float bits
   unsigned *mb_ticket = nullptr;   // [16] last-block tickets

@@ -73,6 +73,26 @@ class DualAveraging:
         return math.exp(self.log_eps_bar)
 
 
+def mass_windows(n_warmup: int, init: int = 75, term: int = 50, base: int = 25):
+    """Stan-style slow-adaptation windows [(start, end)] of the warm-up (R19b):
+    an initial buffer, doubling windows, a terminal buffer; scaled 15% / 75% / 10%
+    when the warm-up is shorter than init + term + base.  Empty below 20 iterations."""
+    if n_warmup < 20:
+        return []
+    if init + term + base > n_warmup:
+        init, term = int(0.15 * n_warmup), int(0.1 * n_warmup)
+        base = n_warmup - init - term
+    out, start, w = [], init, base
+    end_slow = n_warmup - term
+    while start < end_slow:
+        end = start + w
+        if end + 2 * w > end_slow:       # the last window absorbs the remainder
+            end = end_slow
+        out.append((start, end))
+        start, w = end, 2 * w
+    return out
+
+
 def rhat_from_partials(part: np.ndarray, n_chains: int, n: int) -> np.ndarray:
     """Classic R-hat per parameter from Σ m̄_c, Σ m̄_c², Σ s²_c over all chains."""
     s1, s2, sv = part
@@ -133,7 +153,8 @@ class ChainShard:
 
     def __init__(self, problem, x0: np.ndarray, seed: int, L: int, eps0: float,
                  chain_offset: int = 0, n_chains_total: Optional[int] = None, group=None,
-                 stream=None, replicated: bool = False, sampler: str = "hmc", max_depth: int = 8):
+                 stream=None, replicated: bool = False, sampler: str = "hmc", max_depth: int = 8,
+                 adapt_mass: bool = False):
         import torch
         self.torch = torch
         self.pb = problem
@@ -148,6 +169,8 @@ class ChainShard:
         if sampler not in ("hmc", "nuts"):
             raise ValueError(f"sampler {sampler!r}")
         self.sampler, self.max_depth = sampler, max_depth   # NUTS: 2^max_depth leaves cap
+        self.adapt_mass = adapt_mass                        # diagonal mass from warm-up windows (R19b)
+        self.minv = None
         t = lambda *s, dt=torch.float32: torch.zeros(s, dtype=dt, device=self.dev)  # noqa: E731
         self.x = torch.from_numpy(np.ascontiguousarray(x0, np.float32)).to(self.dev)
         self.logp = t(self.C, dt=torch.float64)
@@ -244,10 +267,32 @@ class ChainShard:
         self._allreduce(part)
         return rhat_from_partials(part.cpu().numpy(), self.n_total, self.n_samples)
 
+    def _mass_from_window(self, wmean, wm2, n: int):
+        """Pooled within-chain variance of the window's draws -> regularised M^-1."""
+        torch = self.torch
+        tot = torch.stack([wm2.sum(0).double(), torch.full((self.P,), float(self.C * (n - 1)),
+                                                           dtype=torch.float64, device=self.dev)])
+        self._allreduce(tot)
+        var = tot[0] / tot[1]
+        minv = (n / (n + 5.0)) * var + 1e-3 * (5.0 / (n + 5.0))
+        self.minv = minv.float().contiguous()
+        self.pb.set_inverse_mass(self.minv)
+
     def run(self, n_warmup: int, n_sample: int):
         accs = []
-        for _ in range(n_warmup):
+        windows = mass_windows(n_warmup) if self.adapt_mass else []
+        wmean = wm2 = None
+        for i in range(n_warmup):
             accs.append(self.step(adapt=True))
+            for (a, b) in windows:
+                if a <= i < b:
+                    if i == a:
+                        wmean = self.torch.zeros_like(self.x)
+                        wm2 = self.torch.zeros_like(self.x)
+                    self.pb.stats_update(self.C, x=self.x, n_prev=i - a, mean=wmean, m2=wm2, stream=self.stream)
+                    if i == b - 1:   # window end: new mass, restart step-size adaptation (R19b)
+                        self._mass_from_window(wmean, wm2, b - a)
+                        self.da = DualAveraging(float(self.eps[0]))
         self.end_warmup()
         for _ in range(n_sample):
             self.step(adapt=False, sample=True)
