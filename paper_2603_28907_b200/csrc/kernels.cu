@@ -1174,7 +1174,10 @@ __device__ void circ_apply_fft(const Dft &d, const double *cs, double r, int mod
     for (int lh = ln - 1; lh >= 0; lh--) {
       const int h = 1 << lh, tstep = n >> (lh + 1);
       for (int t = threadIdx.x; t < lines << (ln - 1); t += blockDim.x) {
-        const int line = t >> (ln - 1), bfly = t & ((n >> 1) - 1);
+        // rows: consecutive threads take consecutive butterflies of a row; columns:
+        // consecutive columns (a column-major walk would put a warp on one bank)
+        const int line = pass ? (t & (lines - 1)) : t >> (ln - 1);
+        const int bfly = pass ? t >> by : t & ((n >> 1) - 1);
         const int g = (bfly >> lh) << (lh + 1), k = bfly & (h - 1);
         const int base = pass ? line : line * ny;
         const int i0 = base + (g + k) * st, i1 = i0 + h * st;
@@ -1203,7 +1206,8 @@ __device__ void circ_apply_fft(const Dft &d, const double *cs, double r, int mod
     for (int lh = 0; lh < ln; lh++) {
       const int h = 1 << lh, tstep = n >> (lh + 1);
       for (int t = threadIdx.x; t < lines << (ln - 1); t += blockDim.x) {
-        const int line = t >> (ln - 1), bfly = t & ((n >> 1) - 1);
+        const int line = pass ? t >> (ln - 1) : (t & (lines - 1));   // pass 0: columns
+        const int bfly = pass ? t & ((n >> 1) - 1) : t >> by;
         const int g = (bfly >> lh) << (lh + 1), k = bfly & (h - 1);
         const int base = pass ? line * ny : line;
         const int i0 = base + (g + k) * st, i1 = i0 + h * st;
@@ -1220,11 +1224,14 @@ __device__ void circ_apply_fft(const Dft &d, const double *cs, double r, int mod
   }
 }
 
+#ifndef MT_FFT_MIN_N
+#define MT_FFT_MIN_N 0
+#endif
 template <class In>
 __device__ __forceinline__ void circ_apply(const Dft &d, const double *cs, double r, int mode, In v) {
-  // the FFT's 2 log2 N synchronised stages only pay off on large grids (measured:
-  // Medium n = 32 DFT 6.00 vs FFT 6.41 ms per evaluation; ray-sharded n = 64 DFT 1.50 vs FFT 1.31 ms)
-  if ((d.nx & (d.nx - 1)) == 0 && (d.ny & (d.ny - 1)) == 0 && d.N >= 2048) circ_apply_fft(d, cs, r, mode, v);
+  // power-of-two grids: FFT (measured per evaluation, Medium n = 32: DFT 6.01 vs FFT 5.61 ms;
+  // ray-sharded n = 64: DFT 1.50 vs FFT 0.71 ms); other sizes: the direct sums
+  if ((d.nx & (d.nx - 1)) == 0 && (d.ny & (d.ny - 1)) == 0 && d.N >= MT_FFT_MIN_N) circ_apply_fft(d, cs, r, mode, v);
   else circ_apply_dft(d, cs, r, mode, v);
 }
 
