@@ -6,6 +6,7 @@
 // P = 2 n_x n_y <= 8192 floats, so a block streams it once (coalesced), does
 // the 5-point periodic stencil from shared memory and reduces per-chain
 // scalars without atomics.
+#include <cooperative_groups.h>
 #include <curand_philox4x32_x.h>
 #include <math.h>
 
@@ -1348,6 +1349,113 @@ __global__ void __launch_bounds__(MT_THREADS) k_ncp_finish(FinishArgs a) {
   }
 }
 
+// Cluster variants: a 2-CTA thread-block cluster per chain, CTA l = surface l,
+// so a chain's two surfaces transform on two SMs at once.  The heights need
+// x_0 and x_1 at every node: each CTA reads its partner's x through
+// distributed shared memory; the per-chain scalars meet the same way.
+namespace cgx = cooperative_groups;
+
+__global__ void __cluster_dims__(1, 2, 1) __launch_bounds__(MT_THREADS) k_ncp_heights_cl(FinishArgs a, const float *v) {
+  extern __shared__ double sm[];
+  cgx::cluster_group cluster = cgx::this_cluster();
+  const int c = blockIdx.x, l = blockIdx.y, N = a.N;
+  const float *vc = v + (size_t)c * a.P;
+  const Spec sp = block_spectrum(a.cs, N, vc[2 * N], vc[2 * N + 1], false);
+  const Dft d = dft_setup(sm, a.nx, a.ny);
+  double *xl = sm + 4 * N + 4 * MT_MAX_AXIS;   // [N] this surface's x
+  __shared__ float bandp[4];
+  const float *z = vc + l * N;
+  circ_apply(d, a.cs, sp.r[l], 0, [&](int k) { return (double)z[k]; });
+  double *xw = a.xw + (size_t)c * 2 * N + (size_t)l * N;
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    xl[k] = d.vre[k];
+    xw[k] = d.vre[k];
+  }
+  cluster.sync();
+  const double *x0 = l == 0 ? xl : cluster.map_shared_rank(xl, 0);
+  const double *x1 = l == 1 ? xl : cluster.map_shared_rank(xl, 1);
+  BlockRed vr = {3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f, 0.0, 0.0, 0};
+  const int half = (N + 1) / 2, k0 = l * half, k1 = min(N, k0 + half);   // CTA l: half of the nodes
+  for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+    const NodeH h = node_heights(x0[k], x1[k], sp.inv_sigma[0], sp.inv_sigma[1], a.z_top, false);
+    a.H[tix(c, 0, k, N)] = h.H0;
+    a.H[tix(c, 1, k, N)] = h.H1;
+    a.Hlo[tix(c, 0, k, N)] = h.L0;
+    a.Hlo[tix(c, 1, k, N)] = h.L1;
+    vr.mn0 = fminf(vr.mn0, h.H0); vr.mx0 = fmaxf(vr.mx0, h.H0);
+    vr.mn1 = fminf(vr.mn1, h.H1); vr.mx1 = fmaxf(vr.mx1, h.H1);
+  }
+  const BlockRed r = block_reduce(vr);
+  if (threadIdx.x == 0) { bandp[0] = r.mn0; bandp[1] = r.mx0; bandp[2] = r.mn1; bandp[3] = r.mx1; }
+  cluster.sync();
+  if (l == 0 && threadIdx.x == 0) {
+    const float *o = cluster.map_shared_rank(bandp, 1);
+    a.band[c] = make_float4(fminf(bandp[0], o[0]), fmaxf(bandp[1], o[1]), fminf(bandp[2], o[2]), fmaxf(bandp[3], o[3]));
+  }
+  cluster.sync();   // keep this CTA's shared memory alive until the partner has read it
+}
+
+__global__ void __cluster_dims__(1, 2, 1) __launch_bounds__(MT_THREADS) k_ncp_finish_cl(FinishArgs a) {
+  extern __shared__ double sm[];
+  cgx::cluster_group cluster = cgx::this_cluster();
+  const int c = blockIdx.x, l = blockIdx.y, N = a.N, P = a.P;
+  const float *vc = a.x + (size_t)c * P;
+  float *gc = a.grad + (size_t)c * P;
+  const Spec sp = block_spectrum(a.cs, N, vc[2 * N], vc[2 * N + 1], false);
+  double *gx = sm + 4 * N + 4 * MT_MAX_AXIS;   // [N] ∂ll/∂x_l
+  __shared__ double part[3];                   // Σ z_l², non-finite flag, ∂/∂ρ_l
+  const double *xw = a.xw + (size_t)c * 2 * N;
+  const float *Gt = a.G;
+  double acc[2] = {0.0, 0.0};   // Σ t_l gx_l, Σ z_l²
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    const NodeH h = node_heights(xw[k], xw[N + k], sp.inv_sigma[0], sp.inv_sigma[1], a.z_top, true);
+    const double G0 = Gt[tix(c, 0, k, N)], G1 = Gt[tix(c, 1, k, N)];
+    const double g = l == 0 ? G0 * h.J0 + G1 * h.J10 : G1 * h.J11;
+    gx[k] = g;
+    acc[0] += (l == 0 ? h.t0 : h.t1) * g;
+    const double zv = vc[l * N + k];
+    acc[1] += zv * zv;
+  }
+  block_sum<2>(acc);
+  cluster.sync();   // both CTAs have read ∂ℓ/∂H: clear it (CTA l its surface)
+  float *Gw = const_cast<float *>(a.G);
+  for (int k = threadIdx.x; k < N; k += blockDim.x) Gw[tix(c, l, k, N)] = 0.f;
+  const Dft d = dft_setup(sm, a.nx, a.ny);
+  int bad = 0;
+  circ_apply(d, a.cs, sp.r[l], 0, [&](int k) { return gx[k]; });   // U ∂ll/∂x_l
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    const float gz = (float)((a.prior_on ? -(double)vc[l * N + k] : 0.0) + d.vre[k]);
+    gc[l * N + k] = gz;
+    bad |= !isfinite(gz);
+  }
+  __syncthreads();
+  const float *z = vc + l * N;
+  circ_apply(d, a.cs, sp.r[l], 1, [&](int k) { return (double)z[k]; });   // (dU/dr) z_l
+  double sdot[1] = {0.0};
+  for (int k = threadIdx.x; k < N; k += blockDim.x) sdot[0] += gx[k] * d.vre[k];
+  block_sum<1>(sdot);
+  bad = __syncthreads_or(bad);
+  const double r = sp.r[l];
+  const double gr = r * (1.0 - r) * (sdot[0] - acc[0] * sp.dsig[l]) + (a.prior_on ? 1.0 - 2.0 * r : 0.0);
+  if (threadIdx.x == 0) {
+    gc[2 * N + l] = (float)gr;
+    part[0] = acc[1];
+    part[1] = (bad || !isfinite(gr)) ? 1.0 : 0.0;
+  }
+  cluster.sync();
+  if (l == 0 && threadIdx.x == 0) {
+    const double *o = cluster.map_shared_rank(part, 1);
+    double lp = a.ll[c];
+    if (a.prior_on)
+      lp += -0.5 * (part[0] + o[0]) - N * log(2.0 * M_PI) + log(sp.r[0]) + log1p(-sp.r[0]) + log(sp.r[1]) +
+            log1p(-sp.r[1]);
+    a.ll[c] = 0.0;
+    a.logp[c] = lp;
+    if (a.status) a.status[c] = (part[1] != 0.0 || o[1] != 0.0 || !isfinite(lp)) ? MT_STATUS_NONFINITE : 0;
+  }
+  cluster.sync();
+}
+
 // Leapfrog kicks / drifts in the non-centred coordinates (heights follow in
 // k_ncp_heights): KICK_HALF_DRIFT p += ε/2 g, z += ε p; KICK_FULL_DRIFT p += ε g,
 // z += ε p; KICK_HALF_LAST p += ε/2 g and the kinetic energy ½|p|².
@@ -1399,9 +1507,21 @@ static size_t ncp_smem(const mt_problem *p) {
     const int mx = (6 * MT_MAX_NODES + 4 * MT_MAX_AXIS) * (int)sizeof(double);
     cudaFuncSetAttribute(k_ncp_heights, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_ncp_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_ncp_heights_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_ncp_finish_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     attr = true;
   }
   return (size_t)(4 * p->N + 4 * MT_MAX_AXIS) * sizeof(double);
+}
+
+#ifndef MT_NCP_CLUSTER
+#define MT_NCP_CLUSTER 1
+#endif
+static void launch_ncp_heights(mt_problem *p, const FinishArgs &a, int C, const float *x, cudaStream_t s) {
+  if (MT_NCP_CLUSTER)
+    k_ncp_heights_cl<<<dim3(C, 2), MT_THREADS, ncp_smem(p) + (size_t)p->N * sizeof(double), s>>>(a, x);
+  else
+    k_ncp_heights<<<C, MT_THREADS, ncp_smem(p), s>>>(a, x);
 }
 
 static FinishArgs base_args(mt_problem *p, int C) {
@@ -1435,7 +1555,7 @@ cudaError_t launch_heights(mt_problem *p, int C, const float *x, float *H, float
   a.H = H;
   a.Hlo = p->d_Hlo;
   a.band = band;
-  if (p->ncp) k_ncp_heights<<<C, MT_THREADS, ncp_smem(p), s>>>(a, x);
+  if (p->ncp) launch_ncp_heights(p, a, C, x, s);
   else if (p->sample_r) k_heights_r<<<C, MT_THREADS, 0, s>>>(a, x);
   else k_heights<<<C, MT_THREADS, 0, s>>>(a, x);
   p->all_launches++;
@@ -1456,7 +1576,10 @@ cudaError_t launch_finish(mt_problem *p, int mode, int C, float *x, float *grad,
   }
   if (p->ncp) {   // unfused: the API drives kicks / drifts separately (k_ncp_kick)
     if (mode != FIN_PLAIN) return cudaErrorInvalidValue;
-    k_ncp_finish<<<C, MT_THREADS, ncp_smem(p) + (size_t)2 * p->N * sizeof(double), s>>>(a);
+    if (MT_NCP_CLUSTER)
+      k_ncp_finish_cl<<<dim3(C, 2), MT_THREADS, ncp_smem(p) + (size_t)p->N * sizeof(double), s>>>(a);
+    else
+      k_ncp_finish<<<C, MT_THREADS, ncp_smem(p) + (size_t)2 * p->N * sizeof(double), s>>>(a);
     p->all_launches++;
     return cudaGetLastError();
   }
@@ -1511,7 +1634,7 @@ cudaError_t launch_kick(mt_problem *p, int mode, int C, float *x, float *mom, co
     else k_ncp_kick<KICK_HALF_LAST><<<C, MT_THREADS, 0, s>>>(a);
     p->all_launches++;
     if (mode != KICK_HALF_LAST) {
-      k_ncp_heights<<<C, MT_THREADS, ncp_smem(p), s>>>(a, x);
+      launch_ncp_heights(p, a, C, x, s);
       p->all_launches++;
     }
     return cudaGetLastError();
@@ -1541,7 +1664,7 @@ cudaError_t launch_hmc_begin(mt_problem *p, int C, float *x, const double *logp,
                                        chain_offset);
   p->all_launches++;
   if (p->ncp) {   // heights of the drifted z (k_hmc_begin skipped them)
-    k_ncp_heights<<<C, MT_THREADS, ncp_smem(p), s>>>(a, x);
+    launch_ncp_heights(p, a, C, x, s);
     p->all_launches++;
   }
   return cudaGetLastError();
