@@ -661,3 +661,26 @@ def test_cuda_graph_capture_and_replay(gpu, problems, mode):
     assert np.allclose(lps.cpu().numpy(), lpe.cpu().numpy(), rtol=1e-6)
     if mode == "one_rank_comm":
         pb.detach_comm()
+
+
+def test_gpu_properties_on_random_geometries(gpu, oracle_problem):
+    """Property tests on the device path: for random (rough) ordered
+    surfaces, every ray's muck / air / rock lengths are non-negative and sum to
+    its in-box length, and they equal the oracle's within the north_star bound."""
+    from hypothesis import HealthCheck, given, settings
+    from hypothesis import strategies as st
+    from test_oracle_properties import random_heights
+    mp, op = gpu("small"), oracle_problem("small")
+    s_exit = np.array([op.ray_extent(q)[0] for q in range(op.R)])
+
+    @settings(max_examples=8, deadline=None, suppress_health_check=[HealthCheck.function_scoped_fixture])
+    @given(seed=st.integers(0, 2 ** 31 - 1), rough=st.floats(0.0, 1.0))
+    def check(seed, rough):
+        H = random_heights(np.random.default_rng(seed), op.nx, rough=rough).astype(np.float32)
+        L, O = mp.path_lengths(torch.from_numpy(H[None]).to(DEV))
+        L = L.cpu().numpy()[0].astype(np.float64)
+        assert np.all(L >= -1e-3)
+        assert np.allclose(L.sum(1), s_exit, rtol=1e-5, atol=1e-3)
+        Lo, _ = op.path_lengths(H[None].astype(np.float64))
+        assert np.max(np.abs(L - Lo[0]) / s_exit[:, None]) <= 1e-5
+    check()
