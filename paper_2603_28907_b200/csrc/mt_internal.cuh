@@ -224,6 +224,11 @@ cudaError_t launch_finish(mt_problem *p, int mode, int C, float *x, float *grad,
                           int32_t *status, float *mom, const float *eps, float *kin,
                           cudaStream_t s);
 bool use_mb(const mt_problem *p, int C);   // few chains: multi-block K3 and kicks, unfused leapfrog
+FinishArgs base_args(mt_problem *p, int C);   // per-problem constants of the per-chain kernels
+// ncp.cu (f2 non-centred): heights of x = U z, K3, kick / drift (+ heights)
+void launch_ncp_heights(mt_problem *p, const FinishArgs &a, int C, const float *x, cudaStream_t s);
+void launch_ncp_finish(mt_problem *p, const FinishArgs &a, int C, cudaStream_t s);
+void launch_ncp_kick(mt_problem *p, int mode, const FinishArgs &a, int C, cudaStream_t s);
 cudaError_t launch_kick_drift(mt_problem *p, int C, float *x, float *mom, const float *grad,
                               const float *eps, cudaStream_t s);
 cudaError_t launch_hmc_begin(mt_problem *p, int C, float *x, const double *logp,
