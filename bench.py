@@ -115,32 +115,48 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
 
 
-def cpu_baseline(seconds: float, chains: int = 4, name: str = "chain_sharded", nz: int = 0):
+def cpu_baseline(seconds: float, chains: int = 4, name: str = "chain_sharded", nz: int = 0,
+                 mode: str = "exact", states: str = "posterior"):
     """The fp64 oracle, as it stands, on this host's cores: the workload's
-    geometry, `chains` chains x all its rays per evaluation, repeated for ~`seconds`
-    (nz > 0: the voxel / linearised model's oracle, G rebuilt by every call as the
-    oracle does)."""
+    geometry, `chains` chains x all its rays per evaluation, repeated for ~`seconds`.
+    nz > 0: the voxel / linearised model's oracle (G rebuilt by every call, as the
+    oracle does); mode "sample_r" / "noncentred": the f2 oracles; states "prior":
+    prior-draw chain states."""
     import numpy as np
 
     import oracle
     from paper_2603_28907_b200 import inputs
     prob = inputs.make_problem(name)
     op = oracle.Problem(prob)
-    x = inputs.chain_states(prob["x_true"], chains, inputs.CONFIGS[name].seed).astype(np.float64)
+    cfg = inputs.CONFIGS[name]
+    x = (inputs.prior_states(name, chains) if states == "prior"
+         else inputs.chain_states(prob["x_true"], chains, cfg.seed)).astype(np.float64)
+    rho = np.log(np.asarray(cfg.car_r) / (1.0 - np.asarray(cfg.car_r)))
+    if mode == "sample_r":
+        x = np.concatenate([x, np.broadcast_to(rho, (chains, 2))], axis=1)
+    elif mode == "noncentred":
+        from paper_2603_28907_b200.hmc import noncentred_state
+        x = noncentred_state(x, rho, cfg.n, cfg.n).astype(np.float64)
+    href = np.asarray(prob["H_true"], np.float32).astype(np.float64)
     t0 = time.perf_counter()
     n = 0
     while True:
         if nz:
-            op.voxel_logpost_grad(x, np.asarray(prob["H_true"], np.float32).astype(np.float64), nz)
+            op.voxel_logpost_grad(x, href, nz)
+        elif mode == "sample_r":
+            op.logpost_grad_r(x)
+        elif mode == "noncentred":
+            op.logpost_grad_ncp(x)
         else:
             op.logpost_grad(x)
         n += 1
         if time.perf_counter() - t0 >= seconds:
             break
     dt = time.perf_counter() - t0
+    what = (f" (voxel model, n_z={nz})" if nz else f" ({mode})" if mode != "exact" else "")
     return {"value": n * chains * op.R / dt, "unit": UNIT, "cores": oracle.num_threads(),
             "kind": "oracle",
-            "sample": f"{name} geometry{' (voxel model, n_z=%d)' % nz if nz else ''}, {chains} near-posterior "
+            "sample": f"{name} geometry{what}, {chains} {'prior-draw' if states == 'prior' else 'near-posterior'} "
                       f"chain(s) x {op.R} rays per evaluation, "
                       f"{n} evaluations ({n * chains * op.R:.3g} chain-ray pairs) in {dt:.1f} s, fp64"}
 
@@ -386,7 +402,9 @@ def main():
     base = None
     if ws == 1 and not args.no_cpu_baseline:
         base = cpu_baseline(args.cpu_seconds, chains=1 if ray else 4, name=args.workload,
-                            nz=args.nz if voxel else 0)
+                            nz=args.nz if voxel else 0,
+                            mode="noncentred" if args.noncentred else "sample_r" if args.sample_r else "exact",
+                            states=args.states)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f32",

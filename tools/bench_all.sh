@@ -5,10 +5,10 @@ B=gpurun_out/benchall
 rm -f $B.*.log
 timeout 600 python bench.py > $B.default.log 2>&1
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $B.reference.log 2>&1
-timeout 900 python bench.py --states prior --no-cpu-baseline > $B.prior.log 2>&1
+timeout 900 python bench.py --states prior > $B.prior.log 2>&1
 timeout 600 python bench.py --workload ray_sharded --steps 50 > $B.ray.log 2>&1
 timeout 600 python bench.py --model voxel > $B.voxel.log 2>&1
 timeout 600 python bench.py --model voxel --workload ray_sharded --steps 50 > $B.voxelray.log 2>&1
-timeout 600 python bench.py --noncentred --no-cpu-baseline > $B.ncp.log 2>&1
-timeout 600 python bench.py --sample-r --no-cpu-baseline > $B.sampler.log 2>&1
-timeout 900 python bench.py --sampler nuts --chains-total 1024 --steps 3 --no-cpu-baseline > $B.nuts.log 2>&1
+timeout 600 python bench.py --noncentred > $B.ncp.log 2>&1
+timeout 600 python bench.py --sample-r > $B.sampler.log 2>&1
+timeout 900 python bench.py --sampler nuts --chains-total 1024 --steps 3 > $B.nuts.log 2>&1
