@@ -169,3 +169,32 @@ def test_ncp_chain_sharded_8192_bench_launch(problems, oracle_problem):
     for k, c in enumerate(sel):
         assert abs(lp[c].item() - ref["logp"][k]) <= 1e-4 * abs(ref["logp"][k])
         assert rel_l2(g[c].cpu().numpy().astype(np.float64), ref["grad"][k]) <= 1e-3
+
+
+def test_ncp_with_the_voxel_model(problems, oracle_problem):
+    """Non-centred (f2) × voxel model (f3): with ρ = logit(car_r) the copula scale
+    σ(r) is the fixed-r one, so the voxel oracle at x = U z gives the likelihood;
+    logp = ll − ½|z|² − N ln 2π + Σ ln r(1−r) and ∂/∂z = −z + U ∂ll/∂x."""
+    from test_oracle_prior import dense_Q
+    prob = problems("tiny")
+    op = oracle_problem("tiny")
+    cfg = inputs.CONFIGS["tiny"]
+    r = cfg.car_r[0]
+    rho = np.log(r / (1 - r))
+    C = 3
+    v = ncp_states(prob, op, C, cfg.seed, rho=(rho, rho))
+    mp = Problem(prob, device=0, max_chains=C, noncentred=True)
+    Hr = np.asarray(prob["H_true"], np.float32)
+    mp.voxel_model(60, Hr)
+    lp, g = mp.logpost_grad(torch.from_numpy(v).to(DEV))
+    U = circulant(oracle.ncp_kernel(op.nx, op.ny, r)[0])
+    Q = dense_Q(op.nx, op.ny, r)
+    for c in range(C):
+        z = v[c, :op.P].astype(np.float64)
+        x = np.concatenate([U @ z[:op.N], U @ z[op.N:]])
+        o = op.voxel_logpost_grad(x[None], Hr.astype(np.float64), 60)
+        gx_ll = o["grad"][0] + np.concatenate([Q @ x[:op.N], Q @ x[op.N:]])   # remove the centred prior
+        ref_lp = o["ll_dev"][0] - 0.5 * z @ z - op.N * np.log(2 * np.pi) + 2 * np.log(r * (1 - r))
+        ref_gz = -z + np.concatenate([U @ gx_ll[:op.N], U @ gx_ll[op.N:]])
+        assert abs(lp[c].item() - ref_lp) <= 1e-4 * abs(ref_lp)
+        assert rel_l2(g[c, :op.P].cpu().numpy().astype(np.float64), ref_gz) <= 1e-3
