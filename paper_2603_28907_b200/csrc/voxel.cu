@@ -15,14 +15,15 @@
 //   V3 k_vx_bwd    ∂ℓ/∂H_l(node) = Σ_k (Σ_p G_pv r_p) ∂R̂_v/∂H_l     (SpMVᵀ + chain rule)
 // V3 accumulates ∂ℓ/∂H (one warp per run of <= 512 CSC entries inside a node
 // column, so the voxels next to a detector, crossed by every ray of it, are
-// split over many warps; float atomics) into
-// the same chain-interleaved workspace the exact tracer fills, so K3, the leapfrog/HMC/NUTS drivers, sampled r and ray sharding are
-// unchanged.  Two layouts: chain lanes (C >= 16: a warp = one row / column ×
-// 32 chains, every G entry loaded once per 32 chains, ΔR and r gathers are
-// 128-B lines) and row lanes (C < 16: the lanes split the row / column, warp
-// shuffle reduction, one chain at a time).  Grids are group-major
-// (blockIdx.y = chain group), so one group's ΔR (n_grid·128 B) and r (R·128 B)
-// stay in L2 while its blocks run.
+// split over many warps; float atomics) into the same chain-interleaved
+// workspace the exact tracer fills, so K3, the leapfrog/HMC/NUTS drivers,
+// sampled r and ray sharding are unchanged.  Two layouts: chain lanes
+// (C >= 16: a warp = one row / column × W = 32·VEC chains, VEC = 1, 2, 4
+// chains per lane, every G entry loaded once per W chains, ΔR and r gathers
+// are 128·VEC-byte lines) and row lanes (C < 16: 8-lane teams per CSR row,
+// warp lanes over a CSC run, one chain at a time).  Only the layers within
+// 24 γ of the chain group's height band are read (per-row layer-bucket
+// offsets).  Grids are group-major (blockIdx.y = chain group).
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
@@ -48,8 +49,8 @@ struct VoxArgs {
   float rho_m, rho_a, rho_r;
   const float *H;          // chain-interleaved heights (tix layout)
   const float *R0;         // [ng]
-  float *dR;               // CL: [grp][ng][32]; RL: [c][ng]
-  float *r;                // CL: [grp][R][32];  RL: [c][R]
+  float *dR;               // CL: [grp][ng][32][VEC]; RL: [c][ng]
+  float *r;                // CL: [grp][R][32][VEC];  RL: [c][R]
   const int64_t *rowptr;   // [R+1]
   const uint4 *kofs;       // [R]: 8 uint16 offsets (from the row start) of the first entry of layer >= b·kb
   int kb;                  // layers per offset bucket
