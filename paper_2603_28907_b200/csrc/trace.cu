@@ -239,10 +239,26 @@ __device__ __forceinline__ bool solve32(float h00, float h10, float h01, float h
   const bool p0 = g0 > 0.f;
   const float a2 = 2.f * g2;
   const bool vin = -g1 * a2 > 0.f && fabsf(g1) < Ls * fabsf(a2);   // vertex inside (0, Δs)
+#ifndef MT_LAZY_ROOTS
+#define MT_LAZY_ROOTS 1
+#endif
+#if MT_LAZY_ROOTS
+  // the roots only where a crossing is possible (a no-crossing cell skips RSQ + 2 RCP)
+  auto roots = [&](float &ta, float &tb) {
+    float q = 0.f;
+    if (disc > 0.f) q = -0.5f * (g1 + copysignf(disc * rsqrtf(disc), g1));
+    ta = __fdividef(g0, q);
+    tb = __fdividef(q, g2);
+  };
+#else
   float q = 0.f;
   if (disc > 0.f) q = -0.5f * (g1 + copysignf(disc * rsqrtf(disc), g1));
-  const float ta = __fdividef(g0, q), tb = __fdividef(q, g2);       // the two roots (tb = ±inf if g2 = 0)
+  const float ta0 = __fdividef(g0, q), tb0 = __fdividef(q, g2);       // the two roots (tb = ±inf if g2 = 0)
+  auto roots = [&](float &ta, float &tb) { ta = ta0; tb = tb0; };
+#endif
   if (p0 != (gL > 0.f)) {                         // exactly one crossing
+    float ta, tb;
+    roots(ta, tb);
     // the root in [0, Δs]: of the two, the one nearer the interval (rounding
     // can put the true root just outside when it sits at a cell edge)
     const float ca = fminf(fmaxf(ta, 0.f), Ls), cb = fminf(fmaxf(tb, 0.f), Ls);
@@ -252,6 +268,8 @@ __device__ __forceinline__ bool solve32(float h00, float h10, float h01, float h
     B += p0 ? t : Ls - t;
     emit(u0 + al * t, v0 + be * t, __fdividef(1.f, fabsf(gp)));
   } else if (disc > 0.f && vin && ((g2 > 0.f) == p0)) {   // two crossings
+    float ta, tb;
+    roots(ta, tb);
     const float t1 = fminf(ta, tb), t2 = fmaxf(ta, tb);
     const float gp1 = g1 + a2 * t1, gp2 = g1 + a2 * t2;
     if (fabsf(gp1) < GTHR || fabsf(gp2) < GTHR) return false;
