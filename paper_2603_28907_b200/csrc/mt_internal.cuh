@@ -62,6 +62,7 @@ struct TraceArgs {
   int64_t rays_per_block;
   int C;                        // chains in this call
   const float *H;               // [C][2][N] heights
+  const float2 *H2;             // chain lanes: paired heights (H(i,j), H(i,j+1)) per element
   const float *Hlo;             // fp32 residuals of the fp64 heights (0 for caller heights): the
                                 //   fp64 re-solves of ill-conditioned cells use H + Hlo (HP2)
   const float4 *band;           // [C] (min H0, max H0, min H1, max H1)
@@ -187,6 +188,7 @@ struct mt_problem {
   unsigned *d_redo = nullptr;   // (max_chains x R)-bit overflow bitmap of the deferred-pair queue
   int64_t trav_cells = 0;
   float *d_H = nullptr, *d_G = nullptr, *d_Hlo = nullptr;
+  float2 *d_H2 = nullptr;       // paired heights for the chain-lanes trace (trace.cu k_pair_heights)
   float *d_Hc = nullptr;        // [min(max_chains, 16)][2N] contiguous heights for the ray-lanes trace
   float4 *d_band = nullptr;
   double *d_ll = nullptr;

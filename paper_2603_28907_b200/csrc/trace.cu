@@ -307,6 +307,9 @@ __shared__ float sgeo[4][MT_MAX_AXIS];   // X, Y, 1/ΔX, 1/ΔY
 #ifndef MT_RCAP
 #define MT_RCAP 3
 #endif
+#ifndef MT_H2
+#define MT_H2 1
+#endif
 #ifndef MT_RL_GLOBAL_H
 #define MT_RL_GLOBAL_H 1
 #endif
@@ -588,9 +591,16 @@ __device__ __forceinline__ void cw_surface(const float *__restrict__ Hg, unsigne
                                            float zmax, float &B, int &n, int &defer, float4 *rec) {
   if (zb <= zmin) { B += Ls; return; }            // below the chain's lowest node of this surface
   if (za >= zmax) return;                         // above its highest node
+#if MT_H2
+  // paired heights: element k holds (H(i,j), H(i,j+1)), so a cell's four corners are two 8-byte loads
+  const float2 *p2 = reinterpret_cast<const float2 *>(Hg) + off;
+  const float2 r0 = __ldg(p2), r1 = __ldg(p2 + oy);
+  cw_solve<L>(make_float4(r0.x, r0.y, r1.x, r1.y), w, cg, za, zb, Ls, dz, B, n, defer, rec);
+#else
   const float *p = Hg + off;   // Hg: the heights array (kernel parameter); off: 32-bit element index
   cw_solve<L>(make_float4(__ldg(p), __ldg(p + 32), __ldg(p + oy), __ldg(p + oy + 32)), w, cg, za, zb, Ls,
               dz, B, n, defer, rec);
+#endif
 }
 
 template <int MODE, int NY>
@@ -640,8 +650,10 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a
         const float s1 = __int_as_float(w.y);
         const float zb = s1 * dz, Ls = s1 - s;
         const unsigned off = cell_off32(w.x) + gbase;   // 32-bit element index (C·P < 2^32)
-        cw_surface<0>(a.H, off, w.x, oy, cg, za, zb, Ls, dz, bd.x, bd.y, B0, n0, defer, rec);
-        cw_surface<1>(a.H, off + N * 32, w.x, oy, cg, za, zb, Ls, dz, bd.z, bd.w, B1, n1, defer, rec);
+        cw_surface<0>(MT_H2 ? reinterpret_cast<const float *>(a.H2) : a.H, off, w.x, oy, cg, za, zb, Ls, dz, bd.x,
+                      bd.y, B0, n0, defer, rec);
+        cw_surface<1>(MT_H2 ? reinterpret_cast<const float *>(a.H2) : a.H, off + N * 32, w.x, oy, cg, za, zb, Ls,
+                      dz, bd.z, bd.w, B1, n1, defer, rec);
         if (s1 >= s_hi) break;
         s = s1;
         za = zb;
@@ -1216,6 +1228,14 @@ static int64_t pick_splits(const mt_problem *p, int64_t groups, int64_t blocks_p
   return S < 1 ? 1 : (S > max_s ? max_s : S);
 }
 
+// Paired heights for the chain-lanes trace (MT_H2): H2[t] = (H[t], H[t + 32]),
+// i.e. node (i, j) with its neighbour (i, j + 1) in the same 8 bytes.
+__global__ void k_pair_heights(const float *__restrict__ H, float2 *__restrict__ H2, int64_t n) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  H2[t] = make_float2(H[t], t + 32 < n ? H[t + 32] : 0.f);
+}
+
 cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const float4 *band,
                          float *G, double *ll, float *L, float *O, cudaStream_t s) {
   if (C <= 0 || p->R <= 0) return cudaSuccess;
@@ -1229,6 +1249,12 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
   if (rec) cudaEventRecord(p->ev_a[p->n_rec], s);
   if (chain_lanes) {
     int groups = (C + 31) / 32;
+    if (MT_H2) {
+      const int64_t n = (int64_t)groups * 2 * p->N * 32;
+      k_pair_heights<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(H, p->d_H2, n);
+      a.H2 = p->d_H2;
+      p->all_launches++;
+    }
     // small ray chunks (~512 rays = 64 per warp): compact, L1-friendly regions per
     // block and many waves for load balance
     int64_t S = p->trace_s > 0 ? p->trace_s
