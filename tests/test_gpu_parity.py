@@ -673,7 +673,8 @@ def test_gpu_properties_on_random_geometries(gpu, oracle_problem):
     mp, op = gpu("small"), oracle_problem("small")
     s_exit = np.array([op.ray_extent(q)[0] for q in range(op.R)])
 
-    @settings(max_examples=8, deadline=None, suppress_health_check=[HealthCheck.function_scoped_fixture])
+    @settings(max_examples=8, deadline=None, derandomize=True,
+              suppress_health_check=[HealthCheck.function_scoped_fixture])
     @given(seed=st.integers(0, 2 ** 31 - 1), rough=st.floats(0.0, 1.0))
     def check(seed, rough):
         H = random_heights(np.random.default_rng(seed), op.nx, rough=rough).astype(np.float32)
