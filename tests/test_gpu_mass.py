@@ -119,3 +119,26 @@ def test_chainshard_adapts_a_diagonal_mass(problems):
     assert np.isfinite(out["eps"]) and out["eps"] > 0
     assert torch.isfinite(sh.x).all() and torch.isfinite(sh.logp).all()
     assert 0.4 < np.mean(out["warmup_accept"][-10:]) < 0.99
+
+
+def test_leapfrog_with_extreme_mass(problems, oracle_problem):
+    """Inverse masses spanning six decades (1e-3 .. 1e3) in the fused leapfrog."""
+    prob = problems("small")
+    op = oracle_problem("small")
+    C = 16
+    mp = Problem(prob, device=0, max_chains=C)
+    m = np.exp(np.random.default_rng(4).uniform(np.log(1e-3), np.log(1e3), mp.P)).astype(np.float32)
+    mp.set_inverse_mass(torch.from_numpy(m).to(DEV))
+    x0 = inputs.chain_states(prob["x_true"], C, inputs.CONFIGS["small"].seed)
+    p0 = np.random.default_rng(5).standard_normal(x0.shape).astype(np.float32)
+    e = 2e-7
+    x = torch.from_numpy(x0.copy()).to(DEV)
+    p = torch.from_numpy(p0.copy()).to(DEV)
+    lp, g = mp.logpost_grad(x)
+    mp.leapfrog(x, p, lp, g, torch.full((C,), e, dtype=torch.float32, device=DEV), 10)
+    lg = lambda v: (lambda o: (o["logp"], o["grad"]))(op.logpost_grad(v))  # noqa: E731
+    xo, po, lpo, _ = oracle.leapfrog(x0.astype(np.float64), p0.astype(np.float64), e, 10, lg, minv=m)
+    xd = x.cpu().numpy().astype(np.float64)
+    for c in range(C):
+        assert rel_l2(xd[c], xo[c]) <= 1e-3, (c, rel_l2(xd[c], xo[c]))
+        assert np.linalg.norm(xd[c] - xo[c]) / np.linalg.norm(xo[c] - x0[c]) < 0.05

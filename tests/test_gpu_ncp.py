@@ -198,3 +198,21 @@ def test_ncp_with_the_voxel_model(problems, oracle_problem):
         ref_gz = -z + np.concatenate([U @ gx_ll[:op.N], U @ gx_ll[op.N:]])
         assert abs(lp[c].item() - ref_lp) <= 1e-4 * abs(ref_lp)
         assert rel_l2(g[c, :op.P].cpu().numpy().astype(np.float64), ref_gz) <= 1e-3
+
+
+@pytest.mark.parametrize("rho", [(-3.0, 6.0), (0.0, -1.0)])
+def test_ncp_extreme_dependence(problems, oracle_problem, rho):
+    """r_l = logistic(ρ_l) from 0.047 (nearly independent nodes) to 0.9975
+    (λ_min = 4 − 4r ≈ 0.01: the circulant's largest eigenvalue ≈ 100)."""
+    prob = problems("tiny")
+    op = oracle_problem("tiny")
+    C = 3
+    rng = np.random.default_rng(9)
+    v = np.concatenate([0.3 * rng.standard_normal((C, op.P)), np.tile([list(rho)], (C, 1))], axis=1)
+    v = v.astype(np.float32)
+    mp = Problem(prob, device=0, max_chains=C, noncentred=True)
+    lp, g = mp.logpost_grad(torch.from_numpy(v).to(DEV))
+    ref = op.logpost_grad_ncp(v.astype(np.float64))
+    for c in range(C):
+        assert abs(lp[c].item() - ref["logp"][c]) <= 1e-4 * abs(ref["logp"][c])
+        assert rel_l2(g[c].cpu().numpy().astype(np.float64), ref["grad"][c]) <= 1e-3

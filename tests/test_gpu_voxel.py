@@ -220,3 +220,20 @@ def test_voxel_chain_sharded_8192_bench_launch(oracle_problem, problems):
     logp, grad = mp.logpost_grad(torch.from_numpy(x).to(DEV))
     fails = check(op, prob, x, np.array([0, 4095, 8191]), logp.cpu().numpy(), grad.cpu().numpy())
     assert not fails, fails
+
+
+@pytest.mark.parametrize("nz,gamma", [(1, 1.0), (7, 0.2), (200, 1.0), (60, 8.0)])
+def test_voxel_edge_grids_and_sigmoid_scales(problems, oracle_problem, nz, gamma):
+    """Degenerate and extreme voxel grids (one layer; 1.5 m layers) and sigmoid
+    scales (γ = 0.2 m: nearly Heaviside; 8 m: very smooth) against the oracle."""
+    prob = problems("tiny")
+    op = oracle_problem("tiny")
+    Hr = href(prob)
+    mp = Problem(prob, device=0, max_chains=4)
+    mp.voxel_model(nz, Hr, gamma=gamma)
+    x = inputs.chain_states(prob["x_true"], 4, 1, scale=0.05)
+    logp, grad = mp.logpost_grad(torch.from_numpy(x).to(DEV))
+    out = op.voxel_logpost_grad(x.astype(np.float64), Hr.astype(np.float64), nz, gamma=gamma)
+    for c in range(4):
+        assert abs(logp[c].item() - out["logp"][c]) <= 1e-4 * abs(out["logp"][c]), (c, nz, gamma)
+        assert rel_l2(grad[c].cpu().numpy().astype(np.float64), out["grad"][c]) <= 1e-3, (c, nz, gamma)
