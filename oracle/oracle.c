@@ -139,13 +139,12 @@ void or_heights(const or_problem *p, const double *x, double *H, double *dH) {
   double sig[2], ld;
   for (int l = 0; l < 2; l++) or_torus_spectrum(p->nx, p->ny, p->r[l], &sig[l], &ld);
   for (int k = 0; k < N; k++) {
-    double t[2], u[2], dudx[2];
+    double u[2], dudx[2];
     for (int l = 0; l < 2; l++) {
       double tt = x[l * N + k] / sig[l];
       int clamped = 0;
       if (tt > OR_TCLAMP) { tt = OR_TCLAMP; clamped = 1; }
       if (tt < -OR_TCLAMP) { tt = -OR_TCLAMP; clamped = 1; }
-      t[l] = tt;
       u[l] = 0.5 * erfc(-tt / sqrt(2.0));                       /* Φ(t) */
       dudx[l] = clamped ? 0.0 : exp(-0.5 * tt * tt) / sqrt(2.0 * OR_PI) / sig[l];
     }
