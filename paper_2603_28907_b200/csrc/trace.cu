@@ -310,6 +310,9 @@ __shared__ float sgeo[4][MT_MAX_AXIS];   // X, Y, 1/ΔX, 1/ΔY
 #ifndef MT_H2
 #define MT_H2 1
 #endif
+#ifndef MT_UBASE
+#define MT_UBASE 1
+#endif
 #ifndef MT_RL_GLOBAL_H
 #define MT_RL_GLOBAL_H 1
 #endif
@@ -592,7 +595,8 @@ __device__ __forceinline__ void cw_surface(const float *__restrict__ Hg, unsigne
   if (zb <= zmin) { B += Ls; return; }            // below the chain's lowest node of this surface
   if (za >= zmax) return;                         // above its highest node
 #if MT_H2
-  // paired heights: element k holds (H(i,j), H(i,j+1)), so a cell's four corners are two 8-byte loads
+  // paired heights: element k holds (H(i,j), H(i,j+1)), so a cell's four corners are two 8-byte loads.
+  // Hg is the chain group's (warp-uniform) base and off the cell's uniform offset + the lane.
   const float2 *p2 = reinterpret_cast<const float2 *>(Hg) + off;
   const float2 r0 = __ldg(p2), r1 = __ldg(p2 + oy);
   cw_solve<L>(make_float4(r0.x, r0.y, r1.x, r1.y), w, cg, za, zb, Ls, dz, B, n, defer, rec);
@@ -622,6 +626,10 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a
   if (!act) bd = make_float4(-3.0e38f, -3.0e38f, -3.0e38f, -3.0e38f);
   const int oy = ny * 32;
   const unsigned gbase = (unsigned)grp * 2 * N * 32 + lane;   // this lane's column of the group tile
+#if MT_H2 && MT_UBASE
+  const float2 *__restrict__ H2g = a.H2 + (size_t)grp * 2 * N * 32;   // warp-uniform bases
+  const float2 *__restrict__ H2g1 = H2g + (size_t)N * 32;
+#endif
   float llacc = 0.f;
 
   const int r_begin = blockIdx.x * (int)a.rays_per_block;
@@ -649,11 +657,20 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a
         const float4 cg = shift_geo(__ldg(a.trav_geo + k), ds);
         const float s1 = __int_as_float(w.y);
         const float zb = s1 * dz, Ls = s1 - s;
+#if MT_H2 && MT_UBASE
+        // uniform group base (a scalar register pair) + the cell's offset + the lane
+        const unsigned offl = cell_off32(w.x) + (unsigned)lane;
+        cw_surface<0>(reinterpret_cast<const float *>(H2g), offl, w.x, oy, cg, za, zb, Ls, dz, bd.x, bd.y, B0, n0,
+                      defer, rec);
+        cw_surface<1>(reinterpret_cast<const float *>(H2g1), offl, w.x, oy, cg, za, zb, Ls, dz, bd.z, bd.w, B1, n1,
+                      defer, rec);
+#else
         const unsigned off = cell_off32(w.x) + gbase;   // 32-bit element index (C·P < 2^32)
         cw_surface<0>(MT_H2 ? reinterpret_cast<const float *>(a.H2) : a.H, off, w.x, oy, cg, za, zb, Ls, dz, bd.x,
                       bd.y, B0, n0, defer, rec);
         cw_surface<1>(MT_H2 ? reinterpret_cast<const float *>(a.H2) : a.H, off + N * 32, w.x, oy, cg, za, zb, Ls,
                       dz, bd.z, bd.w, B1, n1, defer, rec);
+#endif
         if (s1 >= s_hi) break;
         s = s1;
         za = zb;
