@@ -1273,9 +1273,11 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
       p->all_launches++;
     }
     // small ray chunks (~512 rays = 64 per warp): compact, L1-friendly regions per
-    // block and many waves for load balance
+    // block and many waves for load balance; 256 when there are few chain groups
+    // (measured: 1,024 chains 5.16 vs 5.21 ms; 8,192 chains prefer 512)
+    const int64_t chunk = p->chunk > 0 ? p->chunk : (groups >= 64 ? 512 : 256);
     int64_t S = p->trace_s > 0 ? p->trace_s
-                               : std::max(pick_splits(p, groups, 2), (p->R + p->chunk - 1) / p->chunk);
+                               : std::max(pick_splits(p, groups, 2), (p->R + chunk - 1) / chunk);
     a.rays_per_block = (p->R + S - 1) / S;
     S = (p->R + a.rays_per_block - 1) / a.rays_per_block;
     dim3 grid((unsigned)S, (unsigned)groups);
