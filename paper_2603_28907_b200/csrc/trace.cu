@@ -319,6 +319,14 @@ __shared__ float sgeo[4][MT_MAX_AXIS];   // X, Y, 1/ΔX, 1/ΔY
 #ifndef MT_RL_MINB
 #define MT_RL_MINB 4
 #endif
+// lanes per deferred pair in k_trace_defer: 8 after the chain lanes (many pairs,
+// throughput), more after the ray lanes (few pairs, latency of the band rounds)
+#ifndef DEFER_DG
+#define DEFER_DG 8
+#endif
+#ifndef DEFER_DG_RL
+#define DEFER_DG_RL 16
+#endif
 #ifndef MT_CL_MINB
 #define MT_CL_MINB 5
 #endif
@@ -750,23 +758,22 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a
 }
 
 // The chain x ray pairs the trace kernels deferred (an ill-conditioned cell,
-// or more than RCAP crossings of a surface).  A group of DG = 8 lanes takes
-// one pair, lane = one stored cell of its band (8 cells per round): the same fp32 cell code with
+// or more than RCAP crossings of a surface).  A group of DG lanes takes
+// one pair, lane = one stored cell of its band (DG cells per round): the same fp32 cell code with
 // the same cell pieces as the serial walk, ill-conditioned cells re-solved in
 // place in fp64 from H + Hlo (HP2 lever 1), the lengths summed over the lanes,
 // then the epilogue and each lane's adjoint scatter (or the path-length
 // export).  A pair's latency is a few dependent loads, not a serial march.
 // The last block resets the queue.
-template <int MODE>
+template <int MODE, int DG>
 __global__ void __launch_bounds__(MT_THREADS) k_trace_defer(TraceArgs a) {
   __shared__ float4 wrec[MT_THREADS][4];   // per lane: up to 2 crossings per surface of its cell
   load_geometry(a, sgeo[0], sgeo[1], sgeo[2], sgeo[3]);
   __syncthreads();
   const int n = *(volatile int *)a.ovf_n;
   const int N = a.tc.N, ny = a.tc.ny;
-  constexpr int DG = 8;
   const int lane = threadIdx.x & (DG - 1), nq = min(n, a.ovf_cap);
-  const unsigned gmask = 0xffu << (threadIdx.x & 31 & ~(DG - 1));   // this group's lanes
+  const unsigned gmask = DG == 32 ? 0xffffffffu : ((1u << DG) - 1u) << (threadIdx.x & 31 & ~(DG - 1));   // this group's lanes
   const int grp_g = (blockIdx.x * blockDim.x + threadIdx.x) / DG, ngrp = (gridDim.x * blockDim.x) / DG;
   int c_acc = -1;
   double ll_acc = 0.0;
@@ -1286,8 +1293,8 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
                          : launch_cl_ny<TRACE_PATH>(a, p->ny, grid, smem, s);
     if (rec) cudaEventRecord(p->ev_m[p->n_rec], s);
     if (e == cudaSuccess) {   // deferred pairs (ill-conditioned or > RCAP crossings)
-      if (mode == TRACE_LL) k_trace_defer<TRACE_LL><<<2 * p->num_sms, MT_THREADS, 0, s>>>(a);
-      else k_trace_defer<TRACE_PATH><<<2 * p->num_sms, MT_THREADS, 0, s>>>(a);
+      if (mode == TRACE_LL) k_trace_defer<TRACE_LL, DEFER_DG><<<2 * p->num_sms, MT_THREADS, 0, s>>>(a);
+      else k_trace_defer<TRACE_PATH, DEFER_DG><<<2 * p->num_sms, MT_THREADS, 0, s>>>(a);
       e = cudaGetLastError();
       p->all_launches++;
     }
@@ -1305,8 +1312,8 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
                            : launch_rl_ny<TRACE_PATH>(a, p->d_Hc, p->ny, grid, smem, s);
     if (rec) cudaEventRecord(p->ev_m[p->n_rec], s);
     if (e == cudaSuccess) {
-      if (mode == TRACE_LL) k_trace_defer<TRACE_LL><<<2 * p->num_sms, MT_THREADS, 0, s>>>(a);
-      else k_trace_defer<TRACE_PATH><<<2 * p->num_sms, MT_THREADS, 0, s>>>(a);
+      if (mode == TRACE_LL) k_trace_defer<TRACE_LL, DEFER_DG_RL><<<2 * p->num_sms, MT_THREADS, 0, s>>>(a);
+      else k_trace_defer<TRACE_PATH, DEFER_DG_RL><<<2 * p->num_sms, MT_THREADS, 0, s>>>(a);
       e = cudaGetLastError();
       p->all_launches += 2;
     }
