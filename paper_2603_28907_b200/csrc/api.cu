@@ -216,7 +216,11 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   const char *ord = getenv("MT_RAY_ORDER");
   if (!(ord && atoi(ord) == 0)) {
     std::vector<uint64_t> key(p->R);
-    double zf = 0.5;   // reference height of the order, as a fraction of z_top
+    // reference height of the order, as a fraction of z_top: mid-height for the chain
+    // lanes (L2 locality of the band cells across a block's rays); lower for the ray
+    // lanes, where lanes are rays and Morton neighbours there have more similar band
+    // walks (configs[4]: 0.405 ms per trace at 0.5, 0.383 at 0.2-0.25, 0.415 at 0)
+    double zf = p->max_chains >= 16 ? 0.5 : 0.22;
     if (const char *e = getenv("MT_ORDER_Z")) zf = atof(e);
     for (int64_t q = 0; q < p->R; q++) {
       double sm = fmin(zf * (double)d->z_top / rb[q].x, (double)rb[q].y);

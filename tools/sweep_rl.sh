@@ -1,7 +1,5 @@
-# tuning sweep for the ray-lanes path (configs[4]); variants built by tools/build_variants.sh
-python tools/trace_bench.py ray_sharded --reps 50
-MT_LIB=variants/libmt_p0.so python tools/trace_bench.py ray_sharded --reps 50
-for s in 296 444 888 1184; do MT_TRACE_S=$s python tools/trace_bench.py ray_sharded --reps 50; done
-python tools/trace_bench.py small --chains 4 --reps 50
-MT_LIB=variants/libmt_p0.so python tools/trace_bench.py small --chains 4 --reps 50
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -m gpu -x 2>&1 | tail -2
+# ray-lanes order change: parity + configs[4] bench lines (exact and voxel)
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/ev2_pytest.log 2>&1; echo "rc $?" >> gpurun_out/ev2_pytest.log
+timeout 600 python bench.py --workload ray_sharded --steps 50 > gpurun_out/ev2_bench_ray.log 2>&1
+timeout 600 python bench.py --model voxel --workload ray_sharded --steps 50 > gpurun_out/ev2_bench_vxray.log 2>&1
+timeout 300 python tools/trace_bench.py ray_sharded --reps 50 > gpurun_out/ev2_tb.log 2>&1
