@@ -96,7 +96,20 @@ typedef struct {
 /* Validate the description, precompute per-ray constants (in-box extent,
  * exterior rock length, deviance-centred log-weight) in double on the host,
  * upload them as an fp32 SoA, allocate the workspace.  Synchronous.
- * Errors: MT_EINVAL (message names the offending field), MT_ENOMEM, MT_ECUDA. */
+ * Errors: MT_EINVAL (message names the offending field), MT_ENOMEM, MT_ECUDA.
+ *
+ * Tuning environment variables, read here (performance only: results are
+ * independent of them up to fp32 summation order; unset = the measured
+ * defaults in DESIGN.md):
+ *   MT_TRACE_K      1 = ray lanes, 32 = chain lanes (default: chain lanes iff C >= 16)
+ *   MT_TRACE_S      trace grid splits over the rays
+ *   MT_CHUNK        rays per chain-lanes block chunk (default 256 / 512)
+ *   MT_OVF_CAP      deferred-pair queue capacity (tests force the bitmap overflow path)
+ *   MT_RAY_ORDER    0 = input ray order instead of the Morton order
+ *   MT_ORDER_Z      reference height of the Morton order, fraction of z_top
+ *   MT_NO_MB        disable the few-chain multi-block K3 / kick kernels
+ *   MT_VX_CH, MT_VX_GCHUNK, MT_VX_VEC, MT_VX_RPW   voxel model (mt_voxel_model)
+ *                   work-item size, gather chunk, chains per lane, rows per warp */
 int mt_problem_create(const mt_problem_desc *desc, mt_problem **out);
 
 /* Free everything the problem owns.  NULL-safe.  Synchronous. */

@@ -252,7 +252,6 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   size_t R = (size_t)(p->R > 0 ? p->R : 1), MC = (size_t)(p->max_chains > 0 ? p->max_chains : 1);
   size_t P = p->P;
   size_t MC32 = (MC + 31) / 32 * 32;   // chain-interleaved workspaces hold whole groups of 32
-  if (const char *e = getenv("MT_SMEMH_LIMIT")) p->smemh_limit = atoi(e);
   cudaError_t e = cudaSuccess;
 #define ALLOC(ptr, bytes)                                        \
   if (e == cudaSuccess) e = cudaMalloc((void **)&(ptr), (bytes));

@@ -199,7 +199,6 @@ struct mt_problem {
   int trace_k = 0;              // chains per block (0 = auto)
   int trace_s = 0;              // ray splits (0 = auto)
   int chunk = 0;                // chain lanes: rays per block (a Morton-ordered chunk; 0 = by chain count)
-  int smemh_limit = 100 * 1024; // stage a 32-chain height tile in smem when it fits
   // batched NUTS workspace (allocated by the first mt_nuts_step)
   float *nuts_ws = nullptr;
   double *nuts_lp = nullptr;
