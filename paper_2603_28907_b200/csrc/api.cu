@@ -263,7 +263,9 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   ALLOC(p->d_perm, sizeof(int32_t) * R);
   ALLOC(p->d_H, sizeof(float) * MC32 * P);
   ALLOC(p->d_Hlo, sizeof(float) * MC32 * P);
-  ALLOC(p->d_Hc, sizeof(float) * (MC < 16 ? MC : 16) * P);
+  // ray-lanes height copies: the ray lanes serve C < 16 unless MT_TRACE_K forces them
+  const bool rl_any_c = p->trace_k != 0 && p->trace_k != 32;
+  ALLOC(p->d_Hc, sizeof(float) * (rl_any_c || MC < 16 ? MC : 16) * P);
   ALLOC(p->d_H2, sizeof(float2) * MC32 * 2 * p->N);
   ALLOC(p->d_G, sizeof(float) * MC32 * P);
   ALLOC(p->d_band, sizeof(float4) * MC);
