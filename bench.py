@@ -309,7 +309,10 @@ def main():
     value = units / (t_ms * 1e-3)
 
     # dominant kernel (K2 trace): algorithmic FP32 flops per launch / measured launch duration
-    work = json.load(open(os.path.join(ROOT, "data", "work_counts.json")))[dname]
+    # (prior-draw states: the oracle's counts on prior draws, tools/count_work.py --prior)
+    wall = json.load(open(os.path.join(ROOT, "data", "work_counts.json")))
+    wkey = dname + "_prior" if args.states == "prior" and dname + "_prior" in wall else dname
+    work = wall[wkey]
     F = work["flops_per_pair"]
     avg_trace_ms = tm["trace_ms"] / max(tm["trace_launches"], 1)       # K2 main + fp64 follow-up
     avg_defer_ms = cnt["defer_ms"] / max(tm["trace_launches"], 1)
@@ -317,13 +320,13 @@ def main():
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "trace_traffic.json")
     if os.path.exists(tpath):
-        tr = json.load(open(tpath)).get(args.workload)
+        tr = json.load(open(tpath)).get(args.workload + ("_prior" if args.states == "prior" else ""))
         traffic = tr.get("bytes_per_launch") if tr and tr.get("chains") == C else None
     roofline = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_NOMINAL, "unit": "TFLOP/s",
                 "frac": achieved / FP32_PEAK_NOMINAL, "traffic": traffic,
                 "kernel": ("K2 = k_trace_rl (ray lanes)" if ray else "K2 = k_trace_cl (chain lanes)")
                           + " + k_trace_defer (fp64 follow-up), per launch pair",
-                "flops_per_pair": F,
+                "flops_per_pair": F, "work_counts": f"data/work_counts.json[{wkey}]",
                 "defer_share_of_trace": avg_defer_ms / avg_trace_ms,
                 "deferred_pairs_per_launch": (cnt["deferred"] - d0) / max(tm["trace_launches"], 1),
                 "trace_share_of_step": tm["trace_ms"] / t_ms if ws == 1 else None,
@@ -341,7 +344,7 @@ def main():
         vtraffic = None
         tpath = os.path.join(ROOT, "profiles", "voxel_traffic.json")
         if os.path.exists(tpath):
-            tr = json.load(open(tpath)).get(args.workload)
+            tr = json.load(open(tpath)).get(args.workload + ("_prior" if args.states == "prior" else ""))
             vtraffic = tr.get("bytes_per_launch") if tr and tr.get("chains") == C else None
         info = pb.voxel_info()
         roofline = {"bound": "l2", "achieved": ach, "peak": l2_peak, "unit": "GB/s", "frac": ach / l2_peak,

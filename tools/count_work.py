@@ -1,7 +1,8 @@
 """Algorithmic work per chain x ray for the roofline.
 
 Runs the ORACLE's instrumentation (§c.1 step 13) on each config's own
-near-posterior chain states and writes data/work_counts.json:
+near-posterior chain states (--prior: prior-draw states, key <name>_prior) and
+writes data/work_counts.json:
   n_inbox  cells of the in-box traversal
   n_band   cells whose z-range meets the chain's band [min H0, max H1]
   n_solve  surface-cells not resolved by the corner-bound test (a quadratic solve)
@@ -14,7 +15,7 @@ FMA = 2, div/sqrt/exp = 1):
   F_SOLVE = 57  cell coefficients (34), roots (8), piece classification (15)
   F_CROSS = 18  crossing position, 1/|g'|, four bilinear adjoint weights
   F_EPI = 14    t = ln(λ/C), expm1, ℓ_p, ∂ℓ/∂O, per-surface factors, accumulate
-Usage: python tools/count_work.py [config ...]
+Usage: python tools/count_work.py [--prior] [config ...]
 """
 import json
 import os
@@ -27,11 +28,12 @@ from paper_2603_28907_b200 import inputs  # noqa: E402
 F_CELL, F_SOLVE, F_CROSS, F_EPI = 14, 57, 18, 14
 
 
-def count(name: str, n_chains: int = 4):
+def count(name: str, n_chains: int = 4, prior: bool = False):
     cfg = inputs.CONFIGS[name]
     prob = inputs.make_problem(name)
     op = oracle.Problem(prob)
-    x = inputs.chain_states(prob["x_true"], n_chains, cfg.seed)
+    x = (inputs.prior_states(name, n_chains) if prior
+         else inputs.chain_states(prob["x_true"], n_chains, cfg.seed))
     out = op.logpost_grad(x.astype("float64"))
     c = out["counters"] / float(n_chains * op.R)
     n_inbox, n_band, n_solve, n_cross = (float(v) for v in c)
@@ -42,10 +44,13 @@ def count(name: str, n_chains: int = 4):
 
 
 if __name__ == "__main__":
-    names = sys.argv[1:] or ["tiny", "small", "medium", "ray_sharded"]
+    prior = "--prior" in sys.argv[1:]   # prior-draw chain states (key <name>_prior)
+    names = [a for a in sys.argv[1:] if a != "--prior"] or ["tiny", "small", "medium", "ray_sharded"]
     path = os.path.join(inputs.DATA_DIR, "work_counts.json")
     data = json.load(open(path)) if os.path.exists(path) else {}
     for n in names:
-        data[inputs.DATA_NAME[n]] = count(n, 1 if n == "ray_sharded" else 4)
-        print(n, json.dumps(data[inputs.DATA_NAME[n]]))
+        key = inputs.DATA_NAME[n] + ("_prior" if prior else "")
+        data[key] = count(n, 1 if n == "ray_sharded" else 4, prior)
+        data[key]["states"] = "prior" if prior else "near-posterior"
+        print(n, json.dumps(data[key]))
     json.dump(data, open(path, "w"), indent=1, sort_keys=True)

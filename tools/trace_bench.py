@@ -57,7 +57,9 @@ def main():
     tm = pb.timing_read()
     cnt = pb.trace_counters()
     tr = tm["trace_ms"] / tm["trace_launches"]
-    work = json.load(open(os.path.join(ROOT, "data", "work_counts.json")))[inputs.DATA_NAME[a.config]]
+    wall = json.load(open(os.path.join(ROOT, "data", "work_counts.json")))
+    key = inputs.DATA_NAME[a.config]
+    work = wall.get(key + "_prior", wall[key]) if a.prior else wall[key]
     F = work["flops_per_pair"]
     pairs = C * pb.R
     print(json.dumps({"config": a.config, "ncp": a.ncp, "states": "prior" if a.prior else "near-posterior", "C": C, "R": pb.R, "K": os.environ.get("MT_TRACE_K", "auto"),
