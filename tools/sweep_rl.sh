@@ -1,8 +1,6 @@
-# ray-lanes A/B: 128-thread blocks (8/SM) vs 256 (4/SM)
-for r in 1 2; do
-python tools/trace_bench.py ray_sharded --reps 50
-MT_LIB=variants/libmt_t128.so python tools/trace_bench.py ray_sharded --reps 50
+# chain-lanes deferred-pair group size A/B at configs[3] (8,192 chains)
+for v in default d4 d16; do
+  if [ $v = default ]; then L=""; else L=variants/libmt_$v.so; fi
+  MT_LIB=$L python tools/trace_bench.py chain_sharded --reps 10
+  MT_LIB=$L python tools/trace_bench.py chain_sharded --reps 10 --prior
 done
-for s in 2368 9472; do MT_TRACE_S=$s MT_LIB=variants/libmt_t128.so python tools/trace_bench.py ray_sharded --reps 50; done
-MT_LIB=variants/libmt_t128.so python tools/trace_bench.py small --chains 4 --reps 50
-python tools/trace_bench.py small --chains 4 --reps 50
