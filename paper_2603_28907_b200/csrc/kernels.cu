@@ -672,6 +672,7 @@ cudaError_t launch_finish(mt_problem *p, int mode, int C, float *x, float *grad,
                           int32_t *status, float *mom, const float *eps, float *kin,
                           cudaStream_t s) {
   if (C <= 0) return cudaSuccess;
+  if (mode != FIN_PLAIN && mode != FIN_STEP && mode != FIN_LAST) return cudaErrorInvalidValue;
   FinishArgs a = base_args(p, C);
   a.x = x; a.grad = grad; a.logp = logp; a.status = status; a.mom = mom; a.eps = eps; a.kin = kin;
   if (use_mb(p, C)) {   // few chains: several blocks per chain (unfused leapfrog)
