@@ -1,6 +1,6 @@
-# chain-lanes deferred-pair group size A/B at configs[3] (8,192 chains)
-for v in default d4 d16; do
+# K3 staged-column A/B at configs[3] on one box (bench step, no CPU baseline / e2e)
+for r in 1 2 3; do
+for v in default st; do
   if [ $v = default ]; then L=""; else L=variants/libmt_$v.so; fi
-  MT_LIB=$L python tools/trace_bench.py chain_sharded --reps 10
-  MT_LIB=$L python tools/trace_bench.py chain_sharded --reps 10 --prior
-done
+  echo "lib $v"; MT_LIB=$L timeout 600 python bench.py --no-cpu-baseline --no-e2e --steps 5 | tail -1
+done; done
