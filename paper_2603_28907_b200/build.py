@@ -26,15 +26,32 @@ def stale() -> bool:
     return any(os.path.getmtime(f) > t for f in sources() + headers())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
-        return SO
-    cmd = [NVCC, *FLAGS, "-shared", "-o", SO, *sources(), "-lcudart", "-ldl"]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd))
-    subprocess.check_call(cmd)
-    return SO
+def build(force: bool = False, verbose: bool = False, out: str = SO, defines=()) -> str:
+    """Compile each translation unit in parallel (separate objects, no device
+    linking: no kernel calls across units), then link the shared library."""
+    from concurrent.futures import ThreadPoolExecutor
+    import tempfile
+    if not force and out == SO and not stale():
+        return out
+    extra = [f"-D{d}" for d in defines]
+    with tempfile.TemporaryDirectory() as d:
+        objs = []
+        cmds = []
+        for src in sources():
+            o = os.path.join(d, os.path.basename(src) + ".o")
+            objs.append(o)
+            cmd = [NVCC, *FLAGS, *extra, "-c", src, "-o", o]
+            if verbose:
+                cmd.insert(1, "-Xptxas=-v")
+            cmds.append(cmd)
+        with ThreadPoolExecutor(max_workers=len(cmds)) as ex:
+            for r in ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), cmds):
+                if verbose or r.returncode:
+                    print(r.stdout + r.stderr)
+                if r.returncode:
+                    raise subprocess.CalledProcessError(r.returncode, r.args)
+        subprocess.check_call([NVCC, *FLAGS, "-shared", "-o", out, *objs, "-lcudart", "-ldl"])
+    return out
 
 
 if __name__ == "__main__":

@@ -80,7 +80,7 @@ int check_chains(const mt_problem *p, int32_t C) {
 
 void free_all(mt_problem *p) {
   voxel_free(p);
-  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_trav_geo, p->d_rl_head, p->d_rl_code, p->d_rl_ovf, p->d_ovf_q, p->d_ovf_n, p->d_redo, p->d_H, p->d_Hlo, p->d_Hc, p->d_H2, p->d_cs, p->d_xw, p->d_minv, p->mb_red, p->mb_band, p->mb_ticket, p->d_G,
+  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_trav_geo, p->d_trav_km, p->d_rl_head, p->d_rl_code, p->d_rl_ovf, p->d_ovf_q, p->d_ovf_n, p->d_redo, p->d_H, p->d_Hlo, p->d_Hc, p->d_cl, p->d_tab, p->d_ray_c, p->d_cs, p->d_xw, p->d_minv, p->mb_red, p->mb_band, p->mb_ticket, p->d_G,
                   p->d_band, p->d_ll, p->d_x0, p->d_g0, p->d_mom, p->d_kin0, p->d_kin1, p->d_lp0};
   for (void *b : bufs)
     if (b) cudaFree(b);
@@ -175,6 +175,7 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   if (const char *e = getenv("MT_TRACE_K")) p->trace_k = atoi(e);
   if (const char *e = getenv("MT_TRACE_S")) p->trace_s = atoi(e);
   if (const char *e = getenv("MT_CHUNK")) p->chunk = atoi(e);
+  if (const char *e = getenv("MT_CL_V")) p->cl_v = atoi(e);
   if (const char *e = getenv("MT_OVF_CAP")) p->ovf_cap = std::max(1, atoi(e));   // (tests: force the overflow path)
 
   // ---- per-ray constants in double (a0) ----
@@ -266,10 +267,10 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   // ray-lanes height copies: the ray lanes serve C < 16 unless MT_TRACE_K forces them
   const bool rl_any_c = p->trace_k != 0 && p->trace_k != 32;
   ALLOC(p->d_Hc, sizeof(float) * (rl_any_c || MC < 16 ? MC : 16) * P);
-  ALLOC(p->d_H2, sizeof(float2) * MC32 * 2 * p->N);
-  ALLOC(p->d_G, sizeof(float) * MC32 * P);
+  ALLOC(p->d_cl, sizeof(uint2) * MC32 * 3 * p->N);
+  ALLOC(p->d_G, sizeof(macc) * MC32 * P);
   ALLOC(p->d_band, sizeof(float4) * MC);
-  ALLOC(p->d_ll, sizeof(double) * MC);
+  ALLOC(p->d_ll, sizeof(macc) * MC);
   ALLOC(p->d_x0, sizeof(float) * MC * P);
   ALLOC(p->d_g0, sizeof(float) * MC * P);
   ALLOC(p->d_mom, sizeof(float) * MC * P);
@@ -300,10 +301,10 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   if (e == cudaSuccess && p->R > 0) e = cudaMemcpy(p->d_ray_b, rb.data(), sizeof(float4) * p->R, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && p->R > 0) e = cudaMemcpy(p->d_obase, ob.data(), sizeof(float) * p->R, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && p->R > 0) e = cudaMemcpy(p->d_perm, p->perm.data(), sizeof(int32_t) * p->R, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemset(p->d_G, 0, sizeof(float) * MC32 * P);
+  if (e == cudaSuccess) e = cudaMemset(p->d_G, 0, sizeof(macc) * MC32 * P);
   if (e == cudaSuccess) e = cudaMemset(p->d_H, 0, sizeof(float) * MC32 * P);
   if (e == cudaSuccess) e = cudaMemset(p->d_Hlo, 0, sizeof(float) * MC32 * P);
-  if (e == cudaSuccess) e = cudaMemset(p->d_ll, 0, sizeof(double) * MC);
+  if (e == cudaSuccess) e = cudaMemset(p->d_ll, 0, sizeof(macc) * MC);
   if (e == cudaSuccess) e = cudaMemset(p->d_ovf_n, 0, sizeof(int) * 4);
   if (e == cudaSuccess) e = cudaMemset(p->d_redo, 0, sizeof(unsigned) * redo_words);
   if (e == cudaSuccess && p->mb_red) {
@@ -582,12 +583,10 @@ int mt_loglik_heights(mt_problem *p, int32_t C, const float *H, double *ll, floa
   k_band_of<<<C, 256, 0, s>>>(H, p->N, p->d_band);
   p->all_launches++;
   CK(cudaGetLastError());
-  CK(cudaMemsetAsync(ll, 0, sizeof(double) * C, s));
   CK(launch_tile(p, C, H, p->d_H, 1, s));
   CK(cudaMemsetAsync(p->d_Hlo, 0, sizeof(float) * ((size_t)(C + 31) / 32 * 32) * p->P, s));   // exact fp32 heights
-  CK(launch_trace(p, TRACE_LL, C, p->d_H, p->d_band, p->d_G, ll, nullptr, nullptr, s));
-  CK(launch_tile(p, C, p->d_G, dldH, 0, s));
-  CK(cudaMemsetAsync(p->d_G, 0, sizeof(float) * ((size_t)(C + 31) / 32 * 32) * p->P, s));
+  CK(launch_trace(p, TRACE_LL, C, p->d_H, p->d_band, p->d_G, p->d_ll, nullptr, nullptr, s));
+  CK(launch_take_acc(p, C, dldH, ll, s));
   return MT_OK;
 }
 

@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_finish(FinishArgs a) {
   float *xc = a.x + (size_t)c * a.P;
   for (int k = threadIdx.x; k < a.P; k += blockDim.x) xs[k] = xc[k];
   __syncthreads();
-  float *Gt = const_cast<float *>(a.G);
+  macc *Gt = const_cast<macc *>(a.G);
   float *gc = a.grad + (size_t)c * a.P;
   float *pc = MODE != FIN_PLAIN ? a.mom + (size_t)c * a.P : nullptr;
   const float eps = MODE != FIN_PLAIN ? a.eps[c] : 0.f;
@@ -58,9 +58,9 @@ __global__ void __launch_bounds__(MT_THREADS) k_finish(FinishArgs a) {
     float x0 = xs[k], x1 = xs[N + k];
     NodeH h = node_heights(x0, x1, a.inv_sigma[0], a.inv_sigma[1], a.z_top, true);
     const size_t t0 = tix(c, 0, k, N), t1 = tix(c, 1, k, N);
-    float G0 = Gt[t0], G1 = Gt[t1];
-    Gt[t0] = 0.f;
-    Gt[t1] = 0.f;
+    const double G0 = dq_g(Gt[t0]), G1 = dq_g(Gt[t1]);
+    Gt[t0] = 0;
+    Gt[t1] = 0;
     double gx0 = (double)G0 * h.J0 + (double)G1 * h.J10;
     double gx1 = (double)G1 * h.J11;
     if (a.prior_on) {
@@ -102,8 +102,8 @@ __global__ void __launch_bounds__(MT_THREADS) k_finish(FinishArgs a) {
   }
   BlockRed r = block_reduce(v);
   if (threadIdx.x == 0) {
-    double lp = a.ll[c] + (a.prior_on ? -0.5 * r.s0 + a.prior_const : 0.0);
-    a.ll[c] = 0.0;
+    double lp = dq_ll(a.ll[c]) + (a.prior_on ? -0.5 * r.s0 + a.prior_const : 0.0);
+    a.ll[c] = 0;
     a.logp[c] = lp;
     int bad = r.bad || !isfinite(lp);
     if (a.status) a.status[c] = bad ? MT_STATUS_NONFINITE : 0;
@@ -182,16 +182,16 @@ __global__ void __launch_bounds__(MT_THREADS) k_finish_mb(FinishArgs a, MbScratc
   const int c = blockIdx.x, N = a.N, ny = a.ny, nx = a.nx;
   const float *xc = a.x + (size_t)c * a.P;
   float *gc = a.grad + (size_t)c * a.P;
-  float *Gt = const_cast<float *>(a.G);
+  macc *Gt = const_cast<macc *>(a.G);
   BlockRed v = {3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f, 0.0, 0.0, 0};
   for (int k = blockIdx.y * blockDim.x + threadIdx.x; k < N; k += gridDim.y * blockDim.x) {
     const int i = k / ny, j = k - i * ny;
     const float x0 = xc[k], x1 = xc[N + k];
     const NodeH h = node_heights(x0, x1, a.inv_sigma[0], a.inv_sigma[1], a.z_top, true);
     const size_t t0 = tix(c, 0, k, N), t1 = tix(c, 1, k, N);
-    const float G0 = Gt[t0], G1 = Gt[t1];
-    Gt[t0] = 0.f;
-    Gt[t1] = 0.f;
+    const double G0 = dq_g(Gt[t0]), G1 = dq_g(Gt[t1]);
+    Gt[t0] = 0;
+    Gt[t1] = 0;
     double gx0 = (double)G0 * h.J0 + (double)G1 * h.J10;
     double gx1 = (double)G1 * h.J11;
     if (a.prior_on) {
@@ -218,8 +218,8 @@ __global__ void __launch_bounds__(MT_THREADS) k_finish_mb(FinishArgs a, MbScratc
   }
   if (mb_last(m.ticket, c) && threadIdx.x == 0) {
     volatile double *rd = m.red + 3 * c;
-    const double lp = a.ll[c] + (a.prior_on ? -0.5 * rd[0] + a.prior_const : 0.0);
-    a.ll[c] = 0.0;
+    const double lp = dq_ll(a.ll[c]) + (a.prior_on ? -0.5 * rd[0] + a.prior_const : 0.0);
+    a.ll[c] = 0;
     a.logp[c] = lp;
     if (a.status) a.status[c] = (rd[2] != 0.0 || !isfinite(lp)) ? MT_STATUS_NONFINITE : 0;
     rd[0] = 0.0;
@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_finish_r(FinishArgs a) {
   for (int k = threadIdx.x; k < a.P; k += blockDim.x) xs[k] = xc[k];
   __syncthreads();
   const Spec sp = block_spectrum(a.cs, N, xs[2 * N], xs[2 * N + 1], a.prior_on != 0);
-  float *Gt = const_cast<float *>(a.G);
+  macc *Gt = const_cast<macc *>(a.G);
   float *gc = a.grad + (size_t)c * a.P;
   float *pc = MODE != FIN_PLAIN ? a.mom + (size_t)c * a.P : nullptr;
   const float eps = MODE != FIN_PLAIN ? a.eps[c] : 0.f;
@@ -466,9 +466,9 @@ __global__ void __launch_bounds__(MT_THREADS) k_finish_r(FinishArgs a) {
     const float x0 = xs[k], x1 = xs[N + k];
     const NodeH h = node_heights(x0, x1, sp.inv_sigma[0], sp.inv_sigma[1], a.z_top, true);
     const size_t t0 = tix(c, 0, k, N), t1 = tix(c, 1, k, N);
-    const float G0 = Gt[t0], G1 = Gt[t1];
-    Gt[t0] = 0.f;
-    Gt[t1] = 0.f;
+    const double G0 = dq_g(Gt[t0]), G1 = dq_g(Gt[t1]);
+    Gt[t0] = 0;
+    Gt[t1] = 0;
     double gx0 = (double)G0 * h.J0 + (double)G1 * h.J10;
     double gx1 = (double)G1 * h.J11;
     acc[4] += h.t0 * gx0;
@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_finish_r(FinishArgs a) {
   }
   block_sum<8>(acc);
   if (threadIdx.x == 0) {
-    double lp = a.ll[c];
+    double lp = dq_ll(a.ll[c]);
     float gr[2];
 #pragma unroll
     for (int l = 0; l < 2; l++) {
@@ -512,7 +512,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_finish_r(FinishArgs a) {
       gr[l] = (float)g;
       gc[2 * N + l] = gr[l];
     }
-    a.ll[c] = 0.0;
+    a.ll[c] = 0;
     a.logp[c] = lp;
     const int bad = acc[7] != 0.0 || !isfinite(lp) || !isfinite(gr[0]) || !isfinite(gr[1]);
     if (a.status) a.status[c] = bad ? MT_STATUS_NONFINITE : 0;
@@ -794,6 +794,29 @@ cudaError_t launch_philox(const uint32_t *ctr, uint32_t k0, uint32_t k1, uint32_
   k_philox<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(reinterpret_cast<const uint4 *>(ctr),
                                                        make_uint2(k0, k1),
                                                        reinterpret_cast<uint4 *>(out), n, use_curand);
+  return cudaGetLastError();
+}
+
+// Fixed-point accumulators -> the caller's ∂ℓ/∂H [C][2N] fp32 and ℓ [C] fp64 (debug /
+// parity entry mt_loglik_heights); the accumulators are cleared.
+__global__ void k_take_acc(int C, int N, macc *G, macc *ll, float *dldH, double *llo) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < C) {
+    llo[t] = dq_ll(ll[t]);
+    ll[t] = 0;
+  }
+  if (t >= (int64_t)C * 2 * N) return;
+  const int c = (int)(t / (2 * N)), m = (int)(t - (int64_t)c * 2 * N);
+  const size_t ti = tix(c, m / N, m % N, N);
+  dldH[t] = (float)dq_g(G[ti]);
+  G[ti] = 0;
+}
+
+cudaError_t launch_take_acc(mt_problem *p, int C, float *dldH, double *ll, cudaStream_t s) {
+  if (C <= 0) return cudaSuccess;
+  const int64_t n = (int64_t)C * 2 * p->N;
+  k_take_acc<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(C, p->N, p->d_G, p->d_ll, dldH, ll);
+  p->all_launches++;
   return cudaGetLastError();
 }
 

@@ -12,6 +12,29 @@
 #define MT_MAX_AXIS 128
 #define MT_MAX_NODES 4096
 #define MT_THREADS 256
+#define MT_TABQ 32   // band-entry levels per ray (chain-lanes trace)
+
+// Fixed-point accumulators (R30).  ∂ℓ/∂H and the log-likelihood are
+// summed as two's-complement int64 with RED.ADD.64: integer adds commute
+// exactly, so every chain's result is bit-identical for any launch shape,
+// order of processing (deferred pairs, dynamic ray queues), chain sharding over
+// GPUs and, all-reduced as integers, ray sharding.
+typedef unsigned long long macc;
+#define MT_GQ 262144.0       // 2^18 units per 1 of ∂ℓ/∂H (range ±3.5e13, resolution 3.8e-6)
+#define MT_LQ 16777216.0     // 2^24 units per 1 of ℓ (range ±5.5e11, resolution 6e-8)
+__device__ __forceinline__ macc q_ll(float v) { return (macc)__float2ll_rn(v * (float)MT_LQ); }
+__device__ __forceinline__ macc q_lld(double v) { return (macc)__double2ll_rn(v * MT_LQ); }
+__device__ __forceinline__ macc q_raw(float v) { return (macc)__float2ll_rn(v); }   // v pre-scaled by MT_GQ
+// Round-to-nearest of |v| < 2^22 to an integer on the FMA/ALU pipes (the magic-number
+// trick: v + 1.5·2^23 puts round(v) in the low mantissa bits); F2I.S64 runs on the
+// quarter-rate conversion unit, which the trace's scatter would otherwise saturate.
+#define MT_QSMALL 4194304.0f
+__device__ __forceinline__ macc q_small(float v) {
+  return (macc)(long long)(__float_as_int(v + 12582912.0f) - 0x4B400000);
+}
+__device__ __forceinline__ macc q_g(float v) { return (macc)__float2ll_rn(v * (float)MT_GQ); }
+__device__ __forceinline__ double dq_g(macc v) { return (double)(long long)v * (1.0 / MT_GQ); }
+__device__ __forceinline__ double dq_ll(macc v) { return (double)(long long)v * (1.0 / MT_LQ); }
 
 // Index of node k of surface l of chain c in the chain-interleaved layout
 // [group = c/32][l][node][c % 32] used for the heights and ∂ℓ/∂H workspaces
@@ -51,6 +74,7 @@ struct TraceArgs {
   const int32_t *trav_off;      // [R+1] CSR offsets of each ray's stored traversal
   const int2 *trav;             // {cell_pack(i, j), s_out bits} per cell, in ray order (a2)
   const float4 *trav_geo;       // per cell {u, v, α, β} at its entry (cell-local coordinates, a0)
+  const float2 *trav_km;        // per cell {K = u β + v α, M = α β}: the ray-only parts of the solve's g1, g2
   // ray-lane traversal replay (k_trace_rl): per ray {n | i0 << 8 | j0 << 15, overflow word},
   // 2-bit exit codes of its cells (0 top, 1 x-line, 2 y-line, 3 vertex) for cells 0..63
   // and the code words of cells >= 64; the exit parameters are recomputed bit-exactly
@@ -62,12 +86,18 @@ struct TraceArgs {
   int64_t rays_per_block;
   int C;                        // chains in this call
   const float *H;               // [C][2][N] heights
-  const float2 *H2;             // chain lanes: paired heights (H(i,j), H(i,j+1)) per element
+  const uint2 *cl;              // chain lanes, per evaluation (k_cell_prep): [group][slot][node][32] 8-byte
+                                //   elements; slot 0: the cell's corner bounds rounded outward to fp16,
+                                //   {half2(min H0, min H1), half2(max H0, max H1)}; slots 1, 2: the paired
+                                //   heights (H_l(i,j), H_l(i,j+1)) of surface l = 0, 1 (fp32 bits)
+  const float4 *ray_c;          // chain lanes: per ray {d_z, 1/d_z, s_exit, first stored cell (int bits)}
+  const uint8_t *tab;           // chain lanes: per ray [MT_TABQ] band-entry cells (relative to the first)
+  float tab_scale;              // MT_TABQ / z_top
   const float *Hlo;             // fp32 residuals of the fp64 heights (0 for caller heights): the
                                 //   fp64 re-solves of ill-conditioned cells use H + Hlo (HP2)
   const float4 *band;           // [C] (min H0, max H0, min H1, max H1)
-  float *G;                     // [C][2][N] ∂ℓ/∂H accumulator (atomic adds)
-  double *ll;                   // [C] deviance-centred log-likelihood accumulator
+  macc *G;                      // [C][2][N] ∂ℓ/∂H accumulator (fixed point MT_GQ, atomic adds)
+  macc *ll;                     // [C] deviance-centred log-likelihood accumulator (fixed point MT_LQ)
   float *Lout, *Oout;           // path-length export: [C][R][3], [C][R]
   float4 *ovf_q;                // chain lanes: deferred pairs {c, ray, s_lo, s_hi} (an ill-
   int *ovf_n, *ovf_done;        //   conditioned cell or > RCAP crossings), done by k_trace_defer
@@ -85,8 +115,8 @@ struct FinishArgs {
   float car_r[2];
   double prior_const;           // Σ_l (1/2 ln det Q_l - N/2 ln 2π)
   int prior_on;
-  const float *G;               // ∂ℓ/∂H [C][2N] (zeroed after use)
-  double *ll;                   // [C] (zeroed after use)
+  const macc *G;                // ∂ℓ/∂H [C][2N], fixed point MT_GQ (zeroed after use)
+  macc *ll;                     // [C] log-likelihood, fixed point MT_LQ (zeroed after use)
   float *x;                     // [C][P]
   float *grad;                  // [C][P]
   double *logp;                 // [C]
@@ -179,6 +209,7 @@ struct mt_problem {
   std::vector<int32_t> perm, inv_perm;   // internal <-> caller ray order (host)
   int2 *d_trav = nullptr;
   float4 *d_trav_geo = nullptr;
+  float2 *d_trav_km = nullptr;
   int2 *d_rl_head = nullptr;
   uint4 *d_rl_code = nullptr;
   uint32_t *d_rl_ovf = nullptr;
@@ -187,17 +218,21 @@ struct mt_problem {
   int ovf_cap = 1 << 22;
   unsigned *d_redo = nullptr;   // (max_chains x R)-bit overflow bitmap of the deferred-pair queue
   int64_t trav_cells = 0;
-  float *d_H = nullptr, *d_G = nullptr, *d_Hlo = nullptr;
-  float2 *d_H2 = nullptr;       // paired heights for the chain-lanes trace (trace.cu k_pair_heights)
+  float *d_H = nullptr, *d_Hlo = nullptr;
+  macc *d_G = nullptr;          // ∂ℓ/∂H accumulator, chain-interleaved, fixed point (R30)
+  uint2 *d_cl = nullptr;        // chain-lanes per-evaluation cell bounds + paired heights (TraceArgs::cl)
+  float4 *d_ray_c = nullptr;    // chain-lanes per-ray record
+  uint8_t *d_tab = nullptr;     // chain-lanes band-entry table [R][MT_TABQ]
   float *d_Hc = nullptr;        // [min(max_chains, 16)][2N] contiguous heights for the ray-lanes trace
   float4 *d_band = nullptr;
-  double *d_ll = nullptr;
+  macc *d_ll = nullptr;         // log-likelihood accumulator, fixed point (R30)
   // HMC workspace
   float *d_x0 = nullptr, *d_g0 = nullptr, *d_mom = nullptr, *d_kin0 = nullptr, *d_kin1 = nullptr;
   double *d_lp0 = nullptr;
   // trace launch shape
   int trace_k = 0;              // chains per block (0 = auto)
   int trace_s = 0;              // ray splits (0 = auto)
+  int cl_v = -1;                // chain-lanes kernel (MT_CL_V): -1 auto (c2 at C >= 64, else v0), 0 v0, 2 c2, 3 v3
   int chunk = 0;                // chain lanes: rays per block (a Morton-ordered chunk; 0 = by chain count)
   // batched NUTS workspace (allocated by the first mt_nuts_step)
   float *nuts_ws = nullptr;
@@ -220,7 +255,7 @@ struct mt_problem {
 cudaError_t launch_heights(mt_problem *p, int C, const float *x, float *H, float4 *band,
                            cudaStream_t s);
 cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const float4 *band,
-                         float *G, double *ll, float *L, float *O, cudaStream_t s);
+                         macc *G, macc *ll, float *L, float *O, cudaStream_t s);
 cudaError_t launch_finish(mt_problem *p, int mode, int C, float *x, float *grad, double *logp,
                           int32_t *status, float *mom, const float *eps, float *kin,
                           cudaStream_t s);
@@ -244,7 +279,7 @@ cudaError_t build_traversal(mt_problem *p);
 // voxel.cu (f3)
 cudaError_t voxel_setup(mt_problem *p, int nz, float gamma, float tau, const float *Href);
 void voxel_free(mt_problem *p);
-cudaError_t launch_voxel(mt_problem *p, int C, const float *H, const float4 *band, float *G, double *ll,
+cudaError_t launch_voxel(mt_problem *p, int C, const float *H, const float4 *band, macc *G, macc *ll,
                          cudaStream_t s);
 cudaError_t launch_kick(mt_problem *p, int mode, int C, float *x, float *mom, const float *grad,
                         const float *eps, float *kin, cudaStream_t s);
@@ -266,6 +301,7 @@ cudaError_t launch_stats(mt_problem *p, int C, const float *x, const float *acc,
                          float *mean, float *m2, unsigned long long *acc_fixed, cudaStream_t s);
 cudaError_t launch_tile(mt_problem *p, int C, const float *src, float *dst, int to_tiled,
                         cudaStream_t s);
+cudaError_t launch_take_acc(mt_problem *p, int C, float *dldH, double *ll, cudaStream_t s);
 cudaError_t launch_summary(mt_problem *p, int C, const float *x, const double *logp, int nz, float gap,
                            double *acc, float *map_x, double *map_logp, cudaStream_t s);
 cudaError_t launch_nested_rhat_partials(mt_problem *p, int C, int M, const float *mean, const float *m2,

@@ -229,14 +229,14 @@ __global__ void __launch_bounds__(MT_THREADS) k_ncp_finish(FinishArgs a) {
   const Spec sp = block_spectrum(a.cs, N, vc[2 * N], vc[2 * N + 1], false);
   double *gx = sm + 4 * N + 4 * MT_MAX_AXIS;   // [2N] ∂ll/∂x
   const double *xw = a.xw + (size_t)c * 2 * N;
-  float *Gt = const_cast<float *>(a.G);
+  macc *Gt = const_cast<macc *>(a.G);
   double acc[4] = {0.0, 0.0, 0.0, 0.0};   // Σ t0 gx0, Σ t1 gx1, Σ z², bad
   for (int k = threadIdx.x; k < N; k += blockDim.x) {
     const NodeH h = node_heights(xw[k], xw[N + k], sp.inv_sigma[0], sp.inv_sigma[1], a.z_top, true);
     const size_t t0 = tix(c, 0, k, N), t1 = tix(c, 1, k, N);
-    const double G0 = Gt[t0], G1 = Gt[t1];
-    Gt[t0] = 0.f;
-    Gt[t1] = 0.f;
+    const double G0 = dq_g(Gt[t0]), G1 = dq_g(Gt[t1]);
+    Gt[t0] = 0;
+    Gt[t1] = 0;
     const double gx0 = G0 * h.J0 + G1 * h.J10, gx1 = G1 * h.J11;
     gx[k] = gx0;
     gx[N + k] = gx1;
@@ -272,10 +272,10 @@ __global__ void __launch_bounds__(MT_THREADS) k_ncp_finish(FinishArgs a) {
   if (threadIdx.x == 0) {
     gc[2 * N] = (float)gr[0];
     gc[2 * N + 1] = (float)gr[1];
-    double lp = a.ll[c];
+    double lp = dq_ll(a.ll[c]);
     if (a.prior_on)
       lp += -0.5 * acc[2] - N * log(2.0 * M_PI) + log(sp.r[0]) + log1p(-sp.r[0]) + log(sp.r[1]) + log1p(-sp.r[1]);
-    a.ll[c] = 0.0;
+    a.ll[c] = 0;
     a.logp[c] = lp;
     if (a.status) a.status[c] = (bad || !isfinite(lp) || !isfinite(gr[0]) || !isfinite(gr[1])) ? MT_STATUS_NONFINITE : 0;
   }
@@ -337,11 +337,11 @@ __global__ void __cluster_dims__(1, 2, 1) __launch_bounds__(MT_THREADS) k_ncp_fi
   double *gx = sm + 4 * N + 4 * MT_MAX_AXIS;   // [N] ∂ll/∂x_l
   __shared__ double part[3];                   // Σ z_l², non-finite flag, ∂/∂ρ_l
   const double *xw = a.xw + (size_t)c * 2 * N;
-  const float *Gt = a.G;
+  const macc *Gt = a.G;
   double acc[2] = {0.0, 0.0};   // Σ t_l gx_l, Σ z_l²
   for (int k = threadIdx.x; k < N; k += blockDim.x) {
     const NodeH h = node_heights(xw[k], xw[N + k], sp.inv_sigma[0], sp.inv_sigma[1], a.z_top, true);
-    const double G0 = Gt[tix(c, 0, k, N)], G1 = Gt[tix(c, 1, k, N)];
+    const double G0 = dq_g(Gt[tix(c, 0, k, N)]), G1 = dq_g(Gt[tix(c, 1, k, N)]);
     const double g = l == 0 ? G0 * h.J0 + G1 * h.J10 : G1 * h.J11;
     gx[k] = g;
     acc[0] += (l == 0 ? h.t0 : h.t1) * g;
@@ -350,8 +350,8 @@ __global__ void __cluster_dims__(1, 2, 1) __launch_bounds__(MT_THREADS) k_ncp_fi
   }
   block_sum<2>(acc);
   cluster.sync();   // both CTAs have read ∂ℓ/∂H: clear it (CTA l its surface)
-  float *Gw = const_cast<float *>(a.G);
-  for (int k = threadIdx.x; k < N; k += blockDim.x) Gw[tix(c, l, k, N)] = 0.f;
+  macc *Gw = const_cast<macc *>(a.G);
+  for (int k = threadIdx.x; k < N; k += blockDim.x) Gw[tix(c, l, k, N)] = 0;
   const Dft d = dft_setup(sm, a.nx, a.ny);
   int bad = 0;
   circ_apply(d, a.cs, sp.r[l], 0, [&](int k) { return gx[k]; });   // U ∂ll/∂x_l
@@ -377,11 +377,11 @@ __global__ void __cluster_dims__(1, 2, 1) __launch_bounds__(MT_THREADS) k_ncp_fi
   cluster.sync();
   if (l == 0 && threadIdx.x == 0) {
     const double *o = cluster.map_shared_rank(part, 1);
-    double lp = a.ll[c];
+    double lp = dq_ll(a.ll[c]);
     if (a.prior_on)
       lp += -0.5 * (part[0] + o[0]) - N * log(2.0 * M_PI) + log(sp.r[0]) + log1p(-sp.r[0]) + log(sp.r[1]) +
             log1p(-sp.r[1]);
-    a.ll[c] = 0.0;
+    a.ll[c] = 0;
     a.logp[c] = lp;
     if (a.status) a.status[c] = (part[1] != 0.0 || o[1] != 0.0 || !isfinite(lp)) ? MT_STATUS_NONFINITE : 0;
   }

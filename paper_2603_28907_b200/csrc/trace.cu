@@ -21,7 +21,9 @@
 //    intra-warp contention).
 //  * ray lanes (small C, e.g. the single-chain ray-sharded config): block = K
 //    chains with shared-memory height and gradient tiles, thread = ray.
+#include <cuda_fp16.h>
 #include <math.h>
+#include <string.h>
 
 #include <algorithm>
 
@@ -283,6 +285,48 @@ __device__ __forceinline__ bool solve32(float h00, float h10, float h01, float h
   return true;
 }
 
+// solve32 with the ray-only parts K = u0 β + v0 α, M = α β stored per cell (a0) and the
+// one-crossing root from the cancellation-free form with |g'| = √D (cl_solve's reading).
+template <class Emit>
+__device__ __forceinline__ bool solve32k(float h00, float h10, float h01, float h11, float4 cg, float2 km,
+                                         float za, float Ls, float dz, float &B, Emit &&emit) {
+  const float u0 = cg.x, v0 = cg.y, al = cg.z, be = cg.w;
+  const float b = h10 - h00, c = h01 - h00, e = (h11 - h10) - (h01 - h00);
+  const float g0 = (h00 - za) + u0 * (b + e * v0) + c * v0;
+  const float g1 = fmaf(b, al, fmaf(c, be, fmaf(e, km.x, -dz)));
+  const float g2 = e * km.y;
+  const float gL = g0 + Ls * (g1 + Ls * g2);
+  if (fabsf(g0) < ZTHR || fabsf(gL) < ZTHR) return false;
+  const bool p0 = g0 > 0.f, pL = gL > 0.f;
+  const float D = fmaf(g1, g1, -4.f * g2 * g0);
+  if (p0 != pL) {
+    if (!(D >= GTHR * GTHR)) return false;
+    const float r = rsqrtf(D), sq = D * r;
+    const float ssq = pL ? sq : -sq;
+    const bool nc = (g1 > 0.f) == pL;
+    const float t = fminf(fmaxf(__fdividef(nc ? -2.f * g0 : ssq - g1, nc ? g1 + ssq : 2.f * g2), 0.f), Ls);
+    B += p0 ? t : Ls - t;
+    emit(u0 + al * t, v0 + be * t, r);
+    return true;
+  }
+  const float a2 = 2.f * g2;
+  const bool vin = -g1 * a2 > 0.f && fabsf(g1) < Ls * fabsf(a2);
+  if (vin && D > 0.f && ((g2 > 0.f) == p0)) {
+    if (!(D >= GTHR * GTHR)) return false;
+    const float r = rsqrtf(D);
+    const float q = -0.5f * (g1 + copysignf(D * r, g1));
+    const float ta = __fdividef(g0, q), tb = __fdividef(q, g2);
+    const float t1 = fminf(ta, tb), t2 = fmaxf(ta, tb);
+    B += p0 ? Ls - (t2 - t1) : (t2 - t1);
+    emit(u0 + al * t1, v0 + be * t1, r);
+    emit(u0 + al * t2, v0 + be * t2, r);
+    return true;
+  }
+  if (vin && fabsf(D) < 2.f * fabsf(a2) * ZTHR) return false;
+  if (p0) B += Ls;
+  return true;
+}
+
 // Stored per-cell geometry {u, v, α, β} is taken at the cell's entry s_in; a
 // walk that starts inside the cell (at the band entry s_lo) moves it by
 // ds = s_lo - s_in.  For every later cell ds = 0 exactly.
@@ -307,12 +351,6 @@ __shared__ float sgeo[4][MT_MAX_AXIS];   // X, Y, 1/ΔX, 1/ΔY
 #ifndef MT_RCAP
 #define MT_RCAP 3
 #endif
-#ifndef MT_H2
-#define MT_H2 1
-#endif
-#ifndef MT_UBASE
-#define MT_UBASE 1
-#endif
 #ifndef MT_RL_GLOBAL_H
 #define MT_RL_GLOBAL_H 1
 #endif
@@ -330,14 +368,28 @@ __shared__ float sgeo[4][MT_MAX_AXIS];   // X, Y, 1/ΔX, 1/ΔY
 #ifndef MT_CL_MINB
 #define MT_CL_MINB 5
 #endif
+#ifndef MT_CACC
+#define MT_CACC 0
+#endif
+#ifndef V0_SOLVE
+#define V0_SOLVE 1
+#endif
+#ifndef V0_LAUNDER
+#define V0_LAUNDER 1
+#endif
+#ifndef V0_TILE
+#define V0_TILE 0
+#endif
 constexpr int RCAP = MT_RCAP;
 
-__device__ __forceinline__ void scatter4(float *Gl, int STRIDE, int base, int ny, float w, float u,
-                                         float v) {
-  atomicAdd(Gl + base * STRIDE, w * (1.f - u) * (1.f - v));
-  atomicAdd(Gl + (base + ny) * STRIDE, w * u * (1.f - v));
-  atomicAdd(Gl + (base + 1) * STRIDE, w * (1.f - u) * v);
-  atomicAdd(Gl + (base + ny + 1) * STRIDE, w * u * v);
+// G_l[node] += w φ_node(u, v) for the cell's 4 corners (a6), fixed point:
+// w is prescaled by MT_GQ (R30).
+__device__ __forceinline__ void scatter4(macc *Gl, int STRIDE, int base, int ny, float w, float u, float v) {
+  const float wa = w * (1.f - u), wb = w * u;
+  atomicAdd(Gl + base * STRIDE, q_raw(wa * (1.f - v)));
+  atomicAdd(Gl + (base + ny) * STRIDE, q_raw(wb * (1.f - v)));
+  atomicAdd(Gl + (base + 1) * STRIDE, q_raw(wa * v));
+  atomicAdd(Gl + (base + ny + 1) * STRIDE, q_raw(wb * v));
 }
 
 // ---------------------------------------------------------------------------
@@ -351,7 +403,7 @@ template <int STRIDE, bool SCAT>
 __device__ __forceinline__ void walk(const Ray &r, const int2 *__restrict__ cells,
                                      const float4 *__restrict__ cgeo, int k, int kend, float s0,
                                      float s_in0, float s_hi, int ny, int N, const float *Hk,
-                                     const float *Hlo, float *Gk, float4 bd, float &B0, float &B1,
+                                     const float *Hlo, macc *Gk, float4 bd, float &B0, float &B1,
                                      float4 *rec, int *n, float f0, float f1) {
   float s = s0, ds = s0 - s_in0;
   for (; k < kend; k++) {
@@ -370,7 +422,7 @@ __device__ __forceinline__ void walk(const Ray &r, const int2 *__restrict__ cell
       const float h00 = p[0], h10 = p[ny * STRIDE], h01 = p[STRIDE], h11 = p[ny * STRIDE + STRIDE];
       if (zb <= fminf(fminf(h00, h10), fminf(h01, h11))) { B += Ls; continue; }
       if (za >= fmaxf(fmaxf(h00, h10), fmaxf(h01, h11))) continue;
-      float *Gl = SCAT ? Gk + (size_t)l * N * STRIDE : nullptr;
+      macc *Gl = SCAT ? Gk + (size_t)l * N * STRIDE : nullptr;
       const float f = l ? f1 : f0;
       auto emit = [&](float u, float v, float ig) {
         if (SCAT) {
@@ -396,27 +448,6 @@ __device__ __forceinline__ void walk(const Ray &r, const int2 *__restrict__ cell
   }
 }
 
-// Scatter recorded crossings: G_l[node] += f_l · φ_node(u, v)/|g'|  (a6).
-template <int STRIDE>
-__device__ __forceinline__ void scatter_recs(const float4 *rec, const int *n, float *Gk, int N, int ny,
-                                             float f0, float f1) {
-#pragma unroll
-  for (int l = 0; l < 2; l++) {
-    for (int m = 0; m < n[l]; m++) {
-      const float4 q = rec[(l * RCAP + m) * MT_THREADS];
-      scatter4(Gk + (size_t)l * N * STRIDE, STRIDE, __float_as_int(q.x), ny, (l ? f1 : f0) * q.w, q.y, q.z);
-    }
-  }
-}
-
-// Trace one chain x ray (generic walk) from its band [s_lo, s_hi]: B0, B1 and,
-// in TRACE_LL mode, the adjoint scatter; returns ℓ_p (or writes the path
-// lengths in TRACE_PATH mode).  The scatter uses the records, or a second,
-// scattering walk when a surface had more than RCAP crossings.
-struct PairOut {
-  float B0, B1;
-};
-
 // First stored cell of the ray whose s_out exceeds s (binary search; the last
 // cell's s_out is s_exit > s), and the entry s_in of that cell.
 __device__ __forceinline__ int band_entry(const int2 *__restrict__ cells, int lo, int hi, float s,
@@ -430,29 +461,6 @@ __device__ __forceinline__ int band_entry(const int2 *__restrict__ cells, int lo
   }
   s_in = lo > first ? __int_as_float(__ldg(&cells[lo - 1].y)) : 0.f;
   return lo;
-}
-
-// Same, warp-cooperative (chain lanes, all 32 lanes converged, uniform
-// arguments): one coalesced load of 32 cells and a ballot per round.
-__device__ __forceinline__ int band_entry_warp(const int2 *__restrict__ cells, int lo, int hi, float s,
-                                               float &s_in) {
-  const int lane = threadIdx.x & 31;
-  float prev = 0.f;   // s_out of the cell before this round (0 before the first cell)
-  for (int b = lo; b < hi; b += 32) {
-    const int k = b + lane;
-    const float so = k < hi ? __int_as_float(__ldg(&cells[k].y)) : 3.0e38f;
-    const unsigned m = __ballot_sync(0xffffffffu, so > s);
-    const float before = __shfl_up_sync(0xffffffffu, so, 1);
-    if (m) {
-      const int f = __ffs(m) - 1;
-      const float sb = __shfl_sync(0xffffffffu, before, f);
-      s_in = f > 0 ? sb : prev;
-      return b + f;
-    }
-    prev = __shfl_sync(0xffffffffu, so, 31);
-  }
-  s_in = prev;
-  return hi - 1;
 }
 
 // Queue overflow: mark pair (c, ray) in the (C x R)-bit redo bitmap.
@@ -501,8 +509,9 @@ __device__ __forceinline__ void load_geometry(const TraceArgs &a, float *Xs, flo
 // traversal builder (create time): thread = ray; count pass then write pass
 // ---------------------------------------------------------------------------
 __global__ void k_build_trav(TraceArgs a, const int32_t *off, int32_t *count, int2 *cells, float4 *cgeo,
+                             float2 *ckm,
                              int2 *rl_head, uint4 *rl_code, uint32_t *rl_ovf,
-                             const int32_t *ovf_off) {
+                             const int32_t *ovf_off, uint8_t *tab) {
   __shared__ float Xs[MT_MAX_AXIS], Ys[MT_MAX_AXIS];
   const int nx = a.tc.nx, ny = a.tc.ny;
   for (int k = threadIdx.x; k < nx; k += blockDim.x) Xs[k] = a.X[k];
@@ -516,6 +525,12 @@ __global__ void k_build_trav(TraceArgs a, const int32_t *off, int32_t *count, in
   int n = 0;
   if (rl_head) rl_head[rr] = make_int2((off[rr + 1] - off[rr]) | (i << 8) | (j << 15), ovf_off[rr]);
   uint32_t cw[4] = {0u, 0u, 0u, 0u};
+  // band-entry table (chain lanes): tab[q] = the first cell whose s_out exceeds the ray
+  // parameter of height q z_top / MT_TABQ (less 1e-5 relative, so rounding of the
+  // trace's level choice can only start it a cell early)
+  int tq = 0;
+  const double lev = (double)a.tc.z_top / MT_TABQ / (double)q.r.dz;
+  uint8_t *tb = tab ? tab + (size_t)rr * MT_TABQ : nullptr;
   for (int guard = 0; guard < 4 * (MT_MAX_AXIS + 2); guard++) {
     float s_ev;
     int fc;
@@ -527,14 +542,19 @@ __global__ void k_build_trav(TraceArgs a, const int32_t *off, int32_t *count, in
     float s1 = fminf(s_ev, q.r.s_exit);
     const float so = fmaxf(s1, s);
     if (cells) {
-      cells[off[rr] + n] = make_int2(cell_pack(i, j, ny), __float_as_int(so));
-      // cell-local entry point and rates (a0), fp64 from the exact fp32 inputs
+      // cell-local entry point and rates (a0), fp64 from the exact fp32 inputs, and the
+      // ray-only parts of the cell solve's g1 and g2 (K = u β + v α, M = α β)
       const double ix = 1.0 / ((double)Xs[i + 1] - (double)Xs[i]);
       const double iy = 1.0 / ((double)Ys[j + 1] - (double)Ys[j]);
       const double u = ((double)q.r.ox + (double)s_in * (double)q.r.dx - (double)Xs[i]) * ix;
       const double v = ((double)q.r.oy + (double)s_in * (double)q.r.dy - (double)Ys[j]) * iy;
-      cgeo[off[rr] + n] = make_float4((float)u, (float)v, (float)((double)q.r.dx * ix), (float)((double)q.r.dy * iy));
+      const float uf = (float)u, vf = (float)v, af = (float)((double)q.r.dx * ix), bf = (float)((double)q.r.dy * iy);
+      cells[off[rr] + n] = make_int2(cell_pack(i, j, ny), __float_as_int(so));
+      cgeo[off[rr] + n] = make_float4(uf, vf, af, bf);
+      ckm[off[rr] + n] = make_float2((float)((double)uf * bf + (double)vf * af), (float)((double)af * bf));
     }
+    if (tb)
+      while (tq < MT_TABQ && (double)so > (double)tq * lev * (1.0 - 1e-5)) tb[tq++] = (uint8_t)n;
     s_in = so;
     n++;
     if (ev & 4) break;
@@ -544,10 +564,413 @@ __global__ void k_build_trav(TraceArgs a, const int32_t *off, int32_t *count, in
   }
   if (count) count[rr] = n;
   if (rl_code) rl_code[rr] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+  if (tb)
+    while (tq < MT_TABQ) tb[tq++] = (uint8_t)n;
 }
 
 // ---------------------------------------------------------------------------
 // K2, chain lanes: warp = one ray x 32 chains, lane = chain
+// ---------------------------------------------------------------------------
+// Per evaluation, k_cell_prep writes per-(chain, cell) corner bounds of both
+// surfaces (the bilinear min / max sit at corners), rounded OUTWARD to fp16
+// and packed as {half2(min H0, min H1), half2(max H0, max H1)}: the walk
+// classifies both surfaces of a cell with one 8-B load and two packed fp16
+// compares (the ray's z range rounded outward too), so a "fully below" /
+// "fully above" decision is always right and only a few more cells than
+// necessary reach the exact fp32 solve.  It also writes the paired heights
+// H2 = (H(i,j), H(i,j+1)) the solve reads (two 8-B loads per surface-cell).
+// Layouts [group][node][32] (bounds) and [group][l][node][32] (H2): a warp's
+// load is one contiguous line.  Lanes c >= C get bounds below every ray.
+__global__ void __launch_bounds__(MT_THREADS) k_cell_prep(const float *__restrict__ H, uint2 *__restrict__ cl, int C,
+                                                        int nx, int ny, int N, int64_t n) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int lane = (int)(t & 31);
+  const int64_t gn = t >> 5;
+  const int grp = (int)(gn / N), node = (int)(gn - (int64_t)grp * N);
+  const int i = node / ny, j = node - i * ny;
+  const bool cell = i < nx - 1 && j < ny - 1;
+  const size_t hb = ((size_t)grp * 2 * N + node) * 32 + lane;   // heights (chain-interleaved)
+  uint2 *o = cl + ((size_t)grp * 3 * N + node) * 32 + lane;      // [group][slot][node][lane]
+  float mn[2], mx[2];
+#pragma unroll
+  for (int l = 0; l < 2; l++) {
+    const float *p = H + hb + (size_t)l * N * 32;
+    const float h00 = p[0], h01 = j + 1 < ny ? p[32] : 0.f;
+    o[(size_t)(1 + l) * N * 32] = make_uint2(__float_as_uint(h00), __float_as_uint(h01));
+    if (cell) {
+      const float h10 = p[ny * 32], h11 = p[ny * 32 + 32];
+      mn[l] = fminf(fminf(h00, h01), fminf(h10, h11));
+      mx[l] = fmaxf(fmaxf(h00, h01), fmaxf(h10, h11));
+    }
+  }
+  if (!cell) return;
+  uint2 b;
+  if (grp * 32 + lane < C) {
+    b.x = (unsigned)__half_as_ushort(__float2half_rd(mn[0])) | ((unsigned)__half_as_ushort(__float2half_rd(mn[1])) << 16);
+    b.y = (unsigned)__half_as_ushort(__float2half_ru(mx[0])) | ((unsigned)__half_as_ushort(__float2half_ru(mx[1])) << 16);
+  } else {
+    b.x = b.y = 0xfc00fc00u;   // -inf: every cell lies "above" an inactive lane's surfaces
+  }
+  o[0] = b;
+}
+
+// One surface of one stored cell for this lane's chain, the ray piece
+// [s, s1] (za = s d_z, Ls = s1 - s) straddling the surface's corner range.
+// g(τ) = h(u0 + ατ, v0 + βτ) - d_z (s + τ) = g0 + g1 τ + g2 τ² (a3).  With
+// g(0), g(Δs) of different signs there is exactly one root, at which
+// |g'| = √D (D = g1² - 4 g0 g2, for either root of a quadratic): it is taken
+// from the form without cancellation — t = -2 g0/(g1 + s√D) when sign g1 =
+// s = sign g(Δs), else (s√D - g1)/(2 g2) — and 1/|g'| = rsqrt(D) is what the
+// adjoint needs (a6).  Equal signs: two roots iff the vertex lies inside and
+// g(vertex) has the other sign.  An ill-conditioned cell (|g| < ZTHR where
+// the ray enters or leaves, |g'| < GTHR at a root, a near-tangent vertex)
+// sets `defer`: the pair is re-done by k_trace_defer (fp32 + in-place fp64).
+// SCAT (the second walk of a pair with more than RCAP crossings of a surface):
+// crossings m >= RCAP are scattered (prescaled weight f), nothing else.
+template <int L, bool SCAT>
+__device__ __forceinline__ void cl_solve(const uint2 *__restrict__ CL, unsigned hi, int oy, float4 cg, float2 km,
+                                         float za, float Ls, float dz, unsigned node, float &B, int &n, int &defer,
+                                         float4 *rec, macc *Gp, float f) {
+  const uint2 r0 = __ldg(CL + hi), r1 = __ldg(CL + (hi + (unsigned)oy));   // (h00, h01), (h10, h11)
+  const float h00 = __uint_as_float(r0.x), h01 = __uint_as_float(r0.y), h10 = __uint_as_float(r1.x),
+              h11 = __uint_as_float(r1.y);
+  const float b = h10 - h00, c = h01 - h00, e = (h11 - h10) - (h01 - h00);
+  const float u0 = cg.x, v0 = cg.y, al = cg.z, be = cg.w;
+  const float g0 = (h00 - za) + u0 * (b + e * v0) + c * v0;
+  const float g1 = fmaf(b, al, fmaf(c, be, fmaf(e, km.x, -dz)));   // K = u0 β + v0 α (stored, a0)
+  const float g2 = e * km.y;                                        // M = α β
+  const float gL = g0 + Ls * (g1 + Ls * g2);
+  auto emit = [&](float t, float ig) {
+    const float u = u0 + al * t, v = v0 + be * t;
+    if (SCAT) {
+      if (n >= RCAP) {
+        const float wv = f * ig, wa = wv * (1.f - u), wb = wv * u;
+        atomicAdd(Gp, q_raw(wa * (1.f - v)));
+        atomicAdd(Gp + oy, q_raw(wb * (1.f - v)));
+        atomicAdd(Gp + 32, q_raw(wa * v));
+        atomicAdd(Gp + oy + 32, q_raw(wb * v));
+      }
+    } else if (n < RCAP) {
+      rec[(L * RCAP + n) * MT_THREADS] = make_float4(__uint_as_float(node), u, v, ig);
+    }
+    n++;
+  };
+  if (fabsf(g0) < ZTHR || fabsf(gL) < ZTHR) { defer = 1; return; }
+  const bool p0 = g0 > 0.f, pL = gL > 0.f;
+  const float D = fmaf(g1, g1, -4.f * g2 * g0);
+  if (p0 != pL) {                                   // exactly one crossing
+    if (!(D >= GTHR * GTHR)) { defer = 1; return; }
+    const float r = rsqrtf(D), sq = D * r;
+    const float ssq = pL ? sq : -sq;
+    const bool nc = (g1 > 0.f) == pL;
+    const float t = fminf(fmaxf(__fdividef(nc ? -2.f * g0 : ssq - g1, nc ? g1 + ssq : 2.f * g2), 0.f), Ls);
+    B += p0 ? t : Ls - t;
+    emit(t, r);
+    return;
+  }
+  const float a2 = 2.f * g2;
+  const bool vin = -g1 * a2 > 0.f && fabsf(g1) < Ls * fabsf(a2);   // vertex inside (0, Δs)
+  if (vin && D > 0.f && ((g2 > 0.f) == p0)) {       // two crossings (rare)
+    if (!(D >= GTHR * GTHR)) { defer = 1; return; }
+    const float r = rsqrtf(D);
+    const float q = -0.5f * (g1 + copysignf(D * r, g1));
+    const float ta = __fdividef(g0, q), tb = __fdividef(q, g2);
+    const float t1 = fminf(ta, tb), t2 = fmaxf(ta, tb);
+    B += p0 ? Ls - (t2 - t1) : (t2 - t1);
+    emit(t1, r);
+    emit(t2, r);
+    return;
+  }
+  if (vin && fabsf(D) < 2.f * fabsf(a2) * ZTHR) { defer = 1; return; }   // near-tangent
+  if (p0) B += Ls;
+}
+
+// The band-entry table (a0) gives the first stored cell to walk: the walk
+// starts at a stored cell boundary s0 <= s_lo (everything before it lies
+// below every surface of the warp's chains), so the stored per-cell entry
+// geometry applies as is.
+struct WalkStart {
+  int k, kend;
+  float s0;
+};
+
+__device__ __forceinline__ WalkStart cl_start(const TraceArgs &a, int rr, int tq, float koff_bits) {
+  WalkStart ws;
+  const int koff = __float_as_int(koff_bits);
+  ws.kend = __ldg(a.trav_off + rr + 1);
+  ws.k = koff + __ldg(a.tab + (size_t)rr * MT_TABQ + tq);
+  ws.s0 = ws.k > koff ? __int_as_float(__ldg(&a.trav[ws.k - 1].y)) : 0.f;
+  return ws;
+}
+
+// Classify the piece [za, zb] of a ray against both surfaces of a cell from the
+// packed fp16 corner bounds: za rounded down and zb rounded up to fp16 (so each
+// decision is conservative), two f16x2 compares with one predicate per half.
+// below_l: zb <= min H_l (the piece lies below surface l); st_l: neither below
+// nor above (za >= max H_l): the piece may cross surface l.
+__device__ __forceinline__ void classify2(float za, float zb, uint2 bq, bool &below0, bool &below1, bool &st0,
+                                          bool &st1) {
+  unsigned b0, b1, a0, a1;
+  asm("{\n\t.reg .pred p, q, r, t;\n\t"
+      ".reg .b16 ha, hb;\n\t"
+      ".reg .b32 za2, zb2;\n\t"
+      "cvt.rm.f16.f32 ha, %4;\n\t"
+      "cvt.rp.f16.f32 hb, %5;\n\t"
+      "mov.b32 za2, {ha, ha};\n\t"
+      "mov.b32 zb2, {hb, hb};\n\t"
+      "setp.le.f16x2 p|q, zb2, %6;\n\t"
+      "setp.ge.f16x2 r|t, za2, %7;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t"
+      "selp.u32 %1, 1, 0, q;\n\t"
+      "selp.u32 %2, 1, 0, r;\n\t"
+      "selp.u32 %3, 1, 0, t;\n\t}"
+      : "=r"(b0), "=r"(b1), "=r"(a0), "=r"(a1)
+      : "f"(za), "f"(zb), "r"(bq.x), "r"(bq.y));
+  below0 = b0;
+  below1 = b1;
+  st0 = !b0 && !a0;
+  st1 = !b1 && !a1;
+}
+
+// Scatter a lane's crossing records (a6): G_l[node] += f_l φ_node(u, v)/|g'| (f prescaled
+// by MT_GQ), fixed point; FAST: every weight below MT_QSMALL.
+// Per-lane cache of one cell's adjoint moments per surface (a6): consecutive rays of a
+// warp (Morton-adjacent) mostly cross a surface in the same cell, so the lane sums
+// W = Σ w, U = Σ w u, V = Σ w v, X = Σ w u v there (w = f/|g'|) and scatters the four
+// node values W - U - V + X, U - X, V - X, X (= Σ w φ_node) only when the cell changes:
+// far fewer 64-bit fixed-point atomics.  The sums follow the warp's fixed ray order, so
+// results stay bit-reproducible for a given launch shape (which depends on R only).
+struct CellAcc {
+  int node;             // cached cell's corner node, -1: empty
+  float W, U, V, X;
+};
+
+__device__ __forceinline__ void acc_flush(CellAcc &c, macc *Gl, int oy) {
+  if (c.node >= 0) {
+    macc *pg = Gl + ((unsigned)c.node << 5);
+    atomicAdd(pg, q_raw((c.W - c.U) - (c.V - c.X)));
+    atomicAdd(pg + oy, q_raw(c.U - c.X));
+    atomicAdd(pg + 32, q_raw(c.V - c.X));
+    atomicAdd(pg + oy + 32, q_raw(c.X));
+  }
+  c.node = -1;
+}
+
+__device__ __forceinline__ void acc_add(CellAcc &c, macc *Gl, int oy, int node, float w, float u, float v) {
+  if (node != c.node) {
+    acc_flush(c, Gl, oy);
+    c.node = node;
+    c.W = c.U = c.V = c.X = 0.f;
+  }
+  const float wu = w * u;
+  c.W += w;
+  c.U += wu;
+  c.V = fmaf(w, v, c.V);
+  c.X = fmaf(wu, v, c.X);
+}
+
+template <bool FAST>
+__device__ __forceinline__ void scatter_recs(const float4 *rec, int m0, int m1, macc *G0, int N, int oy, float f0,
+                                             float f1) {
+#pragma unroll 1
+  for (int m = 0; m < m0 + m1; m++) {
+    const int l = m >= m0;
+    const float4 q = rec[(l ? RCAP + m - m0 : m) * MT_THREADS];
+    const float wv = (l ? f1 : f0) * q.w, u = q.y, v = q.z, wa = wv * (1.f - u), wb = wv * u;
+    macc *pg = G0 + (l ? N * 32 : 0) + (__float_as_uint(q.x) << 5);
+    if (FAST) {
+      atomicAdd(pg, q_small(wa * (1.f - v)));
+      atomicAdd(pg + oy, q_small(wb * (1.f - v)));
+      atomicAdd(pg + 32, q_small(wa * v));
+      atomicAdd(pg + oy + 32, q_small(wb * v));
+    } else {
+      atomicAdd(pg, q_raw(wa * (1.f - v)));
+      atomicAdd(pg + oy, q_raw(wb * (1.f - v)));
+      atomicAdd(pg + 32, q_raw(wa * v));
+      atomicAdd(pg + oy + 32, q_raw(wb * v));
+    }
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a) {
+  extern __shared__ __align__(16) float4 recs[];   // crossing records [2*RCAP][MT_THREADS] (dynamic: a static
+                                                   // array of the same size measured 13% slower, carveout)
+  const int N = a.tc.N, oy = a.tc.ny * 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = blockIdx.y, c = grp * 32 + lane;
+  const bool act = c < a.C;
+  float4 *rec = recs + threadIdx.x;
+  // the warp walks the union band of its 32 chains
+  float zlo = 3.0e38f, zhi = -3.0e38f;
+  if (act) {
+    const float4 bd = __ldg(a.band + c);
+    zlo = bd.x;
+    zhi = bd.w;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    zlo = fminf(zlo, __shfl_xor_sync(0xffffffffu, zlo, o));
+    zhi = fmaxf(zhi, __shfl_xor_sync(0xffffffffu, zhi, o));
+  }
+  const int tq = min(max((int)(zlo * a.tab_scale), 0), MT_TABQ - 1);   // band-entry level
+  // [group][slot][node][lane] 8-byte elements (slot 0 bounds, 1-2 paired heights), addressed by
+  // 32-bit element indices off the array base (C 3N 32 < 2^32)
+  const uint2 *__restrict__ CL = a.cl;
+  const unsigned lb = (unsigned)grp * 3u * (unsigned)N * 32u + (unsigned)lane, n32 = (unsigned)N * 32u;
+  macc llq = 0;
+#if MT_CACC
+  CellAcc ca0{-1, 0.f, 0.f, 0.f, 0.f}, ca1{-1, 0.f, 0.f, 0.f, 0.f};
+#endif
+
+  const int r_begin = blockIdx.x * (int)a.rays_per_block;
+  const int r_end = min((int)a.R, r_begin + (int)a.rays_per_block);
+  for (int rr = r_begin + warp; rr < r_end; rr += MT_THREADS / 32) {
+    const float4 rc = __ldg(a.ray_c + rr);   // {d_z, 1/d_z, s_exit, first cell}
+    const float dz = rc.x, s_exit = rc.z;
+    // band bounds, widened by 1e-6 so rounding can only walk more cells
+    const float s_lo = fminf(zlo * rc.y * (1.f - 1e-6f), s_exit);
+    const float s_hi = fminf(zhi * rc.y * (1.f + 1e-6f), s_exit);
+    float B0 = s_lo, B1 = s_lo;                        // below both surfaces before s_lo
+    int n0 = 0, n1 = 0, defer = 0;
+    WalkStart ws{0, 0, 0.f};
+    if (s_lo < s_exit) {                               // warp-uniform
+      ws = cl_start(a, rr, tq, rc.w);
+      B0 = B1 = ws.s0;
+      float s = ws.s0, za = ws.s0 * dz;
+      // software pipeline: the cell word two cells ahead and the corner bounds one cell
+      // ahead are in flight while a cell is classified and solved
+      int k = ws.k;
+      int2 w1 = __ldg(a.trav + k);
+      int2 w2 = k + 1 < ws.kend ? __ldg(a.trav + k + 1) : make_int2(0, 0);
+      uint2 bq1 = __ldg(CL + (lb + cell_off32(w1.x)));
+      for (; k < ws.kend; k++) {
+        const int2 w = w1;
+        const uint2 bq = bq1;
+        w1 = w2;
+        if (k + 1 < ws.kend) bq1 = __ldg(CL + (lb + cell_off32(w1.x)));
+        if (k + 2 < ws.kend) w2 = __ldg(a.trav + k + 2);
+        const unsigned off = cell_off32(w.x);
+        const float s1 = __int_as_float(w.y);
+        const float zb = s1 * dz, Ls = s1 - s;
+        bool bl0, bl1, st0, st1;
+        classify2(za, zb, bq, bl0, bl1, st0, st1);
+        if (bl0) B0 += Ls;
+        if (bl1) B1 += Ls;
+        if (st0 || st1) {
+          const float4 cg = __ldg(a.trav_geo + k);
+          const float2 km = __ldg(a.trav_km + k);
+          if (st0) cl_solve<0, false>(CL, lb + n32 + off, oy, cg, km, za, Ls, dz, off >> 5, B0, n0, defer, rec, nullptr, 0.f);
+          if (st1) cl_solve<1, false>(CL, lb + 2 * n32 + off, oy, cg, km, za, Ls, dz, off >> 5, B1, n1, defer, rec, nullptr, 0.f);
+        }
+        if (s1 >= s_hi) break;
+        s = s1;
+        za = zb;
+      }
+    }
+    // an ill-conditioned cell: the whole pair goes to k_trace_defer (fp64 re-solve)
+    if (defer) {
+      const int q = atomicAdd(a.ovf_n, 1);
+      if (q < a.ovf_cap) a.ovf_q[q] = make_float4(__int_as_float(c), __int_as_float(rr), s_lo, s_hi);
+      else redo_mark(a, c, rr);   // queue full: the follow-up kernel finds the pair in the bitmap
+    }
+    if (MODE == TRACE_LL) {
+      const bool over = !defer && (n0 > RCAP || n1 > RCAP);   // more crossings than records
+      float f0 = 0.f, f1 = 0.f;
+      macc *G0 = a.G + (size_t)grp * 2 * N * 32 + lane;
+      if (!defer && act) {
+        const float2 rb = __ldg(reinterpret_cast<const float2 *>(a.ray_b + rr) + 1);
+        float dldO;
+        llq += q_ll(epilogue(rb.x, rb.y, a.tc, B0, B1, dldO));
+        f0 = dldO * a.tc.k0 * (float)MT_GQ;
+        f1 = dldO * a.tc.k1 * (float)MT_GQ;
+      }
+      // fixed-point scatter (a6): the corner weights w φ are bounded by |w| = |f|/|g'| <=
+      // |f|/GTHR, so when every lane's bound is below MT_QSMALL the warp converts on the
+      // FMA pipe (q_small), else with F2I.S64
+#if MT_CACC
+      if (!defer) {
+        for (int m = 0; m < min(n0, RCAP); m++) {
+          const float4 q = rec[m * MT_THREADS];
+          acc_add(ca0, G0, oy, (int)__float_as_uint(q.x), f0 * q.w, q.y, q.z);
+        }
+        for (int m = 0; m < min(n1, RCAP); m++) {
+          const float4 q = rec[(RCAP + m) * MT_THREADS];
+          acc_add(ca1, G0 + N * 32, oy, (int)__float_as_uint(q.x), f1 * q.w, q.y, q.z);
+        }
+      }
+#else
+      const int r0 = defer ? 0 : min(n0, RCAP), r1 = defer ? 0 : min(n1, RCAP);
+      if (__all_sync(0xffffffffu, fmaxf(fabsf(f0), fabsf(f1)) * (1.f / GTHR) < MT_QSMALL))
+        scatter_recs<true>(rec, r0, r1, G0, N, oy, f0, f1);
+      else
+        scatter_recs<false>(rec, r0, r1, G0, N, oy, f0, f1);
+#endif
+      if (__any_sync(0xffffffffu, over)) {   // wide bands (e.g. prior draws): re-walk, scatter the rest
+        int m0 = 0, m1 = 0, dd = 0;
+        float Bd = 0.f, s = ws.s0, za = ws.s0 * dz;
+        for (int k = ws.k; k < ws.kend; k++) {
+          const int2 w = __ldg(a.trav + k);
+          const float s1 = __int_as_float(w.y);
+          const float zb = s1 * dz, Ls = s1 - s;
+          if (over) {
+            const unsigned off = cell_off32(w.x);
+            bool bl0, bl1, st0, st1;
+            classify2(za, zb, __ldg(CL + (lb + off)), bl0, bl1, st0, st1);
+            const float4 cg = __ldg(a.trav_geo + k);
+            const float2 km = __ldg(a.trav_km + k);
+            if (n0 > RCAP && st0)
+              cl_solve<0, true>(CL, lb + n32 + off, oy, cg, km, za, Ls, dz, 0u, Bd, m0, dd, nullptr, G0 + off, f0);
+            if (n1 > RCAP && st1)
+              cl_solve<1, true>(CL, lb + 2 * n32 + off, oy, cg, km, za, Ls, dz, 0u, Bd, m1, dd, nullptr, G0 + N * 32 + off, f1);
+          }
+          if (s1 >= s_hi) break;
+          s = s1;
+          za = zb;
+        }
+      }
+    } else if (act && !defer) {
+      const int64_t o = (int64_t)c * a.R + __ldg(a.perm + rr);
+      a.Lout[3 * o + 0] = B0;
+      a.Lout[3 * o + 1] = B1 - B0;
+      a.Lout[3 * o + 2] = s_exit - B1;
+      a.Oout[o] = a.tc.k0 * B0 + a.tc.k1 * B1 + a.obase[rr];
+    }
+  }
+  if (MODE == TRACE_LL && act) {
+    atomicAdd(a.ll + c, llq);
+#if MT_CACC
+    macc *G0 = a.G + (size_t)grp * 2 * N * 32 + lane;
+    acc_flush(ca0, G0, oy);
+    acc_flush(ca1, G0 + N * 32, oy);
+#endif
+  }
+}
+
+// ---- round-1 chain-lanes kernel (A/B baseline while the new one is tuned) ----
+// Same, warp-cooperative (chain lanes, all 32 lanes converged, uniform
+// arguments): one coalesced load of 32 cells and a ballot per round.
+__device__ __forceinline__ int band_entry_warp(const int2 *__restrict__ cells, int lo, int hi, float s,
+                                               float &s_in) {
+  const int lane = threadIdx.x & 31;
+  float prev = 0.f;   // s_out of the cell before this round (0 before the first cell)
+  for (int b = lo; b < hi; b += 32) {
+    const int k = b + lane;
+    const float so = k < hi ? __int_as_float(__ldg(&cells[k].y)) : 3.0e38f;
+    const unsigned m = __ballot_sync(0xffffffffu, so > s);
+    const float before = __shfl_up_sync(0xffffffffu, so, 1);
+    if (m) {
+      const int f = __ffs(m) - 1;
+      const float sb = __shfl_sync(0xffffffffu, before, f);
+      s_in = f > 0 ? sb : prev;
+      return b + f;
+    }
+    prev = __shfl_sync(0xffffffffu, so, 31);
+  }
+  s_in = prev;
+  return hi - 1;
+}
+
 // ---------------------------------------------------------------------------
 // One surface of one stored cell for this lane's chain.  Warp-uniform inputs:
 // the cell word w (node offset, i, j), its geometry cg, the piece [s, s1] of
@@ -557,9 +980,10 @@ __global__ void k_build_trav(TraceArgs a, const int32_t *off, int32_t *count, in
 // to k_trace_defer (same fp32 cell code plus in-place fp64 re-solves), so the
 // hot kernel holds no double-precision code and makes no calls (a call forces
 // the ABI's spills into the loop).
-template <int L>
+template <int L, bool KM = false>
 __device__ __forceinline__ void cw_solve(float4 h, int w, float4 cg, float za, float zb, float Ls,
-                                         float dz, float &B, int &n, int &defer, float4 *rec) {
+                                         float dz, float &B, int &n, int &defer, float4 *rec,
+                                         float2 km = make_float2(0.f, 0.f)) {
   const float h00 = h.x, h01 = h.y, h10 = h.z, h11 = h.w;
   if (zb <= fminf(fminf(h00, h10), fminf(h01, h11))) { B += Ls; return; }   // bilinear min at a corner
   if (za >= fmaxf(fmaxf(h00, h10), fmaxf(h01, h11))) return;
@@ -568,7 +992,11 @@ __device__ __forceinline__ void cw_solve(float4 h, int w, float4 cg, float za, f
     if (n < RCAP) rec[(L * RCAP + n) * MT_THREADS] = make_float4(wbase, u, v, ig);
     n++;
   };
-  if (!solve32(h00, h10, h01, h11, cg, za, Ls, dz, B, emit)) defer = 1;
+  if (KM) {
+    if (!solve32k(h00, h10, h01, h11, cg, km, za, Ls, dz, B, emit)) defer = 1;
+  } else if (!solve32(h00, h10, h01, h11, cg, za, Ls, dz, B, emit)) {
+    defer = 1;
+  }
 }
 
 // Second pass of a pair with more than RCAP crossings of a surface (dℓ/dO now
@@ -576,7 +1004,7 @@ __device__ __forceinline__ void cw_solve(float4 h, int w, float4 cg, float za, f
 // first RCAP were stored and scattered from the records).
 __device__ __forceinline__ void cw_scatter_surface(const float *__restrict__ Hg, unsigned off, int oy, float4 cg,
                                                    float za, float zb, float Ls, float dz, float zmin, float zmax,
-                                                   float *Gp, float f, int &m) {
+                                                   macc *Gp, float f, int &m, float2 km) {
   if (zb <= zmin || za >= zmax) return;
   const float *p = Hg + off;
   const float h00 = __ldg(p), h01 = __ldg(p + 32), h10 = __ldg(p + oy), h11 = __ldg(p + oy + 32);
@@ -585,44 +1013,53 @@ __device__ __forceinline__ void cw_scatter_surface(const float *__restrict__ Hg,
   float Bd = 0.f;
   auto emit = [&](float u, float v, float ig) {
     if (m >= RCAP) {
-      const float wv = f * ig;
-      atomicAdd(Gp, wv * (1.f - u) * (1.f - v));
-      atomicAdd(Gp + oy, wv * u * (1.f - v));
-      atomicAdd(Gp + 32, wv * (1.f - u) * v);
-      atomicAdd(Gp + oy + 32, wv * u * v);
+      const float wv = f * ig, wa = wv * (1.f - u), wb = wv * u;
+      atomicAdd(Gp, q_raw(wa * (1.f - v)));
+      atomicAdd(Gp + oy, q_raw(wb * (1.f - v)));
+      atomicAdd(Gp + 32, q_raw(wa * v));
+      atomicAdd(Gp + oy + 32, q_raw(wb * v));
     }
     m++;
   };
-  solve32(h00, h10, h01, h11, cg, za, Ls, dz, Bd, emit);
+  // the same solve as the first walk (V0_SOLVE), so crossing m is the same crossing
+  if (V0_SOLVE) solve32k(h00, h10, h01, h11, cg, km, za, Ls, dz, Bd, emit);
+  else solve32(h00, h10, h01, h11, cg, za, Ls, dz, Bd, emit);
 }
 
 template <int L>
 __device__ __forceinline__ void cw_surface(const float *__restrict__ Hg, unsigned off, int w, int oy,
                                            float4 cg, float za, float zb, float Ls, float dz, float zmin,
-                                           float zmax, float &B, int &n, int &defer, float4 *rec) {
+                                           float zmax, float &B, int &n, int &defer, float4 *rec, float2 km) {
   if (zb <= zmin) { B += Ls; return; }            // below the chain's lowest node of this surface
   if (za >= zmax) return;                         // above its highest node
-#if MT_H2
   // paired heights: element k holds (H(i,j), H(i,j+1)), so a cell's four corners are two 8-byte loads.
   // Hg is the chain group's (warp-uniform) base and off the cell's uniform offset + the lane.
   const float2 *p2 = reinterpret_cast<const float2 *>(Hg) + off;
   const float2 r0 = __ldg(p2), r1 = __ldg(p2 + oy);
-  cw_solve<L>(make_float4(r0.x, r0.y, r1.x, r1.y), w, cg, za, zb, Ls, dz, B, n, defer, rec);
-#else
-  const float *p = Hg + off;   // Hg: the heights array (kernel parameter); off: 32-bit element index
-  cw_solve<L>(make_float4(__ldg(p), __ldg(p + 32), __ldg(p + oy), __ldg(p + oy + 32)), w, cg, za, zb, Ls,
-              dz, B, n, defer, rec);
-#endif
+  cw_solve<L, V0_SOLVE>(make_float4(r0.x, r0.y, r1.x, r1.y), w, cg, za, zb, Ls, dz, B, n, defer, rec, km);
 }
 
+
 template <int MODE, int NY>
-__global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a) {
+__global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_v0(TraceArgs a) {
   extern __shared__ __align__(16) float4 recs[];    // crossing records [2*RCAP][MT_THREADS]
   const int ny = NY ? NY : a.tc.ny, N = a.tc.N;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int grp = blockIdx.y, c = grp * 32 + lane;
+#if V0_TILE
+  // block order: tiles of V0_TILE ray chunks x all chain groups (L2 reuse of the chunk's
+  // traversal records across groups)
+  const int lin = blockIdx.y * gridDim.x + blockIdx.x, G_ = gridDim.y;
+  const int tile = lin / (G_ * V0_TILE), within = lin - tile * (G_ * V0_TILE);
+  const int grp = within / V0_TILE, chunk = tile * V0_TILE + (within - (within / V0_TILE) * V0_TILE);
+#else
+  const int grp = blockIdx.y, chunk = blockIdx.x;
+#endif
+  const int c = grp * 32 + lane;
   const bool act = c < a.C;
   float4 *rec = recs + threadIdx.x;
+#if V0_LAUNDER
+  asm volatile("mov.b64 %0, %0;" : "+l"(rec));   // keep, do not rematerialise per emit
+#endif
   // this lane's chain band; the warp walks the union band of its 32 chains.
   // Inactive lanes get a band that every cell lies "above" (no loads).
   float4 bd = act ? __ldg(a.band + c) : make_float4(3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f);
@@ -634,13 +1071,16 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a
   if (!act) bd = make_float4(-3.0e38f, -3.0e38f, -3.0e38f, -3.0e38f);
   const int oy = ny * 32;
   const unsigned gbase = (unsigned)grp * 2 * N * 32 + lane;   // this lane's column of the group tile
-#if MT_H2 && MT_UBASE
-  const float2 *__restrict__ H2g = a.H2 + (size_t)grp * 2 * N * 32;   // warp-uniform bases
-  const float2 *__restrict__ H2g1 = H2g + (size_t)N * 32;
+  const float2 *__restrict__ H2g = reinterpret_cast<const float2 *>(a.cl) + (size_t)grp * 3 * N * 32 + (size_t)N * 32;
+#if V0_LAUNDER
+  // opaque copy: otherwise the compiler rematerialises this base from CTAID and the kernel
+  // parameters at every corner load (12 uniform-datapath instructions per surface-cell)
+  asm volatile("mov.b64 %0, %0;" : "+l"(H2g));
 #endif
-  float llacc = 0.f;
+  const float2 *__restrict__ H2g1 = H2g + (size_t)N * 32;   // warp-uniform bases (arena slots 1, 2)
+  macc llq = 0;
 
-  const int r_begin = blockIdx.x * (int)a.rays_per_block;
+  const int r_begin = chunk * (int)a.rays_per_block;
   const int r_end = min((int)a.R, r_begin + (int)a.rays_per_block);
   for (int rr = r_begin + warp; rr < r_end; rr += MT_THREADS / 32) {
     float dz, s_exit;
@@ -665,20 +1105,18 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a
         const float4 cg = shift_geo(__ldg(a.trav_geo + k), ds);
         const float s1 = __int_as_float(w.y);
         const float zb = s1 * dz, Ls = s1 - s;
-#if MT_H2 && MT_UBASE
+        float2 km = make_float2(0.f, 0.f);
+        if (V0_SOLVE) {
+          km = __ldg(a.trav_km + k);
+          km.x = fmaf(2.f * km.y, ds, km.x);   // K of the shifted entry point (first cell only)
+        }
         // uniform group base (a scalar register pair) + the cell's offset + the lane
         const unsigned offl = cell_off32(w.x) + (unsigned)lane;
         cw_surface<0>(reinterpret_cast<const float *>(H2g), offl, w.x, oy, cg, za, zb, Ls, dz, bd.x, bd.y, B0, n0,
-                      defer, rec);
+                      defer, rec, km);
         cw_surface<1>(reinterpret_cast<const float *>(H2g1), offl, w.x, oy, cg, za, zb, Ls, dz, bd.z, bd.w, B1, n1,
-                      defer, rec);
-#else
-        const unsigned off = cell_off32(w.x) + gbase;   // 32-bit element index (C·P < 2^32)
-        cw_surface<0>(MT_H2 ? reinterpret_cast<const float *>(a.H2) : a.H, off, w.x, oy, cg, za, zb, Ls, dz, bd.x,
-                      bd.y, B0, n0, defer, rec);
-        cw_surface<1>(MT_H2 ? reinterpret_cast<const float *>(a.H2) : a.H, off + N * 32, w.x, oy, cg, za, zb, Ls,
-                      dz, bd.z, bd.w, B1, n1, defer, rec);
-#endif
+                      defer, rec, km);
+
         if (s1 >= s_hi) break;
         s = s1;
         za = zb;
@@ -694,32 +1132,33 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a
     if (MODE == TRACE_LL) {
       const bool over = !defer && (n0 > RCAP || n1 > RCAP);   // more crossings than records
       float f0 = 0.f, f1 = 0.f;
-      float *G0 = a.G + (size_t)grp * 2 * N * 32 + lane;
+      macc *G0 = a.G + (size_t)grp * 2 * N * 32 + lane;
       if (!defer && act) {
         const float2 rb = __ldg(reinterpret_cast<const float2 *>(a.ray_b + rr) + 1);
         float dldO;
-        const float ll = epilogue(rb.x, rb.y, a.tc, B0, B1, dldO);
-        llacc += ll;
-        f0 = dldO * a.tc.k0;
-        f1 = dldO * a.tc.k1;
+        llq += q_ll(epilogue(rb.x, rb.y, a.tc, B0, B1, dldO));
+        f0 = dldO * a.tc.k0 * (float)MT_GQ;
+        f1 = dldO * a.tc.k1 * (float)MT_GQ;
         for (int m = 0; m < min(n0, RCAP); m++) {
           const float4 q = rec[m * MT_THREADS];
           const float w = f0 * q.w, u = q.y, v = q.z;
-          float *pg = G0 + ((unsigned)__float_as_int(q.x) << 5);
-          atomicAdd(pg, w * (1.f - u) * (1.f - v));
-          atomicAdd(pg + oy, w * u * (1.f - v));
-          atomicAdd(pg + 32, w * (1.f - u) * v);
-          atomicAdd(pg + oy + 32, w * u * v);
+          macc *pg = G0 + ((unsigned)__float_as_int(q.x) << 5);
+          const float wa = w * (1.f - u), wb = w * u;
+          atomicAdd(pg, q_raw(wa * (1.f - v)));
+          atomicAdd(pg + oy, q_raw(wb * (1.f - v)));
+          atomicAdd(pg + 32, q_raw(wa * v));
+          atomicAdd(pg + oy + 32, q_raw(wb * v));
         }
-        float *G1 = G0 + N * 32;
+        macc *G1 = G0 + N * 32;
         for (int m = 0; m < min(n1, RCAP); m++) {
           const float4 q = rec[(RCAP + m) * MT_THREADS];
           const float w = f1 * q.w, u = q.y, v = q.z;
-          float *pg = G1 + ((unsigned)__float_as_int(q.x) << 5);
-          atomicAdd(pg, w * (1.f - u) * (1.f - v));
-          atomicAdd(pg + oy, w * u * (1.f - v));
-          atomicAdd(pg + 32, w * (1.f - u) * v);
-          atomicAdd(pg + oy + 32, w * u * v);
+          macc *pg = G1 + ((unsigned)__float_as_int(q.x) << 5);
+          const float wa = w * (1.f - u), wb = w * u;
+          atomicAdd(pg, q_raw(wa * (1.f - v)));
+          atomicAdd(pg + oy, q_raw(wb * (1.f - v)));
+          atomicAdd(pg + 32, q_raw(wa * v));
+          atomicAdd(pg + oy + 32, q_raw(wb * v));
         }
       }
       if (__any_sync(0xffffffffu, over)) {   // wide bands (e.g. prior draws): re-walk, scatter the rest
@@ -734,11 +1173,13 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a
           const float s1 = __int_as_float(w.y);
           const float zb = s1 * dz, Ls = s1 - s;
           if (over) {
+            float2 km = __ldg(a.trav_km + k);
+            km.x = fmaf(2.f * km.y, ds, km.x);
             const unsigned off = cell_off32(w.x) + gbase;
-            float *pg = G0 + ((unsigned)(cell_off32(w.x)));
-            if (n0 > RCAP) cw_scatter_surface(a.H, off, oy, cg, za, zb, Ls, dz, bd.x, bd.y, pg, f0, m0);
+            macc *pg = G0 + ((unsigned)(cell_off32(w.x)));
+            if (n0 > RCAP) cw_scatter_surface(a.H, off, oy, cg, za, zb, Ls, dz, bd.x, bd.y, pg, f0, m0, km);
             if (n1 > RCAP) cw_scatter_surface(a.H, off + N * 32, oy, cg, za, zb, Ls, dz, bd.z, bd.w,
-                                              pg + N * 32, f1, m1);
+                                              pg + N * 32, f1, m1, km);
           }
           if (s1 >= s_hi) break;
           s = s1;
@@ -754,7 +1195,231 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a
       a.Oout[o] = a.tc.k0 * B0 + a.tc.k1 * B1 + a.obase[rr];
     }
   }
-  if (MODE == TRACE_LL && act) atomicAdd(a.ll + c, (double)llacc);
+  if (MODE == TRACE_LL && act) atomicAdd(a.ll + c, llq);
+}
+
+// ---------------------------------------------------------------------------
+// K2, chain lanes with two chains per lane (C >= 64): warp = one ray x 64
+// chains, lane l = chains 64g + l and 64g + 32 + l.  The ray's traversal,
+// band entry, cell records and loop control are shared by twice as many
+// chains as in k_trace_v0, and each lane carries two independent solve
+// chains (latency hiding).  Paired heights of both chains in one 16-B load:
+// [g64][l][node][lane] float4 {H_A(i,j), H_A(i,j+1), H_B(i,j), H_B(i,j+1)}
+// (k_cell_prep2).  Blocks run in tiles of C2_TILE ray chunks x all chain
+// groups, so a chunk's traversal records are reused from L2 by every group.
+// ---------------------------------------------------------------------------
+#ifndef C2_TILE
+#define C2_TILE 8
+#endif
+#ifndef C2_RCAP
+#define C2_RCAP 2
+#endif
+#ifndef C2_MINB
+#define C2_MINB 4
+#endif
+
+__global__ void __launch_bounds__(MT_THREADS) k_cell_prep2(const float *__restrict__ H, float4 *__restrict__ H4, int C,
+                                                         int ny, int N, int64_t n) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // [g64][l][node][lane]
+  if (t >= n) return;
+  const int lane = (int)(t & 31);
+  const int64_t q = t >> 5;
+  const int node = (int)(q % N), l = (int)((q / N) & 1), g = (int)(q / (2 * (int64_t)N));
+  const int j = node % ny;
+  float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int v = 0; v < 2; v++) {
+    const int c = g * 64 + v * 32 + lane;
+    if (c < C) {
+      const float *p = H + (((size_t)(c >> 5) * 2 + l) * N + node) * 32 + lane;
+      const float h0 = p[0], h1 = j + 1 < ny ? p[32] : 0.f;
+      if (v == 0) { o.x = h0; o.y = h1; } else { o.z = h0; o.w = h1; }
+    } else if (v == 0) {
+      o.x = o.y = -3.0e38f;   // never loaded: the lane-union band skips inactive chains
+    } else {
+      o.z = o.w = -3.0e38f;
+    }
+  }
+  H4[t] = o;
+}
+
+// One chain's surface-cell from its corners (the corner-bound test, then the solve).
+template <int SLOT, bool SCAT>
+__device__ __forceinline__ void c2_cell(float h00, float h01, float h10, float h11, float4 cg, float2 km, float za,
+                                        float zb, float Ls, float dz, float wbase, float &B, int &n, int &defer,
+                                        float4 *rec, macc *Gp, int oy, float f) {
+  if (zb <= fminf(fminf(h00, h10), fminf(h01, h11))) { B += Ls; return; }   // bilinear min at a corner
+  if (za >= fmaxf(fmaxf(h00, h10), fmaxf(h01, h11))) return;
+  auto emit = [&](float u, float v, float ig) {
+    if (SCAT) {
+      if (n >= C2_RCAP) {
+        const float wv = f * ig, wa = wv * (1.f - u), wb = wv * u;
+        atomicAdd(Gp, q_raw(wa * (1.f - v)));
+        atomicAdd(Gp + oy, q_raw(wb * (1.f - v)));
+        atomicAdd(Gp + 32, q_raw(wa * v));
+        atomicAdd(Gp + oy + 32, q_raw(wb * v));
+      }
+    } else if (n < C2_RCAP) {
+      rec[(SLOT * C2_RCAP + n) * MT_THREADS] = make_float4(wbase, u, v, ig);
+    }
+    n++;
+  };
+  if (!solve32k(h00, h10, h01, h11, cg, km, za, Ls, dz, B, emit)) defer = 1;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(MT_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
+  extern __shared__ __align__(16) float4 recs[];   // [chain v][surface l][C2_RCAP][MT_THREADS]
+  const int N = a.tc.N, oy = a.tc.ny * 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lin = blockIdx.y * gridDim.x + blockIdx.x, G2 = gridDim.y;
+  const int tile = lin / (G2 * C2_TILE), within = lin - tile * (G2 * C2_TILE);
+  const int g = within / C2_TILE, chunk = tile * C2_TILE + (within - (within / C2_TILE) * C2_TILE);
+  const int cA = g * 64 + lane, cB = cA + 32;
+  const bool actA = cA < a.C, actB = cB < a.C;
+  float4 *rec = recs + threadIdx.x;
+  asm volatile("mov.b64 %0, %0;" : "+l"(rec));
+  // lane-union band of its two chains per surface; the warp walks the union over 64 chains
+  float4 bd = make_float4(3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f);
+  if (actA) bd = __ldg(a.band + cA);
+  if (actB) {
+    const float4 b = __ldg(a.band + cB);
+    bd = make_float4(fminf(bd.x, b.x), fmaxf(bd.y, b.y), fminf(bd.z, b.z), fmaxf(bd.w, b.w));
+  }
+  float zlo = bd.x, zhi = bd.w;
+  for (int o = 16; o > 0; o >>= 1) {
+    zlo = fminf(zlo, __shfl_xor_sync(0xffffffffu, zlo, o));
+    zhi = fmaxf(zhi, __shfl_xor_sync(0xffffffffu, zhi, o));
+  }
+  if (!actA && !actB) bd = make_float4(-3.0e38f, -3.0e38f, -3.0e38f, -3.0e38f);
+  const float4 *__restrict__ H4 = reinterpret_cast<const float4 *>(a.cl) + (size_t)g * 2 * N * 32 + lane;
+  asm volatile("mov.b64 %0, %0;" : "+l"(H4));
+  float llA = 0.f, llB = 0.f;
+
+  const int r_begin = chunk * (int)a.rays_per_block;
+  const int r_end = min((int)a.R, r_begin + (int)a.rays_per_block);
+  for (int rr = r_begin + warp; rr < r_end; rr += MT_THREADS / 32) {
+    const float2 rb0 = __ldg(reinterpret_cast<const float2 *>(a.ray_b + rr));
+    const float dz = rb0.x, s_exit = rb0.y;
+    const float s_lo = fminf(__fdividef(zlo, dz) * (1.f - 1e-6f), s_exit);
+    const float s_hi = fminf(__fdividef(zhi, dz) * (1.f + 1e-6f), s_exit);
+    float B0A = s_lo, B1A = s_lo, B0B = s_lo, B1B = s_lo;
+    int n0A = 0, n1A = 0, n0B = 0, n1B = 0, dA = 0, dB = 0;
+    int k0 = 0, kend = 0;
+    float s_in0 = 0.f;
+    if (s_lo < s_exit) {
+      kend = __ldg(a.trav_off + rr + 1);
+      k0 = band_entry_warp(a.trav, __ldg(a.trav_off + rr), kend, s_lo, s_in0);
+      float s = s_lo, za = s_lo * dz, ds = s_lo - s_in0;
+      for (int k = k0; k < kend; k++) {
+        const int2 w = __ldg(a.trav + k);
+        const float4 cg = shift_geo(__ldg(a.trav_geo + k), ds);
+        float2 km = __ldg(a.trav_km + k);
+        km.x = fmaf(2.f * km.y, ds, km.x);
+        const float s1 = __int_as_float(w.y);
+        const float zb = s1 * dz, Ls = s1 - s;
+        const unsigned off = cell_off32(w.x);
+        const float wb = __uint_as_float(off >> 5);
+#pragma unroll
+        for (int l = 0; l < 2; l++) {
+          const float zmin = l ? bd.z : bd.x, zmax = l ? bd.w : bd.y;
+          float &BA = l ? B1A : B0A, &BB = l ? B1B : B0B;
+          int &nA = l ? n1A : n0A, &nB = l ? n1B : n0B;
+          if (zb <= zmin) { BA += Ls; BB += Ls; continue; }   // below both chains' lowest node
+          if (za >= zmax) continue;                            // above both chains' highest node
+          const float4 *p = H4 + (size_t)l * N * 32 + off;
+          const float4 r0 = __ldg(p), r1 = __ldg(p + oy);
+          if (actA) c2_cell<0, false>(r0.x, r0.y, r1.x, r1.y, cg, km, za, zb, Ls, dz, wb, BA, nA, dA, rec + l * C2_RCAP * MT_THREADS, nullptr, 0, 0.f);
+          if (actB) c2_cell<0, false>(r0.z, r0.w, r1.z, r1.w, cg, km, za, zb, Ls, dz, wb, BB, nB, dB, rec + (2 + l) * C2_RCAP * MT_THREADS, nullptr, 0, 0.f);
+        }
+        if (s1 >= s_hi) break;
+        s = s1;
+        za = zb;
+        ds = 0.f;
+      }
+    }
+    if (dA) {
+      const int q = atomicAdd(a.ovf_n, 1);
+      if (q < a.ovf_cap) a.ovf_q[q] = make_float4(__int_as_float(cA), __int_as_float(rr), s_lo, s_hi);
+      else redo_mark(a, cA, rr);
+    }
+    if (dB) {
+      const int q = atomicAdd(a.ovf_n, 1);
+      if (q < a.ovf_cap) a.ovf_q[q] = make_float4(__int_as_float(cB), __int_as_float(rr), s_lo, s_hi);
+      else redo_mark(a, cB, rr);
+    }
+    if (MODE == TRACE_LL) {
+      const bool overA = !dA && (n0A > C2_RCAP || n1A > C2_RCAP), overB = !dB && (n0B > C2_RCAP || n1B > C2_RCAP);
+      float f0A = 0.f, f1A = 0.f, f0B = 0.f, f1B = 0.f;
+      macc *GA = a.G + (size_t)(2 * g) * 2 * N * 32 + lane, *GB = GA + (size_t)2 * N * 32;
+      const float2 rt = __ldg(reinterpret_cast<const float2 *>(a.ray_b + rr) + 1);
+#pragma unroll
+      for (int v = 0; v < 2; v++) {
+        if (v ? (dB || !actB) : (dA || !actA)) continue;
+        float dldO;
+        const float ll = epilogue(rt.x, rt.y, a.tc, v ? B0B : B0A, v ? B1B : B1A, dldO);
+        const float f0 = dldO * a.tc.k0 * (float)MT_GQ, f1 = dldO * a.tc.k1 * (float)MT_GQ;
+        if (v) { llB += ll; f0B = f0; f1B = f1; } else { llA += ll; f0A = f0; f1A = f1; }
+        macc *G = v ? GB : GA;
+        const int m0 = min(v ? n0B : n0A, C2_RCAP), m1 = min(v ? n1B : n1A, C2_RCAP);
+        for (int m = 0; m < m0 + m1; m++) {
+          const int l = m >= m0;
+          const float4 q = rec[((2 * v + l) * C2_RCAP + (l ? m - m0 : m)) * MT_THREADS];
+          const float wv = (l ? f1 : f0) * q.w, u = q.y, vv = q.z, wa = wv * (1.f - u), wbb = wv * u;
+          macc *pg = G + (l ? N * 32 : 0) + (__float_as_uint(q.x) << 5);
+          atomicAdd(pg, q_raw(wa * (1.f - vv)));
+          atomicAdd(pg + oy, q_raw(wbb * (1.f - vv)));
+          atomicAdd(pg + 32, q_raw(wa * vv));
+          atomicAdd(pg + oy + 32, q_raw(wbb * vv));
+        }
+      }
+      if (__any_sync(0xffffffffu, overA || overB)) {   // wide bands: re-walk, scatter crossings m >= RCAP
+        int m0A = 0, m1A = 0, m0B = 0, m1B = 0, dd = 0;
+        float Bd = 0.f, s = s_lo, za = s_lo * dz, ds = s_lo - s_in0;
+        for (int k = k0; k < kend; k++) {
+          const int2 w = __ldg(a.trav + k);
+          const float4 cg = shift_geo(__ldg(a.trav_geo + k), ds);
+          float2 km = __ldg(a.trav_km + k);
+          km.x = fmaf(2.f * km.y, ds, km.x);
+          const float s1 = __int_as_float(w.y);
+          const float zb = s1 * dz, Ls = s1 - s;
+          const unsigned off = cell_off32(w.x);
+#pragma unroll
+          for (int l = 0; l < 2; l++) {
+            const float zmin = l ? bd.z : bd.x, zmax = l ? bd.w : bd.y;
+            if (zb <= zmin || za >= zmax) continue;
+            const float4 *p = H4 + (size_t)l * N * 32 + off;
+            const float4 r0 = __ldg(p), r1 = __ldg(p + oy);
+            if (overA && (l ? n1A : n0A) > C2_RCAP)
+              c2_cell<0, true>(r0.x, r0.y, r1.x, r1.y, cg, km, za, zb, Ls, dz, 0.f, Bd, l ? m1A : m0A, dd, nullptr,
+                               GA + (l ? N * 32 : 0) + (off), oy, l ? f1A : f0A);
+            if (overB && (l ? n1B : n0B) > C2_RCAP)
+              c2_cell<0, true>(r0.z, r0.w, r1.z, r1.w, cg, km, za, zb, Ls, dz, 0.f, Bd, l ? m1B : m0B, dd, nullptr,
+                               GB + (l ? N * 32 : 0) + (off), oy, l ? f1B : f0B);
+          }
+          if (s1 >= s_hi) break;
+          s = s1;
+          za = zb;
+          ds = 0.f;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < 2; v++) {
+        if (v ? (dB || !actB) : (dA || !actA)) continue;
+        const float b0 = v ? B0B : B0A, b1 = v ? B1B : B1A;
+        const int64_t o = (int64_t)(v ? cB : cA) * a.R + __ldg(a.perm + rr);
+        a.Lout[3 * o + 0] = b0;
+        a.Lout[3 * o + 1] = b1 - b0;
+        a.Lout[3 * o + 2] = s_exit - b1;
+        a.Oout[o] = a.tc.k0 * b0 + a.tc.k1 * b1 + a.obase[rr];
+      }
+    }
+  }
+  if (MODE == TRACE_LL) {
+    if (actA) atomicAdd(a.ll + cA, q_ll(llA));
+    if (actB) atomicAdd(a.ll + cB, q_ll(llB));
+  }
 }
 
 // The chain x ray pairs the trace kernels deferred (an ill-conditioned cell,
@@ -776,7 +1441,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_trace_defer(TraceArgs a) {
   const unsigned gmask = DG == 32 ? 0xffffffffu : ((1u << DG) - 1u) << (threadIdx.x & 31 & ~(DG - 1));   // this group's lanes
   const int grp_g = (blockIdx.x * blockDim.x + threadIdx.x) / DG, ngrp = (gridDim.x * blockDim.x) / DG;
   int c_acc = -1;
-  double ll_acc = 0.0;
+  macc ll_acc = 0;   // fixed point per pair (R30): the sum does not depend on the queue order
   // one pair per group of DG lanes (all shuffles / ballots below are group-masked)
   auto process = [&](const int c, const int rr, const float s_lo, const float s_hi) {
     const Ray r = load_ray(a.ray_a, a.ray_b, rr);
@@ -849,13 +1514,13 @@ __global__ void __launch_bounds__(MT_THREADS) k_trace_defer(TraceArgs a) {
         if (c != c_acc) {
           if (c_acc >= 0) atomicAdd(a.ll + c_acc, ll_acc);
           c_acc = c;
-          ll_acc = 0.0;
+          ll_acc = 0;
         }
-        ll_acc += (double)ll;
+        ll_acc += q_ll(ll);
       }
-      const float f0 = dldO * a.tc.k0, f1 = dldO * a.tc.k1;
+      const float f0 = dldO * a.tc.k0 * (float)MT_GQ, f1 = dldO * a.tc.k1 * (float)MT_GQ;
       if (!anyovf) {
-        float *G0 = a.G + off;
+        macc *G0 = a.G + off;
         for (int m = 0; m < nr0; m++) {
           const float4 t = wrec[threadIdx.x][m];
           scatter4(G0, 32, __float_as_int(t.x), ny, f0 * t.w, t.y, t.z);
@@ -932,7 +1597,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_trace_defer(TraceArgs a) {
 template <int MODE, int NY>
 __global__ void __launch_bounds__(MT_THREADS, MT_RL_MINB) k_trace_rl(TraceArgs a, const float *__restrict__ Hc) {
   extern __shared__ __align__(16) float smem[];
-  __shared__ double red[MT_THREADS / 32];
+  __shared__ macc red[MT_THREADS / 32];
   const int ny = NY ? NY : a.tc.ny, N = a.tc.N;
   const int tid = threadIdx.x, c = blockIdx.y;
 #if MT_RL_GLOBAL_H
@@ -951,13 +1616,13 @@ __global__ void __launch_bounds__(MT_THREADS, MT_RL_MINB) k_trace_rl(TraceArgs a
   load_geometry(a, sgeo[0], sgeo[1], sgeo[2], sgeo[3]);
   const float4 bd = __ldg(a.band + c);
   const size_t coff = (size_t)(c >> 5) * 2 * N * 32 + (c & 31);
-  float *G0 = a.G + coff, *G1 = G0 + (size_t)N * 32;
+  macc *G0 = a.G + coff;
   __shared__ int next_ray;
   const int r_begin = blockIdx.x * (int)a.rays_per_block;
   const int r_end = min((int)a.R, r_begin + (int)a.rays_per_block);
   if (tid == 0) next_ray = r_begin;
   __syncthreads();
-  float llacc = 0.f;
+  macc llacc = 0;   // fixed point per pair (R30): independent of which warp took which rays
   const int lane = tid & 31;
   // warps take 32 consecutive (Morton-adjacent) rays at a time from the block's range:
   // thread-serial walks vary in length, and a static split left warps idle at the end
@@ -1085,27 +1750,12 @@ __global__ void __launch_bounds__(MT_THREADS, MT_RL_MINB) k_trace_rl(TraceArgs a
     if (MODE == TRACE_LL) {
       const float2 rt = __ldg(reinterpret_cast<const float2 *>(a.ray_b + rr) + 1);
       float dldO;
-      llacc += epilogue(rt.x, rt.y, a.tc, B0, B1, dldO);
-      const float f0 = dldO * a.tc.k0, f1 = dldO * a.tc.k1;
-      const int oy = ny * 32;
-      for (int m = 0; m < n0; m++) {
-        const float4 q = rec[m * MT_THREADS];
-        const float w = f0 * q.w, u = q.y, v = q.z;
-        float *pg = G0 + ((unsigned)__float_as_int(q.x) << 5);
-        atomicAdd(pg, w * (1.f - u) * (1.f - v));
-        atomicAdd(pg + oy, w * u * (1.f - v));
-        atomicAdd(pg + 32, w * (1.f - u) * v);
-        atomicAdd(pg + oy + 32, w * u * v);
-      }
-      for (int m = 0; m < n1; m++) {
-        const float4 q = rec[(RCAP + m) * MT_THREADS];
-        const float w = f1 * q.w, u = q.y, v = q.z;
-        float *pg = G1 + ((unsigned)__float_as_int(q.x) << 5);
-        atomicAdd(pg, w * (1.f - u) * (1.f - v));
-        atomicAdd(pg + oy, w * u * (1.f - v));
-        atomicAdd(pg + 32, w * (1.f - u) * v);
-        atomicAdd(pg + oy + 32, w * u * v);
-      }
+      llacc += q_ll(epilogue(rt.x, rt.y, a.tc, B0, B1, dldO));
+      const float f0 = dldO * a.tc.k0 * (float)MT_GQ, f1 = dldO * a.tc.k1 * (float)MT_GQ;
+      if (fmaxf(fabsf(f0), fabsf(f1)) * (1.f / GTHR) < MT_QSMALL)
+        scatter_recs<true>(rec, n0, n1, G0, N, ny * 32, f0, f1);
+      else
+        scatter_recs<false>(rec, n0, n1, G0, N, ny * 32, f0, f1);
     } else {
       const int64_t o = (int64_t)c * a.R + __ldg(a.perm + rr);
       a.Lout[3 * o + 0] = B0;
@@ -1115,12 +1765,12 @@ __global__ void __launch_bounds__(MT_THREADS, MT_RL_MINB) k_trace_rl(TraceArgs a
     }
   }
   if (MODE == TRACE_LL) {
-    double v = (double)llacc;
+    macc v = llacc;
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if ((tid & 31) == 0) red[tid >> 5] = v;
     __syncthreads();
     if (tid == 0) {
-      double t = 0;
+      macc t = 0;
       for (int w = 0; w < MT_THREADS / 32; w++) t += red[w];
       atomicAdd(a.ll + c, t);
     }
@@ -1135,7 +1785,7 @@ static TraceArgs base_trace_args(mt_problem *p) {
   a.tc = p->tc;
   a.X = p->d_X; a.Y = p->d_Y;
   a.ray_a = p->d_ray_a; a.ray_b = p->d_ray_b; a.obase = p->d_obase;
-  a.trav_off = p->d_trav_off; a.trav = p->d_trav; a.trav_geo = p->d_trav_geo;
+  a.trav_off = p->d_trav_off; a.trav = p->d_trav; a.trav_geo = p->d_trav_geo; a.trav_km = p->d_trav_km;
   a.rl_head = p->d_rl_head; a.rl_code = p->d_rl_code; a.rl_ovf = p->d_rl_ovf;
   a.perm = p->d_perm;
   a.R = p->R;
@@ -1152,7 +1802,7 @@ cudaError_t build_traversal(mt_problem *p) {
   cudaError_t e = cudaMalloc(&d_cnt, sizeof(int32_t) * p->R);
   if (e != cudaSuccess) return e;
   unsigned nb = (unsigned)((p->R + 127) / 128);
-  k_build_trav<<<nb, 128>>>(a, nullptr, d_cnt, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+  k_build_trav<<<nb, 128>>>(a, nullptr, d_cnt, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
   std::vector<int32_t> cnt(p->R);
   e = cudaMemcpy(cnt.data(), d_cnt, sizeof(int32_t) * p->R, cudaMemcpyDeviceToHost);
   cudaFree(d_cnt);
@@ -1164,14 +1814,29 @@ cudaError_t build_traversal(mt_problem *p) {
     if (tot >= (int64_t)1 << 31) return cudaErrorInvalidValue;   // > 2^31 stored cells
     off[q + 1] = (int32_t)tot;
     ovf[q + 1] = ovf[q] + (cnt[q] > 64 ? (cnt[q] - 64 + 15) / 16 : 0);   // step-code words past 64 cells
+    if (cnt[q] > 255) return cudaErrorInvalidValue;   // band-entry table entries are bytes
   }
   p->trav_cells = tot;
   e = cudaMalloc(&p->d_trav_off, sizeof(int32_t) * (p->R + 1));
-  if (e == cudaSuccess) e = cudaMalloc(&p->d_trav, sizeof(int2) * (p->trav_cells > 0 ? p->trav_cells : 1));
-  if (e == cudaSuccess) e = cudaMalloc(&p->d_trav_geo, sizeof(float4) * (p->trav_cells > 0 ? p->trav_cells : 1));
+  const size_t ncells = p->trav_cells > 0 ? p->trav_cells : 1;
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_trav, sizeof(int2) * ncells);
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_trav_geo, sizeof(float4) * ncells);
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_trav_km, sizeof(float2) * ncells);
   if (e == cudaSuccess) e = cudaMalloc(&p->d_rl_head, sizeof(int2) * p->R);
   if (e == cudaSuccess) e = cudaMalloc(&p->d_rl_code, sizeof(uint4) * p->R);
   if (e == cudaSuccess) e = cudaMalloc(&p->d_rl_ovf, sizeof(uint32_t) * (ovf[p->R] > 0 ? ovf[p->R] : 1));
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_tab, (size_t)MT_TABQ * p->R);
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_ray_c, sizeof(float4) * p->R);
+  if (e == cudaSuccess) {   // chain-lanes ray record {d_z, 1/d_z, s_exit, first stored cell}
+    std::vector<float4> rc(p->R);
+    for (int64_t q = 0; q < p->R; q++) {
+      const float4 b = p->h_rb[q];
+      float kb;
+      memcpy(&kb, &off[q], sizeof(float));   // first stored cell, as int bits
+      rc[q] = make_float4(b.x, (float)(1.0 / (double)b.x), b.y, kb);
+    }
+    e = cudaMemcpy(p->d_ray_c, rc.data(), sizeof(float4) * p->R, cudaMemcpyHostToDevice);
+  }
   int32_t *d_ovfoff = nullptr;
   if (e == cudaSuccess) e = cudaMalloc(&d_ovfoff, sizeof(int32_t) * (p->R + 1));
   if (e == cudaSuccess) e = cudaMemcpy(d_ovfoff, ovf.data(), sizeof(int32_t) * (p->R + 1), cudaMemcpyHostToDevice);
@@ -1182,9 +1847,10 @@ cudaError_t build_traversal(mt_problem *p) {
   a.trav_off = p->d_trav_off;
   a.trav = p->d_trav;
   a.trav_geo = p->d_trav_geo;
+  a.trav_km = p->d_trav_km;
   if (e == cudaSuccess)
-    k_build_trav<<<nb, 128>>>(a, p->d_trav_off, nullptr, p->d_trav, p->d_trav_geo, p->d_rl_head,
-                              p->d_rl_code, p->d_rl_ovf, d_ovfoff);
+    k_build_trav<<<nb, 128>>>(a, p->d_trav_off, nullptr, p->d_trav, p->d_trav_geo, p->d_trav_km, p->d_rl_head,
+                              p->d_rl_code, p->d_rl_ovf, d_ovfoff, p->d_tab);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   cudaFree(d_ovfoff);
@@ -1204,23 +1870,39 @@ static cudaError_t set_smem(Kern k, size_t smem, size_t *done) {
 }
 
 template <int MODE, int NY>
-static cudaError_t launch_cl(const TraceArgs &a, dim3 grid, size_t smem, cudaStream_t s) {
-  static size_t done[16] = {0};
-  cudaError_t e = set_smem(k_trace_cl<MODE, NY>, smem, done);
-  if (e != cudaSuccess) return e;
-  k_trace_cl<MODE, NY><<<grid, MT_THREADS, smem, s>>>(a);
+static cudaError_t launch_v0(const TraceArgs &a, dim3 grid, cudaStream_t s) {
+  k_trace_v0<MODE, NY><<<grid, MT_THREADS, (size_t)16 * 2 * RCAP * MT_THREADS, s>>>(a);
   return cudaGetLastError();
 }
 
 template <int MODE>
-static cudaError_t launch_cl_ny(const TraceArgs &a, int ny, dim3 grid, size_t smem, cudaStream_t s) {
+static cudaError_t launch_v0_ny(const TraceArgs &a, int ny, dim3 grid, cudaStream_t s) {
   switch (ny) {
-    case 8: return launch_cl<MODE, 8>(a, grid, smem, s);
-    case 16: return launch_cl<MODE, 16>(a, grid, smem, s);
-    case 32: return launch_cl<MODE, 32>(a, grid, smem, s);
-    case 64: return launch_cl<MODE, 64>(a, grid, smem, s);
-    default: return launch_cl<MODE, 0>(a, grid, smem, s);
+    case 8: return launch_v0<MODE, 8>(a, grid, s);
+    case 16: return launch_v0<MODE, 16>(a, grid, s);
+    case 32: return launch_v0<MODE, 32>(a, grid, s);
+    case 64: return launch_v0<MODE, 64>(a, grid, s);
+    default: return launch_v0<MODE, 0>(a, grid, s);
   }
+}
+
+template <int MODE>
+static cudaError_t launch_c2(const TraceArgs &a, dim3 grid, cudaStream_t s) {
+  static size_t done[16] = {0};
+  const size_t smem = (size_t)16 * 4 * C2_RCAP * MT_THREADS;
+  cudaError_t e = set_smem(k_trace_c2<MODE>, smem, done);
+  if (e != cudaSuccess) return e;
+  k_trace_c2<MODE><<<grid, MT_THREADS, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int MODE>
+static cudaError_t launch_cl(const TraceArgs &a, dim3 grid, size_t smem, cudaStream_t s) {
+  static size_t done[16] = {0};
+  cudaError_t e = set_smem(k_trace_cl<MODE>, smem, done);
+  if (e != cudaSuccess) return e;
+  k_trace_cl<MODE><<<grid, MT_THREADS, smem, s>>>(a);
+  return cudaGetLastError();
 }
 
 template <int MODE, int NY>
@@ -1252,16 +1934,8 @@ static int64_t pick_splits(const mt_problem *p, int64_t groups, int64_t blocks_p
   return S < 1 ? 1 : (S > max_s ? max_s : S);
 }
 
-// Paired heights for the chain-lanes trace (MT_H2): H2[t] = (H[t], H[t + 32]),
-// i.e. node (i, j) with its neighbour (i, j + 1) in the same 8 bytes.
-__global__ void k_pair_heights(const float *__restrict__ H, float2 *__restrict__ H2, int64_t n) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  H2[t] = make_float2(H[t], t + 32 < n ? H[t + 32] : 0.f);
-}
-
 cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const float4 *band,
-                         float *G, double *ll, float *L, float *O, cudaStream_t s) {
+                         macc *G, macc *ll, float *L, float *O, cudaStream_t s) {
   if (C <= 0 || p->R <= 0) return cudaSuccess;
   if (mode == TRACE_LL && p->vx.nz > 0) return launch_voxel(p, C, H, band, G, ll, s);   // f3 model active
   TraceArgs a = base_trace_args(p);
@@ -1273,24 +1947,38 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
   if (rec) cudaEventRecord(p->ev_a[p->n_rec], s);
   if (chain_lanes) {
     int groups = (C + 31) / 32;
-    if (MT_H2) {
-      const int64_t n = (int64_t)groups * 2 * p->N * 32;
-      k_pair_heights<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(H, p->d_H2, n);
-      a.H2 = p->d_H2;
+    const bool c2 = p->cl_v == 2 || (p->cl_v < 0 && C >= 64);
+    if (c2) {   // two chains per lane: paired heights of both chains
+      const int64_t n = (int64_t)((C + 63) / 64) * 2 * p->N * 32;
+      k_cell_prep2<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(H, reinterpret_cast<float4 *>(p->d_cl), C, p->ny,
+                                                             p->N, n);
+      p->all_launches++;
+    } else {   // per-(chain, cell) bounds and bilinear coefficients
+      const int64_t n = (int64_t)groups * p->N * 32;
+      k_cell_prep<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(H, p->d_cl, C, p->nx, p->ny, p->N, n);
       p->all_launches++;
     }
-    // small ray chunks (~512 rays = 64 per warp): compact, L1-friendly regions per
-    // block and many waves for load balance; 256 when there are few chain groups
-    // (measured: 1,024 chains 5.16 vs 5.21 ms; 8,192 chains prefer 512)
-    const int64_t chunk = p->chunk > 0 ? p->chunk : (groups >= 64 ? 512 : 256);
-    int64_t S = p->trace_s > 0 ? p->trace_s
-                               : std::max(pick_splits(p, groups, 2), (p->R + chunk - 1) / chunk);
-    a.rays_per_block = (p->R + S - 1) / S;
-    S = (p->R + a.rays_per_block - 1) / a.rays_per_block;
+    a.cl = p->d_cl;
+    a.ray_c = p->d_ray_c;
+    a.tab = p->d_tab;
+    a.tab_scale = (float)MT_TABQ / p->z_top;
+    // ray chunks of <= 512 Morton-ordered rays per block (compact, L1-friendly regions, many
+    // waves for load balance).  The shape depends on R only, never on C, so a chain's
+    // result is bit-identical whatever the chain count per GPU (R30, chain sharding).
+    const int64_t chunk = p->chunk > 0 ? p->chunk
+                                       : std::max<int64_t>(32, std::min<int64_t>(512, p->R / (2 * (int64_t)p->num_sms)));
+    a.rays_per_block = chunk;
+    int64_t S = (p->R + chunk - 1) / chunk;
     dim3 grid((unsigned)S, (unsigned)groups);
-    size_t smem = (size_t)16 * 2 * RCAP * MT_THREADS;   // crossing records (geometry is static)
-    e = mode == TRACE_LL ? launch_cl_ny<TRACE_LL>(a, p->ny, grid, smem, s)
-                         : launch_cl_ny<TRACE_PATH>(a, p->ny, grid, smem, s);
+    if (c2) {
+      dim3 grid2((unsigned)S, (unsigned)((C + 63) / 64));
+      if (grid2.x % C2_TILE) grid2.x += C2_TILE - grid2.x % C2_TILE;   // whole tiles (extra chunks are empty)
+      e = mode == TRACE_LL ? launch_c2<TRACE_LL>(a, grid2, s) : launch_c2<TRACE_PATH>(a, grid2, s);
+    } else if (p->cl_v <= 0)
+      e = mode == TRACE_LL ? launch_v0_ny<TRACE_LL>(a, p->ny, grid, s) : launch_v0_ny<TRACE_PATH>(a, p->ny, grid, s);
+    else
+      e = mode == TRACE_LL ? launch_cl<TRACE_LL>(a, grid, (size_t)16 * 2 * RCAP * MT_THREADS, s)
+                           : launch_cl<TRACE_PATH>(a, grid, (size_t)16 * 2 * RCAP * MT_THREADS, s);
     if (rec) cudaEventRecord(p->ev_m[p->n_rec], s);
     if (e == cudaSuccess) {   // deferred pairs (ill-conditioned or > RCAP crossings)
       if (mode == TRACE_LL) k_trace_defer<TRACE_LL, DEFER_DG><<<2 * p->num_sms, MT_THREADS, 0, s>>>(a);

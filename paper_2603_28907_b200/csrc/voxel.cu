@@ -69,8 +69,8 @@ struct VoxArgs {
   int rpw;                 // rays per warp in V2
   int g0;                  // first chain group of this launch (blockIdx.y + g0)
   unsigned long long *gathered;   // optional: += ΔR bytes gathered by V2 (valid chains × 4 B per kept entry)
-  float *G;                // ∂ℓ/∂H out (tix layout)
-  double *ll;              // [C] += Σ_p ℓ_p
+  macc *G;                 // ∂ℓ/∂H out (tix layout)
+  macc *ll;                // [C] += Σ_p ℓ_p
 };
 
 __device__ __forceinline__ float warp_allsum(float v) {
@@ -247,7 +247,7 @@ __device__ __forceinline__ void row_range(const VoxArgs &a, int64_t p, int k_lo,
 
 // Block-sum the per-lane log-likelihood partials and add them to ll[c].
 template <int VEC>
-__device__ __forceinline__ void flush_ll(const double (&mine)[VEC], int lane, int g, int C, double *ll) {
+__device__ __forceinline__ void flush_ll(const double (&mine)[VEC], int lane, int g, int C, macc *ll) {
   __shared__ double sh[VX_WARPS][VEC][32];
 #pragma unroll
   for (int u = 0; u < VEC; u++) sh[threadIdx.x >> 5][u][lane] = mine[u];
@@ -258,7 +258,7 @@ __device__ __forceinline__ void flush_ll(const double (&mine)[VEC], int lane, in
 #pragma unroll
     for (int w = 0; w < VX_WARPS; w++) s += sh[w][u][l];
     const int c = chain_of(g, VEC, u, l);
-    if (c < C) atomicAdd(ll + c, s);
+    if (c < C) atomicAdd(ll + c, q_lld(s));
   }
 }
 
@@ -347,8 +347,8 @@ __global__ void __launch_bounds__(MT_THREADS, VX_MINB) k_vx_bwd_cl(VoxArgs a) {
   for (int u = 0; u < VEC; u++) {
     const int c = chain_of(g, VEC, u, lane);
     if (c < a.C) {   // G is zero on entry (K3 clears what it reads)
-      atomicAdd(a.G + tix(c, 0, it.node, a.N), g0[u]);
-      atomicAdd(a.G + tix(c, 1, it.node, a.N), g1[u]);
+      atomicAdd(a.G + tix(c, 0, it.node, a.N), q_g(g0[u]));
+      atomicAdd(a.G + tix(c, 1, it.node, a.N), q_g(g1[u]));
     }
   }
 }
@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_vx_fwd_rl(VoxArgs a) {
     if (lane == 0 && tot > 0.f) atomicAdd(a.gathered, (unsigned long long)tot * 4ull);
   }
   __syncthreads();
-  if (threadIdx.x < a.C) atomicAdd(a.ll + threadIdx.x, sll[threadIdx.x]);
+  if (threadIdx.x < a.C) atomicAdd(a.ll + threadIdx.x, q_lld(sll[threadIdx.x]));
 }
 
 __global__ void __launch_bounds__(MT_THREADS) k_vx_bwd_rl(VoxArgs a) {
@@ -464,8 +464,8 @@ __global__ void __launch_bounds__(MT_THREADS) k_vx_bwd_rl(VoxArgs a) {
     g0 = warp_allsum(g0);
     g1 = warp_allsum(g1);
     if (lane == 0) {
-      atomicAdd(a.G + tix(c, 0, it.node, a.N), g0);
-      atomicAdd(a.G + tix(c, 1, it.node, a.N), g1);
+      atomicAdd(a.G + tix(c, 0, it.node, a.N), q_g(g0));
+      atomicAdd(a.G + tix(c, 1, it.node, a.N), q_g(g1));
     }
   }
 }
@@ -685,7 +685,7 @@ cudaError_t voxel_setup(mt_problem *p, int nz, float gamma, float tau, const flo
   return e;
 }
 
-cudaError_t launch_voxel(mt_problem *p, int C, const float *H, const float4 *band, float *G, double *ll,
+cudaError_t launch_voxel(mt_problem *p, int C, const float *H, const float4 *band, macc *G, macc *ll,
                          cudaStream_t s) {
   const VoxelState &v = p->vx;
   VoxArgs a;
