@@ -1209,7 +1209,7 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_v0(TraceArgs a
 // groups, so a chunk's traversal records are reused from L2 by every group.
 // ---------------------------------------------------------------------------
 #ifndef C2_TILE
-#define C2_TILE 8
+#define C2_TILE 1
 #endif
 #ifndef C2_RCAP
 #define C2_RCAP 2
@@ -1270,13 +1270,16 @@ __device__ __forceinline__ void c2_cell(float h00, float h01, float h10, float h
 template <int MODE>
 __global__ void __launch_bounds__(MT_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
   extern __shared__ __align__(16) float4 recs[];   // [chain v][surface l][C2_RCAP][MT_THREADS]
-  const int N = a.tc.N, oy = a.tc.ny * 32;
+  int N = a.tc.N, oy = a.tc.ny * 32;
+  asm volatile("" : "+r"(N), "+r"(oy));   // keep in registers (no per-use reload / recompute)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int lin = blockIdx.y * gridDim.x + blockIdx.x, G2 = gridDim.y;
   const int tile = lin / (G2 * C2_TILE), within = lin - tile * (G2 * C2_TILE);
   const int g = within / C2_TILE, chunk = tile * C2_TILE + (within - (within / C2_TILE) * C2_TILE);
   const int cA = g * 64 + lane, cB = cA + 32;
-  const bool actA = cA < a.C, actB = cB < a.C;
+  int acts = (cA < a.C ? 1 : 0) | (cB < a.C ? 2 : 0);
+  asm volatile("" : "+r"(acts));
+  const bool actA = acts & 1, actB = acts & 2;
   float4 *rec = recs + threadIdx.x;
   asm volatile("mov.b64 %0, %0;" : "+l"(rec));
   // lane-union band of its two chains per surface; the warp walks the union over 64 chains
@@ -1305,11 +1308,10 @@ __global__ void __launch_bounds__(MT_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
     const float s_hi = fminf(__fdividef(zhi, dz) * (1.f + 1e-6f), s_exit);
     float B0A = s_lo, B1A = s_lo, B0B = s_lo, B1B = s_lo;
     int n0A = 0, n1A = 0, n0B = 0, n1B = 0, dA = 0, dB = 0;
-    int k0 = 0, kend = 0;
-    float s_in0 = 0.f;
     if (s_lo < s_exit) {
-      kend = __ldg(a.trav_off + rr + 1);
-      k0 = band_entry_warp(a.trav, __ldg(a.trav_off + rr), kend, s_lo, s_in0);
+      const int kend = __ldg(a.trav_off + rr + 1);
+      float s_in0;
+      const int k0 = band_entry_warp(a.trav, __ldg(a.trav_off + rr), kend, s_lo, s_in0);
       float s = s_lo, za = s_lo * dz, ds = s_lo - s_in0;
       for (int k = k0; k < kend; k++) {
         const int2 w = __ldg(a.trav + k);
@@ -1375,6 +1377,9 @@ __global__ void __launch_bounds__(MT_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
       }
       if (__any_sync(0xffffffffu, overA || overB)) {   // wide bands: re-walk, scatter crossings m >= RCAP
         int m0A = 0, m1A = 0, m0B = 0, m1B = 0, dd = 0;
+        const int kend = __ldg(a.trav_off + rr + 1);
+        float s_in0;
+        const int k0 = band_entry_warp(a.trav, __ldg(a.trav_off + rr), kend, s_lo, s_in0);
         float Bd = 0.f, s = s_lo, za = s_lo * dz, ds = s_lo - s_in0;
         for (int k = k0; k < kend; k++) {
           const int2 w = __ldg(a.trav + k);
