@@ -310,9 +310,9 @@ def main():
 
     # dominant kernel (K2 trace): algorithmic FP32 flops per launch / measured launch duration
     # (prior-draw states: the oracle's counts on prior draws, tools/count_work.py --prior)
-    wall = json.load(open(os.path.join(ROOT, "data", "work_counts.json")))
-    wkey = dname + "_prior" if args.states == "prior" and dname + "_prior" in wall else dname
-    work = wall[wkey]
+    wc = json.load(open(os.path.join(ROOT, "data", "work_counts.json")))
+    wkey = dname + "_prior" if args.states == "prior" and dname + "_prior" in wc else dname
+    work = wc[wkey]
     F = work["flops_per_pair"]
     avg_trace_ms = tm["trace_ms"] / max(tm["trace_launches"], 1)       # K2 main + fp64 follow-up
     avg_defer_ms = cnt["defer_ms"] / max(tm["trace_launches"], 1)

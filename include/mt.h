@@ -325,6 +325,14 @@ int mt_path_lengths(mt_problem *p, int32_t C, const float *H, float *L, float *O
 int mt_debug_traversal(mt_problem *p, int64_t ray, int32_t *ij, float *s_in, float *s_out,
                        int32_t cap, int32_t *n);
 
+/* Every ray's stored traversal (a2: the cells the trace kernels read, built
+ * once per problem by the exact device DDA, P:234-235 / R16), in the caller's
+ * ray order of this shard, as CSR with HOST outputs: with ij == NULL only
+ * off [R+1] is written (off[q+1] - off[q] = cells of ray q); then ij
+ * [off[R]][2] receives (i, j) and s_out [off[R]] each cell's exit parameter
+ * (fp32, m).  Synchronous.  MT_EINVAL for a NULL problem or off. */
+int mt_traversal_all(mt_problem *p, int64_t *off, int32_t *ij, float *s_out);
+
 /* Raw Philox4x32-10 words (device in ctr [n][4], out [n][4]; key host). */
 int mt_philox(const uint32_t *ctr, uint32_t key0, uint32_t key1, uint32_t *out, int64_t n,
               mt_stream stream);

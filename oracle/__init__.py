@@ -59,6 +59,7 @@ def lib():
         L.or_ray_extent.argtypes = [ct.c_void_p, ct.c_long, ct.POINTER(ct.c_double), ct.POINTER(ct.c_double)]
         L.or_traversal.restype = ct.c_int
         L.or_traversal.argtypes = [ct.c_void_p, ct.c_long, _ip, _dp, _dp, ct.c_int]
+        L.or_traversal_all.argtypes = [ct.c_void_p, ct.POINTER(ct.c_long), ct.c_void_p, ct.c_void_p]
         L.or_path_lengths.argtypes = [ct.c_void_p, ct.c_int, _dp, _dp, _dp, ct.c_void_p]
         L.or_loglik_grad_H.argtypes = [ct.c_void_p, ct.c_int, _dp, _dp, _dp, _dp, ct.c_void_p, _lp]
         L.or_logpost_grad.argtypes = [ct.c_void_p, ct.c_int, _dp, _dp, _dp, _dp, _dp, _dp,
@@ -204,6 +205,15 @@ class Problem:
         n = lib().or_traversal(self.h, q, ij, si, so, cap)
         assert n <= cap
         return ij[:2 * n].reshape(n, 2), si[:n], so[:n]
+
+    def traversal_all(self):
+        """Every ray's traversal: off [R+1] (int64 CSR), ij [off[R]][2] int32, s_out [off[R]]."""
+        off = np.zeros(self.R + 1, np.int64)
+        lib().or_traversal_all(self.h, off.ctypes.data_as(ct.POINTER(ct.c_long)), None, None)
+        ij = np.zeros((int(off[-1]), 2), np.int32)
+        so = np.zeros(int(off[-1]))
+        lib().or_traversal_all(self.h, off.ctypes.data_as(ct.POINTER(ct.c_long)), ij.ctypes.data, so.ctypes.data)
+        return off, ij, so
 
     def path_lengths(self, H: np.ndarray, with_min_g1: bool = False):
         """H [C][2][nx][ny] -> L [C][R][3] (muck, air, rock), O [C][R] (, min|g'| [C][R])."""

@@ -371,6 +371,34 @@ int or_traversal(const or_problem *p, long q, int *ij, double *s_in, double *s_o
   return or_traverse(p, q, ij, s_in, s_out, cap);
 }
 
+/* Every ray's traversal in one call (the same or_traverse per ray), CSR by ray:
+ * with ij == NULL only off[R+1] is filled (cell counts, prefix-summed); then
+ * ij[2 off[R]] and s_out[off[R]] receive the cells in ray order. */
+void or_traversal_all(const or_problem *p, long *off, int *ij, double *s_out) {
+  const int cap = 2 * (p->nx + p->ny) + 8;
+  if (!ij) {
+    off[0] = 0;
+#pragma omp parallel
+    {
+      int *tij = (int *)malloc(sizeof(int) * 2 * cap);
+      double *ts = (double *)malloc(sizeof(double) * 2 * cap);
+#pragma omp for schedule(static)
+      for (long q = 0; q < p->nray; q++) off[q + 1] = or_traverse(p, q, tij, ts, ts + cap, cap);
+      free(tij);
+      free(ts);
+    }
+    for (long q = 0; q < p->nray; q++) off[q + 1] += off[q];
+    return;
+  }
+#pragma omp parallel
+  {
+    double *ts = (double *)malloc(sizeof(double) * cap);
+#pragma omp for schedule(static)
+    for (long q = 0; q < p->nray; q++) or_traverse(p, q, ij + 2 * off[q], ts, s_out + off[q], cap);
+    free(ts);
+  }
+}
+
 /* Per (chain, ray): L[3] = (muck, air, rock) in-box lengths, O, s_exit.
  * H: [C][2][nx][ny] double. */
 void or_path_lengths(const or_problem *p, int C, const double *H, double *L, double *O,

@@ -42,7 +42,7 @@ class _Desc(ct.Structure):
 EXPORTS = [
     "mt_problem_create", "mt_problem_destroy", "mt_num_params", "mt_num_rays", "mt_loglik_offset",
     "mt_prior_constants", "mt_logpost_grad", "mt_leapfrog", "mt_draw_momenta", "mt_hmc_step",
-    "mt_stats_update", "mt_rhat_partials", "mt_heights", "mt_loglik_heights", "mt_path_lengths", "mt_debug_traversal", "mt_philox",
+    "mt_stats_update", "mt_rhat_partials", "mt_heights", "mt_loglik_heights", "mt_path_lengths", "mt_debug_traversal", "mt_traversal_all", "mt_philox",
     "mt_philox_curand", "mt_timing_start", "mt_timing_read", "mt_trace_counters", "mt_measure_fp32_peak",
     "mt_last_error", "mt_comm_unique_id", "mt_attach_comm", "mt_detach_comm", "mt_nuts_step",
     "mt_nested_rhat_partials", "mt_summary_update", "mt_voxel_model", "mt_voxel_info",
@@ -78,6 +78,7 @@ def lib():
             "mt_loglik_heights": ([vp, i32, vp, vp, vp, vp], ct.c_int),
             "mt_path_lengths": ([vp, i32, vp, vp, vp, vp], ct.c_int),
             "mt_debug_traversal": ([vp, i64, vp, vp, vp, i32, vp], ct.c_int),
+            "mt_traversal_all": ([vp, vp, vp, vp], ct.c_int),
             "mt_philox": ([vp, u32, u32, vp, i64, vp], ct.c_int),
             "mt_philox_curand": ([vp, u32, u32, vp, i64, vp], ct.c_int),
             "mt_timing_start": ([vp, i32], ct.c_int),
@@ -346,6 +347,16 @@ class Problem:
         _check(lib().mt_path_lengths(self.h, C, _ptr(H), _ptr(L), _ptr(O), _stream(stream)),
                "mt_path_lengths")
         return L, O
+
+    def traversal_all(self):
+        """Every ray's stored traversal in the caller's ray order: off [R+1] int64 (CSR),
+        ij [off[R]][2] int32, s_out [off[R]] fp32 (mt_traversal_all; host, synchronous)."""
+        off = np.zeros(self.R + 1, np.int64)
+        _check(lib().mt_traversal_all(self.h, off.ctypes.data, None, None), "mt_traversal_all")
+        ij = np.zeros((int(off[-1]), 2), np.int32)
+        so = np.zeros(int(off[-1]), np.float32)
+        _check(lib().mt_traversal_all(self.h, off.ctypes.data, ij.ctypes.data, so.ctypes.data), "mt_traversal_all")
+        return off, ij, so
 
     def debug_traversal(self, ray: int, cap: Optional[int] = None):
         cap = cap or 2 * (self.nx + self.ny) + 8

@@ -605,6 +605,33 @@ int mt_path_lengths(mt_problem *p, int32_t C, const float *H, float *L, float *O
   return MT_OK;
 }
 
+int mt_traversal_all(mt_problem *p, int64_t *off, int32_t *ij, float *s_out) {
+  if (!p || !off) return set_err(MT_EINVAL, "NULL problem or off");
+  if (ij && !s_out) return set_err(MT_EINVAL, "s_out is NULL");
+  DevGuard g(p->device);
+  CK(cudaDeviceSynchronize());
+  std::vector<int32_t> io(p->R + 1);
+  if (p->R > 0) CK(cudaMemcpy(io.data(), p->d_trav_off, sizeof(int32_t) * (p->R + 1), cudaMemcpyDeviceToHost));
+  off[0] = 0;
+  for (int64_t q = 0; q < p->R; q++) {   // caller ray q = internal ray inv_perm[q]
+    const int64_t k = p->inv_perm[q];
+    off[q + 1] = off[q] + (io[k + 1] - io[k]);
+  }
+  if (!ij || p->R == 0) return MT_OK;
+  std::vector<int2> cells(p->trav_cells > 0 ? p->trav_cells : 1);
+  if (p->trav_cells > 0) CK(cudaMemcpy(cells.data(), p->d_trav, sizeof(int2) * p->trav_cells, cudaMemcpyDeviceToHost));
+  for (int64_t q = 0; q < p->R; q++) {
+    const int64_t k = p->inv_perm[q];
+    int64_t o = off[q];
+    for (int32_t m = io[k]; m < io[k + 1]; m++, o++) {
+      ij[2 * o] = cell_i(cells[m].x);
+      ij[2 * o + 1] = cell_j(cells[m].x);
+      memcpy(&s_out[o], &cells[m].y, sizeof(float));
+    }
+  }
+  return MT_OK;
+}
+
 int mt_debug_traversal(mt_problem *p, int64_t ray, int32_t *ij, float *s_in, float *s_out,
                        int32_t cap, int32_t *n) {
   if (!p) return set_err(MT_EINVAL, "problem is NULL");
@@ -712,6 +739,9 @@ int mt_set_inverse_mass(mt_problem *p, const float *minv, int32_t n) {
     return MT_OK;
   }
   if (n != p->P) return set_err(MT_EINVAL, "n = %d != P = %d", n, p->P);
+  // synchronous on the whole device (mt.h): the producer of minv may run on any stream, and
+  // kernels already queued may still read the old d_minv
+  CK(cudaDeviceSynchronize());
   std::vector<float> h(p->P);
   CK(cudaMemcpy(h.data(), minv, sizeof(float) * p->P, cudaMemcpyDeviceToHost));
   for (int k = 0; k < p->P; k++)

@@ -688,27 +688,24 @@ cudaError_t launch_finish(mt_problem *p, int mode, int C, float *x, float *grad,
     return cudaGetLastError();
   }
   size_t smem = (size_t)p->P * sizeof(float);
-  static bool attr[3] = {false, false, false};
-  if (smem > 48 * 1024 && !attr[mode]) {
-    if (mode == FIN_PLAIN)
-      cudaFuncSetAttribute(k_finish<FIN_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    if (mode == FIN_STEP)
-      cudaFuncSetAttribute(k_finish<FIN_STEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    if (mode == FIN_LAST)
-      cudaFuncSetAttribute(k_finish<FIN_LAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    attr[mode] = true;
+  if (mode < 0 || mode > 2) return cudaErrorInvalidValue;
+  // shared-memory opt-in, once per (device, mode); a failure is returned (and not recorded)
+  static bool attr[64][3] = {}, attr_r[64][3] = {};
+  const int dv = p->device & 63;
+  if (smem > 48 * 1024 && !(p->sample_r ? attr_r : attr)[dv][mode]) {
+    cudaError_t e;
+    if (p->sample_r)
+      e = cudaFuncSetAttribute(mode == FIN_PLAIN ? (const void *)k_finish_r<FIN_PLAIN>
+                               : mode == FIN_STEP ? (const void *)k_finish_r<FIN_STEP> : (const void *)k_finish_r<FIN_LAST>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    else
+      e = cudaFuncSetAttribute(mode == FIN_PLAIN ? (const void *)k_finish<FIN_PLAIN>
+                               : mode == FIN_STEP ? (const void *)k_finish<FIN_STEP> : (const void *)k_finish<FIN_LAST>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    if (e != cudaSuccess) return e;
+    (p->sample_r ? attr_r : attr)[dv][mode] = true;
   }
   if (p->sample_r) {
-    static bool attr_r[3] = {false, false, false};
-    if (smem > 48 * 1024 && !attr_r[mode]) {
-      if (mode == FIN_PLAIN)
-        cudaFuncSetAttribute(k_finish_r<FIN_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-      if (mode == FIN_STEP)
-        cudaFuncSetAttribute(k_finish_r<FIN_STEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-      if (mode == FIN_LAST)
-        cudaFuncSetAttribute(k_finish_r<FIN_LAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-      attr_r[mode] = true;
-    }
     if (mode == FIN_PLAIN) k_finish_r<FIN_PLAIN><<<C, MT_THREADS, smem, s>>>(a);
     else if (mode == FIN_STEP) k_finish_r<FIN_STEP><<<C, MT_THREADS, smem, s>>>(a);
     else k_finish_r<FIN_LAST><<<C, MT_THREADS, smem, s>>>(a);

@@ -412,15 +412,19 @@ __global__ void __launch_bounds__(MT_THREADS) k_ncp_kick(FinishArgs a) {
 
 // dynamic shared memory of the non-centred kernels: 4N doubles of DFT work + twiddles
 // (K3 adds 2N for ∂ll/∂x): up to 200 KiB at N = 4096, so opt in once
+// The shared-memory opt-in is per device: set it once per device of the problem.  A
+// failure is not recorded as done, so the launch that needs it fails and the caller's
+// cudaGetLastError reports it.
 static size_t ncp_smem(const mt_problem *p) {
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[64] = {false};
+  const int d = p->device & 63;
+  if (!attr[d]) {
     const int mx = (6 * MT_MAX_NODES + 4 * MT_MAX_AXIS) * (int)sizeof(double);
-    cudaFuncSetAttribute(k_ncp_heights, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_ncp_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_ncp_heights_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_ncp_finish_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    attr = true;
+    cudaError_t e = cudaFuncSetAttribute(k_ncp_heights, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_ncp_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_ncp_heights_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_ncp_finish_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    attr[d] = e == cudaSuccess;
   }
   return (size_t)(4 * p->N + 4 * MT_MAX_AXIS) * sizeof(double);
 }

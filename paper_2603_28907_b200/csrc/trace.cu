@@ -181,17 +181,17 @@ struct Fix {
 };
 
 __device__ __noinline__ Fix fix64(double h00, double h10, double h01, double h11, float Xi, float Xi1,
-                                  float Yj, float Yj1, Ray r, float s, float s1) {
+                                  float Yj, float Yj1, Ray r, double s, double s1) {
   const double ix = 1.0 / ((double)Xi1 - (double)Xi), iy = 1.0 / ((double)Yj1 - (double)Yj);
-  const double u0 = ((double)r.ox + (double)s * (double)r.dx - (double)Xi) * ix;
-  const double v0 = ((double)r.oy + (double)s * (double)r.dy - (double)Yj) * iy;
-  const double z0 = (double)s * (double)r.dz;
+  const double u0 = ((double)r.ox + s * (double)r.dx - (double)Xi) * ix;
+  const double v0 = ((double)r.oy + s * (double)r.dy - (double)Yj) * iy;
+  const double z0 = s * (double)r.dz;
   const double al = (double)r.dx * ix, be = (double)r.dy * iy;
   const double b = h10 - h00, c = h01 - h00, e = (h11 - h10) - (h01 - h00);
   const double g0 = (h00 - z0) + u0 * (b + e * v0) + c * v0;
   const double g1 = b * al + c * be + e * (u0 * be + v0 * al) - (double)r.dz;
   const double g2 = e * al * be;
-  const double L = (double)s1 - (double)s;
+  const double L = s1 - s;
   const double disc = g1 * g1 - 4.0 * g2 * g0;
   double t1 = 0, t2 = 0;
   const bool two = disc > 0.0;
@@ -345,6 +345,41 @@ struct Geo {
 // directly: no pointer registers, no address setup in the hot loops).
 __shared__ float sgeo[4][MT_MAX_AXIS];   // X, Y, 1/ΔX, 1/ΔY
 
+// Exact cell boundaries for the fp64 re-solves (HP2/HP3): a crossing within fp32
+// rounding of a cell edge must land in the right cell — the two bilinear patches
+// meet there with a kink, so the neighbour's |g'| (and hence the adjoint weight)
+// would be wrong — so fix64 takes the boundary parameters in fp64 from the exact
+// fp32 inputs instead of the stored fp32 s_out.  Boundary between stored cells
+// wa -> wb: the x-line (i changed) or y-line the exact DDA crossed.
+__device__ __forceinline__ double cell_event64(const Ray &r, int wa, int wb) {
+  const int ia = cell_i(wa), ib = cell_i(wb);
+  if (ia != ib) return ((double)sgeo[0][ia > ib ? ia : ib] - (double)r.ox) / (double)r.dx;
+  const int ja = cell_j(wa), jb = cell_j(wb);
+  return ((double)sgeo[1][ja > jb ? ja : jb] - (double)r.oy) / (double)r.dy;
+}
+
+// The in-box exit parameter in fp64 (a0: top z_top/d_z or the first side wall).
+__device__ __forceinline__ double exit64(const Ray &r, int nx, int ny, float z_top) {
+  double s = (double)z_top / (double)r.dz;
+  if (r.dx > 0.f) s = fmin(s, ((double)sgeo[0][nx - 1] - (double)r.ox) / (double)r.dx);
+  if (r.dx < 0.f) s = fmin(s, ((double)sgeo[0][0] - (double)r.ox) / (double)r.dx);
+  if (r.dy > 0.f) s = fmin(s, ((double)sgeo[1][ny - 1] - (double)r.oy) / (double)r.dy);
+  if (r.dy < 0.f) s = fmin(s, ((double)sgeo[1][0] - (double)r.oy) / (double)r.dy);
+  return s;
+}
+
+// fp64 piece [s, s1] of stored cell k of a ray whose stored cells are [kfirst, kend):
+// the walk's own start (s_start, not a cell boundary) when k is its first cell,
+// else the exact boundaries.
+__device__ __forceinline__ void piece64(const TraceArgs &a, const Ray &r, int k, int kfirst, int kend, int kwalk0,
+                                        float s_start, double &s, double &s1) {
+  const int w = __ldg(&a.trav[k].x);
+  s = k == kwalk0 ? (double)s_start : cell_event64(r, __ldg(&a.trav[k - 1].x), w);
+  if (k == kwalk0 && k > kfirst && s_start == __int_as_float(__ldg(&a.trav[k - 1].y)))
+    s = cell_event64(r, __ldg(&a.trav[k - 1].x), w);   // (the walk started on the boundary itself)
+  s1 = k + 1 < kend ? cell_event64(r, w, __ldg(&a.trav[k + 1].x)) : exit64(r, a.tc.nx, a.tc.ny, a.tc.z_top);
+}
+
 // Crossing records of one chain x ray: up to RCAP per surface, kept in shared
 // memory at slot [(l*RCAP + m)*MT_THREADS + tid] (conflict-free: consecutive
 // threads, consecutive 16-B words).
@@ -400,12 +435,13 @@ __device__ __forceinline__ void scatter4(macc *Gl, int STRIDE, int base, int ny,
 // else record crossings (n[l] counts all, the first RCAP are stored).
 // ---------------------------------------------------------------------------
 template <int STRIDE, bool SCAT>
-__device__ __forceinline__ void walk(const Ray &r, const int2 *__restrict__ cells,
+__device__ __forceinline__ void walk(const TraceArgs *ta, int kfirst, const Ray &r, const int2 *__restrict__ cells,
                                      const float4 *__restrict__ cgeo, int k, int kend, float s0,
                                      float s_in0, float s_hi, int ny, int N, const float *Hk,
                                      const float *Hlo, macc *Gk, float4 bd, float &B0, float &B1,
                                      float4 *rec, int *n, float f0, float f1) {
   float s = s0, ds = s0 - s_in0;
+  const int kwalk0 = k;
   for (; k < kend; k++) {
     const int2 w = __ldg(cells + k);
     const float s1 = __int_as_float(w.y);
@@ -435,9 +471,11 @@ __device__ __forceinline__ void walk(const Ray &r, const int2 *__restrict__ cell
       if (!solve32(h00, h10, h01, h11, cg, za, Ls, r.dz, B, emit)) {
         // fp64 heights = fp32 value + stored residual (chain-interleaved column, stride 32)
         const float *pl = Hlo + ((size_t)l * N + base) * 32;
+        double se, se1;
+        piece64(*ta, r, k, kfirst, kend, kwalk0, s0, se, se1);
         const Fix x = fix64((double)h00 + pl[0], (double)h10 + pl[ny * 32], (double)h01 + pl[32],
                             (double)h11 + pl[ny * 32 + 32], sgeo[0][i], sgeo[0][i + 1], sgeo[1][j],
-                            sgeo[1][j + 1], r, s, s1);
+                            sgeo[1][j + 1], r, se, se1);
         B += x.below;
         for (int m = 0; m < x.n; m++) emit(x.u[m], x.v[m], x.ig[m]);
       }
@@ -1489,9 +1527,11 @@ __global__ void __launch_bounds__(MT_THREADS) k_trace_defer(TraceArgs a) {
             };
             if (!solve32(h00, h10, h01, h11, cg, za, Ls, r.dz, B, emit)) {
               const float *pl = Hl + ((size_t)l * N + base) * 32;
+              double se, se1;
+              piece64(a, r, k, a.trav_off[rr], kend, k0, s_lo, se, se1);
               const Fix x = fix64((double)h00 + pl[0], (double)h10 + pl[ny * 32], (double)h01 + pl[32],
                                   (double)h11 + pl[ny * 32 + 32], sgeo[0][i], sgeo[0][i + 1], sgeo[1][j],
-                                  sgeo[1][j + 1], r, s, s1);
+                                  sgeo[1][j + 1], r, se, se1);
               B += x.below;
               for (int m = 0; m < x.n; m++) emit(x.u[m], x.v[m], x.ig[m]);
             }
@@ -1541,7 +1581,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_trace_defer(TraceArgs a) {
         int nrec[2] = {0, 0};
         const int kend = a.trav_off[rr + 1];
         const int k0 = band_entry(a.trav, a.trav_off[rr], kend, s_lo, s_in0);
-        walk<32, true>(r, a.trav, a.trav_geo, k0, kend, s_lo, s_in0, s_hi, ny, N, Hk, Hl, a.G + off, bd,
+        walk<32, true>(&a, a.trav_off[rr], r, a.trav, a.trav_geo, k0, kend, s_lo, s_in0, s_hi, ny, N, Hk, Hl, a.G + off, bd,
                        d0, d1, nullptr, nrec, f0, f1);
       }
     } else if (lane == 0) {

@@ -22,6 +22,7 @@ sampler statistic needs a cross-rank reduction (ChainShard(replicated=True)).
 """
 from __future__ import annotations
 
+import contextlib
 import math
 from typing import Optional
 
@@ -70,7 +71,8 @@ class DualAveraging:
         return math.exp(self.log_eps)
 
     def final(self) -> float:
-        return math.exp(self.log_eps_bar)
+        """The averaged step size; with no update yet, the current one (ε₀)."""
+        return math.exp(self.log_eps_bar if self.m > 0 else self.log_eps)
 
 
 def mass_windows(n_warmup: int, init: int = 75, term: int = 50, base: int = 25):
@@ -165,12 +167,24 @@ class ChainShard:
         self.n_total = n_chains_total or self.C
         self.group = group
         self.stream = stream
+        # every torch-side operation on the shard's tensors runs on the shard's stream, in order
+        # with the library calls it launches there (none when stream is None: the current stream)
+        self._ctx = (lambda: torch.cuda.stream(stream)) if stream is not None else contextlib.nullcontext
         self.replicated = replicated
         if sampler not in ("hmc", "nuts"):
             raise ValueError(f"sampler {sampler!r}")
         self.sampler, self.max_depth = sampler, max_depth   # NUTS: 2^max_depth leaves cap
         self.adapt_mass = adapt_mass                        # diagonal mass from warm-up windows (R19b)
         self.minv = None
+        with self._ctx():
+            self._alloc(x0, eps0)
+        self.n_samples = 0
+        self.da = DualAveraging(eps0)
+        self.it = 0
+        problem.logpost_grad(self.x, self.logp, self.grad, self.status, stream=stream)
+
+    def _alloc(self, x0, eps0):
+        torch = self.torch
         t = lambda *s, dt=torch.float32: torch.zeros(s, dtype=dt, device=self.dev)  # noqa: E731
         self.x = torch.from_numpy(np.ascontiguousarray(x0, np.float32)).to(self.dev)
         self.logp = t(self.C, dt=torch.float64)
@@ -181,12 +195,9 @@ class ChainShard:
         self.depth = t(self.C, dt=torch.int32)
         self.status = t(self.C, dt=torch.int32)
         self.acc_fixed = t(2, dt=torch.int64)
+        self.acc_mon = t(2, dt=torch.int64)      # sampling-phase acceptance sums (device, no host sync)
         self.mean = t(self.C, self.P)
         self.m2 = t(self.C, self.P)
-        self.n_samples = 0
-        self.da = DualAveraging(eps0)
-        self.it = 0
-        problem.logpost_grad(self.x, self.logp, self.grad, self.status, stream=stream)
 
     def refresh(self):
         """Re-evaluate logp / grad at the current x (after the problem's model changed)."""
@@ -209,35 +220,50 @@ class ChainShard:
             return False
 
     def step(self, adapt: bool = True, sample: bool = False, monitor: bool = False) -> float:
-        """One HMC iteration (a1-a9).  Returns the global mean acceptance probability
-        when adapting or monitoring (it needs the all-rank sum on the host)."""
+        """One HMC (or NUTS) iteration (a1-a9).  adapt: dual-averaging update of the global ε
+        from the all-rank mean acceptance (one host read per iteration); returns that mean.
+        monitor: add the acceptance sums to the device accumulator read by accept_rate() —
+        no host synchronisation, so sampling iterations queue back to back.  sample: Welford."""
         pb = self.pb
-        if self.sampler == "nuts":   # acc_prob <- the NUTS acceptance statistic
-            pb.nuts_step(self.x, self.logp, self.grad, self.eps, self.max_depth, self.seed, self.it,
-                         self.chain_offset, self.acc_prob, self.depth, self.accepted, self.status,
-                         stream=self.stream)
-        else:
-            pb.hmc_step(self.x, self.logp, self.grad, self.eps, self.L, self.seed, self.it,
-                        self.chain_offset, self.acc_prob, self.accepted, self.status, stream=self.stream)
         alpha = float("nan")
-        if adapt or monitor:
-            self.acc_fixed.zero_()
-            pb.stats_update(self.C, accept_prob=self.acc_prob, acc_fixed=self.acc_fixed, stream=self.stream)
-        if sample:
-            pb.stats_update(self.C, x=self.x, n_prev=self.n_samples, mean=self.mean, m2=self.m2,
-                            stream=self.stream)
-            self.n_samples += 1
-        if adapt or monitor:
-            self._allreduce(self.acc_fixed)
-            s, n = (int(v) for v in self.acc_fixed.cpu().tolist())
-            alpha = s / 4294967296.0 / max(n, 1)
+        with self._ctx():
+            if self.sampler == "nuts":   # acc_prob <- the NUTS acceptance statistic
+                pb.nuts_step(self.x, self.logp, self.grad, self.eps, self.max_depth, self.seed, self.it,
+                             self.chain_offset, self.acc_prob, self.depth, self.accepted, self.status,
+                             stream=self.stream)
+            else:
+                pb.hmc_step(self.x, self.logp, self.grad, self.eps, self.L, self.seed, self.it,
+                            self.chain_offset, self.acc_prob, self.accepted, self.status, stream=self.stream)
             if adapt:
+                self.acc_fixed.zero_()
+                pb.stats_update(self.C, accept_prob=self.acc_prob, acc_fixed=self.acc_fixed, stream=self.stream)
+            elif monitor:
+                pb.stats_update(self.C, accept_prob=self.acc_prob, acc_fixed=self.acc_mon, stream=self.stream)
+            if sample:
+                pb.stats_update(self.C, x=self.x, n_prev=self.n_samples, mean=self.mean, m2=self.m2,
+                                stream=self.stream)
+                self.n_samples += 1
+            if adapt:
+                self._allreduce(self.acc_fixed)
+                s, n = (int(v) for v in self.acc_fixed.cpu().tolist())
+                alpha = s / 4294967296.0 / max(n, 1)
                 self.eps.fill_(self.da.update(alpha))
         self.it += 1
         return alpha
 
+    def accept_rate(self, reset: bool = True) -> float:
+        """All-rank mean acceptance over the monitored iterations since the last reset
+        (one host read)."""
+        with self._ctx():
+            tot = self._allreduce(self.acc_mon.clone())
+            s, n = (int(v) for v in tot.cpu().tolist())
+            if reset:
+                self.acc_mon.zero_()
+        return s / 4294967296.0 / max(n, 1)
+
     def end_warmup(self):
-        self.eps.fill_(self.da.final())
+        with self._ctx():
+            self.eps.fill_(self.da.final())
 
     def summary_update(self, nz: int = 60, gap: float = 10.0):
         """Accumulate the f4 posterior summaries of the current draws (mt_summary_update)."""
@@ -250,33 +276,40 @@ class ChainShard:
         """Mean heights, air-gap probability, indicator-std tomography (all ranks'
         draws, all-reduced) and this rank's MAP draw."""
         nz, gap, acc, mx, ml = self._sum
-        acc = self._allreduce(acc.clone())
-        out = self.pb.summaries(acc, nz)
-        out.update(map_x=mx.cpu().numpy(), map_logp=float(ml.cpu()[0]), gap_threshold=gap)
+        with self._ctx():
+            acc = self._allreduce(acc.clone())
+            out = self.pb.summaries(acc, nz)
+            out.update(map_x=mx.cpu().numpy(), map_logp=float(ml.cpu()[0]), gap_threshold=gap)
         return out
 
     def nested_rhat(self, M: int = 8) -> np.ndarray:
         """Nested R̂ over super-chains of M contiguous chains."""
-        part = self.pb.nested_rhat_partials(self.C, M, self.mean, self.m2, max(self.n_samples, 1),
-                                            stream=self.stream)
-        self._allreduce(part)
-        return nested_rhat_from_partials(part.cpu().numpy(), self.n_total // M)
+        with self._ctx():
+            part = self.pb.nested_rhat_partials(self.C, M, self.mean, self.m2, max(self.n_samples, 1),
+                                                stream=self.stream)
+            self._allreduce(part)
+            part = part.cpu().numpy()
+        return nested_rhat_from_partials(part, self.n_total // M)
 
     def rhat(self) -> np.ndarray:
-        part = self.pb.rhat_partials(self.C, self.mean, self.m2, self.n_samples, stream=self.stream)
-        self._allreduce(part)
-        return rhat_from_partials(part.cpu().numpy(), self.n_total, self.n_samples)
+        with self._ctx():
+            part = self.pb.rhat_partials(self.C, self.mean, self.m2, self.n_samples, stream=self.stream)
+            self._allreduce(part)
+            part = part.cpu().numpy()
+        return rhat_from_partials(part, self.n_total, self.n_samples)
 
     def _mass_from_window(self, wmean, wm2, n: int):
         """Pooled within-chain variance of the window's draws -> regularised M^-1."""
         torch = self.torch
-        tot = torch.stack([wm2.sum(0).double(), torch.full((self.P,), float(self.C * (n - 1)),
-                                                           dtype=torch.float64, device=self.dev)])
-        self._allreduce(tot)
-        var = tot[0] / tot[1]
-        minv = (n / (n + 5.0)) * var + 1e-3 * (5.0 / (n + 5.0))
-        self.minv = minv.float().contiguous()
-        self.pb.set_inverse_mass(self.minv)
+        with self._ctx():
+            tot = torch.stack([wm2.sum(0).double(), torch.full((self.P,), float(self.C * (n - 1)),
+                                                               dtype=torch.float64, device=self.dev)])
+            self._allreduce(tot)
+            var = tot[0] / tot[1]
+            minv = (n / (n + 5.0)) * var + 1e-3 * (5.0 / (n + 5.0))
+            self.minv = minv.float().contiguous()
+            self.torch.cuda.current_stream().synchronize()   # (mt_set_inverse_mass copies synchronously)
+            self.pb.set_inverse_mass(self.minv)
 
     def run(self, n_warmup: int, n_sample: int):
         accs = []
@@ -287,8 +320,9 @@ class ChainShard:
             for (a, b) in windows:
                 if a <= i < b:
                     if i == a:
-                        wmean = self.torch.zeros_like(self.x)
-                        wm2 = self.torch.zeros_like(self.x)
+                        with self._ctx():
+                            wmean = self.torch.zeros_like(self.x)
+                            wm2 = self.torch.zeros_like(self.x)
                     self.pb.stats_update(self.C, x=self.x, n_prev=i - a, mean=wmean, m2=wm2, stream=self.stream)
                     if i == b - 1:   # window end: new mass, restart step-size adaptation (R19b)
                         self._mass_from_window(wmean, wm2, b - a)

@@ -5,7 +5,9 @@ DESIGN.md "Tolerances":
   lengths     |L_dev - L_ora| <= 1e-5 * L_tot per (chain, ray, unit)
   logpost     |Δ| <= 1e-4 |logp_ora| per chain (deviance-centred form + prior)
   gradient    ||Δ||_2 <= 1e-3 ||g_ora||_2 per chain
-  leapfrog    ||x10_dev - x10_ora||_2 <= 1e-3 ||x10_ora||_2 per chain
+  leapfrog    ||x10_dev - x10_ora||_2 <= 1e-3 ||x10_ora||_2 per chain (north_star as written)
+              and, displacement-relative (R24b),
+              ||x10_dev - x10_ora||_2 <= 1e-3 ||x10_ora - x0||_2 + 2 L 2^-24 ||x0||_2
 """
 import numpy as np
 import pytest
@@ -32,6 +34,17 @@ def gpu(problems):
             cache[key] = Problem(problems(name), device=0, max_chains=max_chains or cfg.chains, **kw)
         return cache[key]
     return get
+
+
+def _record_margin(key, value):
+    import json
+    import os
+    d = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+    os.makedirs(d, exist_ok=True)
+    path = os.path.join(d, "parity_margins.json")
+    data = json.load(open(path)) if os.path.exists(path) else {}
+    data[key] = value
+    json.dump(data, open(path, "w"), indent=1, sort_keys=True)
 
 
 def rel_l2(a, b):
@@ -237,10 +250,18 @@ def test_leapfrog_10_steps(gpu, oracle_problem, name, C):
     xo, po, lpo, go = oracle.leapfrog(x0.astype(np.float64), p0, e, 10,
                                       lambda xx: (lambda o: (o["logp"], o["grad"]))(op.logpost_grad(xx)))
     xd = x.cpu().numpy().astype(np.float64)
+    worst = 0.0
     for c in range(C):
-        assert rel_l2(xd[c], xo[c]) <= 1e-3, (c, rel_l2(xd[c], xo[c]))   # north_star criterion
-        disp = np.linalg.norm(xd[c] - xo[c]) / np.linalg.norm(xo[c] - x0[c])
-        assert disp < 0.05, (c, disp)   # diagnostic: displacement-relative error
+        assert rel_l2(xd[c], xo[c]) <= 1e-3, (c, rel_l2(xd[c], xo[c]))   # north_star criterion as written
+        # displacement-relative (R24b): 1e-3 of the oracle's own displacement, plus the fp32 floor of
+        # the state block (each of the L drifts rounds x once: <= 2^-24 ||x|| per step; factor 2 for
+        # the momentum and gradient roundings it feeds)
+        disp = np.linalg.norm(xo[c] - x0[c])
+        bound = 1e-3 * disp + 2 * 10 * 2.0 ** -24 * np.linalg.norm(x0[c])
+        err = np.linalg.norm(xd[c] - xo[c])
+        worst = max(worst, err / bound)
+        assert err <= bound, (c, err, disp, bound)
+    _record_margin(f"leapfrog10/{name}", worst)
     # logp/grad returned by the fused leapfrog are those of its own final x.  (Comparing with
     # the oracle's trajectory end instead is ill-conditioned: |∇logp| ~ 1e5, so position
     # differences well inside 1e-3 move logp by O(10).)
