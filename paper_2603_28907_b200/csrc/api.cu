@@ -80,7 +80,7 @@ int check_chains(const mt_problem *p, int32_t C) {
 
 void free_all(mt_problem *p) {
   voxel_free(p);
-  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_trav_geo, p->d_trav_km, p->d_rl_head, p->d_rl_code, p->d_rl_ovf, p->d_ovf_q, p->d_ovf_n, p->d_redo, p->d_H, p->d_Hlo, p->d_Hc, p->d_cl, p->d_tab, p->d_ray_c, p->d_cs, p->d_xw, p->d_minv, p->mb_red, p->mb_band, p->mb_ticket, p->d_G,
+  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_trav_geo, p->d_trav_km, p->d_rl_head, p->d_rl_code, p->d_rl_ovf, p->d_ovf_q, p->d_ovf_n, p->d_redo, p->d_H, p->d_Hlo, p->d_Hc, p->d_cl, p->d_cs, p->d_xw, p->d_minv, p->mb_red, p->mb_band, p->mb_ticket, p->d_G,
                   p->d_band, p->d_ll, p->d_x0, p->d_g0, p->d_mom, p->d_kin0, p->d_kin1, p->d_lp0};
   for (void *b : bufs)
     if (b) cudaFree(b);
@@ -267,7 +267,7 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   // ray-lanes height copies: the ray lanes serve C < 16 unless MT_TRACE_K forces them
   const bool rl_any_c = p->trace_k != 0 && p->trace_k != 32;
   ALLOC(p->d_Hc, sizeof(float) * (rl_any_c || MC < 16 ? MC : 16) * P);
-  ALLOC(p->d_cl, sizeof(uint2) * MC32 * 3 * p->N);
+  ALLOC(p->d_cl, sizeof(float2) * (MC32 + 32) * 2 * p->N);   // (+32: whole 64-chain groups for k_cell_prep2)
   ALLOC(p->d_G, sizeof(macc) * MC32 * P);
   ALLOC(p->d_band, sizeof(float4) * MC);
   ALLOC(p->d_ll, sizeof(macc) * MC);

@@ -12,7 +12,6 @@
 #define MT_MAX_AXIS 128
 #define MT_MAX_NODES 4096
 #define MT_THREADS 256
-#define MT_TABQ 32   // band-entry levels per ray (chain-lanes trace)
 
 // Fixed-point accumulators (R30).  ∂ℓ/∂H and the log-likelihood are
 // summed as two's-complement int64 with RED.ADD.64: integer adds commute
@@ -86,13 +85,8 @@ struct TraceArgs {
   int64_t rays_per_block;
   int C;                        // chains in this call
   const float *H;               // [C][2][N] heights
-  const uint2 *cl;              // chain lanes, per evaluation (k_cell_prep): [group][slot][node][32] 8-byte
-                                //   elements; slot 0: the cell's corner bounds rounded outward to fp16,
-                                //   {half2(min H0, min H1), half2(max H0, max H1)}; slots 1, 2: the paired
-                                //   heights (H_l(i,j), H_l(i,j+1)) of surface l = 0, 1 (fp32 bits)
-  const float4 *ray_c;          // chain lanes: per ray {d_z, 1/d_z, s_exit, first stored cell (int bits)}
-  const uint8_t *tab;           // chain lanes: per ray [MT_TABQ] band-entry cells (relative to the first)
-  float tab_scale;              // MT_TABQ / z_top
+  const void *cl;               // chain lanes, per evaluation: paired heights (k_cell_prep: float2
+                                //   [group32][l][node][32]; k_cell_prep2: float4 [group64][l][node][32])
   const float *Hlo;             // fp32 residuals of the fp64 heights (0 for caller heights): the
                                 //   fp64 re-solves of ill-conditioned cells use H + Hlo (HP2)
   const float4 *band;           // [C] (min H0, max H0, min H1, max H1)
@@ -220,9 +214,7 @@ struct mt_problem {
   int64_t trav_cells = 0;
   float *d_H = nullptr, *d_Hlo = nullptr;
   macc *d_G = nullptr;          // ∂ℓ/∂H accumulator, chain-interleaved, fixed point (R30)
-  uint2 *d_cl = nullptr;        // chain-lanes per-evaluation cell bounds + paired heights (TraceArgs::cl)
-  float4 *d_ray_c = nullptr;    // chain-lanes per-ray record
-  uint8_t *d_tab = nullptr;     // chain-lanes band-entry table [R][MT_TABQ]
+  void *d_cl = nullptr;         // chain-lanes paired heights (TraceArgs::cl)
   float *d_Hc = nullptr;        // [min(max_chains, 16)][2N] contiguous heights for the ray-lanes trace
   float4 *d_band = nullptr;
   macc *d_ll = nullptr;         // log-likelihood accumulator, fixed point (R30)
@@ -232,7 +224,7 @@ struct mt_problem {
   // trace launch shape
   int trace_k = 0;              // chains per block (0 = auto)
   int trace_s = 0;              // ray splits (0 = auto)
-  int cl_v = -1;                // chain-lanes kernel (MT_CL_V): -1 auto (c2 at C >= 64, else v0), 0 v0, 2 c2, 3 v3
+  int cl_v = -1;                // chain-lanes kernel (MT_CL_V): -1 auto (c2 at C >= 64, else v0), 0 v0, 2 c2
   int chunk = 0;                // chain lanes: rays per block (a Morton-ordered chunk; 0 = by chain count)
   // batched NUTS workspace (allocated by the first mt_nuts_step)
   float *nuts_ws = nullptr;

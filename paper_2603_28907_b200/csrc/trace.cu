@@ -286,7 +286,7 @@ __device__ __forceinline__ bool solve32(float h00, float h10, float h01, float h
 }
 
 // solve32 with the ray-only parts K = u0 β + v0 α, M = α β stored per cell (a0) and the
-// one-crossing root from the cancellation-free form with |g'| = √D (cl_solve's reading).
+// one-crossing root from the cancellation-free form with |g'| = √D (the chain-lanes solve).
 template <class Emit>
 __device__ __forceinline__ bool solve32k(float h00, float h10, float h01, float h11, float4 cg, float2 km,
                                          float za, float Ls, float dz, float &B, Emit &&emit) {
@@ -549,7 +549,7 @@ __device__ __forceinline__ void load_geometry(const TraceArgs &a, float *Xs, flo
 __global__ void k_build_trav(TraceArgs a, const int32_t *off, int32_t *count, int2 *cells, float4 *cgeo,
                              float2 *ckm,
                              int2 *rl_head, uint4 *rl_code, uint32_t *rl_ovf,
-                             const int32_t *ovf_off, uint8_t *tab) {
+                             const int32_t *ovf_off) {
   __shared__ float Xs[MT_MAX_AXIS], Ys[MT_MAX_AXIS];
   const int nx = a.tc.nx, ny = a.tc.ny;
   for (int k = threadIdx.x; k < nx; k += blockDim.x) Xs[k] = a.X[k];
@@ -563,12 +563,6 @@ __global__ void k_build_trav(TraceArgs a, const int32_t *off, int32_t *count, in
   int n = 0;
   if (rl_head) rl_head[rr] = make_int2((off[rr + 1] - off[rr]) | (i << 8) | (j << 15), ovf_off[rr]);
   uint32_t cw[4] = {0u, 0u, 0u, 0u};
-  // band-entry table (chain lanes): tab[q] = the first cell whose s_out exceeds the ray
-  // parameter of height q z_top / MT_TABQ (less 1e-5 relative, so rounding of the
-  // trace's level choice can only start it a cell early)
-  int tq = 0;
-  const double lev = (double)a.tc.z_top / MT_TABQ / (double)q.r.dz;
-  uint8_t *tb = tab ? tab + (size_t)rr * MT_TABQ : nullptr;
   for (int guard = 0; guard < 4 * (MT_MAX_AXIS + 2); guard++) {
     float s_ev;
     int fc;
@@ -591,8 +585,6 @@ __global__ void k_build_trav(TraceArgs a, const int32_t *off, int32_t *count, in
       cgeo[off[rr] + n] = make_float4(uf, vf, af, bf);
       ckm[off[rr] + n] = make_float2((float)((double)uf * bf + (double)vf * af), (float)((double)af * bf));
     }
-    if (tb)
-      while (tq < MT_TABQ && (double)so > (double)tq * lev * (1.0 - 1e-5)) tb[tq++] = (uint8_t)n;
     s_in = so;
     n++;
     if (ev & 4) break;
@@ -602,210 +594,20 @@ __global__ void k_build_trav(TraceArgs a, const int32_t *off, int32_t *count, in
   }
   if (count) count[rr] = n;
   if (rl_code) rl_code[rr] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
-  if (tb)
-    while (tq < MT_TABQ) tb[tq++] = (uint8_t)n;
 }
 
 // ---------------------------------------------------------------------------
-// K2, chain lanes: warp = one ray x 32 chains, lane = chain
+// K2, chain lanes: warp = one ray x 32 (k_trace_v0) or 64 (k_trace_c2) chains
 // ---------------------------------------------------------------------------
-// Per evaluation, k_cell_prep writes per-(chain, cell) corner bounds of both
-// surfaces (the bilinear min / max sit at corners), rounded OUTWARD to fp16
-// and packed as {half2(min H0, min H1), half2(max H0, max H1)}: the walk
-// classifies both surfaces of a cell with one 8-B load and two packed fp16
-// compares (the ray's z range rounded outward too), so a "fully below" /
-// "fully above" decision is always right and only a few more cells than
-// necessary reach the exact fp32 solve.  It also writes the paired heights
-// H2 = (H(i,j), H(i,j+1)) the solve reads (two 8-B loads per surface-cell).
-// Layouts [group][node][32] (bounds) and [group][l][node][32] (H2): a warp's
-// load is one contiguous line.  Lanes c >= C get bounds below every ray.
-__global__ void __launch_bounds__(MT_THREADS) k_cell_prep(const float *__restrict__ H, uint2 *__restrict__ cl, int C,
-                                                        int nx, int ny, int N, int64_t n) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// Per evaluation, k_cell_prep writes the paired heights the chain-lanes walk
+// reads: H2 = (H_l(i,j), H_l(i,j+1)) per node, [group][l][node][lane], so a
+// cell's four corners of one surface are two 8-B loads of one 256-B line each.
+__global__ void __launch_bounds__(MT_THREADS) k_cell_prep(const float *__restrict__ H, float2 *__restrict__ H2, int ny,
+                                                        int64_t n) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // [group][l][node][lane]
   if (t >= n) return;
-  const int lane = (int)(t & 31);
-  const int64_t gn = t >> 5;
-  const int grp = (int)(gn / N), node = (int)(gn - (int64_t)grp * N);
-  const int i = node / ny, j = node - i * ny;
-  const bool cell = i < nx - 1 && j < ny - 1;
-  const size_t hb = ((size_t)grp * 2 * N + node) * 32 + lane;   // heights (chain-interleaved)
-  uint2 *o = cl + ((size_t)grp * 3 * N + node) * 32 + lane;      // [group][slot][node][lane]
-  float mn[2], mx[2];
-#pragma unroll
-  for (int l = 0; l < 2; l++) {
-    const float *p = H + hb + (size_t)l * N * 32;
-    const float h00 = p[0], h01 = j + 1 < ny ? p[32] : 0.f;
-    o[(size_t)(1 + l) * N * 32] = make_uint2(__float_as_uint(h00), __float_as_uint(h01));
-    if (cell) {
-      const float h10 = p[ny * 32], h11 = p[ny * 32 + 32];
-      mn[l] = fminf(fminf(h00, h01), fminf(h10, h11));
-      mx[l] = fmaxf(fmaxf(h00, h01), fmaxf(h10, h11));
-    }
-  }
-  if (!cell) return;
-  uint2 b;
-  if (grp * 32 + lane < C) {
-    b.x = (unsigned)__half_as_ushort(__float2half_rd(mn[0])) | ((unsigned)__half_as_ushort(__float2half_rd(mn[1])) << 16);
-    b.y = (unsigned)__half_as_ushort(__float2half_ru(mx[0])) | ((unsigned)__half_as_ushort(__float2half_ru(mx[1])) << 16);
-  } else {
-    b.x = b.y = 0xfc00fc00u;   // -inf: every cell lies "above" an inactive lane's surfaces
-  }
-  o[0] = b;
-}
-
-// One surface of one stored cell for this lane's chain, the ray piece
-// [s, s1] (za = s d_z, Ls = s1 - s) straddling the surface's corner range.
-// g(τ) = h(u0 + ατ, v0 + βτ) - d_z (s + τ) = g0 + g1 τ + g2 τ² (a3).  With
-// g(0), g(Δs) of different signs there is exactly one root, at which
-// |g'| = √D (D = g1² - 4 g0 g2, for either root of a quadratic): it is taken
-// from the form without cancellation — t = -2 g0/(g1 + s√D) when sign g1 =
-// s = sign g(Δs), else (s√D - g1)/(2 g2) — and 1/|g'| = rsqrt(D) is what the
-// adjoint needs (a6).  Equal signs: two roots iff the vertex lies inside and
-// g(vertex) has the other sign.  An ill-conditioned cell (|g| < ZTHR where
-// the ray enters or leaves, |g'| < GTHR at a root, a near-tangent vertex)
-// sets `defer`: the pair is re-done by k_trace_defer (fp32 + in-place fp64).
-// SCAT (the second walk of a pair with more than RCAP crossings of a surface):
-// crossings m >= RCAP are scattered (prescaled weight f), nothing else.
-template <int L, bool SCAT>
-__device__ __forceinline__ void cl_solve(const uint2 *__restrict__ CL, unsigned hi, int oy, float4 cg, float2 km,
-                                         float za, float Ls, float dz, unsigned node, float &B, int &n, int &defer,
-                                         float4 *rec, macc *Gp, float f) {
-  const uint2 r0 = __ldg(CL + hi), r1 = __ldg(CL + (hi + (unsigned)oy));   // (h00, h01), (h10, h11)
-  const float h00 = __uint_as_float(r0.x), h01 = __uint_as_float(r0.y), h10 = __uint_as_float(r1.x),
-              h11 = __uint_as_float(r1.y);
-  const float b = h10 - h00, c = h01 - h00, e = (h11 - h10) - (h01 - h00);
-  const float u0 = cg.x, v0 = cg.y, al = cg.z, be = cg.w;
-  const float g0 = (h00 - za) + u0 * (b + e * v0) + c * v0;
-  const float g1 = fmaf(b, al, fmaf(c, be, fmaf(e, km.x, -dz)));   // K = u0 β + v0 α (stored, a0)
-  const float g2 = e * km.y;                                        // M = α β
-  const float gL = g0 + Ls * (g1 + Ls * g2);
-  auto emit = [&](float t, float ig) {
-    const float u = u0 + al * t, v = v0 + be * t;
-    if (SCAT) {
-      if (n >= RCAP) {
-        const float wv = f * ig, wa = wv * (1.f - u), wb = wv * u;
-        atomicAdd(Gp, q_raw(wa * (1.f - v)));
-        atomicAdd(Gp + oy, q_raw(wb * (1.f - v)));
-        atomicAdd(Gp + 32, q_raw(wa * v));
-        atomicAdd(Gp + oy + 32, q_raw(wb * v));
-      }
-    } else if (n < RCAP) {
-      rec[(L * RCAP + n) * MT_THREADS] = make_float4(__uint_as_float(node), u, v, ig);
-    }
-    n++;
-  };
-  if (fabsf(g0) < ZTHR || fabsf(gL) < ZTHR) { defer = 1; return; }
-  const bool p0 = g0 > 0.f, pL = gL > 0.f;
-  const float D = fmaf(g1, g1, -4.f * g2 * g0);
-  if (p0 != pL) {                                   // exactly one crossing
-    if (!(D >= GTHR * GTHR)) { defer = 1; return; }
-    const float r = rsqrtf(D), sq = D * r;
-    const float ssq = pL ? sq : -sq;
-    const bool nc = (g1 > 0.f) == pL;
-    const float t = fminf(fmaxf(__fdividef(nc ? -2.f * g0 : ssq - g1, nc ? g1 + ssq : 2.f * g2), 0.f), Ls);
-    B += p0 ? t : Ls - t;
-    emit(t, r);
-    return;
-  }
-  const float a2 = 2.f * g2;
-  const bool vin = -g1 * a2 > 0.f && fabsf(g1) < Ls * fabsf(a2);   // vertex inside (0, Δs)
-  if (vin && D > 0.f && ((g2 > 0.f) == p0)) {       // two crossings (rare)
-    if (!(D >= GTHR * GTHR)) { defer = 1; return; }
-    const float r = rsqrtf(D);
-    const float q = -0.5f * (g1 + copysignf(D * r, g1));
-    const float ta = __fdividef(g0, q), tb = __fdividef(q, g2);
-    const float t1 = fminf(ta, tb), t2 = fmaxf(ta, tb);
-    B += p0 ? Ls - (t2 - t1) : (t2 - t1);
-    emit(t1, r);
-    emit(t2, r);
-    return;
-  }
-  if (vin && fabsf(D) < 2.f * fabsf(a2) * ZTHR) { defer = 1; return; }   // near-tangent
-  if (p0) B += Ls;
-}
-
-// The band-entry table (a0) gives the first stored cell to walk: the walk
-// starts at a stored cell boundary s0 <= s_lo (everything before it lies
-// below every surface of the warp's chains), so the stored per-cell entry
-// geometry applies as is.
-struct WalkStart {
-  int k, kend;
-  float s0;
-};
-
-__device__ __forceinline__ WalkStart cl_start(const TraceArgs &a, int rr, int tq, float koff_bits) {
-  WalkStart ws;
-  const int koff = __float_as_int(koff_bits);
-  ws.kend = __ldg(a.trav_off + rr + 1);
-  ws.k = koff + __ldg(a.tab + (size_t)rr * MT_TABQ + tq);
-  ws.s0 = ws.k > koff ? __int_as_float(__ldg(&a.trav[ws.k - 1].y)) : 0.f;
-  return ws;
-}
-
-// Classify the piece [za, zb] of a ray against both surfaces of a cell from the
-// packed fp16 corner bounds: za rounded down and zb rounded up to fp16 (so each
-// decision is conservative), two f16x2 compares with one predicate per half.
-// below_l: zb <= min H_l (the piece lies below surface l); st_l: neither below
-// nor above (za >= max H_l): the piece may cross surface l.
-__device__ __forceinline__ void classify2(float za, float zb, uint2 bq, bool &below0, bool &below1, bool &st0,
-                                          bool &st1) {
-  unsigned b0, b1, a0, a1;
-  asm("{\n\t.reg .pred p, q, r, t;\n\t"
-      ".reg .b16 ha, hb;\n\t"
-      ".reg .b32 za2, zb2;\n\t"
-      "cvt.rm.f16.f32 ha, %4;\n\t"
-      "cvt.rp.f16.f32 hb, %5;\n\t"
-      "mov.b32 za2, {ha, ha};\n\t"
-      "mov.b32 zb2, {hb, hb};\n\t"
-      "setp.le.f16x2 p|q, zb2, %6;\n\t"
-      "setp.ge.f16x2 r|t, za2, %7;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t"
-      "selp.u32 %1, 1, 0, q;\n\t"
-      "selp.u32 %2, 1, 0, r;\n\t"
-      "selp.u32 %3, 1, 0, t;\n\t}"
-      : "=r"(b0), "=r"(b1), "=r"(a0), "=r"(a1)
-      : "f"(za), "f"(zb), "r"(bq.x), "r"(bq.y));
-  below0 = b0;
-  below1 = b1;
-  st0 = !b0 && !a0;
-  st1 = !b1 && !a1;
-}
-
-// Scatter a lane's crossing records (a6): G_l[node] += f_l φ_node(u, v)/|g'| (f prescaled
-// by MT_GQ), fixed point; FAST: every weight below MT_QSMALL.
-// Per-lane cache of one cell's adjoint moments per surface (a6): consecutive rays of a
-// warp (Morton-adjacent) mostly cross a surface in the same cell, so the lane sums
-// W = Σ w, U = Σ w u, V = Σ w v, X = Σ w u v there (w = f/|g'|) and scatters the four
-// node values W - U - V + X, U - X, V - X, X (= Σ w φ_node) only when the cell changes:
-// far fewer 64-bit fixed-point atomics.  The sums follow the warp's fixed ray order, so
-// results stay bit-reproducible for a given launch shape (which depends on R only).
-struct CellAcc {
-  int node;             // cached cell's corner node, -1: empty
-  float W, U, V, X;
-};
-
-__device__ __forceinline__ void acc_flush(CellAcc &c, macc *Gl, int oy) {
-  if (c.node >= 0) {
-    macc *pg = Gl + ((unsigned)c.node << 5);
-    atomicAdd(pg, q_raw((c.W - c.U) - (c.V - c.X)));
-    atomicAdd(pg + oy, q_raw(c.U - c.X));
-    atomicAdd(pg + 32, q_raw(c.V - c.X));
-    atomicAdd(pg + oy + 32, q_raw(c.X));
-  }
-  c.node = -1;
-}
-
-__device__ __forceinline__ void acc_add(CellAcc &c, macc *Gl, int oy, int node, float w, float u, float v) {
-  if (node != c.node) {
-    acc_flush(c, Gl, oy);
-    c.node = node;
-    c.W = c.U = c.V = c.X = 0.f;
-  }
-  const float wu = w * u;
-  c.W += w;
-  c.U += wu;
-  c.V = fmaf(w, v, c.V);
-  c.X = fmaf(wu, v, c.X);
+  const int node_j = (int)((t >> 5) % ny);
+  H2[t] = make_float2(H[t], node_j + 1 < ny ? H[t + 32] : 0.f);
 }
 
 template <bool FAST>
@@ -828,160 +630,6 @@ __device__ __forceinline__ void scatter_recs(const float4 *rec, int m0, int m1, 
       atomicAdd(pg + 32, q_raw(wa * v));
       atomicAdd(pg + oy + 32, q_raw(wb * v));
     }
-  }
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_cl(TraceArgs a) {
-  extern __shared__ __align__(16) float4 recs[];   // crossing records [2*RCAP][MT_THREADS] (dynamic: a static
-                                                   // array of the same size measured 13% slower, carveout)
-  const int N = a.tc.N, oy = a.tc.ny * 32;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int grp = blockIdx.y, c = grp * 32 + lane;
-  const bool act = c < a.C;
-  float4 *rec = recs + threadIdx.x;
-  // the warp walks the union band of its 32 chains
-  float zlo = 3.0e38f, zhi = -3.0e38f;
-  if (act) {
-    const float4 bd = __ldg(a.band + c);
-    zlo = bd.x;
-    zhi = bd.w;
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    zlo = fminf(zlo, __shfl_xor_sync(0xffffffffu, zlo, o));
-    zhi = fmaxf(zhi, __shfl_xor_sync(0xffffffffu, zhi, o));
-  }
-  const int tq = min(max((int)(zlo * a.tab_scale), 0), MT_TABQ - 1);   // band-entry level
-  // [group][slot][node][lane] 8-byte elements (slot 0 bounds, 1-2 paired heights), addressed by
-  // 32-bit element indices off the array base (C 3N 32 < 2^32)
-  const uint2 *__restrict__ CL = a.cl;
-  const unsigned lb = (unsigned)grp * 3u * (unsigned)N * 32u + (unsigned)lane, n32 = (unsigned)N * 32u;
-  macc llq = 0;
-#if MT_CACC
-  CellAcc ca0{-1, 0.f, 0.f, 0.f, 0.f}, ca1{-1, 0.f, 0.f, 0.f, 0.f};
-#endif
-
-  const int r_begin = blockIdx.x * (int)a.rays_per_block;
-  const int r_end = min((int)a.R, r_begin + (int)a.rays_per_block);
-  for (int rr = r_begin + warp; rr < r_end; rr += MT_THREADS / 32) {
-    const float4 rc = __ldg(a.ray_c + rr);   // {d_z, 1/d_z, s_exit, first cell}
-    const float dz = rc.x, s_exit = rc.z;
-    // band bounds, widened by 1e-6 so rounding can only walk more cells
-    const float s_lo = fminf(zlo * rc.y * (1.f - 1e-6f), s_exit);
-    const float s_hi = fminf(zhi * rc.y * (1.f + 1e-6f), s_exit);
-    float B0 = s_lo, B1 = s_lo;                        // below both surfaces before s_lo
-    int n0 = 0, n1 = 0, defer = 0;
-    WalkStart ws{0, 0, 0.f};
-    if (s_lo < s_exit) {                               // warp-uniform
-      ws = cl_start(a, rr, tq, rc.w);
-      B0 = B1 = ws.s0;
-      float s = ws.s0, za = ws.s0 * dz;
-      // software pipeline: the cell word two cells ahead and the corner bounds one cell
-      // ahead are in flight while a cell is classified and solved
-      int k = ws.k;
-      int2 w1 = __ldg(a.trav + k);
-      int2 w2 = k + 1 < ws.kend ? __ldg(a.trav + k + 1) : make_int2(0, 0);
-      uint2 bq1 = __ldg(CL + (lb + cell_off32(w1.x)));
-      for (; k < ws.kend; k++) {
-        const int2 w = w1;
-        const uint2 bq = bq1;
-        w1 = w2;
-        if (k + 1 < ws.kend) bq1 = __ldg(CL + (lb + cell_off32(w1.x)));
-        if (k + 2 < ws.kend) w2 = __ldg(a.trav + k + 2);
-        const unsigned off = cell_off32(w.x);
-        const float s1 = __int_as_float(w.y);
-        const float zb = s1 * dz, Ls = s1 - s;
-        bool bl0, bl1, st0, st1;
-        classify2(za, zb, bq, bl0, bl1, st0, st1);
-        if (bl0) B0 += Ls;
-        if (bl1) B1 += Ls;
-        if (st0 || st1) {
-          const float4 cg = __ldg(a.trav_geo + k);
-          const float2 km = __ldg(a.trav_km + k);
-          if (st0) cl_solve<0, false>(CL, lb + n32 + off, oy, cg, km, za, Ls, dz, off >> 5, B0, n0, defer, rec, nullptr, 0.f);
-          if (st1) cl_solve<1, false>(CL, lb + 2 * n32 + off, oy, cg, km, za, Ls, dz, off >> 5, B1, n1, defer, rec, nullptr, 0.f);
-        }
-        if (s1 >= s_hi) break;
-        s = s1;
-        za = zb;
-      }
-    }
-    // an ill-conditioned cell: the whole pair goes to k_trace_defer (fp64 re-solve)
-    if (defer) {
-      const int q = atomicAdd(a.ovf_n, 1);
-      if (q < a.ovf_cap) a.ovf_q[q] = make_float4(__int_as_float(c), __int_as_float(rr), s_lo, s_hi);
-      else redo_mark(a, c, rr);   // queue full: the follow-up kernel finds the pair in the bitmap
-    }
-    if (MODE == TRACE_LL) {
-      const bool over = !defer && (n0 > RCAP || n1 > RCAP);   // more crossings than records
-      float f0 = 0.f, f1 = 0.f;
-      macc *G0 = a.G + (size_t)grp * 2 * N * 32 + lane;
-      if (!defer && act) {
-        const float2 rb = __ldg(reinterpret_cast<const float2 *>(a.ray_b + rr) + 1);
-        float dldO;
-        llq += q_ll(epilogue(rb.x, rb.y, a.tc, B0, B1, dldO));
-        f0 = dldO * a.tc.k0 * (float)MT_GQ;
-        f1 = dldO * a.tc.k1 * (float)MT_GQ;
-      }
-      // fixed-point scatter (a6): the corner weights w φ are bounded by |w| = |f|/|g'| <=
-      // |f|/GTHR, so when every lane's bound is below MT_QSMALL the warp converts on the
-      // FMA pipe (q_small), else with F2I.S64
-#if MT_CACC
-      if (!defer) {
-        for (int m = 0; m < min(n0, RCAP); m++) {
-          const float4 q = rec[m * MT_THREADS];
-          acc_add(ca0, G0, oy, (int)__float_as_uint(q.x), f0 * q.w, q.y, q.z);
-        }
-        for (int m = 0; m < min(n1, RCAP); m++) {
-          const float4 q = rec[(RCAP + m) * MT_THREADS];
-          acc_add(ca1, G0 + N * 32, oy, (int)__float_as_uint(q.x), f1 * q.w, q.y, q.z);
-        }
-      }
-#else
-      const int r0 = defer ? 0 : min(n0, RCAP), r1 = defer ? 0 : min(n1, RCAP);
-      if (__all_sync(0xffffffffu, fmaxf(fabsf(f0), fabsf(f1)) * (1.f / GTHR) < MT_QSMALL))
-        scatter_recs<true>(rec, r0, r1, G0, N, oy, f0, f1);
-      else
-        scatter_recs<false>(rec, r0, r1, G0, N, oy, f0, f1);
-#endif
-      if (__any_sync(0xffffffffu, over)) {   // wide bands (e.g. prior draws): re-walk, scatter the rest
-        int m0 = 0, m1 = 0, dd = 0;
-        float Bd = 0.f, s = ws.s0, za = ws.s0 * dz;
-        for (int k = ws.k; k < ws.kend; k++) {
-          const int2 w = __ldg(a.trav + k);
-          const float s1 = __int_as_float(w.y);
-          const float zb = s1 * dz, Ls = s1 - s;
-          if (over) {
-            const unsigned off = cell_off32(w.x);
-            bool bl0, bl1, st0, st1;
-            classify2(za, zb, __ldg(CL + (lb + off)), bl0, bl1, st0, st1);
-            const float4 cg = __ldg(a.trav_geo + k);
-            const float2 km = __ldg(a.trav_km + k);
-            if (n0 > RCAP && st0)
-              cl_solve<0, true>(CL, lb + n32 + off, oy, cg, km, za, Ls, dz, 0u, Bd, m0, dd, nullptr, G0 + off, f0);
-            if (n1 > RCAP && st1)
-              cl_solve<1, true>(CL, lb + 2 * n32 + off, oy, cg, km, za, Ls, dz, 0u, Bd, m1, dd, nullptr, G0 + N * 32 + off, f1);
-          }
-          if (s1 >= s_hi) break;
-          s = s1;
-          za = zb;
-        }
-      }
-    } else if (act && !defer) {
-      const int64_t o = (int64_t)c * a.R + __ldg(a.perm + rr);
-      a.Lout[3 * o + 0] = B0;
-      a.Lout[3 * o + 1] = B1 - B0;
-      a.Lout[3 * o + 2] = s_exit - B1;
-      a.Oout[o] = a.tc.k0 * B0 + a.tc.k1 * B1 + a.obase[rr];
-    }
-  }
-  if (MODE == TRACE_LL && act) {
-    atomicAdd(a.ll + c, llq);
-#if MT_CACC
-    macc *G0 = a.G + (size_t)grp * 2 * N * 32 + lane;
-    acc_flush(ca0, G0, oy);
-    acc_flush(ca1, G0 + N * 32, oy);
-#endif
   }
 }
 
@@ -1109,13 +757,13 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_v0(TraceArgs a
   if (!act) bd = make_float4(-3.0e38f, -3.0e38f, -3.0e38f, -3.0e38f);
   const int oy = ny * 32;
   const unsigned gbase = (unsigned)grp * 2 * N * 32 + lane;   // this lane's column of the group tile
-  const float2 *__restrict__ H2g = reinterpret_cast<const float2 *>(a.cl) + (size_t)grp * 3 * N * 32 + (size_t)N * 32;
+  const float2 *__restrict__ H2g = reinterpret_cast<const float2 *>(a.cl) + (size_t)grp * 2 * N * 32;
 #if V0_LAUNDER
   // opaque copy: otherwise the compiler rematerialises this base from CTAID and the kernel
   // parameters at every corner load (12 uniform-datapath instructions per surface-cell)
   asm volatile("mov.b64 %0, %0;" : "+l"(H2g));
 #endif
-  const float2 *__restrict__ H2g1 = H2g + (size_t)N * 32;   // warp-uniform bases (arena slots 1, 2)
+  const float2 *__restrict__ H2g1 = H2g + (size_t)N * 32;   // warp-uniform bases of the two surfaces
   macc llq = 0;
 
   const int r_begin = chunk * (int)a.rays_per_block;
@@ -1847,7 +1495,7 @@ cudaError_t build_traversal(mt_problem *p) {
   cudaError_t e = cudaMalloc(&d_cnt, sizeof(int32_t) * p->R);
   if (e != cudaSuccess) return e;
   unsigned nb = (unsigned)((p->R + 127) / 128);
-  k_build_trav<<<nb, 128>>>(a, nullptr, d_cnt, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+  k_build_trav<<<nb, 128>>>(a, nullptr, d_cnt, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
   std::vector<int32_t> cnt(p->R);
   e = cudaMemcpy(cnt.data(), d_cnt, sizeof(int32_t) * p->R, cudaMemcpyDeviceToHost);
   cudaFree(d_cnt);
@@ -1859,7 +1507,6 @@ cudaError_t build_traversal(mt_problem *p) {
     if (tot >= (int64_t)1 << 31) return cudaErrorInvalidValue;   // > 2^31 stored cells
     off[q + 1] = (int32_t)tot;
     ovf[q + 1] = ovf[q] + (cnt[q] > 64 ? (cnt[q] - 64 + 15) / 16 : 0);   // step-code words past 64 cells
-    if (cnt[q] > 255) return cudaErrorInvalidValue;   // band-entry table entries are bytes
   }
   p->trav_cells = tot;
   e = cudaMalloc(&p->d_trav_off, sizeof(int32_t) * (p->R + 1));
@@ -1870,18 +1517,6 @@ cudaError_t build_traversal(mt_problem *p) {
   if (e == cudaSuccess) e = cudaMalloc(&p->d_rl_head, sizeof(int2) * p->R);
   if (e == cudaSuccess) e = cudaMalloc(&p->d_rl_code, sizeof(uint4) * p->R);
   if (e == cudaSuccess) e = cudaMalloc(&p->d_rl_ovf, sizeof(uint32_t) * (ovf[p->R] > 0 ? ovf[p->R] : 1));
-  if (e == cudaSuccess) e = cudaMalloc(&p->d_tab, (size_t)MT_TABQ * p->R);
-  if (e == cudaSuccess) e = cudaMalloc(&p->d_ray_c, sizeof(float4) * p->R);
-  if (e == cudaSuccess) {   // chain-lanes ray record {d_z, 1/d_z, s_exit, first stored cell}
-    std::vector<float4> rc(p->R);
-    for (int64_t q = 0; q < p->R; q++) {
-      const float4 b = p->h_rb[q];
-      float kb;
-      memcpy(&kb, &off[q], sizeof(float));   // first stored cell, as int bits
-      rc[q] = make_float4(b.x, (float)(1.0 / (double)b.x), b.y, kb);
-    }
-    e = cudaMemcpy(p->d_ray_c, rc.data(), sizeof(float4) * p->R, cudaMemcpyHostToDevice);
-  }
   int32_t *d_ovfoff = nullptr;
   if (e == cudaSuccess) e = cudaMalloc(&d_ovfoff, sizeof(int32_t) * (p->R + 1));
   if (e == cudaSuccess) e = cudaMemcpy(d_ovfoff, ovf.data(), sizeof(int32_t) * (p->R + 1), cudaMemcpyHostToDevice);
@@ -1895,7 +1530,7 @@ cudaError_t build_traversal(mt_problem *p) {
   a.trav_km = p->d_trav_km;
   if (e == cudaSuccess)
     k_build_trav<<<nb, 128>>>(a, p->d_trav_off, nullptr, p->d_trav, p->d_trav_geo, p->d_trav_km, p->d_rl_head,
-                              p->d_rl_code, p->d_rl_ovf, d_ovfoff, p->d_tab);
+                              p->d_rl_code, p->d_rl_ovf, d_ovfoff);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   cudaFree(d_ovfoff);
@@ -1941,14 +1576,6 @@ static cudaError_t launch_c2(const TraceArgs &a, dim3 grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int MODE>
-static cudaError_t launch_cl(const TraceArgs &a, dim3 grid, size_t smem, cudaStream_t s) {
-  static size_t done[16] = {0};
-  cudaError_t e = set_smem(k_trace_cl<MODE>, smem, done);
-  if (e != cudaSuccess) return e;
-  k_trace_cl<MODE><<<grid, MT_THREADS, smem, s>>>(a);
-  return cudaGetLastError();
-}
 
 template <int MODE, int NY>
 static cudaError_t launch_rl(const TraceArgs &a, const float *Hc, dim3 grid, size_t smem, cudaStream_t s) {
@@ -1998,15 +1625,12 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
       k_cell_prep2<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(H, reinterpret_cast<float4 *>(p->d_cl), C, p->ny,
                                                              p->N, n);
       p->all_launches++;
-    } else {   // per-(chain, cell) bounds and bilinear coefficients
-      const int64_t n = (int64_t)groups * p->N * 32;
-      k_cell_prep<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(H, p->d_cl, C, p->nx, p->ny, p->N, n);
+    } else {   // paired heights (H(i,j), H(i,j+1))
+      const int64_t n = (int64_t)groups * 2 * p->N * 32;
+      k_cell_prep<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(H, reinterpret_cast<float2 *>(p->d_cl), p->ny, n);
       p->all_launches++;
     }
     a.cl = p->d_cl;
-    a.ray_c = p->d_ray_c;
-    a.tab = p->d_tab;
-    a.tab_scale = (float)MT_TABQ / p->z_top;
     // ray chunks of <= 512 Morton-ordered rays per block (compact, L1-friendly regions, many
     // waves for load balance).  The shape depends on R only, never on C, so a chain's
     // result is bit-identical whatever the chain count per GPU (R30, chain sharding).
@@ -2019,11 +1643,9 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
       dim3 grid2((unsigned)S, (unsigned)((C + 63) / 64));
       if (grid2.x % C2_TILE) grid2.x += C2_TILE - grid2.x % C2_TILE;   // whole tiles (extra chunks are empty)
       e = mode == TRACE_LL ? launch_c2<TRACE_LL>(a, grid2, s) : launch_c2<TRACE_PATH>(a, grid2, s);
-    } else if (p->cl_v <= 0)
+    } else {
       e = mode == TRACE_LL ? launch_v0_ny<TRACE_LL>(a, p->ny, grid, s) : launch_v0_ny<TRACE_PATH>(a, p->ny, grid, s);
-    else
-      e = mode == TRACE_LL ? launch_cl<TRACE_LL>(a, grid, (size_t)16 * 2 * RCAP * MT_THREADS, s)
-                           : launch_cl<TRACE_PATH>(a, grid, (size_t)16 * 2 * RCAP * MT_THREADS, s);
+    }
     if (rec) cudaEventRecord(p->ev_m[p->n_rec], s);
     if (e == cudaSuccess) {   // deferred pairs (ill-conditioned or > RCAP crossings)
       if (mode == TRACE_LL) k_trace_defer<TRACE_LL, DEFER_DG><<<2 * p->num_sms, MT_THREADS, 0, s>>>(a);
