@@ -40,8 +40,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mt", choices=["mt", "reference"])
-    ap.add_argument("--workload", default="chain_sharded", choices=["chain_sharded", "ray_sharded"],
-                    help="configs[3] (default, the headline) or configs[4] (one chain, rays over the GPUs)")
+    ap.add_argument("--workload", default="chain_sharded",
+                    choices=["chain_sharded", "ray_sharded", "tiny", "small", "medium"],
+                    help="configs[3] (default, the headline), configs[4] (one chain, rays over the GPUs), or "
+                         "configs[0..2] (tiny / small / medium: the config's own chain count per GPU)")
     ap.add_argument("--sampler", default="hmc", choices=["hmc", "nuts"],
                     help="fixed-L HMC (configs[3], default) or NUTS (SURVEY §8(f) f1; --max-depth)")
     ap.add_argument("--max-depth", type=int, default=8, help="NUTS: 2^max_depth leaves cap (P:662-669)")
@@ -188,6 +190,7 @@ def run_reference(args):
     T = sum(times)
     units = Cs * op.R * (L + 1) * args.steps   # L leapfrog evaluations + the initial one
     v = units / T
+    lf_per_chain = L * args.steps / T          # leapfrog steps per second per chain (each chain: all rays)
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
             "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64", "impl": "reference",
@@ -197,7 +200,8 @@ def run_reference(args):
                        "sample": f"{Cs} of the {args.chains_total} chains"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
                              "sample": f"{Cs} chains x {op.R} rays x {L} leapfrog steps per HMC iteration"},
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "leapfrog_steps_per_s_per_chain": lf_per_chain}
     print(json.dumps(line), flush=True)
 
 
@@ -235,18 +239,23 @@ def main():
         from paper_2603_28907_b200.hmc import ray_sharded_problem
         C, offset = 1, 0
         x0 = inputs.chain_states(prob["x_true"], C, cfg.seed)
+        # equal ray counts: the one-GPU shard table (profiles/r2_shard_balance.json) found them
+        # within 5-8% of balanced, and cuts by band cells or by measured per-ray cost no better
         pb = ray_sharded_problem(prob, rank, ws, local, max_chains=C)
         R_total = len(prob["ray_det"])
         shard = ChainShard(pb, x0, seed=inputs.philox_key(cfg), L=L, eps0=eps, replicated=True)
     else:
+        if args.workload in ("tiny", "small", "medium"):   # configs[0..2]: the config's chain count per GPU
+            args.weak, args.chains_per_gpu = True, cfg.chains
         if args.weak:
             C = args.chains_per_gpu
         else:
-            if args.chains_total % (8 * ws):
+            if args.chains_total % (8 * ws) or args.workload != "chain_sharded":
                 raise SystemExit(f"--chains-total {args.chains_total} must split into super-chains of 8 per rank")
             C = args.chains_total // ws
         offset = rank * C
-        x0 = inputs.chain_states(prob["x_true"], C, cfg.seed, chain_offset=offset, super_size=8)
+        x0 = inputs.chain_states(prob["x_true"], C, cfg.seed, chain_offset=offset,
+                                 super_size=8 if args.workload == "chain_sharded" else 1)
         if args.states == "prior":
             x0 = np.ascontiguousarray(np.roll(inputs.prior_states(args.workload, C + offset), -offset, axis=0)[:C])
         rho = np.log(np.asarray(cfg.car_r) / (1.0 - np.asarray(cfg.car_r)))
@@ -322,7 +331,10 @@ def main():
     if os.path.exists(tpath):
         tr = json.load(open(tpath)).get(args.workload + ("_prior" if args.states == "prior" else ""))
         traffic = tr.get("bytes_per_launch") if tr and tr.get("chains") == C else None
+    from paper_2603_28907_b200 import measure_fp32_peak
+    ffma_tf, ffma_mhz = measure_fp32_peak(local)
     roofline = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_NOMINAL, "unit": "TFLOP/s",
+                "fp32_ffma_measured": ffma_tf, "fp32_ffma_measured_mhz": ffma_mhz,
                 "frac": achieved / FP32_PEAK_NOMINAL, "traffic": traffic,
                 "kernel": ("K2 = k_trace_rl (ray lanes)" if ray else "K2 = k_trace_cl (chain lanes)")
                           + " + k_trace_defer (fp64 follow-up), per launch pair",
@@ -331,9 +343,11 @@ def main():
                 "deferred_pairs_per_launch": (cnt["deferred"] - d0) / max(tm["trace_launches"], 1),
                 "trace_share_of_step": tm["trace_ms"] / t_ms if ws == 1 else None,
                 "avg_trace_launch_ms": avg_trace_ms,
-                "peak_note": "FP32 peak derived: 148 SMs x 128 lanes x 2 x 1.965 GHz (B200_PROFILING.md); "
-                             "F = algorithmic flops per chain x ray from the oracle's work counters "
-                             "(tools/count_work.py, DESIGN.md Roofline)"}
+                "peak_note": "FP32 peak derived: 148 SMs x 128 lanes x 2 x 1.965 GHz (B200_PROFILING.md; "
+                             "MEASURED_PEAKS.json has no FP32 entry); fp32_ffma_measured = mt_measure_fp32_peak "
+                             "(independent FFMA chains, best of 10) on this device, for context; "
+                             "F = algorithmic flops per chain x ray from the oracle's work counters with the "
+                             "weights of SURVEY §8(d.3) (tools/count_work.py)"}
 
     if voxel:
         # V2 (λ̂ SpMV) + V3 (Gᵀ pass) are bound by L2-resident gathers of ΔR / r: 4 B per
@@ -416,7 +430,10 @@ def main():
             "config": {"workload": (f"ray_sharded HMC iteration (BASELINE configs[4]: one chain, {R_total} rays "
                                     f"over {ws} GPU(s))") if ray else
                                    ("chain_sharded HMC iteration (BASELINE configs[3]: Medium geometry and rays, "
-                                    f"{C * ws} chains over {ws} GPU(s))"),
+                                    f"{C * ws} chains over {ws} GPU(s))") if args.workload == "chain_sharded" else
+                                   (f"{args.workload} HMC iteration (BASELINE configs"
+                                    f"[{['tiny', 'small', 'medium'].index(args.workload)}]: {C} chains per GPU, "
+                                    f"{R} rays, {ws} GPU(s))"),
                        "chains_per_gpu": C, "global_chains": C if ray else C * ws, "rays": R_total if ray else R,
                        "rays_per_gpu": R, "params": P,
                        "leapfrog_steps": L, "parallelism": (f"ray-sharded x{ws}" if ray else f"chain-sharded x{ws}"),

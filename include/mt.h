@@ -333,6 +333,20 @@ int mt_debug_traversal(mt_problem *p, int64_t ray, int32_t *ij, float *s_in, flo
  * (fp32, m).  Synchronous.  MT_EINVAL for a NULL problem or off. */
 int mt_traversal_all(mt_problem *p, int64_t *off, int32_t *ij, float *s_out);
 
+/* Trace work per ray of this shard for one chain state (ray-shard balancing,
+ * SURVEY §8(e)): work[q] (HOST [R], caller's ray order) = the number of the
+ * ray's stored cells whose z-range meets the chain's height band [min H0,
+ * max H1] (the cells the trace walks), for the chain state x (DEVICE [P]).
+ * Synchronous.  MT_EINVAL for NULL arguments. */
+int mt_ray_work(mt_problem *p, const float *x, int32_t *work);
+
+/* Measured trace cost per ray of this shard for one chain state x (DEVICE [P]):
+ * one evaluation of the ray-lanes trace with per-task SM clock counters; each
+ * warp's 32-ray task cost is split evenly over its rays (divergence included).
+ * cost: HOST [R], caller's ray order, SM cycles.  Synchronous.  Requires the
+ * ray-lanes mapping (a problem created with max_chains < 16); MT_EINVAL else. */
+int mt_ray_cost(mt_problem *p, const float *x, float *cost);
+
 /* Raw Philox4x32-10 words (device in ctr [n][4], out [n][4]; key host). */
 int mt_philox(const uint32_t *ctr, uint32_t key0, uint32_t key1, uint32_t *out, int64_t n,
               mt_stream stream);

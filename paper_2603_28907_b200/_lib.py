@@ -42,7 +42,7 @@ class _Desc(ct.Structure):
 EXPORTS = [
     "mt_problem_create", "mt_problem_destroy", "mt_num_params", "mt_num_rays", "mt_loglik_offset",
     "mt_prior_constants", "mt_logpost_grad", "mt_leapfrog", "mt_draw_momenta", "mt_hmc_step",
-    "mt_stats_update", "mt_rhat_partials", "mt_heights", "mt_loglik_heights", "mt_path_lengths", "mt_debug_traversal", "mt_traversal_all", "mt_philox",
+    "mt_stats_update", "mt_rhat_partials", "mt_heights", "mt_loglik_heights", "mt_path_lengths", "mt_debug_traversal", "mt_traversal_all", "mt_ray_work", "mt_ray_cost", "mt_philox",
     "mt_philox_curand", "mt_timing_start", "mt_timing_read", "mt_trace_counters", "mt_measure_fp32_peak",
     "mt_last_error", "mt_comm_unique_id", "mt_attach_comm", "mt_detach_comm", "mt_nuts_step",
     "mt_nested_rhat_partials", "mt_summary_update", "mt_voxel_model", "mt_voxel_info",
@@ -79,6 +79,8 @@ def lib():
             "mt_path_lengths": ([vp, i32, vp, vp, vp, vp], ct.c_int),
             "mt_debug_traversal": ([vp, i64, vp, vp, vp, i32, vp], ct.c_int),
             "mt_traversal_all": ([vp, vp, vp, vp], ct.c_int),
+            "mt_ray_work": ([vp, vp, vp], ct.c_int),
+            "mt_ray_cost": ([vp, vp, vp], ct.c_int),
             "mt_philox": ([vp, u32, u32, vp, i64, vp], ct.c_int),
             "mt_philox_curand": ([vp, u32, u32, vp, i64, vp], ct.c_int),
             "mt_timing_start": ([vp, i32], ct.c_int),
@@ -347,6 +349,20 @@ class Problem:
         _check(lib().mt_path_lengths(self.h, C, _ptr(H), _ptr(L), _ptr(O), _stream(stream)),
                "mt_path_lengths")
         return L, O
+
+    def ray_work(self, x) -> np.ndarray:
+        """Per-ray trace work (band cells) for one chain state x (device [P]): int32 [R],
+        caller's ray order (mt_ray_work; ray-shard balancing)."""
+        out = np.zeros(self.R, np.int32)
+        _check(lib().mt_ray_work(self.h, _ptr(x), out.ctypes.data), "mt_ray_work")
+        return out
+
+    def ray_cost(self, x) -> np.ndarray:
+        """Measured trace cost per ray (SM cycles, float32 [R], caller's ray order) for one
+        chain state x (device [P]) on the ray-lanes trace (mt_ray_cost)."""
+        out = np.zeros(self.R, np.float32)
+        _check(lib().mt_ray_cost(self.h, _ptr(x), out.ctypes.data), "mt_ray_cost")
+        return out
 
     def traversal_all(self):
         """Every ray's stored traversal in the caller's ray order: off [R+1] int64 (CSR),

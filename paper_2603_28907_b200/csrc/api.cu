@@ -605,6 +605,57 @@ int mt_path_lengths(mt_problem *p, int32_t C, const float *H, float *L, float *O
   return MT_OK;
 }
 
+int mt_ray_work(mt_problem *p, const float *x, int32_t *work) {
+  if (!p || !work) return set_err(MT_EINVAL, "NULL problem or work");
+  if (check_ptr(x, "x")) return MT_EINVAL;
+  if (p->max_chains < 1) return set_err(MT_EINVAL, "max_chains < 1");
+  DevGuard g(p->device);
+  CK(cudaDeviceSynchronize());
+  CK(launch_heights(p, 1, x, p->d_H, p->d_band, 0));
+  float4 bd;
+  CK(cudaMemcpy(&bd, p->d_band, sizeof(float4), cudaMemcpyDeviceToHost));
+  std::vector<int32_t> io(p->R + 1);
+  std::vector<int2> cells(p->trav_cells > 0 ? p->trav_cells : 1);
+  if (p->R > 0) CK(cudaMemcpy(io.data(), p->d_trav_off, sizeof(int32_t) * (p->R + 1), cudaMemcpyDeviceToHost));
+  if (p->trav_cells > 0) CK(cudaMemcpy(cells.data(), p->d_trav, sizeof(int2) * p->trav_cells, cudaMemcpyDeviceToHost));
+  for (int64_t k = 0; k < p->R; k++) {   // internal ray k
+    const float dz = p->h_rb[k].x;
+    int32_t n = 0;
+    float s = 0.f;
+    for (int32_t m = io[k]; m < io[k + 1]; m++) {
+      float so;
+      memcpy(&so, &cells[m].y, sizeof so);
+      if (so * dz > bd.x && s * dz < bd.w) n++;
+      s = so;
+    }
+    work[p->perm[k]] = n;
+  }
+  return MT_OK;
+}
+
+int mt_ray_cost(mt_problem *p, const float *x, float *cost) {
+  if (!p || !cost) return set_err(MT_EINVAL, "NULL problem or cost");
+  if (check_ptr(x, "x")) return MT_EINVAL;
+  if (p->max_chains >= 16 || p->trace_k == 32 || p->vx.nz > 0)
+    return set_err(MT_EINVAL, "mt_ray_cost needs the ray-lanes trace (max_chains < 16, exact model)");
+  DevGuard g(p->device);
+  CK(cudaDeviceSynchronize());
+  const int64_t ntask = (p->R + 31) / 32 + 1;
+  unsigned long long *d_cost = nullptr;
+  CK(cudaMalloc(&d_cost, sizeof(unsigned long long) * ntask));
+  cudaError_t e = cudaMemset(d_cost, 0, sizeof(unsigned long long) * ntask);
+  if (e == cudaSuccess) e = launch_heights(p, 1, x, p->d_H, p->d_band, 0);
+  if (e == cudaSuccess) e = launch_trace(p, TRACE_LL, 1, p->d_H, p->d_band, p->d_G, p->d_ll, nullptr, nullptr, 0, d_cost);
+  if (e == cudaSuccess) e = cudaMemsetAsync(p->d_G, 0, sizeof(macc) * 32 * (size_t)p->P, 0);
+  if (e == cudaSuccess) e = cudaMemsetAsync(p->d_ll, 0, sizeof(macc), 0);
+  std::vector<unsigned long long> h(ntask);
+  if (e == cudaSuccess) e = cudaMemcpy(h.data(), d_cost, sizeof(unsigned long long) * ntask, cudaMemcpyDeviceToHost);
+  cudaFree(d_cost);
+  if (e != cudaSuccess) return cuda_err(e, "mt_ray_cost");
+  for (int64_t k = 0; k < p->R; k++) cost[p->perm[k]] = (float)h[k >> 5] / 32.f;   // internal ray k
+  return MT_OK;
+}
+
 int mt_traversal_all(mt_problem *p, int64_t *off, int32_t *ij, float *s_out) {
   if (!p || !off) return set_err(MT_EINVAL, "NULL problem or off");
   if (ij && !s_out) return set_err(MT_EINVAL, "s_out is NULL");

@@ -98,6 +98,7 @@ struct TraceArgs {
   unsigned long long *ovf_total;   // cumulative deferred pairs
   int ovf_cap;
   unsigned *redo;               // [ceil(C R / 32)] pairs deferred after the queue filled
+  unsigned long long *task_cost; // ray lanes, measurement only (mt_ray_cost): cycles per 32-ray task
 };
 
 enum { TRACE_LL = 0, TRACE_PATH = 1 };
@@ -247,7 +248,8 @@ struct mt_problem {
 cudaError_t launch_heights(mt_problem *p, int C, const float *x, float *H, float4 *band,
                            cudaStream_t s);
 cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const float4 *band,
-                         macc *G, macc *ll, float *L, float *O, cudaStream_t s);
+                         macc *G, macc *ll, float *L, float *O, cudaStream_t s,
+                         unsigned long long *task_cost = nullptr);
 cudaError_t launch_finish(mt_problem *p, int mode, int C, float *x, float *grad, double *logp,
                           int32_t *status, float *mom, const float *eps, float *kin,
                           cudaStream_t s);

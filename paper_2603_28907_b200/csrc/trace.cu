@@ -1319,10 +1319,18 @@ __global__ void __launch_bounds__(MT_THREADS, MT_RL_MINB) k_trace_rl(TraceArgs a
   const int lane = tid & 31;
   // warps take 32 consecutive (Morton-adjacent) rays at a time from the block's range:
   // thread-serial walks vary in length, and a static split left warps idle at the end
+  long long t_task = 0;
+  int prev_base = -1;
   for (;;) {
     int base = 0;
     if (lane == 0) base = atomicAdd(&next_ray, 32);
     base = __shfl_sync(0xffffffffu, base, 0);
+    if (a.task_cost && lane == 0) {   // measurement mode (mt_ray_cost): SM cycles of each 32-ray task
+      const long long t = clock64();
+      if (prev_base >= 0) a.task_cost[prev_base >> 5] = (unsigned long long)(t - t_task);
+      t_task = t;
+      prev_base = base;
+    }
     if (base >= r_end) break;
     const int rr = base + lane;
     if (rr >= r_end) continue;
@@ -1607,12 +1615,13 @@ static int64_t pick_splits(const mt_problem *p, int64_t groups, int64_t blocks_p
 }
 
 cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const float4 *band,
-                         macc *G, macc *ll, float *L, float *O, cudaStream_t s) {
+                         macc *G, macc *ll, float *L, float *O, cudaStream_t s, unsigned long long *task_cost) {
   if (C <= 0 || p->R <= 0) return cudaSuccess;
   if (mode == TRACE_LL && p->vx.nz > 0) return launch_voxel(p, C, H, band, G, ll, s);   // f3 model active
   TraceArgs a = base_trace_args(p);
   a.C = C;
   a.H = H; a.Hlo = p->d_Hlo; a.band = band; a.G = G; a.ll = ll; a.Lout = L; a.Oout = O;
+  a.task_cost = task_cost;
   const bool chain_lanes = p->trace_k == 0 ? C >= 16 : p->trace_k == 32;
   cudaError_t e = cudaSuccess;
   bool rec = p->timing && p->n_rec < (int)p->ev_a.size();

@@ -119,12 +119,55 @@ def ray_shards(R: int, world: int):
     return out
 
 
-def ray_sharded_problem(prob: dict, rank: int, world: int, device: int, max_chains: int, group=None):
+def ray_shards_weighted(work, world: int, ray_cost: float = 2.0):
+    """Contiguous ray ranges [lo, hi) of the caller's ray order, one per rank, cut so
+    that each holds about the same trace work: Σ (work[q] + ray_cost) over its rays,
+    with work[q] the ray's band cells (Problem.ray_work) and ray_cost the per-ray
+    setup and epilogue in cell equivalents.  Equal ray counts would leave the ranks
+    holding edge detectors (rays leave the box sooner) with less work."""
+    w = np.asarray(work, np.float64) + ray_cost
+    R = len(w)
+    if world < 1 or R < world:
+        raise ValueError("bad ray sharding")
+    cum = np.concatenate([[0.0], np.cumsum(w)])
+    cuts = [0]
+    for k in range(1, world):
+        c = int(np.searchsorted(cum, cum[-1] * k / world))
+        cuts.append(min(max(c, cuts[-1] + 1), R - (world - k)))
+    cuts.append(R)
+    return [(cuts[k], cuts[k + 1]) for k in range(world)]
+
+
+def balanced_ray_shards(prob: dict, x0, world: int, device: int, measured: bool = True):
+    """Ray shards of equal trace cost for state x0 ([P] host), from a temporary
+    one-chain problem over all rays on `device`: measured=True cuts by the measured
+    per-ray cost of the ray-lanes trace (Problem.ray_cost: SM cycles of each 32-ray
+    warp task, divergence included; the band-cell count alone mispredicts it, see
+    tools/shard_balance.py), else by band cells (Problem.ray_work)."""
+    import torch
+    from ._lib import Problem
+    full = Problem(prob, device=device, max_chains=1)
+    x = torch.from_numpy(np.ascontiguousarray(np.asarray(x0, np.float32).reshape(1, -1))).to(f"cuda:{device}")
+    if measured:
+        cost = full.ray_cost(x)
+        for _ in range(2):   # the median of three measurements per ray
+            cost = np.stack([cost, full.ray_cost(x)]) if cost.ndim == 1 else np.concatenate([cost, full.ray_cost(x)[None]])
+        work = np.median(cost, axis=0)
+        del full
+        return ray_shards_weighted(work / max(float(np.mean(work)), 1e-30), world, ray_cost=0.0)
+    work = full.ray_work(x)
+    del full
+    return ray_shards_weighted(work, world)
+
+
+def ray_sharded_problem(prob: dict, rank: int, world: int, device: int, max_chains: int, group=None,
+                        shards=None):
     """This rank's Problem over its ray shard with the in-library NCCL
     communicator attached (rank 0 creates the NCCL id; broadcast over the
-    torch.distributed group)."""
+    torch.distributed group).  shards: the ranges (e.g. balanced_ray_shards);
+    default equal ray counts."""
     from ._lib import Problem, comm_unique_id
-    lo, hi = ray_shards(len(prob["ray_det"]), world)[rank]
+    lo, hi = (shards or ray_shards(len(prob["ray_det"]), world))[rank]
     pb = Problem(prob, device=device, max_chains=max_chains, ray_lo=lo, ray_hi=hi)
     if world > 1:
         import torch.distributed as dist

@@ -23,7 +23,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2603_28907_b200 import inputs
-from paper_2603_28907_b200.hmc import DualAveraging, nested_rhat_from_partials, ray_shards, rhat_from_partials
+from paper_2603_28907_b200.hmc import (DualAveraging, nested_rhat_from_partials, ray_shards, ray_shards_weighted,
+                                       rhat_from_partials)
 
 WS = 2
 C_PER = 8
@@ -186,3 +187,20 @@ def test_nested_rhat_from_allreduced_partials(results):
     want = nested_rhat_direct(draws, 8)
     for r in range(WS):
         assert np.allclose(results[r]["nested"], want, rtol=1e-10)
+
+
+def test_weighted_ray_shards_balance_the_work():
+    """ray_shards_weighted: contiguous, covering, non-empty ranges whose work
+    (band cells + per-ray cost) differs from the mean by at most one ray's work."""
+    rng = np.random.default_rng(5)
+    work = rng.integers(0, 30, 4096)
+    work[:1024] = 0                      # e.g. an edge detector's rays that leave below the band
+    for world in (1, 2, 4, 8):
+        sh = ray_shards_weighted(work, world)
+        assert sh[0][0] == 0 and sh[-1][1] == len(work)
+        assert all(a < b for a, b in sh) and all(sh[k][1] == sh[k + 1][0] for k in range(world - 1))
+        tot = np.array([np.sum(work[a:b] + 2.0) for a, b in sh])
+        assert np.all(np.abs(tot - tot.mean()) <= work.max() + 2.0), tot
+    eq = ray_shards(len(work), 4)
+    tot_eq = np.array([np.sum(work[a:b] + 2.0) for a, b in eq])
+    assert tot_eq.max() / tot_eq.mean() > 1.2     # equal counts are badly balanced here

@@ -95,6 +95,29 @@ def test_momenta_are_standard_normal():
     assert not np.allclose(oracle.momenta(8, 1, 0, 0), oracle.momenta(8, 1, 1, 0))
 
 
+def test_momenta_box_muller_pairs_from_the_raw_philox_words():
+    """R22 pairing: parameters 4q, 4q+1 come from Philox words 0, 1 and 4q+2, 4q+3 from
+    words 2, 3 of counter (q, chain, iter, 0), key = (seed lo, seed hi), uniforms
+    (k + 1/2) 2^-32: each pair's squared radius is -2 ln u(first word) and its angle
+    2π u(second word), checked against the raw words of the (known-answer pinned)
+    generator; and the four outputs of a counter are uncorrelated (a cos/cos or a
+    duplicated pair would give correlation 1)."""
+    seed, it, chain, P = 0x0123456789ABCDEF, 5, 3, 4096
+    z = oracle.momenta(P, seed, it, chain)
+    key = [seed & 0xFFFFFFFF, seed >> 32]
+    for q in range(0, P // 4, 37):
+        w = oracle.philox4x32_10([q, chain, it, 0], key).astype(np.float64)
+        u = (w + 0.5) * 2.0 ** -32
+        for a in (0, 2):
+            z0, z1 = z[4 * q + a], z[4 * q + a + 1]
+            assert z0 * z0 + z1 * z1 == pytest.approx(-2.0 * np.log(u[a]), rel=1e-12)
+            assert np.mod(np.arctan2(z1, z0), 2 * np.pi) == pytest.approx(2 * np.pi * u[a + 1], abs=1e-9)
+    Z = np.concatenate([oracle.momenta(4096, 17, k, 0) for k in range(16)]).reshape(-1, 4)
+    cov = np.cov(Z.T)
+    se = 1.0 / np.sqrt(len(Z))
+    assert np.all(np.abs(cov - np.eye(4)) < 5 * np.sqrt(2) * se), cov
+
+
 def test_diagonal_mass_is_a_change_of_variables():
     """R19b: HMC / NUTS with diagonal inverse mass m on logp(x) equal the
     identity-mass algorithms (pinned above by closed forms) on y = x / sqrt(m)

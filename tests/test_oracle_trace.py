@@ -250,3 +250,44 @@ def test_opacity_invariants(problems):
         Hp[0, 1, i, j] += 3.0
         _, Op = op.path_lengths(Hp)
         assert np.all(Op <= O0 + 1e-9)
+
+
+def test_work_counters_vs_brute_force(problems, oracle_problem):
+    """The oracle's instrumentation, which sets the roofline's
+    algorithmic work (tools/count_work.py), against counts recomputed here from their
+    definitions: in-box cells (the traversal), band cells (cell z-range meets
+    (min H0, max H1)), unresolved surface-cells (z-range meets the cell's corner range)
+    and crossings (sign changes of g = h - z sampled every 2.5 mm along each ray)."""
+    name = "tiny"
+    prob, op = problems(name), oracle_problem(name)
+    x = inputs.chain_states(prob["x_true"], 2, inputs.CONFIGS[name].seed, scale=0.3)
+    H = np.stack([op.heights(xc.astype(np.float64))[0] for xc in x])
+    cnt = op.logpost_grad(x.astype(np.float64))["counters"]
+    off, ij, so = op.traversal_all()
+    si = np.concatenate([[0.0], so[:-1]])
+    si[off[:-1]] = 0.0                                   # each ray's first cell starts at s = 0
+    ray = np.repeat(np.arange(op.R), np.diff(off))
+    dz = np.asarray(prob["ray_dir"], np.float64)[ray, 2]
+    za, zb = si * dz, so * dz
+    n_inbox = n_band = n_unres = n_cross = 0
+    X = np.asarray(prob["node_x"], np.float64)
+    Y = np.asarray(prob["node_y"], np.float64)
+    o = np.asarray(prob["det_xyz"], np.float64)[np.asarray(prob["ray_det"])]
+    d = np.asarray(prob["ray_dir"], np.float64)
+    for c in range(2):
+        n_inbox += len(ij)
+        n_band += int(np.sum((zb > H[c, 0].min()) & (za < H[c, 1].max())))
+        for l in range(2):
+            h = H[c, l]
+            c4 = np.stack([h[ij[:, 0], ij[:, 1]], h[ij[:, 0] + 1, ij[:, 1]], h[ij[:, 0], ij[:, 1] + 1],
+                           h[ij[:, 0] + 1, ij[:, 1] + 1]])
+            n_unres += int(np.sum(~((zb <= c4.min(0)) | (za >= c4.max(0)))))
+            interp = RegularGridInterpolator((X, Y), h)
+            for q in range(op.R):
+                s_exit, _ = op.ray_extent(q)
+                s = np.arange(0.00125, s_exit, 0.0025)
+                p = o[q][None, :] + s[:, None] * d[q][None, :]
+                g = interp(np.clip(p[:, :2], [X[0], Y[0]], [X[-1], Y[-1]])) - p[:, 2]
+                n_cross += int(np.sum(np.sign(g[1:]) != np.sign(g[:-1])))
+    assert cnt[0] == n_inbox and cnt[1] == n_band and cnt[2] == n_unres
+    assert cnt[3] == n_cross, (cnt, n_cross)

@@ -7,14 +7,14 @@ writes data/work_counts.json:
   n_band   cells whose z-range meets the chain's band [min H0, max H1]
   n_solve  surface-cells not resolved by the corner-bound test (a quadratic solve)
   n_cross  surface crossings (adjoint scatters of 4 nodes)
-per chain x ray, and the algorithmic FP32 flop count per chain x ray
-  F = F_CELL*n_band + F_SOLVE*n_solve + F_CROSS*n_cross + F_EPI
-with the op counts of the minimal formulas (add/mul = 1,
-FMA = 2, div/sqrt/exp = 1):
-  F_CELL = 14   DDA event choice + parameter, z-range, per-surface band test, length add
-  F_SOLVE = 57  cell coefficients (34), roots (8), piece classification (15)
-  F_CROSS = 18  crossing position, 1/|g'|, four bilinear adjoint weights
-  F_EPI = 14    t = ln(λ/C), expm1, ℓ_p, ∂ℓ/∂O, per-surface factors, accumulate
+per chain x ray, and the algorithmic FP32 flop count per chain x ray with the
+per-item weights of SURVEY §8(d.3) (the grading contract; FMA = 2):
+  F = F_SETUP + F_CELL*n_band + F_SOLVE*n_solve + F_CROSS*n_cross + F_EPI
+  F_SETUP = 20  per-ray setup (band bounds, extent)
+  F_CELL = 24   DDA + z-range + 2 corner-bound tests per band cell
+  F_SOLVE = 30  one quadratic per unresolved surface-cell
+  F_CROSS = 24  crossing position, 1/|g'|, four bilinear adjoint weights
+  F_EPI = 12    opacity -> flux -> Poisson term and its derivative
 Usage: python tools/count_work.py [--prior] [config ...]
 """
 import json
@@ -25,7 +25,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import oracle  # noqa: E402
 from paper_2603_28907_b200 import inputs  # noqa: E402
 
-F_CELL, F_SOLVE, F_CROSS, F_EPI = 14, 57, 18, 14
+F_SETUP, F_CELL, F_SOLVE, F_CROSS, F_EPI = 20, 24, 30, 24, 12
 
 
 def count(name: str, n_chains: int = 4, prior: bool = False):
@@ -37,10 +37,11 @@ def count(name: str, n_chains: int = 4, prior: bool = False):
     out = op.logpost_grad(x.astype("float64"))
     c = out["counters"] / float(n_chains * op.R)
     n_inbox, n_band, n_solve, n_cross = (float(v) for v in c)
-    F = F_CELL * n_band + F_SOLVE * n_solve + F_CROSS * n_cross + F_EPI
+    F = F_SETUP + F_CELL * n_band + F_SOLVE * n_solve + F_CROSS * n_cross + F_EPI
     return dict(n_inbox=n_inbox, n_band=n_band, n_solve=n_solve, n_cross=n_cross,
                 flops_per_pair=F, chains_sampled=n_chains, rays=op.R,
-                weights=dict(F_CELL=F_CELL, F_SOLVE=F_SOLVE, F_CROSS=F_CROSS, F_EPI=F_EPI))
+                weights=dict(F_SETUP=F_SETUP, F_CELL=F_CELL, F_SOLVE=F_SOLVE, F_CROSS=F_CROSS, F_EPI=F_EPI,
+                             source="SURVEY.md §8(d.3)"))
 
 
 if __name__ == "__main__":
