@@ -206,6 +206,14 @@ int mt_nuts_step(mt_problem *p, int32_t C, float *x, double *logp, float *grad, 
                  int32_t max_depth, uint64_t seed, uint64_t iter, uint64_t chain_offset, float *accept_stat,
                  int32_t *depth, int32_t *n_leaves, int32_t *status, mt_stream stream);
 
+/* Debug / parity record of mt_nuts_step's leaves (f1; the depth-8 replay test):
+ * while set, every leaf evaluation of the following mt_nuts_step calls stores the
+ * leaf state of all C chains at leaf index k = 2^depth - 1 + t (evaluation order;
+ * leaves skipped because every chain had stopped are not written): th [k][C][P]
+ * float, g [k][C][P] float (its gradient), lp [k][C] double (its logp), for
+ * k < max_leaves.  DEVICE buffers, caller-owned; th == NULL switches it off. */
+int mt_nuts_record(mt_problem *p, float *th, float *g, double *lp, int32_t max_leaves);
+
 /* Per-iteration sampler statistics (step-size adaptation and R-hat, P:652-653,
  * P:671-687; readings R20/R21).  Any of the three groups may be skipped by
  * passing NULL:

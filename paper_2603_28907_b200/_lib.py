@@ -42,7 +42,7 @@ class _Desc(ct.Structure):
 EXPORTS = [
     "mt_problem_create", "mt_problem_destroy", "mt_num_params", "mt_num_rays", "mt_loglik_offset",
     "mt_prior_constants", "mt_logpost_grad", "mt_leapfrog", "mt_draw_momenta", "mt_hmc_step",
-    "mt_stats_update", "mt_rhat_partials", "mt_heights", "mt_loglik_heights", "mt_path_lengths", "mt_debug_traversal", "mt_traversal_all", "mt_ray_work", "mt_ray_cost", "mt_philox",
+    "mt_stats_update", "mt_rhat_partials", "mt_heights", "mt_loglik_heights", "mt_path_lengths", "mt_debug_traversal", "mt_traversal_all", "mt_ray_work", "mt_ray_cost", "mt_nuts_record", "mt_philox",
     "mt_philox_curand", "mt_timing_start", "mt_timing_read", "mt_trace_counters", "mt_measure_fp32_peak",
     "mt_last_error", "mt_comm_unique_id", "mt_attach_comm", "mt_detach_comm", "mt_nuts_step",
     "mt_nested_rhat_partials", "mt_summary_update", "mt_voxel_model", "mt_voxel_info",
@@ -81,6 +81,7 @@ def lib():
             "mt_traversal_all": ([vp, vp, vp, vp], ct.c_int),
             "mt_ray_work": ([vp, vp, vp], ct.c_int),
             "mt_ray_cost": ([vp, vp, vp], ct.c_int),
+            "mt_nuts_record": ([vp, vp, vp, vp, i32], ct.c_int),
             "mt_philox": ([vp, u32, u32, vp, i64, vp], ct.c_int),
             "mt_philox_curand": ([vp, u32, u32, vp, i64, vp], ct.c_int),
             "mt_timing_start": ([vp, i32], ct.c_int),
@@ -356,6 +357,14 @@ class Problem:
         out = np.zeros(self.R, np.int32)
         _check(lib().mt_ray_work(self.h, _ptr(x), out.ctypes.data), "mt_ray_work")
         return out
+
+    def nuts_record(self, th=None, g=None, lp=None):
+        """Record every leaf of the following nuts_step calls into th [K][C][P], g [K][C][P]
+        (float32) and lp [K][C] (float64) device tensors (mt_nuts_record); no args: off."""
+        if th is None:
+            _check(lib().mt_nuts_record(self.h, None, None, None, 0), "mt_nuts_record")
+            return
+        _check(lib().mt_nuts_record(self.h, _ptr(th), _ptr(g), _ptr(lp), th.shape[0]), "mt_nuts_record")
 
     def ray_cost(self, x) -> np.ndarray:
         """Measured trace cost per ray (SM cycles, float32 [R], caller's ray order) for one

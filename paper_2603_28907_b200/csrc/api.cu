@@ -449,6 +449,16 @@ int mt_hmc_step(mt_problem *p, int32_t C, float *x, double *logp, float *grad, c
   return MT_OK;
 }
 
+int mt_nuts_record(mt_problem *p, float *th, float *g, double *lp, int32_t max_leaves) {
+  if (!p) return set_err(MT_EINVAL, "problem is NULL");
+  if (th && (!g || !lp || max_leaves < 0)) return set_err(MT_EINVAL, "bad record buffers");
+  p->nuts_rec_th = th;
+  p->nuts_rec_g = th ? g : nullptr;
+  p->nuts_rec_lp = th ? lp : nullptr;
+  p->nuts_rec_max = th ? max_leaves : 0;
+  return MT_OK;
+}
+
 int mt_nuts_step(mt_problem *p, int32_t C, float *x, double *logp, float *grad, const float *eps,
                  int32_t max_depth, uint64_t seed, uint64_t iter, uint64_t chain_offset, float *accept_stat,
                  int32_t *depth, int32_t *n_leaves, int32_t *status, mt_stream stream) {

@@ -232,6 +232,9 @@ struct mt_problem {
   double *nuts_lp = nullptr;
   NutsChain *nuts_st = nullptr;
   int *nuts_flags = nullptr, *nuts_hflags = nullptr;
+  float *nuts_rec_th = nullptr, *nuts_rec_g = nullptr;   // leaf record (mt_nuts_record)
+  double *nuts_rec_lp = nullptr;
+  int nuts_rec_max = 0;
   // in-library NCCL communicator (ray sharding; comm.cu)
   void *comm = nullptr;
   int comm_rank = 0, comm_world = 1;

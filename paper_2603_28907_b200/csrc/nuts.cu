@@ -352,6 +352,17 @@ cudaError_t run_nuts(mt_problem *p, int C, float *x, double *logp, float *grad, 
           cudaSuccess)
         return e;
       if (p->comm && comm_allreduce_logp_grad(p, C, n.lpw_out, n.gw, s, why) != cudaSuccess) return cudaErrorUnknown;
+      const int leaf = (1 << j) - 1 + t;
+      if (p->nuts_rec_th && leaf < p->nuts_rec_max) {   // debug / parity record of the leaf (mt_nuts_record)
+        const size_t CP = (size_t)C * p->P;
+        if ((e = cudaMemcpyAsync(p->nuts_rec_th + leaf * CP, n.thw, sizeof(float) * CP, cudaMemcpyDeviceToDevice, s)) !=
+                cudaSuccess ||
+            (e = cudaMemcpyAsync(p->nuts_rec_g + leaf * CP, n.gw, sizeof(float) * CP, cudaMemcpyDeviceToDevice, s)) !=
+                cudaSuccess ||
+            (e = cudaMemcpyAsync(p->nuts_rec_lp + (size_t)leaf * C, n.lpw_out, sizeof(double) * C,
+                                 cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+          return e;
+      }
       if ((e = cudaMemsetAsync(p->nuts_flags + 1, 0, sizeof(int), s)) != cudaSuccess) return e;
       k_nuts_leaf<<<C, MT_THREADS, 0, s>>>(a, n, t, seed, iter, chain_offset);
       p->all_launches++;

@@ -900,8 +900,11 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_v0(TraceArgs a
 #ifndef C2_RCAP
 #define C2_RCAP 2
 #endif
+#ifndef C2_THREADS
+#define C2_THREADS 256   // threads per block of k_trace_c2
+#endif
 #ifndef C2_MINB
-#define C2_MINB 4
+#define C2_MINB (1024 / C2_THREADS)
 #endif
 
 __global__ void __launch_bounds__(MT_THREADS) k_cell_prep2(const float *__restrict__ H, float4 *__restrict__ H4, int C,
@@ -946,7 +949,7 @@ __device__ __forceinline__ void c2_cell(float h00, float h01, float h10, float h
         atomicAdd(Gp + oy + 32, q_raw(wb * v));
       }
     } else if (n < C2_RCAP) {
-      rec[(SLOT * C2_RCAP + n) * MT_THREADS] = make_float4(wbase, u, v, ig);
+      rec[(SLOT * C2_RCAP + n) * C2_THREADS] = make_float4(wbase, u, v, ig);
     }
     n++;
   };
@@ -954,8 +957,8 @@ __device__ __forceinline__ void c2_cell(float h00, float h01, float h10, float h
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(MT_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
-  extern __shared__ __align__(16) float4 recs[];   // [chain v][surface l][C2_RCAP][MT_THREADS]
+__global__ void __launch_bounds__(C2_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
+  extern __shared__ __align__(16) float4 recs[];   // [chain v][surface l][C2_RCAP][C2_THREADS]
   int N = a.tc.N, oy = a.tc.ny * 32;
   asm volatile("" : "+r"(N), "+r"(oy));   // keep in registers (no per-use reload / recompute)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -987,7 +990,7 @@ __global__ void __launch_bounds__(MT_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
 
   const int r_begin = chunk * (int)a.rays_per_block;
   const int r_end = min((int)a.R, r_begin + (int)a.rays_per_block);
-  for (int rr = r_begin + warp; rr < r_end; rr += MT_THREADS / 32) {
+  for (int rr = r_begin + warp; rr < r_end; rr += C2_THREADS / 32) {
     const float2 rb0 = __ldg(reinterpret_cast<const float2 *>(a.ray_b + rr));
     const float dz = rb0.x, s_exit = rb0.y;
     const float s_lo = fminf(__fdividef(zlo, dz) * (1.f - 1e-6f), s_exit);
@@ -1017,8 +1020,8 @@ __global__ void __launch_bounds__(MT_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
           if (za >= zmax) continue;                            // above both chains' highest node
           const float4 *p = H4 + (size_t)l * N * 32 + off;
           const float4 r0 = __ldg(p), r1 = __ldg(p + oy);
-          if (actA) c2_cell<0, false>(r0.x, r0.y, r1.x, r1.y, cg, km, za, zb, Ls, dz, wb, BA, nA, dA, rec + l * C2_RCAP * MT_THREADS, nullptr, 0, 0.f);
-          if (actB) c2_cell<0, false>(r0.z, r0.w, r1.z, r1.w, cg, km, za, zb, Ls, dz, wb, BB, nB, dB, rec + (2 + l) * C2_RCAP * MT_THREADS, nullptr, 0, 0.f);
+          if (actA) c2_cell<0, false>(r0.x, r0.y, r1.x, r1.y, cg, km, za, zb, Ls, dz, wb, BA, nA, dA, rec + l * C2_RCAP * C2_THREADS, nullptr, 0, 0.f);
+          if (actB) c2_cell<0, false>(r0.z, r0.w, r1.z, r1.w, cg, km, za, zb, Ls, dz, wb, BB, nB, dB, rec + (2 + l) * C2_RCAP * C2_THREADS, nullptr, 0, 0.f);
         }
         if (s1 >= s_hi) break;
         s = s1;
@@ -1052,7 +1055,7 @@ __global__ void __launch_bounds__(MT_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
         const int m0 = min(v ? n0B : n0A, C2_RCAP), m1 = min(v ? n1B : n1A, C2_RCAP);
         for (int m = 0; m < m0 + m1; m++) {
           const int l = m >= m0;
-          const float4 q = rec[((2 * v + l) * C2_RCAP + (l ? m - m0 : m)) * MT_THREADS];
+          const float4 q = rec[((2 * v + l) * C2_RCAP + (l ? m - m0 : m)) * C2_THREADS];
           const float wv = (l ? f1 : f0) * q.w, u = q.y, vv = q.z, wa = wv * (1.f - u), wbb = wv * u;
           macc *pg = G + (l ? N * 32 : 0) + (__float_as_uint(q.x) << 5);
           atomicAdd(pg, q_raw(wa * (1.f - vv)));
@@ -1577,10 +1580,10 @@ static cudaError_t launch_v0_ny(const TraceArgs &a, int ny, dim3 grid, cudaStrea
 template <int MODE>
 static cudaError_t launch_c2(const TraceArgs &a, dim3 grid, cudaStream_t s) {
   static size_t done[16] = {0};
-  const size_t smem = (size_t)16 * 4 * C2_RCAP * MT_THREADS;
+  const size_t smem = (size_t)16 * 4 * C2_RCAP * C2_THREADS;
   cudaError_t e = set_smem(k_trace_c2<MODE>, smem, done);
   if (e != cudaSuccess) return e;
-  k_trace_c2<MODE><<<grid, MT_THREADS, smem, s>>>(a);
+  k_trace_c2<MODE><<<grid, C2_THREADS, smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -1648,8 +1651,10 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
     a.rays_per_block = chunk;
     int64_t S = (p->R + chunk - 1) / chunk;
     dim3 grid((unsigned)S, (unsigned)groups);
-    if (c2) {
-      dim3 grid2((unsigned)S, (unsigned)((C + 63) / 64));
+    if (c2) {   // (C2_THREADS / 256 chunks per block)
+      a.rays_per_block = chunk * (C2_THREADS / 256);
+      const int64_t S2 = (p->R + a.rays_per_block - 1) / a.rays_per_block;
+      dim3 grid2((unsigned)S2, (unsigned)((C + 63) / 64));
       if (grid2.x % C2_TILE) grid2.x += C2_TILE - grid2.x % C2_TILE;   // whole tiles (extra chunks are empty)
       e = mode == TRACE_LL ? launch_c2<TRACE_LL>(a, grid2, s) : launch_c2<TRACE_PATH>(a, grid2, s);
     } else {
