@@ -743,9 +743,7 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_v0(TraceArgs a
   const int c = grp * 32 + lane;
   const bool act = c < a.C;
   float4 *rec = recs + threadIdx.x;
-#if V0_LAUNDER
-  asm volatile("mov.b64 %0, %0;" : "+l"(rec));   // keep, do not rematerialise per emit
-#endif
+
   // this lane's chain band; the warp walks the union band of its 32 chains.
   // Inactive lanes get a band that every cell lies "above" (no loads).
   float4 bd = act ? __ldg(a.band + c) : make_float4(3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f);
@@ -970,7 +968,6 @@ __global__ void __launch_bounds__(C2_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
   asm volatile("" : "+r"(acts));
   const bool actA = acts & 1, actB = acts & 2;
   float4 *rec = recs + threadIdx.x;
-  asm volatile("mov.b64 %0, %0;" : "+l"(rec));
   // lane-union band of its two chains per surface; the warp walks the union over 64 chains
   float4 bd = make_float4(3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f);
   if (actA) bd = __ldg(a.band + cA);
