@@ -415,7 +415,14 @@ __global__ void k_ffma(float *out, int iters, float a, float b, long long *cycle
 #pragma unroll
   for (int k = 0; k < 8; k++) s += x[k];
   if (s == 1234.5f) out[0] = s;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *cycles = t1 - t0;
+  // clock span over every block resident on SM 0 (clock64 is per SM): block 0
+  // alone finishes early under oldest-first warp scheduling
+  unsigned sm;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  if (sm == 0 && threadIdx.x == 0) {
+    atomicMin((unsigned long long *)&cycles[0], (unsigned long long)t0);
+    atomicMax((unsigned long long *)&cycles[1], (unsigned long long)t1);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -843,7 +850,8 @@ cudaError_t run_fp32_peak(int device, double *tflops, double *mhz) {
   float *out;
   long long *cyc;
   cudaMalloc(&out, sizeof(float));
-  cudaMalloc(&cyc, sizeof(long long));
+  cudaMalloc(&cyc, 2 * sizeof(long long));
+  const long long cyc_init[2] = {0x7fffffffffffffffLL, 0};
   int blocks = prop.multiProcessorCount * 4, threads = 512, iters = 4096;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -851,14 +859,16 @@ cudaError_t run_fp32_peak(int device, double *tflops, double *mhz) {
   k_ffma<<<blocks, threads>>>(out, 64, 1.0000001f, 1e-7f, cyc);  // warm-up
   double best = 0, best_mhz = 0;
   for (int rep = 0; rep < 10; rep++) {
+    cudaMemcpy(cyc, cyc_init, sizeof(cyc_init), cudaMemcpyHostToDevice);
     cudaEventRecord(e0);
     k_ffma<<<blocks, threads>>>(out, iters, 1.0000001f, 1e-7f, cyc);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
-    long long cycles = 0;
-    cudaMemcpy(&cycles, cyc, sizeof(long long), cudaMemcpyDeviceToHost);
+    long long span[2] = {0, 0};
+    cudaMemcpy(span, cyc, sizeof(span), cudaMemcpyDeviceToHost);
+    long long cycles = span[1] - span[0];
     double fl = 2.0 * 64.0 * iters * (double)blocks * threads;
     double tf = fl / (ms * 1e-3) / 1e12;
     if (tf > best) { best = tf; best_mhz = cycles / (ms * 1e3); }
