@@ -80,7 +80,7 @@ int check_chains(const mt_problem *p, int32_t C) {
 
 void free_all(mt_problem *p) {
   voxel_free(p);
-  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_trav_geo, p->d_trav_km, p->d_rl_head, p->d_rl_code, p->d_rl_ovf, p->d_ovf_q, p->d_ovf_n, p->d_redo, p->d_H, p->d_Hlo, p->d_Hc, p->d_cl, p->d_cs, p->d_xw, p->d_minv, p->mb_red, p->mb_band, p->mb_ticket, p->d_G,
+  void *bufs[] = {p->d_X, p->d_Y, p->d_ray_a, p->d_ray_b, p->d_obase, p->d_perm, p->d_trav_off, p->d_trav, p->d_trav_geo, p->d_trav_km, p->d_rl_head, p->d_rl_code, p->d_rl_ovf, p->d_ovf_q, p->d_ovf_n, p->d_redo, p->d_H, p->d_Hlo, p->d_Hc, p->d_cl, p->d_cs, p->d_xw, p->d_minv, p->mb_red, p->mb_band, p->mb_ticket, p->d_xalt, p->d_fin_part, p->d_fin_ticket, p->d_G,
                   p->d_band, p->d_ll, p->d_x0, p->d_g0, p->d_mom, p->d_kin0, p->d_kin1, p->d_lp0};
   for (void *b : bufs)
     if (b) cudaFree(b);
@@ -283,6 +283,11 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   ALLOC(p->d_redo, sizeof(unsigned) * redo_words);
   ALLOC(p->d_cs, sizeof(double) * p->N);
   if (p->ncp) ALLOC(p->d_xw, sizeof(double) * MC * 2 * p->N);
+  if (!getenv("MT_NO_FG")) {   // group-tiled K3: second x buffer, per-tile partials, tickets
+    ALLOC(p->d_xalt, sizeof(float) * MC * P);
+    ALLOC(p->d_fin_part, (size_t)48 * MC32 * ((p->N + 63) / 64));
+    ALLOC(p->d_fin_ticket, sizeof(unsigned) * (MC32 / 32));
+  }
   if (!getenv("MT_NO_MB")) {   // few-chain multi-block K3 / kick scratch (use_mb)
     ALLOC(p->mb_red, sizeof(double) * 16 * 3);
     ALLOC(p->mb_band, sizeof(unsigned) * 16 * 4);
@@ -305,6 +310,7 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   if (e == cudaSuccess) e = cudaMemset(p->d_H, 0, sizeof(float) * MC32 * P);
   if (e == cudaSuccess) e = cudaMemset(p->d_Hlo, 0, sizeof(float) * MC32 * P);
   if (e == cudaSuccess) e = cudaMemset(p->d_ll, 0, sizeof(macc) * MC);
+  if (e == cudaSuccess && p->d_fin_ticket) e = cudaMemset(p->d_fin_ticket, 0, sizeof(unsigned) * (MC32 / 32));
   if (e == cudaSuccess) e = cudaMemset(p->d_ovf_n, 0, sizeof(int) * 4);
   if (e == cudaSuccess) e = cudaMemset(p->d_redo, 0, sizeof(unsigned) * redo_words);
   if (e == cudaSuccess && p->mb_red) {
@@ -393,6 +399,24 @@ static int leapfrog_sharded(mt_problem *p, int C, float *x, float *mom, double *
   return MT_OK;
 }
 
+// L fused evaluations + kicks (x, mom already carry the first half kick + drift).
+// The group-tiled K3 reads x from one buffer and writes the drifted x to the
+// other (the caller's block and d_xalt alternate), so no tile reads a halo node
+// another tile has already updated; the last step (no drift) leaves x in the
+// caller's block.
+static int leapfrog_fused(mt_problem *p, int C, float *x, float *mom, double *logp, float *grad,
+                          int32_t *status, const float *eps, int L, cudaStream_t s) {
+  const bool pp = use_fg(p, C);
+  float *cur = x;
+  for (int step = 1; step <= L; step++) {
+    CK(launch_trace(p, TRACE_LL, C, p->d_H, p->d_band, p->d_G, p->d_ll, nullptr, nullptr, s));
+    float *dst = step < L && pp ? (cur == x ? p->d_xalt : x) : x;
+    CK(launch_finish(p, step < L ? FIN_STEP : FIN_LAST, C, dst, grad, logp, status, mom, eps, p->d_kin1, s, cur));
+    if (step < L) cur = dst;
+  }
+  return MT_OK;
+}
+
 int mt_leapfrog(mt_problem *p, int32_t C, float *x, float *mom, double *logp, float *grad,
                 const float *eps, int32_t L, mt_stream stream) {
   if (int r = check_chains(p, C)) return r;
@@ -405,11 +429,7 @@ int mt_leapfrog(mt_problem *p, int32_t C, float *x, float *mom, double *logp, fl
   cudaStream_t s = (cudaStream_t)stream;
   CK(launch_kick_drift(p, C, x, mom, grad, eps, s));
   if (p->comm || p->ncp || use_mb(p, C)) return leapfrog_sharded(p, C, x, mom, logp, grad, nullptr, eps, L, s);
-  for (int step = 1; step <= L; step++) {
-    CK(launch_trace(p, TRACE_LL, C, p->d_H, p->d_band, p->d_G, p->d_ll, nullptr, nullptr, s));
-    CK(launch_finish(p, step < L ? FIN_STEP : FIN_LAST, C, x, grad, logp, nullptr, mom, eps,
-                     p->d_kin1, s));
-  }
+  if (int r = leapfrog_fused(p, C, x, mom, logp, grad, nullptr, eps, L, s)) return r;
   return MT_OK;
 }
 
@@ -440,11 +460,7 @@ int mt_hmc_step(mt_problem *p, int32_t C, float *x, double *logp, float *grad, c
     CK(launch_hmc_end(p, C, x, logp, grad, seed, iter, chain_offset, accept_prob, accepted, status, s));
     return MT_OK;
   }
-  for (int step = 1; step <= L; step++) {
-    CK(launch_trace(p, TRACE_LL, C, p->d_H, p->d_band, p->d_G, p->d_ll, nullptr, nullptr, s));
-    CK(launch_finish(p, step < L ? FIN_STEP : FIN_LAST, C, x, grad, logp, status, p->d_mom, eps,
-                     p->d_kin1, s));
-  }
+  if (int r = leapfrog_fused(p, C, x, p->d_mom, logp, grad, status, eps, L, s)) return r;
   CK(launch_hmc_end(p, C, x, logp, grad, seed, iter, chain_offset, accept_prob, accepted, status, s));
   return MT_OK;
 }

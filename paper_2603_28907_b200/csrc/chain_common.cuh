@@ -46,6 +46,29 @@ __device__ __forceinline__ NodeH node_heights(double x0, double x1, double is0, 
   return o;
 }
 
+// The Jacobian of node_heights in fp32 (∂H0/∂x0, ∂H1/∂x0, ∂H1/∂x1): the chain rule
+// needs it to fp32 accuracy only (the gradient's tolerance is 1e-3), unlike the
+// heights themselves (HP2), so the group-tiled K3 spends no fp64 copula on it.
+struct JacF {
+  float J0, J10, J11;
+};
+__device__ __forceinline__ JacF node_jac32(float x0, float x1, double is0, double is1, float z_top) {
+  const float s0 = (float)is0, s1 = (float)is1;
+  float t0 = x0 * s0, t1 = x1 * s1;
+  const bool c0 = fabsf(t0) > (float)kTClamp, c1 = fabsf(t1) > (float)kTClamp;
+  t0 = fminf(fmaxf(t0, -(float)kTClamp), (float)kTClamp);
+  t1 = fminf(fmaxf(t1, -(float)kTClamp), (float)kTClamp);
+  const float u0 = 0.5f * erfcf(-t0 * 0.70710678118654752f), u1 = 0.5f * erfcf(-t1 * 0.70710678118654752f);
+  const float inv_sqrt_2pi = 0.39894228040143268f;
+  const float d0 = c0 ? 0.f : expf(-0.5f * t0 * t0) * inv_sqrt_2pi * s0;
+  const float d1 = c1 ? 0.f : expf(-0.5f * t1 * t1) * inv_sqrt_2pi * s1;
+  JacF j;
+  j.J0 = z_top * d0;
+  j.J10 = (1.f - u1) * z_top * d0;
+  j.J11 = (z_top - u0 * z_top) * d1;
+  return j;
+}
+
 // diagonal inverse mass M^-1 (mt_set_inverse_mass; identity when not set):
 // p ~ N(0, M), drift x += ε M^-1 p, kinetic ½ pᵀ M^-1 p (R19b)
 __device__ __forceinline__ float mi(const FinishArgs &a, int k) { return a.minv ? a.minv[k] : 1.f; }

@@ -112,6 +112,222 @@ __global__ void __launch_bounds__(MT_THREADS) k_finish(FinishArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// K3, group-tiled (fixed r, centred, C >= 16): block = one 32-chain group x a
+// tile of FG_T consecutive nodes, lane = chain.  The chain-interleaved streams
+// (∂ℓ/∂H in, its zeroing, next H / Hlo out) are then 256-B / 128-B coalesced
+// lines instead of one 8-B / 4-B word per 256-B / 128-B stride, and the
+// caller-layout rows (x, p in; x, p, grad out) go through shared memory with a
+// 33-float node stride (conflict-free both ways).  The x window carries ny
+// halo nodes on each side, so the torus stencil's four neighbours of every
+// tile node are in it (window position = node - k0 + ny, mod N).  Per-chain
+// sums (prior quadratic, kinetic, band, non-finite flag) go to per-tile
+// partials; the group's last block (ticket) reduces them in tile order, so
+// the result does not depend on block scheduling (R30).  Per-node arithmetic
+// is k_finish's, operation for operation.
+// ---------------------------------------------------------------------------
+#define FG_T 64   // nodes per tile
+struct FinPart {   // 48 B: float4 band | double2 (prior, kinetic) sums | non-finite flag
+  float mn0, mx0, mn1, mx1;
+  double s0, s1;
+  int bad, pad[3];
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(MT_THREADS, 3) k_finish_g(FinishArgs a, FinPart *part, unsigned *ticket) {
+  extern __shared__ float fsm[];
+  const int N = a.N, ny = a.ny, P = a.P;
+  const int tile = blockIdx.x, g = blockIdx.y, ntile = gridDim.x;
+  const int k0 = tile * FG_T, nt = min(FG_T, N - k0);
+  const int W = FG_T + 2 * ny;                                   // x window (halo ny each side)
+  float *xs = fsm;                                               // [2][W][33]
+  float *ms = xs + 2 * W * 33;                                   // [2][FG_T][33] momenta
+  float *gs = ms + (MODE != FIN_PLAIN ? 2 * FG_T * 33 : 0);      // [2][FG_T][33] gradient
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c0 = g * 32, nc = min(32, a.C - c0);
+  const bool act = lane < nc;
+  const int c = c0 + lane;
+  // this thread's ∂ℓ/∂H words first (long-latency, independent of shared memory)
+  macc *Gt = const_cast<macc *>(a.G);
+  macc gq0[FG_T / 8], gq1[FG_T / 8];
+#pragma unroll
+  for (int m = 0; m < FG_T / 8; m++) {
+    const int q = warp + 8 * m;
+    const size_t t0 = ((size_t)(2 * g) * N + k0 + q) * 32 + lane;
+    gq0[m] = (q < nt && act) ? Gt[t0] : 0;
+    gq1[m] = (q < nt && act) ? Gt[t0 + (size_t)N * 32] : 0;
+  }
+  // x window and momenta rows, 8 loads in flight per thread
+  for (int cc = warp; cc < nc; cc += MT_THREADS / 32) {
+    const float *xc = a.xin + (size_t)(c0 + cc) * P;
+    for (int q0 = 0; q0 < W; q0 += 128) {
+      float v[2][4];
+#pragma unroll
+      for (int l = 0; l < 2; l++)
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int q = q0 + lane + 32 * u;
+          int k = (k0 - ny + q) % N;
+          k += k < 0 ? N : 0;
+          v[l][u] = q < W ? xc[l * N + k] : 0.f;
+        }
+#pragma unroll
+      for (int l = 0; l < 2; l++)
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int q = q0 + lane + 32 * u;
+          if (q < W) xs[(l * W + q) * 33 + cc] = v[l][u];
+        }
+    }
+    if (MODE != FIN_PLAIN) {
+      const float *pc = a.mom + (size_t)(c0 + cc) * P;
+      float v[2][FG_T / 32];
+#pragma unroll
+      for (int l = 0; l < 2; l++)
+#pragma unroll
+        for (int u = 0; u < FG_T / 32; u++) {
+          const int q = lane + 32 * u;
+          v[l][u] = q < nt ? pc[l * N + k0 + q] : 0.f;
+        }
+#pragma unroll
+      for (int l = 0; l < 2; l++)
+#pragma unroll
+        for (int u = 0; u < FG_T / 32; u++) {
+          const int q = lane + 32 * u;
+          if (q < nt) ms[(l * FG_T + q) * 33 + cc] = v[l][u];
+        }
+    }
+  }
+  __syncthreads();
+  const float eps = (MODE != FIN_PLAIN && act) ? a.eps[c] : 0.f;
+  float mn0 = 3.0e38f, mx0 = -3.0e38f, mn1 = 3.0e38f, mx1 = -3.0e38f;
+  double s0 = 0.0, s1 = 0.0;
+  int bad = 0;
+  float xn0[FG_T / 8], xn1[FG_T / 8];
+#pragma unroll
+  for (int m = 0; m < FG_T / 8; m++) {
+    const int q = warp + 8 * m;
+    xn0[m] = xn1[m] = 0.f;
+    if (q >= nt || !act) continue;
+    const int k = k0 + q, j = k % ny, pos = q + ny;
+    const float x0 = xs[pos * 33 + lane], x1 = xs[(W + pos) * 33 + lane];
+    const JacF h = node_jac32(x0, x1, a.inv_sigma[0], a.inv_sigma[1], a.z_top);
+    const size_t t0 = ((size_t)(2 * g) * N + k) * 32 + lane, t1 = t0 + (size_t)N * 32;
+    const double G0 = dq_g(gq0[m]), G1 = dq_g(gq1[m]);
+    Gt[t0] = 0;
+    Gt[t1] = 0;
+    double gx0 = (double)G0 * h.J0 + (double)G1 * h.J10;
+    double gx1 = (double)G1 * h.J11;
+    if (a.prior_on) {
+      const int pip = pos + ny, pim = pos - ny;   // (i ± 1, j), torus-wrapped by the window
+      const int pjp = j + 1 == ny ? pos - (ny - 1) : pos + 1, pjm = j == 0 ? pos + (ny - 1) : pos - 1;
+#pragma unroll
+      for (int l = 0; l < 2; l++) {
+        const float *xl = xs + l * W * 33 + lane;
+        double xv = xl[pos * 33];
+        double Qx = 4.0 * xv - (double)a.car_r[l] * ((double)xl[pip * 33] + xl[pim * 33] + xl[pjp * 33] + xl[pjm * 33]);
+        s0 += xv * Qx;
+        if (l == 0) gx0 -= Qx; else gx1 -= Qx;
+      }
+    }
+    const float g0f = (float)gx0, g1f = (float)gx1;
+    bad |= !(isfinite(g0f) && isfinite(g1f));
+    gs[q * 33 + lane] = g0f;
+    gs[(FG_T + q) * 33 + lane] = g1f;
+    if (MODE == FIN_STEP) {  // close this step's half kick, open the next: p += ε g; x += ε p
+      const float p0 = ms[q * 33 + lane] + eps * g0f, p1 = ms[(FG_T + q) * 33 + lane] + eps * g1f;
+      ms[q * 33 + lane] = p0;
+      ms[(FG_T + q) * 33 + lane] = p1;
+      const float a0 = x0 + eps * mi(a, k) * p0, a1 = x1 + eps * mi(a, N + k) * p1;
+      xn0[m] = a0;
+      xn1[m] = a1;
+      NodeH hn = node_heights(a0, a1, a.inv_sigma[0], a.inv_sigma[1], a.z_top, false);
+      a.H[t0] = hn.H0;
+      a.H[t1] = hn.H1;
+      a.Hlo[t0] = hn.L0;
+      a.Hlo[t1] = hn.L1;
+      mn0 = fminf(mn0, hn.H0); mx0 = fmaxf(mx0, hn.H0);
+      mn1 = fminf(mn1, hn.H1); mx1 = fmaxf(mx1, hn.H1);
+    } else if (MODE == FIN_LAST) {  // final half kick
+      const float p0 = ms[q * 33 + lane] + 0.5f * eps * g0f, p1 = ms[(FG_T + q) * 33 + lane] + 0.5f * eps * g1f;
+      ms[q * 33 + lane] = p0;
+      ms[(FG_T + q) * 33 + lane] = p1;
+      s1 += 0.5 * ((double)mi(a, k) * p0 * p0 + (double)mi(a, N + k) * p1 * p1);
+    }
+  }
+  // per-chain partials of this tile: the 8 warps' values, summed in warp order
+  __shared__ float4 wb[MT_THREADS / 32][32];
+  __shared__ double2 ws[MT_THREADS / 32][32];
+  __shared__ int wbad[MT_THREADS / 32][32];
+  __shared__ int last;
+  wb[warp][lane] = make_float4(mn0, mx0, mn1, mx1);
+  ws[warp][lane] = make_double2(s0, s1);
+  wbad[warp][lane] = bad;
+  __syncthreads();   // (all window reads done: the new x may overwrite it)
+  if (MODE == FIN_STEP) {
+#pragma unroll
+    for (int m = 0; m < FG_T / 8; m++) {
+      const int q = warp + 8 * m;
+      if (q < nt && act) {
+        xs[(q + ny) * 33 + lane] = xn0[m];
+        xs[(W + q + ny) * 33 + lane] = xn1[m];
+      }
+    }
+  }
+  if (warp == 0) {
+    float4 b = wb[0][lane];
+    double2 sm = ws[0][lane];
+    int bb = wbad[0][lane];
+    for (int w = 1; w < MT_THREADS / 32; w++) {
+      const float4 o = wb[w][lane];
+      b = make_float4(fminf(b.x, o.x), fmaxf(b.y, o.y), fminf(b.z, o.z), fmaxf(b.w, o.w));
+      sm.x += ws[w][lane].x;
+      sm.y += ws[w][lane].y;
+      bb |= wbad[w][lane];
+    }
+    FinPart *pp = part + ((size_t)g * ntile + tile) * 32 + lane;
+    *reinterpret_cast<float4 *>(pp) = b;
+    *(reinterpret_cast<double2 *>(pp) + 1) = sm;
+    *(reinterpret_cast<int *>(pp) + 8) = bb;
+    __threadfence();
+  }
+  __syncthreads();
+  // write back the caller-layout rows (coalesced along nodes)
+  for (int cc = warp; cc < nc; cc += MT_THREADS / 32) {
+    const size_t row = (size_t)(c0 + cc) * P;
+#pragma unroll
+    for (int l = 0; l < 2; l++)
+      for (int q = lane; q < nt; q += 32) {
+        const int o = l * N + k0 + q;
+        a.grad[row + o] = gs[(l * FG_T + q) * 33 + cc];
+        if (MODE != FIN_PLAIN) a.mom[row + o] = ms[(l * FG_T + q) * 33 + cc];
+        if (MODE == FIN_STEP || (MODE == FIN_LAST && a.xin != a.x)) a.x[row + o] = xs[(l * W + q + ny) * 33 + cc];
+      }
+  }
+  if (threadIdx.x == 0) last = atomicAdd(ticket + g, 1u) == (unsigned)(ntile - 1);
+  __syncthreads();
+  if (!last || warp != 0) return;
+  __threadfence();
+  FinPart r = {3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f, 0.0, 0.0, 0, 0};
+  for (int t = 0; t < ntile; t++) {   // tile order: independent of which block finished last
+    const FinPart *pp = part + ((size_t)g * ntile + t) * 32 + lane;
+    const float4 b = __ldcg(reinterpret_cast<const float4 *>(pp));
+    const double2 s = __ldcg(reinterpret_cast<const double2 *>(pp) + 1);
+    const int bb = __ldcg(reinterpret_cast<const int *>(pp) + 8);
+    r.mn0 = fminf(r.mn0, b.x); r.mx0 = fmaxf(r.mx0, b.y);
+    r.mn1 = fminf(r.mn1, b.z); r.mx1 = fmaxf(r.mx1, b.w);
+    r.s0 += s.x; r.s1 += s.y; r.bad |= bb;
+  }
+  if (lane == 0) ticket[g] = 0;
+  if (!act) return;
+  const double lp = dq_ll(a.ll[c]) + (a.prior_on ? -0.5 * r.s0 + a.prior_const : 0.0);
+  a.ll[c] = 0;
+  a.logp[c] = lp;
+  if (a.status) a.status[c] = (r.bad || !isfinite(lp)) ? MT_STATUS_NONFINITE : 0;
+  if (MODE == FIN_STEP) a.band[c] = make_float4(r.mn0, r.mx0, r.mn1, r.mx1);
+  if (MODE == FIN_LAST && a.kin) a.kin[c] = (float)r.s1;
+}
+
 // Leapfrog kicks from a stored gradient (R19):
 //   KICK_HALF_DRIFT  p += ε/2 g; x += ε p; H(x)   (first step of mt_leapfrog)
 //   KICK_FULL_DRIFT  p += ε g;   x += ε p; H(x)   (ray sharding: after the all-reduce)
@@ -675,13 +891,41 @@ cudaError_t launch_heights(mt_problem *p, int C, const float *x, float *H, float
   return cudaGetLastError();
 }
 
+bool use_fg(const mt_problem *p, int C) {
+  return p->d_fin_part != nullptr && C >= 16 && !p->sample_r && !p->ncp && !use_mb(p, C);
+}
+
+template <int MODE>
+static cudaError_t launch_fg(mt_problem *p, const FinishArgs &a, int C, cudaStream_t s) {
+  static size_t done[64] = {};
+  const int W = FG_T + 2 * p->ny;
+  const size_t smem = sizeof(float) * 33 * (2 * (size_t)W + 2 * FG_T * (MODE == FIN_PLAIN ? 1 : 2));
+  const int dv = p->device & 63;
+  if (smem > 32 * 1024 && done[dv] < smem) {   // (dynamic + 9 KB static must fit the attribute)
+    cudaError_t e = cudaFuncSetAttribute(k_finish_g<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    done[dv] = smem;
+  }
+  const dim3 grid((unsigned)((p->N + FG_T - 1) / FG_T), (unsigned)((C + 31) / 32));
+  k_finish_g<MODE><<<grid, MT_THREADS, smem, s>>>(a, reinterpret_cast<FinPart *>(p->d_fin_part), p->d_fin_ticket);
+  p->all_launches++;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_finish(mt_problem *p, int mode, int C, float *x, float *grad, double *logp,
                           int32_t *status, float *mom, const float *eps, float *kin,
-                          cudaStream_t s) {
+                          cudaStream_t s, const float *xin) {
   if (C <= 0) return cudaSuccess;
   if (mode != FIN_PLAIN && mode != FIN_STEP && mode != FIN_LAST) return cudaErrorInvalidValue;
   FinishArgs a = base_args(p, C);
   a.x = x; a.grad = grad; a.logp = logp; a.status = status; a.mom = mom; a.eps = eps; a.kin = kin;
+  a.xin = xin ? xin : x;
+  if (use_fg(p, C)) {
+    if (mode == FIN_PLAIN) return launch_fg<FIN_PLAIN>(p, a, C, s);
+    if (mode == FIN_STEP) return launch_fg<FIN_STEP>(p, a, C, s);
+    return launch_fg<FIN_LAST>(p, a, C, s);
+  }
+  if (a.xin != x) return cudaErrorInvalidValue;   // (only the group-tiled K3 reads a separate x)
   if (use_mb(p, C)) {   // few chains: several blocks per chain (unfused leapfrog)
     if (mode != FIN_PLAIN) return cudaErrorInvalidValue;
     k_finish_mb<<<dim3(C, mb_blocks(p, C)), MT_THREADS, 0, s>>>(a, mb_scratch(p));

@@ -113,6 +113,8 @@ struct FinishArgs {
   const macc *G;                // ∂ℓ/∂H [C][2N], fixed point MT_GQ (zeroed after use)
   macc *ll;                     // [C] log-likelihood, fixed point MT_LQ (zeroed after use)
   float *x;                     // [C][P]
+  const float *xin;             // [C][P] x to read (group-tiled K3: the leapfrog ping-pongs x between the
+                                // caller's block and d_xalt so no tile reads a neighbour's updated x)
   float *grad;                  // [C][P]
   double *logp;                 // [C]
   int32_t *status;              // [C] or null
@@ -191,6 +193,9 @@ struct mt_problem {
   double *d_cs = nullptr;       // [N] torus spectrum table (sample_r)
   int ncp = 0;                  // f2 non-centred parameterisation (implies sample_r)
   float *d_minv = nullptr;      // [P] diagonal inverse mass (null until mt_set_inverse_mass)
+  float *d_xalt = nullptr;      // [max_chains][P] second x buffer of the group-tiled K3 leapfrog
+  void *d_fin_part = nullptr;   // group-tiled K3 per-tile partials [groups][tiles][32] (FinPart, 48 B)
+  unsigned *d_fin_ticket = nullptr;   // [groups] last-block tickets
   double *mb_red = nullptr;     // few-chain multi-block K3 scratch: [16][3] sums
   unsigned *mb_band = nullptr;  //   [16][4] band as float bits
   unsigned *mb_ticket = nullptr;   // [16] last-block tickets
@@ -255,8 +260,9 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
                          unsigned long long *task_cost = nullptr);
 cudaError_t launch_finish(mt_problem *p, int mode, int C, float *x, float *grad, double *logp,
                           int32_t *status, float *mom, const float *eps, float *kin,
-                          cudaStream_t s);
+                          cudaStream_t s, const float *xin = nullptr);
 bool use_mb(const mt_problem *p, int C);   // few chains: multi-block K3 and kicks, unfused leapfrog
+bool use_fg(const mt_problem *p, int C);   // group-tiled K3 (the fused leapfrog ping-pongs x, d_xalt)
 FinishArgs base_args(mt_problem *p, int C);   // per-problem constants of the per-chain kernels
 // ncp.cu (f2 non-centred): heights of x = U z, K3, kick / drift (+ heights)
 void launch_ncp_heights(mt_problem *p, const FinishArgs &a, int C, const float *x, cudaStream_t s);

@@ -905,6 +905,7 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_v0(TraceArgs a
 #define C2_MINB (1024 / C2_THREADS)
 #endif
 
+
 __global__ void __launch_bounds__(MT_THREADS) k_cell_prep2(const float *__restrict__ H, float4 *__restrict__ H4, int C,
                                                          int ny, int N, int64_t n) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // [g64][l][node][lane]
@@ -1649,7 +1650,7 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
     int64_t S = (p->R + chunk - 1) / chunk;
     dim3 grid((unsigned)S, (unsigned)groups);
     if (c2) {   // (C2_THREADS / 256 chunks per block)
-      a.rays_per_block = chunk * (C2_THREADS / 256);
+      a.rays_per_block = std::max<int64_t>(32, chunk * C2_THREADS / 256);
       const int64_t S2 = (p->R + a.rays_per_block - 1) / a.rays_per_block;
       dim3 grid2((unsigned)S2, (unsigned)((C + 63) / 64));
       if (grid2.x % C2_TILE) grid2.x += C2_TILE - grid2.x % C2_TILE;   // whole tiles (extra chunks are empty)

@@ -1,4 +1,5 @@
-timeout 300 python tools/trace_bench.py ray_sharded > gpurun_out/tb_v30.log 2>&1
-timeout 300 python tools/trace_bench.py small >> gpurun_out/tb_v30.log 2>&1
-timeout 600 python tools/parity_margin.py ray_sharded > gpurun_out/pm_v30.log 2>&1
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_v30.log 2>&1
+mkdir -p gpurun_out
+timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_k3c.log 2>&1
+bash tools/gpu_r2.sh k3c notest default nogb t128m9 t128m8
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_exhaustive.py tests/test_gpu_dist.py -m gpu -x -q > gpurun_out/pytest_k3c.log 2>&1; echo "rc $?" >> gpurun_out/pytest_k3c.log
+timeout 600 ncu --set full --clock-control none -k regex:"k_finish_g" -s 2 -c 1 -o gpurun_out/k3i -f python tools/trace_bench.py chain_sharded --reps 3 > gpurun_out/ncu_k3i.log 2>&1
