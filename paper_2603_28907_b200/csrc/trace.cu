@@ -955,6 +955,22 @@ __device__ __forceinline__ void c2_cell(float h00, float h01, float h10, float h
   if (!solve32k(h00, h10, h01, h11, cg, km, za, Ls, dz, B, emit)) defer = 1;
 }
 
+// Same, with the lane's crossing counters and defer flags packed in one register
+// (fields of 5 bits, saturating at 31: n0A @0, n1A @5, n0B @10, n1B @15; defer
+// bits 20 / 21), the record slot already offset by the caller.
+__device__ __forceinline__ void c2_cellp(float h00, float h01, float h10, float h11, float4 cg, float2 km, float za,
+                                         float zb, float Ls, float dz, float wbase, float &B, unsigned &cnt,
+                                         const int sh, const unsigned dbit, float4 *rec) {
+  if (zb <= fminf(fminf(h00, h10), fminf(h01, h11))) { B += Ls; return; }   // bilinear min at a corner
+  if (za >= fmaxf(fmaxf(h00, h10), fmaxf(h01, h11))) return;
+  auto emit = [&](float u, float v, float ig) {
+    const unsigned n = (cnt >> sh) & 31u;
+    if (n < C2_RCAP) rec[n * C2_THREADS] = make_float4(wbase, u, v, ig);
+    if (n < 31u) cnt += 1u << sh;
+  };
+  if (!solve32k(h00, h10, h01, h11, cg, km, za, Ls, dz, B, emit)) cnt |= dbit;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(C2_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
   extern __shared__ __align__(16) float4 recs[];   // [chain v][surface l][C2_RCAP][C2_THREADS]
@@ -984,7 +1000,9 @@ __global__ void __launch_bounds__(C2_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
   if (!actA && !actB) bd = make_float4(-3.0e38f, -3.0e38f, -3.0e38f, -3.0e38f);
   const float4 *__restrict__ H4 = reinterpret_cast<const float4 *>(a.cl) + (size_t)g * 2 * N * 32 + lane;
   asm volatile("mov.b64 %0, %0;" : "+l"(H4));
-  float llA = 0.f, llB = 0.f;
+  __shared__ float sll[2][C2_THREADS];   // per-lane log-likelihood sums (kept out of the registers)
+  sll[0][threadIdx.x] = 0.f;
+  sll[1][threadIdx.x] = 0.f;
 
   const int r_begin = chunk * (int)a.rays_per_block;
   const int r_end = min((int)a.R, r_begin + (int)a.rays_per_block);
@@ -994,7 +1012,7 @@ __global__ void __launch_bounds__(C2_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
     const float s_lo = fminf(__fdividef(zlo, dz) * (1.f - 1e-6f), s_exit);
     const float s_hi = fminf(__fdividef(zhi, dz) * (1.f + 1e-6f), s_exit);
     float B0A = s_lo, B1A = s_lo, B0B = s_lo, B1B = s_lo;
-    int n0A = 0, n1A = 0, n0B = 0, n1B = 0, dA = 0, dB = 0;
+    unsigned cnt = 0;   // packed counters / defer flags (c2_cellp)
     if (s_lo < s_exit) {
       const int kend = __ldg(a.trav_off + rr + 1);
       float s_in0;
@@ -1013,13 +1031,14 @@ __global__ void __launch_bounds__(C2_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
         for (int l = 0; l < 2; l++) {
           const float zmin = l ? bd.z : bd.x, zmax = l ? bd.w : bd.y;
           float &BA = l ? B1A : B0A, &BB = l ? B1B : B0B;
-          int &nA = l ? n1A : n0A, &nB = l ? n1B : n0B;
           if (zb <= zmin) { BA += Ls; BB += Ls; continue; }   // below both chains' lowest node
           if (za >= zmax) continue;                            // above both chains' highest node
           const float4 *p = H4 + (size_t)l * N * 32 + off;
           const float4 r0 = __ldg(p), r1 = __ldg(p + oy);
-          if (actA) c2_cell<0, false>(r0.x, r0.y, r1.x, r1.y, cg, km, za, zb, Ls, dz, wb, BA, nA, dA, rec + l * C2_RCAP * C2_THREADS, nullptr, 0, 0.f);
-          if (actB) c2_cell<0, false>(r0.z, r0.w, r1.z, r1.w, cg, km, za, zb, Ls, dz, wb, BB, nB, dB, rec + (2 + l) * C2_RCAP * C2_THREADS, nullptr, 0, 0.f);
+          if (actA) c2_cellp(r0.x, r0.y, r1.x, r1.y, cg, km, za, zb, Ls, dz, wb, BA, cnt, l ? 5 : 0, 1u << 20,
+                             rec + l * C2_RCAP * C2_THREADS);
+          if (actB) c2_cellp(r0.z, r0.w, r1.z, r1.w, cg, km, za, zb, Ls, dz, wb, BB, cnt, l ? 15 : 10, 1u << 21,
+                             rec + (2 + l) * C2_RCAP * C2_THREADS);
         }
         if (s1 >= s_hi) break;
         s = s1;
@@ -1027,6 +1046,8 @@ __global__ void __launch_bounds__(C2_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
         ds = 0.f;
       }
     }
+    const int dA = (cnt >> 20) & 1, dB = (cnt >> 21) & 1;
+    const int n0A = cnt & 31, n1A = (cnt >> 5) & 31, n0B = (cnt >> 10) & 31, n1B = (cnt >> 15) & 31;
     if (dA) {
       const int q = atomicAdd(a.ovf_n, 1);
       if (q < a.ovf_cap) a.ovf_q[q] = make_float4(__int_as_float(cA), __int_as_float(rr), s_lo, s_hi);
@@ -1048,7 +1069,8 @@ __global__ void __launch_bounds__(C2_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
         float dldO;
         const float ll = epilogue(rt.x, rt.y, a.tc, v ? B0B : B0A, v ? B1B : B1A, dldO);
         const float f0 = dldO * a.tc.k0 * (float)MT_GQ, f1 = dldO * a.tc.k1 * (float)MT_GQ;
-        if (v) { llB += ll; f0B = f0; f1B = f1; } else { llA += ll; f0A = f0; f1A = f1; }
+        sll[v][threadIdx.x] += ll;
+        if (v) { f0B = f0; f1B = f1; } else { f0A = f0; f1A = f1; }
         macc *G = v ? GB : GA;
         const int m0 = min(v ? n0B : n0A, C2_RCAP), m1 = min(v ? n1B : n1A, C2_RCAP);
         for (int m = 0; m < m0 + m1; m++) {
@@ -1109,8 +1131,8 @@ __global__ void __launch_bounds__(C2_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
     }
   }
   if (MODE == TRACE_LL) {
-    if (actA) atomicAdd(a.ll + cA, q_ll(llA));
-    if (actB) atomicAdd(a.ll + cB, q_ll(llB));
+    if (actA) atomicAdd(a.ll + cA, q_ll(sll[0][threadIdx.x]));
+    if (actB) atomicAdd(a.ll + cB, q_ll(sll[1][threadIdx.x]));
   }
 }
 
