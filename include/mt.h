@@ -257,6 +257,17 @@ int mt_nested_rhat_partials(mt_problem *p, int32_t C, int32_t M, const float *me
 int mt_summary_update(mt_problem *p, int32_t C, const float *x, const double *logp, int32_t nz, float gap,
                       double *acc, float *map_x, double *map_logp, mt_stream stream);
 
+/* The summaries from the accumulators of mt_summary_update (R27):
+ *   acc  DEVICE double, as filled by mt_summary_update (acc[0] >= 1 draws).
+ *   out  DEVICE double [3N + 3 N nz], caller-owned:
+ *        [0, 2N)        mean heights, [surface][node];
+ *        [2N, 3N)       air-gap exceedance probability per node;
+ *        [3N, 3N+3N nz) indicator std sqrt(max(E[D²] - E[D]², 0)), laid out
+ *                       [unit l][node][layer k] (indicator-std tomography,
+ *                       P:789-811).
+ * Asynchronous on `stream`.  Errors: MT_EINVAL (NULL, nz < 1), MT_ECUDA. */
+int mt_summary_finalize(mt_problem *p, int32_t nz, const double *acc, double *out, mt_stream stream);
+
 /* Diagonal inverse mass matrix M^-1 for HMC and NUTS (NumPyro's default
  * adapted diagonal mass, the paper's sampler P:643-653; R19b):
  * momenta p ~ N(0, M), drift x += ε M^-1 p, kinetic energy ½ pᵀ M^-1 p, the

@@ -45,7 +45,7 @@ EXPORTS = [
     "mt_stats_update", "mt_rhat_partials", "mt_heights", "mt_loglik_heights", "mt_path_lengths", "mt_debug_traversal", "mt_traversal_all", "mt_ray_work", "mt_ray_cost", "mt_nuts_record", "mt_philox",
     "mt_philox_curand", "mt_timing_start", "mt_timing_read", "mt_trace_counters", "mt_measure_fp32_peak",
     "mt_last_error", "mt_comm_unique_id", "mt_attach_comm", "mt_detach_comm", "mt_nuts_step",
-    "mt_nested_rhat_partials", "mt_summary_update", "mt_voxel_model", "mt_voxel_info",
+    "mt_nested_rhat_partials", "mt_summary_update", "mt_summary_finalize", "mt_voxel_model", "mt_voxel_info",
     "mt_voxel_counters", "mt_measure_l2_gather", "mt_set_inverse_mass",
 ]
 
@@ -74,6 +74,7 @@ def lib():
             "mt_rhat_partials": ([vp, i32, vp, vp, i32, vp, vp], ct.c_int),
             "mt_nested_rhat_partials": ([vp, i32, i32, vp, vp, i32, vp, vp], ct.c_int),
             "mt_summary_update": ([vp, i32, vp, vp, i32, ct.c_float, vp, vp, vp, vp], ct.c_int),
+            "mt_summary_finalize": ([vp, i32, vp, vp, vp], ct.c_int),
             "mt_heights": ([vp, i32, vp, vp, vp], ct.c_int),
             "mt_loglik_heights": ([vp, i32, vp, vp, vp, vp], ct.c_int),
             "mt_path_lengths": ([vp, i32, vp, vp, vp, vp], ct.c_int),
@@ -305,18 +306,18 @@ class Problem:
         return acc, torch.zeros(self.P, dtype=torch.float32, device=dev), \
             torch.full((1,), float("-inf"), dtype=torch.float64, device=dev)
 
-    def summaries(self, acc, nz: int):
-        """Host assembly: mean heights [2][nx][ny], air-gap exceedance probability
-        [nx][ny], indicator std [3][nx][ny][nz]."""
-        a = acc.cpu().numpy()
+    def summaries(self, acc, nz: int, stream=None):
+        """Mean heights [2][nx][ny], air-gap exceedance probability [nx][ny] and
+        indicator std [3][nx][ny][nz], assembled on the device by
+        mt_summary_finalize."""
+        import torch
         N = self.nx * self.ny
-        n = a[0]
-        meanH = (a[1:1 + 2 * N] / n).reshape(2, self.nx, self.ny)
-        gap = (a[1 + 2 * N:1 + 3 * N] / n).reshape(self.nx, self.ny)
-        sd = a[1 + 3 * N:1 + 3 * N + 3 * N * nz] / n
-        sd2 = a[1 + 3 * N + 3 * N * nz:] / n
-        std = np.sqrt(np.maximum(sd2 - sd * sd, 0.0)).reshape(3, self.nx, self.ny, nz)
-        return dict(mean_heights=meanH, gap_probability=gap, indicator_std=std, draws=int(n))
+        out = torch.empty(3 * N * (1 + nz), dtype=torch.float64, device=acc.device)
+        _check(lib().mt_summary_finalize(self.h, nz, _ptr(acc), _ptr(out), _stream(stream)), "mt_summary_finalize")
+        o = out.cpu().numpy()
+        return dict(mean_heights=o[:2 * N].reshape(2, self.nx, self.ny),
+                    gap_probability=o[2 * N:3 * N].reshape(self.nx, self.ny),
+                    indicator_std=o[3 * N:].reshape(3, self.nx, self.ny, nz), draws=int(acc[0].item()))
 
     # -- parity / debug ------------------------------------------------------
     def heights(self, x, stream=None):

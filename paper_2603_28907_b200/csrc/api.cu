@@ -567,6 +567,15 @@ int mt_summary_update(mt_problem *p, int32_t C, const float *x, const double *lo
   return MT_OK;
 }
 
+int mt_summary_finalize(mt_problem *p, int32_t nz, const double *acc, double *out, mt_stream stream) {
+  if (!p) return set_err(MT_EINVAL, "problem is NULL");
+  if (nz < 1) return set_err(MT_EINVAL, "nz = %d < 1", nz);
+  if (check_ptr(acc, "acc") || check_ptr(out, "out")) return MT_EINVAL;
+  DevGuard g(p->device);
+  CK(launch_summary_finalize(p, nz, acc, out, (cudaStream_t)stream));
+  return MT_OK;
+}
+
 int mt_heights(mt_problem *p, int32_t C, const float *x, float *H, mt_stream stream) {
   if (int r = check_chains(p, C)) return r;
   if (C == 0) return MT_OK;

@@ -305,6 +305,7 @@ cudaError_t launch_stats(mt_problem *p, int C, const float *x, const float *acc,
 cudaError_t launch_tile(mt_problem *p, int C, const float *src, float *dst, int to_tiled,
                         cudaStream_t s);
 cudaError_t launch_take_acc(mt_problem *p, int C, float *dldH, double *ll, cudaStream_t s);
+cudaError_t launch_summary_finalize(mt_problem *p, int nz, const double *acc, double *out, cudaStream_t s);
 cudaError_t launch_summary(mt_problem *p, int C, const float *x, const double *logp, int nz, float gap,
                            double *acc, float *map_x, double *map_logp, cudaStream_t s);
 cudaError_t launch_nested_rhat_partials(mt_problem *p, int C, int M, const float *mean, const float *m2,

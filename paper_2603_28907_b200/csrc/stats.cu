@@ -183,6 +183,30 @@ __global__ void k_map_update(int C, int P, const float *x, const double *logp, f
     for (int k = threadIdx.x; k < P; k += blockDim.x) map_x[k] = x[(size_t)best * P + k];
 }
 
+// f4 assembly (R27) from the accumulators of k_summary_update:
+// out = [mean heights 2N | air-gap exceedance probability N | indicator std
+// 3 N nz], std = sqrt(max(E[D²] - E[D]², 0)) per (unit, node, layer).
+__global__ void k_summary_finalize(const double *acc, int N, int nz, double *out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n3 = 3 * (int64_t)N, nd = 3 * (int64_t)N * nz;
+  if (t >= n3 + nd) return;
+  const double n = acc[0];
+  if (t < n3) {
+    out[t] = acc[1 + t] / n;
+  } else {
+    const int64_t q = t - n3;
+    const double m = acc[1 + n3 + q] / n, m2 = acc[1 + n3 + nd + q] / n;
+    out[t] = sqrt(fmax(m2 - m * m, 0.0));
+  }
+}
+
+cudaError_t launch_summary_finalize(mt_problem *p, int nz, const double *acc, double *out, cudaStream_t s) {
+  const int64_t n = 3 * (int64_t)p->N * (1 + nz);
+  k_summary_finalize<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(acc, p->N, nz, out);
+  p->all_launches++;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_summary(mt_problem *p, int C, const float *x, const double *logp, int nz, float gap,
                            double *acc, float *map_x, double *map_logp, cudaStream_t s) {
   cudaError_t e = launch_heights(p, C, x, p->d_H, p->d_band, s);

@@ -1144,8 +1144,11 @@ __global__ void __launch_bounds__(C2_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
 // then the epilogue and each lane's adjoint scatter (or the path-length
 // export).  A pair's latency is a few dependent loads, not a serial march.
 // The last block resets the queue.
+#ifndef DEFER_MINB
+#define DEFER_MINB 2   // resident blocks per SM of k_trace_defer (launch bound and grid)
+#endif
 template <int MODE, int DG>
-__global__ void __launch_bounds__(MT_THREADS) k_trace_defer(TraceArgs a) {
+__global__ void __launch_bounds__(MT_THREADS, DEFER_MINB) k_trace_defer(TraceArgs a) {
   __shared__ float4 wrec[MT_THREADS][4];   // per lane: up to 2 crossings per surface of its cell
   load_geometry(a, sgeo[0], sgeo[1], sgeo[2], sgeo[3]);
   __syncthreads();
@@ -1682,8 +1685,8 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
     }
     if (rec) cudaEventRecord(p->ev_m[p->n_rec], s);
     if (e == cudaSuccess) {   // deferred pairs (ill-conditioned or > RCAP crossings)
-      if (mode == TRACE_LL) k_trace_defer<TRACE_LL, DEFER_DG><<<2 * p->num_sms, MT_THREADS, 0, s>>>(a);
-      else k_trace_defer<TRACE_PATH, DEFER_DG><<<2 * p->num_sms, MT_THREADS, 0, s>>>(a);
+      if (mode == TRACE_LL) k_trace_defer<TRACE_LL, DEFER_DG><<<DEFER_MINB * p->num_sms, MT_THREADS, 0, s>>>(a);
+      else k_trace_defer<TRACE_PATH, DEFER_DG><<<DEFER_MINB * p->num_sms, MT_THREADS, 0, s>>>(a);
       e = cudaGetLastError();
       p->all_launches++;
     }
