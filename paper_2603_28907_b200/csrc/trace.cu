@@ -955,55 +955,37 @@ __device__ __forceinline__ void c2_cell(float h00, float h01, float h10, float h
   if (!solve32k(h00, h10, h01, h11, cg, km, za, Ls, dz, B, emit)) defer = 1;
 }
 
+// Crossing records of k_trace_c2, [chain v][surface l][C2_RCAP][thread] (static:
+// the slot address is a constant offset from the thread's, no shared-window
+// pointer to rematerialise).
+__shared__ __align__(16) float4 c2_recs[4 * C2_RCAP][C2_THREADS];
+__shared__ float c2_sll[2][C2_THREADS];   // per-lane log-likelihood sums (kept out of the registers)
+
 // Same, with the lane's crossing counters and defer flags packed in one register
 // (fields of 5 bits, saturating at 31: n0A @0, n1A @5, n0B @10, n1B @15; defer
-// bits 20 / 21), the record slot already offset by the caller.
+// bits 20 / 21); records of (chain v, surface l) at slots slot0 = (2v + l) RCAP.
 __device__ __forceinline__ void c2_cellp(float h00, float h01, float h10, float h11, float4 cg, float2 km, float za,
                                          float zb, float Ls, float dz, float wbase, float &B, unsigned &cnt,
-                                         const int sh, const unsigned dbit, float4 *rec) {
+                                         const int sh, const unsigned dbit, const int slot0) {
   if (zb <= fminf(fminf(h00, h10), fminf(h01, h11))) { B += Ls; return; }   // bilinear min at a corner
   if (za >= fmaxf(fmaxf(h00, h10), fmaxf(h01, h11))) return;
   auto emit = [&](float u, float v, float ig) {
     const unsigned n = (cnt >> sh) & 31u;
-    if (n < C2_RCAP) rec[n * C2_THREADS] = make_float4(wbase, u, v, ig);
+    if (n < C2_RCAP) c2_recs[slot0 + n][threadIdx.x] = make_float4(wbase, u, v, ig);
     if (n < 31u) cnt += 1u << sh;
   };
   if (!solve32k(h00, h10, h01, h11, cg, km, za, Ls, dz, B, emit)) cnt |= dbit;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(C2_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
-  extern __shared__ __align__(16) float4 recs[];   // [chain v][surface l][C2_RCAP][C2_THREADS]
-  int N = a.tc.N, oy = a.tc.ny * 32;
-  asm volatile("" : "+r"(N), "+r"(oy));   // keep in registers (no per-use reload / recompute)
+// The ray loop of k_trace_c2; FULL: both chains of every lane are active (every
+// 64-chain group but a ragged last one), so the per-chain guards compile away.
+template <int MODE, bool FULL>
+__device__ __forceinline__ void c2_rays(const TraceArgs &a, int N, int oy, const int g, const int chunk,
+                                        const int acts, const float4 bd, const float zlo, const float zhi,
+                                        const float4 *__restrict__ H4) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int lin = blockIdx.y * gridDim.x + blockIdx.x, G2 = gridDim.y;
-  const int tile = lin / (G2 * C2_TILE), within = lin - tile * (G2 * C2_TILE);
-  const int g = within / C2_TILE, chunk = tile * C2_TILE + (within - (within / C2_TILE) * C2_TILE);
   const int cA = g * 64 + lane, cB = cA + 32;
-  int acts = (cA < a.C ? 1 : 0) | (cB < a.C ? 2 : 0);
-  asm volatile("" : "+r"(acts));
-  const bool actA = acts & 1, actB = acts & 2;
-  float4 *rec = recs + threadIdx.x;
-  // lane-union band of its two chains per surface; the warp walks the union over 64 chains
-  float4 bd = make_float4(3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f);
-  if (actA) bd = __ldg(a.band + cA);
-  if (actB) {
-    const float4 b = __ldg(a.band + cB);
-    bd = make_float4(fminf(bd.x, b.x), fmaxf(bd.y, b.y), fminf(bd.z, b.z), fmaxf(bd.w, b.w));
-  }
-  float zlo = bd.x, zhi = bd.w;
-  for (int o = 16; o > 0; o >>= 1) {
-    zlo = fminf(zlo, __shfl_xor_sync(0xffffffffu, zlo, o));
-    zhi = fmaxf(zhi, __shfl_xor_sync(0xffffffffu, zhi, o));
-  }
-  if (!actA && !actB) bd = make_float4(-3.0e38f, -3.0e38f, -3.0e38f, -3.0e38f);
-  const float4 *__restrict__ H4 = reinterpret_cast<const float4 *>(a.cl) + (size_t)g * 2 * N * 32 + lane;
-  asm volatile("mov.b64 %0, %0;" : "+l"(H4));
-  __shared__ float sll[2][C2_THREADS];   // per-lane log-likelihood sums (kept out of the registers)
-  sll[0][threadIdx.x] = 0.f;
-  sll[1][threadIdx.x] = 0.f;
-
+  const bool actA = FULL || (acts & 1), actB = FULL || (acts & 2);
   const int r_begin = chunk * (int)a.rays_per_block;
   const int r_end = min((int)a.R, r_begin + (int)a.rays_per_block);
   for (int rr = r_begin + warp; rr < r_end; rr += C2_THREADS / 32) {
@@ -1036,9 +1018,9 @@ __global__ void __launch_bounds__(C2_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
           const float4 *p = H4 + (size_t)l * N * 32 + off;
           const float4 r0 = __ldg(p), r1 = __ldg(p + oy);
           if (actA) c2_cellp(r0.x, r0.y, r1.x, r1.y, cg, km, za, zb, Ls, dz, wb, BA, cnt, l ? 5 : 0, 1u << 20,
-                             rec + l * C2_RCAP * C2_THREADS);
+                             l * C2_RCAP);
           if (actB) c2_cellp(r0.z, r0.w, r1.z, r1.w, cg, km, za, zb, Ls, dz, wb, BB, cnt, l ? 15 : 10, 1u << 21,
-                             rec + (2 + l) * C2_RCAP * C2_THREADS);
+                             (2 + l) * C2_RCAP);
         }
         if (s1 >= s_hi) break;
         s = s1;
@@ -1069,13 +1051,13 @@ __global__ void __launch_bounds__(C2_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
         float dldO;
         const float ll = epilogue(rt.x, rt.y, a.tc, v ? B0B : B0A, v ? B1B : B1A, dldO);
         const float f0 = dldO * a.tc.k0 * (float)MT_GQ, f1 = dldO * a.tc.k1 * (float)MT_GQ;
-        sll[v][threadIdx.x] += ll;
+        c2_sll[v][threadIdx.x] += ll;
         if (v) { f0B = f0; f1B = f1; } else { f0A = f0; f1A = f1; }
         macc *G = v ? GB : GA;
         const int m0 = min(v ? n0B : n0A, C2_RCAP), m1 = min(v ? n1B : n1A, C2_RCAP);
         for (int m = 0; m < m0 + m1; m++) {
           const int l = m >= m0;
-          const float4 q = rec[((2 * v + l) * C2_RCAP + (l ? m - m0 : m)) * C2_THREADS];
+          const float4 q = c2_recs[(2 * v + l) * C2_RCAP + (l ? m - m0 : m)][threadIdx.x];
           const float wv = (l ? f1 : f0) * q.w, u = q.y, vv = q.z, wa = wv * (1.f - u), wbb = wv * u;
           macc *pg = G + (l ? N * 32 : 0) + (__float_as_uint(q.x) << 5);
           atomicAdd(pg, q_raw(wa * (1.f - vv)));
@@ -1130,9 +1112,42 @@ __global__ void __launch_bounds__(C2_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
       }
     }
   }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(C2_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
+  int N = a.tc.N, oy = a.tc.ny * 32;
+  asm volatile("" : "+r"(N), "+r"(oy));   // keep in registers (no per-use reload / recompute)
+  const int lane = threadIdx.x & 31;
+  const int lin = blockIdx.y * gridDim.x + blockIdx.x, G2 = gridDim.y;
+  const int tile = lin / (G2 * C2_TILE), within = lin - tile * (G2 * C2_TILE);
+  const int g = within / C2_TILE, chunk = tile * C2_TILE + (within - (within / C2_TILE) * C2_TILE);
+  const int cA = g * 64 + lane, cB = cA + 32;
+  int acts = (cA < a.C ? 1 : 0) | (cB < a.C ? 2 : 0);
+  asm volatile("" : "+r"(acts));
+  const bool actA = acts & 1, actB = acts & 2;
+  // lane-union band of its two chains per surface; the warp walks the union over 64 chains
+  float4 bd = make_float4(3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f);
+  if (actA) bd = __ldg(a.band + cA);
+  if (actB) {
+    const float4 b = __ldg(a.band + cB);
+    bd = make_float4(fminf(bd.x, b.x), fmaxf(bd.y, b.y), fminf(bd.z, b.z), fmaxf(bd.w, b.w));
+  }
+  float zlo = bd.x, zhi = bd.w;
+  for (int o = 16; o > 0; o >>= 1) {
+    zlo = fminf(zlo, __shfl_xor_sync(0xffffffffu, zlo, o));
+    zhi = fmaxf(zhi, __shfl_xor_sync(0xffffffffu, zhi, o));
+  }
+  if (!actA && !actB) bd = make_float4(-3.0e38f, -3.0e38f, -3.0e38f, -3.0e38f);
+  const float4 *__restrict__ H4 = reinterpret_cast<const float4 *>(a.cl) + (size_t)g * 2 * N * 32 + lane;
+  asm volatile("mov.b64 %0, %0;" : "+l"(H4));
+  c2_sll[0][threadIdx.x] = 0.f;
+  c2_sll[1][threadIdx.x] = 0.f;
+  if (g * 64 + 64 <= a.C) c2_rays<MODE, true>(a, N, oy, g, chunk, acts, bd, zlo, zhi, H4);
+  else c2_rays<MODE, false>(a, N, oy, g, chunk, acts, bd, zlo, zhi, H4);
   if (MODE == TRACE_LL) {
-    if (actA) atomicAdd(a.ll + cA, q_ll(sll[0][threadIdx.x]));
-    if (actB) atomicAdd(a.ll + cB, q_ll(sll[1][threadIdx.x]));
+    if (actA) atomicAdd(a.ll + cA, q_ll(c2_sll[0][threadIdx.x]));
+    if (actB) atomicAdd(a.ll + cB, q_ll(c2_sll[1][threadIdx.x]));
   }
 }
 
@@ -1602,11 +1617,7 @@ static cudaError_t launch_v0_ny(const TraceArgs &a, int ny, dim3 grid, cudaStrea
 
 template <int MODE>
 static cudaError_t launch_c2(const TraceArgs &a, dim3 grid, cudaStream_t s) {
-  static size_t done[16] = {0};
-  const size_t smem = (size_t)16 * 4 * C2_RCAP * C2_THREADS;
-  cudaError_t e = set_smem(k_trace_c2<MODE>, smem, done);
-  if (e != cudaSuccess) return e;
-  k_trace_c2<MODE><<<grid, C2_THREADS, smem, s>>>(a);
+  k_trace_c2<MODE><<<grid, C2_THREADS, 0, s>>>(a);   // (records in static shared memory)
   return cudaGetLastError();
 }
 
