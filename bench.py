@@ -106,6 +106,16 @@ class ClockSampler:
                 continue
             rows.append(v)
         os.unlink(self.f.name)
+        post = False
+        if not rows:   # a timed region shorter than one 200-ms sample: query once, right after it
+            try:
+                out = subprocess.run(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=20).stdout
+                rows = [[t.strip() for t in ln.split(",")] for ln in out.splitlines()]
+                rows = [v for v in rows if len(v) >= 9 and (gpu_index is None or v[0] == str(gpu_index))]
+                post = True
+            except Exception:
+                rows = []
         if not rows:
             return None
         sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
@@ -113,8 +123,11 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].strip() == "Active"})
         load = [s for s in sm if s > 0.5 * max(sm)] if sm else []
-        return {"sm_mhz": statistics.median(load) if load else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+        ck = {"sm_mhz": statistics.median(load) if load else None,
+              "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+        if post:
+            ck["sampled"] = "once, right after the timed region (shorter than the 200-ms sampling period)"
+        return ck
 
 
 def cpu_baseline(seconds: float, chains: int = 4, name: str = "chain_sharded", nz: int = 0,

@@ -5,9 +5,9 @@ B=gpurun_out/benchall
 rm -f $B.*.log
 timeout 600 python bench.py > $B.default.log 2>&1
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $B.reference.log 2>&1
-for w in tiny small medium; do
-  timeout 600 python bench.py --workload $w --steps 20 > $B.$w.log 2>&1
-done
+timeout 600 python bench.py --workload tiny --steps 2000 > $B.tiny.log 2>&1
+timeout 600 python bench.py --workload small --steps 1000 > $B.small.log 2>&1
+timeout 600 python bench.py --workload medium --steps 20 > $B.medium.log 2>&1
 timeout 900 python bench.py --states prior > $B.prior.log 2>&1
 timeout 600 python bench.py --workload ray_sharded --steps 50 > $B.ray.log 2>&1
 timeout 600 python bench.py --model voxel > $B.voxel.log 2>&1
