@@ -528,16 +528,15 @@ __device__ __forceinline__ float epilogue(float tb, float cnt, const TraceConsts
   return -lam;
 }
 
-__device__ __forceinline__ void load_geometry(const TraceArgs &a, float *Xs, float *Ys, float *idx,
-                                              float *idy) {
+__device__ __forceinline__ void load_geometry(const TraceArgs &a) {   // -> sgeo (indexed directly)
   const int nx = a.tc.nx, ny = a.tc.ny;
   for (int k = threadIdx.x; k < nx; k += blockDim.x) {
-    Xs[k] = a.X[k];
-    idx[k] = k < nx - 1 ? 1.f / (a.X[k + 1] - a.X[k]) : 0.f;
+    sgeo[0][k] = a.X[k];
+    sgeo[2][k] = k < nx - 1 ? 1.f / (a.X[k + 1] - a.X[k]) : 0.f;
   }
   for (int k = threadIdx.x; k < ny; k += blockDim.x) {
-    Ys[k] = a.Y[k];
-    idy[k] = k < ny - 1 ? 1.f / (a.Y[k + 1] - a.Y[k]) : 0.f;
+    sgeo[1][k] = a.Y[k];
+    sgeo[3][k] = k < ny - 1 ? 1.f / (a.Y[k + 1] - a.Y[k]) : 0.f;
   }
 }
 
@@ -1165,7 +1164,7 @@ __global__ void __launch_bounds__(C2_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
 template <int MODE, int DG>
 __global__ void __launch_bounds__(MT_THREADS, DEFER_MINB) k_trace_defer(TraceArgs a) {
   __shared__ float4 wrec[MT_THREADS][4];   // per lane: up to 2 crossings per surface of its cell
-  load_geometry(a, sgeo[0], sgeo[1], sgeo[2], sgeo[3]);
+  load_geometry(a);
   __syncthreads();
   const int n = *(volatile int *)a.ovf_n;
   const int N = a.tc.N, ny = a.tc.ny;
@@ -1347,7 +1346,7 @@ __global__ void __launch_bounds__(MT_THREADS, MT_RL_MINB) k_trace_rl(TraceArgs a
     for (int k = tid; k < 2 * N; k += MT_THREADS) Hs[k] = __ldg(src + k);
   }
 #endif
-  load_geometry(a, sgeo[0], sgeo[1], sgeo[2], sgeo[3]);
+  load_geometry(a);
   const float4 bd = __ldg(a.band + c);
   const size_t coff = (size_t)(c >> 5) * 2 * N * 32 + (c & 31);
   macc *G0 = a.G + coff;

@@ -291,3 +291,17 @@ def test_work_counters_vs_brute_force(problems, oracle_problem):
                 n_cross += int(np.sum(np.sign(g[1:]) != np.sign(g[:-1])))
     assert cnt[0] == n_inbox and cnt[1] == n_band and cnt[2] == n_unres
     assert cnt[3] == n_cross, (cnt, n_cross)
+
+
+@pytest.mark.parametrize("name", ["tiny", "small"])
+def test_bulk_traversal_equals_the_per_ray_traversal(problems, oracle_problem, name):
+    """or_traversal_all (the bulk CSR the exhaustive GPU test compares against) is the
+    per-ray traversal (itself pinned by exact rational brute force above), ray by ray:
+    same cells in the same order, same exit parameters."""
+    op = oracle_problem(name)
+    off, ij, so = op.traversal_all()
+    assert off[0] == 0 and np.all(np.diff(off) >= 0)
+    for q in range(0, op.R, 1 if op.R <= 256 else 53):
+        ij_q, _, so_q = op.traversal(q)
+        assert np.array_equal(ij[off[q]:off[q + 1]], ij_q), q
+        assert np.array_equal(so[off[q]:off[q + 1]], so_q), q
