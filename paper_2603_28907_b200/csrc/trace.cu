@@ -35,7 +35,7 @@ namespace {
 #define MT_GTHR 0.05f
 #endif
 #ifndef MT_ZTHR
-#define MT_ZTHR 1e-3f
+#define MT_ZTHR 1e-4f
 #endif
 constexpr float GTHR = MT_GTHR;   // |g'| below which a crossing is re-solved in fp64
 constexpr float ZTHR = MT_ZTHR;   // near-tangent band (m) re-solved in fp64
@@ -1052,17 +1052,22 @@ __device__ __forceinline__ void c2_rays(const TraceArgs &a, int N, int oy, const
         const float f0 = dldO * a.tc.k0 * (float)MT_GQ, f1 = dldO * a.tc.k1 * (float)MT_GQ;
         c2_sll[v][threadIdx.x] += ll;
         if (v) { f0B = f0; f1B = f1; } else { f0A = f0; f1A = f1; }
-        macc *G = v ? GB : GA;
-        const int m0 = min(v ? n0B : n0A, C2_RCAP), m1 = min(v ? n1B : n1A, C2_RCAP);
-        for (int m = 0; m < m0 + m1; m++) {
-          const int l = m >= m0;
-          const float4 q = c2_recs[(2 * v + l) * C2_RCAP + (l ? m - m0 : m)][threadIdx.x];
-          const float wv = (l ? f1 : f0) * q.w, u = q.y, vv = q.z, wa = wv * (1.f - u), wbb = wv * u;
-          macc *pg = G + (l ? N * 32 : 0) + (__float_as_uint(q.x) << 5);
-          atomicAdd(pg, q_raw(wa * (1.f - vv)));
-          atomicAdd(pg + oy, q_raw(wbb * (1.f - vv)));
-          atomicAdd(pg + 32, q_raw(wa * vv));
-          atomicAdd(pg + oy + 32, q_raw(wbb * vv));
+#pragma unroll
+        for (int l = 0; l < 2; l++) {   // records of surface l: slots (2v + l) RCAP + m, m < min(n, RCAP)
+          const int ml = min(l ? (v ? n1B : n1A) : (v ? n0B : n0A), C2_RCAP);
+          const float fl = l ? f1 : f0;
+          macc *Gl = (v ? GB : GA) + (l ? N * 32 : 0);
+#pragma unroll
+          for (int m = 0; m < C2_RCAP; m++) {
+            if (m >= ml) break;
+            const float4 q = c2_recs[(2 * v + l) * C2_RCAP + m][threadIdx.x];
+            const float wv = fl * q.w, u = q.y, vv = q.z, wa = wv * (1.f - u), wbb = wv * u;
+            macc *pg = Gl + (__float_as_uint(q.x) << 5);
+            atomicAdd(pg, q_raw(wa * (1.f - vv)));
+            atomicAdd(pg + oy, q_raw(wbb * (1.f - vv)));
+            atomicAdd(pg + 32, q_raw(wa * vv));
+            atomicAdd(pg + oy + 32, q_raw(wbb * vv));
+          }
         }
       }
       if (__any_sync(0xffffffffu, overA || overB)) {   // wide bands: re-walk, scatter crossings m >= RCAP

@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/pytest_full2.log 2>&1; echo "rc $?" >> gpurun_out/pytest_full2.log
-CFG_LIST="ray_sharded" bash tools/gpu_r2.sh rlsm notest default rlsm default rlsm
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke2.log 2>&1; echo "rc $?" >> gpurun_out/smoke2.log
+bash tools/gpu_r2.sh pk1 notest default prev default prev
+timeout 1200 python -m pytest tests/test_gpu_exhaustive.py tests/test_gpu_launch_shapes.py tests/test_gpu_dist.py -m gpu -q > gpurun_out/pytest_pk1.log 2>&1; echo "rc $?" >> gpurun_out/pytest_pk1.log
