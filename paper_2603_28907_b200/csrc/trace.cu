@@ -386,9 +386,6 @@ __device__ __forceinline__ void piece64(const TraceArgs &a, const Ray &r, int k,
 #ifndef MT_RCAP
 #define MT_RCAP 3
 #endif
-#ifndef RL_ADDR32
-#define RL_ADDR32 0
-#endif
 #ifndef MT_RL_GLOBAL_H
 #define MT_RL_GLOBAL_H 1
 #endif
@@ -1345,7 +1342,6 @@ __global__ void __launch_bounds__(MT_THREADS, MT_RL_MINB) k_trace_rl(TraceArgs a
   // the chain's heights straight from global memory (L1-resident: 2N floats);
   // shared memory holds only the crossing records, so more blocks fit per SM
   const float *__restrict__ Hs = Hc + (size_t)c * 2 * N;
-  const int hc0 = c * 2 * N;   // (RL_ADDR32: 32-bit element offsets from the kernel parameter)
   float4 *rec = reinterpret_cast<float4 *>(smem) + tid;                        // [2*RCAP][MT_THREADS]
 #else
   float *Hs = smem;                                                            // [2N]
@@ -1474,20 +1470,12 @@ __global__ void __launch_bounds__(MT_THREADS, MT_RL_MINB) k_trace_rl(TraceArgs a
           const int base = i * ny + j, w = base << 5;
           if (zb <= bd.x) B0 += Ls;
           else if (za < bd.y) {
-#if RL_ADDR32
-            const float *p = Hc + (unsigned)(hc0 + base);
-#else
             const float *p = Hs + base;
-#endif
             cw_solve<0>(make_float4(p[0], p[1], p[ny], p[ny + 1]), w, cg, za, zb, Ls, dz, B0, n0, defer, rec);
           }
           if (zb <= bd.z) B1 += Ls;
           else if (za < bd.w) {
-#if RL_ADDR32
-            const float *p = Hc + (unsigned)(hc0 + N + base);
-#else
             const float *p = Hs + N + base;
-#endif
             cw_solve<1>(make_float4(p[0], p[1], p[ny], p[ny + 1]), w, cg, za, zb, Ls, dz, B1, n1, defer, rec);
           }
           if (s1 >= s_hi) break;

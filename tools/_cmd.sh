@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-bash tools/gpu_r2.sh pk1 notest default prev default prev
-timeout 1200 python -m pytest tests/test_gpu_exhaustive.py tests/test_gpu_launch_shapes.py tests/test_gpu_dist.py -m gpu -q > gpurun_out/pytest_pk1.log 2>&1; echo "rc $?" >> gpurun_out/pytest_pk1.log
+bash tools/gpu_r2.sh unp1 notest default unp default unp
+CFG_LIST="ray_sharded" bash tools/gpu_r2.sh ra1 notest default ra32 default ra32
