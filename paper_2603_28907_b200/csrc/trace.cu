@@ -403,9 +403,6 @@ __device__ __forceinline__ void piece64(const TraceArgs &a, const Ray &r, int k,
 #ifndef MT_CL_MINB
 #define MT_CL_MINB 5
 #endif
-#ifndef MT_CACC
-#define MT_CACC 0
-#endif
 #ifndef V0_SOLVE
 #define V0_SOLVE 1
 #endif
@@ -1645,14 +1642,6 @@ static cudaError_t launch_rl_ny(const TraceArgs &a, const float *Hc, int ny, dim
     case 64: return launch_rl<MODE, 64>(a, Hc, grid, smem, s);
     default: return launch_rl<MODE, 0>(a, Hc, grid, smem, s);
   }
-}
-
-static int64_t pick_splits(const mt_problem *p, int64_t groups, int64_t blocks_per_sm) {
-  if (p->trace_s > 0) return p->trace_s;
-  int64_t target = (int64_t)p->num_sms * blocks_per_sm * 4;   // ~4 waves of resident blocks
-  int64_t S = (target + groups - 1) / groups;
-  int64_t max_s = (p->R + 63) / 64;
-  return S < 1 ? 1 : (S > max_s ? max_s : S);
 }
 
 cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const float4 *band,
