@@ -208,9 +208,10 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
             "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64", "impl": "reference",
             "data": "synthetic (seeded Medium geometry; counts = Poisson of the oracle's truth)",
-            "config": {"workload": "chain_sharded HMC iteration (Medium geometry)", "chains": Cs,
-                       "rays": op.R, "leapfrog_steps": L, "params": op.P,
-                       "sample": f"{Cs} of the {args.chains_total} chains"},
+            "config": {"workload": ("chain_sharded HMC iteration (BASELINE configs[3]: Medium geometry and rays, "
+                                    f"{args.chains_total} chains over {args.gpus} GPU(s))"),
+                       "global_chains": args.chains_total, "rays": op.R, "leapfrog_steps": L, "params": op.P,
+                       "sample": f"{Cs} of the {args.chains_total} chains per timed HMC iteration (fp64 oracle)"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
                              "sample": f"{Cs} chains x {op.R} rays x {L} leapfrog steps per HMC iteration"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
