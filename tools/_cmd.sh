@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-bash tools/gpu_r2.sh qe1 notest default qf ex default qf ex
+bash tools/gpu_r2.sh pf1 notest default pf default pf
