@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-bash tools/gpu_r2.sh pf1 notest default pf default pf
+bash tools/gpu_r2.sh pp1 notest default pp default pp
