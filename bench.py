@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--chains-per-gpu", type=int, default=1024)
     ap.add_argument("--leapfrog", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="replay each timed HMC step from a CUDA graph (auto: HMC without a ray-shard communicator)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
@@ -295,8 +297,12 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        shard.step(adapt=False, sample=True, monitor=True)
+    use_graph = args.graph == "on" or (args.graph == "auto" and args.sampler == "hmc" and not (ray and ws > 1))
+    for w in range(args.warmup):   # (graph mode: the first warm-up step runs eagerly, then capture + replays)
+        if use_graph and w > 0:
+            shard.step_graph(sample=True, monitor=True)
+        else:
+            shard.step(adapt=False, sample=True, monitor=True)
     barrier()
     l2_peak = None
     if voxel:
@@ -312,7 +318,10 @@ def main():
     for k in range(args.steps):
         flush.zero_()
         ev[k][0].record()
-        shard.step(adapt=False, sample=True, monitor=True)
+        if use_graph:
+            shard.step_graph(sample=True, monitor=True)
+        else:
+            shard.step(adapt=False, sample=True, monitor=True)
         ev[k][1].record()
     barrier()
     wall = time.perf_counter() - wall0
@@ -321,6 +330,19 @@ def main():
     tm = pb.timing_read()
     cnt = pb.trace_counters()
     gathered = (pb.voxel_gathered_bytes() - g0) if voxel else 0
+    if use_graph:
+        # graph replays carry no host-side counters or per-launch events: the evaluations
+        # are L per step, the launches those of one captured step, and the per-launch
+        # kernel times come from one eager calibration step after the timed region
+        evals_g = args.steps * L
+        pb.timing_start(L + 8)
+        shard.step(adapt=False, sample=True, monitor=True)
+        torch.cuda.synchronize()
+        cal, cal_cnt = pb.timing_read(), pb.trace_counters()
+        per = 1.0 / max(cal["trace_launches"], 1)
+        tm = {"trace_ms": cal["trace_ms"] * per * evals_g, "trace_launches": evals_g,
+              "all_launches": shard.launches_per_graph_step * args.steps}
+        cnt = {"deferred": cnt["deferred"], "defer_ms": cal_cnt["defer_ms"] * per * evals_g}
     t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -460,7 +482,10 @@ def main():
                        "phase": "sampling (fixed eps from the 100-iteration dual-averaging warm-up, "
                                 "tools/tune_eps.py; Welford + all-reduced acceptance sums each step)",
                        "eps": eps,
-                       "l2": "flushed between timed steps (256 MiB write, outside the events)"},
+                       "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                       "launch": ("each step replayed from a CUDA graph (ChainShard.step_graph); per-launch kernel "
+                                  "times from one eager step after the timed region") if use_graph else
+                                 "eager launches"},
             "roofline": roofline, "cpu_baseline": base, "e2e": e2e, "clocks": ck,
             "gpu_launches": tm["all_launches"],
             "leapfrog_steps_per_s_per_chain": evals / (t_ms * 1e-3),

@@ -257,6 +257,18 @@ int mt_nested_rhat_partials(mt_problem *p, int32_t C, int32_t M, const float *me
 int mt_summary_update(mt_problem *p, int32_t C, const float *x, const double *logp, int32_t nz, float gap,
                       double *acc, float *map_x, double *map_logp, mt_stream stream);
 
+/* Device-side step counters, for capturing a sampling step in a CUDA graph (a
+ * captured launch keeps the host scalars it was captured with):
+ *   iter    DEVICE uint64 [1] or NULL: mt_hmc_step then takes the Philox iteration
+ *           (R22) from *iter instead of its `iter` argument, and adds 1 to *iter at
+ *           the end of the step (in stream order);
+ *   n_prev  DEVICE int32 [1] or NULL: mt_stats_update's Welford update then takes
+ *           the count from *n_prev instead of its `n_prev` argument and adds 1.
+ * Caller-owned; NULL restores the host arguments.  The results are those of the
+ * host-argument calls with the same values (tests/test_gpu_graph.py).
+ * Errors: MT_EINVAL (p NULL). */
+int mt_set_step_counters(mt_problem *p, uint64_t *iter, int32_t *n_prev);
+
 /* The summaries from the accumulators of mt_summary_update (R27):
  *   acc  DEVICE double, as filled by mt_summary_update (acc[0] >= 1 draws).
  *   out  DEVICE double [3N + 3 N nz], caller-owned:

@@ -45,7 +45,8 @@ EXPORTS = [
     "mt_stats_update", "mt_rhat_partials", "mt_heights", "mt_loglik_heights", "mt_path_lengths", "mt_debug_traversal", "mt_traversal_all", "mt_ray_work", "mt_ray_cost", "mt_nuts_record", "mt_philox",
     "mt_philox_curand", "mt_timing_start", "mt_timing_read", "mt_trace_counters", "mt_measure_fp32_peak",
     "mt_last_error", "mt_comm_unique_id", "mt_attach_comm", "mt_detach_comm", "mt_nuts_step",
-    "mt_nested_rhat_partials", "mt_summary_update", "mt_summary_finalize", "mt_voxel_model", "mt_voxel_info",
+    "mt_nested_rhat_partials", "mt_summary_update", "mt_summary_finalize", "mt_set_step_counters",
+    "mt_voxel_model", "mt_voxel_info",
     "mt_voxel_counters", "mt_measure_l2_gather", "mt_set_inverse_mass",
 ]
 
@@ -75,6 +76,7 @@ def lib():
             "mt_nested_rhat_partials": ([vp, i32, i32, vp, vp, i32, vp, vp], ct.c_int),
             "mt_summary_update": ([vp, i32, vp, vp, i32, ct.c_float, vp, vp, vp, vp], ct.c_int),
             "mt_summary_finalize": ([vp, i32, vp, vp, vp], ct.c_int),
+            "mt_set_step_counters": ([vp, vp, vp], ct.c_int),
             "mt_heights": ([vp, i32, vp, vp, vp], ct.c_int),
             "mt_loglik_heights": ([vp, i32, vp, vp, vp, vp], ct.c_int),
             "mt_path_lengths": ([vp, i32, vp, vp, vp, vp], ct.c_int),
@@ -275,6 +277,17 @@ class Problem:
         """a9: fixed-point acceptance sums (int64 [2]) and Welford mean/M2 of x."""
         _check(lib().mt_stats_update(self.h, C, _ptr(x), _ptr(accept_prob), n_prev, _ptr(mean), _ptr(m2),
                                      _ptr(acc_fixed), _stream(stream)), "mt_stats_update")
+
+    def set_step_counters(self, iter_dev=None, n_prev_dev=None):
+        """Device step counters for CUDA-graph capture (mt_set_step_counters): int64 [1]
+        Philox iteration read and advanced by mt_hmc_step, int32 [1] Welford count read
+        and advanced by mt_stats_update; None restores the host arguments."""
+        import torch
+        if iter_dev is not None:
+            _dev_tensor(iter_dev, torch.int64, (1,), self.device, "iter")
+        if n_prev_dev is not None:
+            _dev_tensor(n_prev_dev, torch.int32, (1,), self.device, "n_prev")
+        _check(lib().mt_set_step_counters(self.h, _ptr(iter_dev), _ptr(n_prev_dev)), "mt_set_step_counters")
 
     def rhat_partials(self, C: int, mean, m2, n: int, out=None, stream=None):
         import torch

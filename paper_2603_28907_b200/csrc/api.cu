@@ -567,6 +567,13 @@ int mt_summary_update(mt_problem *p, int32_t C, const float *x, const double *lo
   return MT_OK;
 }
 
+int mt_set_step_counters(mt_problem *p, uint64_t *iter, int32_t *n_prev) {
+  if (!p) return set_err(MT_EINVAL, "problem is NULL");
+  p->d_iter = iter;
+  p->d_nprev = n_prev;
+  return MT_OK;
+}
+
 int mt_summary_finalize(mt_problem *p, int32_t nz, const double *acc, double *out, mt_stream stream) {
   if (!p) return set_err(MT_EINVAL, "problem is NULL");
   if (nz < 1) return set_err(MT_EINVAL, "nz = %d < 1", nz);

@@ -503,8 +503,10 @@ __global__ void __launch_bounds__(MT_THREADS) k_kick_mb(FinishArgs a, MbScratch 
 __global__ void __launch_bounds__(MT_THREADS) k_hmc_begin(FinishArgs a, const double *logp,
                                                           float *x0s, float *g0s, double *lp0,
                                                           float *kin0, uint64_t seed,
-                                                          uint64_t iter, uint64_t chain_offset) {
+                                                          uint64_t iter, uint64_t chain_offset,
+                                                          const uint64_t *iter_dev) {
   const int c = blockIdx.x, N = a.N, P = a.P;
+  if (iter_dev) iter = *iter_dev;   // device step counter (graph replay)
   float *xc = a.x + (size_t)c * P, *pc = a.mom + (size_t)c * P;
   const float *gc = a.grad + (size_t)c * P;
   const float eps = a.eps[c];
@@ -568,8 +570,9 @@ __global__ void __launch_bounds__(MT_THREADS) k_hmc_end(FinishArgs a, const floa
                                                         const float *kin0, const float *kin1,
                                                         uint64_t seed, uint64_t iter,
                                                         uint64_t chain_offset, float *acc_prob,
-                                                        int32_t *accepted) {
+                                                        int32_t *accepted, const uint64_t *iter_dev) {
   __shared__ int s_acc;
+  if (iter_dev) iter = *iter_dev;
   const int c = blockIdx.x, P = a.P;
   if (threadIdx.x == 0) {
     double H0 = -lp0[c] + (double)kin0[c];
@@ -1007,7 +1010,7 @@ cudaError_t launch_hmc_begin(mt_problem *p, int C, float *x, const double *logp,
   FinishArgs a = base_args(p, C);
   a.x = x; a.mom = p->d_mom; a.grad = const_cast<float *>(grad); a.eps = eps;
   k_hmc_begin<<<C, MT_THREADS, 0, s>>>(a, logp, p->d_x0, p->d_g0, p->d_lp0, p->d_kin0, seed, iter,
-                                       chain_offset);
+                                       chain_offset, p->d_iter);
   p->all_launches++;
   if (p->ncp) {   // heights of the drifted z (k_hmc_begin skipped them)
     launch_ncp_heights(p, a, C, x, s);
@@ -1022,8 +1025,13 @@ cudaError_t launch_hmc_end(mt_problem *p, int C, float *x, double *logp, float *
   FinishArgs a = base_args(p, C);
   a.x = x; a.logp = logp; a.grad = grad; a.status = status;
   k_hmc_end<<<C, MT_THREADS, 0, s>>>(a, p->d_x0, p->d_g0, p->d_lp0, p->d_kin0, p->d_kin1, seed,
-                                     iter, chain_offset, acc_prob, accepted);
+                                     iter, chain_offset, acc_prob, accepted, p->d_iter);
   p->all_launches++;
+  if (p->d_iter) {   // the step's Philox iteration is used: advance the device counter
+    cudaError_t e = launch_counter_add(p->d_iter, nullptr, s);
+    if (e != cudaSuccess) return e;
+    p->all_launches++;
+  }
   return cudaGetLastError();
 }
 

@@ -193,6 +193,8 @@ struct mt_problem {
   double *d_cs = nullptr;       // [N] torus spectrum table (sample_r)
   int ncp = 0;                  // f2 non-centred parameterisation (implies sample_r)
   float *d_minv = nullptr;      // [P] diagonal inverse mass (null until mt_set_inverse_mass)
+  uint64_t *d_iter = nullptr;   // device step counters (mt_set_step_counters, caller-owned): Philox
+  int32_t *d_nprev = nullptr;   //   iteration of mt_hmc_step, Welford count of mt_stats_update
   float *d_xalt = nullptr;      // [max_chains][P] second x buffer of the group-tiled K3 leapfrog
   void *d_fin_part = nullptr;   // group-tiled K3 per-tile partials [groups][tiles][32] (FinPart, 48 B)
   unsigned *d_fin_ticket = nullptr;   // [groups] last-block tickets
@@ -306,6 +308,7 @@ cudaError_t launch_tile(mt_problem *p, int C, const float *src, float *dst, int 
                         cudaStream_t s);
 cudaError_t launch_take_acc(mt_problem *p, int C, float *dldH, double *ll, cudaStream_t s);
 cudaError_t launch_summary_finalize(mt_problem *p, int nz, const double *acc, double *out, cudaStream_t s);
+cudaError_t launch_counter_add(uint64_t *iter, int32_t *nprev, cudaStream_t s);   // stats.cu
 cudaError_t launch_summary(mt_problem *p, int C, const float *x, const double *logp, int nz, float gap,
                            double *acc, float *map_x, double *map_logp, cudaStream_t s);
 cudaError_t launch_nested_rhat_partials(mt_problem *p, int C, int M, const float *mean, const float *m2,

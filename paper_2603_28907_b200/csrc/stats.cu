@@ -25,9 +25,11 @@ __global__ void k_accept_sum(int C, const float *acc, unsigned long long *out) {
   }
 }
 
-__global__ void k_welford(int64_t n, const float4 *x, float4 *mean, float4 *m2, float inv_cnt) {
+__global__ void k_welford(int64_t n, const float4 *x, float4 *mean, float4 *m2, float inv_cnt,
+                          const int32_t *nprev_dev) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
+  if (nprev_dev) inv_cnt = 1.0f / (float)(*nprev_dev + 1);   // device step counter (graph replay)
   float4 v = x[t], m = mean[t], s = m2[t];
   float d0 = v.x - m.x, d1 = v.y - m.y, d2 = v.z - m.z, d3 = v.w - m.w;
   m.x += d0 * inv_cnt; m.y += d1 * inv_cnt; m.z += d2 * inv_cnt; m.w += d3 * inv_cnt;
@@ -36,9 +38,11 @@ __global__ void k_welford(int64_t n, const float4 *x, float4 *mean, float4 *m2, 
   m2[t] = s;
 }
 
-__global__ void k_welford_scalar(int64_t n, const float *x, float *mean, float *m2, float inv_cnt) {
+__global__ void k_welford_scalar(int64_t n, const float *x, float *mean, float *m2, float inv_cnt,
+                                 const int32_t *nprev_dev) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
+  if (nprev_dev) inv_cnt = 1.0f / (float)(*nprev_dev + 1);
   float v = x[t], m = mean[t];
   float d = v - m;
   m += d * inv_cnt;
@@ -220,6 +224,18 @@ cudaError_t launch_summary(mt_problem *p, int C, const float *x, const double *l
   return cudaGetLastError();
 }
 
+// Device step counters (mt_set_step_counters): +1 on the Philox iteration and / or the
+// Welford count, inside the captured step.
+__global__ void k_counter_add(uint64_t *iter, int32_t *nprev) {
+  if (iter) *iter += 1;
+  if (nprev) *nprev += 1;
+}
+
+cudaError_t launch_counter_add(uint64_t *iter, int32_t *nprev, cudaStream_t s) {
+  k_counter_add<<<1, 1, 0, s>>>(iter, nprev);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_stats(mt_problem *p, int C, const float *x, const float *acc, int32_t n_prev,
                          float *mean, float *m2, unsigned long long *acc_fixed, cudaStream_t s) {
   if (C <= 0) return cudaSuccess;
@@ -234,11 +250,15 @@ cudaError_t launch_stats(mt_problem *p, int C, const float *x, const float *acc,
       int64_t n4 = n / 4;
       k_welford<<<(unsigned)((n4 + 255) / 256), 256, 0, s>>>(
           n4, reinterpret_cast<const float4 *>(x), reinterpret_cast<float4 *>(mean),
-          reinterpret_cast<float4 *>(m2), inv);
+          reinterpret_cast<float4 *>(m2), inv, p->d_nprev);
     } else {
-      k_welford_scalar<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, x, mean, m2, inv);
+      k_welford_scalar<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, x, mean, m2, inv, p->d_nprev);
     }
     p->all_launches++;
+    if (p->d_nprev) {   // advance the device count after this update
+      k_counter_add<<<1, 1, 0, s>>>(nullptr, p->d_nprev);
+      p->all_launches++;
+    }
   }
   return cudaGetLastError();
 }

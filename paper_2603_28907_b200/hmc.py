@@ -294,6 +294,50 @@ class ChainShard:
         self.it += 1
         return alpha
 
+    def step_graph(self, sample: bool = True, monitor: bool = True) -> None:
+        """One sampling iteration (no adaptation), replayed from a CUDA graph: the
+        step's ~4L + 5 launches reach the GPU as one graph launch, which matters where
+        launches dominate (the small configs).  The Philox iteration and the Welford
+        count live on the device (mt_set_step_counters) and advance inside the graph,
+        so every replay is the next iteration and the results equal those of
+        step(adapt=False, sample, monitor) bit for bit (tests/test_gpu_graph.py).
+        HMC without a ray-shard communicator; the graph is captured on first use and
+        again when the flags change.  launches_per_graph_step: the library launches
+        one replay performs."""
+        torch = self.torch
+        if self.sampler != "hmc":
+            raise ValueError("step_graph: HMC only")
+        key = (sample, monitor)
+        if getattr(self, "_graph_key", None) != key:
+            if getattr(self, "_it_dev", None) is None:
+                self._it_dev = torch.zeros(1, dtype=torch.int64, device=self.dev)
+                self._n_dev = torch.zeros(1, dtype=torch.int32, device=self.dev)
+            cur = torch.cuda.current_stream(self.dev) if self.stream is None else self.stream
+            s = torch.cuda.Stream(device=self.dev)
+            with torch.cuda.stream(cur):
+                self._it_dev.fill_(self.it)
+                self._n_dev.fill_(self.n_samples)
+            s.wait_stream(cur)
+            self.pb.set_step_counters(self._it_dev, self._n_dev)
+            self.pb.timing_start(0)   # (counts the launches captured below; records no events)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                self.pb.hmc_step(self.x, self.logp, self.grad, self.eps, self.L, self.seed, self.it,
+                                 self.chain_offset, self.acc_prob, self.accepted, self.status, stream=s)
+                if monitor:
+                    self.pb.stats_update(self.C, accept_prob=self.acc_prob, acc_fixed=self.acc_mon, stream=s)
+                if sample:
+                    self.pb.stats_update(self.C, x=self.x, n_prev=self.n_samples, mean=self.mean, m2=self.m2,
+                                         stream=s)
+            self.launches_per_graph_step = self.pb.timing_read()["all_launches"]
+            cur.wait_stream(s)
+            self._graph, self._graph_key = g, key
+        with self._ctx():
+            self._graph.replay()
+        self.it += 1
+        if sample:
+            self.n_samples += 1
+
     def accept_rate(self, reset: bool = True) -> float:
         """All-rank mean acceptance over the monitored iterations since the last reset
         (one host read)."""
