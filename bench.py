@@ -431,14 +431,17 @@ def main():
             shard.x.copy_(xh, non_blocking=True)
             shard.grad.copy_(gh, non_blocking=True)
             shard.logp.copy_(lph, non_blocking=True)
-            shard.step(adapt=False, sample=True, monitor=True)
+            if use_graph:
+                shard.step_graph(sample=True, monitor=True)
+            else:
+                shard.step(adapt=False, sample=True, monitor=True)
             xh.copy_(shard.x, non_blocking=True)
             gh.copy_(shard.grad, non_blocking=True)
             lph.copy_(shard.logp, non_blocking=True)
             aph.copy_(shard.acc_prob, non_blocking=True)
         e1.record()
         barrier()
-        evals_e2e = pb.timing_read()["trace_launches"]
+        evals_e2e = args.steps * L if use_graph else pb.timing_read()["trace_launches"]
         te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
         if dist is not None:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
