@@ -285,7 +285,7 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
   if (p->ncp) ALLOC(p->d_xw, sizeof(double) * MC * 2 * p->N);
   if (!getenv("MT_NO_FG")) {   // group-tiled K3: second x buffer, per-tile partials, tickets
     ALLOC(p->d_xalt, sizeof(float) * MC * P);
-    ALLOC(p->d_fin_part, (size_t)48 * MC32 * ((p->N + 63) / 64));
+    ALLOC(p->d_fin_part, (size_t)48 * MC32 * ((p->N + 15) / 16));   // (tiles of >= 16 nodes)
     ALLOC(p->d_fin_ticket, sizeof(unsigned) * (MC32 / 32));
   }
   if (!getenv("MT_NO_MB")) {   // few-chain multi-block K3 / kick scratch (use_mb)

@@ -126,7 +126,9 @@ __global__ void __launch_bounds__(MT_THREADS) k_finish(FinishArgs a) {
 // the result does not depend on block scheduling (R30).  Per-node arithmetic
 // is k_finish's, operation for operation.
 // ---------------------------------------------------------------------------
-#define FG_T 64   // nodes per tile
+// nodes per tile: 64 for the plain K3, 32 for the fused leapfrog (STEP / LAST hold
+// momenta and gradient tiles too: 32-node tiles keep 4 blocks per SM, 0.35 vs 0.41 ms)
+template <int MODE> struct FgTile { static constexpr int T = MODE == FIN_PLAIN ? 64 : 32; };
 struct FinPart {   // 48 B: float4 band | double2 (prior, kinetic) sums | non-finite flag
   float mn0, mx0, mn1, mx1;
   double s0, s1;
@@ -134,7 +136,8 @@ struct FinPart {   // 48 B: float4 band | double2 (prior, kinetic) sums | non-fi
 };
 
 template <int MODE>
-__global__ void __launch_bounds__(MT_THREADS, 3) k_finish_g(FinishArgs a, FinPart *part, unsigned *ticket) {
+__global__ void __launch_bounds__(MT_THREADS, 4) k_finish_g(FinishArgs a, FinPart *part, unsigned *ticket) {
+  constexpr int FG_T = FgTile<MODE>::T;
   extern __shared__ float fsm[];
   const int N = a.N, ny = a.ny, P = a.P;
   const int tile = blockIdx.x, g = blockIdx.y, ntile = gridDim.x;
@@ -901,6 +904,7 @@ bool use_fg(const mt_problem *p, int C) {
 template <int MODE>
 static cudaError_t launch_fg(mt_problem *p, const FinishArgs &a, int C, cudaStream_t s) {
   static size_t done[64] = {};
+  constexpr int FG_T = FgTile<MODE>::T;
   const int W = FG_T + 2 * p->ny;
   const size_t smem = sizeof(float) * 33 * (2 * (size_t)W + 2 * FG_T * (MODE == FIN_PLAIN ? 1 : 2));
   const int dv = p->device & 63;
