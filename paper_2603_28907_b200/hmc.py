@@ -321,7 +321,9 @@ class ChainShard:
             self.pb.set_step_counters(self._it_dev, self._n_dev)
             self.pb.timing_start(0)   # (counts the launches captured below; records no events)
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=s):
+            # thread-local capture: other threads' CUDA calls (e.g. an NCCL process group's
+            # watchdog under torchrun) must not invalidate the capture
+            with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
                 self.pb.hmc_step(self.x, self.logp, self.grad, self.eps, self.L, self.seed, self.it,
                                  self.chain_offset, self.acc_prob, self.accepted, self.status, stream=s)
                 if monitor:
