@@ -894,6 +894,12 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_v0(TraceArgs a
 #ifndef C2_RCAP
 #define C2_RCAP 2
 #endif
+#ifndef C2_PREF
+#define C2_PREF 0   // experiment: next ray's header loaded one ray ahead
+#endif
+#ifndef C2_WIN
+#define C2_WIN 0    // experiment: band cell words by one coalesced load + shuffles
+#endif
 #ifndef C2_THREADS
 #define C2_THREADS 256   // threads per block of k_trace_c2
 #endif
@@ -984,20 +990,61 @@ __device__ __forceinline__ void c2_rays(const TraceArgs &a, int N, int oy, const
   const bool actA = FULL || (acts & 1), actB = FULL || (acts & 2);
   const int r_begin = chunk * (int)a.rays_per_block;
   const int r_end = min((int)a.R, r_begin + (int)a.rays_per_block);
+#if C2_PREF
+  // the next ray's header (ray constants, traversal range) loaded one ray ahead
+  float2 nrb = make_float2(1.f, 0.f);
+  int nk0 = 0, nk1 = 0;
+  if (r_begin + warp < r_end) {
+    nrb = __ldg(reinterpret_cast<const float2 *>(a.ray_b + r_begin + warp));
+    if (C2_PREF == 1) {
+      nk0 = __ldg(a.trav_off + r_begin + warp);
+      nk1 = __ldg(a.trav_off + r_begin + warp + 1);
+    }
+  }
+#endif
   for (int rr = r_begin + warp; rr < r_end; rr += C2_THREADS / 32) {
+#if C2_PREF
+    const float2 rb0 = nrb;
+    const int kbeg = C2_PREF == 1 ? nk0 : __ldg(a.trav_off + rr), kend = C2_PREF == 1 ? nk1 : __ldg(a.trav_off + rr + 1);
+    if (rr + C2_THREADS / 32 < r_end) {
+      nrb = __ldg(reinterpret_cast<const float2 *>(a.ray_b + rr + C2_THREADS / 32));
+      if (C2_PREF == 1) {
+        nk0 = __ldg(a.trav_off + rr + C2_THREADS / 32);
+        nk1 = __ldg(a.trav_off + rr + C2_THREADS / 32 + 1);
+      }
+    }
+#else
     const float2 rb0 = __ldg(reinterpret_cast<const float2 *>(a.ray_b + rr));
+#endif
     const float dz = rb0.x, s_exit = rb0.y;
     const float s_lo = fminf(__fdividef(zlo, dz) * (1.f - 1e-6f), s_exit);
     const float s_hi = fminf(__fdividef(zhi, dz) * (1.f + 1e-6f), s_exit);
     float B0A = s_lo, B1A = s_lo, B0B = s_lo, B1B = s_lo;
     unsigned cnt = 0;   // packed counters / defer flags (c2_cellp)
     if (s_lo < s_exit) {
-      const int kend = __ldg(a.trav_off + rr + 1);
+#if !C2_PREF
+      const int kend = __ldg(a.trav_off + rr + 1), kbeg = __ldg(a.trav_off + rr);
+#endif
       float s_in0;
-      const int k0 = band_entry_warp(a.trav, __ldg(a.trav_off + rr), kend, s_lo, s_in0);
+      const int k0 = band_entry_warp(a.trav, kbeg, kend, s_lo, s_in0);
       float s = s_lo, za = s_lo * dz, ds = s_lo - s_in0;
+#if C2_WIN
+      // the band's cell words, one per lane, from one coalesced load (broadcast per cell by shuffle)
+      int2 wl = make_int2(0, 0);
+      if (k0 + lane < kend) wl = __ldg(a.trav + k0 + lane);
+#endif
       for (int k = k0; k < kend; k++) {
+#if C2_WIN
+        int2 w;
+        if (k - k0 < 32) {
+          w.x = __shfl_sync(0xffffffffu, wl.x, k - k0);
+          w.y = __shfl_sync(0xffffffffu, wl.y, k - k0);
+        } else {
+          w = __ldg(a.trav + k);
+        }
+#else
         const int2 w = __ldg(a.trav + k);
+#endif
         const float4 cg = shift_geo(__ldg(a.trav_geo + k), ds);
         float2 km = __ldg(a.trav_km + k);
         km.x = fmaf(2.f * km.y, ds, km.x);
@@ -1616,8 +1663,21 @@ static cudaError_t launch_v0_ny(const TraceArgs &a, int ny, dim3 grid, cudaStrea
   }
 }
 
+#ifndef C2_CARVE
+#define C2_CARVE -1   // preferred shared-memory carveout (percent) of k_trace_c2; -1: driver default
+#endif
 template <int MODE>
 static cudaError_t launch_c2(const TraceArgs &a, dim3 grid, cudaStream_t s) {
+  if (C2_CARVE >= 0) {
+    static bool done[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!done[dev & 63]) {
+      cudaError_t e = cudaFuncSetAttribute(k_trace_c2<MODE>, cudaFuncAttributePreferredSharedMemoryCarveout, C2_CARVE);
+      if (e != cudaSuccess) return e;
+      done[dev & 63] = true;
+    }
+  }
   k_trace_c2<MODE><<<grid, C2_THREADS, 0, s>>>(a);   // (records in static shared memory)
   return cudaGetLastError();
 }
