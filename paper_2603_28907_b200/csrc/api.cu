@@ -234,7 +234,16 @@ int mt_problem_create(const mt_problem_desc *d, mt_problem **out) {
       for (int b = 0; b < 16; b++) m |= (uint64_t)((ci >> b) & 1) << (2 * b) | (uint64_t)((cj >> b) & 1) << (2 * b + 1);
       key[q] = (m << 32) | (uint64_t)q;
     }
-    std::sort(p->perm.begin(), p->perm.end(), [&](int32_t a, int32_t b) { return key[a] < key[b]; });
+    // MT_ORDER_DET=1 (experiment): detector-major, the Morton order within each detector
+    const char *od = getenv("MT_ORDER_DET");
+    if (od && atoi(od) == 1) {
+      const int32_t *det = d->ray_det + d->ray_lo;
+      std::sort(p->perm.begin(), p->perm.end(), [&](int32_t a, int32_t b) {
+        return det[a] != det[b] ? det[a] < det[b] : key[a] < key[b];
+      });
+    } else {
+      std::sort(p->perm.begin(), p->perm.end(), [&](int32_t a, int32_t b) { return key[a] < key[b]; });
+    }
     std::vector<float4> ra2(p->R), rb2(p->R);
     std::vector<float> ob2(p->R);
     for (int64_t k = 0; k < p->R; k++) {
