@@ -234,11 +234,19 @@ def main():
     ws, rank, local = dist_env()
     if ws != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}: launch N>1 with torchrun")
+    # MT_BENCH_BACKEND=gloo (tests only): the N > 1 control flow with every rank on the
+    # devices present (ranks may share one); the driver's multi-GPU runs use NCCL
+    backend = os.environ.get("MT_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device(f"cuda:{local}")
 
     ray = args.workload == "ray_sharded"

@@ -894,12 +894,6 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_v0(TraceArgs a
 #ifndef C2_RCAP
 #define C2_RCAP 1   // crossing records per (chain, surface); more re-walk in-kernel (see launch_c2)
 #endif
-#ifndef C2_PREF
-#define C2_PREF 0   // experiment: next ray's header loaded one ray ahead
-#endif
-#ifndef C2_WIN
-#define C2_WIN 0    // experiment: band cell words by one coalesced load + shuffles
-#endif
 #ifndef C2_THREADS
 #define C2_THREADS 256   // threads per block of k_trace_c2
 #endif
@@ -933,30 +927,6 @@ __global__ void __launch_bounds__(MT_THREADS) k_cell_prep2(const float *__restri
   H4[t] = o;
 }
 
-#ifndef C2_NA
-#define C2_NA 0   // experiment: per-cell ray geometry loaded without L1 allocation
-#endif
-// The per-cell ray geometry of the walk is read once per (ray, chain group): with
-// C2_NA it bypasses L1 allocation, leaving L1 to the corner lines that rays share.
-__device__ __forceinline__ float4 ldg_cell4(const float4 *p) {
-#if C2_NA
-  float4 r;
-  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
-  return r;
-#else
-  return __ldg(p);
-#endif
-}
-__device__ __forceinline__ float2 ldg_cell2(const float2 *p) {
-#if C2_NA
-  float2 r;
-  asm("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "l"(p));
-  return r;
-#else
-  return __ldg(p);
-#endif
-}
-
 // One chain's surface-cell from its corners (the corner-bound test, then the solve).
 template <int SLOT, bool SCAT>
 __device__ __forceinline__ void c2_cell(float h00, float h01, float h10, float h11, float4 cg, float2 km, float za,
@@ -984,20 +954,7 @@ __device__ __forceinline__ void c2_cell(float h00, float h01, float h10, float h
 // Crossing records of k_trace_c2, [chain v][surface l][C2_RCAP][thread] (static:
 // the slot address is a constant offset from the thread's, no shared-window
 // pointer to rematerialise).
-#ifndef C2_REC12
-#define C2_REC12 0
-#endif
-#if C2_REC12
-// 12-B records in three planes: node | u (18-bit fixed point) << 14, v, 1/|g'| (a
-// smaller shared-memory footprint leaves more of the SM's 256 KB to the L1 that
-// serves the corner loads; u to 2^-18, far inside the 1e-3 gradient tolerance)
-__shared__ unsigned c2_rnu[4 * C2_RCAP][C2_THREADS];
-__shared__ float c2_rv[4 * C2_RCAP][C2_THREADS];
-__shared__ float c2_rig[4 * C2_RCAP][C2_THREADS];
-#define C2_UQ 262143.f
-#else
 __shared__ __align__(16) float4 c2_recs[4 * C2_RCAP][C2_THREADS];
-#endif
 __shared__ float c2_sll[2][C2_THREADS];   // per-lane log-likelihood sums (kept out of the registers)
 
 // Same, with the lane's crossing counters and defer flags packed in one register
@@ -1010,16 +967,7 @@ __device__ __forceinline__ void c2_cellp(float h00, float h01, float h10, float 
   if (za >= fmaxf(fmaxf(h00, h10), fmaxf(h01, h11))) return;
   auto emit = [&](float u, float v, float ig) {
     const unsigned n = (cnt >> sh) & 31u;
-#if C2_REC12
-    if (n < C2_RCAP) {
-      c2_rnu[slot0 + n][threadIdx.x] =
-          __float_as_uint(wbase) | (__float2uint_rn(__saturatef(u) * C2_UQ) << 14);
-      c2_rv[slot0 + n][threadIdx.x] = v;
-      c2_rig[slot0 + n][threadIdx.x] = ig;
-    }
-#else
     if (n < C2_RCAP) c2_recs[slot0 + n][threadIdx.x] = make_float4(wbase, u, v, ig);
-#endif
     if (n < 31u) cnt += 1u << sh;
   };
   if (!solve32k(h00, h10, h01, h11, cg, km, za, Ls, dz, B, emit)) cnt |= dbit;
@@ -1036,63 +984,22 @@ __device__ __forceinline__ void c2_rays(const TraceArgs &a, int N, int oy, const
   const bool actA = FULL || (acts & 1), actB = FULL || (acts & 2);
   const int r_begin = chunk * (int)a.rays_per_block;
   const int r_end = min((int)a.R, r_begin + (int)a.rays_per_block);
-#if C2_PREF
-  // the next ray's header (ray constants, traversal range) loaded one ray ahead
-  float2 nrb = make_float2(1.f, 0.f);
-  int nk0 = 0, nk1 = 0;
-  if (r_begin + warp < r_end) {
-    nrb = __ldg(reinterpret_cast<const float2 *>(a.ray_b + r_begin + warp));
-    if (C2_PREF == 1) {
-      nk0 = __ldg(a.trav_off + r_begin + warp);
-      nk1 = __ldg(a.trav_off + r_begin + warp + 1);
-    }
-  }
-#endif
   for (int rr = r_begin + warp; rr < r_end; rr += C2_THREADS / 32) {
-#if C2_PREF
-    const float2 rb0 = nrb;
-    const int kbeg = C2_PREF == 1 ? nk0 : __ldg(a.trav_off + rr), kend = C2_PREF == 1 ? nk1 : __ldg(a.trav_off + rr + 1);
-    if (rr + C2_THREADS / 32 < r_end) {
-      nrb = __ldg(reinterpret_cast<const float2 *>(a.ray_b + rr + C2_THREADS / 32));
-      if (C2_PREF == 1) {
-        nk0 = __ldg(a.trav_off + rr + C2_THREADS / 32);
-        nk1 = __ldg(a.trav_off + rr + C2_THREADS / 32 + 1);
-      }
-    }
-#else
     const float2 rb0 = __ldg(reinterpret_cast<const float2 *>(a.ray_b + rr));
-#endif
     const float dz = rb0.x, s_exit = rb0.y;
     const float s_lo = fminf(__fdividef(zlo, dz) * (1.f - 1e-6f), s_exit);
     const float s_hi = fminf(__fdividef(zhi, dz) * (1.f + 1e-6f), s_exit);
     float B0A = s_lo, B1A = s_lo, B0B = s_lo, B1B = s_lo;
     unsigned cnt = 0;   // packed counters / defer flags (c2_cellp)
     if (s_lo < s_exit) {
-#if !C2_PREF
       const int kend = __ldg(a.trav_off + rr + 1), kbeg = __ldg(a.trav_off + rr);
-#endif
       float s_in0;
       const int k0 = band_entry_warp(a.trav, kbeg, kend, s_lo, s_in0);
       float s = s_lo, za = s_lo * dz, ds = s_lo - s_in0;
-#if C2_WIN
-      // the band's cell words, one per lane, from one coalesced load (broadcast per cell by shuffle)
-      int2 wl = make_int2(0, 0);
-      if (k0 + lane < kend) wl = __ldg(a.trav + k0 + lane);
-#endif
       for (int k = k0; k < kend; k++) {
-#if C2_WIN
-        int2 w;
-        if (k - k0 < 32) {
-          w.x = __shfl_sync(0xffffffffu, wl.x, k - k0);
-          w.y = __shfl_sync(0xffffffffu, wl.y, k - k0);
-        } else {
-          w = __ldg(a.trav + k);
-        }
-#else
         const int2 w = __ldg(a.trav + k);
-#endif
-        const float4 cg = shift_geo(ldg_cell4(a.trav_geo + k), ds);
-        float2 km = ldg_cell2(a.trav_km + k);
+        const float4 cg = shift_geo(__ldg(a.trav_geo + k), ds);
+        float2 km = __ldg(a.trav_km + k);
         km.x = fmaf(2.f * km.y, ds, km.x);
         const float s1 = __int_as_float(w.y);
         const float zb = s1 * dz, Ls = s1 - s;
@@ -1150,17 +1057,9 @@ __device__ __forceinline__ void c2_rays(const TraceArgs &a, int N, int oy, const
 #pragma unroll
           for (int m = 0; m < C2_RCAP; m++) {
             if (m >= ml) break;
-#if C2_REC12
-            const int sl = (2 * v + l) * C2_RCAP + m;
-            const unsigned nu = c2_rnu[sl][threadIdx.x];
-            const float wv = fl * c2_rig[sl][threadIdx.x], u = (float)(nu >> 14) * (1.f / C2_UQ), vv = c2_rv[sl][threadIdx.x];
-            const float wa = wv * (1.f - u), wbb = wv * u;
-            macc *pg = Gl + ((nu & 0x3FFFu) << 5);
-#else
             const float4 q = c2_recs[(2 * v + l) * C2_RCAP + m][threadIdx.x];
             const float wv = fl * q.w, u = q.y, vv = q.z, wa = wv * (1.f - u), wbb = wv * u;
             macc *pg = Gl + (__float_as_uint(q.x) << 5);
-#endif
             atomicAdd(pg, q_raw(wa * (1.f - vv)));
             atomicAdd(pg + oy, q_raw(wbb * (1.f - vv)));
             atomicAdd(pg + 32, q_raw(wa * vv));
