@@ -392,6 +392,9 @@ __device__ __forceinline__ void piece64(const TraceArgs &a, const Ray &r, int k,
 #ifndef MT_RL_MINB
 #define MT_RL_MINB 4
 #endif
+#ifndef RL_KM
+#define RL_KM 1   // ray lanes use solve32k (K, M from the cell geometry; -1.8% vs solve32)
+#endif
 // lanes per deferred pair in k_trace_defer: 8 after the chain lanes (many pairs,
 // throughput), more after the ray lanes (few pairs, latency of the band rounds)
 #ifndef DEFER_DG
@@ -894,6 +897,9 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_v0(TraceArgs a
 #ifndef C2_RCAP
 #define C2_RCAP 1   // crossing records per (chain, surface); more re-walk in-kernel (see launch_c2)
 #endif
+#ifndef C2_KMC
+#define C2_KMC 0   // experiment: K, M of solve32k formed in-lane from the cell geometry (no trav_km load)
+#endif
 #ifndef C2_THREADS
 #define C2_THREADS 256   // threads per block of k_trace_c2
 #endif
@@ -999,8 +1005,8 @@ __device__ __forceinline__ void c2_rays(const TraceArgs &a, int N, int oy, const
       for (int k = k0; k < kend; k++) {
         const int2 w = __ldg(a.trav + k);
         const float4 cg = shift_geo(__ldg(a.trav_geo + k), ds);
-        float2 km = __ldg(a.trav_km + k);
-        km.x = fmaf(2.f * km.y, ds, km.x);
+        float2 km = C2_KMC ? make_float2(fmaf(cg.x, cg.w, cg.y * cg.z), cg.z * cg.w) : __ldg(a.trav_km + k);
+        if (!C2_KMC) km.x = fmaf(2.f * km.y, ds, km.x);
         const float s1 = __int_as_float(w.y);
         const float zb = s1 * dz, Ls = s1 - s;
         const unsigned off = cell_off32(w.x);
@@ -1076,8 +1082,8 @@ __device__ __forceinline__ void c2_rays(const TraceArgs &a, int N, int oy, const
         for (int k = k0; k < kend; k++) {
           const int2 w = __ldg(a.trav + k);
           const float4 cg = shift_geo(__ldg(a.trav_geo + k), ds);
-          float2 km = __ldg(a.trav_km + k);
-          km.x = fmaf(2.f * km.y, ds, km.x);
+          float2 km = C2_KMC ? make_float2(fmaf(cg.x, cg.w, cg.y * cg.z), cg.z * cg.w) : __ldg(a.trav_km + k);
+          if (!C2_KMC) km.x = fmaf(2.f * km.y, ds, km.x);
           const float s1 = __int_as_float(w.y);
           const float zb = s1 * dz, Ls = s1 - s;
           const unsigned off = cell_off32(w.x);
@@ -1465,15 +1471,17 @@ __global__ void __launch_bounds__(MT_THREADS, MT_RL_MINB) k_trace_rl(TraceArgs a
                                         (fmaf(s, rd.y, ro.y) - sgeo[1][j]) * iy, rd.x * ix, rd.y * iy);
           const float zb = s1 * dz, Ls = s1 - s;
           const int base = i * ny + j, w = base << 5;
+          // the ray-only solve terms K = u0 β + v0 α, M = α β of solve32k (the chain lanes store them)
+          const float2 km = RL_KM ? make_float2(fmaf(cg.x, cg.w, cg.y * cg.z), cg.z * cg.w) : make_float2(0.f, 0.f);
           if (zb <= bd.x) B0 += Ls;
           else if (za < bd.y) {
             const float *p = Hs + base;
-            cw_solve<0>(make_float4(p[0], p[1], p[ny], p[ny + 1]), w, cg, za, zb, Ls, dz, B0, n0, defer, rec);
+            cw_solve<0, RL_KM>(make_float4(p[0], p[1], p[ny], p[ny + 1]), w, cg, za, zb, Ls, dz, B0, n0, defer, rec, km);
           }
           if (zb <= bd.z) B1 += Ls;
           else if (za < bd.w) {
             const float *p = Hs + N + base;
-            cw_solve<1>(make_float4(p[0], p[1], p[ny], p[ny + 1]), w, cg, za, zb, Ls, dz, B1, n1, defer, rec);
+            cw_solve<1, RL_KM>(make_float4(p[0], p[1], p[ny], p[ny + 1]), w, cg, za, zb, Ls, dz, B1, n1, defer, rec, km);
           }
           if (s1 >= s_hi) break;
           s = s1;
