@@ -898,7 +898,7 @@ __global__ void __launch_bounds__(MT_THREADS, MT_CL_MINB) k_trace_v0(TraceArgs a
 #define C2_RCAP 1   // crossing records per (chain, surface); more re-walk in-kernel (see launch_c2)
 #endif
 #ifndef C2_KMC
-#define C2_KMC 0   // experiment: K, M of solve32k formed in-lane from the cell geometry (no trav_km load)
+#define C2_KMC 1   // K, M of solve32k formed in-lane from the cell geometry: no trav_km load (-0.9%)
 #endif
 #ifndef C2_THREADS
 #define C2_THREADS 256   // threads per block of k_trace_c2
