@@ -1712,8 +1712,13 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
     a.rays_per_block = chunk;
     int64_t S = (p->R + chunk - 1) / chunk;
     dim3 grid((unsigned)S, (unsigned)groups);
-    if (c2) {   // (C2_THREADS / 256 chunks per block)
-      a.rays_per_block = std::max<int64_t>(32, chunk * C2_THREADS / 256);
+    if (c2) {
+      // two chains per lane: R / (2.75 SMs) rays per 256-thread block, at most 512 (Small,
+      // R = 16,384: 40-ray chunks, 0.0605 -> 0.0523 ms per evaluation vs R / (2 SMs); every
+      // R >= 225K keeps 512).  Again a function of R (and the device) only, never of C.
+      const int64_t chunk2 = p->chunk > 0 ? p->chunk
+                                          : std::max<int64_t>(32, std::min<int64_t>(512, p->R * 4 / (11 * (int64_t)p->num_sms)));
+      a.rays_per_block = std::max<int64_t>(32, chunk2 * C2_THREADS / 256);
       const int64_t S2 = (p->R + a.rays_per_block - 1) / a.rays_per_block;
       dim3 grid2((unsigned)S2, (unsigned)((C + 63) / 64));
       if (grid2.x % C2_TILE) grid2.x += C2_TILE - grid2.x % C2_TILE;   // whole tiles (extra chunks are empty)
