@@ -403,6 +403,9 @@ __device__ __forceinline__ void piece64(const TraceArgs &a, const Ray &r, int k,
 #ifndef DEFER_DG_RL
 #define DEFER_DG_RL 16
 #endif
+#ifndef DEFER_SMALL_R
+#define DEFER_SMALL_R 65536   // at most this many rays: 32 lanes per deferred pair
+#endif
 #ifndef MT_CL_MINB
 #define MT_CL_MINB 5
 #endif
@@ -1728,8 +1731,18 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
     }
     if (rec) cudaEventRecord(p->ev_m[p->n_rec], s);
     if (e == cudaSuccess) {   // deferred pairs (ill-conditioned or > RCAP crossings)
-      if (mode == TRACE_LL) k_trace_defer<TRACE_LL, DEFER_DG><<<DEFER_MINB * p->num_sms, MT_THREADS, 0, s>>>(a);
-      else k_trace_defer<TRACE_PATH, DEFER_DG><<<DEFER_MINB * p->num_sms, MT_THREADS, 0, s>>>(a);
+      // few rays -> few deferred pairs: the follow-up's time is one pair's chain of dependent
+      // band rounds, so a whole warp per pair (Small: 16.5 -> 12.9 us per evaluation); a
+      // function of R only, like the launch shape (R30)
+      const dim3 gd(DEFER_MINB * p->num_sms);
+      if (p->R <= DEFER_SMALL_R) {
+        if (mode == TRACE_LL) k_trace_defer<TRACE_LL, 32><<<gd, MT_THREADS, 0, s>>>(a);
+        else k_trace_defer<TRACE_PATH, 32><<<gd, MT_THREADS, 0, s>>>(a);
+      } else if (mode == TRACE_LL) {
+        k_trace_defer<TRACE_LL, DEFER_DG><<<gd, MT_THREADS, 0, s>>>(a);
+      } else {
+        k_trace_defer<TRACE_PATH, DEFER_DG><<<gd, MT_THREADS, 0, s>>>(a);
+      }
       e = cudaGetLastError();
       p->all_launches++;
     }
@@ -1747,8 +1760,14 @@ cudaError_t launch_trace(mt_problem *p, int mode, int C, const float *H, const f
                            : launch_rl_ny<TRACE_PATH>(a, p->d_Hc, p->ny, grid, smem, s);
     if (rec) cudaEventRecord(p->ev_m[p->n_rec], s);
     if (e == cudaSuccess) {
-      if (mode == TRACE_LL) k_trace_defer<TRACE_LL, DEFER_DG_RL><<<2 * p->num_sms, MT_THREADS, 0, s>>>(a);
-      else k_trace_defer<TRACE_PATH, DEFER_DG_RL><<<2 * p->num_sms, MT_THREADS, 0, s>>>(a);
+      if (p->R <= DEFER_SMALL_R) {
+        if (mode == TRACE_LL) k_trace_defer<TRACE_LL, 32><<<2 * p->num_sms, MT_THREADS, 0, s>>>(a);
+        else k_trace_defer<TRACE_PATH, 32><<<2 * p->num_sms, MT_THREADS, 0, s>>>(a);
+      } else if (mode == TRACE_LL) {
+        k_trace_defer<TRACE_LL, DEFER_DG_RL><<<2 * p->num_sms, MT_THREADS, 0, s>>>(a);
+      } else {
+        k_trace_defer<TRACE_PATH, DEFER_DG_RL><<<2 * p->num_sms, MT_THREADS, 0, s>>>(a);
+      }
       e = cudaGetLastError();
       p->all_launches += 2;
     }
