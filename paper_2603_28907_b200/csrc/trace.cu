@@ -964,7 +964,6 @@ __device__ __forceinline__ void c2_cell(float h00, float h01, float h10, float h
 // the slot address is a constant offset from the thread's, no shared-window
 // pointer to rematerialise).
 __shared__ __align__(16) float4 c2_recs[4 * C2_RCAP][C2_THREADS];
-__shared__ float c2_sll[2][C2_THREADS];   // per-lane log-likelihood sums (kept out of the registers)
 
 // Same, with the lane's crossing counters and defer flags packed in one register
 // (fields of 5 bits, saturating at 31: n0A @0, n1A @5, n0B @10, n1B @15; defer
@@ -987,7 +986,7 @@ __device__ __forceinline__ void c2_cellp(float h00, float h01, float h10, float 
 template <int MODE, bool FULL>
 __device__ __forceinline__ void c2_rays(const TraceArgs &a, int N, int oy, const int g, const int chunk,
                                         const int acts, const float4 bd, const float zlo, const float zhi,
-                                        const float4 *__restrict__ H4) {
+                                        const float4 *__restrict__ H4, float &sllA, float &sllB) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int cA = g * 64 + lane, cB = cA + 32;
   const bool actA = FULL || (acts & 1), actB = FULL || (acts & 2);
@@ -1056,7 +1055,7 @@ __device__ __forceinline__ void c2_rays(const TraceArgs &a, int N, int oy, const
         float dldO;
         const float ll = epilogue(rt.x, rt.y, a.tc, v ? B0B : B0A, v ? B1B : B1A, dldO);
         const float f0 = dldO * a.tc.k0 * (float)MT_GQ, f1 = dldO * a.tc.k1 * (float)MT_GQ;
-        c2_sll[v][threadIdx.x] += ll;
+        if (v) sllB += ll; else sllA += ll;
         if (v) { f0B = f0; f1B = f1; } else { f0A = f0; f1A = f1; }
 #pragma unroll
         for (int l = 0; l < 2; l++) {   // records of surface l: slots (2v + l) RCAP + m, m < min(n, RCAP)
@@ -1151,13 +1150,12 @@ __global__ void __launch_bounds__(C2_THREADS, C2_MINB) k_trace_c2(TraceArgs a) {
   if (!actA && !actB) bd = make_float4(-3.0e38f, -3.0e38f, -3.0e38f, -3.0e38f);
   const float4 *__restrict__ H4 = reinterpret_cast<const float4 *>(a.cl) + (size_t)g * 2 * N * 32 + lane;
   asm volatile("mov.b64 %0, %0;" : "+l"(H4));
-  c2_sll[0][threadIdx.x] = 0.f;
-  c2_sll[1][threadIdx.x] = 0.f;
-  if (g * 64 + 64 <= a.C) c2_rays<MODE, true>(a, N, oy, g, chunk, acts, bd, zlo, zhi, H4);
-  else c2_rays<MODE, false>(a, N, oy, g, chunk, acts, bd, zlo, zhi, H4);
+  float sllA = 0.f, sllB = 0.f;
+  if (g * 64 + 64 <= a.C) c2_rays<MODE, true>(a, N, oy, g, chunk, acts, bd, zlo, zhi, H4, sllA, sllB);
+  else c2_rays<MODE, false>(a, N, oy, g, chunk, acts, bd, zlo, zhi, H4, sllA, sllB);
   if (MODE == TRACE_LL) {
-    if (actA) atomicAdd(a.ll + cA, q_ll(c2_sll[0][threadIdx.x]));
-    if (actB) atomicAdd(a.ll + cB, q_ll(c2_sll[1][threadIdx.x]));
+    if (actA) atomicAdd(a.ll + cA, q_ll(sllA));
+    if (actB) atomicAdd(a.ll + cB, q_ll(sllB));
   }
 }
 
